@@ -1,0 +1,449 @@
+"""Benchmark of the B200 hybrid-head decode attention (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload llama3-8b-128k|llama3-8b-32k|qwen3-8b-128k|llama3-8b-64k-b16|tiny]
+                    [--select tokens|blocks]
+
+A STEP is one decode step of hybrid-head attention over ALL layers
+(decode_engine.hpp:109-151): per layer the pooled split-KV attention kernel
+(retrieval + sparse heads), the split-KV merge and the cluster top-k into the
+per-head index cache, in layer order, CUDA-graph replayed.  Inputs (q, K/V
+caches, 17 GiB at 128K) are resident in HBM and far larger than the 126 MB L2,
+so no flush is needed between steps.
+
+value     : device time per decode step in us (= us/token at batch 1), max over
+            ranks, CUDA events around exactly K replays.
+e2e       : the same step through the public C-ABI call (HybridDecoder.decode_step,
+            eager) with the step's inputs copied from pinned host memory (q of
+            every layer + the new token's K/V row of every layer) and the
+            attention outputs copied back, all inside the timed region.
+roofline  : dominant kernel = hybrid_attn_kernel; achieved = its algorithmic
+            bytes (K/V rows touched + Q + O) / its CUDA-event
+            duration, measured inside the graph on the launching stream.
+cpu_baseline / --impl reference : the reference's own CPU operator
+            hh::kernel::run<float> (kernel_sim.hpp:237-279, oracle/_ref built from
+            the reference headers) on a bounded sample (one layer of the
+            workload's dominant role pattern), extrapolated by block count.
+Multi-GPU (torchrun): KV heads are sharded across ranks (index propagation is
+per head index, so no collective is needed on the data path).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "decode attention us/token at 128K (1/2/4/8 B200); achieved HBM GB/s vs peak"
+
+WORKLOADS = {
+    # name: (layers, kv heads, group, d, context, top-k, batch, dtype)
+    "llama3-8b-128k": dict(NL=32, H=8, G=4, d=128, L=131072, k=4096, B=1, dtype="bf16"),
+    "llama3-8b-32k": dict(NL=32, H=8, G=4, d=128, L=32768, k=2048, B=1, dtype="bf16"),
+    "qwen3-8b-128k": dict(NL=36, H=8, G=4, d=128, L=131072, k=4096, B=1, dtype="bf16"),
+    "llama3-8b-64k-b16": dict(NL=32, H=8, G=4, d=128, L=65536, k=2048, B=16, dtype="bf16"),
+    "tiny": dict(NL=4, H=2, G=4, d=64, L=4096, k=256, B=1, dtype="f32"),
+}
+
+
+def make_roles(NL, H, frac, seed):
+    """Layer 0 all retrieval (decode_engine.hpp:121); above it a seeded choice
+    of retrieval heads so that frac of all (layer, head) slots are retrieval
+    (12.5 % = 32/256 on Llama-3-8B)."""
+    roles = np.ones((NL, H), dtype=np.uint8)
+    roles[0] = 0
+    n_extra = max(0, int(round(frac * NL * H)) - H)
+    rng = np.random.default_rng(seed)
+    slots = rng.choice((NL - 1) * H, size=min(n_extra, (NL - 1) * H), replace=False)
+    for s in slots:
+        roles[1 + s // H, s % H] = 0
+    return roles
+
+
+def shard_heads(roles, L, k, world, rank):
+    """Assign KV heads to ranks, balancing per-token rows (LPT greedy)."""
+    NL, H = roles.shape
+    work = [sum(L if roles[l, g] == 0 else min(k, L) for l in range(NL)) for g in range(H)]
+    load = [0] * world
+    owner = [0] * H
+    for g in sorted(range(H), key=lambda g: -work[g]):
+        r = min(range(world), key=lambda r: load[r])
+        owner[g] = r
+        load[r] += work[g]
+    return [g for g in range(H) if owner[g] == rank]
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "samples": len(self.samples), "reasons": sorted(self.reasons)}
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------- CPU
+def cpu_sample(wl, roles, K_host=None, V_host=None, q_host=None, reps=1, want_out=False):
+    """Time the reference CPU operator on one layer of the dominant role
+    pattern and extrapolate to a whole decode step by block count.
+
+    Returns (us_per_step, info dict)."""
+    from oracle import pyoracle
+    lib = pyoracle.ref()
+    kind = "reference"
+    if lib is None:
+        lib, kind = pyoracle.orc(), "port"
+    NL, H, G, d, L, k, B = (wl[x] for x in ("NL", "H", "G", "d", "L", "k", "B"))
+    bs = 64
+    nb = (L + bs - 1) // bs
+    nblk = min((k + bs - 1) // bs, nb)
+    rng = np.random.default_rng(7)
+    if K_host is None:
+        K_host = rng.uniform(-1, 1, (H, L, d)).astype(np.float32)
+        V_host = rng.uniform(-1, 1, (H, L, d)).astype(np.float32)
+        q_host = rng.uniform(-1, 1, (H * G, d)).astype(np.float32)
+    # sample: one retrieval head (all blocks) + H-1 sparse heads (top-k blocks)
+    blocks = [np.arange(nb)] + [np.sort(rng.choice(nb, nblk, replace=False)) for _ in range(H - 1)]
+    sample_blocks = nb + (H - 1) * nblk
+    total_blocks = B * sum(nb if roles[l, g] == 0 else nblk for l in range(NL) for g in range(H))
+    cores = os.cpu_count() or 1
+    splits = 16 * H
+    if kind == "reference":
+        best, _ = lib.kernel_run_time(K_host, V_host, q_host, blocks, batch=1, group=G, seq_len=L,
+                                      scale=1 / np.sqrt(d), num_splits=splits, n_workers=cores,
+                                      reps=reps)
+    else:
+        cores = 1
+        t0 = time.perf_counter()
+        lib.kernel_run(K_host, V_host, q_host, blocks, batch=1, group=G, seq_len=L,
+                       scale=1 / np.sqrt(d), num_splits=splits, dtype=np.float32)
+        best = time.perf_counter() - t0
+    us = best * 1e6 * total_blocks / sample_blocks
+    info = {"kind": kind, "cores": cores,
+            "sample": (f"hh::kernel::run<float> one layer: 1 retrieval head ({nb} blocks) + "
+                       f"{H - 1} sparse heads ({nblk} blocks), L={L}, d={d}, G={G}, "
+                       f"{splits} splits, {cores} workers; {best * 1e3:.1f} ms, scaled x"
+                       f"{total_blocks / sample_blocks:.2f} by block count to one decode step "
+                       f"(selection pass not included)")}
+    return us, info
+
+
+def run_reference_arm(args, wl, roles, rank, world):
+    if rank != 0:
+        return
+    # warm-up + timed samples of the reference CPU path on the same workload
+    from oracle import pyoracle  # noqa: F401
+    rng = np.random.default_rng(7)
+    H, L, d, G = wl["H"], wl["L"], wl["d"], wl["G"]
+    K = rng.uniform(-1, 1, (H, L, d)).astype(np.float32)
+    V = rng.uniform(-1, 1, (H, L, d)).astype(np.float32)
+    q = rng.uniform(-1, 1, (H * G, d)).astype(np.float32)
+    for _ in range(args.warmup):
+        cpu_sample(wl, roles, K, V, q)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        us, info = cpu_sample(wl, roles, K, V, q)
+        vals.append(us)
+    wall = time.perf_counter() - t0
+    v = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "us/token",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": v / 1e3, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic U(-1,1)",
+        "config": config_of(args, wl),
+        "cpu_baseline": {"value": v, "unit": "us/token", **info},
+        "e2e": {"value": v, "unit": "us/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_of(args, wl):
+    c = {"workload": args.workload, "layers": wl["NL"], "q_heads": wl["H"] * wl["G"],
+         "kv_heads": wl["H"], "head_dim": wl["d"], "context": wl["L"], "top_k": wl["k"],
+         "batch": wl["B"], "retrieval_fraction": args.retrieval_frac, "select": args.select,
+         "parallelism": f"head-sharded x{args.gpus}" if args.gpus > 1 else "single GPU",
+         "l2": "inputs larger than L2 (KV caches >> 126 MB), no flush"}
+    return c
+
+
+# ----------------------------------------------------------------------- GPU
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="llama3-8b-128k", choices=list(WORKLOADS))
+    ap.add_argument("--select", default="tokens", choices=["tokens", "blocks"])
+    ap.add_argument("--retrieval-frac", type=float, default=0.125)
+    ap.add_argument("--seed", type=int, default=2602)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-full", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    wl = dict(WORKLOADS[args.workload])
+    roles = make_roles(wl["NL"], wl["H"], args.retrieval_frac, args.seed)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, wl, roles, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2602_04541_b200 as P
+
+    NL, H, G, d, L, k, B = (wl[x] for x in ("NL", "H", "G", "d", "L", "k", "B"))
+    my_heads = shard_heads(roles, L, k, world, rank) if world > 1 else list(range(H))
+    Hr = len(my_heads)
+    r_roles = np.ascontiguousarray(roles[:, my_heads])
+    dt = torch.bfloat16 if wl["dtype"] == "bf16" else torch.float32
+    esz = 2 if dt == torch.bfloat16 else 4
+    seq_cap = L
+    dev = torch.device("cuda", local)
+    gen = torch.Generator(device=dev).manual_seed(args.seed + rank)
+    K = torch.empty((NL, B, Hr, seq_cap, d), dtype=dt, device=dev)
+    V = torch.empty_like(K)
+    for t in (K, V):
+        for l in range(NL):
+            t[l].uniform_(-1, 1, generator=gen)
+    q = torch.empty((NL, B, Hr * G, d), dtype=dt, device=dev).uniform_(-1, 1, generator=gen)
+    out = torch.empty_like(q)
+    stream = torch.cuda.Stream(device=dev)
+    pol = P.SparsityPolicy.top_k(k)
+    dec = P.HybridDecoder(n_layers=NL, batch=B, n_kv_heads=Hr, group_size=G, d_head=d,
+                          seq_cap=seq_cap, roles=r_roles, policy=pol, dtype=dt, select=args.select)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def time_graph(dd, steps, warm):
+        with torch.cuda.stream(stream):
+            for _ in range(warm):
+                dd.replay(stream=stream)
+        stream.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(steps):
+                dd.replay(stream=stream)
+            e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        barrier()
+        return e0.elapsed_time(e1) / steps  # ms per step
+
+    # ---- headline: graph-replayed decode steps
+    with torch.cuda.stream(stream):
+        dec.capture(q, K, V, L, out, stream=stream)
+    launches_per_step = dec.launches_per_step(L)
+    lc0 = P.lib().lyc_launch_count()
+    with ClockSampler(local) as clk:
+        ms = time_graph(dec, args.steps, args.warmup)
+        # keep the GPU busy >= ~1 s so the sampler sees the loaded clock
+        t_end = time.time() + max(0.0, 1.0 - ms * args.steps / 1e3)
+        with torch.cuda.stream(stream):
+            while time.time() < t_end:
+                for _ in range(20):
+                    dec.replay(stream=stream)
+                stream.synchronize()
+    launched = P.lib().lyc_launch_count() - lc0
+    ms = allmax(ms)
+    step_us = ms * 1e3
+    step_bytes = dec.step_bytes(L)
+
+    # ---- roofline of the dominant kernel (attention), events inside the graph
+    dec.set_timing(True)
+    with torch.cuda.stream(stream):
+        dec.capture(q, K, V, L, out, stream=stream)
+        for _ in range(args.warmup):
+            dec.replay(stream=stream)
+    stream.synchronize()
+    per_layer = np.zeros(NL)
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            dec.replay(stream=stream)
+        per_layer += dec.attn_ms()
+    per_layer /= args.steps
+    attn_bytes = np.array([dec.layer_attn_bytes(l, L) for l in range(NL)], dtype=np.float64)
+    attn_ms_total = float(per_layer.sum())
+    achieved = attn_bytes.sum() / (attn_ms_total / 1e3) / 1e9
+    dec.set_timing(False)
+    pk, pk_kind = peaks()
+    peak = float(pk["hbm_gbs"])
+
+    # ---- same-GPU full-attention decode (every head dense, no selection)
+    full = None
+    if not args.no_full:
+        fdec = P.HybridDecoder(n_layers=NL, batch=B, n_kv_heads=Hr, group_size=G, d_head=d,
+                               seq_cap=seq_cap, roles=np.zeros((NL, Hr), np.uint8), policy=pol,
+                               dtype=dt, select="none")
+        fout = torch.empty_like(q)
+        with torch.cuda.stream(stream):
+            fdec.capture(q, K, V, L, fout, stream=stream)
+        fms = allmax(time_graph(fdec, args.steps, args.warmup))
+        fbytes = fdec.step_bytes(L)
+        full = {"us_per_token": fms * 1e3, "hbm_gbs": fbytes / (fms / 1e3) / 1e9,
+                "speedup_hybrid_vs_full": fms / ms}
+        fdec.close()
+
+    # ---- e2e through the public API with host buffers
+    q_h = torch.empty(q.shape, dtype=dt, pin_memory=True)
+    q_h.copy_(q.cpu())
+    kv_new_h = torch.empty((2, NL, B, Hr, d), dtype=dt, pin_memory=True)
+    kv_new_h[0].copy_(K[:, :, :, L - 1].cpu())
+    kv_new_h[1].copy_(V[:, :, :, L - 1].cpu())
+    kv_new_d = torch.empty(kv_new_h.shape, dtype=dt, device=dev)
+    out_h = torch.empty(out.shape, dtype=dt, pin_memory=True)
+    e2e_steps = max(3, args.steps // 2)
+
+    def e2e_step():
+        q.copy_(q_h, non_blocking=True)
+        kv_new_d.copy_(kv_new_h, non_blocking=True)
+        K[:, :, :, L - 1].copy_(kv_new_d[0])
+        V[:, :, :, L - 1].copy_(kv_new_d[1])
+        dec.decode_step(q, K, V, L, out, stream=stream)
+        out_h.copy_(out, non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            e2e_step()
+    stream.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            e2e_step()
+        e1.record(stream)
+    e1.synchronize()
+    barrier()
+    e2e_ms = allmax(e0.elapsed_time(e1) / e2e_steps)
+    h2d = q_h.numel() * esz + kv_new_h.numel() * esz
+    d2h = out_h.numel() * esz
+
+    # ---- CPU baseline (rank 0, N == 1): the reference operator on the host
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            nb_ = min(L, 131072)
+            Kh = K[0, 0, :, :nb_].float().cpu().numpy()
+            Vh = V[0, 0, :, :nb_].float().cpu().numpy()
+            qh = q[0, 0].float().cpu().numpy()
+            wl_c = dict(wl, L=nb_)
+            us, info = cpu_sample(wl_c, roles, Kh, Vh, qh)
+            us *= L / nb_ if nb_ < L else 1.0
+            cpu = {"value": us, "unit": "us/token", **info}
+        except Exception as e:  # the baseline must not kill the bench line
+            cpu = {"value": None, "unit": "us/token", "error": repr(e)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": step_us / B if B > 1 else step_us,
+            "unit": "us/token", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": wl["dtype"], "data": "synthetic U(-1,1) q/K/V, seeded roles",
+            "config": config_of(args, wl),
+            "tokens_per_s": B / (ms / 1e3),
+            "step_hbm_gbs": step_bytes / (ms / 1e3) / 1e9 if world == 1 else None,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": pk_kind,
+                         "frac_of_8TBs": achieved / 8000.0,
+                         "kernel": "hybrid_attn_kernel (all layers)",
+                         "attn_us_per_step": attn_ms_total * 1e3,
+                         "layer0_gbs": attn_bytes[0] / (per_layer[0] / 1e3) / 1e9,
+                         "bytes_per_step": float(attn_bytes.sum())},
+            "full_attention": full,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_ms * 1e3, "unit": "us/token", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "api": "HybridDecoder.decode_step (eager C-ABI)"},
+            "gpu_launches": int(launches_per_step * args.steps),
+            "launches_per_step": int(launches_per_step),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dec.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

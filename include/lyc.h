@@ -1,0 +1,176 @@
+/*
+ * lyc.h -- C-ABI of the B200-native LycheeDecode hybrid-head decode attention.
+ *
+ * This is the drop-in boundary for the reference's hot path (the header-only
+ * C++ library `hh` under /root/reference/proj/include).  Every entry point
+ * names the reference interface it replaces.  Plain pointers and sizes only;
+ * device pointers are CUDA global-memory addresses on the current device,
+ * streams are cudaStream_t passed as void*.
+ *
+ * Error model (reference throws, we return):
+ *   LYC_EINVAL  <-> std::invalid_argument   (shape / set / config violations)
+ *   LYC_ESTATE  <-> std::logic_error        (engine state)
+ *   LYC_ECUDA   CUDA runtime failure;  LYC_ENOTSUP unsupported shape on device
+ * lyc_last_error() returns the thread-local message of the last failure.
+ * Validation happens on the host before any launch; no entry point
+ * synchronises the stream except where documented.
+ */
+#ifndef LYC_H_
+#define LYC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LYC_OK 0
+#define LYC_EINVAL (-1)
+#define LYC_ESTATE (-2)
+#define LYC_ECUDA (-3)
+#define LYC_ENOTSUP (-4)
+#define LYC_ENCCL (-5)
+
+#define LYC_DTYPE_F32 0
+#define LYC_DTYPE_BF16 1
+
+/* policy.hpp:22 SparsityPolicy::Kind (TopP / Threshold are host-only) */
+#define LYC_POLICY_TOPK 0
+#define LYC_POLICY_TOPP 1
+#define LYC_POLICY_THRESHOLD 2
+#define LYC_POLICY_RATIO 3
+
+#define LYC_SELECT_TOKENS 0 /* token-granular TokenSet (decode_engine.hpp:132) */
+#define LYC_SELECT_BLOCKS 1 /* block-granular BlockIndexSet (kernel_sim.hpp:20-42) */
+#define LYC_SELECT_NONE 2   /* no selection: every head dense (full-attention baseline) */
+
+const char* lyc_last_error(void);
+const char* lyc_version(void);
+/* Number of CUDA kernels this thread has launched through the library. */
+int64_t lyc_launch_count(void);
+
+/* ---------------------------------------------------------------------------
+ * Host planning and cost model (kernel_sim.hpp / policy.hpp).
+ * ------------------------------------------------------------------------- */
+
+/* kernel_sim.hpp:63-110 plan_splits.  head_blocks[b*H+g] = list sizes.
+ * Outputs split_blocks[b*S+s], head_split_count[b*H+g] and up to max_units
+ * unit records (b, s, g, begin, end, head_local_split) in emission order.
+ * Returns the number of units (>= 0) or LYC_EINVAL (num_splits < 1, or a
+ * batch item with zero blocks). */
+int64_t lyc_plan_splits(int64_t batch, int64_t n_kv_heads, const int64_t* head_blocks,
+                        int64_t num_splits, int64_t* split_blocks, int64_t* head_split_count,
+                        int64_t* units, int64_t max_units);
+
+/* kernel_sim.hpp:284-316 latency_model.  out6 = {total_blocks,
+ * pooled_critical_blocks, naive_critical_blocks, bytes_per_block,
+ * pooled_critical_bytes, naive_critical_bytes}; out2 = {mean_split_blocks,
+ * balance_ratio}. */
+int lyc_latency_model(int64_t batch, int64_t n_kv_heads, const int64_t* head_blocks,
+                      int64_t num_splits, int64_t bytes_per_block, int64_t* out6, double* out2);
+
+/* policy.hpp:57-62 fraction_budget. */
+int64_t lyc_fraction_budget(double frac, int64_t n);
+
+/* ---------------------------------------------------------------------------
+ * Operator: hh::kernel::run (kernel_sim.hpp:237-279) on device memory.
+ * ------------------------------------------------------------------------- */
+typedef struct lyc_workload {
+  int64_t batch, n_kv_heads, group_size, d_head, seq_len, block_size;
+  int64_t kv_row_stride; /* rows between consecutive (b, g) slabs (>= seq_len) */
+  float scale;
+  int32_t dtype;         /* LYC_DTYPE_* of k, v, q and out */
+  const void* k;         /* device [B*H][kv_row_stride][d] (Workload::keys)   */
+  const void* v;         /* device [B*H][kv_row_stride][d] (Workload::values) */
+  const void* q;         /* device [B*Hq][d]  (Workload::queries, h = g*G+j)  */
+  const int64_t* blk_off;/* HOST CSR offsets [B*H+1] (BlockIndexSet::ids)     */
+  const int64_t* blk_ids;/* HOST block ids, ascending per (b, g)              */
+} lyc_workload;
+
+/* Validates like Workload::validate (kernel_sim.hpp:136-145), plans like
+ * plan_splits, executes every (b, split) cell as one CTA and merges like
+ * combine (205-225).  out: device [B*Hq][d] (dtype).  exec_counts (optional):
+ * device uint32 [B*H][n_blocks], incremented once per executed (b, g, list
+ * index) -- the conservation counter of kernel_sim.hpp:192-193.  Host-side
+ * copies of the plan are staged internally (not the decode hot path). */
+int lyc_workload_run(const lyc_workload* w, int64_t num_splits, void* out, uint32_t* exec_counts,
+                     void* stream);
+
+/* attention.hpp:108-123 args_top_k over a device float vector: the min(k, n)
+ * largest, ties to the lower index, written ascending to out (device int32).
+ * Returns the count written or an error.  Uses the same cluster radix-select
+ * kernel as the decode path. */
+int64_t lyc_args_top_k(const float* scores, int64_t n, int64_t k, int32_t* out, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Decoder: the decode_step attention loop (decode_engine.hpp:109-151) with the
+ * role mask (rolemap.hpp:33-35, layer 0 forced retrieval at :121), the TopK /
+ * Ratio policy (policy.hpp:64-72) and the cross-layer per-KV-head index cache
+ * sets_ (decode_engine.hpp:251).
+ * ------------------------------------------------------------------------- */
+typedef struct lyc_decode_config {
+  int32_t n_layers, batch, n_kv_heads, group_size, d_head;
+  int32_t dtype;         /* LYC_DTYPE_* */
+  int64_t seq_cap;       /* KV rows allocated per (layer, b, g) slab */
+  int32_t policy_kind;   /* LYC_POLICY_TOPK or LYC_POLICY_RATIO */
+  int32_t select_mode;   /* LYC_SELECT_TOKENS or LYC_SELECT_BLOCKS */
+  int64_t top_k;         /* TopK budget in tokens (blocks mode: ceil(k / block_size) blocks) */
+  double ratio;          /* Ratio theta in (0, 1) */
+  int32_t block_size;    /* 64 (tile) */
+  int32_t num_splits;    /* splits per batch item; 0 = one CTA per SM */
+  float scale;           /* softmax scale; 0 -> 1/sqrt(d_head) */
+  const uint8_t* roles;  /* host [n_layers][n_kv_heads]; 0 = Retrieval, 1 = Sparse */
+} lyc_decode_config;
+
+typedef struct lyc_decoder lyc_decoder;
+
+int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out);
+int lyc_decoder_destroy(lyc_decoder* dec);
+
+/* One decode step over all layers.  Device buffers:
+ *   q   [n_layers][B][Hq][d]            queries of the step
+ *   k,v [n_layers][B][H][seq_cap][d]    caches, rows 0..seq_len-1 valid
+ *   out [n_layers][B][Hq][d]            attention outputs
+ * seq_len = t+1 (current token included, decode_engine.hpp:98).  Stream
+ * ordered; the index cache (sets_) is updated in place. */
+int lyc_decoder_step(lyc_decoder* dec, const void* q, const void* k, const void* v,
+                     int64_t seq_len, void* out, void* stream);
+
+/* Single layer (decode_engine.hpp:120-143): q_l/out_l are [B][Hq][d]; k/v are
+ * the full caches.  Layers must be issued in order within a step. */
+int lyc_decoder_layer(lyc_decoder* dec, int32_t layer, const void* q_l, const void* k,
+                      const void* v, int64_t seq_len, void* out_l, void* stream);
+
+/* Capture lyc_decoder_step into a CUDA graph for fixed pointers / seq_len,
+ * then replay it.  replay returns LYC_ESTATE if nothing was captured. */
+int lyc_decoder_capture(lyc_decoder* dec, const void* q, const void* k, const void* v,
+                        int64_t seq_len, void* out, void* stream);
+int lyc_decoder_replay(lyc_decoder* dec, void* stream);
+
+/* The device index cache: ids [B*H][k_cap] int32 (ascending token ids, or
+ * block ids in blocks mode), counts [B*H] int32. */
+int lyc_decoder_index_cache(lyc_decoder* dec, int32_t** ids, int32_t** counts, int64_t* k_cap);
+
+/* Number of kernel launches one step issues (for the bench's gpu_launches). */
+int64_t lyc_decoder_launches_per_step(lyc_decoder* dec, int64_t seq_len);
+
+/* Algorithmic HBM bytes of one step: K/V rows touched + Q
+ * in + O out + index reads/writes. */
+int64_t lyc_decoder_step_bytes(lyc_decoder* dec, int64_t seq_len);
+
+/* Algorithmic HBM bytes of layer `layer`'s attention kernel (K/V rows + Q + O). */
+int64_t lyc_decoder_layer_attn_bytes(lyc_decoder* dec, int32_t layer, int64_t seq_len);
+
+/* Kernel timing: when enabled, CUDA events bracket every attention-kernel
+ * launch of subsequent steps (also inside a captured graph, as event nodes).
+ * lyc_decoder_attn_ms fills ms[n_layers] with the durations of the most recent
+ * completed step (synchronises on the last event). */
+int lyc_decoder_set_timing(lyc_decoder* dec, int enable);
+int lyc_decoder_attn_ms(lyc_decoder* dec, float* ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LYC_H_ */

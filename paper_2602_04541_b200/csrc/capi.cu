@@ -1,0 +1,826 @@
+// capi.cu -- host side of the C-ABI (include/lyc.h): validation with the
+// reference's error semantics, the pooled split planner (kernel_sim.hpp:63-110),
+// device plan upload, kernel launches and CUDA-graph capture of a decode step.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/lyc.h"
+#include "lyc_plan.h"
+
+namespace lyc {
+cudaError_t launch_attn(const LycAttnParams& p, int dtype, int d, int batch, cudaStream_t st);
+int attn_stages(int dtype, int d);
+cudaError_t launch_merge(const LycMergeParams& p, int dtype, cudaStream_t st);
+cudaError_t launch_topk(const LycTopkParams& p, int rows, int cluster, cudaStream_t st);
+int topk_cluster_size(int n, int max_slice);
+size_t topk_smem_bytes(int slice);
+cudaError_t launch_float_keys(const float* s, uint32_t* keys, int64_t n, cudaStream_t st);
+}  // namespace lyc
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& m) { throw Error{code, m}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(LYC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+int64_t guarded(F&& f) {
+  try {
+    return f();
+  } catch (const Error& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return LYC_ECUDA;
+  }
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
+int elem_bytes(int dtype) { return dtype == LYC_DTYPE_BF16 ? 2 : 4; }
+
+bool supported_d(int dtype, int64_t d) {
+  if (dtype == LYC_DTYPE_BF16) return d == 64 || d == 128 || d == 256;
+  if (dtype == LYC_DTYPE_F32) return d == 16 || d == 32 || d == 64 || d == 128;
+  return false;
+}
+
+// ------------------------------------------------------------- planner
+// plan_splits (kernel_sim.hpp:63-110): per batch item the concatenated
+// per-head item lists are cut into num_splits chunks of base + (s < rem)
+// items, then mapped back to (head, begin, end, head_local_split) units.
+struct HostLaunch {
+  std::vector<LycSlot> slots;        // [B*H]
+  std::vector<LycUnit> units;
+  std::vector<int32_t> split_off;    // [B*S + 1]
+  std::vector<LycMergeTask> merges;
+  std::vector<int32_t> sel_rows;     // selection index -> index-cache row
+  int batch = 0, heads = 0, splits = 0;
+};
+
+void plan_launch(HostLaunch& L, int batch, int heads, int splits, int group) {
+  L.batch = batch;
+  L.heads = heads;
+  L.splits = splits;
+  L.units.clear();
+  L.split_off.assign((size_t)batch * splits + 1, 0);
+  L.merges.clear();
+  for (int b = 0; b < batch; ++b) {
+    int64_t total = 0;
+    for (int g = 0; g < heads; ++g) {
+      LycSlot& s = L.slots[(size_t)b * heads + g];
+      s.n_units = 0;
+      s.first_unit = -1;
+      total += s.n_items;
+    }
+    if (total == 0) fail(LYC_EINVAL, "plan_splits: batch item has zero blocks");
+    const int64_t base = total / splits, rem = total % splits;
+    int head = 0;
+    int64_t offset = 0;
+    for (int s = 0; s < splits; ++s) {
+      L.split_off[(size_t)b * splits + s] = (int32_t)L.units.size();
+      int64_t want = base + (s < rem ? 1 : 0);
+      while (want > 0) {
+        while (L.slots[(size_t)b * heads + head].n_items == offset) {
+          ++head;
+          offset = 0;
+        }
+        LycSlot& sl = L.slots[(size_t)b * heads + head];
+        const int64_t take = std::min<int64_t>(sl.n_items - offset, want);
+        LycUnit u;
+        u.slot = b * heads + head;
+        u.begin = (int32_t)offset;
+        u.end = (int32_t)(offset + take);
+        u.hls = sl.n_units;
+        if (sl.n_units == 0) sl.first_unit = (int32_t)L.units.size();
+        sl.n_units++;
+        L.units.push_back(u);
+        offset += take;
+        want -= take;
+      }
+    }
+  }
+  L.split_off[(size_t)batch * splits] = (int32_t)L.units.size();
+  for (size_t i = 0; i < L.slots.size(); ++i)
+    if (L.slots[i].n_units > 1)
+      for (int j = 0; j < group; ++j) L.merges.push_back(LycMergeTask{(int32_t)i, j});
+}
+
+// Device copy of one HostLaunch; returns the device pointers inside `blob`.
+struct DevLaunch {
+  LycSlot* slots = nullptr;
+  LycUnit* units = nullptr;
+  int32_t* split_off = nullptr;
+  LycMergeTask* merges = nullptr;
+  int32_t* sel_rows = nullptr;
+  int n_units = 0, n_merges = 0, n_sel = 0;
+};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+size_t launch_bytes(const HostLaunch& L) {
+  return align_up(L.slots.size() * sizeof(LycSlot), 256) +
+         align_up(L.units.size() * sizeof(LycUnit), 256) +
+         align_up(L.split_off.size() * 4, 256) +
+         align_up(std::max<size_t>(1, L.merges.size()) * sizeof(LycMergeTask), 256) +
+         align_up(std::max<size_t>(1, L.sel_rows.size()) * 4, 256);
+}
+
+// Serialise L into host staging at `off` and return device pointers relative
+// to `dev_base`.
+DevLaunch stage_launch(const HostLaunch& L, std::vector<uint8_t>& host, size_t& off,
+                       uint8_t* dev_base) {
+  DevLaunch d;
+  auto put = [&](const void* src, size_t bytes, size_t reserve) -> void* {
+    if (host.size() < off + reserve) host.resize(off + reserve);
+    if (bytes) std::memcpy(host.data() + off, src, bytes);
+    void* dp = dev_base + off;
+    off += reserve;
+    return dp;
+  };
+  d.slots = (LycSlot*)put(L.slots.data(), L.slots.size() * sizeof(LycSlot),
+                          align_up(L.slots.size() * sizeof(LycSlot), 256));
+  d.units = (LycUnit*)put(L.units.data(), L.units.size() * sizeof(LycUnit),
+                          align_up(L.units.size() * sizeof(LycUnit), 256));
+  d.split_off = (int32_t*)put(L.split_off.data(), L.split_off.size() * 4,
+                              align_up(L.split_off.size() * 4, 256));
+  d.merges = (LycMergeTask*)put(L.merges.data(), L.merges.size() * sizeof(LycMergeTask),
+                                align_up(std::max<size_t>(1, L.merges.size()) * sizeof(LycMergeTask), 256));
+  d.sel_rows = (int32_t*)put(L.sel_rows.data(), L.sel_rows.size() * 4,
+                             align_up(std::max<size_t>(1, L.sel_rows.size()) * 4, 256));
+  d.n_units = (int)L.units.size();
+  d.n_merges = (int)L.merges.size();
+  d.n_sel = (int)L.sel_rows.size();
+  return d;
+}
+
+}  // namespace
+
+// =================================================================== C-ABI
+extern "C" {
+
+const char* lyc_last_error(void) { return g_err.c_str(); }
+const char* lyc_version(void) { return "lyc-b200 0.1 (sm_100a)"; }
+int64_t lyc_launch_count(void) { return g_launches; }
+
+int64_t lyc_plan_splits(int64_t batch, int64_t n_kv_heads, const int64_t* head_blocks,
+                        int64_t num_splits, int64_t* split_blocks, int64_t* head_split_count,
+                        int64_t* units, int64_t max_units) {
+  return guarded([&]() -> int64_t {
+    if (num_splits < 1) fail(LYC_EINVAL, "plan_splits: num_splits must be >= 1");
+    int64_t nu = 0;
+    for (int64_t b = 0; b < batch; ++b) {
+      int64_t total = 0;
+      for (int64_t g = 0; g < n_kv_heads; ++g) total += head_blocks[b * n_kv_heads + g];
+      if (total == 0) fail(LYC_EINVAL, "plan_splits: batch item has zero blocks");
+      const int64_t base = total / num_splits, rem = total % num_splits;
+      for (int64_t g = 0; g < n_kv_heads; ++g) head_split_count[b * n_kv_heads + g] = 0;
+      int64_t head = 0, offset = 0;
+      for (int64_t s = 0; s < num_splits; ++s) {
+        int64_t want = base + (s < rem ? 1 : 0);
+        split_blocks[b * num_splits + s] = want;
+        while (want > 0) {
+          while (head_blocks[b * n_kv_heads + head] == offset) {
+            ++head;
+            offset = 0;
+          }
+          const int64_t take = std::min(head_blocks[b * n_kv_heads + head] - offset, want);
+          if (units && nu < max_units) {
+            int64_t* u = units + nu * 6;
+            u[0] = b;
+            u[1] = s;
+            u[2] = head;
+            u[3] = offset;
+            u[4] = offset + take;
+            u[5] = head_split_count[b * n_kv_heads + head];
+          }
+          head_split_count[b * n_kv_heads + head]++;
+          ++nu;
+          offset += take;
+          want -= take;
+        }
+      }
+    }
+    return nu;
+  });
+}
+
+int lyc_latency_model(int64_t batch, int64_t n_kv_heads, const int64_t* head_blocks,
+                      int64_t num_splits, int64_t bytes_per_block, int64_t* out6, double* out2) {
+  return (int)guarded([&]() -> int64_t {
+    std::vector<int64_t> sb((size_t)(batch * std::max<int64_t>(num_splits, 1)));
+    std::vector<int64_t> hsc((size_t)(batch * n_kv_heads));
+    const int64_t nu = lyc_plan_splits(batch, n_kv_heads, head_blocks, num_splits, sb.data(),
+                                       hsc.data(), nullptr, 0);
+    if (nu < 0) fail((int)nu, g_err);
+    int64_t total = 0, pooled = 0, naive = 0, cells = 0;
+    for (int64_t b = 0; b < batch; ++b) {
+      for (int64_t s = 0; s < num_splits; ++s) {
+        total += sb[b * num_splits + s];
+        pooled = std::max(pooled, sb[b * num_splits + s]);
+        ++cells;
+      }
+      for (int64_t g = 0; g < n_kv_heads; ++g) naive = std::max(naive, head_blocks[b * n_kv_heads + g]);
+    }
+    const double mean = (double)total / (double)cells;
+    out6[0] = total;
+    out6[1] = pooled;
+    out6[2] = naive;
+    out6[3] = bytes_per_block;
+    out6[4] = pooled * bytes_per_block;
+    out6[5] = naive * bytes_per_block;
+    out2[0] = mean;
+    out2[1] = mean > 0.0 ? (double)pooled / mean : 0.0;
+    return LYC_OK;
+  });
+}
+
+int64_t lyc_fraction_budget(double frac, int64_t n) {
+  const double raw = frac * (double)n;
+  const double c = std::ceil(raw - 1e-9);
+  int64_t b = c < 0 ? 0 : (int64_t)c;
+  b = std::max<int64_t>(b, 1);
+  return std::min(b, n);
+}
+
+// ------------------------------------------------------------- kernel::run
+int lyc_workload_run(const lyc_workload* w, int64_t num_splits, void* out, uint32_t* exec_counts,
+                     void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!w) fail(LYC_EINVAL, "Workload: null");
+    if (w->batch < 1 || w->n_kv_heads < 1 || w->group_size < 1 || w->d_head < 1 ||
+        w->seq_len < 1 || w->block_size < 1)
+      fail(LYC_EINVAL, "Workload: all dimensions must be >= 1");
+    if (num_splits < 1) fail(LYC_EINVAL, "plan_splits: num_splits must be >= 1");
+    if (!supported_d(w->dtype, w->d_head)) fail(LYC_ENOTSUP, "Workload: unsupported d_head/dtype on device");
+    if (w->group_size > (w->dtype == LYC_DTYPE_BF16 ? 16 : 8))
+      fail(LYC_ENOTSUP, "Workload: group_size too large for the device kernel");
+    if (w->kv_row_stride < w->seq_len) fail(LYC_EINVAL, "Workload: kv_row_stride < seq_len");
+    const int64_t B = w->batch, H = w->n_kv_heads, G = w->group_size, D = w->d_head;
+    const int64_t nb = (w->seq_len + w->block_size - 1) / w->block_size;
+    // BlockIndexSet::validate (kernel_sim.hpp:27-41)
+    std::vector<int32_t> ids;
+    ids.reserve((size_t)w->blk_off[B * H]);
+    for (int64_t s = 0; s < B * H; ++s) {
+      if (w->blk_off[s + 1] < w->blk_off[s]) fail(LYC_EINVAL, "BlockIndexSet: slot count mismatch");
+      for (int64_t i = w->blk_off[s]; i < w->blk_off[s + 1]; ++i) {
+        const int64_t id = w->blk_ids[i];
+        if (id < 0 || id >= nb) fail(LYC_EINVAL, "BlockIndexSet: block id out of range");
+        if (i > w->blk_off[s] && id <= w->blk_ids[i - 1])
+          fail(LYC_EINVAL, "BlockIndexSet: block ids must be strictly ascending");
+        ids.push_back((int32_t)id);
+      }
+    }
+    HostLaunch L;
+    L.slots.resize((size_t)(B * H));
+    for (int64_t b = 0; b < B; ++b)
+      for (int64_t g = 0; g < H; ++g) {
+        LycSlot& s = L.slots[(size_t)(b * H + g)];
+        std::memset(&s, 0, sizeof(s));
+        s.kv_off = (b * H + g) * w->kv_row_stride * D;
+        s.kind = ITEM_BLOCKS;
+        s.n_items = (int32_t)(w->blk_off[b * H + g + 1] - w->blk_off[b * H + g]);
+        s.list_len = s.n_items;
+        s.q_row = (int32_t)(b * H * G + g * G);
+        s.sel = -1;
+      }
+    plan_launch(L, (int)B, (int)H, (int)num_splits, (int)G);
+    for (auto& s : L.slots)
+      if (s.n_units == 0) fail(LYC_EINVAL, "combine: head has no partials");
+    // device staging: [plan | ids | part_o | part_lse]
+    std::vector<uint8_t> host;
+    size_t off = 0;
+    const size_t plan_b = launch_bytes(L);
+    const size_t ids_b = align_up(std::max<size_t>(1, ids.size()) * 4, 256);
+    const size_t po_b = align_up((size_t)L.units.size() * G * D * 4, 256);
+    const size_t pl_b = align_up((size_t)L.units.size() * G * 4, 256);
+    uint8_t* dev = nullptr;
+    cuda_check(cudaMallocAsync((void**)&dev, plan_b + ids_b + po_b + pl_b, st), "cudaMallocAsync");
+    int32_t* d_ids = (int32_t*)(dev + plan_b);
+    for (int64_t s = 0; s < B * H; ++s) L.slots[(size_t)s].list = d_ids + w->blk_off[s];
+    DevLaunch dl = stage_launch(L, host, off, dev);
+    host.resize(plan_b + ids_b);
+    if (!ids.empty()) std::memcpy(host.data() + plan_b, ids.data(), ids.size() * 4);
+    cuda_check(cudaMemcpyAsync(dev, host.data(), host.size(), cudaMemcpyHostToDevice, st), "H2D plan");
+    LycAttnParams ap{};
+    ap.k = w->k;
+    ap.v = w->v;
+    ap.q = w->q;
+    ap.out = out;
+    ap.slots = dl.slots;
+    ap.units = dl.units;
+    ap.split_off = dl.split_off;
+    ap.part_o = (float*)(dev + plan_b + ids_b);
+    ap.part_lse = (float*)(dev + plan_b + ids_b + po_b);
+    ap.exec_counts = exec_counts;
+    ap.counts_stride = (int32_t)nb;
+    ap.n_splits = (int32_t)num_splits;
+    ap.seq_len = (int32_t)w->seq_len;
+    ap.block_size = (int32_t)w->block_size;
+    ap.group = (int32_t)G;
+    ap.sel_mode = SEL_NONE;
+    ap.scale = w->scale;
+    ap.scale_log2 = w->scale * 1.4426950408889634f;
+    cuda_check(lyc::launch_attn(ap, w->dtype, (int)D, (int)B, st), "attention launch");
+    ++g_launches;
+    if (dl.n_merges) {
+      LycMergeParams mp{};
+      mp.part_o = ap.part_o;
+      mp.part_lse = ap.part_lse;
+      mp.slots = dl.slots;
+      mp.tasks = dl.merges;
+      mp.out = out;
+      mp.n_tasks = dl.n_merges;
+      mp.group = (int32_t)G;
+      mp.chunks = (int32_t)((D + 31) / 32);
+      mp.d = (int32_t)D;
+      cuda_check(lyc::launch_merge(mp, w->dtype, st), "merge launch");
+      ++g_launches;
+    }
+    // the pageable host staging buffer must outlive the async copy
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    cuda_check(cudaFreeAsync(dev, st), "cudaFreeAsync");
+    return LYC_OK;
+  });
+}
+
+int64_t lyc_args_top_k(const float* scores, int64_t n, int64_t k, int32_t* out, void* stream) {
+  return guarded([&]() -> int64_t {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (k < 1) fail(LYC_EINVAL, "args_top_k: k must be >= 1");
+    const int64_t take = std::min(k, n);
+    if (take == 0) return 0;
+    if (n > (int64_t)16 * 32768) fail(LYC_ENOTSUP, "args_top_k: n too large for one cluster");
+    const int cluster = lyc::topk_cluster_size((int)n, 16384);
+    const int slice = (int)((n + cluster - 1) / cluster);
+    uint8_t* dev = nullptr;
+    cuda_check(cudaMallocAsync((void**)&dev, align_up((size_t)n * 4, 256) + 256, st), "cudaMallocAsync");
+    uint32_t* keys = (uint32_t*)dev;
+    int32_t* row = (int32_t*)(dev + align_up((size_t)n * 4, 256));
+    cuda_check(cudaMemsetAsync(row, 0, 4, st), "memset");
+    cuda_check(lyc::launch_float_keys(scores, keys, n, st), "keys launch");
+    LycTopkParams tp{};
+    tp.keys = keys;
+    tp.key_stride = n;
+    tp.n = (int32_t)n;
+    tp.k = (int32_t)take;
+    tp.out = out;
+    tp.out_row = row;
+    tp.out_stride = 0;
+    tp.out_count = nullptr;
+    tp.slice = slice;
+    tp.clear_keys = 0;
+    cuda_check(lyc::launch_topk(tp, 1, cluster, st), "topk launch");
+    g_launches += 2;
+    cuda_check(cudaFreeAsync(dev, st), "cudaFreeAsync");
+    return take;
+  });
+}
+
+// ------------------------------------------------------------- decoder
+struct lyc_decoder {
+  lyc_decode_config cfg{};
+  std::vector<uint8_t> roles;
+  int B = 0, H = 0, G = 0, Hq = 0, D = 0, NL = 0, S = 0, bs = 64;
+  int64_t k_cap = 0;
+  int32_t* idx = nullptr;      // [B*H][k_cap]
+  int32_t* idx_count = nullptr;
+  uint32_t* sel_keys = nullptr;
+  int64_t sel_stride = 0;
+  float* part_o = nullptr;
+  float* part_lse = nullptr;
+  size_t part_units = 0;
+  uint8_t* blob = nullptr;
+  size_t blob_cap = 0;
+  int64_t planned_seq = -1;
+  struct Layer {
+    LycAttnParams ap;
+    LycMergeParams mp;
+    LycTopkParams tp;
+    int n_sel = 0, cluster = 1, n_merges = 0;
+  };
+  std::vector<Layer> layers;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pre, ev_post;  // per layer, around the attention kernel
+  std::vector<uint8_t> staging;
+
+  bool retrieval(int l, int g) const { return l == 0 || roles[(size_t)l * H + g] == 0; }
+
+  int64_t budget(int64_t seq) const {  // tokens (or blocks) kept per sparse head
+    if (cfg.select_mode == LYC_SELECT_BLOCKS) {
+      const int64_t nb = (seq + bs - 1) / bs;
+      if (cfg.policy_kind == LYC_POLICY_RATIO) return lyc_fraction_budget(1.0 - cfg.ratio, nb);
+      return std::min<int64_t>((cfg.top_k + bs - 1) / bs, nb);
+    }
+    if (cfg.policy_kind == LYC_POLICY_RATIO) return lyc_fraction_budget(1.0 - cfg.ratio, seq);
+    return std::min<int64_t>(cfg.top_k, seq);
+  }
+};
+
+namespace {
+
+void decoder_plan(lyc_decoder* d, int64_t seq) {
+  if (seq < 1) fail(LYC_EINVAL, "decode_step: seq_len must be >= 1");
+  if (seq > d->cfg.seq_cap) fail(LYC_EINVAL, "decode_step: seq_len exceeds seq_cap");
+  if (seq > (int64_t)16 * 32768 && d->cfg.select_mode == LYC_SELECT_TOKENS)
+    fail(LYC_ENOTSUP, "decode_step: token-mode selection supports seq_len <= 524288");
+  if (d->planned_seq == seq) return;
+  const int B = d->B, H = d->H, G = d->G, D = d->D;
+  const int64_t kb = d->budget(seq);
+  const bool blocks = d->cfg.select_mode == LYC_SELECT_BLOCKS;
+  const int64_t nb = (seq + d->bs - 1) / d->bs;
+  std::vector<HostLaunch> hl((size_t)d->NL);
+  size_t total = 0, max_units = 0;
+  for (int l = 0; l < d->NL; ++l) {
+    HostLaunch& L = hl[(size_t)l];
+    L.slots.resize((size_t)B * H);
+    for (int b = 0; b < B; ++b)
+      for (int g = 0; g < H; ++g) {
+        LycSlot& s = L.slots[(size_t)b * H + g];
+        std::memset(&s, 0, sizeof(s));
+        s.kv_off = (((int64_t)l * B + b) * H + g) * d->cfg.seq_cap * D;
+        s.q_row = b * H * G + g * G;
+        if (d->retrieval(l, g)) {
+          s.kind = ITEM_DENSE;
+          s.n_items = (int32_t)nb;
+          if (d->cfg.select_mode != LYC_SELECT_NONE) {
+            s.sel = (int32_t)L.sel_rows.size();
+            L.sel_rows.push_back(b * H + g);
+          } else {
+            s.sel = -1;
+          }
+        } else {
+          s.kind = blocks ? ITEM_BLOCKS : ITEM_TOKENS;
+          s.list = d->idx + (int64_t)(b * H + g) * d->k_cap;
+          s.list_len = (int32_t)kb;
+          s.n_items = blocks ? (int32_t)kb : (int32_t)((kb + LYC_TILE - 1) / LYC_TILE);
+          s.sel = -1;
+        }
+      }
+    plan_launch(L, B, H, d->S, G);
+    total += launch_bytes(L);
+    max_units = std::max(max_units, L.units.size());
+  }
+  if (max_units > d->part_units) {
+    cudaFree(d->part_o);
+    cudaFree(d->part_lse);
+    d->part_o = d->part_lse = nullptr;
+    cuda_check(cudaMalloc(&d->part_o, max_units * G * D * 4), "cudaMalloc part_o");
+    cuda_check(cudaMalloc(&d->part_lse, max_units * G * 4), "cudaMalloc part_lse");
+    d->part_units = max_units;
+  }
+  if (total > d->blob_cap) {
+    cudaFree(d->blob);
+    d->blob = nullptr;
+    cuda_check(cudaMalloc(&d->blob, total), "cudaMalloc plan");
+    d->blob_cap = total;
+  }
+  d->staging.assign(total, 0);
+  size_t off = 0;
+  d->layers.assign((size_t)d->NL, {});
+  const int64_t sel_n = blocks ? nb : seq;
+  const int cluster = lyc::topk_cluster_size((int)sel_n, 16384);
+  for (int l = 0; l < d->NL; ++l) {
+    HostLaunch& L = hl[(size_t)l];
+    DevLaunch dl = stage_launch(L, d->staging, off, d->blob);
+    lyc_decoder::Layer& ly = d->layers[(size_t)l];
+    LycAttnParams& ap = ly.ap;
+    std::memset(&ap, 0, sizeof(ap));
+    ap.slots = dl.slots;
+    ap.units = dl.units;
+    ap.split_off = dl.split_off;
+    ap.part_o = d->part_o;
+    ap.part_lse = d->part_lse;
+    ap.sel_keys = d->sel_keys;
+    ap.sel_stride = d->sel_stride;
+    ap.n_splits = d->S;
+    ap.seq_len = (int32_t)seq;
+    ap.block_size = d->bs;
+    ap.group = G;
+    ap.sel_mode = d->cfg.select_mode == LYC_SELECT_NONE ? SEL_NONE
+                  : blocks ? SEL_BLOCK_KEYS : SEL_TOKEN_KEYS;
+    ap.scale = d->cfg.scale;
+    ap.scale_log2 = d->cfg.scale * 1.4426950408889634f;
+    LycMergeParams& mp = ly.mp;
+    std::memset(&mp, 0, sizeof(mp));
+    mp.part_o = d->part_o;
+    mp.part_lse = d->part_lse;
+    mp.slots = dl.slots;
+    mp.tasks = dl.merges;
+    mp.n_tasks = dl.n_merges;
+    mp.group = G;
+    mp.chunks = (D + 31) / 32;
+    mp.d = D;
+    ly.n_merges = dl.n_merges;
+    LycTopkParams& tp = ly.tp;
+    std::memset(&tp, 0, sizeof(tp));
+    tp.keys = d->sel_keys;
+    tp.key_stride = d->sel_stride;
+    tp.n = (int32_t)sel_n;
+    tp.k = (int32_t)kb;
+    tp.out = d->idx;
+    tp.out_row = dl.sel_rows;
+    tp.out_stride = d->k_cap;
+    tp.out_count = d->idx_count;
+    tp.slice = (int32_t)((sel_n + cluster - 1) / cluster);
+    tp.clear_keys = blocks ? 1 : 0;
+    ly.n_sel = dl.n_sel;
+    ly.cluster = cluster;
+  }
+  cuda_check(cudaMemcpy(d->blob, d->staging.data(), total, cudaMemcpyHostToDevice), "H2D plan");
+  d->planned_seq = seq;
+}
+
+void decoder_layer(lyc_decoder* d, int l, const void* q_l, const void* k, const void* v,
+                   void* out_l, cudaStream_t st) {
+  lyc_decoder::Layer& ly = d->layers[(size_t)l];
+  ly.ap.k = k;
+  ly.ap.v = v;
+  ly.ap.q = q_l;
+  ly.ap.out = out_l;
+  if (d->timing) cuda_check(cudaEventRecord(d->ev_pre[(size_t)l], st), "event record");
+  cuda_check(lyc::launch_attn(ly.ap, d->cfg.dtype, d->D, d->B, st), "attention launch");
+  if (d->timing) cuda_check(cudaEventRecord(d->ev_post[(size_t)l], st), "event record");
+  ++g_launches;
+  if (ly.n_merges) {
+    ly.mp.out = out_l;
+    cuda_check(lyc::launch_merge(ly.mp, d->cfg.dtype, st), "merge launch");
+    ++g_launches;
+  }
+  if (ly.n_sel) {
+    cuda_check(lyc::launch_topk(ly.tp, ly.n_sel, ly.cluster, st), "topk launch");
+    ++g_launches;
+  }
+}
+
+void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, int64_t seq,
+                  void* out, cudaStream_t st) {
+  decoder_plan(d, seq);
+  const size_t qstride = (size_t)d->B * d->Hq * d->D * elem_bytes(d->cfg.dtype);
+  for (int l = 0; l < d->NL; ++l)
+    decoder_layer(d, l, (const uint8_t*)q + l * qstride, k, v, (uint8_t*)out + l * qstride, st);
+}
+
+}  // namespace
+
+int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
+  return (int)guarded([&]() -> int64_t {
+    if (!cfg || !out) fail(LYC_EINVAL, "decoder: null argument");
+    const lyc_decode_config& c = *cfg;
+    if (c.n_layers < 1 || c.batch < 1 || c.n_kv_heads < 1 || c.group_size < 1 || c.d_head < 1 ||
+        c.seq_cap < 1)
+      fail(LYC_EINVAL, "ModelConfig: all dimensions must be >= 1");
+    if (!supported_d(c.dtype, c.d_head)) fail(LYC_ENOTSUP, "decoder: unsupported d_head/dtype");
+    if (c.group_size > (c.dtype == LYC_DTYPE_BF16 ? 16 : 8))
+      fail(LYC_ENOTSUP, "decoder: group_size too large for the device kernel");
+    if (c.policy_kind == LYC_POLICY_TOPK) {
+      if (c.top_k < 1) fail(LYC_EINVAL, "top_k: k must be >= 1");
+    } else if (c.policy_kind == LYC_POLICY_RATIO) {
+      if (!(c.ratio > 0.0 && c.ratio < 1.0)) fail(LYC_EINVAL, "ratio: theta must lie in (0,1)");
+    } else if (c.policy_kind == LYC_POLICY_TOPP || c.policy_kind == LYC_POLICY_THRESHOLD) {
+      fail(LYC_ENOTSUP, "decoder: TopP/Threshold selection is not implemented on device");
+    } else {
+      fail(LYC_EINVAL, "decoder: unknown policy");
+    }
+    if (c.select_mode != LYC_SELECT_TOKENS && c.select_mode != LYC_SELECT_BLOCKS &&
+        c.select_mode != LYC_SELECT_NONE)
+      fail(LYC_EINVAL, "decoder: unknown select mode");
+    if (c.select_mode == LYC_SELECT_NONE)
+      for (int64_t i = 0; i < (int64_t)c.n_layers * c.n_kv_heads; ++i)
+        if (c.roles[i] != 0) fail(LYC_EINVAL, "decoder: sparse heads need a selection mode");
+    if (c.block_size != 0 && c.block_size != 64) fail(LYC_ENOTSUP, "decoder: block_size must be 64");
+    if (!c.roles) fail(LYC_EINVAL, "RoleMap: null roles");
+    for (int g = 0; g < c.n_kv_heads; ++g)
+      if (c.roles[g] != 0) fail(LYC_EINVAL, "RoleMap: layer 0 heads must all be Retrieval");
+    auto* d = new lyc_decoder();
+    d->cfg = c;
+    d->roles.assign(c.roles, c.roles + (size_t)c.n_layers * c.n_kv_heads);
+    d->cfg.roles = nullptr;
+    if (d->cfg.scale == 0.f) d->cfg.scale = (float)(1.0 / std::sqrt((double)c.d_head));
+    d->B = c.batch;
+    d->H = c.n_kv_heads;
+    d->G = c.group_size;
+    d->Hq = d->H * d->G;
+    d->D = c.d_head;
+    d->NL = c.n_layers;
+    d->bs = 64;
+    d->S = c.num_splits > 0 ? c.num_splits : std::max(1, num_sms() / d->B);
+    const int64_t nb_cap = (c.seq_cap + d->bs - 1) / d->bs;
+    if (c.select_mode == LYC_SELECT_BLOCKS) {
+      d->k_cap = c.policy_kind == LYC_POLICY_RATIO ? nb_cap
+                                                   : std::min<int64_t>((c.top_k + 63) / 64, nb_cap);
+      d->sel_stride = nb_cap;
+    } else {
+      d->k_cap = c.policy_kind == LYC_POLICY_RATIO ? c.seq_cap : std::min<int64_t>(c.top_k, c.seq_cap);
+      d->sel_stride = c.seq_cap;
+    }
+    try {
+      const size_t rows = (size_t)d->B * d->H;
+      cuda_check(cudaMalloc(&d->idx, rows * d->k_cap * 4), "cudaMalloc index cache");
+      cuda_check(cudaMalloc(&d->idx_count, rows * 4), "cudaMalloc index counts");
+      cuda_check(cudaMemset(d->idx, 0, rows * d->k_cap * 4), "memset");
+      cuda_check(cudaMemset(d->idx_count, 0, rows * 4), "memset");
+      cuda_check(cudaMalloc(&d->sel_keys, rows * d->sel_stride * 4), "cudaMalloc keys");
+      cuda_check(cudaMemset(d->sel_keys, 0, rows * d->sel_stride * 4), "memset");
+    } catch (...) {
+      lyc_decoder_destroy(d);
+      throw;
+    }
+    *out = d;
+    return LYC_OK;
+  });
+}
+
+int lyc_decoder_destroy(lyc_decoder* d) {
+  if (!d) return LYC_OK;
+  if (d->exec) cudaGraphExecDestroy(d->exec);
+  for (auto e : d->ev_pre) cudaEventDestroy(e);
+  for (auto e : d->ev_post) cudaEventDestroy(e);
+  if (d->graph) cudaGraphDestroy(d->graph);
+  cudaFree(d->idx);
+  cudaFree(d->idx_count);
+  cudaFree(d->sel_keys);
+  cudaFree(d->part_o);
+  cudaFree(d->part_lse);
+  cudaFree(d->blob);
+  delete d;
+  return LYC_OK;
+}
+
+int lyc_decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, int64_t seq_len,
+                     void* out, void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    decoder_step(d, q, k, v, seq_len, out, (cudaStream_t)stream);
+    return LYC_OK;
+  });
+}
+
+int lyc_decoder_layer(lyc_decoder* d, int32_t layer, const void* q_l, const void* k, const void* v,
+                      int64_t seq_len, void* out_l, void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    if (layer < 0 || layer >= d->NL) fail(LYC_EINVAL, "decoder: layer out of range");
+    decoder_plan(d, seq_len);
+    decoder_layer(d, layer, q_l, k, v, out_l, (cudaStream_t)stream);
+    return LYC_OK;
+  });
+}
+
+int lyc_decoder_capture(lyc_decoder* d, const void* q, const void* k, const void* v,
+                        int64_t seq_len, void* out, void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    cudaStream_t st = (cudaStream_t)stream;
+    decoder_plan(d, seq_len);  // host work + plan upload outside the capture
+    if (d->exec) {
+      cudaGraphExecDestroy(d->exec);
+      d->exec = nullptr;
+    }
+    if (d->graph) {
+      cudaGraphDestroy(d->graph);
+      d->graph = nullptr;
+    }
+    const int64_t before = g_launches;
+    cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+    try {
+      decoder_step(d, q, k, v, seq_len, out, st);
+    } catch (...) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(st, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    g_launches = before;  // captured launches execute on replay
+    cuda_check(cudaStreamEndCapture(st, &d->graph), "end capture");
+    cuda_check(cudaGraphInstantiate(&d->exec, d->graph, 0), "graph instantiate");
+    return LYC_OK;
+  });
+}
+
+int lyc_decoder_replay(lyc_decoder* d, void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    if (!d || !d->exec) fail(LYC_ESTATE, "decoder: no captured step");
+    cuda_check(cudaGraphLaunch(d->exec, (cudaStream_t)stream), "graph launch");
+    g_launches += lyc_decoder_launches_per_step(d, d->planned_seq);
+    return LYC_OK;
+  });
+}
+
+int lyc_decoder_index_cache(lyc_decoder* d, int32_t** ids, int32_t** counts, int64_t* k_cap) {
+  if (!d) return LYC_EINVAL;
+  if (ids) *ids = d->idx;
+  if (counts) *counts = d->idx_count;
+  if (k_cap) *k_cap = d->k_cap;
+  return LYC_OK;
+}
+
+int64_t lyc_decoder_launches_per_step(lyc_decoder* d, int64_t seq_len) {
+  return guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    decoder_plan(d, seq_len);
+    int64_t n = 0;
+    for (auto& ly : d->layers) n += 1 + (ly.n_merges > 0) + (ly.n_sel > 0);
+    return n;
+  });
+}
+
+int64_t lyc_decoder_step_bytes(lyc_decoder* d, int64_t seq) {
+  return guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    const int64_t e = elem_bytes(d->cfg.dtype), D = d->D;
+    const int64_t kb = d->budget(seq);
+    const bool blocks = d->cfg.select_mode == LYC_SELECT_BLOCKS;
+    const int64_t sparse_rows = blocks ? std::min<int64_t>(kb * d->bs, seq) : kb;
+    int64_t bytes = 0;
+    for (int l = 0; l < d->NL; ++l)
+      for (int g = 0; g < d->H; ++g) {
+        const bool r = d->retrieval(l, g);
+        bytes += (int64_t)d->B * ((r ? seq : sparse_rows) * 2 * D * e + 4 * kb);
+      }
+    bytes += (int64_t)d->NL * d->B * d->Hq * D * e * 2;  // Q in, O out
+    return bytes;
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int64_t lyc_decoder_layer_attn_bytes(lyc_decoder* d, int32_t layer, int64_t seq) {
+  return guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    if (layer < 0 || layer >= d->NL) fail(LYC_EINVAL, "decoder: layer out of range");
+    const int64_t e = elem_bytes(d->cfg.dtype), D = d->D;
+    const int64_t kb = d->cfg.select_mode == LYC_SELECT_NONE ? seq : d->budget(seq);
+    const bool blocks = d->cfg.select_mode == LYC_SELECT_BLOCKS;
+    const int64_t sparse_rows = blocks ? std::min<int64_t>(kb * d->bs, seq) : kb;
+    int64_t bytes = 0;
+    for (int g = 0; g < d->H; ++g) {
+      const bool r = d->retrieval(layer, g);
+      bytes += (int64_t)d->B * ((r ? seq : sparse_rows) * 2 * D * e + (r ? 0 : 4 * kb));
+    }
+    bytes += (int64_t)d->B * d->Hq * D * e * 2;  // Q in, O out
+    return bytes;
+  });
+}
+
+int lyc_decoder_set_timing(lyc_decoder* d, int enable) {
+  return (int)guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    if (enable && d->ev_pre.empty()) {
+      d->ev_pre.resize((size_t)d->NL);
+      d->ev_post.resize((size_t)d->NL);
+      for (int l = 0; l < d->NL; ++l) {
+        cuda_check(cudaEventCreate(&d->ev_pre[(size_t)l]), "event create");
+        cuda_check(cudaEventCreate(&d->ev_post[(size_t)l]), "event create");
+      }
+    }
+    d->timing = enable != 0;
+    return LYC_OK;
+  });
+}
+
+int lyc_decoder_attn_ms(lyc_decoder* d, float* ms) {
+  return (int)guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    if (d->ev_pre.empty()) fail(LYC_ESTATE, "decoder: timing was never enabled");
+    cuda_check(cudaEventSynchronize(d->ev_post.back()), "event sync");
+    for (int l = 0; l < d->NL; ++l)
+      cuda_check(cudaEventElapsedTime(&ms[l], d->ev_pre[(size_t)l], d->ev_post[(size_t)l]),
+                 "event elapsed");
+    return LYC_OK;
+  });
+}
+
+}  // extern "C"

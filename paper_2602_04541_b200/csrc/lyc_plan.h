@@ -1,0 +1,95 @@
+// lyc_plan.h -- device work descriptors shared by the host planner (capi.cu)
+// and the kernels (attn.cu, epilogue.cu).  Plain structs, uploaded once per
+// plan and read-only on the device.
+//
+// A "slot" is one (batch item b, KV head g) of one launch.  Its work list is
+// a sequence of ITEMS; each item expands to ceil(block_size/64) TILES of <= 64
+// KV rows (the kernels' unit of TMA staging):
+//   ITEM_DENSE  item i -> rows [i*bs, min((i+1)*bs, seq))          retrieval head
+//   ITEM_BLOCKS item i -> rows of block list[i]                     BlockIndexSet
+//   ITEM_TOKENS item i -> rows list[i*64 .. min(i*64+64, list_len)) TokenSet
+// The pooled plan (kernel_sim.hpp:63-110) cuts each batch item's concatenated
+// item list into num_splits contiguous chunks; a chunk's per-slot pieces are
+// UNITS.  One CTA executes one split (Algorithm 2).
+#pragma once
+#include <stdint.h>
+
+#define LYC_TILE 64
+
+enum { ITEM_DENSE = 0, ITEM_BLOCKS = 1, ITEM_TOKENS = 2 };
+
+struct LycSlot {
+  int64_t kv_off;        // element offset of this slot's [S_cap][d] K/V slab
+  const int32_t* list;   // ITEM_BLOCKS: block ids; ITEM_TOKENS: token ids (device)
+  int32_t kind;          // ITEM_*
+  int32_t n_items;       // items in the work list
+  int32_t list_len;      // ITEM_TOKENS: number of token ids
+  int32_t first_unit;    // global index of the slot's first unit (units are consecutive)
+  int32_t n_units;       // head_split_count
+  int32_t q_row;         // first query/output row: b*Hq + g*G
+  int32_t sel;           // selection output row (-1: none)
+  int32_t pad;
+};
+
+struct LycUnit {
+  int32_t slot;
+  int32_t begin;  // item range [begin, end) in the slot's work list
+  int32_t end;
+  int32_t hls;    // head-local split id
+};
+
+// Selection outputs written by the attention kernel for slots with sel >= 0.
+enum { SEL_NONE = 0, SEL_TOKEN_KEYS = 1, SEL_BLOCK_KEYS = 2 };
+
+struct LycAttnParams {
+  const void* k;            // [...][S_cap][d] (slot kv_off)
+  const void* v;
+  const void* q;            // [rows][d]
+  void* out;                // [rows][d]
+  const LycSlot* slots;
+  const LycUnit* units;
+  const int32_t* split_off; // [B * n_splits + 1] unit ranges per (b, split)
+  float* part_o;            // [n_units][G][d]  normalized partial outputs
+  float* part_lse;          // [n_units][G]     base-2 log-sum-exp
+  uint32_t* sel_keys;       // [n_sel][sel_stride]
+  uint32_t* exec_counts;    // optional [n_slots][counts_stride] per item
+  int64_t sel_stride;
+  int32_t counts_stride;
+  int32_t n_splits;         // splits per batch item (grid.x)
+  int32_t seq_len;
+  int32_t block_size;
+  int32_t group;            // G
+  int32_t sel_mode;         // SEL_*
+  float scale;              // softmax scale (1/sqrt(d))
+  float scale_log2;         // scale * log2(e)
+};
+
+struct LycMergeTask {       // one (slot, q head j) pair needing a split-KV merge
+  int32_t slot;
+  int32_t j;
+};
+
+struct LycMergeParams {
+  const float* part_o;
+  const float* part_lse;
+  const LycSlot* slots;
+  const LycMergeTask* tasks;
+  void* out;
+  int32_t n_tasks;
+  int32_t group;
+  int32_t chunks;           // ceil(d / 32)
+  int32_t d;
+};
+
+struct LycTopkParams {
+  uint32_t* keys;           // [n_sel][key_stride] order-preserving keys
+  int64_t key_stride;
+  int32_t n;                // candidates per selection row (seq_len or n_blocks)
+  int32_t k;                // how many to keep (already min(k, n))
+  int32_t* out;             // index cache base
+  const int32_t* out_row;   // [n_sel] -> row in the index cache
+  int64_t out_stride;       // index cache row stride (k_cap)
+  int32_t* out_count;       // [cache rows] number of ids written (may be null)
+  int32_t slice;            // keys per CTA of the cluster
+  int32_t clear_keys;       // zero keys after use (block-max keys are atomicMax'ed)
+};

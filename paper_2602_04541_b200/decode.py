@@ -1,0 +1,210 @@
+"""Mirror of the reference decode-step attention loop and its selection API.
+
+* ``SparsityPolicy`` / ``fraction_budget`` -- policy.hpp:20-62 (TopK and Ratio
+  run on the device; TopP / Threshold raise ``NotSupported``).
+* ``args_top_k``   -- attention.hpp:108-123 on a device score vector.
+* ``HybridDecoder`` -- decode_engine.hpp:109-151: per layer, retrieval heads
+  (layer 0, or role R in the RoleMap, rolemap.hpp:33-35) run dense split-KV
+  attention and refresh the per-KV-head index cache (``sets_``,
+  decode_engine.hpp:251) from the pooled-query scores; sparse heads attend to
+  the set inherited from the nearest earlier retrieval layer of the same head
+  index.  All of it runs in the in-tree ``liblyc.so``.
+
+Device layouts (the C-ABI, include/lyc.h):
+  q, out : [n_layers][B][Hq][d]          K, V : [n_layers][B][H][seq_cap][d]
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import InvalidArgument, NotSupported, check, lib
+
+
+def fraction_budget(frac: float, n: int) -> int:
+    """policy.hpp:57-62."""
+    return int(lib().lyc_fraction_budget(float(frac), int(n)))
+
+
+@dataclass
+class SparsityPolicy:
+    """policy.hpp:20-53."""
+    kind: str = "topk"
+    k: int = 1
+    value: float = 0.0
+
+    @staticmethod
+    def top_k(k: int) -> "SparsityPolicy":
+        if k < 1:
+            raise InvalidArgument("top_k: k must be >= 1")
+        return SparsityPolicy("topk", k, 0.0)
+
+    @staticmethod
+    def ratio(theta: float) -> "SparsityPolicy":
+        if not (0.0 < theta < 1.0):
+            raise InvalidArgument("ratio: theta must lie in (0,1)")
+        return SparsityPolicy("ratio", 0, theta)
+
+    @staticmethod
+    def top_p(p: float) -> "SparsityPolicy":
+        if not (0.0 < p <= 1.0):
+            raise InvalidArgument("top_p: p must lie in (0,1]")
+        return SparsityPolicy("topp", 0, p)
+
+    @staticmethod
+    def threshold(tau: float) -> "SparsityPolicy":
+        if not (tau > 0.0):
+            raise InvalidArgument("threshold: tau must be positive")
+        return SparsityPolicy("threshold", 0, tau)
+
+    def code(self) -> int:
+        return {"topk": _lib.POLICY_TOPK, "topp": _lib.POLICY_TOPP,
+                "threshold": _lib.POLICY_THRESHOLD, "ratio": _lib.POLICY_RATIO}[self.kind]
+
+    def budget(self, n: int) -> int:
+        if self.kind == "topk":
+            return min(self.k, n)
+        if self.kind == "ratio":
+            return fraction_budget(1.0 - self.value, n)
+        raise NotSupported(f"{self.kind}: data-dependent budget")
+
+
+def args_top_k(scores: torch.Tensor, k: int, *, stream=None) -> torch.Tensor:
+    """attention.hpp:108-123 on the GPU: indices of the min(k, n) largest
+    fp32 scores, ties to the lower index, ascending (int32 device tensor)."""
+    s = scores.to(torch.float32).contiguous()
+    if not s.is_cuda:
+        s = s.cuda()
+    n = s.numel()
+    out = torch.empty(max(min(k, n), 1), dtype=torch.int32, device=s.device)
+    st = stream if stream is not None else torch.cuda.current_stream(s.device)
+    cnt = check(lib().lyc_args_top_k(s.data_ptr(), n, k, out.data_ptr(), st.cuda_stream))
+    return out[:cnt]
+
+
+class HybridDecoder:
+    """Device decode engine for the hybrid-head attention of one step.
+
+    roles: [n_layers][n_kv_heads] with 0 = Retrieval, 1 = Sparse (RoleMap).
+    select: 'tokens' (TokenSet, decode_engine.hpp:132) or 'blocks'
+    (BlockIndexSet of ceil(k/64) blocks, the paper's block-sparse kernel)."""
+
+    def __init__(self, *, n_layers: int, batch: int, n_kv_heads: int, group_size: int,
+                 d_head: int, seq_cap: int, roles, policy: SparsityPolicy,
+                 dtype: torch.dtype = torch.bfloat16, select: str = "tokens",
+                 num_splits: int = 0, scale: float = 0.0):
+        self.n_layers, self.batch, self.n_kv_heads = n_layers, batch, n_kv_heads
+        self.group_size, self.d_head, self.seq_cap = group_size, d_head, seq_cap
+        self.dtype = dtype
+        self.policy = policy
+        self.select = select
+        r = np.ascontiguousarray(np.asarray(roles, dtype=np.uint8).reshape(n_layers, n_kv_heads))
+        self.roles = r
+        if policy.kind in ("topp", "threshold"):
+            raise NotSupported(f"{policy.kind}: not implemented on device")
+        cfg = _lib.lyc_decode_config(
+            n_layers=n_layers, batch=batch, n_kv_heads=n_kv_heads, group_size=group_size,
+            d_head=d_head,
+            dtype=_lib.DTYPE_BF16 if dtype == torch.bfloat16 else _lib.DTYPE_F32,
+            seq_cap=seq_cap, policy_kind=policy.code(),
+            select_mode={"tokens": _lib.SELECT_TOKENS, "blocks": _lib.SELECT_BLOCKS,
+                         "none": _lib.SELECT_NONE}[select],
+            top_k=policy.k, ratio=policy.value, block_size=64, num_splits=num_splits,
+            scale=scale, roles=r.ctypes.data)
+        h = C.c_void_p()
+        check(lib().lyc_decoder_create(C.byref(cfg), C.byref(h)))
+        self._h = h
+        self.captured = None
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().lyc_decoder_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _stream(stream):
+        return (stream if stream is not None else torch.cuda.current_stream()).cuda_stream
+
+    def decode_step(self, q, k_cache, v_cache, seq_len: int, out=None, *, stream=None):
+        """All layers of one step (decode_engine.hpp:109-151)."""
+        if out is None:
+            out = torch.empty_like(q)
+        check(lib().lyc_decoder_step(self._h, q.data_ptr(), k_cache.data_ptr(),
+                                     v_cache.data_ptr(), seq_len, out.data_ptr(),
+                                     self._stream(stream)))
+        return out
+
+    def layer(self, l: int, q_l, k_cache, v_cache, seq_len: int, out_l=None, *, stream=None):
+        """One layer (decode_engine.hpp:120-143); layers in order within a step."""
+        if out_l is None:
+            out_l = torch.empty_like(q_l)
+        check(lib().lyc_decoder_layer(self._h, l, q_l.data_ptr(), k_cache.data_ptr(),
+                                      v_cache.data_ptr(), seq_len, out_l.data_ptr(),
+                                      self._stream(stream)))
+        return out_l
+
+    def capture(self, q, k_cache, v_cache, seq_len: int, out, *, stream=None):
+        """Capture one step into a CUDA graph (fixed pointers and seq_len)."""
+        check(lib().lyc_decoder_capture(self._h, q.data_ptr(), k_cache.data_ptr(),
+                                        v_cache.data_ptr(), seq_len, out.data_ptr(),
+                                        self._stream(stream)))
+        self.captured = (q, k_cache, v_cache, seq_len, out)
+
+    def replay(self, *, stream=None):
+        check(lib().lyc_decoder_replay(self._h, self._stream(stream)))
+
+    def index_cache(self):
+        """(ids [B*H][k_cap] int32 device view, counts [B*H]) -- the sets_."""
+        ids, cnt, kcap = C.c_void_p(), C.c_void_p(), C.c_int64()
+        check(lib().lyc_decoder_index_cache(self._h, C.byref(ids), C.byref(cnt), C.byref(kcap)))
+        rows = self.batch * self.n_kv_heads
+        dev = torch.device("cuda", torch.cuda.current_device())
+        ids_t = _wrap_device(ids.value, rows * kcap.value, dev).view(rows, kcap.value)
+        cnt_t = _wrap_device(cnt.value, rows, dev)
+        return ids_t, cnt_t
+
+    def token_sets(self) -> List[List[np.ndarray]]:
+        """Host copy of the index cache as [b][g] ascending id arrays."""
+        ids, cnt = self.index_cache()
+        ids, cnt = ids.cpu().numpy(), cnt.cpu().numpy()
+        H = self.n_kv_heads
+        return [[ids[b * H + g, : cnt[b * H + g]].copy() for g in range(H)]
+                for b in range(self.batch)]
+
+    def launches_per_step(self, seq_len: int) -> int:
+        return check(lib().lyc_decoder_launches_per_step(self._h, seq_len))
+
+    def step_bytes(self, seq_len: int) -> int:
+        return check(lib().lyc_decoder_step_bytes(self._h, seq_len))
+
+    def layer_attn_bytes(self, layer: int, seq_len: int) -> int:
+        return check(lib().lyc_decoder_layer_attn_bytes(self._h, layer, seq_len))
+
+    def set_timing(self, enable: bool = True):
+        """CUDA events around every attention-kernel launch (graph-capturable)."""
+        check(lib().lyc_decoder_set_timing(self._h, int(bool(enable))))
+
+    def attn_ms(self) -> np.ndarray:
+        """Per-layer attention-kernel durations (ms) of the last completed step."""
+        ms = np.zeros(self.n_layers, dtype=np.float32)
+        check(lib().lyc_decoder_attn_ms(self._h, ms.ctypes.data))
+        return ms
+
+
+def _wrap_device(ptr: int, n: int, dev) -> torch.Tensor:
+    """Zero-copy int32 view of library-owned device memory (no ownership)."""
+    class _Holder:
+        __cuda_array_interface__ = {
+            "shape": (n,), "typestr": "<i4", "data": (ptr, False), "version": 3, "strides": None}
+    return torch.as_tensor(_Holder(), device=dev)

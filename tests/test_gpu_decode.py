@@ -1,0 +1,239 @@
+"""GPU parity of the hybrid-head decode step (decode_engine.hpp:109-151)
+against the oracle restatement of the same loop on identical inputs.
+
+Index sets: the GPU ranks fp32 pooled scores (sum_j q_j.k over the packed GQA
+rows, fused in the attention kernel); the oracle ranks f64 softmax weights of
+the pooled query (decode_engine.hpp:129-132).  Softmax is monotone, so the
+sets agree exactly except where fp rounding reorders scores that are equal to
+within DELTA of the k-th score (the documented tie band); swaps are counted
+and must lie inside that band.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-5
+BF16_TOL = 2e-2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2602_04541_b200  # noqa: F401
+    torch.cuda.set_device(0)
+
+
+def rel_err(got, ref):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    return np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-3)
+
+
+def synth(seed, NL, B, H, G, d, seq, seq_cap, dtype):
+    g = torch.Generator().manual_seed(seed)
+    q = (torch.rand((NL, B, H * G, d), generator=g) * 2 - 1).to(dtype)
+    K = (torch.rand((NL, B, H, seq_cap, d), generator=g) * 2 - 1).to(dtype)
+    V = (torch.rand((NL, B, H, seq_cap, d), generator=g) * 2 - 1).to(dtype)
+    return q, K, V
+
+
+def roles_for(NL, H, retrieval_above_0, seed=0):
+    r = np.ones((NL, H), dtype=np.uint8)
+    r[0] = 0
+    for (l, g) in retrieval_above_0:
+        r[l, g] = 0
+    return r
+
+
+def pooled_scores(q_l, K_lg, group, g, seq):
+    """f64 pooled-query scores (without scale) of head g at one layer."""
+    qq = q_l[g * group:(g + 1) * group].astype(np.float64)
+    pooled = qq.sum(0) / group
+    return K_lg[:seq].astype(np.float64) @ pooled
+
+
+def check_set(got, ref, scores, k, rel_band=2e-6):
+    """Exact, or swaps confined to |s - s_(k)| <= band."""
+    got, ref = set(got.tolist()), set(ref.tolist())
+    assert len(got) == len(ref)
+    if got == ref:
+        return 0
+    kth = np.sort(scores)[::-1][min(k, len(scores)) - 1]
+    band = rel_band * np.abs(scores).max() * 4
+    for t in got ^ ref:
+        assert abs(scores[t] - kth) <= band, (t, scores[t], kth)
+    return len(got - ref)
+
+
+def run_case(orc, *, NL, B, H, G, d, seq, seq_cap, dtype, roles, policy, select="tokens",
+             seed=0, layerwise=False):
+    import paper_2602_04541_b200 as P
+    q, K, V = synth(seed, NL, B, H, G, d, seq, seq_cap, dtype)
+    dec = P.HybridDecoder(n_layers=NL, batch=B, n_kv_heads=H, group_size=G, d_head=d,
+                          seq_cap=seq_cap, roles=roles, policy=policy, dtype=dtype, select=select)
+    qd, Kd, Vd = q.cuda(), K.cuda(), V.cuda()
+    traces = []
+    if layerwise:
+        out = torch.empty_like(qd)
+        for l in range(NL):
+            dec.layer(l, qd[l], Kd, Vd, seq, out[l])
+            traces.append(dec.token_sets())
+    else:
+        out = dec.decode_step(qd, Kd, Vd, seq)
+    torch.cuda.synchronize()
+    return dec, q.float().numpy(), K.float().numpy(), V.float().numpy(), out.float().cpu().numpy(), traces
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_tiny_config_fp32_token_mode(orc, seed):
+    """BASELINE configs[0]: 4 layers, 8 q / 2 KV heads, d 64, 4K context,
+    top-k 256, fp32, batch 1 -- outputs, final sets and per-layer traces."""
+    import paper_2602_04541_b200 as P
+    NL, B, H, G, d, seq = 4, 1, 2, 4, 64, 4096
+    roles = roles_for(NL, H, [(2, 1)])
+    dec, q, K, V, out, traces = run_case(orc, NL=NL, B=B, H=H, G=G, d=d, seq=seq, seq_cap=seq,
+                                         dtype=torch.float32, roles=roles,
+                                         policy=P.SparsityPolicy.top_k(256), seed=seed,
+                                         layerwise=True)
+    r = orc.decode_step(q[:, 0], K[:, 0], V[:, 0], roles, seq=seq, scale=1 / np.sqrt(d),
+                        kind="topk", k=256, trace=True)
+    assert rel_err(out[:, 0], r["out"]) < FP32_TOL
+    swaps = 0
+    for l in range(NL):
+        for g in range(H):
+            src = max(ll for ll in range(l + 1) if roles[ll, g] == 0 or ll == 0)
+            sc = pooled_scores(q[src, 0], K[src, 0, g], G, g, seq)
+            swaps += check_set(traces[l][0][g], r["trace"][l][g], sc, 256)
+    assert swaps == 0
+
+
+def test_llama_like_bf16_token_mode(orc):
+    """Llama-3-8B head shapes (32 q / 8 KV, d 128), bf16, shortened context."""
+    import paper_2602_04541_b200 as P
+    NL, B, H, G, d, seq = 3, 1, 8, 4, 128, 8192
+    roles = roles_for(NL, H, [(1, 3), (2, 5)])
+    dec, q, K, V, out, traces = run_case(orc, NL=NL, B=B, H=H, G=G, d=d, seq=seq, seq_cap=seq + 64,
+                                         dtype=torch.bfloat16, roles=roles,
+                                         policy=P.SparsityPolicy.top_k(512), seed=3,
+                                         layerwise=True)
+    Kc, Vc = K[:, 0], V[:, 0]
+    r = orc.decode_step(q[:, 0], Kc, Vc, roles, seq=seq, scale=1 / np.sqrt(d), kind="topk", k=512,
+                        trace=True)
+    assert rel_err(out[:, 0], r["out"]) < BF16_TOL
+    swaps = 0
+    for l in range(NL):
+        for g in range(H):
+            src = max(ll for ll in range(l + 1) if roles[ll, g] == 0)
+            sc = pooled_scores(q[src, 0], K[src, 0, g], G, g, seq)
+            swaps += check_set(traces[l][0][g], r["trace"][l][g], sc, 512)
+    print("tie-band swaps:", swaps)
+
+
+def test_batch_and_ratio_policy(orc):
+    """Batch > 1 (independent sequences) and the Ratio policy (policy.hpp:71-72)."""
+    import paper_2602_04541_b200 as P
+    NL, B, H, G, d, seq = 3, 3, 2, 2, 64, 1000
+    roles = roles_for(NL, H, [(1, 0)])
+    dec, q, K, V, out, _ = run_case(orc, NL=NL, B=B, H=H, G=G, d=d, seq=seq, seq_cap=1024,
+                                    dtype=torch.float32, roles=roles,
+                                    policy=P.SparsityPolicy.ratio(0.8), seed=5)
+    sets = dec.token_sets()
+    for b in range(B):
+        r = orc.decode_step(q[:, b], K[:, b], V[:, b], roles, seq=seq, scale=1 / np.sqrt(d),
+                            kind="ratio", value=0.8)
+        assert rel_err(out[:, b], r["out"]) < FP32_TOL
+        for g in range(H):
+            assert len(sets[b][g]) == orc.fraction_budget(0.2, seq)
+            assert np.array_equal(sets[b][g], r["sets"][g])
+
+
+def test_full_budget_sparse_equals_dense(orc):
+    """decode_engine_test.cpp:184-222: a budget >= seq makes sparse heads dense."""
+    import paper_2602_04541_b200 as P
+    NL, B, H, G, d, seq = 3, 1, 2, 4, 64, 700
+    sparse = roles_for(NL, H, [])
+    dense = np.zeros((NL, H), dtype=np.uint8)
+    _, q, K, V, out_s, _ = run_case(orc, NL=NL, B=B, H=H, G=G, d=d, seq=seq, seq_cap=768,
+                                    dtype=torch.float32, roles=sparse,
+                                    policy=P.SparsityPolicy.top_k(100000), seed=9)
+    _, _, _, _, out_d, _ = run_case(orc, NL=NL, B=B, H=H, G=G, d=d, seq=seq, seq_cap=768,
+                                    dtype=torch.float32, roles=dense,
+                                    policy=P.SparsityPolicy.top_k(4), seed=9)
+    assert rel_err(out_s, out_d) < FP32_TOL
+
+
+def test_block_mode_matches_composed_oracle(orc):
+    """Block-sparse selection (the paper's kernel): block score = max pooled
+    score over the block's rows; top ceil(k/64) blocks; kernel::run on them."""
+    import paper_2602_04541_b200 as P
+    NL, B, H, G, d, seq, k = 2, 1, 4, 4, 128, 4000, 640
+    roles = roles_for(NL, H, [])
+    dec, q, K, V, out, traces = run_case(orc, NL=NL, B=B, H=H, G=G, d=d, seq=seq, seq_cap=4096,
+                                         dtype=torch.bfloat16, roles=roles,
+                                         policy=P.SparsityPolicy.top_k(k), select="blocks",
+                                         seed=11, layerwise=True)
+    nblk = (k + 63) // 64
+    # layer 0: dense retrieval for every head
+    r0 = orc.kernel_run(K[0, 0, :, :seq], V[0, 0, :, :seq], q[0, 0], [list(range((seq + 63) // 64))] * H, batch=1,
+                        group=G, seq_len=seq, scale=1 / np.sqrt(d), dtype=np.float64,
+                        num_splits=4)
+    assert rel_err(out[0, 0], r0) < BF16_TOL
+    blocks = []
+    for g in range(H):
+        pq = q[0, 0, g * G:(g + 1) * G].astype(np.float64).mean(0)
+        ref_blocks = orc.block_select(pq, K[0, 0, g], seq, 1 / np.sqrt(d), 64, nblk)
+        got = traces[0][0][g]
+        if not np.array_equal(got, ref_blocks):
+            sc = orc.pooled_scores(pq, K[0, 0, g], seq, 1.0)
+            bm = np.array([sc[i * 64:(i + 1) * 64].max() for i in range((seq + 63) // 64)])
+            check_set(got, ref_blocks, bm, nblk)
+        blocks.append(got.tolist())
+    r1 = orc.kernel_run(K[1, 0, :, :seq], V[1, 0, :, :seq], q[1, 0], blocks, batch=1, group=G, seq_len=seq,
+                        scale=1 / np.sqrt(d), dtype=np.float64, num_splits=3)
+    assert rel_err(out[1, 0], r1) < BF16_TOL
+
+
+def test_graph_replay_matches_eager_and_is_deterministic(orc):
+    import paper_2602_04541_b200 as P
+    NL, B, H, G, d, seq = 4, 1, 8, 4, 128, 5000
+    roles = roles_for(NL, H, [(1, 2), (3, 7)])
+    q, K, V = synth(21, NL, B, H, G, d, seq, 5120, torch.bfloat16)
+    q, K, V = q.cuda(), K.cuda(), V.cuda()
+    dec = P.HybridDecoder(n_layers=NL, batch=B, n_kv_heads=H, group_size=G, d_head=d, seq_cap=5120,
+                          roles=roles, policy=P.SparsityPolicy.top_k(300))
+    eager = dec.decode_step(q, K, V, seq)
+    sets_eager = dec.token_sets()
+    out = torch.empty_like(q)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        dec.capture(q, K, V, seq, out, stream=s)
+        for _ in range(3):
+            dec.replay(stream=s)
+    s.synchronize()
+    assert torch.equal(out, eager)
+    sets = dec.token_sets()
+    assert all(np.array_equal(a, b) for ra, rb in zip(sets, sets_eager) for a, b in zip(ra, rb))
+
+
+def test_decoder_errors():
+    import paper_2602_04541_b200 as P
+    bad = np.ones((2, 2), dtype=np.uint8)  # layer 0 must be retrieval (rolemap.hpp:54-56)
+    with pytest.raises(P.InvalidArgument):
+        P.HybridDecoder(n_layers=2, batch=1, n_kv_heads=2, group_size=2, d_head=64, seq_cap=128,
+                        roles=bad, policy=P.SparsityPolicy.top_k(4))
+    with pytest.raises(P.InvalidArgument):
+        P.SparsityPolicy.top_k(0)
+    with pytest.raises(P.NotSupported):
+        P.HybridDecoder(n_layers=2, batch=1, n_kv_heads=2, group_size=2, d_head=64, seq_cap=128,
+                        roles=np.zeros((2, 2)), policy=P.SparsityPolicy.top_p(0.9))
+    dec = P.HybridDecoder(n_layers=2, batch=1, n_kv_heads=2, group_size=2, d_head=64, seq_cap=128,
+                          roles=np.zeros((2, 2)), policy=P.SparsityPolicy.top_k(4))
+    q = torch.zeros((2, 1, 4, 64), dtype=torch.bfloat16, device="cuda")
+    kv = torch.zeros((2, 1, 2, 128, 64), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(P.InvalidArgument):
+        dec.decode_step(q, kv, kv, 129)  # beyond seq_cap
+    with pytest.raises(P.LogicError):
+        dec.replay()
