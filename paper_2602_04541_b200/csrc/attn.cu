@@ -4,60 +4,68 @@
 //
 // One CTA executes one split of the pooled plan: a sequence of UNITS, each a
 // contiguous item range of one slot (b, KV head).  Retrieval (ITEM_DENSE),
-// block-sparse (ITEM_BLOCKS) and token-sparse (ITEM_TOKENS) slots share the
-// same pipeline; only the row addresses differ:
+// block-sparse (ITEM_BLOCKS) and token-sparse (ITEM_TOKENS) slots share one
+// smem ring of 64-row K/V tiles:
 //
-//   warp 4 (producer): for every 64-row tile, one lane per row issues a
-//     cp.async.bulk (TMA engine) of the K row and the V row into a padded
-//     smem ring (row stride d*e+16 B -> conflict-free ldmatrix), completion
-//     counted in bytes on the stage's mbarrier.  Gathered and contiguous
-//     tiles are the same instruction stream.
-//   warps 0-3 (consumers): each owns 16 rows of every tile; all G query heads
-//     of the GQA group are packed as the 16-row A operand of mma.sync
-//     m16n8k16 (bf16 -> fp32), so K and V are read from smem exactly once per
-//     tile for the whole group.  Online softmax (attention.hpp:161-181) in the
-//     exp2 domain with warp-shuffle row max/sum.
+//   warps 4-5 (producers):
+//     * full contiguous tiles (retrieval heads, selected blocks): one thread
+//       issues 2D tensor-map TMA boxes (64 rows x 128 B panel, 128B swizzle
+//       for bf16) -- 4 instructions per 32 KB stage, completion counted in
+//       bytes on the stage's mbarrier;
+//     * gathered tiles (token-sparse heads, ragged tails): all 64 producer
+//       threads issue coalesced 16-B cp.async (LDGSTS) of the indexed rows
+//       straight into the same swizzled layout, zero-filling masked rows, and
+//       arrive on the mbarrier when their copies land.
+//   warps 0-3 (consumers): each owns 16 rows of every tile; the G <= 8 query
+//     heads of the GQA group are packed as the A operand of mma.sync m16n8k16
+//     (bf16 -> fp32), so every K/V byte is read from smem once for the whole
+//     group.  Online softmax (attention.hpp:161-181) in the exp2 domain with
+//     quad-shuffle row max/sum; P goes C-fragment -> A-fragment in registers.
 //   Fused selection (retrieval slots with sel >= 0): the pooled-query score
-//   of every row, sum_j q_j.k (= G * pooled_q.k, attention.hpp:127-146 and
-//   decode_engine.hpp:129-132), is reduced across the packed rows with three
-//   shuffles and written as an order-preserving uint32 key (token mode) or
-//   atomically max-folded per block (block mode).
-//   End of unit: the 4 warps' (m, l, o) states are merged through smem and
-//   written as a normalized partial + base-2 LSE (kernel_sim.hpp:195-198), or
-//   directly as the final output when the slot has a single unit.
+//     sum_j q_j.k of every row (= G * pooled_q.k, attention.hpp:127-146,
+//     decode_engine.hpp:129-132) is reduced across the packed rows with three
+//     shuffles and written as an order-preserving uint32 key (token mode) or
+//     max-folded per block (block mode).
+//   End of unit: the 4 warps' (m, l, o) are merged through smem and written
+//     as a normalized partial + base-2 LSE (kernel_sim.hpp:195-198), or as
+//     the final output when the slot has a single unit.
 #include "lyc_common.cuh"
 #include "lyc_plan.h"
 
 namespace lyc {
 
 constexpr int kConsumerWarps = 4;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
-
-template <typename T>
-struct ElemBytes;
-template <>
-struct ElemBytes<__nv_bfloat16> {
-  static constexpr int v = 2;
-};
-template <>
-struct ElemBytes<float> {
-  static constexpr int v = 4;
-};
+constexpr int kProducerWarps = 2;
+constexpr int kProducerThreads = kProducerWarps * 32;
+constexpr int kThreads = (kConsumerWarps + kProducerWarps) * 32;
+constexpr int kMaxG = 8;
 
 template <typename T, int D>
 struct AttnCfg {
-  static constexpr int kRowBytes = D * ElemBytes<T>::v;
-  static constexpr int kRowStride = kRowBytes + 16;  // +16 B: rows rotate 4 banks
-  static constexpr int kTileBytes = LYC_TILE * kRowStride;
+  static constexpr int kE = (int)sizeof(T);
+  static constexpr bool kSwizzle = kE == 2;        // bf16 tiles: 128-B swizzled panels
+  static constexpr int kRowBytes = D * kE;
+  static constexpr int kPanelBytes = LYC_TILE * 128;
+  static constexpr int kTileBytes = LYC_TILE * kRowBytes;
   static constexpr int kStageBytes = 2 * kTileBytes;  // K tile then V tile
-  static constexpr int kMaxG = 16;
+  static constexpr int kChunksPerRow = kRowBytes / 16;
   static constexpr int kMergeBytes = kConsumerWarps * kMaxG * (D + 2) * 4;
-  static constexpr int kQBytes = (ElemBytes<T>::v == 4) ? (kMaxG + 1) * D * 4 : 0;
-  static constexpr int kBudget = 200 * 1024;
-  static constexpr int kStagesRaw = (kBudget - kMergeBytes - kQBytes) / kStageBytes;
+  static constexpr int kQBytes = kE == 4 ? (kMaxG + 1) * D * 4 : 0;
+  static constexpr int kMaxSmem = 232448 - 1024;   // 227 KB opt-in minus alignment slack
+  static constexpr int kFixed = kMergeBytes + kQBytes + 256;
+  static constexpr int kStagesRaw = (kMaxSmem - kFixed) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-  static constexpr int kSmem = kStages * kStageBytes + kMergeBytes + kQBytes + 2 * kStages * 8 + 16;
+  static constexpr int kSmem = kStages * kStageBytes + kFixed + 1024;
   static_assert(kStages >= 2, "not enough shared memory for a 2-stage ring");
+  static_assert(kRowBytes % 16 == 0 && (!kSwizzle || kRowBytes % 128 == 0), "row layout");
+
+  // byte offset of 16-B chunk c of tile row r
+  __device__ __forceinline__ static uint32_t off(int r, int c) {
+    if constexpr (kSwizzle)
+      return (uint32_t)((c >> 3) * kPanelBytes + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+    else
+      return (uint32_t)(r * kRowBytes + c * 16);
+  }
 };
 
 struct Tile {
@@ -87,47 +95,77 @@ __device__ __forceinline__ Tile tile_of(const LycSlot& s, int item, int sub, int
   return t;
 }
 
-__device__ __forceinline__ int tile_row(const Tile& t, int r) {
-  const int rr = r < t.nvalid ? r : 0;  // invalid rows re-load row 0 (finite data, masked)
-  return t.ids ? __ldg(t.ids + rr) : t.lo + rr;
-}
-
 // ---------------------------------------------------------------- producer
 template <typename T, int D>
 __device__ __forceinline__ void produce(const LycAttnParams& p, uint8_t* ring, uint64_t* full,
-                                        uint64_t* empty, int ub, int ue, int lane) {
+                                        uint64_t* empty, int ub, int ue, int pt) {
   using C = AttnCfg<T, D>;
+  constexpr int CPR = C::kChunksPerRow;
+  constexpr int kRowsPerRound = kProducerThreads / CPR > 0 ? kProducerThreads / CPR : 1;
+  constexpr int kRounds = LYC_TILE / kRowsPerRound;
+  static_assert(kProducerThreads % CPR == 0 || CPR % kProducerThreads == 0, "producer mapping");
   const uint64_t pol = policy_evict_first();
   const char* kbase = static_cast<const char*>(p.k);
   const char* vbase = static_cast<const char*>(p.v);
+  if (pt == 0) {
+    prefetch_tensormap(&p.tmap_k);
+    prefetch_tensormap(&p.tmap_v);
+  }
+  const int my_c = pt % CPR;
+  const int my_r0 = pt / CPR;
   int stage = 0;
   uint32_t phase = 0;
   for (int u = ub; u < ue; ++u) {
     const LycUnit un = p.units[u];
     const LycSlot s = p.slots[un.slot];
     const int tpi = tiles_per_item(s, p.block_size);
-    const int64_t slab = s.kv_off * ElemBytes<T>::v;
+    const int row0 = (int)(s.kv_off / D);  // tensor-map row of the slab's row 0
     for (int it = un.begin; it < un.end; ++it) {
-      if (p.exec_counts && lane == 0)
+      if (p.exec_counts && pt == 0)
         atomicAdd(p.exec_counts + (int64_t)un.slot * p.counts_stride + it, 1u);
       for (int sub = 0; sub < tpi; ++sub) {
         const Tile t = tile_of(s, it, sub, p.seq_len, p.block_size);
-        const int r0 = tile_row(t, lane), r1 = tile_row(t, lane + 32);
-        mbar_wait(&empty[stage], phase ^ 1);
-        if (lane == 0) mbar_arrive_expect_tx(&full[stage], 2 * LYC_TILE * C::kRowBytes);
-        __syncwarp();
         uint8_t* kd = ring + stage * C::kStageBytes;
         uint8_t* vd = kd + C::kTileBytes;
-        bulk_g2s_stream(kd + lane * C::kRowStride, kbase + slab + (int64_t)r0 * C::kRowBytes,
-                        C::kRowBytes, &full[stage], pol);
-        bulk_g2s_stream(vd + lane * C::kRowStride, vbase + slab + (int64_t)r0 * C::kRowBytes,
-                        C::kRowBytes, &full[stage], pol);
-        bulk_g2s_stream(kd + (lane + 32) * C::kRowStride,
-                        kbase + slab + (int64_t)r1 * C::kRowBytes, C::kRowBytes, &full[stage],
-                        pol);
-        bulk_g2s_stream(vd + (lane + 32) * C::kRowStride,
-                        vbase + slab + (int64_t)r1 * C::kRowBytes, C::kRowBytes, &full[stage],
-                        pol);
+        if (t.ids == nullptr && t.nvalid == LYC_TILE) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (pt == 0) {
+            mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+            if constexpr (C::kSwizzle) {
+#pragma unroll
+              for (int h = 0; h < C::kRowBytes / 128; ++h) {
+                tma_load_2d(kd + h * C::kPanelBytes, &p.tmap_k, h * (128 / C::kE), row0 + t.lo,
+                            &full[stage], pol);
+                tma_load_2d(vd + h * C::kPanelBytes, &p.tmap_v, h * (128 / C::kE), row0 + t.lo,
+                            &full[stage], pol);
+              }
+            } else {
+              tma_load_2d(kd, &p.tmap_k, 0, row0 + t.lo, &full[stage], pol);
+              tma_load_2d(vd, &p.tmap_v, 0, row0 + t.lo, &full[stage], pol);
+            }
+          } else {
+            mbar_arrive(&full[stage]);
+          }
+        } else {
+          // gathered / ragged tile: coalesced 16-B cp.async, masked rows zero-filled
+          int rows[kRounds];
+#pragma unroll
+          for (int i = 0; i < kRounds; ++i) {
+            const int r = my_r0 + i * kRowsPerRound;
+            rows[i] = r < t.nvalid ? (t.ids ? __ldg(t.ids + r) : t.lo + r) : -1;
+          }
+          mbar_wait(&empty[stage], phase ^ 1);
+#pragma unroll
+          for (int i = 0; i < kRounds; ++i) {
+            const int r = my_r0 + i * kRowsPerRound;
+            const int64_t src = (int64_t)(rows[i] < 0 ? 0 : rows[i]) * C::kRowBytes + my_c * 16 +
+                                s.kv_off * C::kE;
+            const uint32_t nbytes = rows[i] < 0 ? 0u : 16u;
+            cp_async_16(kd + C::off(r, my_c), kbase + src, nbytes);
+            cp_async_16(vd + C::off(r, my_c), vbase + src, nbytes);
+          }
+          cp_async_mbar_arrive(&full[stage]);
+        }
         if (++stage == C::kStages) {
           stage = 0;
           phase ^= 1;
@@ -162,7 +200,6 @@ __device__ __forceinline__ void store_out<__nv_bfloat16>(__nv_bfloat16* dst, flo
 template <typename T, int D>
 __device__ __forceinline__ void unit_epilogue(const LycAttnParams& p, const LycSlot& s, int u,
                                               float* mo, float* ml, int tid) {
-  using C = AttnCfg<T, D>;
   const int G = p.group;
   consumer_bar();
   const bool direct = s.n_units == 1;
@@ -170,14 +207,14 @@ __device__ __forceinline__ void unit_epilogue(const LycAttnParams& p, const LycS
     const int j = idx / D, d = idx - j * D;
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, ml[(w * C::kMaxG + j) * 2]);
+    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, ml[(w * kMaxG + j) * 2]);
     float L = 0.f, O = 0.f;
 #pragma unroll
     for (int w = 0; w < kConsumerWarps; ++w) {
-      const float mw = ml[(w * C::kMaxG + j) * 2];
+      const float mw = ml[(w * kMaxG + j) * 2];
       const float f = mw == -INFINITY ? 0.f : exp2f(mw - M);
-      L += ml[(w * C::kMaxG + j) * 2 + 1] * f;
-      O += mo[(w * C::kMaxG + j) * D + d] * f;
+      L += ml[(w * kMaxG + j) * 2 + 1] * f;
+      O += mo[(w * kMaxG + j) * D + d] * f;
     }
     const float o = O / L;
     if (direct) {
@@ -191,7 +228,9 @@ __device__ __forceinline__ void unit_epilogue(const LycAttnParams& p, const LycS
 }
 
 // ---------------------------------------------------------------- bf16 path
-// Consumer warp w handles rows [16w, 16w+16) of each 64-row tile.
+// Consumer warp w handles rows [16w, 16w+16) of each 64-row tile.  Query rows
+// j < G <= 8 sit in A-fragment rows 0..7; rows 8..15 are zero, so only the c0/c1
+// halves of the score / output fragments carry data.
 template <int D>
 __device__ __forceinline__ void consume_bf16(const LycAttnParams& p, uint8_t* ring,
                                              uint64_t* full, uint64_t* empty, float* mo,
@@ -200,9 +239,16 @@ __device__ __forceinline__ void consume_bf16(const LycAttnParams& p, uint8_t* ri
   constexpr int KS = D / 16;  // k-steps over d for QK^T
   constexpr int NT = D / 8;   // n-tiles over d for PV
   const int G = p.group;
-  const int qr = lane >> 2;   // A/C row of this lane (and qr + 8)
+  const int qr = lane >> 2;   // A/C row of this lane
   const int qc = (lane & 3) * 2;
   const int t0 = warp * 16;
+  const int sw = lane & 7;    // every ldmatrix row address below has (row & 7) == lane & 7
+  // K (non-trans): row t0 + (lane>>4)*8 + (lane&7), chunk 2kk + ((lane>>3)&1)
+  const uint32_t k_row = (uint32_t)(t0 + (lane >> 4) * 8 + (lane & 7)) * 128;
+  const int k_x = (lane >> 3) & 1;
+  // V (trans): row t0 + (lane&7) + ((lane>>3)&1)*8, chunk 2*n2 + (lane>>4)
+  const uint32_t v_row = (uint32_t)(t0 + (lane & 7) + ((lane >> 3) & 1) * 8) * 128;
+  const int v_x = lane >> 4;
   int stage = 0;
   uint32_t phase = 0;
   const __nv_bfloat16* Q = static_cast<const __nv_bfloat16*>(p.q);
@@ -211,20 +257,14 @@ __device__ __forceinline__ void consume_bf16(const LycAttnParams& p, uint8_t* ri
     const LycUnit un = p.units[u];
     const LycSlot s = p.slots[un.slot];
     const int tpi = tiles_per_item(s, p.block_size);
-    // ---- Q fragments: rows j < G of the group, zero elsewhere.
-    uint32_t qa[KS][4];
+    uint32_t qa0[KS], qa2[KS];
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) {
-#pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const int row = qr + (h & 1) * 8;
-        const int col = kk * 16 + qc + (h >> 1) * 8;
-        qa[kk][h] = row < G ? __ldg(reinterpret_cast<const uint32_t*>(
-                                  Q + (int64_t)(s.q_row + row) * D + col))
-                            : 0u;
-      }
+      const __nv_bfloat16* qrow = Q + (int64_t)(s.q_row + qr) * D + kk * 16 + qc;
+      qa0[kk] = qr < G ? __ldg(reinterpret_cast<const uint32_t*>(qrow)) : 0u;
+      qa2[kk] = qr < G ? __ldg(reinterpret_cast<const uint32_t*>(qrow + 8)) : 0u;
     }
-    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    float m0 = -INFINITY, l0 = 0.f;
     float o[NT][4];
 #pragma unroll
     for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
@@ -238,16 +278,13 @@ __device__ __forceinline__ void consume_bf16(const LycAttnParams& p, uint8_t* ri
         const uint8_t* vs = ks + C::kTileBytes;
         // ---- S = Q K^T for this warp's 16 rows (two n-tiles of 8)
         float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-        {
-          const uint8_t* kp = ks + (t0 + (lane >> 4) * 8 + (lane & 7)) * C::kRowStride +
-                              ((lane >> 3) & 1) * 16;
 #pragma unroll
-          for (int kk = 0; kk < KS; ++kk) {
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4(b0, b1, b2, b3, kp + kk * 32);
-            mma_bf16(sc[0], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b0, b1);
-            mma_bf16(sc[1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b2, b3);
-          }
+        for (int kk = 0; kk < KS; ++kk) {
+          uint32_t b0, b1, b2, b3;
+          const int c = 2 * (kk & 3) + k_x;
+          ldsm_x4(b0, b1, b2, b3, ks + (kk >> 2) * C::kPanelBytes + k_row + ((c ^ sw) << 4));
+          mma_bf16(sc[0], qa0[kk], 0u, qa2[kk], 0u, b0, b1);
+          mma_bf16(sc[1], qa0[kk], 0u, qa2[kk], 0u, b2, b3);
         }
         // ---- fused selection score: sum over packed rows (rows >= G are 0)
         if (want_sel) {
@@ -256,7 +293,7 @@ __device__ __forceinline__ void consume_bf16(const LycAttnParams& p, uint8_t* ri
           for (int n = 0; n < 2; ++n)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              float v = sc[n][e] + sc[n][e + 2];
+              float v = sc[n][e];
               v += __shfl_xor_sync(0xffffffffu, v, 4);
               v += __shfl_xor_sync(0xffffffffu, v, 8);
               v += __shfl_xor_sync(0xffffffffu, v, 16);
@@ -285,56 +322,36 @@ __device__ __forceinline__ void consume_bf16(const LycAttnParams& p, uint8_t* ri
               atomicMax(p.sel_keys + (int64_t)s.sel * p.sel_stride + it, km);
           }
         }
-        // ---- online softmax (exp2 domain), rows qr (e=0,1) and qr+8 (e=2,3)
-        float x[2][4];
+        // ---- online softmax (exp2 domain) for row qr
+        float x[2][2];
 #pragma unroll
         for (int n = 0; n < 2; ++n)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int r = t0 + n * 8 + qc + (e & 1);
-            x[n][e] = r < t.nvalid ? sc[n][e] * p.scale_log2 : -INFINITY;
-          }
-        const float mx0 = warp_max4(fmaxf(fmaxf(x[0][0], x[0][1]), fmaxf(x[1][0], x[1][1])));
-        const float mx1 = warp_max4(fmaxf(fmaxf(x[0][2], x[0][3]), fmaxf(x[1][2], x[1][3])));
-        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-        const float r0 = m0 == -INFINITY ? 0.f : fast_exp2(m0 - mn0);
-        const float r1 = m1 == -INFINITY ? 0.f : fast_exp2(m1 - mn1);
-        const float u0 = mn0 == -INFINITY ? 0.f : mn0;
-        const float u1 = mn1 == -INFINITY ? 0.f : mn1;
-        float pr[2][4];
-#pragma unroll
-        for (int n = 0; n < 2; ++n) {
-          pr[n][0] = fast_exp2(x[n][0] - u0);
-          pr[n][1] = fast_exp2(x[n][1] - u0);
-          pr[n][2] = fast_exp2(x[n][2] - u1);
-          pr[n][3] = fast_exp2(x[n][3] - u1);
-        }
-        l0 = l0 * r0 + pr[0][0] + pr[0][1] + pr[1][0] + pr[1][1];
-        l1 = l1 * r1 + pr[0][2] + pr[0][3] + pr[1][2] + pr[1][3];
-        m0 = mn0;
-        m1 = mn1;
+          for (int e = 0; e < 2; ++e)
+            x[n][e] = t0 + n * 8 + qc + e < t.nvalid ? sc[n][e] * p.scale_log2 : -INFINITY;
+        const float mx = warp_max4(fmaxf(fmaxf(x[0][0], x[0][1]), fmaxf(x[1][0], x[1][1])));
+        const float mn = fmaxf(m0, mx);
+        const float rs = m0 == -INFINITY ? 0.f : fast_exp2(m0 - mn);
+        const float mu = mn == -INFINITY ? 0.f : mn;
+        const float p00 = fast_exp2(x[0][0] - mu), p01 = fast_exp2(x[0][1] - mu);
+        const float p10 = fast_exp2(x[1][0] - mu), p11 = fast_exp2(x[1][1] - mu);
+        l0 = l0 * rs + p00 + p01 + p10 + p11;
+        m0 = mn;
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
-          o[n][0] *= r0;
-          o[n][1] *= r0;
-          o[n][2] *= r1;
-          o[n][3] *= r1;
+          o[n][0] *= rs;
+          o[n][1] *= rs;
         }
         // ---- O += P V ; P (C layout) -> A fragment without a smem round trip
-        const uint32_t pa0 = pack_bf16(pr[0][0], pr[0][1]);
-        const uint32_t pa1 = pack_bf16(pr[0][2], pr[0][3]);
-        const uint32_t pa2 = pack_bf16(pr[1][0], pr[1][1]);
-        const uint32_t pa3 = pack_bf16(pr[1][2], pr[1][3]);
-        {
-          const uint8_t* vp = vs + (t0 + (lane & 7) + ((lane >> 3) & 1) * 8) * C::kRowStride +
-                              (lane >> 4) * 16;
+        const uint32_t pa0 = pack_bf16(p00, p01);
+        const uint32_t pa2 = pack_bf16(p10, p11);
 #pragma unroll
-          for (int n2 = 0; n2 < D / 16; ++n2) {
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4_t(b0, b1, b2, b3, vp + n2 * 32);
-            mma_bf16(o[2 * n2], pa0, pa1, pa2, pa3, b0, b1);
-            mma_bf16(o[2 * n2 + 1], pa0, pa1, pa2, pa3, b2, b3);
-          }
+        for (int n2 = 0; n2 < D / 16; ++n2) {
+          uint32_t b0, b1, b2, b3;
+          const int c = 2 * (n2 & 3) + v_x;
+          ldsm_x4_t(b0, b1, b2, b3, vs + (n2 >> 2) * C::kPanelBytes + v_row + ((c ^ sw) << 4));
+          mma_bf16(o[2 * n2], pa0, 0u, pa2, 0u, b0, b1);
+          mma_bf16(o[2 * n2 + 1], pa0, 0u, pa2, 0u, b2, b3);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
@@ -347,45 +364,30 @@ __device__ __forceinline__ void consume_bf16(const LycAttnParams& p, uint8_t* ri
     // ---- per-warp state -> smem, then cross-warp merge
     l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
     l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-    if ((lane & 3) == 0) {
-      if (qr < G) {
-        ml[(warp * C::kMaxG + qr) * 2] = m0;
-        ml[(warp * C::kMaxG + qr) * 2 + 1] = l0;
-      }
-      if (qr + 8 < G) {
-        ml[(warp * C::kMaxG + qr + 8) * 2] = m1;
-        ml[(warp * C::kMaxG + qr + 8) * 2 + 1] = l1;
-      }
+    if ((lane & 3) == 0 && qr < G) {
+      ml[(warp * kMaxG + qr) * 2] = m0;
+      ml[(warp * kMaxG + qr) * 2 + 1] = l0;
     }
+    if (qr < G) {
 #pragma unroll
-    for (int n = 0; n < NT; ++n) {
-      const int d = n * 8 + qc;
-      if (qr < G) {
-        mo[(warp * C::kMaxG + qr) * D + d] = o[n][0];
-        mo[(warp * C::kMaxG + qr) * D + d + 1] = o[n][1];
-      }
-      if (qr + 8 < G) {
-        mo[(warp * C::kMaxG + qr + 8) * D + d] = o[n][2];
-        mo[(warp * C::kMaxG + qr + 8) * D + d + 1] = o[n][3];
-      }
+      for (int n = 0; n < NT; ++n)
+        *reinterpret_cast<float2*>(&mo[(warp * kMaxG + qr) * D + n * 8 + qc]) =
+            make_float2(o[n][0], o[n][1]);
     }
     unit_epilogue<__nv_bfloat16, D>(p, s, u, mo, ml, warp * 32 + lane);
   }
 }
 
 // ---------------------------------------------------------------- fp32 path
-// CUDA-core FP32 (exact fp32 products, serial-order-free accumulation); used
-// for the fp32 parity configs.  Lane l of warp w owns row t0 + (l & 15) for the
-// scores (half h = l >> 4 of the d range), and d columns l, l+32, ... for PV.
+// CUDA-core FP32 (exact fp32 products); used for the fp32 parity configs.
+// Lane l of warp w owns row t0 + (l & 15) for the scores (half h = l >> 4 of
+// the d range), and d columns l, l+32, ... for PV.  Tiles are unswizzled.
 template <int D>
 __device__ __forceinline__ void consume_f32(const LycAttnParams& p, uint8_t* ring,
                                             uint64_t* full, uint64_t* empty, float* mo,
                                             float* ml, float* qs, int ub, int ue, int warp,
                                             int lane) {
   using C = AttnCfg<float, D>;
-  constexpr int MAXG = 8;
   constexpr int DH = D / 2;
   constexpr int DC = (D + 31) / 32;
   const int G = p.group;
@@ -400,9 +402,9 @@ __device__ __forceinline__ void consume_f32(const LycAttnParams& p, uint8_t* rin
     const LycSlot s = p.slots[un.slot];
     const int tpi = tiles_per_item(s, p.block_size);
     const bool want_sel = s.sel >= 0 && p.sel_mode != SEL_NONE;
-    float m[MAXG], l[MAXG], o[MAXG][DC];
+    float m[kMaxG], l[kMaxG], o[kMaxG][DC];
 #pragma unroll
-    for (int j = 0; j < MAXG; ++j) {
+    for (int j = 0; j < kMaxG; ++j) {
       m[j] = -INFINITY;
       l[j] = 0.f;
 #pragma unroll
@@ -425,22 +427,22 @@ __device__ __forceinline__ void consume_f32(const LycAttnParams& p, uint8_t* rin
       for (int sub = 0; sub < tpi; ++sub) {
         const Tile t = tile_of(s, it, sub, p.seq_len, p.block_size);
         mbar_wait(&full[stage], phase);
-        const float* krow =
-            reinterpret_cast<const float*>(ring + stage * C::kStageBytes + (t0 + tr) * C::kRowStride);
-        const float* vs = reinterpret_cast<const float*>(ring + stage * C::kStageBytes + C::kTileBytes);
-        float sc[MAXG], pooled = 0.f;
+        const uint8_t* ks = ring + stage * C::kStageBytes;
+        const float* krow = reinterpret_cast<const float*>(ks + (t0 + tr) * C::kRowBytes);
+        const uint8_t* vs = ks + C::kTileBytes;
+        float sc[kMaxG], pooled = 0.f;
 #pragma unroll
-        for (int j = 0; j < MAXG; ++j) sc[j] = 0.f;
+        for (int j = 0; j < kMaxG; ++j) sc[j] = 0.f;
         for (int dd = 0; dd < DH; ++dd) {
           const int d = half * DH + dd;
           const float kv = krow[d];
 #pragma unroll
-          for (int j = 0; j < MAXG; ++j)
+          for (int j = 0; j < kMaxG; ++j)
             if (j < G) sc[j] = fmaf(qs[j * D + d], kv, sc[j]);
           if (want_sel) pooled = fmaf(qs[G * D + d], kv, pooled);
         }
 #pragma unroll
-        for (int j = 0; j < MAXG; ++j) sc[j] += __shfl_xor_sync(0xffffffffu, sc[j], 16);
+        for (int j = 0; j < kMaxG; ++j) sc[j] += __shfl_xor_sync(0xffffffffu, sc[j], 16);
         const bool valid = t0 + tr < t.nvalid;
         if (want_sel) {
           pooled += __shfl_xor_sync(0xffffffffu, pooled, 16);
@@ -450,18 +452,21 @@ __device__ __forceinline__ void consume_f32(const LycAttnParams& p, uint8_t* rin
           } else {
             uint32_t km = (half == 0 && valid) ? float_key(pooled) : 0u;
 #pragma unroll
-            for (int off = 1; off < 16; off <<= 1) km = max(km, __shfl_xor_sync(0xffffffffu, km, off));
-            if (lane == 0 && km != 0u) atomicMax(p.sel_keys + (int64_t)s.sel * p.sel_stride + it, km);
+            for (int off = 1; off < 16; off <<= 1)
+              km = max(km, __shfl_xor_sync(0xffffffffu, km, off));
+            if (lane == 0 && km != 0u)
+              atomicMax(p.sel_keys + (int64_t)s.sel * p.sel_stride + it, km);
           }
         }
-        float pr[MAXG];
+        float pr[kMaxG];
 #pragma unroll
-        for (int j = 0; j < MAXG; ++j) {
+        for (int j = 0; j < kMaxG; ++j) {
           if (j >= G) break;
           const float x = valid ? sc[j] * p.scale_log2 : -INFINITY;
           float mx = x;
 #pragma unroll
-          for (int off = 1; off < 16; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+          for (int off = 1; off < 16; off <<= 1)
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
           const float mn = fmaxf(m[j], mx);
           const float r = m[j] == -INFINITY ? 0.f : exp2f(m[j] - mn);
           const float uu = mn == -INFINITY ? 0.f : mn;
@@ -475,10 +480,9 @@ __device__ __forceinline__ void consume_f32(const LycAttnParams& p, uint8_t* rin
           for (int c = 0; c < DC; ++c) o[j][c] *= r;
         }
         for (int rr = 0; rr < 16; ++rr) {
-          const float* vrow = reinterpret_cast<const float*>(
-              reinterpret_cast<const uint8_t*>(vs) + (t0 + rr) * C::kRowStride);
+          const float* vrow = reinterpret_cast<const float*>(vs + (t0 + rr) * C::kRowBytes);
 #pragma unroll
-          for (int j = 0; j < MAXG; ++j) {
+          for (int j = 0; j < kMaxG; ++j) {
             if (j >= G) break;
             const float pj = __shfl_sync(0xffffffffu, pr[j], rr);
 #pragma unroll
@@ -495,15 +499,15 @@ __device__ __forceinline__ void consume_f32(const LycAttnParams& p, uint8_t* rin
       }
     }
 #pragma unroll
-    for (int j = 0; j < MAXG; ++j) {
+    for (int j = 0; j < kMaxG; ++j) {
       if (j >= G) break;
       if (lane == 0) {
-        ml[(warp * C::kMaxG + j) * 2] = m[j];
-        ml[(warp * C::kMaxG + j) * 2 + 1] = l[j];
+        ml[(warp * kMaxG + j) * 2] = m[j];
+        ml[(warp * kMaxG + j) * 2 + 1] = l[j];
       }
 #pragma unroll
       for (int c = 0; c < DC; ++c)
-        if (c * 32 + lane < D) mo[(warp * C::kMaxG + j) * D + c * 32 + lane] = o[j][c];
+        if (c * 32 + lane < D) mo[(warp * kMaxG + j) * D + c * 32 + lane] = o[j][c];
     }
     unit_epilogue<float, D>(p, s, u, mo, ml, warp * 32 + lane);
   }
@@ -512,11 +516,14 @@ __device__ __forceinline__ void consume_f32(const LycAttnParams& p, uint8_t* rin
 template <typename T, int D>
 __global__ void __launch_bounds__(kThreads, 1) hybrid_attn_kernel(const __grid_constant__ LycAttnParams p) {
   using C = AttnCfg<T, D>;
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-B alignment for the 128B-swizzle atoms of the TMA destinations
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* ring = smem;
   float* mo = reinterpret_cast<float*>(smem + C::kStages * C::kStageBytes);
-  float* ml = mo + kConsumerWarps * C::kMaxG * D;
-  float* qs = ml + kConsumerWarps * C::kMaxG * 2;
+  float* ml = mo + kConsumerWarps * kMaxG * D;
+  float* qs = ml + kConsumerWarps * kMaxG * 2;
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(qs) + C::kQBytes);
   uint64_t* empty = full + C::kStages;
 
@@ -526,14 +533,14 @@ __global__ void __launch_bounds__(kThreads, 1) hybrid_attn_kernel(const __grid_c
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], kProducerThreads);
       mbar_init(&empty[s], kConsumerWarps);
     }
     fence_mbar_init();
   }
   __syncthreads();
-  if (warp == kConsumerWarps) {
-    produce<T, D>(p, ring, full, empty, ub, ue, lane);
+  if (warp >= kConsumerWarps) {
+    produce<T, D>(p, ring, full, empty, ub, ue, threadIdx.x - kConsumerWarps * 32);
   } else if constexpr (sizeof(T) == 2) {
     consume_bf16<D>(p, ring, full, empty, mo, ml, ub, ue, warp, lane);
   } else {

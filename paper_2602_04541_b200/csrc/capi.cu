@@ -14,6 +14,8 @@
 #include "../../include/lyc.h"
 #include "lyc_plan.h"
 
+#include <cudaTypedefs.h>
+
 namespace lyc {
 cudaError_t launch_attn(const LycAttnParams& p, int dtype, int d, int batch, cudaStream_t st);
 int attn_stages(int dtype, int d);
@@ -181,6 +183,38 @@ DevLaunch stage_launch(const HostLaunch& L, std::vector<uint8_t>& host, size_t& 
   return d;
 }
 
+// 2D TMA views of a K or V cache: dim0 = d, dim1 = every row of every slab.
+// bf16: box 64 x 64 (one 128-B panel), 128B swizzle; fp32: box d x 64, no swizzle.
+void encode_kv_maps(LycAttnParams& ap, const void* k, const void* v, int64_t rows, int D,
+                    int dtype) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cuda_check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q),
+               "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
+    if (q != cudaDriverEntryPointSuccess || !fn) fail(LYC_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  if (rows >= ((int64_t)1 << 31)) fail(LYC_ENOTSUP, "KV cache has >= 2^31 rows");
+  const bool bf16 = dtype == LYC_DTYPE_BF16;
+  const int e = bf16 ? 2 : 4;
+  cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)D * e};
+  cuuint32_t box[2] = {bf16 ? 64u : (cuuint32_t)D, (cuuint32_t)LYC_TILE};
+  cuuint32_t estr[2] = {1, 1};
+  const void* ptrs[2] = {k, v};
+  CUtensorMap* maps[2] = {&ap.tmap_k, &ap.tmap_v};
+  for (int i = 0; i < 2; ++i) {
+    CUresult r = encode(maps[i], bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                        2, const_cast<void*>(ptrs[i]), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        bf16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(LYC_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  }
+}
+
 }  // namespace
 
 // =================================================================== C-ABI
@@ -281,7 +315,7 @@ int lyc_workload_run(const lyc_workload* w, int64_t num_splits, void* out, uint3
       fail(LYC_EINVAL, "Workload: all dimensions must be >= 1");
     if (num_splits < 1) fail(LYC_EINVAL, "plan_splits: num_splits must be >= 1");
     if (!supported_d(w->dtype, w->d_head)) fail(LYC_ENOTSUP, "Workload: unsupported d_head/dtype on device");
-    if (w->group_size > (w->dtype == LYC_DTYPE_BF16 ? 16 : 8))
+    if (w->group_size > 8)
       fail(LYC_ENOTSUP, "Workload: group_size too large for the device kernel");
     if (w->kv_row_stride < w->seq_len) fail(LYC_EINVAL, "Workload: kv_row_stride < seq_len");
     const int64_t B = w->batch, H = w->n_kv_heads, G = w->group_size, D = w->d_head;
@@ -349,6 +383,7 @@ int lyc_workload_run(const lyc_workload* w, int64_t num_splits, void* out, uint3
     ap.sel_mode = SEL_NONE;
     ap.scale = w->scale;
     ap.scale_log2 = w->scale * 1.4426950408889634f;
+    encode_kv_maps(ap, w->k, w->v, B * H * w->kv_row_stride, (int)D, w->dtype);
     cuda_check(lyc::launch_attn(ap, w->dtype, (int)D, (int)B, st), "attention launch");
     ++g_launches;
     if (dl.n_merges) {
@@ -421,6 +456,9 @@ struct lyc_decoder {
   uint8_t* blob = nullptr;
   size_t blob_cap = 0;
   int64_t planned_seq = -1;
+  LycAttnParams maps{};        // tensor maps for the last (k, v) pointers
+  const void* map_k = nullptr;
+  const void* map_v = nullptr;
   struct Layer {
     LycAttnParams ap;
     LycMergeParams mp;
@@ -564,13 +602,25 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
 void decoder_layer(lyc_decoder* d, int l, const void* q_l, const void* k, const void* v,
                    void* out_l, cudaStream_t st) {
   lyc_decoder::Layer& ly = d->layers[(size_t)l];
+  if (k != d->map_k || v != d->map_v) {
+    encode_kv_maps(d->maps, k, v, (int64_t)d->NL * d->B * d->H * d->cfg.seq_cap, d->D, d->cfg.dtype);
+    d->map_k = k;
+    d->map_v = v;
+  }
+  ly.ap.tmap_k = d->maps.tmap_k;
+  ly.ap.tmap_v = d->maps.tmap_v;
   ly.ap.k = k;
   ly.ap.v = v;
   ly.ap.q = q_l;
   ly.ap.out = out_l;
-  if (d->timing) cuda_check(cudaEventRecord(d->ev_pre[(size_t)l], st), "event record");
+  // External records become event nodes when the stream is being captured.
+  if (d->timing)
+    cuda_check(cudaEventRecordWithFlags(d->ev_pre[(size_t)l], st, cudaEventRecordExternal),
+               "event record");
   cuda_check(lyc::launch_attn(ly.ap, d->cfg.dtype, d->D, d->B, st), "attention launch");
-  if (d->timing) cuda_check(cudaEventRecord(d->ev_post[(size_t)l], st), "event record");
+  if (d->timing)
+    cuda_check(cudaEventRecordWithFlags(d->ev_post[(size_t)l], st, cudaEventRecordExternal),
+               "event record");
   ++g_launches;
   if (ly.n_merges) {
     ly.mp.out = out_l;
@@ -601,7 +651,7 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
         c.seq_cap < 1)
       fail(LYC_EINVAL, "ModelConfig: all dimensions must be >= 1");
     if (!supported_d(c.dtype, c.d_head)) fail(LYC_ENOTSUP, "decoder: unsupported d_head/dtype");
-    if (c.group_size > (c.dtype == LYC_DTYPE_BF16 ? 16 : 8))
+    if (c.group_size > 8)
       fail(LYC_ENOTSUP, "decoder: group_size too large for the device kernel");
     if (c.policy_kind == LYC_POLICY_TOPK) {
       if (c.top_k < 1) fail(LYC_EINVAL, "top_k: k must be >= 1");

@@ -12,6 +12,7 @@
 // item list into num_splits contiguous chunks; a chunk's per-slot pieces are
 // UNITS.  One CTA executes one split (Algorithm 2).
 #pragma once
+#include <cuda.h>  // CUtensorMap (type only; encoded through the runtime's driver entry point)
 #include <stdint.h>
 
 #define LYC_TILE 64
@@ -42,6 +43,11 @@ struct LycUnit {
 enum { SEL_NONE = 0, SEL_TOKEN_KEYS = 1, SEL_BLOCK_KEYS = 2 };
 
 struct LycAttnParams {
+  // 2D TMA views of the K and V caches: dim0 = d (elements), dim1 = all rows
+  // of all slabs; box = one 128-B column panel (bf16, 128B swizzle) or the
+  // whole row (fp32, no swizzle) x 64 rows.
+  CUtensorMap tmap_k;
+  CUtensorMap tmap_v;
   const void* k;            // [...][S_cap][d] (slot kv_off)
   const void* v;
   const void* q;            // [rows][d]
