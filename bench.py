@@ -314,6 +314,7 @@ def main():
     with torch.cuda.stream(stream):
         dec.capture(q, K, V, L, out, stream=stream)
     launches_per_step = dec.launches_per_step(L)
+    fused = dec.fused
     lc0 = P.lib().lyc_launch_count()
     with ClockSampler(local) as clk:
         ms = time_graph(dec, args.steps, args.warmup)
@@ -427,9 +428,12 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_kind": pk_kind,
                          "frac_of_8TBs": achieved / 8000.0,
-                         "kernel": "hybrid_attn_kernel (all layers)",
+                         "kernel": ("hybrid_step_kernel (whole step: attention + merge + "
+                                    "selection of all layers, 1 launch)") if fused
+                                   else "hybrid_attn_kernel (all layers)",
                          "attn_us_per_step": attn_ms_total * 1e3,
-                         "layer0_gbs": attn_bytes[0] / (per_layer[0] / 1e3) / 1e9,
+                         "layer0_gbs": None if fused
+                                       else attn_bytes[0] / (per_layer[0] / 1e3) / 1e9,
                          "bytes_per_step": float(attn_bytes.sum())},
             "full_attention": full,
             "cpu_baseline": cpu,

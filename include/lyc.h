@@ -169,6 +169,12 @@ int64_t lyc_decoder_layer_attn_bytes(lyc_decoder* dec, int32_t layer, int64_t se
 int lyc_decoder_set_timing(lyc_decoder* dec, int enable);
 int lyc_decoder_attn_ms(lyc_decoder* dec, float* ms);
 
+/* 1 when lyc_decoder_step runs the persistent whole-step kernel (one launch:
+ * attention, split-KV merge and selection of every layer), 0 when it issues
+ * per-layer kernels (attention, merge, cluster top-k).  In fused mode
+ * lyc_decoder_attn_ms reports the step kernel's duration in ms[0]. */
+int lyc_decoder_is_fused(lyc_decoder* dec);
+
 #ifdef __cplusplus
 }
 #endif

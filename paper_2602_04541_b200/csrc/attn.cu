@@ -1,558 +1,49 @@
-// attn.cu -- the pooled hybrid-head split-KV decode attention kernel
-// (Algorithm 2; CPU reference kernel_sim.hpp:169-201
-// run_split and attention.hpp:50-104 dense/sparse attention).
-//
-// One CTA executes one split of the pooled plan: a sequence of UNITS, each a
-// contiguous item range of one slot (b, KV head).  Retrieval (ITEM_DENSE),
-// block-sparse (ITEM_BLOCKS) and token-sparse (ITEM_TOKENS) slots share one
-// smem ring of 64-row K/V tiles:
-//
-//   warps 4-5 (producers):
-//     * full contiguous tiles (retrieval heads, selected blocks): one thread
-//       issues 2D tensor-map TMA boxes (64 rows x 128 B panel, 128B swizzle
-//       for bf16) -- 4 instructions per 32 KB stage, completion counted in
-//       bytes on the stage's mbarrier;
-//     * gathered tiles (token-sparse heads, ragged tails): all 64 producer
-//       threads issue coalesced 16-B cp.async (LDGSTS) of the indexed rows
-//       straight into the same swizzled layout, zero-filling masked rows, and
-//       arrive on the mbarrier when their copies land.
-//   warps 0-3 (consumers): each owns 16 rows of every tile; the G <= 8 query
-//     heads of the GQA group are packed as the A operand of mma.sync m16n8k16
-//     (bf16 -> fp32), so every K/V byte is read from smem once for the whole
-//     group.  Online softmax (attention.hpp:161-181) in the exp2 domain with
-//     quad-shuffle row max/sum; P goes C-fragment -> A-fragment in registers.
-//   Fused selection (retrieval slots with sel >= 0): the pooled-query score
-//     sum_j q_j.k of every row (= G * pooled_q.k, attention.hpp:127-146,
-//     decode_engine.hpp:129-132) is reduced across the packed rows with three
-//     shuffles and written as an order-preserving uint32 key (token mode) or
-//     max-folded per block (block mode).
-//   End of unit: the 4 warps' (m, l, o) are merged through smem and written
-//     as a normalized partial + base-2 LSE (kernel_sim.hpp:195-198), or as
-//     the final output when the slot has a single unit.
-#include "lyc_common.cuh"
-#include "lyc_plan.h"
+// attn.cu -- per-launch kernels of the hybrid-head decode attention:
+//   hybrid_attn_kernel  one layer's pooled split-KV attention (Algorithm 2,
+//                       PAPER.md:543-557; kernel_sim.hpp:169-201 run_split),
+//                       used by lyc_workload_run (hh::kernel::run) and
+//                       lyc_decoder_layer;
+//   split_merge_kernel  the LSE merge (kernel_sim.hpp:205-225 combine).
+// The device building blocks live in attn_core.cuh; the persistent whole-step
+// kernel is step.cu.
+#include "attn_core.cuh"
 
 namespace lyc {
 
-constexpr int kConsumerWarps = 4;
-constexpr int kProducerWarps = 2;
-constexpr int kProducerThreads = kProducerWarps * 32;
-constexpr int kThreads = (kConsumerWarps + kProducerWarps) * 32;
-constexpr int kMaxG = 8;
+constexpr int kAttnThreads = (kConsumerWarps + kProducerWarps) * 32;
 
 template <typename T, int D>
-struct AttnCfg {
-  static constexpr int kE = (int)sizeof(T);
-  static constexpr bool kSwizzle = kE == 2;        // bf16 tiles: 128-B swizzled panels
-  static constexpr int kRowBytes = D * kE;
-  static constexpr int kPanelBytes = LYC_TILE * 128;
-  static constexpr int kTileBytes = LYC_TILE * kRowBytes;
-  static constexpr int kStageBytes = 2 * kTileBytes;  // K tile then V tile
-  static constexpr int kChunksPerRow = kRowBytes / 16;
-  static constexpr int kMergeBytes = kConsumerWarps * kMaxG * (D + 2) * 4;
-  static constexpr int kQBytes = kE == 4 ? (kMaxG + 1) * D * 4 : 0;
-  static constexpr int kMaxSmem = 232448 - 1024;   // 227 KB opt-in minus alignment slack
-  static constexpr int kFixed = kMergeBytes + kQBytes + 256;
-  static constexpr int kStagesRaw = (kMaxSmem - kFixed) / kStageBytes;
-  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-  static constexpr int kSmem = kStages * kStageBytes + kFixed + 1024;
-  static_assert(kStages >= 2, "not enough shared memory for a 2-stage ring");
-  static_assert(kRowBytes % 16 == 0 && (!kSwizzle || kRowBytes % 128 == 0), "row layout");
-
-  // byte offset of 16-B chunk c of tile row r
-  __device__ __forceinline__ static uint32_t off(int r, int c) {
-    if constexpr (kSwizzle)
-      return (uint32_t)((c >> 3) * kPanelBytes + r * 128 + (((c & 7) ^ (r & 7)) << 4));
-    else
-      return (uint32_t)(r * kRowBytes + c * 16);
-  }
-};
-
-struct Tile {
-  int32_t lo;            // first row (contiguous tiles)
-  int32_t nvalid;        // valid rows in this tile
-  const int32_t* ids;    // token ids (gathered tiles) or nullptr
-};
-
-__device__ __forceinline__ int tiles_per_item(const LycSlot& s, int bs) {
-  return s.kind == ITEM_TOKENS ? 1 : (bs + LYC_TILE - 1) / LYC_TILE;
-}
-
-__device__ __forceinline__ Tile tile_of(const LycSlot& s, int item, int sub, int seq, int bs) {
-  Tile t;
-  if (s.kind == ITEM_TOKENS) {
-    t.ids = s.list + (int64_t)item * LYC_TILE;
-    t.lo = 0;
-    t.nvalid = min(LYC_TILE, s.list_len - item * LYC_TILE);
-  } else {
-    const int blk = s.kind == ITEM_DENSE ? item : __ldg(s.list + item);
-    const int b0 = blk * bs;
-    const int hi = min(b0 + bs, seq);
-    t.ids = nullptr;
-    t.lo = b0 + sub * LYC_TILE;
-    t.nvalid = max(0, min(LYC_TILE, hi - t.lo));
-  }
-  return t;
-}
-
-// ---------------------------------------------------------------- producer
-template <typename T, int D>
-__device__ __forceinline__ void produce(const LycAttnParams& p, uint8_t* ring, uint64_t* full,
-                                        uint64_t* empty, int ub, int ue, int pt) {
-  using C = AttnCfg<T, D>;
-  constexpr int CPR = C::kChunksPerRow;
-  constexpr int kRowsPerRound = kProducerThreads / CPR > 0 ? kProducerThreads / CPR : 1;
-  constexpr int kRounds = LYC_TILE / kRowsPerRound;
-  static_assert(kProducerThreads % CPR == 0 || CPR % kProducerThreads == 0, "producer mapping");
-  const uint64_t pol = policy_evict_first();
-  const char* kbase = static_cast<const char*>(p.k);
-  const char* vbase = static_cast<const char*>(p.v);
-  if (pt == 0) {
-    prefetch_tensormap(&p.tmap_k);
-    prefetch_tensormap(&p.tmap_v);
-  }
-  const int my_c = pt % CPR;
-  const int my_r0 = pt / CPR;
-  int stage = 0;
-  uint32_t phase = 0;
-  for (int u = ub; u < ue; ++u) {
-    const LycUnit un = p.units[u];
-    const LycSlot s = p.slots[un.slot];
-    const int tpi = tiles_per_item(s, p.block_size);
-    const int row0 = (int)(s.kv_off / D);  // tensor-map row of the slab's row 0
-    for (int it = un.begin; it < un.end; ++it) {
-      if (p.exec_counts && pt == 0)
-        atomicAdd(p.exec_counts + (int64_t)un.slot * p.counts_stride + it, 1u);
-      for (int sub = 0; sub < tpi; ++sub) {
-        const Tile t = tile_of(s, it, sub, p.seq_len, p.block_size);
-        uint8_t* kd = ring + stage * C::kStageBytes;
-        uint8_t* vd = kd + C::kTileBytes;
-        if (t.ids == nullptr && t.nvalid == LYC_TILE) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          if (pt == 0) {
-            mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-            if constexpr (C::kSwizzle) {
-#pragma unroll
-              for (int h = 0; h < C::kRowBytes / 128; ++h) {
-                tma_load_2d(kd + h * C::kPanelBytes, &p.tmap_k, h * (128 / C::kE), row0 + t.lo,
-                            &full[stage], pol);
-                tma_load_2d(vd + h * C::kPanelBytes, &p.tmap_v, h * (128 / C::kE), row0 + t.lo,
-                            &full[stage], pol);
-              }
-            } else {
-              tma_load_2d(kd, &p.tmap_k, 0, row0 + t.lo, &full[stage], pol);
-              tma_load_2d(vd, &p.tmap_v, 0, row0 + t.lo, &full[stage], pol);
-            }
-          } else {
-            mbar_arrive(&full[stage]);
-          }
-        } else {
-          // gathered / ragged tile: coalesced 16-B cp.async, masked rows zero-filled
-          int rows[kRounds];
-#pragma unroll
-          for (int i = 0; i < kRounds; ++i) {
-            const int r = my_r0 + i * kRowsPerRound;
-            rows[i] = r < t.nvalid ? (t.ids ? __ldg(t.ids + r) : t.lo + r) : -1;
-          }
-          mbar_wait(&empty[stage], phase ^ 1);
-#pragma unroll
-          for (int i = 0; i < kRounds; ++i) {
-            const int r = my_r0 + i * kRowsPerRound;
-            const int64_t src = (int64_t)(rows[i] < 0 ? 0 : rows[i]) * C::kRowBytes + my_c * 16 +
-                                s.kv_off * C::kE;
-            const uint32_t nbytes = rows[i] < 0 ? 0u : 16u;
-            cp_async_16(kd + C::off(r, my_c), kbase + src, nbytes);
-            cp_async_16(vd + C::off(r, my_c), vbase + src, nbytes);
-          }
-          cp_async_mbar_arrive(&full[stage]);
-        }
-        if (++stage == C::kStages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    }
-  }
-}
-
-__device__ __forceinline__ void consumer_bar() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
-}
-
-__device__ __forceinline__ float warp_max4(float v) {  // max over the 4 lanes of a quad
-  v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 1));
-  return fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 2));
-}
-
-template <typename T>
-__device__ __forceinline__ void store_out(T* dst, float v);
-template <>
-__device__ __forceinline__ void store_out<float>(float* dst, float v) {
-  *dst = v;
-}
-template <>
-__device__ __forceinline__ void store_out<__nv_bfloat16>(__nv_bfloat16* dst, float v) {
-  *dst = __float2bfloat16_rn(v);
-}
-
-// Merge the consumer warps' (m, l, o) for one unit and emit partial / output.
-// merge smem layout: o[w][j][D] then ml[w][j][2].
-template <typename T, int D>
-__device__ __forceinline__ void unit_epilogue(const LycAttnParams& p, const LycSlot& s, int u,
-                                              float* mo, float* ml, int tid) {
-  const int G = p.group;
-  consumer_bar();
-  const bool direct = s.n_units == 1;
-  for (int idx = tid; idx < G * D; idx += kConsumerWarps * 32) {
-    const int j = idx / D, d = idx - j * D;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, ml[(w * kMaxG + j) * 2]);
-    float L = 0.f, O = 0.f;
-#pragma unroll
-    for (int w = 0; w < kConsumerWarps; ++w) {
-      const float mw = ml[(w * kMaxG + j) * 2];
-      const float f = mw == -INFINITY ? 0.f : exp2f(mw - M);
-      L += ml[(w * kMaxG + j) * 2 + 1] * f;
-      O += mo[(w * kMaxG + j) * D + d] * f;
-    }
-    const float o = O / L;
-    if (direct) {
-      store_out<T>(static_cast<T*>(p.out) + (int64_t)(s.q_row + j) * D + d, o);
-    } else {
-      p.part_o[((int64_t)u * G + j) * D + d] = o;
-      if (d == 0) p.part_lse[(int64_t)u * G + j] = log2f(L) + M;
-    }
-  }
-  consumer_bar();
-}
-
-// ---------------------------------------------------------------- bf16 path
-// Consumer warp w handles rows [16w, 16w+16) of each 64-row tile.  Query rows
-// j < G <= 8 sit in A-fragment rows 0..7; rows 8..15 are zero, so only the c0/c1
-// halves of the score / output fragments carry data.
-template <int D>
-__device__ __forceinline__ void consume_bf16(const LycAttnParams& p, uint8_t* ring,
-                                             uint64_t* full, uint64_t* empty, float* mo,
-                                             float* ml, int ub, int ue, int warp, int lane) {
-  using C = AttnCfg<__nv_bfloat16, D>;
-  constexpr int KS = D / 16;  // k-steps over d for QK^T
-  constexpr int NT = D / 8;   // n-tiles over d for PV
-  const int G = p.group;
-  const int qr = lane >> 2;   // A/C row of this lane
-  const int qc = (lane & 3) * 2;
-  const int t0 = warp * 16;
-  const int sw = lane & 7;    // every ldmatrix row address below has (row & 7) == lane & 7
-  // K (non-trans): row t0 + (lane>>4)*8 + (lane&7), chunk 2kk + ((lane>>3)&1)
-  const uint32_t k_row = (uint32_t)(t0 + (lane >> 4) * 8 + (lane & 7)) * 128;
-  const int k_x = (lane >> 3) & 1;
-  // V (trans): row t0 + (lane&7) + ((lane>>3)&1)*8, chunk 2*n2 + (lane>>4)
-  const uint32_t v_row = (uint32_t)(t0 + (lane & 7) + ((lane >> 3) & 1) * 8) * 128;
-  const int v_x = lane >> 4;
-  int stage = 0;
-  uint32_t phase = 0;
-  const __nv_bfloat16* Q = static_cast<const __nv_bfloat16*>(p.q);
-
-  for (int u = ub; u < ue; ++u) {
-    const LycUnit un = p.units[u];
-    const LycSlot s = p.slots[un.slot];
-    const int tpi = tiles_per_item(s, p.block_size);
-    uint32_t qa0[KS], qa2[KS];
-#pragma unroll
-    for (int kk = 0; kk < KS; ++kk) {
-      const __nv_bfloat16* qrow = Q + (int64_t)(s.q_row + qr) * D + kk * 16 + qc;
-      qa0[kk] = qr < G ? __ldg(reinterpret_cast<const uint32_t*>(qrow)) : 0u;
-      qa2[kk] = qr < G ? __ldg(reinterpret_cast<const uint32_t*>(qrow + 8)) : 0u;
-    }
-    float m0 = -INFINITY, l0 = 0.f;
-    float o[NT][4];
-#pragma unroll
-    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-    const bool want_sel = s.sel >= 0 && p.sel_mode != SEL_NONE;
-
-    for (int it = un.begin; it < un.end; ++it) {
-      for (int sub = 0; sub < tpi; ++sub) {
-        const Tile t = tile_of(s, it, sub, p.seq_len, p.block_size);
-        mbar_wait(&full[stage], phase);
-        const uint8_t* ks = ring + stage * C::kStageBytes;
-        const uint8_t* vs = ks + C::kTileBytes;
-        // ---- S = Q K^T for this warp's 16 rows (two n-tiles of 8)
-        float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-#pragma unroll
-        for (int kk = 0; kk < KS; ++kk) {
-          uint32_t b0, b1, b2, b3;
-          const int c = 2 * (kk & 3) + k_x;
-          ldsm_x4(b0, b1, b2, b3, ks + (kk >> 2) * C::kPanelBytes + k_row + ((c ^ sw) << 4));
-          mma_bf16(sc[0], qa0[kk], 0u, qa2[kk], 0u, b0, b1);
-          mma_bf16(sc[1], qa0[kk], 0u, qa2[kk], 0u, b2, b3);
-        }
-        // ---- fused selection score: sum over packed rows (rows >= G are 0)
-        if (want_sel) {
-          float ps[2][2];
-#pragma unroll
-          for (int n = 0; n < 2; ++n)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              float v = sc[n][e];
-              v += __shfl_xor_sync(0xffffffffu, v, 4);
-              v += __shfl_xor_sync(0xffffffffu, v, 8);
-              v += __shfl_xor_sync(0xffffffffu, v, 16);
-              ps[n][e] = v;
-            }
-          if (p.sel_mode == SEL_TOKEN_KEYS) {
-            if (lane < 4) {
-#pragma unroll
-              for (int n = 0; n < 2; ++n) {
-                const int r = t0 + n * 8 + qc;
-                uint32_t* dst = p.sel_keys + (int64_t)s.sel * p.sel_stride + t.lo + r;
-                if (r < t.nvalid) dst[0] = float_key(ps[n][0]);
-                if (r + 1 < t.nvalid) dst[1] = float_key(ps[n][1]);
-              }
-            }
-          } else {  // SEL_BLOCK_KEYS: max over valid rows of this block
-            uint32_t km = 0u;
-#pragma unroll
-            for (int n = 0; n < 2; ++n)
-#pragma unroll
-              for (int e = 0; e < 2; ++e)
-                if (t0 + n * 8 + qc + e < t.nvalid) km = max(km, float_key(ps[n][e]));
-            km = max(km, __shfl_xor_sync(0xffffffffu, km, 1));
-            km = max(km, __shfl_xor_sync(0xffffffffu, km, 2));
-            if (lane == 0 && km != 0u)
-              atomicMax(p.sel_keys + (int64_t)s.sel * p.sel_stride + it, km);
-          }
-        }
-        // ---- online softmax (exp2 domain) for row qr
-        float x[2][2];
-#pragma unroll
-        for (int n = 0; n < 2; ++n)
-#pragma unroll
-          for (int e = 0; e < 2; ++e)
-            x[n][e] = t0 + n * 8 + qc + e < t.nvalid ? sc[n][e] * p.scale_log2 : -INFINITY;
-        const float mx = warp_max4(fmaxf(fmaxf(x[0][0], x[0][1]), fmaxf(x[1][0], x[1][1])));
-        const float mn = fmaxf(m0, mx);
-        const float rs = m0 == -INFINITY ? 0.f : fast_exp2(m0 - mn);
-        const float mu = mn == -INFINITY ? 0.f : mn;
-        const float p00 = fast_exp2(x[0][0] - mu), p01 = fast_exp2(x[0][1] - mu);
-        const float p10 = fast_exp2(x[1][0] - mu), p11 = fast_exp2(x[1][1] - mu);
-        l0 = l0 * rs + p00 + p01 + p10 + p11;
-        m0 = mn;
-#pragma unroll
-        for (int n = 0; n < NT; ++n) {
-          o[n][0] *= rs;
-          o[n][1] *= rs;
-        }
-        // ---- O += P V ; P (C layout) -> A fragment without a smem round trip
-        const uint32_t pa0 = pack_bf16(p00, p01);
-        const uint32_t pa2 = pack_bf16(p10, p11);
-#pragma unroll
-        for (int n2 = 0; n2 < D / 16; ++n2) {
-          uint32_t b0, b1, b2, b3;
-          const int c = 2 * (n2 & 3) + v_x;
-          ldsm_x4_t(b0, b1, b2, b3, vs + (n2 >> 2) * C::kPanelBytes + v_row + ((c ^ sw) << 4));
-          mma_bf16(o[2 * n2], pa0, 0u, pa2, 0u, b0, b1);
-          mma_bf16(o[2 * n2 + 1], pa0, 0u, pa2, 0u, b2, b3);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
-        if (++stage == C::kStages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    }
-    // ---- per-warp state -> smem, then cross-warp merge
-    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-    if ((lane & 3) == 0 && qr < G) {
-      ml[(warp * kMaxG + qr) * 2] = m0;
-      ml[(warp * kMaxG + qr) * 2 + 1] = l0;
-    }
-    if (qr < G) {
-#pragma unroll
-      for (int n = 0; n < NT; ++n)
-        *reinterpret_cast<float2*>(&mo[(warp * kMaxG + qr) * D + n * 8 + qc]) =
-            make_float2(o[n][0], o[n][1]);
-    }
-    unit_epilogue<__nv_bfloat16, D>(p, s, u, mo, ml, warp * 32 + lane);
-  }
-}
-
-// ---------------------------------------------------------------- fp32 path
-// CUDA-core FP32 (exact fp32 products); used for the fp32 parity configs.
-// Lane l of warp w owns row t0 + (l & 15) for the scores (half h = l >> 4 of
-// the d range), and d columns l, l+32, ... for PV.  Tiles are unswizzled.
-template <int D>
-__device__ __forceinline__ void consume_f32(const LycAttnParams& p, uint8_t* ring,
-                                            uint64_t* full, uint64_t* empty, float* mo,
-                                            float* ml, float* qs, int ub, int ue, int warp,
-                                            int lane) {
-  using C = AttnCfg<float, D>;
-  constexpr int DH = D / 2;
-  constexpr int DC = (D + 31) / 32;
-  const int G = p.group;
-  const int t0 = warp * 16;
-  const int tr = lane & 15, half = lane >> 4;
-  int stage = 0;
-  uint32_t phase = 0;
-  const float* Q = static_cast<const float*>(p.q);
-
-  for (int u = ub; u < ue; ++u) {
-    const LycUnit un = p.units[u];
-    const LycSlot s = p.slots[un.slot];
-    const int tpi = tiles_per_item(s, p.block_size);
-    const bool want_sel = s.sel >= 0 && p.sel_mode != SEL_NONE;
-    float m[kMaxG], l[kMaxG], o[kMaxG][DC];
-#pragma unroll
-    for (int j = 0; j < kMaxG; ++j) {
-      m[j] = -INFINITY;
-      l[j] = 0.f;
-#pragma unroll
-      for (int c = 0; c < DC; ++c) o[j][c] = 0.f;
-    }
-    // stage the group's queries (rows 0..G-1) and the pooled query (row G,
-    // gqa_pool_queries order: acc += q_j for j = 0..G-1, then acc /= G)
-    const int tid = warp * 32 + lane;
-    for (int d = tid; d < D; d += kConsumerWarps * 32) {
-      float acc = 0.f;
-      for (int j = 0; j < G; ++j) {
-        const float v = __ldg(Q + (int64_t)(s.q_row + j) * D + d);
-        qs[j * D + d] = v;
-        acc += v;
-      }
-      qs[G * D + d] = acc / (float)G;
-    }
-    consumer_bar();
-    for (int it = un.begin; it < un.end; ++it) {
-      for (int sub = 0; sub < tpi; ++sub) {
-        const Tile t = tile_of(s, it, sub, p.seq_len, p.block_size);
-        mbar_wait(&full[stage], phase);
-        const uint8_t* ks = ring + stage * C::kStageBytes;
-        const float* krow = reinterpret_cast<const float*>(ks + (t0 + tr) * C::kRowBytes);
-        const uint8_t* vs = ks + C::kTileBytes;
-        float sc[kMaxG], pooled = 0.f;
-#pragma unroll
-        for (int j = 0; j < kMaxG; ++j) sc[j] = 0.f;
-        for (int dd = 0; dd < DH; ++dd) {
-          const int d = half * DH + dd;
-          const float kv = krow[d];
-#pragma unroll
-          for (int j = 0; j < kMaxG; ++j)
-            if (j < G) sc[j] = fmaf(qs[j * D + d], kv, sc[j]);
-          if (want_sel) pooled = fmaf(qs[G * D + d], kv, pooled);
-        }
-#pragma unroll
-        for (int j = 0; j < kMaxG; ++j) sc[j] += __shfl_xor_sync(0xffffffffu, sc[j], 16);
-        const bool valid = t0 + tr < t.nvalid;
-        if (want_sel) {
-          pooled += __shfl_xor_sync(0xffffffffu, pooled, 16);
-          if (p.sel_mode == SEL_TOKEN_KEYS) {
-            if (half == 0 && valid)
-              p.sel_keys[(int64_t)s.sel * p.sel_stride + t.lo + t0 + tr] = float_key(pooled);
-          } else {
-            uint32_t km = (half == 0 && valid) ? float_key(pooled) : 0u;
-#pragma unroll
-            for (int off = 1; off < 16; off <<= 1)
-              km = max(km, __shfl_xor_sync(0xffffffffu, km, off));
-            if (lane == 0 && km != 0u)
-              atomicMax(p.sel_keys + (int64_t)s.sel * p.sel_stride + it, km);
-          }
-        }
-        float pr[kMaxG];
-#pragma unroll
-        for (int j = 0; j < kMaxG; ++j) {
-          if (j >= G) break;
-          const float x = valid ? sc[j] * p.scale_log2 : -INFINITY;
-          float mx = x;
-#pragma unroll
-          for (int off = 1; off < 16; off <<= 1)
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-          const float mn = fmaxf(m[j], mx);
-          const float r = m[j] == -INFINITY ? 0.f : exp2f(m[j] - mn);
-          const float uu = mn == -INFINITY ? 0.f : mn;
-          pr[j] = exp2f(x - uu);
-          float ps = half == 0 ? pr[j] : 0.f;
-#pragma unroll
-          for (int off = 1; off < 32; off <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
-          l[j] = l[j] * r + ps;
-          m[j] = mn;
-#pragma unroll
-          for (int c = 0; c < DC; ++c) o[j][c] *= r;
-        }
-        for (int rr = 0; rr < 16; ++rr) {
-          const float* vrow = reinterpret_cast<const float*>(vs + (t0 + rr) * C::kRowBytes);
-#pragma unroll
-          for (int j = 0; j < kMaxG; ++j) {
-            if (j >= G) break;
-            const float pj = __shfl_sync(0xffffffffu, pr[j], rr);
-#pragma unroll
-            for (int c = 0; c < DC; ++c)
-              if (c * 32 + lane < D) o[j][c] = fmaf(pj, vrow[c * 32 + lane], o[j][c]);
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
-        if (++stage == C::kStages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kMaxG; ++j) {
-      if (j >= G) break;
-      if (lane == 0) {
-        ml[(warp * kMaxG + j) * 2] = m[j];
-        ml[(warp * kMaxG + j) * 2 + 1] = l[j];
-      }
-#pragma unroll
-      for (int c = 0; c < DC; ++c)
-        if (c * 32 + lane < D) mo[(warp * kMaxG + j) * D + c * 32 + lane] = o[j][c];
-    }
-    unit_epilogue<float, D>(p, s, u, mo, ml, warp * 32 + lane);
-  }
-}
-
-template <typename T, int D>
-__global__ void __launch_bounds__(kThreads, 1) hybrid_attn_kernel(const __grid_constant__ LycAttnParams p) {
+__global__ void __launch_bounds__(kAttnThreads, 1) hybrid_attn_kernel(const __grid_constant__ LycAttnParams p) {
   using C = AttnCfg<T, D>;
   extern __shared__ uint8_t smem_raw[];
-  // 1024-B alignment for the 128B-swizzle atoms of the TMA destinations
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint8_t* ring = smem;
-  float* mo = reinterpret_cast<float*>(smem + C::kStages * C::kStageBytes);
-  float* ml = mo + kConsumerWarps * kMaxG * D;
-  float* qs = ml + kConsumerWarps * kMaxG * 2;
-  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(qs) + C::kQBytes);
-  uint64_t* empty = full + C::kStages;
-
+  const AttnSmem<T, D> sm = AttnSmem<T, D>::carve(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cell = blockIdx.y * p.n_splits + blockIdx.x;
-  const int ub = p.split_off[cell], ue = p.split_off[cell + 1];
+  const int cell = blockIdx.y * p.v.n_splits + blockIdx.x;
+  const int ub = p.v.split_off[cell], ue = p.v.split_off[cell + 1];
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&full[s], kProducerThreads);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&sm.full[s], kProducerThreads);
+      mbar_init(&sm.empty[s], kConsumerWarps);
     }
     fence_mbar_init();
   }
   __syncthreads();
+  int stage = 0;
+  uint32_t phase = 0;
   if (warp >= kConsumerWarps) {
-    produce<T, D>(p, ring, full, empty, ub, ue, threadIdx.x - kConsumerWarps * 32);
-  } else if constexpr (sizeof(T) == 2) {
-    consume_bf16<D>(p, ring, full, empty, mo, ml, ub, ue, warp, lane);
+    const int pt = threadIdx.x - kConsumerWarps * 32;
+    if (pt == 0) {
+      prefetch_tensormap(&p.tmap_k);
+      prefetch_tensormap(&p.tmap_v);
+    }
+    produce_units<T, D>(p.v, &p.tmap_k, &p.tmap_v, sm.ring, sm.full, sm.empty, ub, ue, pt, stage,
+                        phase, NoWaits{});
   } else {
-    consume_f32<D>(p, ring, full, empty, mo, ml, qs, ub, ue, warp, lane);
+    consume_units<T, D>(p.v, sm, ub, ue, warp, lane, stage, phase);
   }
 }
 
-// ---------------------------------------------------------------- merge
-// kernel_sim.hpp:205-225 combine, for slots with > 1 unit.  One warp per
-// (task = (slot, j), 32-column chunk); lanes stride over the slot's partials
-// in head-local split order, then a fixed-shape butterfly reduces across
-// lanes -> bitwise deterministic for a given plan.
 template <typename T>
 __global__ void __launch_bounds__(128) split_merge_kernel(const __grid_constant__ LycMergeParams p) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -561,51 +52,7 @@ __global__ void __launch_bounds__(128) split_merge_kernel(const __grid_constant_
   if (task >= p.n_tasks) return;
   const LycMergeTask tk = p.tasks[task];
   const LycSlot s = p.slots[tk.slot];
-  const int D = p.d;
-  const int G = p.group;
-  float M = -INFINITY;
-  for (int i = lane; i < s.n_units; i += 32)
-    M = fmaxf(M, __ldcg(p.part_lse + (int64_t)(s.first_unit + i) * G + tk.j));
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-  float den = 0.f;
-  float acc[32];
-#pragma unroll
-  for (int c = 0; c < 32; ++c) acc[c] = 0.f;
-  for (int i = lane; i < s.n_units; i += 32) {
-    const int64_t u = s.first_unit + i;
-    const float w = exp2f(__ldcg(p.part_lse + u * G + tk.j) - M);
-    den += w;
-    const float4* src = reinterpret_cast<const float4*>(p.part_o + (u * G + tk.j) * D + chunk * 32);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      if (chunk * 32 + 4 * c >= D) break;
-      const float4 v = __ldcg(src + c);
-      acc[4 * c] = fmaf(w, v.x, acc[4 * c]);
-      acc[4 * c + 1] = fmaf(w, v.y, acc[4 * c + 1]);
-      acc[4 * c + 2] = fmaf(w, v.z, acc[4 * c + 2]);
-      acc[4 * c + 3] = fmaf(w, v.w, acc[4 * c + 3]);
-    }
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) den += __shfl_xor_sync(0xffffffffu, den, off);
-  // reduce-scatter butterfly: after 5 rounds lane l holds column l's sum.
-#pragma unroll
-  for (int r = 0; r < 5; ++r) {
-    const int half = 16 >> r;
-    const bool upper = (lane & half) != 0;
-#pragma unroll
-    for (int c = 0; c < half; ++c) {
-      const float send = upper ? acc[c] : acc[c + half];
-      const float keep = upper ? acc[c + half] : acc[c];
-      acc[c] = keep + __shfl_xor_sync(0xffffffffu, send, half);
-    }
-  }
-  // lane's column: bits of lane select the kept half at each round
-  const int col = lane;  // round r keeps the half selected by lane bit (16 >> r)
-  if (chunk * 32 + col < D)
-    store_out<T>(static_cast<T*>(p.out) + (int64_t)(s.q_row + tk.j) * D + chunk * 32 + col,
-               acc[0] / den);
+  merge_task<T>(p.part_o, p.part_lse, s, tk.j, chunk, p.group, p.d, p.out, lane);
 }
 
 // ---------------------------------------------------------------- launchers
@@ -619,8 +66,8 @@ static cudaError_t launch_attn_t(const LycAttnParams& p, int batch, cudaStream_t
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid(p.n_splits, batch);
-  hybrid_attn_kernel<T, D><<<grid, kThreads, C::kSmem, st>>>(p);
+  dim3 grid(p.v.n_splits, batch);
+  hybrid_attn_kernel<T, D><<<grid, kAttnThreads, C::kSmem, st>>>(p);
   return cudaGetLastError();
 }
 
@@ -640,24 +87,6 @@ cudaError_t launch_attn(const LycAttnParams& p, int dtype, int d, int batch, cud
     }
   }
   return cudaErrorInvalidValue;
-}
-
-int attn_stages(int dtype, int d) {
-  if (dtype == 1) {
-    switch (d) {
-      case 64: return AttnCfg<__nv_bfloat16, 64>::kStages;
-      case 128: return AttnCfg<__nv_bfloat16, 128>::kStages;
-      case 256: return AttnCfg<__nv_bfloat16, 256>::kStages;
-    }
-  } else {
-    switch (d) {
-      case 16: return AttnCfg<float, 16>::kStages;
-      case 32: return AttnCfg<float, 32>::kStages;
-      case 64: return AttnCfg<float, 64>::kStages;
-      case 128: return AttnCfg<float, 128>::kStages;
-    }
-  }
-  return 0;
 }
 
 cudaError_t launch_merge(const LycMergeParams& p, int dtype, cudaStream_t st) {

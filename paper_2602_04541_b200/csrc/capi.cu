@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -24,6 +25,8 @@ cudaError_t launch_topk(const LycTopkParams& p, int rows, int cluster, cudaStrea
 int topk_cluster_size(int n, int max_slice);
 size_t topk_smem_bytes(int slice);
 cudaError_t launch_float_keys(const float* s, uint32_t* keys, int64_t n, cudaStream_t st);
+cudaError_t launch_step(const LycStepParams& p, int dtype, int d, int batch, cudaStream_t st);
+bool step_supported(int dtype, int d);
 }  // namespace lyc
 
 namespace {
@@ -304,6 +307,7 @@ int64_t lyc_fraction_budget(double frac, int64_t n) {
   return std::min(b, n);
 }
 
+
 // ------------------------------------------------------------- kernel::run
 int lyc_workload_run(const lyc_workload* w, int64_t num_splits, void* out, uint32_t* exec_counts,
                      void* stream) {
@@ -315,8 +319,7 @@ int lyc_workload_run(const lyc_workload* w, int64_t num_splits, void* out, uint3
       fail(LYC_EINVAL, "Workload: all dimensions must be >= 1");
     if (num_splits < 1) fail(LYC_EINVAL, "plan_splits: num_splits must be >= 1");
     if (!supported_d(w->dtype, w->d_head)) fail(LYC_ENOTSUP, "Workload: unsupported d_head/dtype on device");
-    if (w->group_size > 8)
-      fail(LYC_ENOTSUP, "Workload: group_size too large for the device kernel");
+    if (w->group_size > 8) fail(LYC_ENOTSUP, "Workload: group_size > 8 not supported by the device kernel");
     if (w->kv_row_stride < w->seq_len) fail(LYC_EINVAL, "Workload: kv_row_stride < seq_len");
     const int64_t B = w->batch, H = w->n_kv_heads, G = w->group_size, D = w->d_head;
     const int64_t nb = (w->seq_len + w->block_size - 1) / w->block_size;
@@ -345,6 +348,7 @@ int lyc_workload_run(const lyc_workload* w, int64_t num_splits, void* out, uint3
         s.list_len = s.n_items;
         s.q_row = (int32_t)(b * H * G + g * G);
         s.sel = -1;
+        s.dep = -1;
       }
     plan_launch(L, (int)B, (int)H, (int)num_splits, (int)G);
     for (auto& s : L.slots)
@@ -364,32 +368,34 @@ int lyc_workload_run(const lyc_workload* w, int64_t num_splits, void* out, uint3
     host.resize(plan_b + ids_b);
     if (!ids.empty()) std::memcpy(host.data() + plan_b, ids.data(), ids.size() * 4);
     cuda_check(cudaMemcpyAsync(dev, host.data(), host.size(), cudaMemcpyHostToDevice, st), "H2D plan");
-    LycAttnParams ap{};
-    ap.k = w->k;
-    ap.v = w->v;
-    ap.q = w->q;
-    ap.out = out;
-    ap.slots = dl.slots;
-    ap.units = dl.units;
-    ap.split_off = dl.split_off;
-    ap.part_o = (float*)(dev + plan_b + ids_b);
-    ap.part_lse = (float*)(dev + plan_b + ids_b + po_b);
-    ap.exec_counts = exec_counts;
-    ap.counts_stride = (int32_t)nb;
-    ap.n_splits = (int32_t)num_splits;
-    ap.seq_len = (int32_t)w->seq_len;
-    ap.block_size = (int32_t)w->block_size;
-    ap.group = (int32_t)G;
-    ap.sel_mode = SEL_NONE;
-    ap.scale = w->scale;
-    ap.scale_log2 = w->scale * 1.4426950408889634f;
+    LycAttnParams ap;
+    std::memset(&ap, 0, sizeof(ap));
+    LycView& v = ap.v;
+    v.k = w->k;
+    v.v = w->v;
+    v.q = w->q;
+    v.out = out;
+    v.slots = dl.slots;
+    v.units = dl.units;
+    v.split_off = dl.split_off;
+    v.part_o = (float*)(dev + plan_b + ids_b);
+    v.part_lse = (float*)(dev + plan_b + ids_b + po_b);
+    v.exec_counts = exec_counts;
+    v.counts_stride = (int32_t)nb;
+    v.n_splits = (int32_t)num_splits;
+    v.seq_len = (int32_t)w->seq_len;
+    v.block_size = (int32_t)w->block_size;
+    v.group = (int32_t)G;
+    v.sel_mode = SEL_NONE;
+    v.scale = w->scale;
+    v.scale_log2 = w->scale * 1.4426950408889634f;
     encode_kv_maps(ap, w->k, w->v, B * H * w->kv_row_stride, (int)D, w->dtype);
     cuda_check(lyc::launch_attn(ap, w->dtype, (int)D, (int)B, st), "attention launch");
     ++g_launches;
     if (dl.n_merges) {
       LycMergeParams mp{};
-      mp.part_o = ap.part_o;
-      mp.part_lse = ap.part_lse;
+      mp.part_o = v.part_o;
+      mp.part_lse = v.part_lse;
       mp.slots = dl.slots;
       mp.tasks = dl.merges;
       mp.out = out;
@@ -440,38 +446,48 @@ int64_t lyc_args_top_k(const float* scores, int64_t n, int64_t k, int32_t* out, 
   });
 }
 
+}  // extern "C"
+
 // ------------------------------------------------------------- decoder
 struct lyc_decoder {
   lyc_decode_config cfg{};
   std::vector<uint8_t> roles;
   int B = 0, H = 0, G = 0, Hq = 0, D = 0, NL = 0, S = 0, bs = 64;
+  bool fused = false;           // whole step in one persistent launch (step.cu)
   int64_t k_cap = 0;
-  int32_t* idx = nullptr;      // [B*H][k_cap]
+  int32_t* idx = nullptr;       // [B*H][k_cap]
   int32_t* idx_count = nullptr;
-  uint32_t* sel_keys = nullptr;
+  uint32_t* sel_keys = nullptr; // [2][B*H][sel_stride]
   int64_t sel_stride = 0;
+  uint32_t* hist = nullptr;     // [2][3][B*H][LYC_BINS]
+  uint32_t* team = nullptr;     // [2][B*H][n_ctas][2]
+  uint32_t* ctr = nullptr;      // [NL][CTR_PER_LAYER] + 2
   float* part_o = nullptr;
   float* part_lse = nullptr;
   size_t part_units = 0;
   uint8_t* blob = nullptr;
   size_t blob_cap = 0;
   int64_t planned_seq = -1;
-  LycAttnParams maps{};        // tensor maps for the last (k, v) pointers
+  LycAttnParams maps{};         // tensor maps for the last (k, v) pointers
   const void* map_k = nullptr;
   const void* map_v = nullptr;
   struct Layer {
-    LycAttnParams ap;
+    LycAttnParams ap;           // per-layer kernel path
     LycMergeParams mp;
     LycTopkParams tp;
+    LycLayerDesc desc;          // step kernel path
     int n_sel = 0, cluster = 1, n_merges = 0;
   };
   std::vector<Layer> layers;
+  LycLayerDesc* d_layers = nullptr;  // device copy of the step descriptors
+  int64_t n_keys = 0, k_sel = 0;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   bool timing = false;
-  std::vector<cudaEvent_t> ev_pre, ev_post;  // per layer, around the attention kernel
+  std::vector<cudaEvent_t> ev_pre, ev_post;  // per layer (per-layer path) or [0] (fused)
   std::vector<uint8_t> staging;
 
+  int n_ctas() const { return S * B; }
   bool retrieval(int l, int g) const { return l == 0 || roles[(size_t)l * H + g] == 0; }
 
   int64_t budget(int64_t seq) const {  // tokens (or blocks) kept per sparse head
@@ -487,18 +503,97 @@ struct lyc_decoder {
 
 namespace {
 
+// The step kernel's split order: per batch item, slots whose index list is
+// produced by the immediately preceding layer's selection (pool B) are placed
+// after everything else (pool A) inside every split, so each CTA streams its
+// independent tiles while that selection is still running.
+void plan_step_launch(HostLaunch& L, int batch, int heads, int splits, int group, int layer) {
+  L.batch = batch;
+  L.heads = heads;
+  L.splits = splits;
+  L.units.clear();
+  L.merges.clear();
+  L.split_off.assign((size_t)batch * splits + 1, 0);
+  std::vector<std::vector<std::vector<LycUnit>>> per_split((size_t)batch);
+  for (int b = 0; b < batch; ++b) {
+    per_split[(size_t)b].assign((size_t)splits, {});
+    int64_t total = 0;
+    for (int g = 0; g < heads; ++g) {
+      LycSlot& s = L.slots[(size_t)b * heads + g];
+      s.n_units = 0;
+      total += s.n_items;
+    }
+    if (total == 0) fail(LYC_EINVAL, "plan_splits: batch item has zero blocks");
+    for (int pool = 0; pool < 2; ++pool) {
+      std::vector<int> hs;
+      int64_t tot = 0;
+      for (int g = 0; g < heads; ++g) {
+        const LycSlot& s = L.slots[(size_t)b * heads + g];
+        const bool late = s.dep >= 0 && s.dep == layer - 1;
+        if ((pool == 1) == late && s.n_items > 0) {
+          hs.push_back(g);
+          tot += s.n_items;
+        }
+      }
+      if (tot == 0) continue;
+      const int64_t base = tot / splits, rem = tot % splits;
+      size_t hi = 0;
+      int64_t offset = 0;
+      for (int sp = 0; sp < splits; ++sp) {
+        int64_t want = base + (sp < rem ? 1 : 0);
+        while (want > 0) {
+          while (L.slots[(size_t)b * heads + hs[hi]].n_items == offset) {
+            ++hi;
+            offset = 0;
+          }
+          LycSlot& sl = L.slots[(size_t)b * heads + hs[hi]];
+          const int64_t take = std::min<int64_t>(sl.n_items - offset, want);
+          LycUnit u;
+          u.slot = b * heads + hs[hi];
+          u.begin = (int32_t)offset;
+          u.end = (int32_t)(offset + take);
+          u.hls = sl.n_units++;
+          per_split[(size_t)b][(size_t)sp].push_back(u);
+          offset += take;
+          want -= take;
+        }
+      }
+    }
+  }
+  for (int b = 0; b < batch; ++b)
+    for (int sp = 0; sp < splits; ++sp) {
+      L.split_off[(size_t)b * splits + sp] = (int32_t)L.units.size();
+      for (const LycUnit& u : per_split[(size_t)b][(size_t)sp]) L.units.push_back(u);
+    }
+  L.split_off[(size_t)batch * splits] = (int32_t)L.units.size();
+  int32_t base = 0;  // partial-output base of every slot (units of a slot need not be adjacent)
+  for (auto& s : L.slots) {
+    s.first_unit = base;
+    base += s.n_units;
+  }
+  for (size_t i = 0; i < L.slots.size(); ++i)
+    if (L.slots[i].n_units > 1)
+      for (int j = 0; j < group; ++j) L.merges.push_back(LycMergeTask{(int32_t)i, j});
+}
+
+void free_dev(void* p) {
+  if (p) cudaFree(p);
+}
+
 void decoder_plan(lyc_decoder* d, int64_t seq) {
   if (seq < 1) fail(LYC_EINVAL, "decode_step: seq_len must be >= 1");
   if (seq > d->cfg.seq_cap) fail(LYC_EINVAL, "decode_step: seq_len exceeds seq_cap");
-  if (seq > (int64_t)16 * 32768 && d->cfg.select_mode == LYC_SELECT_TOKENS)
+  if (!d->fused && seq > (int64_t)16 * 32768 && d->cfg.select_mode == LYC_SELECT_TOKENS)
     fail(LYC_ENOTSUP, "decode_step: token-mode selection supports seq_len <= 524288");
   if (d->planned_seq == seq) return;
   const int B = d->B, H = d->H, G = d->G, D = d->D;
   const int64_t kb = d->budget(seq);
   const bool blocks = d->cfg.select_mode == LYC_SELECT_BLOCKS;
+  const bool none = d->cfg.select_mode == LYC_SELECT_NONE;
   const int64_t nb = (seq + d->bs - 1) / d->bs;
   std::vector<HostLaunch> hl((size_t)d->NL);
-  size_t total = 0, max_units = 0;
+  size_t total = 0, max_parts = 0;
+  std::vector<int> last_r((size_t)H, 0);  // nearest retrieval layer of each head so far
   for (int l = 0; l < d->NL; ++l) {
     HostLaunch& L = hl[(size_t)l];
     L.slots.resize((size_t)B * H);
@@ -508,37 +603,45 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
         std::memset(&s, 0, sizeof(s));
         s.kv_off = (((int64_t)l * B + b) * H + g) * d->cfg.seq_cap * D;
         s.q_row = b * H * G + g * G;
+        s.dep = -1;
+        s.sel = -1;
         if (d->retrieval(l, g)) {
           s.kind = ITEM_DENSE;
           s.n_items = (int32_t)nb;
-          if (d->cfg.select_mode != LYC_SELECT_NONE) {
+          if (!none) {
             s.sel = (int32_t)L.sel_rows.size();
             L.sel_rows.push_back(b * H + g);
-          } else {
-            s.sel = -1;
           }
         } else {
           s.kind = blocks ? ITEM_BLOCKS : ITEM_TOKENS;
           s.list = d->idx + (int64_t)(b * H + g) * d->k_cap;
           s.list_len = (int32_t)kb;
           s.n_items = blocks ? (int32_t)kb : (int32_t)((kb + LYC_TILE - 1) / LYC_TILE);
-          s.sel = -1;
+          s.dep = last_r[(size_t)g];
         }
       }
-    plan_launch(L, B, H, d->S, G);
+    for (int g = 0; g < H; ++g)
+      if (d->retrieval(l, g)) last_r[(size_t)g] = l;
+    if (d->fused)
+      plan_step_launch(L, B, H, d->S, G, l);
+    else
+      plan_launch(L, B, H, d->S, G);
     total += launch_bytes(L);
-    max_units = std::max(max_units, L.units.size());
+    size_t parts = 0;
+    for (auto& s : L.slots) parts += (size_t)s.n_units;
+    max_parts = std::max(max_parts, parts);
   }
-  if (max_units > d->part_units) {
-    cudaFree(d->part_o);
-    cudaFree(d->part_lse);
+  total += align_up(sizeof(LycLayerDesc) * d->NL, 256);
+  if (max_parts > d->part_units) {
+    free_dev(d->part_o);
+    free_dev(d->part_lse);
     d->part_o = d->part_lse = nullptr;
-    cuda_check(cudaMalloc(&d->part_o, max_units * G * D * 4), "cudaMalloc part_o");
-    cuda_check(cudaMalloc(&d->part_lse, max_units * G * 4), "cudaMalloc part_lse");
-    d->part_units = max_units;
+    cuda_check(cudaMalloc(&d->part_o, max_parts * G * D * 4), "cudaMalloc part_o");
+    cuda_check(cudaMalloc(&d->part_lse, max_parts * G * 4), "cudaMalloc part_lse");
+    d->part_units = max_parts;
   }
   if (total > d->blob_cap) {
-    cudaFree(d->blob);
+    free_dev(d->blob);
     d->blob = nullptr;
     cuda_check(cudaMalloc(&d->blob, total), "cudaMalloc plan");
     d->blob_cap = total;
@@ -547,28 +650,30 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
   size_t off = 0;
   d->layers.assign((size_t)d->NL, {});
   const int64_t sel_n = blocks ? nb : seq;
-  const int cluster = lyc::topk_cluster_size((int)sel_n, 16384);
+  d->n_keys = sel_n;
+  d->k_sel = kb;
+  const int cluster = lyc::topk_cluster_size((int)std::min<int64_t>(sel_n, 1 << 30), 16384);
+  std::vector<LycLayerDesc> descs((size_t)d->NL);
   for (int l = 0; l < d->NL; ++l) {
     HostLaunch& L = hl[(size_t)l];
     DevLaunch dl = stage_launch(L, d->staging, off, d->blob);
     lyc_decoder::Layer& ly = d->layers[(size_t)l];
-    LycAttnParams& ap = ly.ap;
-    std::memset(&ap, 0, sizeof(ap));
-    ap.slots = dl.slots;
-    ap.units = dl.units;
-    ap.split_off = dl.split_off;
-    ap.part_o = d->part_o;
-    ap.part_lse = d->part_lse;
-    ap.sel_keys = d->sel_keys;
-    ap.sel_stride = d->sel_stride;
-    ap.n_splits = d->S;
-    ap.seq_len = (int32_t)seq;
-    ap.block_size = d->bs;
-    ap.group = G;
-    ap.sel_mode = d->cfg.select_mode == LYC_SELECT_NONE ? SEL_NONE
-                  : blocks ? SEL_BLOCK_KEYS : SEL_TOKEN_KEYS;
-    ap.scale = d->cfg.scale;
-    ap.scale_log2 = d->cfg.scale * 1.4426950408889634f;
+    std::memset(&ly.ap, 0, sizeof(ly.ap));
+    LycView& v = ly.ap.v;
+    v.slots = dl.slots;
+    v.units = dl.units;
+    v.split_off = dl.split_off;
+    v.part_o = d->part_o;
+    v.part_lse = d->part_lse;
+    v.sel_keys = d->sel_keys;
+    v.sel_stride = d->sel_stride;
+    v.n_splits = d->S;
+    v.seq_len = (int32_t)seq;
+    v.block_size = d->bs;
+    v.group = G;
+    v.sel_mode = none ? SEL_NONE : blocks ? SEL_BLOCK_KEYS : SEL_TOKEN_KEYS;
+    v.scale = d->cfg.scale;
+    v.scale_log2 = d->cfg.scale * 1.4426950408889634f;
     LycMergeParams& mp = ly.mp;
     std::memset(&mp, 0, sizeof(mp));
     mp.part_o = d->part_o;
@@ -594,33 +699,54 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
     tp.clear_keys = blocks ? 1 : 0;
     ly.n_sel = dl.n_sel;
     ly.cluster = cluster;
+    LycLayerDesc& ds = descs[(size_t)l];
+    ds.slots = dl.slots;
+    ds.units = dl.units;
+    ds.split_off = dl.split_off;
+    ds.merges = dl.merges;
+    ds.sel_rows = dl.sel_rows;
+    ds.n_merges = dl.n_merges;
+    ds.n_sel = dl.n_sel;
+    ly.desc = ds;
   }
+  d->d_layers = (LycLayerDesc*)(d->blob + off);
+  std::memcpy(d->staging.data() + off, descs.data(), sizeof(LycLayerDesc) * d->NL);
   cuda_check(cudaMemcpy(d->blob, d->staging.data(), total, cudaMemcpyHostToDevice), "H2D plan");
+  // a new plan restarts the step counters (any previous step has completed:
+  // the synchronous copy above serialises with the legacy stream)
+  cuda_check(cudaMemset(d->ctr, 0, ((size_t)d->NL * CTR_PER_LAYER + 2) * 4), "memset counters");
+  cuda_check(cudaDeviceSynchronize(), "sync");
   d->planned_seq = seq;
+}
+
+void ensure_maps(lyc_decoder* d, const void* k, const void* v) {
+  if (k != d->map_k || v != d->map_v) {
+    encode_kv_maps(d->maps, k, v, (int64_t)d->NL * d->B * d->H * d->cfg.seq_cap, d->D,
+                   d->cfg.dtype);
+    d->map_k = k;
+    d->map_v = v;
+  }
+}
+
+void record(lyc_decoder* d, std::vector<cudaEvent_t>& ev, size_t i, cudaStream_t st) {
+  // External records become event nodes when the stream is being captured.
+  if (d->timing)
+    cuda_check(cudaEventRecordWithFlags(ev[i], st, cudaEventRecordExternal), "event record");
 }
 
 void decoder_layer(lyc_decoder* d, int l, const void* q_l, const void* k, const void* v,
                    void* out_l, cudaStream_t st) {
   lyc_decoder::Layer& ly = d->layers[(size_t)l];
-  if (k != d->map_k || v != d->map_v) {
-    encode_kv_maps(d->maps, k, v, (int64_t)d->NL * d->B * d->H * d->cfg.seq_cap, d->D, d->cfg.dtype);
-    d->map_k = k;
-    d->map_v = v;
-  }
+  ensure_maps(d, k, v);
   ly.ap.tmap_k = d->maps.tmap_k;
   ly.ap.tmap_v = d->maps.tmap_v;
-  ly.ap.k = k;
-  ly.ap.v = v;
-  ly.ap.q = q_l;
-  ly.ap.out = out_l;
-  // External records become event nodes when the stream is being captured.
-  if (d->timing)
-    cuda_check(cudaEventRecordWithFlags(d->ev_pre[(size_t)l], st, cudaEventRecordExternal),
-               "event record");
+  ly.ap.v.k = k;
+  ly.ap.v.v = v;
+  ly.ap.v.q = q_l;
+  ly.ap.v.out = out_l;
+  record(d, d->ev_pre, (size_t)l, st);
   cuda_check(lyc::launch_attn(ly.ap, d->cfg.dtype, d->D, d->B, st), "attention launch");
-  if (d->timing)
-    cuda_check(cudaEventRecordWithFlags(d->ev_post[(size_t)l], st, cudaEventRecordExternal),
-               "event record");
+  record(d, d->ev_post, (size_t)l, st);
   ++g_launches;
   if (ly.n_merges) {
     ly.mp.out = out_l;
@@ -636,12 +762,58 @@ void decoder_layer(lyc_decoder* d, int l, const void* q_l, const void* k, const 
 void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, int64_t seq,
                   void* out, cudaStream_t st) {
   decoder_plan(d, seq);
-  const size_t qstride = (size_t)d->B * d->Hq * d->D * elem_bytes(d->cfg.dtype);
-  for (int l = 0; l < d->NL; ++l)
-    decoder_layer(d, l, (const uint8_t*)q + l * qstride, k, v, (uint8_t*)out + l * qstride, st);
+  const int esz = elem_bytes(d->cfg.dtype);
+  const size_t qstride = (size_t)d->B * d->Hq * d->D;
+  if (!d->fused) {
+    for (int l = 0; l < d->NL; ++l)
+      decoder_layer(d, l, (const uint8_t*)q + l * qstride * esz, k, v,
+                    (uint8_t*)out + l * qstride * esz, st);
+    return;
+  }
+  ensure_maps(d, k, v);
+  LycStepParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.tmap_k = d->maps.tmap_k;
+  p.tmap_v = d->maps.tmap_v;
+  p.k = k;
+  p.v = v;
+  p.q = q;
+  p.out = out;
+  p.q_layer_stride = (int64_t)qstride;
+  p.layers = d->d_layers;
+  p.part_o = d->part_o;
+  p.part_lse = d->part_lse;
+  p.sel_keys = d->sel_keys;
+  p.sel_stride = d->sel_stride;
+  p.hist = d->hist;
+  p.team = d->team;
+  p.ctr = d->ctr;
+  p.idx = d->idx;
+  p.idx_stride = d->k_cap;
+  p.idx_count = d->idx_count;
+  p.n_layers = d->NL;
+  p.max_sel = d->B * d->H;
+  p.n_keys = (int32_t)d->n_keys;
+  p.k_sel = (int32_t)d->k_sel;
+  p.n_splits = d->S;
+  p.n_ctas = d->n_ctas();
+  p.seq_len = (int32_t)seq;
+  p.block_size = d->bs;
+  p.group = d->G;
+  p.sel_mode = d->cfg.select_mode == LYC_SELECT_NONE    ? SEL_NONE
+               : d->cfg.select_mode == LYC_SELECT_BLOCKS ? SEL_BLOCK_KEYS
+                                                         : SEL_TOKEN_KEYS;
+  p.scale = d->cfg.scale;
+  p.scale_log2 = d->cfg.scale * 1.4426950408889634f;
+  record(d, d->ev_pre, 0, st);
+  cuda_check(lyc::launch_step(p, d->cfg.dtype, d->D, d->B, st), "step launch");
+  record(d, d->ev_post, 0, st);
+  ++g_launches;
 }
 
 }  // namespace
+
+extern "C" {
 
 int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
   return (int)guarded([&]() -> int64_t {
@@ -651,8 +823,7 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
         c.seq_cap < 1)
       fail(LYC_EINVAL, "ModelConfig: all dimensions must be >= 1");
     if (!supported_d(c.dtype, c.d_head)) fail(LYC_ENOTSUP, "decoder: unsupported d_head/dtype");
-    if (c.group_size > 8)
-      fail(LYC_ENOTSUP, "decoder: group_size too large for the device kernel");
+    if (c.group_size > 8) fail(LYC_ENOTSUP, "decoder: group_size > 8 not supported by the device kernel");
     if (c.policy_kind == LYC_POLICY_TOPK) {
       if (c.top_k < 1) fail(LYC_EINVAL, "top_k: k must be >= 1");
     } else if (c.policy_kind == LYC_POLICY_RATIO) {
@@ -665,13 +836,13 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
     if (c.select_mode != LYC_SELECT_TOKENS && c.select_mode != LYC_SELECT_BLOCKS &&
         c.select_mode != LYC_SELECT_NONE)
       fail(LYC_EINVAL, "decoder: unknown select mode");
-    if (c.select_mode == LYC_SELECT_NONE)
-      for (int64_t i = 0; i < (int64_t)c.n_layers * c.n_kv_heads; ++i)
-        if (c.roles[i] != 0) fail(LYC_EINVAL, "decoder: sparse heads need a selection mode");
     if (c.block_size != 0 && c.block_size != 64) fail(LYC_ENOTSUP, "decoder: block_size must be 64");
     if (!c.roles) fail(LYC_EINVAL, "RoleMap: null roles");
     for (int g = 0; g < c.n_kv_heads; ++g)
       if (c.roles[g] != 0) fail(LYC_EINVAL, "RoleMap: layer 0 heads must all be Retrieval");
+    if (c.select_mode == LYC_SELECT_NONE)
+      for (int64_t i = 0; i < (int64_t)c.n_layers * c.n_kv_heads; ++i)
+        if (c.roles[i] != 0) fail(LYC_EINVAL, "decoder: sparse heads need a selection mode");
     auto* d = new lyc_decoder();
     d->cfg = c;
     d->roles.assign(c.roles, c.roles + (size_t)c.n_layers * c.n_kv_heads);
@@ -684,7 +855,11 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
     d->D = c.d_head;
     d->NL = c.n_layers;
     d->bs = 64;
-    d->S = c.num_splits > 0 ? c.num_splits : std::max(1, num_sms() / d->B);
+    const int sms = num_sms();
+    d->S = c.num_splits > 0 ? c.num_splits : std::max(1, sms / d->B);
+    // the persistent step kernel needs every CTA co-resident (1 CTA per SM)
+    d->fused = lyc::step_supported(c.dtype, c.d_head) && d->S * d->B <= sms &&
+               (int64_t)d->B * d->H <= 252 && std::getenv("LYC_NO_FUSED_STEP") == nullptr;
     const int64_t nb_cap = (c.seq_cap + d->bs - 1) / d->bs;
     if (c.select_mode == LYC_SELECT_BLOCKS) {
       d->k_cap = c.policy_kind == LYC_POLICY_RATIO ? nb_cap
@@ -700,8 +875,13 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
       cuda_check(cudaMalloc(&d->idx_count, rows * 4), "cudaMalloc index counts");
       cuda_check(cudaMemset(d->idx, 0, rows * d->k_cap * 4), "memset");
       cuda_check(cudaMemset(d->idx_count, 0, rows * 4), "memset");
-      cuda_check(cudaMalloc(&d->sel_keys, rows * d->sel_stride * 4), "cudaMalloc keys");
-      cuda_check(cudaMemset(d->sel_keys, 0, rows * d->sel_stride * 4), "memset");
+      cuda_check(cudaMalloc(&d->sel_keys, 2 * rows * d->sel_stride * 4), "cudaMalloc keys");
+      cuda_check(cudaMemset(d->sel_keys, 0, 2 * rows * d->sel_stride * 4), "memset");
+      cuda_check(cudaMalloc(&d->hist, 2 * 3 * rows * LYC_BINS * 4), "cudaMalloc hist");
+      cuda_check(cudaMemset(d->hist, 0, 2 * 3 * rows * LYC_BINS * 4), "memset");
+      cuda_check(cudaMalloc(&d->team, 2 * rows * (size_t)d->n_ctas() * 2 * 4), "cudaMalloc team");
+      cuda_check(cudaMalloc(&d->ctr, ((size_t)d->NL * CTR_PER_LAYER + 2) * 4), "cudaMalloc ctr");
+      cuda_check(cudaMemset(d->ctr, 0, ((size_t)d->NL * CTR_PER_LAYER + 2) * 4), "memset");
     } catch (...) {
       lyc_decoder_destroy(d);
       throw;
@@ -714,15 +894,18 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
 int lyc_decoder_destroy(lyc_decoder* d) {
   if (!d) return LYC_OK;
   if (d->exec) cudaGraphExecDestroy(d->exec);
+  if (d->graph) cudaGraphDestroy(d->graph);
   for (auto e : d->ev_pre) cudaEventDestroy(e);
   for (auto e : d->ev_post) cudaEventDestroy(e);
-  if (d->graph) cudaGraphDestroy(d->graph);
-  cudaFree(d->idx);
-  cudaFree(d->idx_count);
-  cudaFree(d->sel_keys);
-  cudaFree(d->part_o);
-  cudaFree(d->part_lse);
-  cudaFree(d->blob);
+  free_dev(d->idx);
+  free_dev(d->idx_count);
+  free_dev(d->sel_keys);
+  free_dev(d->hist);
+  free_dev(d->team);
+  free_dev(d->ctr);
+  free_dev(d->part_o);
+  free_dev(d->part_lse);
+  free_dev(d->blob);
   delete d;
   return LYC_OK;
 }
@@ -741,6 +924,11 @@ int lyc_decoder_layer(lyc_decoder* d, int32_t layer, const void* q_l, const void
   return (int)guarded([&]() -> int64_t {
     if (!d) fail(LYC_EINVAL, "decoder: null");
     if (layer < 0 || layer >= d->NL) fail(LYC_EINVAL, "decoder: layer out of range");
+    if (d->fused) {
+      // the single-layer entry uses the per-layer kernels and their plan
+      d->fused = false;
+      d->planned_seq = -1;
+    }
     decoder_plan(d, seq_len);
     decoder_layer(d, layer, q_l, k, v, out_l, (cudaStream_t)stream);
     return LYC_OK;
@@ -753,6 +941,7 @@ int lyc_decoder_capture(lyc_decoder* d, const void* q, const void* k, const void
     if (!d) fail(LYC_EINVAL, "decoder: null");
     cudaStream_t st = (cudaStream_t)stream;
     decoder_plan(d, seq_len);  // host work + plan upload outside the capture
+    ensure_maps(d, k, v);
     if (d->exec) {
       cudaGraphExecDestroy(d->exec);
       d->exec = nullptr;
@@ -799,6 +988,7 @@ int64_t lyc_decoder_launches_per_step(lyc_decoder* d, int64_t seq_len) {
   return guarded([&]() -> int64_t {
     if (!d) fail(LYC_EINVAL, "decoder: null");
     decoder_plan(d, seq_len);
+    if (d->fused) return 1;
     int64_t n = 0;
     for (auto& ly : d->layers) n += 1 + (ly.n_merges > 0) + (ly.n_sel > 0);
     return n;
@@ -808,24 +998,11 @@ int64_t lyc_decoder_launches_per_step(lyc_decoder* d, int64_t seq_len) {
 int64_t lyc_decoder_step_bytes(lyc_decoder* d, int64_t seq) {
   return guarded([&]() -> int64_t {
     if (!d) fail(LYC_EINVAL, "decoder: null");
-    const int64_t e = elem_bytes(d->cfg.dtype), D = d->D;
-    const int64_t kb = d->budget(seq);
-    const bool blocks = d->cfg.select_mode == LYC_SELECT_BLOCKS;
-    const int64_t sparse_rows = blocks ? std::min<int64_t>(kb * d->bs, seq) : kb;
     int64_t bytes = 0;
-    for (int l = 0; l < d->NL; ++l)
-      for (int g = 0; g < d->H; ++g) {
-        const bool r = d->retrieval(l, g);
-        bytes += (int64_t)d->B * ((r ? seq : sparse_rows) * 2 * D * e + 4 * kb);
-      }
-    bytes += (int64_t)d->NL * d->B * d->Hq * D * e * 2;  // Q in, O out
+    for (int l = 0; l < d->NL; ++l) bytes += lyc_decoder_layer_attn_bytes(d, l, seq);
     return bytes;
   });
 }
-
-}  // extern "C"
-
-extern "C" {
 
 int64_t lyc_decoder_layer_attn_bytes(lyc_decoder* d, int32_t layer, int64_t seq) {
   return guarded([&]() -> int64_t {
@@ -865,12 +1042,16 @@ int lyc_decoder_attn_ms(lyc_decoder* d, float* ms) {
   return (int)guarded([&]() -> int64_t {
     if (!d) fail(LYC_EINVAL, "decoder: null");
     if (d->ev_pre.empty()) fail(LYC_ESTATE, "decoder: timing was never enabled");
-    cuda_check(cudaEventSynchronize(d->ev_post.back()), "event sync");
-    for (int l = 0; l < d->NL; ++l)
+    const int n = d->fused ? 1 : d->NL;
+    cuda_check(cudaEventSynchronize(d->ev_post[(size_t)n - 1]), "event sync");
+    for (int l = 0; l < d->NL; ++l) ms[l] = 0.f;
+    for (int l = 0; l < n; ++l)
       cuda_check(cudaEventElapsedTime(&ms[l], d->ev_pre[(size_t)l], d->ev_post[(size_t)l]),
                  "event elapsed");
     return LYC_OK;
   });
 }
+
+int lyc_decoder_is_fused(lyc_decoder* d) { return d && d->fused ? 1 : 0; }
 
 }  // extern "C"

@@ -1,9 +1,9 @@
 // lyc_plan.h -- device work descriptors shared by the host planner (capi.cu)
-// and the kernels (attn.cu, epilogue.cu).  Plain structs, uploaded once per
-// plan and read-only on the device.
+// and the kernels (attn_core.cuh, attn.cu, step.cu).  Plain structs, uploaded
+// once per plan and read-only on the device.
 //
-// A "slot" is one (batch item b, KV head g) of one launch.  Its work list is
-// a sequence of ITEMS; each item expands to ceil(block_size/64) TILES of <= 64
+// A "slot" is one (batch item b, KV head g) of one layer.  Its work list is a
+// sequence of ITEMS; each item expands to ceil(block_size/64) TILES of <= 64
 // KV rows (the kernels' unit of TMA staging):
 //   ITEM_DENSE  item i -> rows [i*bs, min((i+1)*bs, seq))          retrieval head
 //   ITEM_BLOCKS item i -> rows of block list[i]                     BlockIndexSet
@@ -16,6 +16,7 @@
 #include <stdint.h>
 
 #define LYC_TILE 64
+#define LYC_BINS 2048
 
 enum { ITEM_DENSE = 0, ITEM_BLOCKS = 1, ITEM_TOKENS = 2 };
 
@@ -29,7 +30,7 @@ struct LycSlot {
   int32_t n_units;       // head_split_count
   int32_t q_row;         // first query/output row: b*Hq + g*G
   int32_t sel;           // selection output row (-1: none)
-  int32_t pad;
+  int32_t dep;           // layer whose selection wrote `list` (-1: none / already complete)
 };
 
 struct LycUnit {
@@ -39,15 +40,11 @@ struct LycUnit {
   int32_t hls;    // head-local split id
 };
 
-// Selection outputs written by the attention kernel for slots with sel >= 0.
+// Selection outputs written by the attention consumers for slots with sel >= 0.
 enum { SEL_NONE = 0, SEL_TOKEN_KEYS = 1, SEL_BLOCK_KEYS = 2 };
 
-struct LycAttnParams {
-  // 2D TMA views of the K and V caches: dim0 = d (elements), dim1 = all rows
-  // of all slabs; box = one 128-B column panel (bf16, 128B swizzle) or the
-  // whole row (fp32, no swizzle) x 64 rows.
-  CUtensorMap tmap_k;
-  CUtensorMap tmap_v;
+// Everything one layer's attention needs except the tensor maps.
+struct LycView {
   const void* k;            // [...][S_cap][d] (slot kv_off)
   const void* v;
   const void* q;            // [rows][d]
@@ -58,6 +55,7 @@ struct LycAttnParams {
   float* part_o;            // [n_units][G][d]  normalized partial outputs
   float* part_lse;          // [n_units][G]     base-2 log-sum-exp
   uint32_t* sel_keys;       // [n_sel][sel_stride]
+  uint32_t* hist1;          // optional [n_sel][LYC_BINS]: fused first radix pass
   uint32_t* exec_counts;    // optional [n_slots][counts_stride] per item
   int64_t sel_stride;
   int32_t counts_stride;
@@ -68,6 +66,15 @@ struct LycAttnParams {
   int32_t sel_mode;         // SEL_*
   float scale;              // softmax scale (1/sqrt(d))
   float scale_log2;         // scale * log2(e)
+};
+
+struct LycAttnParams {
+  // 2D TMA views of the K and V caches: dim0 = d (elements), dim1 = all rows
+  // of all slabs; box = one 128-B column panel (bf16, 128B swizzle) or the
+  // whole row (fp32, no swizzle) x 64 rows.
+  CUtensorMap tmap_k;
+  CUtensorMap tmap_v;
+  LycView v;
 };
 
 struct LycMergeTask {       // one (slot, q head j) pair needing a split-KV merge
@@ -98,4 +105,61 @@ struct LycTopkParams {
   int32_t* out_count;       // [cache rows] number of ids written (may be null)
   int32_t slice;            // keys per CTA of the cluster
   int32_t clear_keys;       // zero keys after use (block-max keys are atomicMax'ed)
+};
+
+// ---------------------------------------------------------------------------
+// Persistent decode-step kernel (step.cu): one launch runs every layer.
+struct LycLayerDesc {
+  const LycSlot* slots;
+  const LycUnit* units;
+  const int32_t* split_off;
+  const LycMergeTask* merges;
+  const int32_t* sel_rows;  // selection index -> index-cache row
+  int32_t n_merges;
+  int32_t n_sel;
+};
+
+// Per-layer device counters (monotonic; a step adds n_ctas to each).
+enum {
+  CTR_ATTN = 0,      // CTAs that finished the layer's attention units
+  CTR_MERGE = 1,     // CTAs that finished the layer's merge tasks (layer output final)
+  CTR_SEL0 = 2,      // selection phase barriers
+  CTR_SEL1 = 3,
+  CTR_SEL2 = 4,
+  CTR_SEL3 = 5,
+  CTR_SELDONE = 6,   // CTAs that finished writing the layer's index-cache rows
+  CTR_PER_LAYER = 8
+};
+
+struct LycStepParams {
+  CUtensorMap tmap_k;
+  CUtensorMap tmap_v;
+  const void* k;
+  const void* v;
+  const void* q;             // [n_layers][B][Hq][d]
+  void* out;                 // [n_layers][B][Hq][d]
+  int64_t q_layer_stride;    // elements between consecutive layers of q / out
+  const LycLayerDesc* layers;
+  float* part_o;
+  float* part_lse;
+  uint32_t* sel_keys;        // [2 parity][max_sel][sel_stride]
+  int64_t sel_stride;
+  uint32_t* hist;            // [2 parity][3 passes][max_sel][LYC_BINS]
+  uint32_t* team;            // [2 parity][max_sel][n_ctas][2]
+  uint32_t* ctr;             // [n_layers][CTR_PER_LAYER], then [epoch, exits]
+  int32_t* idx;              // index cache [B*H][idx_stride]
+  int64_t idx_stride;
+  int32_t* idx_count;        // [B*H]
+  int32_t n_layers;
+  int32_t max_sel;
+  int32_t n_keys;            // selection candidates per row (seq_len or n_blocks)
+  int32_t k_sel;             // ids kept per row (min(k, n_keys))
+  int32_t n_splits;
+  int32_t n_ctas;            // n_splits * batch
+  int32_t seq_len;
+  int32_t block_size;
+  int32_t group;
+  int32_t sel_mode;
+  float scale;
+  float scale_log2;
 };

@@ -191,6 +191,11 @@ class HybridDecoder:
     def layer_attn_bytes(self, layer: int, seq_len: int) -> int:
         return check(lib().lyc_decoder_layer_attn_bytes(self._h, layer, seq_len))
 
+    @property
+    def fused(self) -> bool:
+        """True when decode_step runs the persistent whole-step kernel."""
+        return bool(lib().lyc_decoder_is_fused(self._h))
+
     def set_timing(self, enable: bool = True):
         """CUDA events around every attention-kernel launch (graph-capturable)."""
         check(lib().lyc_decoder_set_timing(self._h, int(bool(enable))))

@@ -237,3 +237,73 @@ def test_decoder_errors():
         dec.decode_step(q, kv, kv, 129)  # beyond seq_cap
     with pytest.raises(P.LogicError):
         dec.replay()
+
+
+@pytest.mark.parametrize("select", ["tokens", "blocks"])
+def test_fused_step_matches_per_layer_kernels(orc, select):
+    """The persistent whole-step kernel (one launch: attention, merge and the
+    grid-wide radix selection of every layer) against the per-layer kernels
+    (attention + merge + cluster top-k launches) on the same inputs: identical
+    index sets, outputs equal up to merge-order rounding."""
+    import paper_2602_04541_b200 as P
+    NL, B, H, G, d, seq = 5, 2, 8, 4, 128, 6000
+    roles = roles_for(NL, H, [(1, 3), (2, 5), (3, 0), (4, 3)])
+    q, K, V = synth(17, NL, B, H, G, d, seq, 6016, torch.bfloat16)
+    q, K, V = q.cuda(), K.cuda(), V.cuda()
+    mk = lambda: P.HybridDecoder(n_layers=NL, batch=B, n_kv_heads=H, group_size=G, d_head=d,
+                                 seq_cap=6016, roles=roles, policy=P.SparsityPolicy.top_k(700),
+                                 select=select)
+    fused = mk()
+    assert fused.fused
+    out_f = fused.decode_step(q, K, V, seq)
+    per = mk()
+    out_p = torch.empty_like(q)
+    for l in range(NL):
+        per.layer(l, q[l], K, V, seq, out_p[l])
+    torch.cuda.synchronize()
+    sf, sp = fused.token_sets(), per.token_sets()
+    assert all(np.array_equal(a, b) for ra, rb in zip(sf, sp) for a, b in zip(ra, rb))
+    assert rel_err(out_f.float().cpu().numpy(), out_p.float().cpu().numpy()) < 1e-2
+
+
+def test_fused_step_llama_like_vs_oracle(orc):
+    """decode_step through the fused kernel vs the oracle decode loop."""
+    import paper_2602_04541_b200 as P
+    NL, B, H, G, d, seq = 4, 1, 8, 4, 128, 9000
+    roles = roles_for(NL, H, [(1, 1), (2, 6), (3, 1)])
+    dec, q, K, V, out, _ = run_case(orc, NL=NL, B=B, H=H, G=G, d=d, seq=seq, seq_cap=9024,
+                                    dtype=torch.bfloat16, roles=roles,
+                                    policy=P.SparsityPolicy.top_k(1000), seed=23)
+    assert dec.fused
+    r = orc.decode_step(q[:, 0], K[:, 0], V[:, 0], roles, seq=seq, scale=1 / np.sqrt(d), kind="topk",
+                        k=1000)
+    assert rel_err(out[:, 0], r["out"]) < BF16_TOL
+    sets = dec.token_sets()[0]
+    for g in range(H):
+        src = max(l for l in range(NL) if roles[l, g] == 0)
+        sc = pooled_scores(q[src, 0], K[src, 0, g], G, g, seq)
+        check_set(sets[g], r["sets"][g], sc, 1000)
+
+
+def test_fused_step_repeated_and_replanned(orc):
+    """Step counters are monotonic across launches and reset on re-plan: the
+    same step twice is bitwise identical; a different seq_len re-plans."""
+    import paper_2602_04541_b200 as P
+    NL, B, H, G, d = 3, 1, 4, 4, 64
+    roles = roles_for(NL, H, [(2, 1)])
+    q, K, V = synth(29, NL, B, H, G, d, 3000, 3072, torch.bfloat16)
+    q, K, V = q.cuda(), K.cuda(), V.cuda()
+    dec = P.HybridDecoder(n_layers=NL, batch=B, n_kv_heads=H, group_size=G, d_head=d, seq_cap=3072,
+                          roles=roles, policy=P.SparsityPolicy.top_k(200))
+    a = dec.decode_step(q, K, V, 3000).clone()
+    sa = dec.token_sets()
+    for _ in range(3):
+        b = dec.decode_step(q, K, V, 3000)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert all(np.array_equal(x, y) for rx, ry in zip(sa, dec.token_sets()) for x, y in zip(rx, ry))
+    c = dec.decode_step(q, K, V, 2999)
+    r = orc.decode_step(q[:, 0].float().cpu().numpy(), K[:, 0].float().cpu().numpy(),
+                        V[:, 0].float().cpu().numpy(), roles, seq=2999, scale=1 / np.sqrt(d),
+                        kind="topk", k=200)
+    assert rel_err(c[:, 0].float().cpu().numpy(), r["out"]) < BF16_TOL
