@@ -39,15 +39,26 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
                : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  const uint32_t addr = smem_u32(bar);
+__device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t phase) {
+  uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "LAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
-      "@!p bra LAB_WAIT;\n\t}" ::"r"(addr),
-      "r"(phase)
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(phase)
       : "memory");
+  return ok != 0;
+}
+
+// Waits for the given phase parity.  A wait that never completes is a bug
+// (e.g. a lost arrival); trap after ~20 s instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try_wait(addr, phase)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_wait(addr, phase))
+    if (clock64() - t0 > 40000000000LL) __trap();
 }
 
 // 1D bulk copy global -> shared through the TMA engine, completion counted

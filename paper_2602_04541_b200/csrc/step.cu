@@ -40,8 +40,15 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   return v;
 }
 
+// Grid-level wait on a monotonic counter; traps after ~20 s (a lost signal is
+// a bug -- fail the launch instead of hanging the GPU).
 __device__ __forceinline__ void spin_until(const uint32_t* ctr, uint32_t target) {
-  while ((int)(ld_acquire(ctr) - target) < 0) __nanosleep(40);
+  if ((int)(ld_acquire(ctr) - target) >= 0) return;
+  const long long t0 = clock64();
+  while ((int)(ld_acquire(ctr) - target) < 0) {
+    __nanosleep(40);
+    if (clock64() - t0 > 40000000000LL) __trap();
+  }
 }
 
 __device__ __forceinline__ void group_bar(int id, int n) {
