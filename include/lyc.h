@@ -175,6 +175,14 @@ int lyc_decoder_attn_ms(lyc_decoder* dec, float* ms);
  * lyc_decoder_attn_ms reports the step kernel's duration in ms[0]. */
 int lyc_decoder_is_fused(lyc_decoder* dec);
 
+/* Step timeline (fused mode): when enabled, the step kernel stamps
+ * %globaltimer (ns) for 8 events per layer per CTA: consumers begin / end,
+ * epilogue sees the layer's attention done, merge done, selection barriers
+ * 0-2, selection done.  lyc_decoder_trace copies [n_layers][8][n_ctas]
+ * stamps into out (cap entries) and returns the count (out = NULL: size query). */
+int lyc_decoder_set_trace(lyc_decoder* dec, int enable);
+int64_t lyc_decoder_trace(lyc_decoder* dec, unsigned long long* out, int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

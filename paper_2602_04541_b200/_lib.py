@@ -22,7 +22,7 @@ SYMBOLS = [
     "lyc_decoder_destroy", "lyc_decoder_step", "lyc_decoder_layer", "lyc_decoder_capture",
     "lyc_decoder_replay", "lyc_decoder_index_cache", "lyc_decoder_launches_per_step",
     "lyc_decoder_step_bytes", "lyc_decoder_layer_attn_bytes", "lyc_decoder_set_timing",
-    "lyc_decoder_attn_ms", "lyc_decoder_is_fused",
+    "lyc_decoder_attn_ms", "lyc_decoder_is_fused", "lyc_decoder_set_trace", "lyc_decoder_trace",
 ]
 
 
@@ -118,6 +118,10 @@ def lib() -> C.CDLL:
     L.lyc_decoder_attn_ms.argtypes = [vp, vp]
     L.lyc_decoder_is_fused.restype = C.c_int
     L.lyc_decoder_is_fused.argtypes = [vp]
+    L.lyc_decoder_set_trace.restype = C.c_int
+    L.lyc_decoder_set_trace.argtypes = [vp, C.c_int]
+    L.lyc_decoder_trace.restype = i64
+    L.lyc_decoder_trace.argtypes = [vp, vp, i64]
     _lib = L
     return L
 

@@ -52,7 +52,8 @@ struct AttnCfg {
   static constexpr int kQBytes = kE == 4 ? (kMaxG + 1) * D * 4 : 0;
   static constexpr int kMaxSmem = 232448 - 1024;   // 227 KB opt-in minus alignment slack
   static constexpr int kExtraBytes = 4096;         // scratch of the step kernel's epilogue warps
-  static constexpr int kFixed = kMergeBytes + kQBytes + 512 + kExtraBytes;
+  static constexpr int kHistBytes = LYC_BINS * 4;  // per-CTA first-pass selection histogram
+  static constexpr int kFixed = kMergeBytes + kQBytes + 512 + kExtraBytes + kHistBytes;
   static constexpr int kStagesRaw = (kMaxSmem - kFixed) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kSmem = kStages * kStageBytes + kFixed + 1024;
@@ -78,6 +79,7 @@ struct AttnSmem {
   uint64_t* full;
   uint64_t* empty;
   uint8_t* extra;  // kExtraBytes scratch for other warp roles
+  uint32_t* hist;  // [LYC_BINS] first radix pass of the unit's selection keys (zero between units)
 
   __device__ __forceinline__ static AttnSmem carve(uint8_t* raw) {
     using C = AttnCfg<T, D>;
@@ -91,6 +93,7 @@ struct AttnSmem {
     s.full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(s.qs) + C::kQBytes);
     s.empty = s.full + C::kStages;
     s.extra = reinterpret_cast<uint8_t*>(s.empty + C::kStages);
+    s.hist = reinterpret_cast<uint32_t*>(s.extra + C::kExtraBytes);
     return s;
   }
 };
@@ -146,17 +149,38 @@ __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMa
   const char* vbase = static_cast<const char*>(p.v);
   const int my_c = pt % CPR;
   const int my_r0 = pt / CPR;
+  // Row indices (gathered tiles) and block ids (block lists) of the NEXT tile
+  // are loaded while the current tile is issued: one L2 round trip per unit
+  // instead of one per tile.
+  auto load_rows = [&](const Tile& t, int* rows) {
+    if (t.ids == nullptr && t.nvalid == LYC_TILE) return;
+#pragma unroll
+    for (int i = 0; i < kRounds; ++i) {
+      const int r = my_r0 + i * kRowsPerRound;
+      rows[i] = r < t.nvalid ? (t.ids ? __ldcg(t.ids + r) : t.lo + r) : -1;
+    }
+  };
   for (int u = ub; u < ue; ++u) {
     const LycUnit un = p.units[u];
     const LycSlot s = p.slots[un.slot];
     waits.unit(s);
     const int tpi = tiles_per_item(s, p.block_size);
     const int row0 = (int)(s.kv_off / D);  // tensor-map row of the slab's row 0
-    for (int it = un.begin; it < un.end; ++it) {
-      if (p.exec_counts && pt == 0)
+    const int nt = (un.end - un.begin) * tpi;
+    Tile t = tile_of(s, un.begin, 0, p.seq_len, p.block_size);
+    int rows[kRounds];
+    load_rows(t, rows);
+    for (int f = 0; f < nt; ++f) {
+      const int it = un.begin + f / tpi, sub = f % tpi;
+      if (p.exec_counts && pt == 0 && sub == 0)
         atomicAdd(p.exec_counts + (int64_t)un.slot * p.counts_stride + it, 1u);
-      for (int sub = 0; sub < tpi; ++sub) {
-        const Tile t = tile_of(s, it, sub, p.seq_len, p.block_size);
+      Tile tn = t;
+      int rows_n[kRounds];
+      if (f + 1 < nt) {
+        tn = tile_of(s, un.begin + (f + 1) / tpi, (f + 1) % tpi, p.seq_len, p.block_size);
+        load_rows(tn, rows_n);
+      }
+      {
         if (it == s.n_items - 1 && sub == tpi - 1) waits.last_tile();
         uint8_t* kd = ring + stage * C::kStageBytes;
         uint8_t* vd = kd + C::kTileBytes;
@@ -181,12 +205,6 @@ __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMa
           }
         } else {
           // gathered / ragged tile: coalesced 16-B cp.async, masked rows zero-filled
-          int rows[kRounds];
-#pragma unroll
-          for (int i = 0; i < kRounds; ++i) {
-            const int r = my_r0 + i * kRowsPerRound;
-            rows[i] = r < t.nvalid ? (t.ids ? __ldcg(t.ids + r) : t.lo + r) : -1;
-          }
           mbar_wait(&empty[stage], phase ^ 1);
 #pragma unroll
           for (int i = 0; i < kRounds; ++i) {
@@ -204,6 +222,9 @@ __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMa
           phase ^= 1;
         }
       }
+      t = tn;
+#pragma unroll
+      for (int i = 0; i < kRounds; ++i) rows[i] = rows_n[i];
     }
   }
 }
@@ -231,7 +252,8 @@ __device__ __forceinline__ void store_out<__nv_bfloat16>(__nv_bfloat16* dst, flo
 // Merge the consumer warps' (m, l, o) for one unit and emit partial / output.
 template <typename T, int D>
 __device__ __forceinline__ void unit_epilogue(const LycView& p, const LycSlot& s, int u,
-                                              float* mo, float* ml, int tid) {
+                                              float* mo, float* ml, int tid, uint32_t* hist_s,
+                                              uint32_t* hist_g) {
   const int G = p.group;
   consumer_bar();
   const bool direct = s.n_units == 1;
@@ -254,6 +276,15 @@ __device__ __forceinline__ void unit_epilogue(const LycView& p, const LycSlot& s
     } else {
       p.part_o[((int64_t)u * G + j) * D + d] = o;
       if (d == 0) p.part_lse[(int64_t)u * G + j] = log2f(L) + M;
+    }
+  }
+  if (hist_g) {  // flush the unit's first-pass histogram (few non-zero bins) and re-zero it
+    for (int b = tid; b < LYC_BINS; b += kConsumerWarps * 32) {
+      const uint32_t c = hist_s[b];
+      if (c) {
+        atomicAdd(hist_g + b, c);
+        hist_s[b] = 0u;
+      }
     }
   }
   consumer_bar();
@@ -349,8 +380,10 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
                   const int r = t0 + n * 8 + qc + e;
                   const bool ok = r < t.nvalid;
                   const uint32_t key = float_key(ps[n][e]);
-                  if (ok) dst[r] = key;
-                  if (hist) hist_add(hist, key >> 21, ok, 0xFu, lane);
+                  if (ok) {
+                    dst[r] = key;
+                    if (hist) atomicAdd(sm.hist + (key >> 21), 1u);
+                  }
                 }
             }
           } else {  // SEL_BLOCK_KEYS: max over valid rows of this block
@@ -424,7 +457,8 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
         *reinterpret_cast<float2*>(&sm.mo[(warp * kMaxG + qr) * D + n * 8 + qc]) =
             make_float2(o[n][0], o[n][1]);
     }
-    unit_epilogue<__nv_bfloat16, D>(p, s, s.first_unit + un.hls, sm.mo, sm.ml, warp * 32 + lane);
+    unit_epilogue<__nv_bfloat16, D>(p, s, s.first_unit + un.hls, sm.mo, sm.ml, warp * 32 + lane,
+                                    sm.hist, hist);
   }
 }
 
@@ -498,8 +532,10 @@ __device__ __forceinline__ void consume_units_f32(const LycView& p, const AttnSm
           if (p.sel_mode == SEL_TOKEN_KEYS) {
             if (half == 0) {
               const uint32_t key = float_key(pooled);
-              if (valid) p.sel_keys[(int64_t)s.sel * p.sel_stride + t.lo + t0 + tr] = key;
-              if (hist) hist_add(hist, key >> 21, valid, 0xFFFFu, lane);
+              if (valid) {
+                p.sel_keys[(int64_t)s.sel * p.sel_stride + t.lo + t0 + tr] = key;
+                if (hist) atomicAdd(sm.hist + (key >> 21), 1u);
+              }
             }
           } else {
             uint32_t km = (half == 0 && valid) ? float_key(pooled) : 0u;
@@ -561,7 +597,8 @@ __device__ __forceinline__ void consume_units_f32(const LycView& p, const AttnSm
       for (int c = 0; c < DC; ++c)
         if (c * 32 + lane < D) sm.mo[(warp * kMaxG + j) * D + c * 32 + lane] = o[j][c];
     }
-    unit_epilogue<float, D>(p, s, s.first_unit + un.hls, sm.mo, sm.ml, warp * 32 + lane);
+    unit_epilogue<float, D>(p, s, s.first_unit + un.hls, sm.mo, sm.ml, warp * 32 + lane, sm.hist,
+                            hist);
   }
 }
 

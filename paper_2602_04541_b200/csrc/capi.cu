@@ -25,8 +25,9 @@ cudaError_t launch_topk(const LycTopkParams& p, int rows, int cluster, cudaStrea
 int topk_cluster_size(int n, int max_slice);
 size_t topk_smem_bytes(int slice);
 cudaError_t launch_float_keys(const float* s, uint32_t* keys, int64_t n, cudaStream_t st);
-cudaError_t launch_step(const LycStepParams& p, int dtype, int d, int batch, cudaStream_t st);
+cudaError_t launch_step(const LycStepParams& p, int dtype, int d, cudaStream_t st);
 bool step_supported(int dtype, int d);
+int step_select_capacity(int dtype, int d);
 }  // namespace lyc
 
 namespace {
@@ -459,9 +460,10 @@ struct lyc_decoder {
   int32_t* idx_count = nullptr;
   uint32_t* sel_keys = nullptr; // [2][B*H][sel_stride]
   int64_t sel_stride = 0;
-  uint32_t* hist = nullptr;     // [2][3][B*H][LYC_BINS]
-  uint32_t* team = nullptr;     // [2][B*H][n_ctas][2]
+  uint32_t* hist = nullptr;     // [2][B*H][LYC_BINS] fused first-pass histograms
+  int n_sel_ctas = 0;           // fused mode: selection CTAs (4-CTA clusters)
   uint32_t* ctr = nullptr;      // [NL][CTR_PER_LAYER] + 2
+  unsigned long long* trace = nullptr;  // optional step timeline [NL][8][n_ctas]
   float* part_o = nullptr;
   float* part_lse = nullptr;
   size_t part_units = 0;
@@ -585,6 +587,15 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
   if (seq > d->cfg.seq_cap) fail(LYC_EINVAL, "decode_step: seq_len exceeds seq_cap");
   if (!d->fused && seq > (int64_t)16 * 32768 && d->cfg.select_mode == LYC_SELECT_TOKENS)
     fail(LYC_ENOTSUP, "decode_step: token-mode selection supports seq_len <= 524288");
+  if (d->fused && d->n_sel_ctas > 0) {
+    // a selection cluster keeps a row's keys in shared memory
+    const int64_t nk = d->cfg.select_mode == LYC_SELECT_BLOCKS ? (seq + d->bs - 1) / d->bs : seq;
+    if (nk > 4LL * lyc::step_select_capacity(d->cfg.dtype, d->D)) {
+      d->fused = false;
+      d->n_sel_ctas = 0;
+      d->planned_seq = -1;
+    }
+  }
   if (d->planned_seq == seq) return;
   const int B = d->B, H = d->H, G = d->G, D = d->D;
   const int64_t kb = d->budget(seq);
@@ -714,7 +725,7 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
   cuda_check(cudaMemcpy(d->blob, d->staging.data(), total, cudaMemcpyHostToDevice), "H2D plan");
   // a new plan restarts the step counters (any previous step has completed:
   // the synchronous copy above serialises with the legacy stream)
-  cuda_check(cudaMemset(d->ctr, 0, ((size_t)d->NL * CTR_PER_LAYER + 2) * 4), "memset counters");
+  cuda_check(cudaMemset(d->ctr, 0, LYC_CTR_WORDS(d->NL) * 4), "memset counters");
   cuda_check(cudaDeviceSynchronize(), "sync");
   d->planned_seq = seq;
 }
@@ -786,17 +797,18 @@ void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, i
   p.sel_keys = d->sel_keys;
   p.sel_stride = d->sel_stride;
   p.hist = d->hist;
-  p.team = d->team;
   p.ctr = d->ctr;
   p.idx = d->idx;
   p.idx_stride = d->k_cap;
   p.idx_count = d->idx_count;
+  p.trace = d->trace;
   p.n_layers = d->NL;
   p.max_sel = d->B * d->H;
   p.n_keys = (int32_t)d->n_keys;
   p.k_sel = (int32_t)d->k_sel;
   p.n_splits = d->S;
   p.n_ctas = d->n_ctas();
+  p.n_sel_ctas = d->n_sel_ctas;
   p.seq_len = (int32_t)seq;
   p.block_size = d->bs;
   p.group = d->G;
@@ -806,7 +818,7 @@ void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, i
   p.scale = d->cfg.scale;
   p.scale_log2 = d->cfg.scale * 1.4426950408889634f;
   record(d, d->ev_pre, 0, st);
-  cuda_check(lyc::launch_step(p, d->cfg.dtype, d->D, d->B, st), "step launch");
+  cuda_check(lyc::launch_step(p, d->cfg.dtype, d->D, st), "step launch");
   record(d, d->ev_post, 0, st);
   ++g_launches;
 }
@@ -856,10 +868,23 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
     d->NL = c.n_layers;
     d->bs = 64;
     const int sms = num_sms();
-    d->S = c.num_splits > 0 ? c.num_splits : std::max(1, sms / d->B);
-    // the persistent step kernel needs every CTA co-resident (1 CTA per SM)
-    d->fused = lyc::step_supported(c.dtype, c.d_head) && d->S * d->B <= sms &&
-               (int64_t)d->B * d->H <= 252 && std::getenv("LYC_NO_FUSED_STEP") == nullptr;
+    // The persistent step kernel needs every CTA co-resident (1 CTA per SM):
+    // n_attn = S*B attention CTAs (a multiple of the 4-CTA cluster) plus two
+    // 4-CTA selection clusters when the decoder selects.
+    d->fused = lyc::step_supported(c.dtype, c.d_head) && std::getenv("LYC_NO_FUSED_STEP") == nullptr;
+    d->n_sel_ctas = d->fused && c.select_mode != LYC_SELECT_NONE ? 8 : 0;
+    if (c.num_splits > 0) {
+      d->S = c.num_splits;
+    } else if (d->fused) {
+      d->S = std::max(1, (sms - d->n_sel_ctas) / d->B);
+      while (d->S > 1 && (d->S * d->B) % 4) --d->S;
+    } else {
+      d->S = std::max(1, sms / d->B);
+    }
+    if (d->fused && ((d->S * d->B) % 4 != 0 || d->S * d->B + d->n_sel_ctas > sms)) {
+      d->fused = false;
+      d->n_sel_ctas = 0;
+    }
     const int64_t nb_cap = (c.seq_cap + d->bs - 1) / d->bs;
     if (c.select_mode == LYC_SELECT_BLOCKS) {
       d->k_cap = c.policy_kind == LYC_POLICY_RATIO ? nb_cap
@@ -877,11 +902,10 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
       cuda_check(cudaMemset(d->idx_count, 0, rows * 4), "memset");
       cuda_check(cudaMalloc(&d->sel_keys, 2 * rows * d->sel_stride * 4), "cudaMalloc keys");
       cuda_check(cudaMemset(d->sel_keys, 0, 2 * rows * d->sel_stride * 4), "memset");
-      cuda_check(cudaMalloc(&d->hist, 2 * 3 * rows * LYC_BINS * 4), "cudaMalloc hist");
-      cuda_check(cudaMemset(d->hist, 0, 2 * 3 * rows * LYC_BINS * 4), "memset");
-      cuda_check(cudaMalloc(&d->team, 2 * rows * (size_t)d->n_ctas() * 2 * 4), "cudaMalloc team");
-      cuda_check(cudaMalloc(&d->ctr, ((size_t)d->NL * CTR_PER_LAYER + 2) * 4), "cudaMalloc ctr");
-      cuda_check(cudaMemset(d->ctr, 0, ((size_t)d->NL * CTR_PER_LAYER + 2) * 4), "memset");
+      cuda_check(cudaMalloc(&d->hist, 2 * rows * LYC_BINS * 4), "cudaMalloc hist");
+      cuda_check(cudaMemset(d->hist, 0, 2 * rows * LYC_BINS * 4), "memset");
+      cuda_check(cudaMalloc(&d->ctr, LYC_CTR_WORDS(d->NL) * 4), "cudaMalloc ctr");
+      cuda_check(cudaMemset(d->ctr, 0, LYC_CTR_WORDS(d->NL) * 4), "memset");
     } catch (...) {
       lyc_decoder_destroy(d);
       throw;
@@ -901,8 +925,8 @@ int lyc_decoder_destroy(lyc_decoder* d) {
   free_dev(d->idx_count);
   free_dev(d->sel_keys);
   free_dev(d->hist);
-  free_dev(d->team);
   free_dev(d->ctr);
+  free_dev(d->trace);
   free_dev(d->part_o);
   free_dev(d->part_lse);
   free_dev(d->blob);
@@ -1053,5 +1077,32 @@ int lyc_decoder_attn_ms(lyc_decoder* d, float* ms) {
 }
 
 int lyc_decoder_is_fused(lyc_decoder* d) { return d && d->fused ? 1 : 0; }
+
+int lyc_decoder_set_trace(lyc_decoder* d, int enable) {
+  return (int)guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    if (enable && !d->trace) {
+      cuda_check(cudaMalloc(&d->trace, (size_t)d->NL * 8 * d->n_ctas() * 8), "cudaMalloc trace");
+      cuda_check(cudaMemset(d->trace, 0, (size_t)d->NL * 8 * d->n_ctas() * 8), "memset trace");
+    }
+    if (!enable) {
+      free_dev(d->trace);
+      d->trace = nullptr;
+    }
+    return LYC_OK;
+  });
+}
+
+int64_t lyc_decoder_trace(lyc_decoder* d, unsigned long long* out, int64_t cap) {
+  return guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    if (!d->trace) fail(LYC_ESTATE, "decoder: tracing is off");
+    const int64_t n = (int64_t)d->NL * 8 * d->n_ctas();
+    if (!out) return n;  // size query
+    if (cap < n) fail(LYC_EINVAL, "decoder: trace buffer too small");
+    cuda_check(cudaMemcpy(out, d->trace, (size_t)n * 8, cudaMemcpyDeviceToHost), "D2H trace");
+    return n;
+  });
+}
 
 }  // extern "C"

@@ -130,6 +130,10 @@ enum {
   CTR_SELDONE = 6,   // CTAs that finished writing the layer's index-cache rows
   CTR_PER_LAYER = 8
 };
+// Counters sit 256 B apart (separate L2 lines / slices): many CTAs poll them.
+#define LYC_CTR_STRIDE 64
+#define LYC_CTR(base, l, e) ((base) + ((size_t)(l) * CTR_PER_LAYER + (e)) * LYC_CTR_STRIDE)
+#define LYC_CTR_WORDS(n_layers) (((size_t)(n_layers) * CTR_PER_LAYER + 2) * LYC_CTR_STRIDE)
 
 struct LycStepParams {
   CUtensorMap tmap_k;
@@ -144,18 +148,19 @@ struct LycStepParams {
   float* part_lse;
   uint32_t* sel_keys;        // [2 parity][max_sel][sel_stride]
   int64_t sel_stride;
-  uint32_t* hist;            // [2 parity][3 passes][max_sel][LYC_BINS]
-  uint32_t* team;            // [2 parity][max_sel][n_ctas][2]
-  uint32_t* ctr;             // [n_layers][CTR_PER_LAYER], then [epoch, exits]
+  uint32_t* hist;            // [2 parity][max_sel][LYC_BINS] fused first-pass histograms
+  uint32_t* ctr;             // LYC_CTR counters: [n_layers][CTR_PER_LAYER], then epoch, exits
   int32_t* idx;              // index cache [B*H][idx_stride]
   int64_t idx_stride;
   int32_t* idx_count;        // [B*H]
+  unsigned long long* trace; // optional [n_layers][8 events][n_ctas] %globaltimer stamps
   int32_t n_layers;
   int32_t max_sel;
   int32_t n_keys;            // selection candidates per row (seq_len or n_blocks)
   int32_t k_sel;             // ids kept per row (min(k, n_keys))
   int32_t n_splits;
-  int32_t n_ctas;            // n_splits * batch
+  int32_t n_ctas;            // attention CTAs = n_splits * batch (grid index 0..n_ctas-1)
+  int32_t n_sel_ctas;        // selection CTAs after them (4-CTA clusters)
   int32_t seq_len;
   int32_t block_size;
   int32_t group;

@@ -1,38 +1,44 @@
 // step.cu -- the persistent decode-step kernel: every layer of one decode step
 // (decode_engine.hpp:109-151) in ONE launch, one CTA per SM.
 //
-// Warp roles per CTA (256 threads):
-//   0-3 consumers  attention of this CTA's split of layer l (attn_core.cuh);
-//                  layer l+1 starts only after layer l's outputs are final
-//                  (device counter), emulating the model's layer dependency.
-//   4-5 producers  stream the K/V tiles of layer l, l+1, ... continuously
-//                  through the smem ring: the next layer's history rows are in
-//                  flight while layer l is still being merged.  Tiles whose
-//                  index list comes from a selection wait for that selection;
-//                  the tile holding the current token waits for the previous
-//                  layer (its K/V row is produced after it).
-//   6-7 epilogue   after the whole grid finishes layer l's attention:
-//                  (a) the split-KV LSE merge (kernel_sim.hpp:205-225), work
-//                      spread over every CTA;
-//                  (b) exact top-k selection for the layer's retrieval heads
-//                      (args_top_k, attention.hpp:108-123: largest k, ties to
-//                      the lower index, ascending) as a grid-wide radix select:
-//                      the consumers already built the first 11-bit histogram
-//                      while scoring; three more passes over each CTA's key
-//                      slice, separated by grid barriers, fix the k-th key T
-//                      exactly; an ordered compaction writes the index cache.
-//                  Selection runs concurrently with the next layer's attention
-//                  (Algorithm 2's workload pooling applied to selection).
+// The grid is 1-D with 4-CTA clusters.  The first n_attn CTAs are ATTENTION
+// CTAs (256 threads):
+//   warps 0-3 consumers  attention of this CTA's split of layer l
+//                        (attn_core.cuh); layer l+1 starts only after layer
+//                        l's outputs are final (device counter) -- the model's
+//                        layer dependency;
+//   warps 4-5 producers  stream the K/V tiles of layer l, l+1, ... continuously
+//                        through the smem ring: the next layer's history rows
+//                        are in flight while layer l is being merged.  Tiles
+//                        whose index list comes from a selection wait for it;
+//                        the tile holding the current token waits for the
+//                        previous layer (its K/V row is produced after it);
+//   warps 6-7 epilogue   the split-KV LSE merge of layer l (kernel_sim.hpp:
+//                        205-225), spread over every attention CTA.
+// The last n_sel clusters are SELECTION clusters (Algorithm 2's pooling
+// applied to the selection): after layer l's attention they compute, for each
+// of its retrieval heads, args_top_k over the pooled-query keys
+// (attention.hpp:108-123: the k largest, ties to the lower index, ascending)
+// as an exact radix select: the consumers already produced the first 11-bit
+// histogram while scoring; each CTA of the cluster holds a quarter of the
+// keys in shared memory, two more passes reduce their histograms through
+// DSMEM, and an ordered compaction writes the index cache.  Selection runs
+// concurrently with the next layer's attention.
 // Grid-wide coordination uses monotonic per-layer counters in global memory
-// (a step adds n_ctas to each); the launch is cooperative so every CTA is
-// co-resident.
+// (a step adds the number of participating CTAs); every CTA is co-resident
+// (cooperative launch, one CTA per SM).
+#include <cooperative_groups.h>
+
 #include "attn_core.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace lyc {
 
 constexpr int kEpiWarps = 2;
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kStepThreads = (kConsumerWarps + kProducerWarps + kEpiWarps) * 32;
+constexpr int kSelCluster = 4;
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
@@ -46,7 +52,7 @@ __device__ __forceinline__ void spin_until(const uint32_t* ctr, uint32_t target)
   if ((int)(ld_acquire(ctr) - target) >= 0) return;
   const long long t0 = clock64();
   while ((int)(ld_acquire(ctr) - target) < 0) {
-    __nanosleep(40);
+    __nanosleep(128);
     if (clock64() - t0 > 40000000000LL) __trap();
   }
 }
@@ -61,20 +67,30 @@ __device__ __forceinline__ void signal(uint32_t* ctr) {
   atomicAdd(ctr, 1u);
 }
 
+// Debug timeline: %globaltimer (ns) of event ev of layer l on this CTA.
+enum { EV_CONS_BEGIN = 0, EV_CONS_END, EV_EPI_ATTN, EV_MERGE, EV_SEL0, EV_SEL1, EV_SEL2, EV_SELDONE };
+__device__ __forceinline__ void stamp(const LycStepParams& p, int l, int ev, int cta) {
+  if (p.trace) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[((size_t)l * 8 + ev) * p.n_ctas + cta] = t;
+  }
+}
+
 struct StepWaits {
   const uint32_t* ctr;
-  uint32_t target;
+  uint32_t t_attn, t_sel;
   int layer;
   int pt;
-  __device__ __forceinline__ void wait(const uint32_t* c) const {
+  __device__ __forceinline__ void wait(const uint32_t* c, uint32_t target) const {
     if (pt == 0) spin_until(c, target);
     group_bar(3, kProducerThreads);
   }
   __device__ __forceinline__ void unit(const LycSlot& s) const {
-    if (s.dep >= 0) wait(ctr + s.dep * CTR_PER_LAYER + CTR_SELDONE);
+    if (s.dep >= 0) wait(LYC_CTR(ctr, s.dep, CTR_SELDONE), t_sel);
   }
   __device__ __forceinline__ void last_tile() const {
-    if (layer > 0) wait(ctr + (layer - 1) * CTR_PER_LAYER + CTR_MERGE);
+    if (layer > 0) wait(LYC_CTR(ctr, layer - 1, CTR_MERGE), t_attn);
   }
 };
 
@@ -91,9 +107,8 @@ __device__ __forceinline__ LycView layer_view(const LycStepParams& p, const LycL
   v.part_o = p.part_o;
   v.part_lse = p.part_lse;
   v.sel_keys = p.sel_keys + (int64_t)(l & 1) * p.max_sel * p.sel_stride;
-  v.hist1 = p.sel_mode == SEL_TOKEN_KEYS
-                ? p.hist + (int64_t)((l & 1) * 3) * p.max_sel * LYC_BINS
-                : nullptr;
+  v.hist1 = p.sel_mode == SEL_TOKEN_KEYS ? p.hist + (int64_t)(l & 1) * p.max_sel * LYC_BINS
+                                         : nullptr;
   v.exec_counts = nullptr;
   v.sel_stride = p.sel_stride;
   v.counts_stride = 0;
@@ -108,8 +123,8 @@ __device__ __forceinline__ LycView layer_view(const LycStepParams& p, const LycL
 }
 
 // ---------------------------------------------------------------- selection
-// Warp-level search of a 2048-bin histogram (from the top bin down) for the
-// bin holding the krem-th largest candidate.  Returns (digit, count above).
+// Warp-level search of a histogram (from the top bin down) for the bin that
+// holds the krem-th largest candidate.  Returns (digit, count above it).
 __device__ __forceinline__ void find_digit(const uint32_t* h, int nbins, uint32_t krem,
                                            uint32_t& digit, uint32_t& above, int lane) {
   const int per = nbins / 32;  // 64 (11-bit) or 32 (10-bit) bins per lane
@@ -120,7 +135,7 @@ __device__ __forceinline__ void find_digit(const uint32_t* h, int nbins, uint32_
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
     if (q * 4 >= per) break;
-    const uint4 v = __ldcg(src + q);
+    const uint4 v = src[q];
     cnt[4 * q] = v.x;
     cnt[4 * q + 1] = v.y;
     cnt[4 * q + 2] = v.z;
@@ -153,214 +168,182 @@ __device__ __forceinline__ void find_digit(const uint32_t* h, int nbins, uint32_
   above = __shfl_sync(0xffffffffu, a, src_lane);
 }
 
-struct SelScratch {      // per selection row, in the epilogue smem scratch
-  uint32_t prefix;       // key bits fixed so far
-  uint32_t krem;         // candidates still to take among keys matching prefix
-  uint32_t take_eq;      // phase E: ties this CTA takes
-  uint32_t out_base;     // phase E: output offset of this CTA
+// Shared memory of a selection CTA (carved from the same dynamic allocation).
+struct SelSmem {
+  uint32_t hist[2][LYC_BINS];  // local pass histograms (double-buffered for DSMEM readers)
+  uint32_t ghist[LYC_BINS];    // cluster-summed histogram
+  uint32_t warp_tot[32];
+  uint32_t counts[2];          // this CTA's (count > T, count == T)
+  uint32_t digit, above;
+  uint32_t keys[1];            // slice of the row's keys (capacity p.sel_cap)
 };
 
-__device__ __forceinline__ void grid_barrier_epi(uint32_t* ctr, uint32_t target, int et) {
-  group_bar(2, kEpiThreads);
-  if (et == 0) {
-    signal(ctr);
-    spin_until(ctr, target);
+// Block-wide inclusive scan (256 threads).
+__device__ __forceinline__ uint32_t block_scan(uint32_t v, uint32_t* warp_tot, uint32_t& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kWarps = kStepThreads / 32;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t n = __shfl_up_sync(0xffffffffu, v, off);
+    if (lane >= off) v += n;
   }
-  group_bar(2, kEpiThreads);
+  if (lane == 31) warp_tot[warp] = v;
+  __syncthreads();
+  uint32_t before = 0;
+  total = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    const uint32_t t = warp_tot[w];
+    before += w < warp ? t : 0u;
+    total += t;
+  }
+  __syncthreads();
+  return v + before;
 }
 
-template <typename T, int D>
-__device__ void select_layer(const LycStepParams& p, const LycLayerDesc& L, int l, int cta,
-                             uint32_t target, int et, SelScratch* ss, uint32_t* scan) {
-  const int lane = et & 31, w = et >> 5;
-  const int n = p.n_keys;
-  const int lo = (int)((int64_t)cta * n / p.n_ctas);
-  const int hi = (int)((int64_t)(cta + 1) * n / p.n_ctas);
-  uint32_t* lc = p.ctr + l * CTR_PER_LAYER;
-  auto keys_of = [&](int r) {
-    return p.sel_keys + ((int64_t)(l & 1) * p.max_sel + r) * p.sel_stride;
-  };
-  auto hist_of = [&](int r, int pass) {
-    return p.hist + ((int64_t)((l & 1) * 3 + pass) * p.max_sel + r) * LYC_BINS;
-  };
-  const int nsel = L.n_sel;
+// Sum the cluster's pass histograms into ghist and locate the digit.
+__device__ __forceinline__ void cluster_digit(cg::cluster_group& cl, SelSmem& sh, int buf,
+                                              int nbins, uint32_t krem) {
+  cl.sync();  // every CTA's local histogram is complete
+  const int C = (int)cl.num_blocks();
+  for (int b = threadIdx.x; b < nbins; b += kStepThreads) {
+    uint32_t s = 0;
+    for (int c = 0; c < C; ++c) s += cl.map_shared_rank(&sh.hist[buf][0], c)[b];
+    sh.ghist[b] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t d, a;
+    find_digit(sh.ghist, nbins, krem, d, a, threadIdx.x);
+    if (threadIdx.x == 0) {
+      sh.digit = d;
+      sh.above = a;
+    }
+  }
+  __syncthreads();
+}
 
-  if (p.sel_mode == SEL_BLOCK_KEYS) {
-    // block keys were max-folded by atomics: build the first-pass histogram here
-    for (int r = 0; r < nsel; ++r) {
-      const uint32_t* kr = keys_of(r);
-      uint32_t* h = hist_of(r, 0);
-      for (int i0 = lo; i0 < hi; i0 += kEpiThreads) {
-        const int i = i0 + et;
-        const bool ok = i < hi;
-        const uint32_t key = ok ? __ldcg(kr + i) : 0u;
-        hist_add(h, key >> 21, ok, 0xffffffffu, lane);
+// One row: the k largest of n keys (ties to the lower index), ascending,
+// into out[0..k).  h1 (token mode) holds the grid-wide first-pass histogram.
+__device__ void select_row(cg::cluster_group& cl, SelSmem& sh, const LycStepParams& p,
+                           uint32_t* keys_g, const uint32_t* h1, int32_t* out) {
+  const int tid = threadIdx.x;
+  const int C = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  const int n = p.n_keys;
+  const int slice = ((n + C - 1) / C + 3) & ~3;
+  const int lo = min(n, rank * slice);
+  const int cnt = max(0, min(slice, n - lo));
+  // load this CTA's slice (block-mode keys are reset for the next use)
+  for (int i = tid; i < cnt; i += kStepThreads) {
+    sh.keys[i] = __ldcg(keys_g + lo + i);
+    if (p.sel_mode == SEL_BLOCK_KEYS) keys_g[lo + i] = 0u;
+  }
+  uint32_t krem = (uint32_t)p.k_sel;
+  // ---- pass 1 (bits 31..21)
+  for (int b = tid; b < LYC_BINS; b += kStepThreads) sh.hist[0][b] = 0u;
+  __syncthreads();
+  uint32_t d1, a1;
+  if (h1) {
+    for (int b = tid; b < LYC_BINS; b += kStepThreads) sh.ghist[b] = __ldcg(h1 + b);
+    __syncthreads();
+    if (tid < 32) {
+      uint32_t d, a;
+      find_digit(sh.ghist, LYC_BINS, krem, d, a, tid);
+      if (tid == 0) {
+        sh.digit = d;
+        sh.above = a;
       }
     }
-    grid_barrier_epi(lc + CTR_SEL3, target, et);
+    __syncthreads();
+    cl.sync();  // every CTA read h1 before it is reset below
+  } else {
+    for (int i = tid; i < cnt; i += kStepThreads) atomicAdd(&sh.hist[0][sh.keys[i] >> 21], 1u);
+    __syncthreads();
+    cluster_digit(cl, sh, 0, LYC_BINS, krem);
   }
-  // ---- pass 1 digit (bits 31..21) from the fused histogram; pass 2 histogram
-  for (int r = w; r < nsel; r += kEpiWarps) {
-    uint32_t d, a;
-    find_digit(hist_of(r, 0), 2048, (uint32_t)p.k_sel, d, a, lane);
-    if (lane == 0) {
-      ss[r].prefix = d << 21;
-      ss[r].krem = (uint32_t)p.k_sel - a;
-    }
+  d1 = sh.digit;
+  a1 = sh.above;
+  krem -= a1;
+  // ---- pass 2 (bits 20..10) among keys with top bits == d1
+  for (int b = tid; b < LYC_BINS; b += kStepThreads) sh.hist[1][b] = 0u;
+  __syncthreads();
+  for (int i = tid; i < cnt; i += kStepThreads) {
+    const uint32_t key = sh.keys[i];
+    if ((key >> 21) == d1) atomicAdd(&sh.hist[1][(key >> 10) & 0x7ffu], 1u);
   }
-  group_bar(2, kEpiThreads);
-  for (int r = 0; r < nsel; ++r) {
-    const uint32_t* kr = keys_of(r);
-    uint32_t* h = hist_of(r, 1);
-    const uint32_t pre = ss[r].prefix >> 21;
-    for (int i0 = lo; i0 < hi; i0 += kEpiThreads) {
-      const int i = i0 + et;
-      const uint32_t key = i < hi ? __ldcg(kr + i) : 0u;
-      const bool ok = i < hi && (key >> 21) == pre;
-      hist_add(h, (key >> 10) & 0x7ffu, ok, 0xffffffffu, lane);
-    }
+  __syncthreads();
+  cluster_digit(cl, sh, 1, LYC_BINS, krem);
+  const uint32_t d2 = sh.digit;
+  krem -= sh.above;
+  // ---- pass 3 (bits 9..0)
+  const uint32_t pre22 = (d1 << 11) | d2;
+  for (int b = tid; b < LYC_BINS; b += kStepThreads) sh.hist[0][b] = 0u;
+  __syncthreads();
+  for (int i = tid; i < cnt; i += kStepThreads) {
+    const uint32_t key = sh.keys[i];
+    if ((key >> 10) == pre22) atomicAdd(&sh.hist[0][key & 0x3ffu], 1u);
   }
-  grid_barrier_epi(lc + CTR_SEL0, target, et);
-  // ---- pass 2 digit (bits 20..10); pass 3 histogram
-  for (int r = w; r < nsel; r += kEpiWarps) {
-    uint32_t d, a;
-    find_digit(hist_of(r, 1), 2048, ss[r].krem, d, a, lane);
-    if (lane == 0) {
-      ss[r].prefix |= d << 10;
-      ss[r].krem -= a;
-    }
+  __syncthreads();
+  cluster_digit(cl, sh, 0, 1024, krem);
+  const uint32_t T = (pre22 << 10) | sh.digit;
+  krem -= sh.above;  // ties of T to take, cluster-wide
+  // ---- emission: cluster scan of (count > T, count == T) over ranks
+  uint32_t gt = 0, eq = 0;
+  for (int i = tid; i < cnt; i += kStepThreads) {
+    const uint32_t key = sh.keys[i];
+    gt += key > T;
+    eq += key == T;
   }
-  group_bar(2, kEpiThreads);
-  for (int r = 0; r < nsel; ++r) {
-    const uint32_t* kr = keys_of(r);
-    uint32_t* h = hist_of(r, 2);
-    const uint32_t pre = ss[r].prefix >> 10;
-    for (int i0 = lo; i0 < hi; i0 += kEpiThreads) {
-      const int i = i0 + et;
-      const uint32_t key = i < hi ? __ldcg(kr + i) : 0u;
-      const bool ok = i < hi && (key >> 10) == pre;
-      hist_add(h, key & 0x3ffu, ok, 0xffffffffu, lane);
-    }
+  uint32_t tgt, teq;
+  block_scan(gt, sh.warp_tot, tgt);
+  block_scan(eq, sh.warp_tot, teq);
+  if (tid == 0) {
+    sh.counts[0] = tgt;
+    sh.counts[1] = teq;
   }
-  grid_barrier_epi(lc + CTR_SEL1, target, et);
-  // ---- pass 3 digit (bits 9..0): T exact; count > T and == T in this slice
-  for (int r = w; r < nsel; r += kEpiWarps) {
-    uint32_t d, a;
-    find_digit(hist_of(r, 2), 1024, ss[r].krem, d, a, lane);
-    if (lane == 0) {
-      ss[r].prefix |= d;
-      ss[r].krem -= a;  // ties of T to take, grid-wide
-    }
+  cl.sync();
+  uint32_t base = 0, eqb = 0;
+  for (int c = 0; c < rank; ++c) {
+    const uint32_t* rc = cl.map_shared_rank(sh.counts, c);
+    const uint32_t cg_ = rc[0], ce = rc[1];
+    base += cg_ + (krem > eqb ? min(ce, krem - eqb) : 0u);
+    eqb += ce;
   }
-  group_bar(2, kEpiThreads);
-  for (int r = 0; r < nsel; ++r) {
-    const uint32_t* kr = keys_of(r);
-    const uint32_t T = ss[r].prefix;
-    uint32_t gt = 0, eq = 0;
-    for (int i = lo + et; i < hi; i += kEpiThreads) {
-      const uint32_t key = __ldcg(kr + i);
-      gt += key > T;
-      eq += key == T;
-    }
+  const uint32_t take_eq = krem > eqb ? min(sh.counts[1], krem - eqb) : 0u;
+  uint32_t run_gt = 0, run_eq = 0;
+  constexpr int kPer = 4;
+  for (int b0 = 0; b0 < cnt; b0 += kStepThreads * kPer) {
+    const int i0 = b0 + tid * kPer;
+    uint32_t kv[kPer];
+    uint32_t g = 0, e = 0;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      gt += __shfl_xor_sync(0xffffffffu, gt, off);
-      eq += __shfl_xor_sync(0xffffffffu, eq, off);
+    for (int q = 0; q < kPer; ++q) {
+      const bool ok = i0 + q < cnt;
+      kv[q] = ok ? sh.keys[i0 + q] : 0u;
+      g += ok && kv[q] > T;
+      e += ok && kv[q] == T;
     }
-    if (lane == 0) {
-      scan[2 * w] = gt;
-      scan[2 * w + 1] = eq;
+    uint32_t tot;
+    const uint32_t mine = (e << 16) | g;
+    const uint32_t incl = block_scan(mine, sh.warp_tot, tot);
+    uint32_t gb = run_gt + ((incl - mine) & 0xffffu);
+    uint32_t eb = run_eq + ((incl - mine) >> 16);
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      if (i0 + q >= cnt) break;
+      const bool is_gt = kv[q] > T, is_eq = kv[q] == T;
+      if (is_gt || (is_eq && eb < take_eq)) out[base + gb + min(eb, take_eq)] = lo + i0 + q;
+      gb += is_gt;
+      eb += is_eq;
     }
-    group_bar(2, kEpiThreads);
-    if (et == 0) {
-      uint32_t* tm = p.team + (((int64_t)(l & 1) * p.max_sel + r) * p.n_ctas + cta) * 2;
-      tm[0] = scan[0] + scan[2];
-      tm[1] = scan[1] + scan[3];
-    }
-    group_bar(2, kEpiThreads);
+    run_gt += tot & 0xffffu;
+    run_eq += tot >> 16;
   }
-  grid_barrier_epi(lc + CTR_SEL2, target, et);
-  // ---- ordered compaction of this slice into the index cache
-  for (int r = w; r < nsel; r += kEpiWarps) {
-    const uint32_t* tm = p.team + ((int64_t)(l & 1) * p.max_sel + r) * p.n_ctas * 2;
-    uint32_t base = 0, eqb = 0;
-    for (int c = lane; c < cta; c += 32) {
-      base += __ldcg(tm + 2 * c);
-      eqb += __ldcg(tm + 2 * c + 1);
-    }
-    // the ties taken by earlier CTAs are min(their ties, remaining) in order:
-    // sum_{c<cta} take_c = min(eq_before, krem)
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      base += __shfl_xor_sync(0xffffffffu, base, off);
-      eqb += __shfl_xor_sync(0xffffffffu, eqb, off);
-    }
-    if (lane == 0) {
-      const uint32_t krem = ss[r].krem;
-      const uint32_t mine_eq = __ldcg(tm + 2 * cta + 1);
-      ss[r].out_base = base + min(eqb, krem);
-      ss[r].take_eq = krem > eqb ? min(mine_eq, krem - eqb) : 0u;
-    }
-  }
-  group_bar(2, kEpiThreads);
-  for (int r = 0; r < nsel; ++r) {
-    const uint32_t* kr = keys_of(r);
-    const uint32_t T = ss[r].prefix, take_eq = ss[r].take_eq;
-    int32_t* out = p.idx + (int64_t)__ldg(L.sel_rows + r) * p.idx_stride + ss[r].out_base;
-    uint32_t run_gt = 0, run_eq = 0;
-    constexpr int kPer = 4;
-    for (int base = lo; base < hi; base += kEpiThreads * kPer) {
-      const int i0 = base + et * kPer;
-      uint32_t kv[kPer];
-      uint32_t g = 0, e = 0;
-#pragma unroll
-      for (int q = 0; q < kPer; ++q) {
-        const bool ok = i0 + q < hi;
-        kv[q] = ok ? __ldcg(kr + i0 + q) : 0u;
-        g += ok && kv[q] > T;
-        e += ok && kv[q] == T;
-      }
-      const uint32_t mine = (e << 16) | g;
-      uint32_t incl = mine;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += t;
-      }
-      if (lane == 31) scan[w] = incl;
-      group_bar(2, kEpiThreads);
-      const uint32_t wbefore = w == 0 ? 0u : scan[0];
-      const uint32_t total = scan[0] + scan[1];
-      group_bar(2, kEpiThreads);
-      const uint32_t excl = incl - mine + wbefore;
-      uint32_t gb = run_gt + (excl & 0xffffu);
-      uint32_t eb = run_eq + (excl >> 16);
-#pragma unroll
-      for (int q = 0; q < kPer; ++q) {
-        if (i0 + q >= hi) break;
-        const bool is_gt = kv[q] > T, is_eq = kv[q] == T;
-        if (is_gt || (is_eq && eb < take_eq)) out[gb + min(eb, take_eq)] = i0 + q;
-        gb += is_gt;
-        eb += is_eq;
-      }
-      run_gt += total & 0xffffu;
-      run_eq += total >> 16;
-    }
-    // reset this CTA's share of the histograms (and block keys) for reuse
-    for (int pass = 0; pass < 3; ++pass) {
-      uint32_t* h = hist_of(r, pass);
-      const int b0 = (int)((int64_t)cta * LYC_BINS / p.n_ctas);
-      const int b1 = (int)((int64_t)(cta + 1) * LYC_BINS / p.n_ctas);
-      for (int b = b0 + et; b < b1; b += kEpiThreads) h[b] = 0u;
-    }
-    if (p.sel_mode == SEL_BLOCK_KEYS) {
-      uint32_t* kw = p.sel_keys + ((int64_t)(l & 1) * p.max_sel + r) * p.sel_stride;
-      for (int i = lo + et; i < hi; i += kEpiThreads) kw[i] = 0u;
-    }
-    if (cta == 0 && et == 0 && p.idx_count) p.idx_count[__ldg(L.sel_rows + r)] = p.k_sel;
-  }
-  group_bar(2, kEpiThreads);
-  if (et == 0) signal(lc + CTR_SELDONE);
+  // reset the fused first-pass histogram for its next use (all CTAs read it
+  // before the cl.sync of pass 1)
+  if (h1 && rank == 0)
+    for (int b = tid; b < LYC_BINS; b += kStepThreads) const_cast<uint32_t*>(h1)[b] = 0u;
+  cl.sync();  // remote reads of counts / hist done before the next row reuses them
 }
 
 // ---------------------------------------------------------------- kernel
@@ -368,103 +351,149 @@ template <typename T, int D>
 __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __grid_constant__ LycStepParams p) {
   using C = AttnCfg<T, D>;
   extern __shared__ uint8_t smem_raw[];
-  const AttnSmem<T, D> sm = AttnSmem<T, D>::carve(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cta = blockIdx.y * p.n_splits + blockIdx.x;
-  uint32_t* ctrl = p.ctr + p.n_layers * CTR_PER_LAYER;  // [0] completed steps, [1] exits
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&sm.full[s], kProducerThreads);
-      mbar_init(&sm.empty[s], kConsumerWarps);
-    }
-    fence_mbar_init();
-    reinterpret_cast<uint32_t*>(sm.extra)[0] = ld_acquire(ctrl);
-  }
+  const int cta = blockIdx.x;
+  const int n_total = p.n_ctas + p.n_sel_ctas;
+  uint32_t* ctrl = LYC_CTR(p.ctr, p.n_layers, 0);  // completed steps; exits at + stride
+  __shared__ uint32_t s_epoch;
+  if (threadIdx.x == 0) s_epoch = ld_acquire(ctrl);
   __syncthreads();
-  const uint32_t target = (reinterpret_cast<uint32_t*>(sm.extra)[0] + 1u) * (uint32_t)p.n_ctas;
-  __syncthreads();
+  const uint32_t epoch1 = s_epoch + 1u;
+  const uint32_t t_attn = epoch1 * (uint32_t)p.n_ctas;
+  const uint32_t t_sel = epoch1 * (uint32_t)p.n_sel_ctas;
   constexpr int esz = (int)sizeof(T);
 
-  if (warp < kConsumerWarps) {
-    const int tid = threadIdx.x;
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int l = 0; l < p.n_layers; ++l) {
-      if (l > 0) {
-        if (tid == 0) {
-          spin_until(p.ctr + (l - 1) * CTR_PER_LAYER + CTR_MERGE, target);
-          // key / histogram buffers of this parity are free once layer l-2's
-          // selection (if any) finished
-          if (l >= 2 && p.layers[l - 2].n_sel > 0)
-            spin_until(p.ctr + (l - 2) * CTR_PER_LAYER + CTR_SELDONE, target);
-          __threadfence();
-        }
-        consumer_bar();
-      }
-      const LycLayerDesc L = p.layers[l];
-      const LycView v = layer_view(p, L, l, esz);
-      const int cell = blockIdx.y * p.n_splits + blockIdx.x;
-      consume_units<T, D>(v, sm, L.split_off[cell], L.split_off[cell + 1], warp, lane, stage,
-                          phase);
-      consumer_bar();
-      if (tid == 0) signal(p.ctr + l * CTR_PER_LAYER + CTR_ATTN);
-    }
-  } else if (warp < kConsumerWarps + kProducerWarps) {
-    const int pt = threadIdx.x - kConsumerWarps * 32;
-    if (pt == 0) {
-      prefetch_tensormap(&p.tmap_k);
-      prefetch_tensormap(&p.tmap_v);
-    }
-    int stage = 0;
-    uint32_t phase = 0;
+  if (cta >= p.n_ctas) {
+    // ======================== selection cluster ========================
+    cg::cluster_group cl = cg::this_cluster();
+    SelSmem& sh = *reinterpret_cast<SelSmem*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const int sc = (cta - p.n_ctas) / kSelCluster;
+    const int n_sc = p.n_sel_ctas / kSelCluster;
     for (int l = 0; l < p.n_layers; ++l) {
       const LycLayerDesc L = p.layers[l];
-      const LycView v = layer_view(p, L, l, esz);
-      const int cell = blockIdx.y * p.n_splits + blockIdx.x;
-      StepWaits waits{p.ctr, target, l, pt};
-      produce_units<T, D>(v, &p.tmap_k, &p.tmap_v, sm.ring, sm.full, sm.empty,
-                          L.split_off[cell], L.split_off[cell + 1], pt, stage, phase, waits);
-    }
-  } else {
-    const int et = threadIdx.x - (kConsumerWarps + kProducerWarps) * 32;
-    const int ew = et >> 5;
-    SelScratch* ss = reinterpret_cast<SelScratch*>(sm.extra + 64);
-    uint32_t* scan = reinterpret_cast<uint32_t*>(sm.extra + 16);
-    const int chunks = (D + 31) / 32;
-    for (int l = 0; l < p.n_layers; ++l) {
-      const LycLayerDesc L = p.layers[l];
-      uint32_t* lc = p.ctr + l * CTR_PER_LAYER;
-      if (et == 0) {
-        spin_until(lc + CTR_ATTN, target);
+      if (L.n_sel == 0 || p.sel_mode == SEL_NONE) continue;
+      if (threadIdx.x == 0) {
+        spin_until(LYC_CTR(p.ctr, l, CTR_ATTN), t_attn);
         __threadfence();
+        stamp(p, l, EV_SEL0, cta - p.n_ctas);
       }
-      group_bar(2, kEpiThreads);
-      // (a) split-KV merge, spread over all CTAs' epilogue warps
-      const int total = L.n_merges * chunks;
-      const uint8_t* outl = static_cast<const uint8_t*>(p.out) + (int64_t)l * p.q_layer_stride * esz;
-      for (int t = cta * kEpiWarps + ew; t < total; t += p.n_ctas * kEpiWarps) {
-        const LycMergeTask tk = L.merges[t / chunks];
-        const LycSlot s = L.slots[tk.slot];
-        merge_task<T>(p.part_o, p.part_lse, s, tk.j, t % chunks, p.group, D,
-                      const_cast<uint8_t*>(outl), lane);
+      __syncthreads();
+      for (int r = sc; r < L.n_sel; r += n_sc) {
+        uint32_t* kg = p.sel_keys + ((int64_t)(l & 1) * p.max_sel + r) * p.sel_stride;
+        const uint32_t* h1 = p.sel_mode == SEL_TOKEN_KEYS
+                                 ? p.hist + ((int64_t)(l & 1) * p.max_sel + r) * LYC_BINS
+                                 : nullptr;
+        const int row = __ldg(L.sel_rows + r);
+        select_row(cl, sh, p, kg, h1, p.idx + (int64_t)row * p.idx_stride);
+        if (threadIdx.x == 0 && cl.block_rank() == 0 && p.idx_count) p.idx_count[row] = p.k_sel;
       }
-      group_bar(2, kEpiThreads);
-      if (et == 0) signal(lc + CTR_MERGE);
-      // (b) selection for this layer's retrieval heads
-      if (L.n_sel > 0 && p.sel_mode != SEL_NONE)
-        select_layer<T, D>(p, L, l, cta, target, et, ss, scan);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        stamp(p, l, EV_SELDONE, cta - p.n_ctas);
+        signal(LYC_CTR(p.ctr, l, CTR_SELDONE));
+      }
+    }
+    cl.sync();
+  } else {
+    // ======================== attention CTA ========================
+    const AttnSmem<T, D> sm = AttnSmem<T, D>::carve(smem_raw);
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < C::kStages; ++s) {
+        mbar_init(&sm.full[s], kProducerThreads);
+        mbar_init(&sm.empty[s], kConsumerWarps);
+      }
+      fence_mbar_init();
+    }
+    for (int b = threadIdx.x; b < LYC_BINS; b += kStepThreads) sm.hist[b] = 0u;
+    __syncthreads();
+    const int bb = cta / p.n_splits, split = cta - bb * p.n_splits;
+    const int cell = bb * p.n_splits + split;
+    if (warp < kConsumerWarps) {
+      const int tid = threadIdx.x;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int l = 0; l < p.n_layers; ++l) {
+        if (l > 0) {
+          if (tid == 0) {
+            spin_until(LYC_CTR(p.ctr, l - 1, CTR_MERGE), t_attn);
+            // key / histogram buffers of this parity are free once layer l-2's
+            // selection (if any) finished
+            if (l >= 2 && p.layers[l - 2].n_sel > 0 && p.sel_mode != SEL_NONE)
+              spin_until(LYC_CTR(p.ctr, l - 2, CTR_SELDONE), t_sel);
+            __threadfence();
+          }
+          consumer_bar();
+        }
+        if (tid == 0) stamp(p, l, EV_CONS_BEGIN, cta);
+        const LycLayerDesc L = p.layers[l];
+        const LycView v = layer_view(p, L, l, esz);
+        consume_units<T, D>(v, sm, L.split_off[cell], L.split_off[cell + 1], warp, lane, stage,
+                            phase);
+        consumer_bar();
+        if (tid == 0) {
+          stamp(p, l, EV_CONS_END, cta);
+          signal(LYC_CTR(p.ctr, l, CTR_ATTN));
+        }
+      }
+    } else if (warp < kConsumerWarps + kProducerWarps) {
+      const int pt = threadIdx.x - kConsumerWarps * 32;
+      if (pt == 0) {
+        prefetch_tensormap(&p.tmap_k);
+        prefetch_tensormap(&p.tmap_v);
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int l = 0; l < p.n_layers; ++l) {
+        const LycLayerDesc L = p.layers[l];
+        const LycView v = layer_view(p, L, l, esz);
+        StepWaits waits{p.ctr, t_attn, t_sel, l, pt};
+        produce_units<T, D>(v, &p.tmap_k, &p.tmap_v, sm.ring, sm.full, sm.empty,
+                            L.split_off[cell], L.split_off[cell + 1], pt, stage, phase, waits);
+      }
+    } else {
+      const int et = threadIdx.x - (kConsumerWarps + kProducerWarps) * 32;
+      const int ew = et >> 5;
+      const int chunks = (D + 31) / 32;
+      for (int l = 0; l < p.n_layers; ++l) {
+        const LycLayerDesc L = p.layers[l];
+        if (et == 0) {
+          spin_until(LYC_CTR(p.ctr, l, CTR_ATTN), t_attn);
+          __threadfence();
+          stamp(p, l, EV_EPI_ATTN, cta);
+        }
+        group_bar(2, kEpiThreads);
+        // split-KV merge, spread over all attention CTAs' epilogue warps
+        const int total = L.n_merges * chunks;
+        uint8_t* outl = static_cast<uint8_t*>(p.out) + (int64_t)l * p.q_layer_stride * esz;
+        for (int t = cta * kEpiWarps + ew; t < total; t += p.n_ctas * kEpiWarps) {
+          const LycMergeTask tk = L.merges[t / chunks];
+          const LycSlot s = L.slots[tk.slot];
+          merge_task<T>(p.part_o, p.part_lse, s, tk.j, t % chunks, p.group, D, outl, lane);
+        }
+        group_bar(2, kEpiThreads);
+        if (et == 0) {
+          stamp(p, l, EV_MERGE, cta);
+          signal(LYC_CTR(p.ctr, l, CTR_MERGE));
+        }
+      }
     }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t done = atomicAdd(ctrl + 1, 1u);
-    if (done == target - 1u) atomicAdd(ctrl, 1u);  // last CTA out: one more completed step
+    const uint32_t done = atomicAdd(ctrl + LYC_CTR_STRIDE, 1u);
+    if (done == epoch1 * (uint32_t)n_total - 1u) atomicAdd(ctrl, 1u);  // last CTA out
   }
 }
 
 template <typename T, int D>
-static cudaError_t launch_step_t(const LycStepParams& p, int batch, cudaStream_t st) {
+int step_sel_capacity() {  // keys a selection CTA keeps in shared memory
+  using C = AttnCfg<T, D>;
+  return (int)((C::kSmem - 1024 - (int)sizeof(SelSmem)) / 4);
+}
+
+template <typename T, int D>
+static cudaError_t launch_step_t(const LycStepParams& p, cudaStream_t st) {
   using C = AttnCfg<T, D>;
   static bool configured = false;
   if (!configured) {
@@ -474,33 +503,54 @@ static cudaError_t launch_step_t(const LycStepParams& p, int batch, cudaStream_t
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.n_splits, batch);
+  cfg.gridDim = dim3(p.n_ctas + p.n_sel_ctas);
   cfg.blockDim = dim3(kStepThreads);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kSelCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, hybrid_step_kernel<T, D>, p);
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, hybrid_step_kernel<T, D>, p);
+  if (e == cudaErrorInvalidValue || e == cudaErrorNotSupported) {
+    (void)cudaGetLastError();  // cooperative + cluster unsupported: co-residency is still
+    cfg.numAttrs = 1;          // guaranteed by 1 CTA/SM and grid <= #SMs (checked on host)
+    e = cudaLaunchKernelEx(&cfg, hybrid_step_kernel<T, D>, p);
+  }
+  return e;
 }
 
-cudaError_t launch_step(const LycStepParams& p, int dtype, int d, int batch, cudaStream_t st) {
+cudaError_t launch_step(const LycStepParams& p, int dtype, int d, cudaStream_t st) {
   if (dtype == 1) {
     switch (d) {
-      case 64: return launch_step_t<__nv_bfloat16, 64>(p, batch, st);
-      case 128: return launch_step_t<__nv_bfloat16, 128>(p, batch, st);
+      case 64: return launch_step_t<__nv_bfloat16, 64>(p, st);
+      case 128: return launch_step_t<__nv_bfloat16, 128>(p, st);
     }
   } else {
     switch (d) {
-      case 16: return launch_step_t<float, 16>(p, batch, st);
-      case 32: return launch_step_t<float, 32>(p, batch, st);
-      case 64: return launch_step_t<float, 64>(p, batch, st);
-      case 128: return launch_step_t<float, 128>(p, batch, st);
+      case 16: return launch_step_t<float, 16>(p, st);
+      case 32: return launch_step_t<float, 32>(p, st);
+      case 64: return launch_step_t<float, 64>(p, st);
+      case 128: return launch_step_t<float, 128>(p, st);
     }
   }
   return cudaErrorInvalidValue;
+}
+
+int step_select_capacity(int dtype, int d) {
+  if (dtype == 1) return d == 64 ? step_sel_capacity<__nv_bfloat16, 64>()
+                                 : step_sel_capacity<__nv_bfloat16, 128>();
+  switch (d) {
+    case 16: return step_sel_capacity<float, 16>();
+    case 32: return step_sel_capacity<float, 32>();
+    case 64: return step_sel_capacity<float, 64>();
+    default: return step_sel_capacity<float, 128>();
+  }
 }
 
 bool step_supported(int dtype, int d) {

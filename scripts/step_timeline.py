@@ -1,0 +1,65 @@
+"""Per-layer timeline of one fused decode step (debug tool, run under gpurun).
+
+    python scripts/step_timeline.py [--workload llama3-8b-128k] [--select tokens]
+
+Prints, per layer, the retrieval-head count and (relative to the step start,
+in microseconds): first consumer start, last consumer end (all attention
+units done), merge done, selection barriers and selection done -- each the
+max (or min for starts) over the CTAs.
+"""
+import argparse
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import bench  # noqa: E402
+import paper_2602_04541_b200 as P  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="llama3-8b-128k")
+    ap.add_argument("--select", default="tokens")
+    ap.add_argument("--layers", type=int, default=0)
+    a = ap.parse_args()
+    wl = dict(bench.WORKLOADS[a.workload])
+    if a.layers:
+        wl["NL"] = a.layers
+    NL, H, G, d, L, k, B = (wl[x] for x in ("NL", "H", "G", "d", "L", "k", "B"))
+    roles = bench.make_roles(NL, H, 0.125, 2602)
+    dt = torch.bfloat16 if wl["dtype"] == "bf16" else torch.float32
+    K = torch.empty((NL, B, H, L, d), dtype=dt, device="cuda")
+    V = torch.empty_like(K)
+    for t in (K, V):
+        for l in range(NL):
+            t[l].uniform_(-1, 1)
+    q = torch.empty((NL, B, H * G, d), dtype=dt, device="cuda").uniform_(-1, 1)
+    dec = P.HybridDecoder(n_layers=NL, batch=B, n_kv_heads=H, group_size=G, d_head=d, seq_cap=L,
+                          roles=roles, policy=P.SparsityPolicy.top_k(k), dtype=dt, select=a.select)
+    assert dec.fused, "timeline needs the fused step kernel"
+    for _ in range(3):
+        out = dec.decode_step(q, K, V, L)
+    dec.set_trace(True)
+    out = dec.decode_step(q, K, V, L)
+    torch.cuda.synchronize()
+    tr = dec.trace().astype(np.int64)
+    t0 = tr[0, 0].min()
+    rel = (tr - t0) / 1e3
+    names = ["cons_begin(min)", "cons_end(max)", "epi_attn(max)", "merge(max)", "sel0", "sel1",
+             "sel2", "seldone"]
+    print(f"{'l':>3} {'R':>2} " + " ".join(f"{n:>15}" for n in names))
+    for l in range(NL):
+        nr = int((roles[l] == 0).sum()) if l else H
+        vals = [rel[l, 0].min(), rel[l, 1].max(), rel[l, 2].max(), rel[l, 3].max()]
+        for e in range(4, 8):
+            vals.append(rel[l, e].max() if tr[l, e].max() > t0 else float("nan"))
+        print(f"{l:3d} {nr:2d} " + " ".join(f"{v:15.1f}" for v in vals))
+    print("step span us:", (tr.max() - t0) / 1e3)
+
+
+if __name__ == "__main__":
+    main()
