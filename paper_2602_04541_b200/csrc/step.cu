@@ -1,8 +1,7 @@
 // step.cu -- the persistent decode-step kernel: every layer of one decode step
 // (decode_engine.hpp:109-151) in ONE launch, one CTA per SM.
 //
-// The grid is 1-D with 4-CTA clusters.  The first n_attn CTAs are ATTENTION
-// CTAs (256 threads):
+// The first n_ctas CTAs of the 1-D grid are ATTENTION CTAs (256 threads):
 //   warps 0-3 consumers  attention of this CTA's split of layer l
 //                        (attn_core.cuh); layer l+1 starts only after layer
 //                        l's outputs are final (device counter) -- the model's
@@ -15,30 +14,26 @@
 //                        previous layer (its K/V row is produced after it);
 //   warps 6-7 epilogue   the split-KV LSE merge of layer l (kernel_sim.hpp:
 //                        205-225), spread over every attention CTA.
-// The last n_sel clusters are SELECTION clusters (Algorithm 2's pooling
-// applied to the selection): after layer l's attention they compute, for each
-// of its retrieval heads, args_top_k over the pooled-query keys
+// The last n_sel_ctas CTAs form SELECTION TEAMS of 4 (Algorithm 2's pooling
+// applied to the selection): after layer l's attention, a team computes for
+// each of its retrieval heads args_top_k over the pooled-query keys
 // (attention.hpp:108-123: the k largest, ties to the lower index, ascending)
-// as an exact radix select: the consumers already produced the first 11-bit
-// histogram while scoring; each CTA of the cluster holds a quarter of the
-// keys in shared memory, two more passes reduce their histograms through
-// DSMEM, and an ordered compaction writes the index cache.  Selection runs
-// concurrently with the next layer's attention.
-// Grid-wide coordination uses monotonic per-layer counters in global memory
-// (a step adds the number of participating CTAs); every CTA is co-resident
-// (cooperative launch, one CTA per SM).
-#include <cooperative_groups.h>
-
+// as an exact radix select.  The consumers already produced the first 11-bit
+// histogram while scoring; each team CTA holds a quarter of the keys in
+// shared memory; two more passes exchange 2048-bin histograms through global
+// memory behind per-row team barriers; an ordered compaction writes the
+// index cache.  Selection runs concurrently with the next layer's attention.
+// Grid-wide coordination uses monotonic counters in global memory (each step
+// adds the number of participating CTAs); the launch is cooperative, so every
+// CTA is co-resident.
 #include "attn_core.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace lyc {
 
 constexpr int kEpiWarps = 2;
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kStepThreads = (kConsumerWarps + kProducerWarps + kEpiWarps) * 32;
-constexpr int kSelCluster = 4;
+constexpr int kTeam = 4;  // CTAs per selection team
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
@@ -67,13 +62,13 @@ __device__ __forceinline__ void signal(uint32_t* ctr) {
   atomicAdd(ctr, 1u);
 }
 
-// Debug timeline: %globaltimer (ns) of event ev of layer l on this CTA.
+// Debug timeline: %globaltimer (ns) of event ev of layer l on slot `who`.
 enum { EV_CONS_BEGIN = 0, EV_CONS_END, EV_EPI_ATTN, EV_MERGE, EV_SEL0, EV_SEL1, EV_SEL2, EV_SELDONE };
-__device__ __forceinline__ void stamp(const LycStepParams& p, int l, int ev, int cta) {
+__device__ __forceinline__ void stamp(const LycStepParams& p, int l, int ev, int who) {
   if (p.trace) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.trace[((size_t)l * 8 + ev) * p.n_ctas + cta] = t;
+    p.trace[((size_t)l * 8 + ev) * p.n_ctas + who] = t;
   }
 }
 
@@ -170,12 +165,11 @@ __device__ __forceinline__ void find_digit(const uint32_t* h, int nbins, uint32_
 
 // Shared memory of a selection CTA (carved from the same dynamic allocation).
 struct SelSmem {
-  uint32_t hist[2][LYC_BINS];  // local pass histograms (double-buffered for DSMEM readers)
-  uint32_t ghist[LYC_BINS];    // cluster-summed histogram
+  uint32_t hist[LYC_BINS];   // this CTA's pass histogram
+  uint32_t ghist[LYC_BINS];  // team-summed histogram
   uint32_t warp_tot[32];
-  uint32_t counts[2];          // this CTA's (count > T, count == T)
   uint32_t digit, above;
-  uint32_t keys[1];            // slice of the row's keys (capacity p.sel_cap)
+  uint32_t keys[1];          // this CTA's slice of the row's keys (capacity sel_cap)
 };
 
 // Block-wide inclusive scan (256 threads).
@@ -201,20 +195,40 @@ __device__ __forceinline__ uint32_t block_scan(uint32_t v, uint32_t* warp_tot, u
   return v + before;
 }
 
-// Sum the cluster's pass histograms into ghist and locate the digit.
-__device__ __forceinline__ void cluster_digit(cg::cluster_group& cl, SelSmem& sh, int buf,
-                                              int nbins, uint32_t krem) {
-  cl.sync();  // every CTA's local histogram is complete
-  const int C = (int)cl.num_blocks();
-  for (int b = threadIdx.x; b < nbins; b += kStepThreads) {
-    uint32_t s = 0;
-    for (int c = 0; c < C; ++c) s += cl.map_shared_rank(&sh.hist[buf][0], c)[b];
-    sh.ghist[b] = s;
+struct Team {
+  uint32_t* bar;        // this row's barrier counters (kTeam arrivals each per step)
+  uint32_t* xch;        // [2][kTeam][LYC_BINS] histogram exchange buffers of this team
+  uint32_t* cnt;        // [kTeam][2] count exchange
+  uint32_t target;      // epoch1 * kTeam
+  int rank;
+
+  __device__ __forceinline__ void barrier(int b) const {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      signal(bar + b * 16);
+      spin_until(bar + b * 16, target);
+    }
+    __syncthreads();
   }
-  __syncthreads();
+  // Publish the local histogram, barrier b, sum the team's histograms into ghist.
+  __device__ __forceinline__ void exchange(SelSmem& sh, int buf, int nbins, int b) const {
+    uint32_t* mine = xch + ((size_t)buf * kTeam + rank) * LYC_BINS;
+    for (int i = threadIdx.x; i < nbins; i += kStepThreads) mine[i] = sh.hist[i];
+    barrier(b);
+    for (int i = threadIdx.x; i < nbins; i += kStepThreads) {
+      uint32_t s = 0;
+#pragma unroll
+      for (int c = 0; c < kTeam; ++c) s += __ldcg(xch + ((size_t)buf * kTeam + c) * LYC_BINS + i);
+      sh.ghist[i] = s;
+    }
+    __syncthreads();
+  }
+};
+
+__device__ __forceinline__ void digit_of(SelSmem& sh, const uint32_t* h, int nbins, uint32_t krem) {
   if (threadIdx.x < 32) {
     uint32_t d, a;
-    find_digit(sh.ghist, nbins, krem, d, a, threadIdx.x);
+    find_digit(h, nbins, krem, d, a, threadIdx.x);
     if (threadIdx.x == 0) {
       sh.digit = d;
       sh.above = a;
@@ -225,69 +239,58 @@ __device__ __forceinline__ void cluster_digit(cg::cluster_group& cl, SelSmem& sh
 
 // One row: the k largest of n keys (ties to the lower index), ascending,
 // into out[0..k).  h1 (token mode) holds the grid-wide first-pass histogram.
-__device__ void select_row(cg::cluster_group& cl, SelSmem& sh, const LycStepParams& p,
-                           uint32_t* keys_g, const uint32_t* h1, int32_t* out) {
+__device__ void select_row(SelSmem& sh, const Team& tm, const LycStepParams& p, uint32_t* keys_g,
+                           uint32_t* h1, int32_t* out) {
   const int tid = threadIdx.x;
-  const int C = (int)cl.num_blocks(), rank = (int)cl.block_rank();
   const int n = p.n_keys;
-  const int slice = ((n + C - 1) / C + 3) & ~3;
-  const int lo = min(n, rank * slice);
+  const int slice = ((n + kTeam - 1) / kTeam + 3) & ~3;
+  const int lo = min(n, tm.rank * slice);
   const int cnt = max(0, min(slice, n - lo));
-  // load this CTA's slice (block-mode keys are reset for the next use)
+  // this CTA's slice (block-mode keys are reset for their next use)
   for (int i = tid; i < cnt; i += kStepThreads) {
     sh.keys[i] = __ldcg(keys_g + lo + i);
     if (p.sel_mode == SEL_BLOCK_KEYS) keys_g[lo + i] = 0u;
   }
   uint32_t krem = (uint32_t)p.k_sel;
   // ---- pass 1 (bits 31..21)
-  for (int b = tid; b < LYC_BINS; b += kStepThreads) sh.hist[0][b] = 0u;
-  __syncthreads();
-  uint32_t d1, a1;
   if (h1) {
     for (int b = tid; b < LYC_BINS; b += kStepThreads) sh.ghist[b] = __ldcg(h1 + b);
     __syncthreads();
-    if (tid < 32) {
-      uint32_t d, a;
-      find_digit(sh.ghist, LYC_BINS, krem, d, a, tid);
-      if (tid == 0) {
-        sh.digit = d;
-        sh.above = a;
-      }
-    }
-    __syncthreads();
-    cl.sync();  // every CTA read h1 before it is reset below
   } else {
-    for (int i = tid; i < cnt; i += kStepThreads) atomicAdd(&sh.hist[0][sh.keys[i] >> 21], 1u);
+    for (int b = tid; b < LYC_BINS; b += kStepThreads) sh.hist[b] = 0u;
     __syncthreads();
-    cluster_digit(cl, sh, 0, LYC_BINS, krem);
+    for (int i = tid; i < cnt; i += kStepThreads) atomicAdd(&sh.hist[sh.keys[i] >> 21], 1u);
+    tm.exchange(sh, 1, LYC_BINS, 0);
   }
-  d1 = sh.digit;
-  a1 = sh.above;
-  krem -= a1;
-  // ---- pass 2 (bits 20..10) among keys with top bits == d1
-  for (int b = tid; b < LYC_BINS; b += kStepThreads) sh.hist[1][b] = 0u;
+  digit_of(sh, sh.ghist, LYC_BINS, krem);
+  const uint32_t d1 = sh.digit;
+  krem -= sh.above;
+  // ---- pass 2 (bits 20..10) among keys whose top bits are d1
+  for (int b = tid; b < LYC_BINS; b += kStepThreads) sh.hist[b] = 0u;
   __syncthreads();
   for (int i = tid; i < cnt; i += kStepThreads) {
     const uint32_t key = sh.keys[i];
-    if ((key >> 21) == d1) atomicAdd(&sh.hist[1][(key >> 10) & 0x7ffu], 1u);
+    if ((key >> 21) == d1) atomicAdd(&sh.hist[(key >> 10) & 0x7ffu], 1u);
   }
-  __syncthreads();
-  cluster_digit(cl, sh, 1, LYC_BINS, krem);
+  tm.exchange(sh, 0, LYC_BINS, 1);  // also orders every member's read of h1 before its reset
+  digit_of(sh, sh.ghist, LYC_BINS, krem);
   const uint32_t d2 = sh.digit;
   krem -= sh.above;
+  if (h1 && tm.rank == 0)  // reset the fused histogram for its next use
+    for (int b = tid; b < LYC_BINS; b += kStepThreads) h1[b] = 0u;
   // ---- pass 3 (bits 9..0)
   const uint32_t pre22 = (d1 << 11) | d2;
-  for (int b = tid; b < LYC_BINS; b += kStepThreads) sh.hist[0][b] = 0u;
+  for (int b = tid; b < 1024; b += kStepThreads) sh.hist[b] = 0u;
   __syncthreads();
   for (int i = tid; i < cnt; i += kStepThreads) {
     const uint32_t key = sh.keys[i];
-    if ((key >> 10) == pre22) atomicAdd(&sh.hist[0][key & 0x3ffu], 1u);
+    if ((key >> 10) == pre22) atomicAdd(&sh.hist[key & 0x3ffu], 1u);
   }
-  __syncthreads();
-  cluster_digit(cl, sh, 0, 1024, krem);
+  tm.exchange(sh, 1, 1024, 2);
+  digit_of(sh, sh.ghist, 1024, krem);
   const uint32_t T = (pre22 << 10) | sh.digit;
-  krem -= sh.above;  // ties of T to take, cluster-wide
-  // ---- emission: cluster scan of (count > T, count == T) over ranks
+  krem -= sh.above;  // ties of T to take, team-wide
+  // ---- emission: team scan of (count > T, count == T) over ranks
   uint32_t gt = 0, eq = 0;
   for (int i = tid; i < cnt; i += kStepThreads) {
     const uint32_t key = sh.keys[i];
@@ -298,18 +301,17 @@ __device__ void select_row(cg::cluster_group& cl, SelSmem& sh, const LycStepPara
   block_scan(gt, sh.warp_tot, tgt);
   block_scan(eq, sh.warp_tot, teq);
   if (tid == 0) {
-    sh.counts[0] = tgt;
-    sh.counts[1] = teq;
+    tm.cnt[tm.rank * 2] = tgt;
+    tm.cnt[tm.rank * 2 + 1] = teq;
   }
-  cl.sync();
+  tm.barrier(3);
   uint32_t base = 0, eqb = 0;
-  for (int c = 0; c < rank; ++c) {
-    const uint32_t* rc = cl.map_shared_rank(sh.counts, c);
-    const uint32_t cg_ = rc[0], ce = rc[1];
+  for (int c = 0; c < tm.rank; ++c) {
+    const uint32_t cg_ = __ldcg(tm.cnt + 2 * c), ce = __ldcg(tm.cnt + 2 * c + 1);
     base += cg_ + (krem > eqb ? min(ce, krem - eqb) : 0u);
     eqb += ce;
   }
-  const uint32_t take_eq = krem > eqb ? min(sh.counts[1], krem - eqb) : 0u;
+  const uint32_t take_eq = krem > eqb ? min(teq, krem - eqb) : 0u;
   uint32_t run_gt = 0, run_eq = 0;
   constexpr int kPer = 4;
   for (int b0 = 0; b0 < cnt; b0 += kStepThreads * kPer) {
@@ -339,11 +341,7 @@ __device__ void select_row(cg::cluster_group& cl, SelSmem& sh, const LycStepPara
     run_gt += tot & 0xffffu;
     run_eq += tot >> 16;
   }
-  // reset the fused first-pass histogram for its next use (all CTAs read it
-  // before the cl.sync of pass 1)
-  if (h1 && rank == 0)
-    for (int b = tid; b < LYC_BINS; b += kStepThreads) const_cast<uint32_t*>(h1)[b] = 0u;
-  cl.sync();  // remote reads of counts / hist done before the next row reuses them
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------- kernel
@@ -364,37 +362,42 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
   constexpr int esz = (int)sizeof(T);
 
   if (cta >= p.n_ctas) {
-    // ======================== selection cluster ========================
-    cg::cluster_group cl = cg::this_cluster();
+    // ======================== selection team ========================
     SelSmem& sh = *reinterpret_cast<SelSmem*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    const int sc = (cta - p.n_ctas) / kSelCluster;
-    const int n_sc = p.n_sel_ctas / kSelCluster;
+    const int sid = cta - p.n_ctas;
+    const int team = sid / kTeam;
+    const int n_teams = p.n_sel_ctas / kTeam;
+    Team tm;
+    tm.rank = sid % kTeam;
+    tm.target = epoch1 * (uint32_t)kTeam;
+    tm.xch = p.sel_xch + (size_t)team * (2 * kTeam * LYC_BINS + 64);
+    tm.cnt = tm.xch + 2 * kTeam * LYC_BINS;
     for (int l = 0; l < p.n_layers; ++l) {
       const LycLayerDesc L = p.layers[l];
       if (L.n_sel == 0 || p.sel_mode == SEL_NONE) continue;
       if (threadIdx.x == 0) {
         spin_until(LYC_CTR(p.ctr, l, CTR_ATTN), t_attn);
         __threadfence();
-        stamp(p, l, EV_SEL0, cta - p.n_ctas);
+        stamp(p, l, EV_SEL0, sid);
       }
       __syncthreads();
-      for (int r = sc; r < L.n_sel; r += n_sc) {
+      for (int r = team; r < L.n_sel; r += n_teams) {
         uint32_t* kg = p.sel_keys + ((int64_t)(l & 1) * p.max_sel + r) * p.sel_stride;
-        const uint32_t* h1 = p.sel_mode == SEL_TOKEN_KEYS
-                                 ? p.hist + ((int64_t)(l & 1) * p.max_sel + r) * LYC_BINS
-                                 : nullptr;
+        uint32_t* h1 = p.sel_mode == SEL_TOKEN_KEYS
+                           ? p.hist + ((int64_t)(l & 1) * p.max_sel + r) * LYC_BINS
+                           : nullptr;
         const int row = __ldg(L.sel_rows + r);
-        select_row(cl, sh, p, kg, h1, p.idx + (int64_t)row * p.idx_stride);
-        if (threadIdx.x == 0 && cl.block_rank() == 0 && p.idx_count) p.idx_count[row] = p.k_sel;
+        tm.bar = p.sel_bar + ((size_t)l * p.max_sel + r) * 64;
+        select_row(sh, tm, p, kg, h1, p.idx + (int64_t)row * p.idx_stride);
+        if (threadIdx.x == 0 && tm.rank == 0 && p.idx_count) p.idx_count[row] = p.k_sel;
       }
       __syncthreads();
       if (threadIdx.x == 0) {
-        stamp(p, l, EV_SELDONE, cta - p.n_ctas);
+        stamp(p, l, EV_SELDONE, sid);
         signal(LYC_CTR(p.ctr, l, CTR_SELDONE));
       }
     }
-    cl.sync();
   } else {
     // ======================== attention CTA ========================
     const AttnSmem<T, D> sm = AttnSmem<T, D>::carve(smem_raw);
@@ -407,8 +410,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
     }
     for (int b = threadIdx.x; b < LYC_BINS; b += kStepThreads) sm.hist[b] = 0u;
     __syncthreads();
-    const int bb = cta / p.n_splits, split = cta - bb * p.n_splits;
-    const int cell = bb * p.n_splits + split;
+    const int cell = cta;  // = b * n_splits + split
     if (warp < kConsumerWarps) {
       const int tid = threadIdx.x;
       int stage = 0;
@@ -507,22 +509,12 @@ static cudaError_t launch_step_t(const LycStepParams& p, cudaStream_t st) {
   cfg.blockDim = dim3(kStepThreads);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kSelCluster;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeCooperative;
-  attr[1].val.cooperative = 1;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, hybrid_step_kernel<T, D>, p);
-  if (e == cudaErrorInvalidValue || e == cudaErrorNotSupported) {
-    (void)cudaGetLastError();  // cooperative + cluster unsupported: co-residency is still
-    cfg.numAttrs = 1;          // guaranteed by 1 CTA/SM and grid <= #SMs (checked on host)
-    e = cudaLaunchKernelEx(&cfg, hybrid_step_kernel<T, D>, p);
-  }
-  return e;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, hybrid_step_kernel<T, D>, p);
 }
 
 cudaError_t launch_step(const LycStepParams& p, int dtype, int d, cudaStream_t st) {
@@ -552,6 +544,14 @@ int step_select_capacity(int dtype, int d) {
     default: return step_sel_capacity<float, 128>();
   }
 }
+
+// Global scratch of the selection teams (words): per team, 2 x kTeam
+// histogram exchange buffers plus the count exchange; per (layer, row), the
+// team-barrier counters (4 used, 64 words apart).
+size_t step_sel_xch_words(int n_sel_ctas) {
+  return (size_t)(n_sel_ctas / kTeam) * (2 * kTeam * LYC_BINS + 64);
+}
+size_t step_sel_bar_words(int n_layers, int max_sel) { return (size_t)n_layers * max_sel * 64; }
 
 bool step_supported(int dtype, int d) {
   return dtype == 1 ? (d == 64 || d == 128) : (d == 16 || d == 32 || d == 64 || d == 128);
