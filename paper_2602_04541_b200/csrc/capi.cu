@@ -881,7 +881,7 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
     // n_attn = S*B attention CTAs (a multiple of the 4-CTA cluster) plus two
     // 4-CTA selection clusters when the decoder selects.
     d->fused = lyc::step_supported(c.dtype, c.d_head) && std::getenv("LYC_NO_FUSED_STEP") == nullptr;
-    d->n_sel_ctas = d->fused && c.select_mode != LYC_SELECT_NONE ? 8 : 0;
+    d->n_sel_ctas = d->fused && c.select_mode != LYC_SELECT_NONE ? 16 : 0;  // 4 teams of 4
     if (c.num_splits > 0) {
       d->S = c.num_splits;
     } else if (d->fused) {
@@ -898,10 +898,10 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
     if (c.select_mode == LYC_SELECT_BLOCKS) {
       d->k_cap = c.policy_kind == LYC_POLICY_RATIO ? nb_cap
                                                    : std::min<int64_t>((c.top_k + 63) / 64, nb_cap);
-      d->sel_stride = nb_cap;
+      d->sel_stride = (nb_cap + 3) & ~(int64_t)3;  // 16-B aligned key rows
     } else {
       d->k_cap = c.policy_kind == LYC_POLICY_RATIO ? c.seq_cap : std::min<int64_t>(c.top_k, c.seq_cap);
-      d->sel_stride = c.seq_cap;
+      d->sel_stride = (c.seq_cap + 3) & ~(int64_t)3;
     }
     try {
       const size_t rows = (size_t)d->B * d->H;

@@ -169,7 +169,8 @@ struct SelSmem {
   uint32_t ghist[LYC_BINS];  // team-summed histogram
   uint32_t warp_tot[32];
   uint32_t digit, above;
-  uint32_t keys[1];          // this CTA's slice of the row's keys (capacity sel_cap)
+  uint64_t bar;              // completion of the slice's bulk copy
+  uint32_t keys[1];          // this CTA's slice of the row's keys (capacity sel_cap), 16-B aligned
 };
 
 // Block-wide inclusive scan (256 threads).
@@ -213,13 +214,26 @@ struct Team {
   // Publish the local histogram, barrier b, sum the team's histograms into ghist.
   __device__ __forceinline__ void exchange(SelSmem& sh, int buf, int nbins, int b) const {
     uint32_t* mine = xch + ((size_t)buf * kTeam + rank) * LYC_BINS;
+    __syncthreads();  // the local histogram's shared-memory atomics are complete
     for (int i = threadIdx.x; i < nbins; i += kStepThreads) mine[i] = sh.hist[i];
     barrier(b);
-    for (int i = threadIdx.x; i < nbins; i += kStepThreads) {
-      uint32_t s = 0;
+    // thread t sums bins [4t, 4t+4) (+1024) of every member: all loads in flight
+    const int nv = nbins / 4;
+    for (int v0 = 0; v0 < nv; v0 += kStepThreads) {
+      const int v = v0 + threadIdx.x;
+      uint4 part[kTeam];
 #pragma unroll
-      for (int c = 0; c < kTeam; ++c) s += __ldcg(xch + ((size_t)buf * kTeam + c) * LYC_BINS + i);
-      sh.ghist[i] = s;
+      for (int c = 0; c < kTeam; ++c)
+        part[c] = __ldcg(reinterpret_cast<const uint4*>(xch + ((size_t)buf * kTeam + c) * LYC_BINS) + v);
+      uint4 s = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int c = 0; c < kTeam; ++c) {
+        s.x += part[c].x;
+        s.y += part[c].y;
+        s.z += part[c].z;
+        s.w += part[c].w;
+      }
+      reinterpret_cast<uint4*>(sh.ghist)[v] = s;
     }
     __syncthreads();
   }
@@ -240,21 +254,46 @@ __device__ __forceinline__ void digit_of(SelSmem& sh, const uint32_t* h, int nbi
 // One row: the k largest of n keys (ties to the lower index), ascending,
 // into out[0..k).  h1 (token mode) holds the grid-wide first-pass histogram.
 __device__ void select_row(SelSmem& sh, const Team& tm, const LycStepParams& p, uint32_t* keys_g,
-                           uint32_t* h1, int32_t* out) {
+                           uint32_t* h1, int32_t* out, uint32_t& bar_phase, int l, int sid) {
   const int tid = threadIdx.x;
   const int n = p.n_keys;
   const int slice = ((n + kTeam - 1) / kTeam + 3) & ~3;
   const int lo = min(n, tm.rank * slice);
   const int cnt = max(0, min(slice, n - lo));
-  // this CTA's slice (block-mode keys are reset for their next use)
-  for (int i = tid; i < cnt; i += kStepThreads) {
-    sh.keys[i] = __ldcg(keys_g + lo + i);
-    if (p.sel_mode == SEL_BLOCK_KEYS) keys_g[lo + i] = 0u;
+  // this CTA's slice (lo and slice are multiples of 4): the 16-B aligned body
+  // by TMA bulk copies on one mbarrier, the < 4-key tail by plain loads
+  {
+    const int nv = cnt >> 2;
+    if (tid == 0 && nv > 0) {
+      fence_proxy_async();  // prior generic reads of keys[] before the async-proxy overwrite
+      mbar_arrive_expect_tx(&sh.bar, (uint32_t)nv * 16u);
+      constexpr int kChunk = 2048;  // 16-B vectors per bulk copy (32 KB)
+      for (int v = 0; v < nv; v += kChunk)
+        bulk_g2s(sh.keys + 4 * v, keys_g + lo + 4 * v, (uint32_t)min(kChunk, nv - v) * 16u,
+                 &sh.bar);
+    }
+    for (int i = (nv << 2) + tid; i < cnt; i += kStepThreads) sh.keys[i] = __ldcg(keys_g + lo + i);
+    if (nv > 0) {
+      mbar_wait(&sh.bar, bar_phase);
+      bar_phase ^= 1u;
+      if (tid == 0) stamp(p, l, EV_SEL0, sid);
+    }
+    __syncthreads();
+    if (p.sel_mode == SEL_BLOCK_KEYS) {
+      __syncthreads();
+      for (int i = tid; i < cnt; i += kStepThreads) keys_g[lo + i] = 0u;
+    }
   }
   uint32_t krem = (uint32_t)p.k_sel;
   // ---- pass 1 (bits 31..21)
   if (h1) {
-    for (int b = tid; b < LYC_BINS; b += kStepThreads) sh.ghist[b] = __ldcg(h1 + b);
+    const uint4* h = reinterpret_cast<const uint4*>(h1);
+    uint4* g = reinterpret_cast<uint4*>(sh.ghist);
+    uint4 buf[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) buf[q] = __ldcg(h + q * kStepThreads + tid);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) g[q * kStepThreads + tid] = buf[q];
     __syncthreads();
   } else {
     for (int b = tid; b < LYC_BINS; b += kStepThreads) sh.hist[b] = 0u;
@@ -273,6 +312,7 @@ __device__ void select_row(SelSmem& sh, const Team& tm, const LycStepParams& p, 
     if ((key >> 21) == d1) atomicAdd(&sh.hist[(key >> 10) & 0x7ffu], 1u);
   }
   tm.exchange(sh, 0, LYC_BINS, 1);  // also orders every member's read of h1 before its reset
+  if (tid == 0) stamp(p, l, EV_SEL1, sid);
   digit_of(sh, sh.ghist, LYC_BINS, krem);
   const uint32_t d2 = sh.digit;
   krem -= sh.above;
@@ -287,6 +327,7 @@ __device__ void select_row(SelSmem& sh, const Team& tm, const LycStepParams& p, 
     if ((key >> 10) == pre22) atomicAdd(&sh.hist[key & 0x3ffu], 1u);
   }
   tm.exchange(sh, 1, 1024, 2);
+  if (tid == 0) stamp(p, l, EV_SEL2, sid);
   digit_of(sh, sh.ghist, 1024, krem);
   const uint32_t T = (pre22 << 10) | sh.digit;
   krem -= sh.above;  // ties of T to take, team-wide
@@ -313,7 +354,7 @@ __device__ void select_row(SelSmem& sh, const Team& tm, const LycStepParams& p, 
   }
   const uint32_t take_eq = krem > eqb ? min(teq, krem - eqb) : 0u;
   uint32_t run_gt = 0, run_eq = 0;
-  constexpr int kPer = 4;
+  constexpr int kPer = 8;
   for (int b0 = 0; b0 < cnt; b0 += kStepThreads * kPer) {
     const int i0 = b0 + tid * kPer;
     uint32_t kv[kPer];
@@ -373,13 +414,18 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
     tm.target = epoch1 * (uint32_t)kTeam;
     tm.xch = p.sel_xch + (size_t)team * (2 * kTeam * LYC_BINS + 64);
     tm.cnt = tm.xch + 2 * kTeam * LYC_BINS;
+    if (threadIdx.x == 0) {
+      mbar_init(&sh.bar, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    uint32_t bar_phase = 0;
     for (int l = 0; l < p.n_layers; ++l) {
       const LycLayerDesc L = p.layers[l];
       if (L.n_sel == 0 || p.sel_mode == SEL_NONE) continue;
       if (threadIdx.x == 0) {
         spin_until(LYC_CTR(p.ctr, l, CTR_ATTN), t_attn);
         __threadfence();
-        stamp(p, l, EV_SEL0, sid);
       }
       __syncthreads();
       for (int r = team; r < L.n_sel; r += n_teams) {
@@ -389,7 +435,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
                            : nullptr;
         const int row = __ldg(L.sel_rows + r);
         tm.bar = p.sel_bar + ((size_t)l * p.max_sel + r) * 64;
-        select_row(sh, tm, p, kg, h1, p.idx + (int64_t)row * p.idx_stride);
+        select_row(sh, tm, p, kg, h1, p.idx + (int64_t)row * p.idx_stride, bar_phase, l, sid);
         if (threadIdx.x == 0 && tm.rank == 0 && p.idx_count) p.idx_count[row] = p.k_sel;
       }
       __syncthreads();
