@@ -28,8 +28,6 @@ cudaError_t launch_float_keys(const float* s, uint32_t* keys, int64_t n, cudaStr
 cudaError_t launch_step(const LycStepParams& p, int dtype, int d, cudaStream_t st);
 bool step_supported(int dtype, int d);
 int step_select_capacity(int dtype, int d);
-size_t step_sel_xch_words(int n_sel_ctas);
-size_t step_sel_bar_words(int n_layers, int max_sel);
 }  // namespace lyc
 
 namespace {
@@ -463,9 +461,7 @@ struct lyc_decoder {
   uint32_t* sel_keys = nullptr; // [2][B*H][sel_stride]
   int64_t sel_stride = 0;
   uint32_t* hist = nullptr;     // [2][B*H][LYC_BINS] fused first-pass histograms
-  int n_sel_ctas = 0;           // fused mode: selection CTAs (teams of 4)
-  uint32_t* sel_xch = nullptr;  // selection-team exchange buffers
-  uint32_t* sel_bar = nullptr;  // selection-team barrier counters
+  int n_sel_ctas = 0;           // fused mode: selection CTAs (one row at a time each)
   uint32_t* ctr = nullptr;      // [NL][CTR_PER_LAYER] + 2
   unsigned long long* trace = nullptr;  // optional step timeline [NL][8][n_ctas]
   float* part_o = nullptr;
@@ -730,9 +726,6 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
   // a new plan restarts the step counters (any previous step has completed:
   // the synchronous copy above serialises with the legacy stream)
   cuda_check(cudaMemset(d->ctr, 0, LYC_CTR_WORDS(d->NL) * 4), "memset counters");
-  if (d->sel_bar)
-    cuda_check(cudaMemset(d->sel_bar, 0,
-                          lyc::step_sel_bar_words(d->NL, d->B * d->H) * 4), "memset sel_bar");
   cuda_check(cudaDeviceSynchronize(), "sync");
   d->planned_seq = seq;
 }
@@ -804,8 +797,6 @@ void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, i
   p.sel_keys = d->sel_keys;
   p.sel_stride = d->sel_stride;
   p.hist = d->hist;
-  p.sel_xch = d->sel_xch;
-  p.sel_bar = d->sel_bar;
   p.ctr = d->ctr;
   p.idx = d->idx;
   p.idx_stride = d->k_cap;
@@ -881,16 +872,18 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
     // n_attn = S*B attention CTAs (a multiple of the 4-CTA cluster) plus two
     // 4-CTA selection clusters when the decoder selects.
     d->fused = lyc::step_supported(c.dtype, c.d_head) && std::getenv("LYC_NO_FUSED_STEP") == nullptr;
-    d->n_sel_ctas = d->fused && c.select_mode != LYC_SELECT_NONE ? 16 : 0;  // 4 teams of 4
+    // selection CTAs: one row (b, retrieval head) at a time each
+    const char* env_sel = std::getenv("LYC_SEL_CTAS");
+    const int want_sel = env_sel ? std::max(1, std::atoi(env_sel)) : 8;
+    d->n_sel_ctas = d->fused && c.select_mode != LYC_SELECT_NONE ? want_sel : 0;
     if (c.num_splits > 0) {
       d->S = c.num_splits;
     } else if (d->fused) {
       d->S = std::max(1, (sms - d->n_sel_ctas) / d->B);
-      while (d->S > 1 && (d->S * d->B) % 4) --d->S;
     } else {
       d->S = std::max(1, sms / d->B);
     }
-    if (d->fused && ((d->S * d->B) % 4 != 0 || d->S * d->B + d->n_sel_ctas > sms)) {
+    if (d->fused && d->S * d->B + d->n_sel_ctas > sms) {
       d->fused = false;
       d->n_sel_ctas = 0;
     }
@@ -913,13 +906,6 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
       cuda_check(cudaMemset(d->sel_keys, 0, 2 * rows * d->sel_stride * 4), "memset");
       cuda_check(cudaMalloc(&d->hist, 2 * rows * LYC_BINS * 4), "cudaMalloc hist");
       cuda_check(cudaMemset(d->hist, 0, 2 * rows * LYC_BINS * 4), "memset");
-      if (d->n_sel_ctas) {
-        const size_t xw = lyc::step_sel_xch_words(d->n_sel_ctas);
-        const size_t bw = lyc::step_sel_bar_words(d->NL, (int)rows);
-        cuda_check(cudaMalloc(&d->sel_xch, xw * 4), "cudaMalloc sel_xch");
-        cuda_check(cudaMalloc(&d->sel_bar, bw * 4), "cudaMalloc sel_bar");
-        cuda_check(cudaMemset(d->sel_bar, 0, bw * 4), "memset");
-      }
       cuda_check(cudaMalloc(&d->ctr, LYC_CTR_WORDS(d->NL) * 4), "cudaMalloc ctr");
       cuda_check(cudaMemset(d->ctr, 0, LYC_CTR_WORDS(d->NL) * 4), "memset");
     } catch (...) {
@@ -941,8 +927,6 @@ int lyc_decoder_destroy(lyc_decoder* d) {
   free_dev(d->idx_count);
   free_dev(d->sel_keys);
   free_dev(d->hist);
-  free_dev(d->sel_xch);
-  free_dev(d->sel_bar);
   free_dev(d->ctr);
   free_dev(d->trace);
   free_dev(d->part_o);

@@ -150,8 +150,6 @@ struct LycStepParams {
   int64_t sel_stride;
   uint32_t* hist;            // [2 parity][max_sel][LYC_BINS] fused first-pass histograms
   uint32_t* ctr;             // LYC_CTR counters: [n_layers][CTR_PER_LAYER], then epoch, exits
-  uint32_t* sel_xch;         // selection-team histogram / count exchange (step.cu)
-  uint32_t* sel_bar;         // selection-team barrier counters [n_layers][max_sel][64]
   int32_t* idx;              // index cache [B*H][idx_stride]
   int64_t idx_stride;
   int32_t* idx_count;        // [B*H]

@@ -14,15 +14,15 @@
 //                        previous layer (its K/V row is produced after it);
 //   warps 6-7 epilogue   the split-KV LSE merge of layer l (kernel_sim.hpp:
 //                        205-225), spread over every attention CTA.
-// The last n_sel_ctas CTAs form SELECTION TEAMS of 4 (Algorithm 2's pooling
-// applied to the selection): after layer l's attention, a team computes for
-// each of its retrieval heads args_top_k over the pooled-query keys
+// The last n_sel_ctas CTAs are SELECTION CTAs (Algorithm 2's pooling applied
+// to the selection): after layer l's attention, each computes for its share of
+// the layer's retrieval heads args_top_k over the pooled-query keys
 // (attention.hpp:108-123: the k largest, ties to the lower index, ascending)
-// as an exact radix select.  The consumers already produced the first 11-bit
-// histogram while scoring; each team CTA holds a quarter of the keys in
-// shared memory; two more passes exchange 2048-bin histograms through global
-// memory behind per-row team barriers; an ordered compaction writes the
-// index cache.  Selection runs concurrently with the next layer's attention.
+// as an exact radix select that needs no inter-CTA synchronisation: the
+// consumers already produced the first 11-bit histogram while scoring, one
+// TMA-pipelined pass over the keys builds an "above the boundary bin" bitmap
+// plus the boundary-bin candidates, and the rest runs in shared memory.
+// Selection runs concurrently with the next layer's attention.
 // Grid-wide coordination uses monotonic counters in global memory (each step
 // adds the number of participating CTAs); the launch is cooperative, so every
 // CTA is co-resident.
@@ -33,7 +33,6 @@ namespace lyc {
 constexpr int kEpiWarps = 2;
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kStepThreads = (kConsumerWarps + kProducerWarps + kEpiWarps) * 32;
-constexpr int kTeam = 4;  // CTAs per selection team
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
@@ -163,14 +162,41 @@ __device__ __forceinline__ void find_digit(const uint32_t* h, int nbins, uint32_
   above = __shfl_sync(0xffffffffu, a, src_lane);
 }
 
-// Shared memory of a selection CTA (carved from the same dynamic allocation).
-struct SelSmem {
-  uint32_t hist[LYC_BINS];   // this CTA's pass histogram
-  uint32_t ghist[LYC_BINS];  // team-summed histogram
+// ---- selection CTA: one row at a time, entirely on-chip after one key stream
+constexpr int kChunkKeys = 8192;  // keys per streamed chunk (32 KB, one TMA bulk copy)
+constexpr int kRing = 3;          // chunks in flight
+
+struct SelHdr {
+  uint32_t hist[LYC_BINS];
   uint32_t warp_tot[32];
+  uint64_t bars[kRing];
   uint32_t digit, above;
-  uint64_t bar;              // completion of the slice's bulk copy
-  uint32_t keys[1];          // this CTA's slice of the row's keys (capacity sel_cap), 16-B aligned
+};
+
+// Dynamic layout: ring | header | bitmap[nwords] | cand keys[cap] | cand idx[cap]
+struct SelSmem {
+  uint32_t (*ring)[kChunkKeys];
+  SelHdr* h;
+  uint32_t* bitmap;  // bit i: key i selected
+  uint32_t* ckey;    // boundary-bin candidates, index order
+  uint32_t* cidx;
+  int cap;
+
+  __device__ static SelSmem carve(uint8_t* raw, int total_bytes, int nwords) {
+    SelSmem s;
+    uint8_t* base = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const int avail = total_bytes - (int)(base - raw);
+    s.ring = reinterpret_cast<uint32_t(*)[kChunkKeys]>(base);
+    s.h = reinterpret_cast<SelHdr*>(base + kRing * kChunkKeys * 4);
+    s.bitmap = reinterpret_cast<uint32_t*>(s.h + 1);
+    uint32_t* c = s.bitmap + ((nwords + 3) & ~3);
+    const int used = (int)(reinterpret_cast<uint8_t*>(c) - base);
+    s.cap = max(0, (avail - used) / 8);
+    s.ckey = c;
+    s.cidx = c + s.cap;
+    return s;
+  }
 };
 
 // Block-wide inclusive scan (256 threads).
@@ -196,195 +222,217 @@ __device__ __forceinline__ uint32_t block_scan(uint32_t v, uint32_t* warp_tot, u
   return v + before;
 }
 
-struct Team {
-  uint32_t* bar;        // this row's barrier counters (kTeam arrivals each per step)
-  uint32_t* xch;        // [2][kTeam][LYC_BINS] histogram exchange buffers of this team
-  uint32_t* cnt;        // [kTeam][2] count exchange
-  uint32_t target;      // epoch1 * kTeam
-  int rank;
-
-  __device__ __forceinline__ void barrier(int b) const {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      signal(bar + b * 16);
-      spin_until(bar + b * 16, target);
-    }
-    __syncthreads();
-  }
-  // Publish the local histogram, barrier b, sum the team's histograms into ghist.
-  __device__ __forceinline__ void exchange(SelSmem& sh, int buf, int nbins, int b) const {
-    uint32_t* mine = xch + ((size_t)buf * kTeam + rank) * LYC_BINS;
-    __syncthreads();  // the local histogram's shared-memory atomics are complete
-    for (int i = threadIdx.x; i < nbins; i += kStepThreads) mine[i] = sh.hist[i];
-    barrier(b);
-    // thread t sums bins [4t, 4t+4) (+1024) of every member: all loads in flight
-    const int nv = nbins / 4;
-    for (int v0 = 0; v0 < nv; v0 += kStepThreads) {
-      const int v = v0 + threadIdx.x;
-      uint4 part[kTeam];
-#pragma unroll
-      for (int c = 0; c < kTeam; ++c)
-        part[c] = __ldcg(reinterpret_cast<const uint4*>(xch + ((size_t)buf * kTeam + c) * LYC_BINS) + v);
-      uint4 s = make_uint4(0, 0, 0, 0);
-#pragma unroll
-      for (int c = 0; c < kTeam; ++c) {
-        s.x += part[c].x;
-        s.y += part[c].y;
-        s.z += part[c].z;
-        s.w += part[c].w;
-      }
-      reinterpret_cast<uint4*>(sh.ghist)[v] = s;
-    }
-    __syncthreads();
-  }
-};
-
-__device__ __forceinline__ void digit_of(SelSmem& sh, const uint32_t* h, int nbins, uint32_t krem) {
+__device__ __forceinline__ void digit_of(SelHdr* h, int nbins, uint32_t krem) {
   if (threadIdx.x < 32) {
     uint32_t d, a;
-    find_digit(h, nbins, krem, d, a, threadIdx.x);
+    find_digit(h->hist, nbins, krem, d, a, threadIdx.x);
     if (threadIdx.x == 0) {
-      sh.digit = d;
-      sh.above = a;
+      h->digit = d;
+      h->above = a;
     }
   }
   __syncthreads();
+}
+
+// Streams keys[0, n) through the TMA ring; f(base, chunk, cnt) runs on every
+// thread for each chunk in order and must not read the chunk after returning.
+// `phases` holds the per-slot mbarrier parities (persistent across calls).
+template <typename F>
+__device__ __forceinline__ void stream_keys(const SelSmem& sh, const uint32_t* keys, int n,
+                                            uint32_t& phases, F&& f) {
+  const int nck = (n + kChunkKeys - 1) / kChunkKeys;
+  auto issue = [&](int c) {
+    const int cnt = min(kChunkKeys, n - c * kChunkKeys);
+    const uint32_t bytes = (uint32_t)((cnt + 3) & ~3) * 4u;  // key rows are padded to 4
+    uint64_t* bar = &sh.h->bars[c % kRing];
+    mbar_arrive_expect_tx(bar, bytes);
+    bulk_g2s(sh.ring[c % kRing], keys + (size_t)c * kChunkKeys, bytes, bar);
+  };
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fence_proxy_async();  // earlier generic reads of the ring precede its async overwrite
+    for (int c = 0; c < min(kRing, nck); ++c) issue(c);
+  }
+  for (int c = 0; c < nck; ++c) {
+    const int slot = c % kRing;
+    mbar_wait(&sh.h->bars[slot], (phases >> slot) & 1u);
+    phases ^= 1u << slot;
+    f(c * kChunkKeys, sh.ring[slot], min(kChunkKeys, n - c * kChunkKeys));
+    __syncthreads();
+    if (threadIdx.x == 0 && c + kRing < nck) {
+      fence_proxy_async();
+      issue(c + kRing);
+    }
+  }
 }
 
 // One row: the k largest of n keys (ties to the lower index), ascending,
-// into out[0..k).  h1 (token mode) holds the grid-wide first-pass histogram.
-__device__ void select_row(SelSmem& sh, const Team& tm, const LycStepParams& p, uint32_t* keys_g,
-                           uint32_t* h1, int32_t* out, uint32_t& bar_phase, int l, int sid) {
+// into out[0..k).  h1 (token mode) is the grid-wide first-pass histogram
+// (bits 31..21) built by the attention consumers; otherwise it is computed
+// here.  The radix descends until the boundary bin fits the candidate store
+// (normally right after pass 1); ONE streaming pass then classifies every key:
+// above the boundary prefix -> bitmap bit, inside it -> candidate (key, index)
+// in index order.  The remaining radix passes run on the candidates in shared
+// memory, the selected candidates join the bitmap, and a popcount scan of the
+// bitmap emits the indices in ascending order.
+__device__ void select_row(uint8_t* smem_raw, int smem_bytes, const LycStepParams& p,
+                           uint32_t* keys_g, uint32_t* h1, int32_t* out, uint32_t& phases, int l,
+                           int sid) {
   const int tid = threadIdx.x;
   const int n = p.n_keys;
-  const int slice = ((n + kTeam - 1) / kTeam + 3) & ~3;
-  const int lo = min(n, tm.rank * slice);
-  const int cnt = max(0, min(slice, n - lo));
-  // this CTA's slice (lo and slice are multiples of 4): the 16-B aligned body
-  // by TMA bulk copies on one mbarrier, the < 4-key tail by plain loads
-  {
-    const int nv = cnt >> 2;
-    if (tid == 0 && nv > 0) {
-      fence_proxy_async();  // prior generic reads of keys[] before the async-proxy overwrite
-      mbar_arrive_expect_tx(&sh.bar, (uint32_t)nv * 16u);
-      constexpr int kChunk = 2048;  // 16-B vectors per bulk copy (32 KB)
-      for (int v = 0; v < nv; v += kChunk)
-        bulk_g2s(sh.keys + 4 * v, keys_g + lo + 4 * v, (uint32_t)min(kChunk, nv - v) * 16u,
-                 &sh.bar);
-    }
-    for (int i = (nv << 2) + tid; i < cnt; i += kStepThreads) sh.keys[i] = __ldcg(keys_g + lo + i);
-    if (nv > 0) {
-      mbar_wait(&sh.bar, bar_phase);
-      bar_phase ^= 1u;
-      if (tid == 0) stamp(p, l, EV_SEL0, sid);
-    }
-    __syncthreads();
-    if (p.sel_mode == SEL_BLOCK_KEYS) {
-      __syncthreads();
-      for (int i = tid; i < cnt; i += kStepThreads) keys_g[lo + i] = 0u;
-    }
-  }
+  const int nwords = (n + 31) / 32;
+  const SelSmem sh = SelSmem::carve(smem_raw, smem_bytes, nwords);
+  SelHdr* H = sh.h;
   uint32_t krem = (uint32_t)p.k_sel;
   // ---- pass 1 (bits 31..21)
   if (h1) {
-    const uint4* h = reinterpret_cast<const uint4*>(h1);
-    uint4* g = reinterpret_cast<uint4*>(sh.ghist);
+    const uint4* src = reinterpret_cast<const uint4*>(h1);
     uint4 buf[2];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) buf[q] = __ldcg(h + q * kStepThreads + tid);
+    for (int q = 0; q < 2; ++q) buf[q] = __ldcg(src + q * kStepThreads + tid);
 #pragma unroll
-    for (int q = 0; q < 2; ++q) g[q * kStepThreads + tid] = buf[q];
+    for (int q = 0; q < 2; ++q) reinterpret_cast<uint4*>(H->hist)[q * kStepThreads + tid] = buf[q];
     __syncthreads();
   } else {
-    for (int b = tid; b < LYC_BINS; b += kStepThreads) sh.hist[b] = 0u;
-    __syncthreads();
-    for (int i = tid; i < cnt; i += kStepThreads) atomicAdd(&sh.hist[sh.keys[i] >> 21], 1u);
-    tm.exchange(sh, 1, LYC_BINS, 0);
+    for (int b = tid; b < LYC_BINS; b += kStepThreads) H->hist[b] = 0u;
+    stream_keys(sh, keys_g, n, phases, [&](int, const uint32_t* ck, int cnt) {
+      for (int i = tid; i < cnt; i += kStepThreads) atomicAdd(&H->hist[ck[i] >> 21], 1u);
+    });
   }
-  digit_of(sh, sh.ghist, LYC_BINS, krem);
-  const uint32_t d1 = sh.digit;
-  krem -= sh.above;
-  // ---- pass 2 (bits 20..10) among keys whose top bits are d1
-  for (int b = tid; b < LYC_BINS; b += kStepThreads) sh.hist[b] = 0u;
-  __syncthreads();
-  for (int i = tid; i < cnt; i += kStepThreads) {
-    const uint32_t key = sh.keys[i];
-    if ((key >> 21) == d1) atomicAdd(&sh.hist[(key >> 10) & 0x7ffu], 1u);
+  digit_of(H, LYC_BINS, krem);
+  uint32_t P = H->digit;  // boundary prefix
+  int shift = 21;         // key >> shift is the prefix
+  krem -= H->above;
+  uint32_t n_eq = H->hist[P];
+  if (n_eq > (uint32_t)sh.cap) {  // rare: boundary bin too big -> descend on the stream
+    for (int b = tid; b < LYC_BINS; b += kStepThreads) H->hist[b] = 0u;
+    stream_keys(sh, keys_g, n, phases, [&](int, const uint32_t* ck, int cnt) {
+      for (int i = tid; i < cnt; i += kStepThreads)
+        if ((ck[i] >> 21) == P) atomicAdd(&H->hist[(ck[i] >> 10) & 0x7ffu], 1u);
+    });
+    digit_of(H, LYC_BINS, krem);
+    P = (P << 11) | H->digit;
+    shift = 10;
+    krem -= H->above;
+    n_eq = H->hist[H->digit];
+    if (n_eq > (uint32_t)sh.cap) {
+      for (int b = tid; b < 1024; b += kStepThreads) H->hist[b] = 0u;
+      stream_keys(sh, keys_g, n, phases, [&](int, const uint32_t* ck, int cnt) {
+        for (int i = tid; i < cnt; i += kStepThreads)
+          if ((ck[i] >> 10) == P) atomicAdd(&H->hist[ck[i] & 0x3ffu], 1u);
+      });
+      digit_of(H, 1024, krem);
+      P = (P << 10) | H->digit;  // the k-th key T itself; krem of its ties are taken
+      shift = 0;
+      krem -= H->above;
+    }
   }
-  tm.exchange(sh, 0, LYC_BINS, 1);  // also orders every member's read of h1 before its reset
-  if (tid == 0) stamp(p, l, EV_SEL1, sid);
-  digit_of(sh, sh.ghist, LYC_BINS, krem);
-  const uint32_t d2 = sh.digit;
-  krem -= sh.above;
-  if (h1 && tm.rank == 0)  // reset the fused histogram for its next use
-    for (int b = tid; b < LYC_BINS; b += kStepThreads) h1[b] = 0u;
-  // ---- pass 3 (bits 9..0)
-  const uint32_t pre22 = (d1 << 11) | d2;
-  for (int b = tid; b < 1024; b += kStepThreads) sh.hist[b] = 0u;
-  __syncthreads();
-  for (int i = tid; i < cnt; i += kStepThreads) {
-    const uint32_t key = sh.keys[i];
-    if ((key >> 10) == pre22) atomicAdd(&sh.hist[key & 0x3ffu], 1u);
-  }
-  tm.exchange(sh, 1, 1024, 2);
-  if (tid == 0) stamp(p, l, EV_SEL2, sid);
-  digit_of(sh, sh.ghist, 1024, krem);
-  const uint32_t T = (pre22 << 10) | sh.digit;
-  krem -= sh.above;  // ties of T to take, team-wide
-  // ---- emission: team scan of (count > T, count == T) over ranks
-  uint32_t gt = 0, eq = 0;
-  for (int i = tid; i < cnt; i += kStepThreads) {
-    const uint32_t key = sh.keys[i];
-    gt += key > T;
-    eq += key == T;
-  }
-  uint32_t tgt, teq;
-  block_scan(gt, sh.warp_tot, tgt);
-  block_scan(eq, sh.warp_tot, teq);
-  if (tid == 0) {
-    tm.cnt[tm.rank * 2] = tgt;
-    tm.cnt[tm.rank * 2 + 1] = teq;
-  }
-  tm.barrier(3);
-  uint32_t base = 0, eqb = 0;
-  for (int c = 0; c < tm.rank; ++c) {
-    const uint32_t cg_ = __ldcg(tm.cnt + 2 * c), ce = __ldcg(tm.cnt + 2 * c + 1);
-    base += cg_ + (krem > eqb ? min(ce, krem - eqb) : 0u);
-    eqb += ce;
-  }
-  const uint32_t take_eq = krem > eqb ? min(teq, krem - eqb) : 0u;
-  uint32_t run_gt = 0, run_eq = 0;
-  constexpr int kPer = 8;
-  for (int b0 = 0; b0 < cnt; b0 += kStepThreads * kPer) {
-    const int i0 = b0 + tid * kPer;
-    uint32_t kv[kPer];
-    uint32_t g = 0, e = 0;
+  if (tid == 0) stamp(p, l, EV_SEL0, sid);
+  // ---- classify every key against the prefix P
+  uint32_t run = 0;  // candidates (or ties of T) so far, index order
+  stream_keys(sh, keys_g, n, phases, [&](int base, const uint32_t* ck, int cnt) {
+    // thread t owns 32 consecutive keys = one bitmap word, read as 8 rotated
+    // 16-B vectors (conflict-free)
+    uint32_t word = 0, eqm = 0;
+    const int k0 = tid * 32;
 #pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-      const bool ok = i0 + q < cnt;
-      kv[q] = ok ? sh.keys[i0 + q] : 0u;
-      g += ok && kv[q] > T;
-      e += ok && kv[q] == T;
+    for (int q = 0; q < 8; ++q) {
+      const int qq = (q + tid) & 7;
+      const uint4 v = reinterpret_cast<const uint4*>(ck + k0)[qq];
+      const uint32_t kv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = qq * 4 + e;
+        const bool ok = k0 + j < cnt;
+        const uint32_t pre = shift ? kv[e] >> shift : kv[e];
+        word |= (ok && pre > P) ? (1u << j) : 0u;
+        eqm |= (ok && pre == P) ? (1u << j) : 0u;
+      }
     }
     uint32_t tot;
-    const uint32_t mine = (e << 16) | g;
-    const uint32_t incl = block_scan(mine, sh.warp_tot, tot);
-    uint32_t gb = run_gt + ((incl - mine) & 0xffffu);
-    uint32_t eb = run_eq + ((incl - mine) >> 16);
-#pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-      if (i0 + q >= cnt) break;
-      const bool is_gt = kv[q] > T, is_eq = kv[q] == T;
-      if (is_gt || (is_eq && eb < take_eq)) out[base + gb + min(eb, take_eq)] = lo + i0 + q;
-      gb += is_gt;
-      eb += is_eq;
+    const uint32_t c = __popc(eqm);
+    const uint32_t incl = block_scan(c, H->warp_tot, tot);
+    uint32_t pos = run + incl - c;
+    if (shift == 0) {  // ties of T: take the first krem by index
+      while (eqm) {
+        const int j = __ffs(eqm) - 1;
+        eqm &= eqm - 1;
+        if (pos < krem) word |= 1u << j;
+        ++pos;
+      }
+    } else {
+      while (eqm) {
+        const int j = __ffs(eqm) - 1;
+        eqm &= eqm - 1;
+        sh.ckey[pos] = ck[k0 + j];
+        sh.cidx[pos] = (uint32_t)(base + k0 + j);
+        ++pos;
+      }
     }
-    run_gt += tot & 0xffffu;
-    run_eq += tot >> 16;
+    if (k0 < cnt) sh.bitmap[base / 32 + tid] = word;
+    run += tot;
+  });
+  // ---- finish the radix on the candidates
+  if (shift > 0) {
+    const int nc = (int)run;
+    if (shift == 21) {
+      for (int b = tid; b < LYC_BINS; b += kStepThreads) H->hist[b] = 0u;
+      __syncthreads();
+      for (int i = tid; i < nc; i += kStepThreads)
+        atomicAdd(&H->hist[(sh.ckey[i] >> 10) & 0x7ffu], 1u);
+      __syncthreads();
+      digit_of(H, LYC_BINS, krem);
+      P = (P << 11) | H->digit;
+      krem -= H->above;
+    }
+    for (int b = tid; b < 1024; b += kStepThreads) H->hist[b] = 0u;
+    __syncthreads();
+    for (int i = tid; i < nc; i += kStepThreads)
+      if ((sh.ckey[i] >> 10) == P) atomicAdd(&H->hist[sh.ckey[i] & 0x3ffu], 1u);
+    __syncthreads();
+    digit_of(H, 1024, krem);
+    const uint32_t T = (P << 10) | H->digit;
+    krem -= H->above;  // ties of T to take (lowest indices first)
+    // selected candidates join the bitmap: key > T, or the first krem ties
+    uint32_t tie_run = 0;
+    for (int b0 = 0; b0 < nc; b0 += kStepThreads) {
+      const int i = b0 + tid;
+      const uint32_t key = i < nc ? sh.ckey[i] : 0u;
+      const bool is_eq = i < nc && key == T;
+      uint32_t tot;
+      const uint32_t incl = block_scan(is_eq ? 1u : 0u, H->warp_tot, tot);
+      const uint32_t rank = tie_run + incl - (is_eq ? 1u : 0u);
+      if (i < nc && (key > T || (is_eq && rank < krem)))
+        atomicOr(&sh.bitmap[sh.cidx[i] >> 5], 1u << (sh.cidx[i] & 31));
+      tie_run += tot;
+    }
+    __syncthreads();
   }
+  if (tid == 0) stamp(p, l, EV_SEL1, sid);
+  // ---- emit the set bits in ascending order
+  const int per = (nwords + kStepThreads - 1) / kStepThreads;
+  const int w0 = min(nwords, tid * per), w1 = min(nwords, w0 + per);
+  uint32_t cnt = 0;
+  for (int w = w0; w < w1; ++w) cnt += __popc(sh.bitmap[w]);
+  uint32_t tot;
+  uint32_t pos = block_scan(cnt, H->warp_tot, tot) - cnt;
+  for (int w = w0; w < w1; ++w) {
+    uint32_t m = sh.bitmap[w];
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      out[pos++] = w * 32 + j;
+    }
+  }
+  if (h1)  // reset the fused histogram for its next use
+    for (int b = tid; b < LYC_BINS; b += kStepThreads) h1[b] = 0u;
+  if (p.sel_mode == SEL_BLOCK_KEYS)  // block keys are max-folded: reset the row
+    for (int i = tid; i < n; i += kStepThreads) keys_g[i] = 0u;
+  if (tid == 0) stamp(p, l, EV_SEL2, sid);
   __syncthreads();
 }
 
+// ---------------------------------------------------------------- kernel
 // ---------------------------------------------------------------- kernel
 template <typename T, int D>
 __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __grid_constant__ LycStepParams p) {
@@ -403,23 +451,16 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
   constexpr int esz = (int)sizeof(T);
 
   if (cta >= p.n_ctas) {
-    // ======================== selection team ========================
-    SelSmem& sh = *reinterpret_cast<SelSmem*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+
+    // ======================== selection CTA ========================
     const int sid = cta - p.n_ctas;
-    const int team = sid / kTeam;
-    const int n_teams = p.n_sel_ctas / kTeam;
-    Team tm;
-    tm.rank = sid % kTeam;
-    tm.target = epoch1 * (uint32_t)kTeam;
-    tm.xch = p.sel_xch + (size_t)team * (2 * kTeam * LYC_BINS + 64);
-    tm.cnt = tm.xch + 2 * kTeam * LYC_BINS;
     if (threadIdx.x == 0) {
-      mbar_init(&sh.bar, 1);
+      SelHdr* H = SelSmem::carve(smem_raw, C::kSmem, 0).h;
+      for (int s = 0; s < kRing; ++s) mbar_init(&H->bars[s], 1);
       fence_mbar_init();
     }
     __syncthreads();
-    uint32_t bar_phase = 0;
+    uint32_t phases = 0;
     for (int l = 0; l < p.n_layers; ++l) {
       const LycLayerDesc L = p.layers[l];
       if (L.n_sel == 0 || p.sel_mode == SEL_NONE) continue;
@@ -428,15 +469,15 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
         __threadfence();
       }
       __syncthreads();
-      for (int r = team; r < L.n_sel; r += n_teams) {
+      for (int r = sid; r < L.n_sel; r += p.n_sel_ctas) {
         uint32_t* kg = p.sel_keys + ((int64_t)(l & 1) * p.max_sel + r) * p.sel_stride;
         uint32_t* h1 = p.sel_mode == SEL_TOKEN_KEYS
                            ? p.hist + ((int64_t)(l & 1) * p.max_sel + r) * LYC_BINS
                            : nullptr;
         const int row = __ldg(L.sel_rows + r);
-        tm.bar = p.sel_bar + ((size_t)l * p.max_sel + r) * 64;
-        select_row(sh, tm, p, kg, h1, p.idx + (int64_t)row * p.idx_stride, bar_phase, l, sid);
-        if (threadIdx.x == 0 && tm.rank == 0 && p.idx_count) p.idx_count[row] = p.k_sel;
+        select_row(smem_raw, C::kSmem, p, kg, h1, p.idx + (int64_t)row * p.idx_stride, phases, l,
+                   sid);
+        if (threadIdx.x == 0 && p.idx_count) p.idx_count[row] = p.k_sel;
       }
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -535,12 +576,6 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
 }
 
 template <typename T, int D>
-int step_sel_capacity() {  // keys a selection CTA keeps in shared memory
-  using C = AttnCfg<T, D>;
-  return (int)((C::kSmem - 1024 - (int)sizeof(SelSmem)) / 4);
-}
-
-template <typename T, int D>
 static cudaError_t launch_step_t(const LycStepParams& p, cudaStream_t st) {
   using C = AttnCfg<T, D>;
   static bool configured = false;
@@ -580,24 +615,7 @@ cudaError_t launch_step(const LycStepParams& p, int dtype, int d, cudaStream_t s
   return cudaErrorInvalidValue;
 }
 
-int step_select_capacity(int dtype, int d) {
-  if (dtype == 1) return d == 64 ? step_sel_capacity<__nv_bfloat16, 64>()
-                                 : step_sel_capacity<__nv_bfloat16, 128>();
-  switch (d) {
-    case 16: return step_sel_capacity<float, 16>();
-    case 32: return step_sel_capacity<float, 32>();
-    case 64: return step_sel_capacity<float, 64>();
-    default: return step_sel_capacity<float, 128>();
-  }
-}
-
-// Global scratch of the selection teams (words): per team, 2 x kTeam
-// histogram exchange buffers plus the count exchange; per (layer, row), the
-// team-barrier counters (4 used, 64 words apart).
-size_t step_sel_xch_words(int n_sel_ctas) {
-  return (size_t)(n_sel_ctas / kTeam) * (2 * kTeam * LYC_BINS + 64);
-}
-size_t step_sel_bar_words(int n_layers, int max_sel) { return (size_t)n_layers * max_sel * 64; }
+int step_select_capacity(int, int) { return 1 << 16; }  // keys per row / 4 (bitmap bound)
 
 bool step_supported(int dtype, int d) {
   return dtype == 1 ? (d == 64 || d == 128) : (d == 16 || d == 32 || d == 64 || d == 128);
