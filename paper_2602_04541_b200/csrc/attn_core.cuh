@@ -51,7 +51,7 @@ struct AttnCfg {
   static constexpr int kMergeBytes = kConsumerWarps * kMaxG * (D + 2) * 4;
   static constexpr int kQBytes = kE == 4 ? (kMaxG + 1) * D * 4 : 0;
   static constexpr int kMaxSmem = 232448 - 1024;   // 227 KB opt-in minus alignment slack
-  static constexpr int kExtraBytes = 4096;         // scratch of the step kernel's epilogue warps
+  static constexpr int kExtraBytes = 44 * 1024;    // step kernel's epilogue warps (selection items)
   static constexpr int kHistBytes = LYC_BINS * 4;  // per-CTA first-pass selection histogram
   static constexpr int kFixed = kMergeBytes + kQBytes + 512 + kExtraBytes + kHistBytes;
   static constexpr int kStagesRaw = (kMaxSmem - kFixed) / kStageBytes;
@@ -92,11 +92,20 @@ struct AttnSmem {
     s.qs = s.ml + kConsumerWarps * kMaxG * 2;
     s.full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(s.qs) + C::kQBytes);
     s.empty = s.full + C::kStages;
-    s.extra = reinterpret_cast<uint8_t*>(s.empty + C::kStages);
+    s.extra = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(s.empty + C::kStages) + 127) & ~static_cast<uintptr_t>(127));
     s.hist = reinterpret_cast<uint32_t*>(s.extra + C::kExtraBytes);
     return s;
   }
 };
+
+// Ring depth in use: fewer stages than the smem capacity keep fewer bytes in
+// flight per SM -- enough to saturate HBM without inflating the memory
+// system's queueing latency for the latency-bound work (merge, selection).
+template <typename C>
+__device__ __forceinline__ int ring_stages(const LycView& p) {
+  return (p.stages > 0 && p.stages < C::kStages) ? p.stages : C::kStages;
+}
 
 struct Tile {
   int32_t lo;            // first row (contiguous tiles)
@@ -217,7 +226,7 @@ __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMa
           }
           cp_async_mbar_arrive(&full[stage]);
         }
-        if (++stage == C::kStages) {
+        if (++stage == ring_stages<C>(p)) {
           stage = 0;
           phase ^= 1;
         }
@@ -438,7 +447,7 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[stage]);
-        if (++stage == C::kStages) {
+        if (++stage == ring_stages<C>(p)) {
           stage = 0;
           phase ^= 1;
         }
@@ -580,7 +589,7 @@ __device__ __forceinline__ void consume_units_f32(const LycView& p, const AttnSm
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[stage]);
-        if (++stage == C::kStages) {
+        if (++stage == ring_stages<C>(p)) {
           stage = 0;
           phase ^= 1;
         }

@@ -27,7 +27,8 @@ size_t topk_smem_bytes(int slice);
 cudaError_t launch_float_keys(const float* s, uint32_t* keys, int64_t n, cudaStream_t st);
 cudaError_t launch_step(const LycStepParams& p, int dtype, int d, cudaStream_t st);
 bool step_supported(int dtype, int d);
-int step_select_capacity(int dtype, int d);
+int64_t step_max_keys();
+int step_item_keys();
 }  // namespace lyc
 
 namespace {
@@ -461,7 +462,12 @@ struct lyc_decoder {
   uint32_t* sel_keys = nullptr; // [2][B*H][sel_stride]
   int64_t sel_stride = 0;
   uint32_t* hist = nullptr;     // [2][B*H][LYC_BINS] fused first-pass histograms
-  int n_sel_ctas = 0;           // fused mode: selection CTAs (one row at a time each)
+  uint32_t* sel_bitmap = nullptr;  // fused-mode pooled selection scratch (see LycStepParams)
+  int64_t bitmap_stride = 0;
+  uint32_t* sel_cand = nullptr;
+  uint32_t* sel_ccnt = nullptr;
+  uint32_t* sel_rowctr = nullptr;
+  int stages = 0;               // attention ring stages in use (0 = all; env LYC_STAGES)
   uint32_t* ctr = nullptr;      // [NL][CTR_PER_LAYER] + 2
   unsigned long long* trace = nullptr;  // optional step timeline [NL][8][n_ctas]
   float* part_o = nullptr;
@@ -587,12 +593,12 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
   if (seq > d->cfg.seq_cap) fail(LYC_EINVAL, "decode_step: seq_len exceeds seq_cap");
   if (!d->fused && seq > (int64_t)16 * 32768 && d->cfg.select_mode == LYC_SELECT_TOKENS)
     fail(LYC_ENOTSUP, "decode_step: token-mode selection supports seq_len <= 524288");
-  if (d->fused && d->n_sel_ctas > 0) {
-    // a selection cluster keeps a row's keys in shared memory
-    const int64_t nk = d->cfg.select_mode == LYC_SELECT_BLOCKS ? (seq + d->bs - 1) / d->bs : seq;
-    if (nk > 4LL * lyc::step_select_capacity(d->cfg.dtype, d->D)) {
+  if (d->fused && d->cfg.select_mode != LYC_SELECT_NONE) {
+    // pooled selection limits: <= 64 items per row; block keys in one item
+    const bool blk = d->cfg.select_mode == LYC_SELECT_BLOCKS;
+    const int64_t nk = blk ? (seq + d->bs - 1) / d->bs : seq;
+    if (nk > lyc::step_max_keys() || (blk && nk > lyc::step_item_keys())) {
       d->fused = false;
-      d->n_sel_ctas = 0;
       d->planned_seq = -1;
     }
   }
@@ -685,6 +691,7 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
     v.sel_mode = none ? SEL_NONE : blocks ? SEL_BLOCK_KEYS : SEL_TOKEN_KEYS;
     v.scale = d->cfg.scale;
     v.scale_log2 = d->cfg.scale * 1.4426950408889634f;
+    v.stages = d->stages;
     LycMergeParams& mp = ly.mp;
     std::memset(&mp, 0, sizeof(mp));
     mp.part_o = d->part_o;
@@ -726,6 +733,8 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
   // a new plan restarts the step counters (any previous step has completed:
   // the synchronous copy above serialises with the legacy stream)
   cuda_check(cudaMemset(d->ctr, 0, LYC_CTR_WORDS(d->NL) * 4), "memset counters");
+  if (d->sel_rowctr)
+    cuda_check(cudaMemset(d->sel_rowctr, 0, (size_t)d->NL * d->B * d->H * 16 * 4), "memset rowctr");
   cuda_check(cudaDeviceSynchronize(), "sync");
   d->planned_seq = seq;
 }
@@ -797,6 +806,11 @@ void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, i
   p.sel_keys = d->sel_keys;
   p.sel_stride = d->sel_stride;
   p.hist = d->hist;
+  p.sel_bitmap = d->sel_bitmap;
+  p.bitmap_stride = d->bitmap_stride;
+  p.sel_cand = d->sel_cand;
+  p.sel_ccnt = d->sel_ccnt;
+  p.sel_rowctr = d->sel_rowctr;
   p.ctr = d->ctr;
   p.idx = d->idx;
   p.idx_stride = d->k_cap;
@@ -808,7 +822,6 @@ void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, i
   p.k_sel = (int32_t)d->k_sel;
   p.n_splits = d->S;
   p.n_ctas = d->n_ctas();
-  p.n_sel_ctas = d->n_sel_ctas;
   p.seq_len = (int32_t)seq;
   p.block_size = d->bs;
   p.group = d->G;
@@ -817,6 +830,7 @@ void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, i
                                                          : SEL_TOKEN_KEYS;
   p.scale = d->cfg.scale;
   p.scale_log2 = d->cfg.scale * 1.4426950408889634f;
+  p.stages = d->stages;
   record(d, d->ev_pre, 0, st);
   cuda_check(lyc::launch_step(p, d->cfg.dtype, d->D, st), "step launch");
   record(d, d->ev_post, 0, st);
@@ -868,25 +882,12 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
     d->NL = c.n_layers;
     d->bs = 64;
     const int sms = num_sms();
-    // The persistent step kernel needs every CTA co-resident (1 CTA per SM):
-    // n_attn = S*B attention CTAs (a multiple of the 4-CTA cluster) plus two
-    // 4-CTA selection clusters when the decoder selects.
+    // The persistent step kernel needs every CTA co-resident: 1 CTA per SM,
+    // S*B <= #SMs.
     d->fused = lyc::step_supported(c.dtype, c.d_head) && std::getenv("LYC_NO_FUSED_STEP") == nullptr;
-    // selection CTAs: one row (b, retrieval head) at a time each
-    const char* env_sel = std::getenv("LYC_SEL_CTAS");
-    const int want_sel = env_sel ? std::max(1, std::atoi(env_sel)) : 8;
-    d->n_sel_ctas = d->fused && c.select_mode != LYC_SELECT_NONE ? want_sel : 0;
-    if (c.num_splits > 0) {
-      d->S = c.num_splits;
-    } else if (d->fused) {
-      d->S = std::max(1, (sms - d->n_sel_ctas) / d->B);
-    } else {
-      d->S = std::max(1, sms / d->B);
-    }
-    if (d->fused && d->S * d->B + d->n_sel_ctas > sms) {
-      d->fused = false;
-      d->n_sel_ctas = 0;
-    }
+    if (const char* env_st = std::getenv("LYC_STAGES")) d->stages = std::max(0, std::atoi(env_st));
+    d->S = c.num_splits > 0 ? c.num_splits : std::max(1, sms / d->B);
+    if (d->fused && d->S * d->B > sms) d->fused = false;
     const int64_t nb_cap = (c.seq_cap + d->bs - 1) / d->bs;
     if (c.select_mode == LYC_SELECT_BLOCKS) {
       d->k_cap = c.policy_kind == LYC_POLICY_RATIO ? nb_cap
@@ -906,6 +907,14 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
       cuda_check(cudaMemset(d->sel_keys, 0, 2 * rows * d->sel_stride * 4), "memset");
       cuda_check(cudaMalloc(&d->hist, 2 * rows * LYC_BINS * 4), "cudaMalloc hist");
       cuda_check(cudaMemset(d->hist, 0, 2 * rows * LYC_BINS * 4), "memset");
+      if (d->fused && c.select_mode != LYC_SELECT_NONE) {  // pooled-selection scratch
+        d->bitmap_stride = ((d->sel_stride + 31) / 32 + 3) & ~(int64_t)3;
+        cuda_check(cudaMalloc(&d->sel_bitmap, 2 * rows * d->bitmap_stride * 4), "cudaMalloc bitmap");
+        cuda_check(cudaMalloc(&d->sel_cand, 2 * rows * 2 * d->sel_stride * 4), "cudaMalloc cand");
+        cuda_check(cudaMalloc(&d->sel_ccnt, 2 * rows * 64 * 4), "cudaMalloc ccnt");
+        cuda_check(cudaMalloc(&d->sel_rowctr, (size_t)d->NL * rows * 16 * 4), "cudaMalloc rowctr");
+        cuda_check(cudaMemset(d->sel_rowctr, 0, (size_t)d->NL * rows * 16 * 4), "memset");
+      }
       cuda_check(cudaMalloc(&d->ctr, LYC_CTR_WORDS(d->NL) * 4), "cudaMalloc ctr");
       cuda_check(cudaMemset(d->ctr, 0, LYC_CTR_WORDS(d->NL) * 4), "memset");
     } catch (...) {
@@ -927,6 +936,10 @@ int lyc_decoder_destroy(lyc_decoder* d) {
   free_dev(d->idx_count);
   free_dev(d->sel_keys);
   free_dev(d->hist);
+  free_dev(d->sel_bitmap);
+  free_dev(d->sel_cand);
+  free_dev(d->sel_ccnt);
+  free_dev(d->sel_rowctr);
   free_dev(d->ctr);
   free_dev(d->trace);
   free_dev(d->part_o);

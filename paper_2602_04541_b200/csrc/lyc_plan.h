@@ -66,6 +66,7 @@ struct LycView {
   int32_t sel_mode;         // SEL_*
   float scale;              // softmax scale (1/sqrt(d))
   float scale_log2;         // scale * log2(e)
+  int32_t stages;           // ring stages in use (<= the kernel's capacity; 0 = all)
 };
 
 struct LycAttnParams {
@@ -149,6 +150,11 @@ struct LycStepParams {
   uint32_t* sel_keys;        // [2 parity][max_sel][sel_stride]
   int64_t sel_stride;
   uint32_t* hist;            // [2 parity][max_sel][LYC_BINS] fused first-pass histograms
+  uint32_t* sel_bitmap;      // [2 parity][max_sel][bitmap_stride] selected-key bitmaps
+  int64_t bitmap_stride;
+  uint32_t* sel_cand;        // [2 parity][max_sel][2][sel_stride] boundary-bin candidates
+  uint32_t* sel_ccnt;        // [2 parity][max_sel][64] candidates per item
+  uint32_t* sel_rowctr;      // [n_layers][max_sel][16] finished items per row (monotonic)
   uint32_t* ctr;             // LYC_CTR counters: [n_layers][CTR_PER_LAYER], then epoch, exits
   int32_t* idx;              // index cache [B*H][idx_stride]
   int64_t idx_stride;
@@ -159,12 +165,12 @@ struct LycStepParams {
   int32_t n_keys;            // selection candidates per row (seq_len or n_blocks)
   int32_t k_sel;             // ids kept per row (min(k, n_keys))
   int32_t n_splits;
-  int32_t n_ctas;            // attention CTAs = n_splits * batch (grid index 0..n_ctas-1)
-  int32_t n_sel_ctas;        // selection CTAs after them (4-CTA clusters)
+  int32_t n_ctas;            // CTAs = n_splits * batch (grid index = b * n_splits + split)
   int32_t seq_len;
   int32_t block_size;
   int32_t group;
   int32_t sel_mode;
   float scale;
   float scale_log2;
+  int32_t stages;            // attention ring stages in use (0 = all)
 };

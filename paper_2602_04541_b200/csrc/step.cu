@@ -1,7 +1,7 @@
 // step.cu -- the persistent decode-step kernel: every layer of one decode step
-// (decode_engine.hpp:109-151) in ONE launch, one CTA per SM.
+// (decode_engine.hpp:109-151) in ONE launch, one CTA per SM, all SMs.
 //
-// The first n_ctas CTAs of the 1-D grid are ATTENTION CTAs (256 threads):
+// Warp roles of every CTA (256 threads):
 //   warps 0-3 consumers  attention of this CTA's split of layer l
 //                        (attn_core.cuh); layer l+1 starts only after layer
 //                        l's outputs are final (device counter) -- the model's
@@ -12,20 +12,23 @@
 //                        whose index list comes from a selection wait for it;
 //                        the tile holding the current token waits for the
 //                        previous layer (its K/V row is produced after it);
-//   warps 6-7 epilogue   the split-KV LSE merge of layer l (kernel_sim.hpp:
-//                        205-225), spread over every attention CTA.
-// The last n_sel_ctas CTAs are SELECTION CTAs (Algorithm 2's pooling applied
-// to the selection): after layer l's attention, each computes for its share of
-// the layer's retrieval heads args_top_k over the pooled-query keys
-// (attention.hpp:108-123: the k largest, ties to the lower index, ascending)
-// as an exact radix select that needs no inter-CTA synchronisation: the
-// consumers already produced the first 11-bit histogram while scoring, one
-// TMA-pipelined pass over the keys builds an "above the boundary bin" bitmap
-// plus the boundary-bin candidates, and the rest runs in shared memory.
-// Selection runs concurrently with the next layer's attention.
+//   warps 6-7 epilogue   after the whole grid finished layer l's attention:
+//                        (a) the split-KV LSE merge (kernel_sim.hpp:205-225);
+//                        (b) the selection of the layer's retrieval heads --
+//                            args_top_k over the pooled-query keys
+//                            (attention.hpp:108-123: the k largest, ties to the
+//                            lower index, ascending) as an exact radix select.
+//                        Both are pooled over ALL CTAs (Algorithm 2's workload
+//                        pooling applied to the epilogue): merge tasks and
+//                        32 KB key "items" are dealt round-robin.
+// Selection per retrieval head: the consumers built the first 11-bit
+// histogram while scoring; every item classifies its 8192 keys against the
+// boundary bin (bitmap word per 32 keys, boundary-bin candidates in index
+// order); the CTA that completes a head's LAST item finishes the radix on the
+// candidates, adds the selected ones to the bitmap and emits the set bits in
+// ascending order into the index cache.  No grid barrier: a per-head counter.
 // Grid-wide coordination uses monotonic counters in global memory (each step
-// adds the number of participating CTAs); the launch is cooperative, so every
-// CTA is co-resident.
+// adds a fixed amount); the launch is cooperative, so every CTA is co-resident.
 #include "attn_core.cuh"
 
 namespace lyc {
@@ -33,6 +36,7 @@ namespace lyc {
 constexpr int kEpiWarps = 2;
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kStepThreads = (kConsumerWarps + kProducerWarps + kEpiWarps) * 32;
+constexpr int kItemKeys = 8192;  // keys per selection item (32 KB, one TMA bulk copy)
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
@@ -61,19 +65,21 @@ __device__ __forceinline__ void signal(uint32_t* ctr) {
   atomicAdd(ctr, 1u);
 }
 
-// Debug timeline: %globaltimer (ns) of event ev of layer l on slot `who`.
+__device__ __forceinline__ void epi_bar() { group_bar(2, kEpiThreads); }
+
+// Debug timeline: %globaltimer (ns) of event ev of layer l on CTA `cta`.
 enum { EV_CONS_BEGIN = 0, EV_CONS_END, EV_EPI_ATTN, EV_MERGE, EV_SEL0, EV_SEL1, EV_SEL2, EV_SELDONE };
-__device__ __forceinline__ void stamp(const LycStepParams& p, int l, int ev, int who) {
+__device__ __forceinline__ void stamp(const LycStepParams& p, int l, int ev, int cta) {
   if (p.trace) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.trace[((size_t)l * 8 + ev) * p.n_ctas + who] = t;
+    p.trace[((size_t)l * 8 + ev) * p.n_ctas + cta] = t;
   }
 }
 
 struct StepWaits {
-  const uint32_t* ctr;
-  uint32_t t_attn, t_sel;
+  const LycStepParams* p;
+  uint32_t epoch1;
   int layer;
   int pt;
   __device__ __forceinline__ void wait(const uint32_t* c, uint32_t target) const {
@@ -81,10 +87,11 @@ struct StepWaits {
     group_bar(3, kProducerThreads);
   }
   __device__ __forceinline__ void unit(const LycSlot& s) const {
-    if (s.dep >= 0) wait(LYC_CTR(ctr, s.dep, CTR_SELDONE), t_sel);
+    if (s.dep >= 0)  // every retrieval head of layer dep finished its selection
+      wait(LYC_CTR(p->ctr, s.dep, CTR_SELDONE), epoch1 * (uint32_t)p->layers[s.dep].n_sel);
   }
   __device__ __forceinline__ void last_tile() const {
-    if (layer > 0) wait(LYC_CTR(ctr, layer - 1, CTR_MERGE), t_attn);
+    if (layer > 0) wait(LYC_CTR(p->ctr, layer - 1, CTR_MERGE), epoch1 * (uint32_t)p->n_ctas);
   }
 };
 
@@ -113,6 +120,7 @@ __device__ __forceinline__ LycView layer_view(const LycStepParams& p, const LycL
   v.sel_mode = p.sel_mode;
   v.scale = p.scale;
   v.scale_log2 = p.scale_log2;
+  v.stages = p.stages;
   return v;
 }
 
@@ -120,7 +128,8 @@ __device__ __forceinline__ LycView layer_view(const LycStepParams& p, const LycL
 // Warp-level search of a histogram (from the top bin down) for the bin that
 // holds the krem-th largest candidate.  Returns (digit, count above it).
 __device__ __forceinline__ void find_digit(const uint32_t* h, int nbins, uint32_t krem,
-                                           uint32_t& digit, uint32_t& above, int lane) {
+                                           uint32_t& digit, uint32_t& above, int lane,
+                                           bool global) {
   const int per = nbins / 32;  // 64 (11-bit) or 32 (10-bit) bins per lane
   const int hi = nbins - 1 - lane * per;  // lane owns bins hi, hi-1, ..., hi-per+1
   uint32_t cnt[64];
@@ -129,7 +138,7 @@ __device__ __forceinline__ void find_digit(const uint32_t* h, int nbins, uint32_
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
     if (q * 4 >= per) break;
-    const uint4 v = src[q];
+    const uint4 v = global ? __ldcg(src + q) : src[q];
     cnt[4 * q] = v.x;
     cnt[4 * q + 1] = v.y;
     cnt[4 * q + 2] = v.z;
@@ -162,408 +171,355 @@ __device__ __forceinline__ void find_digit(const uint32_t* h, int nbins, uint32_
   above = __shfl_sync(0xffffffffu, a, src_lane);
 }
 
-// ---- selection CTA: one row at a time, entirely on-chip after one key stream
-constexpr int kChunkKeys = 8192;  // keys per streamed chunk (32 KB, one TMA bulk copy)
-constexpr int kRing = 3;          // chunks in flight
-
-struct SelHdr {
+// Epilogue scratch (inside AttnSmem::extra, 44 KB).
+struct EpiSmem {
+  uint32_t keys[kItemKeys];  // one item's keys (TMA bulk destination)
   uint32_t hist[LYC_BINS];
-  uint32_t warp_tot[32];
-  uint64_t bars[kRing];
-  uint32_t digit, above;
+  uint32_t scan[64];
+  uint32_t seg[72];          // candidate segment starts (items <= 64) + total
+  uint64_t bar;
+  uint32_t digit, above, last, pad;
 };
 
-// Dynamic layout: ring | header | bitmap[nwords] | cand keys[cap] | cand idx[cap]
-struct SelSmem {
-  uint32_t (*ring)[kChunkKeys];
-  SelHdr* h;
-  uint32_t* bitmap;  // bit i: key i selected
-  uint32_t* ckey;    // boundary-bin candidates, index order
-  uint32_t* cidx;
-  int cap;
-
-  __device__ static SelSmem carve(uint8_t* raw, int total_bytes, int nwords) {
-    SelSmem s;
-    uint8_t* base = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    const int avail = total_bytes - (int)(base - raw);
-    s.ring = reinterpret_cast<uint32_t(*)[kChunkKeys]>(base);
-    s.h = reinterpret_cast<SelHdr*>(base + kRing * kChunkKeys * 4);
-    s.bitmap = reinterpret_cast<uint32_t*>(s.h + 1);
-    uint32_t* c = s.bitmap + ((nwords + 3) & ~3);
-    const int used = (int)(reinterpret_cast<uint8_t*>(c) - base);
-    s.cap = max(0, (avail - used) / 8);
-    s.ckey = c;
-    s.cidx = c + s.cap;
-    return s;
-  }
-};
-
-// Block-wide inclusive scan (256 threads).
-__device__ __forceinline__ uint32_t block_scan(uint32_t v, uint32_t* warp_tot, uint32_t& total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int kWarps = kStepThreads / 32;
+// 64-thread inclusive scan (2 warps).
+__device__ __forceinline__ uint32_t epi_scan(uint32_t v, uint32_t* scan, int et, uint32_t& total) {
+  const int lane = et & 31, w = et >> 5;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
     const uint32_t n = __shfl_up_sync(0xffffffffu, v, off);
     if (lane >= off) v += n;
   }
-  if (lane == 31) warp_tot[warp] = v;
-  __syncthreads();
-  uint32_t before = 0;
-  total = 0;
-#pragma unroll
-  for (int w = 0; w < kWarps; ++w) {
-    const uint32_t t = warp_tot[w];
-    before += w < warp ? t : 0u;
-    total += t;
-  }
-  __syncthreads();
+  if (lane == 31) scan[w] = v;
+  epi_bar();
+  const uint32_t before = w ? scan[0] : 0u;
+  total = scan[0] + scan[1];
+  epi_bar();
   return v + before;
 }
 
-__device__ __forceinline__ void digit_of(SelHdr* h, int nbins, uint32_t krem) {
-  if (threadIdx.x < 32) {
+// Digit of a histogram by warp 0 of the epilogue; result broadcast via smem.
+__device__ __forceinline__ void epi_digit(EpiSmem& es, const uint32_t* h, bool global, int nbins,
+                                          uint32_t krem, int et) {
+  if (et < 32) {
     uint32_t d, a;
-    find_digit(h->hist, nbins, krem, d, a, threadIdx.x);
-    if (threadIdx.x == 0) {
-      h->digit = d;
-      h->above = a;
+    find_digit(h, nbins, krem, d, a, et, global);
+    if (et == 0) {
+      es.digit = d;
+      es.above = a;
     }
   }
-  __syncthreads();
+  epi_bar();
 }
 
-// Streams keys[0, n) through the TMA ring; f(base, chunk, cnt) runs on every
-// thread for each chunk in order and must not read the chunk after returning.
-// `phases` holds the per-slot mbarrier parities (persistent across calls).
-template <typename F>
-__device__ __forceinline__ void stream_keys(const SelSmem& sh, const uint32_t* keys, int n,
-                                            uint32_t& phases, F&& f) {
-  const int nck = (n + kChunkKeys - 1) / kChunkKeys;
-  auto issue = [&](int c) {
-    const int cnt = min(kChunkKeys, n - c * kChunkKeys);
-    const uint32_t bytes = (uint32_t)((cnt + 3) & ~3) * 4u;  // key rows are padded to 4
-    uint64_t* bar = &sh.h->bars[c % kRing];
-    mbar_arrive_expect_tx(bar, bytes);
-    bulk_g2s(sh.ring[c % kRing], keys + (size_t)c * kChunkKeys, bytes, bar);
-  };
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    fence_proxy_async();  // earlier generic reads of the ring precede its async overwrite
-    for (int c = 0; c < min(kRing, nck); ++c) issue(c);
-  }
-  for (int c = 0; c < nck; ++c) {
-    const int slot = c % kRing;
-    mbar_wait(&sh.h->bars[slot], (phases >> slot) & 1u);
-    phases ^= 1u << slot;
-    f(c * kChunkKeys, sh.ring[slot], min(kChunkKeys, n - c * kChunkKeys));
-    __syncthreads();
-    if (threadIdx.x == 0 && c + kRing < nck) {
-      fence_proxy_async();
-      issue(c + kRing);
-    }
-  }
+struct SelRow {
+  uint32_t* keys;     // keys of the row [n]
+  uint32_t* h1;       // fused first-pass histogram (token mode) or nullptr
+  uint32_t* bitmap;   // [n_words]
+  uint32_t* ckey;     // [n] candidate keys, item q's segment at q*kItemKeys
+  uint32_t* cidx;     // [n] candidate indices
+  uint32_t* ccnt;     // [n_items] candidates per item
+  uint32_t* ctr;      // per-row item counter
+};
+
+__device__ __forceinline__ SelRow sel_row(const LycStepParams& p, int l, int r) {
+  const int64_t pr = (int64_t)(l & 1) * p.max_sel + r;
+  SelRow s;
+  s.keys = p.sel_keys + pr * p.sel_stride;
+  s.h1 = p.sel_mode == SEL_TOKEN_KEYS ? p.hist + pr * LYC_BINS : nullptr;
+  s.bitmap = p.sel_bitmap + pr * p.bitmap_stride;
+  s.ckey = p.sel_cand + pr * 2 * p.sel_stride;
+  s.cidx = s.ckey + p.sel_stride;
+  s.ccnt = p.sel_ccnt + pr * 64;
+  s.ctr = p.sel_rowctr + ((int64_t)l * p.max_sel + r) * 16;
+  return s;
 }
 
-// One row: the k largest of n keys (ties to the lower index), ascending,
-// into out[0..k).  h1 (token mode) is the grid-wide first-pass histogram
-// (bits 31..21) built by the attention consumers; otherwise it is computed
-// here.  The radix descends until the boundary bin fits the candidate store
-// (normally right after pass 1); ONE streaming pass then classifies every key:
-// above the boundary prefix -> bitmap bit, inside it -> candidate (key, index)
-// in index order.  The remaining radix passes run on the candidates in shared
-// memory, the selected candidates join the bitmap, and a popcount scan of the
-// bitmap emits the indices in ascending order.
-__device__ void select_row(uint8_t* smem_raw, int smem_bytes, const LycStepParams& p,
-                           uint32_t* keys_g, uint32_t* h1, int32_t* out, uint32_t& phases, int l,
-                           int sid) {
-  const int tid = threadIdx.x;
+// Classify item q of one row: keys above the boundary bin set bitmap bits,
+// keys inside it become candidates (index order).  Returns true to the whole
+// group if this was the row's last item (the caller then finishes the row).
+__device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, uint32_t epoch1,
+                              EpiSmem& es, uint32_t& bar_phase, int et) {
   const int n = p.n_keys;
-  const int nwords = (n + 31) / 32;
-  const SelSmem sh = SelSmem::carve(smem_raw, smem_bytes, nwords);
-  SelHdr* H = sh.h;
-  uint32_t krem = (uint32_t)p.k_sel;
-  // ---- pass 1 (bits 31..21)
-  if (h1) {
-    const uint4* src = reinterpret_cast<const uint4*>(h1);
-    uint4 buf[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) buf[q] = __ldcg(src + q * kStepThreads + tid);
-#pragma unroll
-    for (int q = 0; q < 2; ++q) reinterpret_cast<uint4*>(H->hist)[q * kStepThreads + tid] = buf[q];
-    __syncthreads();
-  } else {
-    for (int b = tid; b < LYC_BINS; b += kStepThreads) H->hist[b] = 0u;
-    stream_keys(sh, keys_g, n, phases, [&](int, const uint32_t* ck, int cnt) {
-      for (int i = tid; i < cnt; i += kStepThreads) atomicAdd(&H->hist[ck[i] >> 21], 1u);
-    });
+  const int lo = q * kItemKeys;
+  const int cnt = min(kItemKeys, n - lo);
+  if (et == 0) {
+    fence_proxy_async();
+    const uint32_t bytes = (uint32_t)((cnt + 3) & ~3) * 4u;  // key rows are padded to 4
+    mbar_arrive_expect_tx(&es.bar, bytes);
+    bulk_g2s(es.keys, R.keys + lo, bytes, &es.bar);
   }
-  digit_of(H, LYC_BINS, krem);
-  uint32_t P = H->digit;  // boundary prefix
-  int shift = 21;         // key >> shift is the prefix
-  krem -= H->above;
-  uint32_t n_eq = H->hist[P];
-  if (n_eq > (uint32_t)sh.cap) {  // rare: boundary bin too big -> descend on the stream
-    for (int b = tid; b < LYC_BINS; b += kStepThreads) H->hist[b] = 0u;
-    stream_keys(sh, keys_g, n, phases, [&](int, const uint32_t* ck, int cnt) {
-      for (int i = tid; i < cnt; i += kStepThreads)
-        if ((ck[i] >> 21) == P) atomicAdd(&H->hist[(ck[i] >> 10) & 0x7ffu], 1u);
-    });
-    digit_of(H, LYC_BINS, krem);
-    P = (P << 11) | H->digit;
-    shift = 10;
-    krem -= H->above;
-    n_eq = H->hist[H->digit];
-    if (n_eq > (uint32_t)sh.cap) {
-      for (int b = tid; b < 1024; b += kStepThreads) H->hist[b] = 0u;
-      stream_keys(sh, keys_g, n, phases, [&](int, const uint32_t* ck, int cnt) {
-        for (int i = tid; i < cnt; i += kStepThreads)
-          if ((ck[i] >> 10) == P) atomicAdd(&H->hist[ck[i] & 0x3ffu], 1u);
-      });
-      digit_of(H, 1024, krem);
-      P = (P << 10) | H->digit;  // the k-th key T itself; krem of its ties are taken
-      shift = 0;
-      krem -= H->above;
-    }
+  // boundary bin d1 (bits 31..21) of the whole row
+  const uint32_t* h = R.h1;
+  if (!h) {  // block mode: the row is a single item -- histogram it here
+    mbar_wait(&es.bar, bar_phase);
+    for (int b = et; b < LYC_BINS; b += kEpiThreads) es.hist[b] = 0u;
+    epi_bar();
+    for (int i = et; i < cnt; i += kEpiThreads) atomicAdd(&es.hist[es.keys[i] >> 21], 1u);
+    epi_bar();
+    h = es.hist;
   }
-  if (tid == 0) stamp(p, l, EV_SEL0, sid);
-  // ---- classify every key against the prefix P
-  uint32_t run = 0;  // candidates (or ties of T) so far, index order
-  stream_keys(sh, keys_g, n, phases, [&](int base, const uint32_t* ck, int cnt) {
-    // thread t owns 32 consecutive keys = one bitmap word, read as 8 rotated
-    // 16-B vectors (conflict-free)
-    uint32_t word = 0, eqm = 0;
-    const int k0 = tid * 32;
+  epi_digit(es, h, R.h1 != nullptr, LYC_BINS, (uint32_t)p.k_sel, et);
+  const uint32_t d1 = es.digit;
+  mbar_wait(&es.bar, bar_phase);
+  bar_phase ^= 1u;
+  // thread et owns 128 consecutive keys = 4 bitmap words, read as rotated 16-B
+  // vectors (conflict-free)
+  uint32_t words[4] = {0u, 0u, 0u, 0u}, eqm[4] = {0u, 0u, 0u, 0u};
+  const int k0 = et * 128;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int qq = (q + tid) & 7;
-      const uint4 v = reinterpret_cast<const uint4*>(ck + k0)[qq];
+  for (int w = 0; w < 4; ++w) {
+#pragma unroll
+    for (int qv = 0; qv < 8; ++qv) {
+      const int qq = (qv + et) & 7;
+      const uint4 v = reinterpret_cast<const uint4*>(es.keys + k0 + w * 32)[qq];
       const uint32_t kv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int j = qq * 4 + e;
-        const bool ok = k0 + j < cnt;
-        const uint32_t pre = shift ? kv[e] >> shift : kv[e];
-        word |= (ok && pre > P) ? (1u << j) : 0u;
-        eqm |= (ok && pre == P) ? (1u << j) : 0u;
+        const bool ok = k0 + w * 32 + j < cnt;
+        const uint32_t top = kv[e] >> 21;
+        words[w] |= (ok && top > d1) ? (1u << j) : 0u;
+        eqm[w] |= (ok && top == d1) ? (1u << j) : 0u;
       }
     }
-    uint32_t tot;
-    const uint32_t c = __popc(eqm);
-    const uint32_t incl = block_scan(c, H->warp_tot, tot);
-    uint32_t pos = run + incl - c;
-    if (shift == 0) {  // ties of T: take the first krem by index
-      while (eqm) {
-        const int j = __ffs(eqm) - 1;
-        eqm &= eqm - 1;
-        if (pos < krem) word |= 1u << j;
-        ++pos;
-      }
-    } else {
-      while (eqm) {
-        const int j = __ffs(eqm) - 1;
-        eqm &= eqm - 1;
-        sh.ckey[pos] = ck[k0 + j];
-        sh.cidx[pos] = (uint32_t)(base + k0 + j);
-        ++pos;
-      }
-    }
-    if (k0 < cnt) sh.bitmap[base / 32 + tid] = word;
-    run += tot;
-  });
-  // ---- finish the radix on the candidates
-  if (shift > 0) {
-    const int nc = (int)run;
-    if (shift == 21) {
-      for (int b = tid; b < LYC_BINS; b += kStepThreads) H->hist[b] = 0u;
-      __syncthreads();
-      for (int i = tid; i < nc; i += kStepThreads)
-        atomicAdd(&H->hist[(sh.ckey[i] >> 10) & 0x7ffu], 1u);
-      __syncthreads();
-      digit_of(H, LYC_BINS, krem);
-      P = (P << 11) | H->digit;
-      krem -= H->above;
-    }
-    for (int b = tid; b < 1024; b += kStepThreads) H->hist[b] = 0u;
-    __syncthreads();
-    for (int i = tid; i < nc; i += kStepThreads)
-      if ((sh.ckey[i] >> 10) == P) atomicAdd(&H->hist[sh.ckey[i] & 0x3ffu], 1u);
-    __syncthreads();
-    digit_of(H, 1024, krem);
-    const uint32_t T = (P << 10) | H->digit;
-    krem -= H->above;  // ties of T to take (lowest indices first)
-    // selected candidates join the bitmap: key > T, or the first krem ties
-    uint32_t tie_run = 0;
-    for (int b0 = 0; b0 < nc; b0 += kStepThreads) {
-      const int i = b0 + tid;
-      const uint32_t key = i < nc ? sh.ckey[i] : 0u;
-      const bool is_eq = i < nc && key == T;
-      uint32_t tot;
-      const uint32_t incl = block_scan(is_eq ? 1u : 0u, H->warp_tot, tot);
-      const uint32_t rank = tie_run + incl - (is_eq ? 1u : 0u);
-      if (i < nc && (key > T || (is_eq && rank < krem)))
-        atomicOr(&sh.bitmap[sh.cidx[i] >> 5], 1u << (sh.cidx[i] & 31));
-      tie_run += tot;
-    }
-    __syncthreads();
   }
-  if (tid == 0) stamp(p, l, EV_SEL1, sid);
-  // ---- emit the set bits in ascending order
-  const int per = (nwords + kStepThreads - 1) / kStepThreads;
-  const int w0 = min(nwords, tid * per), w1 = min(nwords, w0 + per);
+#pragma unroll
+  for (int w = 0; w < 4; ++w)
+    if (k0 + w * 32 < cnt) R.bitmap[(lo + k0) / 32 + w] = words[w];
+  const uint32_t c = __popc(eqm[0]) + __popc(eqm[1]) + __popc(eqm[2]) + __popc(eqm[3]);
+  uint32_t total;
+  uint32_t pos = epi_scan(c, es.scan, et, total) - c;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    uint32_t m = eqm[w];
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      const int i = k0 + w * 32 + j;
+      R.ckey[lo + pos] = es.keys[i];
+      R.cidx[lo + pos] = (uint32_t)(lo + i);
+      ++pos;
+    }
+  }
+  if (et == 0) R.ccnt[q] = total;
+  epi_bar();
+  if (et == 0) {
+    __threadfence();
+    const int items = (n + kItemKeys - 1) / kItemKeys;
+    const uint32_t old = atomicAdd(R.ctr, 1u);
+    es.last = old == epoch1 * (uint32_t)items - 1u;
+    if (es.last) __threadfence();  // acquire the other items' writes
+  }
+  epi_bar();
+  return es.last != 0;
+}
+
+// Finish one row after its last item: radix passes 2-3 over the candidates,
+// selected candidates join the bitmap, ascending emission of the set bits.
+__device__ void finish_row(const LycStepParams& p, const SelRow& R, int32_t* out, EpiSmem& es,
+                           int et) {
+  const int n = p.n_keys;
+  const int items = (n + kItemKeys - 1) / kItemKeys;
+  const int nwords = (n + 31) / 32;
+  uint32_t krem = (uint32_t)p.k_sel;
+  // boundary bin again (block mode: es.hist still holds the item histogram)
+  epi_digit(es, R.h1 ? R.h1 : es.hist, R.h1 != nullptr, LYC_BINS, krem, et);
+  const uint32_t d1 = es.digit;
+  krem -= es.above;
+  // candidate segments: item q's candidates are [seg[q], seg[q+1]) in index order
+  const uint32_t c_mine = et < items ? __ldcg(R.ccnt + et) : 0u;
+  uint32_t nc_u;
+  const uint32_t incl = epi_scan(c_mine, es.scan, et, nc_u);
+  if (et < items) es.seg[et + 1] = incl;
+  if (et == 0) es.seg[0] = 0u;
+  epi_bar();
+  const int nc = (int)nc_u;
+  auto cand = [&](int i, uint32_t& key, uint32_t& idx) {
+    int qi = 0;
+    while ((uint32_t)i >= es.seg[qi + 1]) ++qi;
+    const uint32_t off = (uint32_t)qi * kItemKeys + ((uint32_t)i - es.seg[qi]);
+    key = __ldcg(R.ckey + off);
+    idx = __ldcg(R.cidx + off);
+  };
+  // pass 2 (bits 20..10)
+  for (int b = et; b < LYC_BINS; b += kEpiThreads) es.hist[b] = 0u;
+  epi_bar();
+  for (int i = et; i < nc; i += kEpiThreads) {
+    uint32_t key, idx;
+    cand(i, key, idx);
+    atomicAdd(&es.hist[(key >> 10) & 0x7ffu], 1u);
+  }
+  epi_bar();
+  epi_digit(es, es.hist, false, LYC_BINS, krem, et);
+  const uint32_t P = (d1 << 11) | es.digit;
+  krem -= es.above;
+  // pass 3 (bits 9..0)
+  for (int b = et; b < 1024; b += kEpiThreads) es.hist[b] = 0u;
+  epi_bar();
+  for (int i = et; i < nc; i += kEpiThreads) {
+    uint32_t key, idx;
+    cand(i, key, idx);
+    if ((key >> 10) == P) atomicAdd(&es.hist[key & 0x3ffu], 1u);
+  }
+  epi_bar();
+  epi_digit(es, es.hist, false, 1024, krem, et);
+  const uint32_t T = (P << 10) | es.digit;
+  krem -= es.above;  // ties of T to take (lowest indices first)
+  // selected candidates join the bitmap
+  uint32_t tie_run = 0;
+  for (int b0 = 0; b0 < nc; b0 += kEpiThreads) {
+    const int i = b0 + et;
+    uint32_t key = 0, idx = 0;
+    if (i < nc) cand(i, key, idx);
+    const bool is_eq = i < nc && key == T;
+    uint32_t tot;
+    const uint32_t inc = epi_scan(is_eq ? 1u : 0u, es.scan, et, tot);
+    const uint32_t rank = tie_run + inc - (is_eq ? 1u : 0u);
+    if (i < nc && (key > T || (is_eq && rank < krem)))
+      atomicOr(R.bitmap + (idx >> 5), 1u << (idx & 31));
+    tie_run += tot;
+  }
+  __threadfence();
+  epi_bar();
+  // ascending emission of the set bits
+  const int per = (nwords + kEpiThreads - 1) / kEpiThreads;
+  const int w0 = min(nwords, et * per), w1 = min(nwords, w0 + per);
   uint32_t cnt = 0;
-  for (int w = w0; w < w1; ++w) cnt += __popc(sh.bitmap[w]);
+  for (int w = w0; w < w1; ++w) cnt += __popc(__ldcg(R.bitmap + w));
   uint32_t tot;
-  uint32_t pos = block_scan(cnt, H->warp_tot, tot) - cnt;
+  uint32_t pos = epi_scan(cnt, es.scan, et, tot) - cnt;
   for (int w = w0; w < w1; ++w) {
-    uint32_t m = sh.bitmap[w];
+    uint32_t m = __ldcg(R.bitmap + w);
     while (m) {
       const int j = __ffs(m) - 1;
       m &= m - 1;
       out[pos++] = w * 32 + j;
     }
   }
-  if (h1)  // reset the fused histogram for its next use
-    for (int b = tid; b < LYC_BINS; b += kStepThreads) h1[b] = 0u;
-  if (p.sel_mode == SEL_BLOCK_KEYS)  // block keys are max-folded: reset the row
-    for (int i = tid; i < n; i += kStepThreads) keys_g[i] = 0u;
-  if (tid == 0) stamp(p, l, EV_SEL2, sid);
-  __syncthreads();
+  // reset the per-row inputs for their next use
+  if (R.h1)
+    for (int b = et; b < LYC_BINS; b += kEpiThreads) R.h1[b] = 0u;
+  if (p.sel_mode == SEL_BLOCK_KEYS)
+    for (int i = et; i < n; i += kEpiThreads) R.keys[i] = 0u;
+  epi_bar();
 }
 
-// ---------------------------------------------------------------- kernel
 // ---------------------------------------------------------------- kernel
 template <typename T, int D>
 __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __grid_constant__ LycStepParams p) {
   using C = AttnCfg<T, D>;
+  static_assert(sizeof(EpiSmem) <= C::kExtraBytes, "epilogue scratch does not fit");
   extern __shared__ uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
-  const int n_total = p.n_ctas + p.n_sel_ctas;
   uint32_t* ctrl = LYC_CTR(p.ctr, p.n_layers, 0);  // completed steps; exits at + stride
   __shared__ uint32_t s_epoch;
-  if (threadIdx.x == 0) s_epoch = ld_acquire(ctrl);
+  const AttnSmem<T, D> sm = AttnSmem<T, D>::carve(smem_raw);
+  EpiSmem& es = *reinterpret_cast<EpiSmem*>(sm.extra);
+  if (threadIdx.x == 0) {
+    s_epoch = ld_acquire(ctrl);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&sm.full[s], kProducerThreads);
+      mbar_init(&sm.empty[s], kConsumerWarps);
+    }
+    mbar_init(&es.bar, 1);
+    fence_mbar_init();
+  }
+  for (int b = threadIdx.x; b < LYC_BINS; b += kStepThreads) sm.hist[b] = 0u;
   __syncthreads();
   const uint32_t epoch1 = s_epoch + 1u;
   const uint32_t t_attn = epoch1 * (uint32_t)p.n_ctas;
-  const uint32_t t_sel = epoch1 * (uint32_t)p.n_sel_ctas;
   constexpr int esz = (int)sizeof(T);
+  const int cell = cta;  // = b * n_splits + split
 
-  if (cta >= p.n_ctas) {
-
-    // ======================== selection CTA ========================
-    const int sid = cta - p.n_ctas;
-    if (threadIdx.x == 0) {
-      SelHdr* H = SelSmem::carve(smem_raw, C::kSmem, 0).h;
-      for (int s = 0; s < kRing; ++s) mbar_init(&H->bars[s], 1);
-      fence_mbar_init();
+  if (warp < kConsumerWarps) {
+    // ---------------- consumers
+    const int tid = threadIdx.x;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int l = 0; l < p.n_layers; ++l) {
+      if (l > 0) {
+        if (tid == 0) {
+          spin_until(LYC_CTR(p.ctr, l - 1, CTR_MERGE), t_attn);
+          // key / histogram buffers of this parity are free once layer l-2's
+          // selection (if any) finished
+          if (l >= 2 && p.layers[l - 2].n_sel > 0 && p.sel_mode != SEL_NONE)
+            spin_until(LYC_CTR(p.ctr, l - 2, CTR_SELDONE),
+                       epoch1 * (uint32_t)p.layers[l - 2].n_sel);
+          __threadfence();
+        }
+        consumer_bar();
+      }
+      if (tid == 0) stamp(p, l, EV_CONS_BEGIN, cta);
+      const LycLayerDesc L = p.layers[l];
+      const LycView v = layer_view(p, L, l, esz);
+      consume_units<T, D>(v, sm, L.split_off[cell], L.split_off[cell + 1], warp, lane, stage,
+                          phase);
+      consumer_bar();
+      if (tid == 0) {
+        stamp(p, l, EV_CONS_END, cta);
+        signal(LYC_CTR(p.ctr, l, CTR_ATTN));
+      }
     }
-    __syncthreads();
-    uint32_t phases = 0;
+  } else if (warp < kConsumerWarps + kProducerWarps) {
+    // ---------------- producers
+    const int pt = threadIdx.x - kConsumerWarps * 32;
+    if (pt == 0) {
+      prefetch_tensormap(&p.tmap_k);
+      prefetch_tensormap(&p.tmap_v);
+    }
+    int stage = 0;
+    uint32_t phase = 0;
     for (int l = 0; l < p.n_layers; ++l) {
       const LycLayerDesc L = p.layers[l];
-      if (L.n_sel == 0 || p.sel_mode == SEL_NONE) continue;
-      if (threadIdx.x == 0) {
-        spin_until(LYC_CTR(p.ctr, l, CTR_ATTN), t_attn);
-        __threadfence();
-      }
-      __syncthreads();
-      for (int r = sid; r < L.n_sel; r += p.n_sel_ctas) {
-        uint32_t* kg = p.sel_keys + ((int64_t)(l & 1) * p.max_sel + r) * p.sel_stride;
-        uint32_t* h1 = p.sel_mode == SEL_TOKEN_KEYS
-                           ? p.hist + ((int64_t)(l & 1) * p.max_sel + r) * LYC_BINS
-                           : nullptr;
-        const int row = __ldg(L.sel_rows + r);
-        select_row(smem_raw, C::kSmem, p, kg, h1, p.idx + (int64_t)row * p.idx_stride, phases, l,
-                   sid);
-        if (threadIdx.x == 0 && p.idx_count) p.idx_count[row] = p.k_sel;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        stamp(p, l, EV_SELDONE, sid);
-        signal(LYC_CTR(p.ctr, l, CTR_SELDONE));
-      }
+      const LycView v = layer_view(p, L, l, esz);
+      StepWaits waits{&p, epoch1, l, pt};
+      produce_units<T, D>(v, &p.tmap_k, &p.tmap_v, sm.ring, sm.full, sm.empty,
+                          L.split_off[cell], L.split_off[cell + 1], pt, stage, phase, waits);
     }
   } else {
-    // ======================== attention CTA ========================
-    const AttnSmem<T, D> sm = AttnSmem<T, D>::carve(smem_raw);
-    if (threadIdx.x == 0) {
-      for (int s = 0; s < C::kStages; ++s) {
-        mbar_init(&sm.full[s], kProducerThreads);
-        mbar_init(&sm.empty[s], kConsumerWarps);
+    // ---------------- epilogue: merge + pooled selection
+    const int et = threadIdx.x - (kConsumerWarps + kProducerWarps) * 32;
+    const int ew = et >> 5;
+    const int chunks = (D + 31) / 32;
+    const int items = (p.n_keys + kItemKeys - 1) / kItemKeys;
+    uint32_t bar_phase = 0;
+    for (int l = 0; l < p.n_layers; ++l) {
+      const LycLayerDesc L = p.layers[l];
+      if (et == 0) {
+        spin_until(LYC_CTR(p.ctr, l, CTR_ATTN), t_attn);
+        __threadfence();
+        stamp(p, l, EV_EPI_ATTN, cta);
       }
-      fence_mbar_init();
-    }
-    for (int b = threadIdx.x; b < LYC_BINS; b += kStepThreads) sm.hist[b] = 0u;
-    __syncthreads();
-    const int cell = cta;  // = b * n_splits + split
-    if (warp < kConsumerWarps) {
-      const int tid = threadIdx.x;
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int l = 0; l < p.n_layers; ++l) {
-        if (l > 0) {
-          if (tid == 0) {
-            spin_until(LYC_CTR(p.ctr, l - 1, CTR_MERGE), t_attn);
-            // key / histogram buffers of this parity are free once layer l-2's
-            // selection (if any) finished
-            if (l >= 2 && p.layers[l - 2].n_sel > 0 && p.sel_mode != SEL_NONE)
-              spin_until(LYC_CTR(p.ctr, l - 2, CTR_SELDONE), t_sel);
-            __threadfence();
+      epi_bar();
+      // (a) split-KV merge
+      const int total = L.n_merges * chunks;
+      uint8_t* outl = static_cast<uint8_t*>(p.out) + (int64_t)l * p.q_layer_stride * esz;
+      for (int t = cta * kEpiWarps + ew; t < total; t += p.n_ctas * kEpiWarps) {
+        const LycMergeTask tk = L.merges[t / chunks];
+        const LycSlot s = L.slots[tk.slot];
+        merge_task<T>(p.part_o, p.part_lse, s, tk.j, t % chunks, p.group, D, outl, lane);
+      }
+      epi_bar();
+      if (et == 0) {
+        stamp(p, l, EV_MERGE, cta);
+        signal(LYC_CTR(p.ctr, l, CTR_MERGE));
+      }
+      // (b) selection items of this layer's retrieval heads
+      if (L.n_sel > 0 && p.sel_mode != SEL_NONE) {
+        const int n_items = L.n_sel * items;
+        for (int it = cta; it < n_items; it += p.n_ctas) {
+          const int r = it / items, q = it - r * items;
+          const SelRow R = sel_row(p, l, r);
+          if (classify_item(p, R, q, epoch1, es, bar_phase, et)) {
+            const int row = __ldg(L.sel_rows + r);
+            finish_row(p, R, p.idx + (int64_t)row * p.idx_stride, es, et);
+            if (et == 0) {
+              if (p.idx_count) p.idx_count[row] = p.k_sel;
+              stamp(p, l, EV_SELDONE, cta);
+              signal(LYC_CTR(p.ctr, l, CTR_SELDONE));
+            }
           }
-          consumer_bar();
-        }
-        if (tid == 0) stamp(p, l, EV_CONS_BEGIN, cta);
-        const LycLayerDesc L = p.layers[l];
-        const LycView v = layer_view(p, L, l, esz);
-        consume_units<T, D>(v, sm, L.split_off[cell], L.split_off[cell + 1], warp, lane, stage,
-                            phase);
-        consumer_bar();
-        if (tid == 0) {
-          stamp(p, l, EV_CONS_END, cta);
-          signal(LYC_CTR(p.ctr, l, CTR_ATTN));
-        }
-      }
-    } else if (warp < kConsumerWarps + kProducerWarps) {
-      const int pt = threadIdx.x - kConsumerWarps * 32;
-      if (pt == 0) {
-        prefetch_tensormap(&p.tmap_k);
-        prefetch_tensormap(&p.tmap_v);
-      }
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int l = 0; l < p.n_layers; ++l) {
-        const LycLayerDesc L = p.layers[l];
-        const LycView v = layer_view(p, L, l, esz);
-        StepWaits waits{p.ctr, t_attn, t_sel, l, pt};
-        produce_units<T, D>(v, &p.tmap_k, &p.tmap_v, sm.ring, sm.full, sm.empty,
-                            L.split_off[cell], L.split_off[cell + 1], pt, stage, phase, waits);
-      }
-    } else {
-      const int et = threadIdx.x - (kConsumerWarps + kProducerWarps) * 32;
-      const int ew = et >> 5;
-      const int chunks = (D + 31) / 32;
-      for (int l = 0; l < p.n_layers; ++l) {
-        const LycLayerDesc L = p.layers[l];
-        if (et == 0) {
-          spin_until(LYC_CTR(p.ctr, l, CTR_ATTN), t_attn);
-          __threadfence();
-          stamp(p, l, EV_EPI_ATTN, cta);
-        }
-        group_bar(2, kEpiThreads);
-        // split-KV merge, spread over all attention CTAs' epilogue warps
-        const int total = L.n_merges * chunks;
-        uint8_t* outl = static_cast<uint8_t*>(p.out) + (int64_t)l * p.q_layer_stride * esz;
-        for (int t = cta * kEpiWarps + ew; t < total; t += p.n_ctas * kEpiWarps) {
-          const LycMergeTask tk = L.merges[t / chunks];
-          const LycSlot s = L.slots[tk.slot];
-          merge_task<T>(p.part_o, p.part_lse, s, tk.j, t % chunks, p.group, D, outl, lane);
-        }
-        group_bar(2, kEpiThreads);
-        if (et == 0) {
-          stamp(p, l, EV_MERGE, cta);
-          signal(LYC_CTR(p.ctr, l, CTR_MERGE));
         }
       }
     }
@@ -571,7 +527,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t done = atomicAdd(ctrl + LYC_CTR_STRIDE, 1u);
-    if (done == epoch1 * (uint32_t)n_total - 1u) atomicAdd(ctrl, 1u);  // last CTA out
+    if (done == t_attn - 1u) atomicAdd(ctrl, 1u);  // last CTA out: one more completed step
   }
 }
 
@@ -586,7 +542,7 @@ static cudaError_t launch_step_t(const LycStepParams& p, cudaStream_t st) {
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.n_ctas + p.n_sel_ctas);
+  cfg.gridDim = dim3(p.n_ctas);
   cfg.blockDim = dim3(kStepThreads);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = st;
@@ -615,7 +571,9 @@ cudaError_t launch_step(const LycStepParams& p, int dtype, int d, cudaStream_t s
   return cudaErrorInvalidValue;
 }
 
-int step_select_capacity(int, int) { return 1 << 16; }  // keys per row / 4 (bitmap bound)
+// Largest selection row (keys) the fused step supports: <= 64 items per row.
+int64_t step_max_keys() { return (int64_t)64 * kItemKeys; }
+int step_item_keys() { return kItemKeys; }
 
 bool step_supported(int dtype, int d) {
   return dtype == 1 ? (d == 64 || d == 128) : (d == 16 || d == 32 || d == 64 || d == 128);
