@@ -171,12 +171,16 @@ __device__ __forceinline__ void find_digit(const uint32_t* h, int nbins, uint32_
   above = __shfl_sync(0xffffffffu, a, src_lane);
 }
 
-// Epilogue scratch (inside AttnSmem::extra, 44 KB).
+// Epilogue scratch (inside AttnSmem::extra).
+constexpr int kEpiBufWords = 12288;  // 48 KB
 struct EpiSmem {
-  uint32_t keys[kItemKeys];  // one item's keys (TMA bulk destination)
+  // classify: one item's keys [kItemKeys]; finish: bitmap [nwords] followed by
+  // the candidates' keys and indices
+  uint32_t buf[kEpiBufWords];
   uint32_t hist[LYC_BINS];
   uint32_t scan[64];
-  uint32_t seg[72];          // candidate segment starts (items <= 64) + total
+  uint32_t seg[72];          // finish: smem start of each item's candidate segment
+  uint32_t cnt[72];          // finish: candidates of each item
   uint64_t bar;
   uint32_t digit, above, last, pad;
 };
@@ -246,7 +250,7 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
     fence_proxy_async();
     const uint32_t bytes = (uint32_t)((cnt + 3) & ~3) * 4u;  // key rows are padded to 4
     mbar_arrive_expect_tx(&es.bar, bytes);
-    bulk_g2s(es.keys, R.keys + lo, bytes, &es.bar);
+    bulk_g2s(es.buf, R.keys + lo, bytes, &es.bar);
   }
   // boundary bin d1 (bits 31..21) of the whole row
   const uint32_t* h = R.h1;
@@ -254,7 +258,7 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
     mbar_wait(&es.bar, bar_phase);
     for (int b = et; b < LYC_BINS; b += kEpiThreads) es.hist[b] = 0u;
     epi_bar();
-    for (int i = et; i < cnt; i += kEpiThreads) atomicAdd(&es.hist[es.keys[i] >> 21], 1u);
+    for (int i = et; i < cnt; i += kEpiThreads) atomicAdd(&es.hist[es.buf[i] >> 21], 1u);
     epi_bar();
     h = es.hist;
   }
@@ -271,7 +275,7 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
 #pragma unroll
     for (int qv = 0; qv < 8; ++qv) {
       const int qq = (qv + et) & 7;
-      const uint4 v = reinterpret_cast<const uint4*>(es.keys + k0 + w * 32)[qq];
+      const uint4 v = reinterpret_cast<const uint4*>(es.buf + k0 + w * 32)[qq];
       const uint32_t kv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -296,7 +300,7 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
       const int j = __ffs(m) - 1;
       m &= m - 1;
       const int i = k0 + w * 32 + j;
-      R.ckey[lo + pos] = es.keys[i];
+      R.ckey[lo + pos] = es.buf[i];
       R.cidx[lo + pos] = (uint32_t)(lo + i);
       ++pos;
     }
@@ -314,40 +318,77 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
   return es.last != 0;
 }
 
-// Finish one row after its last item: radix passes 2-3 over the candidates,
-// selected candidates join the bitmap, ascending emission of the set bits.
+// Finish one row after its last item.  One thread bulk-copies the row's bitmap
+// and every item's candidate segment (keys and indices, 16-B aligned) into
+// shared memory -- all copies in flight at once -- then radix passes 2-3 run
+// on the candidates, the selected ones join the bitmap, and the set bits are
+// emitted in ascending order.  Rows whose boundary bin holds more candidates
+// than fit on chip fall back to reading them from L2.
 __device__ void finish_row(const LycStepParams& p, const SelRow& R, int32_t* out, EpiSmem& es,
-                           int et) {
+                           uint32_t& bar_phase, int et) {
   const int n = p.n_keys;
   const int items = (n + kItemKeys - 1) / kItemKeys;
   const int nwords = (n + 31) / 32;
+  const int bm_words = (nwords + 3) & ~3;
   uint32_t krem = (uint32_t)p.k_sel;
   // boundary bin again (block mode: es.hist still holds the item histogram)
   epi_digit(es, R.h1 ? R.h1 : es.hist, R.h1 != nullptr, LYC_BINS, krem, et);
   const uint32_t d1 = es.digit;
   krem -= es.above;
-  // candidate segments: item q's candidates are [seg[q], seg[q+1]) in index order
+  // candidate segments: item q's candidates land at smem [seg[q], seg[q] + cnt[q])
   const uint32_t c_mine = et < items ? __ldcg(R.ccnt + et) : 0u;
-  uint32_t nc_u;
-  const uint32_t incl = epi_scan(c_mine, es.scan, et, nc_u);
-  if (et < items) es.seg[et + 1] = incl;
-  if (et == 0) es.seg[0] = 0u;
+  const uint32_t c_pad = (c_mine + 3) & ~3u;
+  uint32_t padded;
+  const uint32_t incl = epi_scan(c_pad, es.scan, et, padded);
+  if (et < items) {
+    es.seg[et] = incl - c_pad;
+    es.cnt[et] = c_mine;
+  }
+  const int cap = (kEpiBufWords - bm_words) / 2;  // candidates that fit next to the bitmap
+  const bool on_chip = (int)padded <= cap;
+  uint32_t* bmp = es.buf;
+  uint32_t* skey = es.buf + bm_words;
+  uint32_t* sidx = skey + cap;
   epi_bar();
-  const int nc = (int)nc_u;
-  auto cand = [&](int i, uint32_t& key, uint32_t& idx) {
-    int qi = 0;
-    while ((uint32_t)i >= es.seg[qi + 1]) ++qi;
-    const uint32_t off = (uint32_t)qi * kItemKeys + ((uint32_t)i - es.seg[qi]);
-    key = __ldcg(R.ckey + off);
-    idx = __ldcg(R.cidx + off);
+  if (et == 0) {
+    fence_proxy_async();
+    uint32_t bytes = (uint32_t)bm_words * 4u;
+    if (on_chip) bytes += padded * 8u;
+    mbar_arrive_expect_tx(&es.bar, bytes);
+    bulk_g2s(bmp, R.bitmap, (uint32_t)bm_words * 4u, &es.bar);
+    if (on_chip)
+      for (int q = 0; q < items; ++q) {
+        const uint32_t b = ((es.cnt[q] + 3) & ~3u) * 4u;
+        if (b) {
+          bulk_g2s(skey + es.seg[q], R.ckey + (size_t)q * kItemKeys, b, &es.bar);
+          bulk_g2s(sidx + es.seg[q], R.cidx + (size_t)q * kItemKeys, b, &es.bar);
+        }
+      }
+  }
+  mbar_wait(&es.bar, bar_phase);
+  bar_phase ^= 1u;
+  // i-th padded slot -> (valid?, key, index); slots past a segment's count are padding
+  auto slot = [&](int i, uint32_t& key, uint32_t& idx) -> bool {
+    int q = 0;
+    while (q + 1 < items && (uint32_t)i >= es.seg[q + 1]) ++q;
+    const uint32_t off = (uint32_t)i - es.seg[q];
+    if (off >= es.cnt[q]) return false;
+    if (on_chip) {
+      key = skey[i];
+      idx = sidx[i];
+    } else {
+      key = __ldcg(R.ckey + (size_t)q * kItemKeys + off);
+      idx = __ldcg(R.cidx + (size_t)q * kItemKeys + off);
+    }
+    return true;
   };
+  const int ns = (int)padded;
   // pass 2 (bits 20..10)
   for (int b = et; b < LYC_BINS; b += kEpiThreads) es.hist[b] = 0u;
   epi_bar();
-  for (int i = et; i < nc; i += kEpiThreads) {
+  for (int i = et; i < ns; i += kEpiThreads) {
     uint32_t key, idx;
-    cand(i, key, idx);
-    atomicAdd(&es.hist[(key >> 10) & 0x7ffu], 1u);
+    if (slot(i, key, idx)) atomicAdd(&es.hist[(key >> 10) & 0x7ffu], 1u);
   }
   epi_bar();
   epi_digit(es, es.hist, false, LYC_BINS, krem, et);
@@ -356,40 +397,37 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int32_t* out
   // pass 3 (bits 9..0)
   for (int b = et; b < 1024; b += kEpiThreads) es.hist[b] = 0u;
   epi_bar();
-  for (int i = et; i < nc; i += kEpiThreads) {
+  for (int i = et; i < ns; i += kEpiThreads) {
     uint32_t key, idx;
-    cand(i, key, idx);
-    if ((key >> 10) == P) atomicAdd(&es.hist[key & 0x3ffu], 1u);
+    if (slot(i, key, idx) && (key >> 10) == P) atomicAdd(&es.hist[key & 0x3ffu], 1u);
   }
   epi_bar();
   epi_digit(es, es.hist, false, 1024, krem, et);
   const uint32_t T = (P << 10) | es.digit;
   krem -= es.above;  // ties of T to take (lowest indices first)
-  // selected candidates join the bitmap
+  // selected candidates join the (on-chip) bitmap, ties in index order
   uint32_t tie_run = 0;
-  for (int b0 = 0; b0 < nc; b0 += kEpiThreads) {
+  for (int b0 = 0; b0 < ns; b0 += kEpiThreads) {
     const int i = b0 + et;
     uint32_t key = 0, idx = 0;
-    if (i < nc) cand(i, key, idx);
-    const bool is_eq = i < nc && key == T;
+    const bool ok = i < ns && slot(i, key, idx);
+    const bool is_eq = ok && key == T;
     uint32_t tot;
     const uint32_t inc = epi_scan(is_eq ? 1u : 0u, es.scan, et, tot);
     const uint32_t rank = tie_run + inc - (is_eq ? 1u : 0u);
-    if (i < nc && (key > T || (is_eq && rank < krem)))
-      atomicOr(R.bitmap + (idx >> 5), 1u << (idx & 31));
+    if (ok && (key > T || (is_eq && rank < krem))) atomicOr(bmp + (idx >> 5), 1u << (idx & 31));
     tie_run += tot;
   }
-  __threadfence();
   epi_bar();
   // ascending emission of the set bits
   const int per = (nwords + kEpiThreads - 1) / kEpiThreads;
   const int w0 = min(nwords, et * per), w1 = min(nwords, w0 + per);
   uint32_t cnt = 0;
-  for (int w = w0; w < w1; ++w) cnt += __popc(__ldcg(R.bitmap + w));
+  for (int w = w0; w < w1; ++w) cnt += __popc(bmp[w]);
   uint32_t tot;
   uint32_t pos = epi_scan(cnt, es.scan, et, tot) - cnt;
   for (int w = w0; w < w1; ++w) {
-    uint32_t m = __ldcg(R.bitmap + w);
+    uint32_t m = bmp[w];
     while (m) {
       const int j = __ffs(m) - 1;
       m &= m - 1;
@@ -513,7 +551,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
           const SelRow R = sel_row(p, l, r);
           if (classify_item(p, R, q, epoch1, es, bar_phase, et)) {
             const int row = __ldg(L.sel_rows + r);
-            finish_row(p, R, p.idx + (int64_t)row * p.idx_stride, es, et);
+            finish_row(p, R, p.idx + (int64_t)row * p.idx_stride, es, bar_phase, et);
             if (et == 0) {
               if (p.idx_count) p.idx_count[row] = p.k_sel;
               stamp(p, l, EV_SELDONE, cta);
