@@ -51,7 +51,8 @@ struct AttnCfg {
   static constexpr int kMergeBytes = kConsumerWarps * kMaxG * (D + 2) * 4;
   static constexpr int kQBytes = kE == 4 ? (kMaxG + 1) * D * 4 : 0;
   static constexpr int kMaxSmem = 232448 - 1024;   // 227 KB opt-in minus alignment slack
-  static constexpr int kExtraBytes = 58 * 1024;    // step kernel's epilogue warps (selection)
+  // the step kernel's epilogue warps (selection); the step kernel is built for d <= 128 only
+  static constexpr int kExtraBytes = D <= 128 ? 58 * 1024 : 0;
   static constexpr int kHistBytes = LYC_BINS * 4;  // per-CTA first-pass selection histogram
   static constexpr int kFixed = kMergeBytes + kQBytes + 512 + kExtraBytes + kHistBytes;
   static constexpr int kStagesRaw = (kMaxSmem - kFixed) / kStageBytes;
