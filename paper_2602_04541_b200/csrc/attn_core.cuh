@@ -350,6 +350,7 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
     for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = 0.f;
     const bool want_sel = s.sel >= 0 && p.sel_mode != SEL_NONE;
     uint32_t* hist = (want_sel && p.hist1) ? p.hist1 + (int64_t)s.sel * LYC_BINS : nullptr;
+    uint32_t* hist16 = (want_sel && p.hist16) ? p.hist16 + (int64_t)s.sel * 65536 : nullptr;
 
     for (int it = un.begin; it < un.end; ++it) {
       for (int sub = 0; sub < tpi; ++sub) {
@@ -393,6 +394,7 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
                   if (ok) {
                     dst[r] = key;
                     if (hist) atomicAdd(sm.hist + (key >> 21), 1u);
+                    if (hist16) atomicAdd(hist16 + (key >> 16), 1u);
                   }
                 }
             }
@@ -495,6 +497,7 @@ __device__ __forceinline__ void consume_units_f32(const LycView& p, const AttnSm
     const int tpi = tiles_per_item(s, p.block_size);
     const bool want_sel = s.sel >= 0 && p.sel_mode != SEL_NONE;
     uint32_t* hist = (want_sel && p.hist1) ? p.hist1 + (int64_t)s.sel * LYC_BINS : nullptr;
+    uint32_t* hist16 = (want_sel && p.hist16) ? p.hist16 + (int64_t)s.sel * 65536 : nullptr;
     float m[kMaxG], l[kMaxG], o[kMaxG][DC];
 #pragma unroll
     for (int j = 0; j < kMaxG; ++j) {
@@ -545,6 +548,7 @@ __device__ __forceinline__ void consume_units_f32(const LycView& p, const AttnSm
               if (valid) {
                 p.sel_keys[(int64_t)s.sel * p.sel_stride + t.lo + t0 + tr] = key;
                 if (hist) atomicAdd(sm.hist + (key >> 21), 1u);
+                if (hist16) atomicAdd(hist16 + (key >> 16), 1u);
               }
             }
           } else {

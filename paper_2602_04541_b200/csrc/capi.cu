@@ -467,6 +467,7 @@ struct lyc_decoder {
   uint32_t* sel_cand = nullptr;
   uint32_t* sel_ccnt = nullptr;
   uint32_t* sel_rowctr = nullptr;
+  uint32_t* hist16 = nullptr;   // [2][B*H][65536] fused 16-bit-prefix histograms
   int stages = 0;               // attention ring stages in use (0 = all; env LYC_STAGES)
   uint32_t* ctr = nullptr;      // [NL][CTR_PER_LAYER] + 2
   unsigned long long* trace = nullptr;  // optional step timeline [NL][8][n_ctas]
@@ -811,6 +812,7 @@ void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, i
   p.sel_cand = d->sel_cand;
   p.sel_ccnt = d->sel_ccnt;
   p.sel_rowctr = d->sel_rowctr;
+  p.hist16 = d->hist16;
   p.ctr = d->ctr;
   p.idx = d->idx;
   p.idx_stride = d->k_cap;
@@ -913,6 +915,10 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
         cuda_check(cudaMalloc(&d->sel_cand, 2 * rows * 2 * d->sel_stride * 4), "cudaMalloc cand");
         cuda_check(cudaMalloc(&d->sel_ccnt, 2 * rows * 64 * 4), "cudaMalloc ccnt");
         cuda_check(cudaMalloc(&d->sel_rowctr, (size_t)d->NL * rows * 16 * 4), "cudaMalloc rowctr");
+        if (c.select_mode == LYC_SELECT_TOKENS) {
+          cuda_check(cudaMalloc(&d->hist16, 2 * rows * 65536 * 4), "cudaMalloc hist16");
+          cuda_check(cudaMemset(d->hist16, 0, 2 * rows * 65536 * 4), "memset");
+        }
         cuda_check(cudaMemset(d->sel_rowctr, 0, (size_t)d->NL * rows * 16 * 4), "memset");
       }
       cuda_check(cudaMalloc(&d->ctr, LYC_CTR_WORDS(d->NL) * 4), "cudaMalloc ctr");
@@ -940,6 +946,7 @@ int lyc_decoder_destroy(lyc_decoder* d) {
   free_dev(d->sel_cand);
   free_dev(d->sel_ccnt);
   free_dev(d->sel_rowctr);
+  free_dev(d->hist16);
   free_dev(d->ctr);
   free_dev(d->trace);
   free_dev(d->part_o);

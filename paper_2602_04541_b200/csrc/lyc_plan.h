@@ -56,6 +56,7 @@ struct LycView {
   float* part_lse;          // [n_units][G]     base-2 log-sum-exp
   uint32_t* sel_keys;       // [n_sel][sel_stride]
   uint32_t* hist1;          // optional [n_sel][LYC_BINS]: fused first radix pass
+  uint32_t* hist16;         // optional [n_sel][65536]: fused 16-bit-prefix histogram
   uint32_t* exec_counts;    // optional [n_slots][counts_stride] per item
   int64_t sel_stride;
   int32_t counts_stride;
@@ -150,6 +151,7 @@ struct LycStepParams {
   uint32_t* sel_keys;        // [2 parity][max_sel][sel_stride]
   int64_t sel_stride;
   uint32_t* hist;            // [2 parity][max_sel][LYC_BINS] fused first-pass histograms
+  uint32_t* hist16;          // [2 parity][max_sel][65536] fused 16-bit-prefix histograms
   uint32_t* sel_bitmap;      // [2 parity][max_sel][bitmap_stride] selected-key bitmaps
   int64_t bitmap_stride;
   uint32_t* sel_cand;        // [2 parity][max_sel][2][sel_stride] boundary-bin candidates

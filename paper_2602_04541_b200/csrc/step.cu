@@ -110,6 +110,8 @@ __device__ __forceinline__ LycView layer_view(const LycStepParams& p, const LycL
   v.sel_keys = p.sel_keys + (int64_t)(l & 1) * p.max_sel * p.sel_stride;
   v.hist1 = p.sel_mode == SEL_TOKEN_KEYS ? p.hist + (int64_t)(l & 1) * p.max_sel * LYC_BINS
                                          : nullptr;
+  v.hist16 = p.sel_mode == SEL_TOKEN_KEYS ? p.hist16 + (int64_t)(l & 1) * p.max_sel * 65536
+                                          : nullptr;
   v.exec_counts = nullptr;
   v.sel_stride = p.sel_stride;
   v.counts_stride = 0;
@@ -135,15 +137,23 @@ __device__ __forceinline__ void find_digit(const uint32_t* h, int nbins, uint32_
   uint32_t cnt[64];
   uint32_t sum = 0;
   const uint4* src = reinterpret_cast<const uint4*>(h + hi - per + 1);
+  if (per >= 4) {
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    if (q * 4 >= per) break;
-    const uint4 v = global ? __ldcg(src + q) : src[q];
-    cnt[4 * q] = v.x;
-    cnt[4 * q + 1] = v.y;
-    cnt[4 * q + 2] = v.z;
-    cnt[4 * q + 3] = v.w;
-    sum += v.x + v.y + v.z + v.w;
+    for (int q = 0; q < 16; ++q) {
+      if (q * 4 >= per) break;
+      const uint4 v = global ? __ldcg(src + q) : src[q];
+      cnt[4 * q] = v.x;
+      cnt[4 * q + 1] = v.y;
+      cnt[4 * q + 2] = v.z;
+      cnt[4 * q + 3] = v.w;
+      sum += v.x + v.y + v.z + v.w;
+    }
+  } else {  // small histograms (< 128 bins)
+    for (int i = 0; i < per; ++i) {
+      const uint32_t* a = h + hi - per + 1 + i;
+      cnt[i] = global ? __ldcg(a) : *a;
+      sum += cnt[i];
+    }
   }
   uint32_t incl = sum;
 #pragma unroll
@@ -218,6 +228,7 @@ __device__ __forceinline__ void epi_digit(EpiSmem& es, const uint32_t* h, bool g
 struct SelRow {
   uint32_t* keys;     // keys of the row [n]
   uint32_t* h1;       // fused first-pass histogram (token mode) or nullptr
+  uint32_t* h16;      // fused 16-bit-prefix histogram [65536] (token mode) or nullptr
   uint32_t* bitmap;   // [n_words]
   uint32_t* ckey;     // [n] candidate keys, item q's segment at q*kItemKeys
   uint32_t* cidx;     // [n] candidate indices
@@ -230,6 +241,7 @@ __device__ __forceinline__ SelRow sel_row(const LycStepParams& p, int l, int r) 
   SelRow s;
   s.keys = p.sel_keys + pr * p.sel_stride;
   s.h1 = p.sel_mode == SEL_TOKEN_KEYS ? p.hist + pr * LYC_BINS : nullptr;
+  s.h16 = (p.sel_mode == SEL_TOKEN_KEYS && p.hist16) ? p.hist16 + pr * 65536 : nullptr;
   s.bitmap = p.sel_bitmap + pr * p.bitmap_stride;
   s.ckey = p.sel_cand + pr * 2 * p.sel_stride;
   s.cidx = s.ckey + p.sel_stride;
@@ -238,32 +250,76 @@ __device__ __forceinline__ SelRow sel_row(const LycStepParams& p, int l, int r) 
   return s;
 }
 
-// Classify item q of one row: keys above the boundary bin set bitmap bits,
+// The boundary prefix of a row.  Token mode: the 11-bit bin d1 from the fused
+// first-pass histogram, refined to 16 bits with the 32 sub-bins of d1 in the
+// fused 16-bit histogram -- the boundary bin then holds ~1e2 keys.  Block mode
+// (one item): the 11-bit bin of the item's own histogram (es.hist).
+// Sets es.digit = prefix, es.above = keys strictly above it, es.last = shift.
+__device__ __forceinline__ void row_prefix(const LycStepParams& p, const SelRow& R, EpiSmem& es,
+                                           int et) {
+  const uint32_t k = (uint32_t)p.k_sel;
+  epi_digit(es, R.h1 ? R.h1 : es.hist, R.h1 != nullptr, LYC_BINS, k, et);
+  if (!R.h16) {
+    if (et == 0) es.last = 21u;
+    epi_bar();
+    return;
+  }
+  const uint32_t d1 = es.digit, a1 = es.above;
+  epi_bar();
+  if (et < 32) {
+    // sub-bins of d1, highest first: lane i holds sub-bin 31 - i
+    const uint32_t c = __ldcg(R.h16 + d1 * 32u + (31u - (uint32_t)et));
+    uint32_t incl = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t n = __shfl_up_sync(0xffffffffu, incl, off);
+      if (et >= off) incl += n;
+    }
+    const uint32_t krem = k - a1;
+    const bool mine = incl - c < krem && krem <= incl;
+    const unsigned who = __ballot_sync(0xffffffffu, mine);
+    const int src = __ffs(who) - 1;
+    const uint32_t above = __shfl_sync(0xffffffffu, incl - c, src);
+    if (et == 0) {
+      es.digit = (d1 << 5) | (31u - (uint32_t)src);
+      es.above = a1 + above;
+      es.last = 16u;
+    }
+  }
+  epi_bar();
+}
+
+// Classify item q of one row: keys above the boundary prefix set bitmap bits,
 // keys inside it become candidates (index order).  Returns true to the whole
 // group if this was the row's last item (the caller then finishes the row).
 __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, uint32_t epoch1,
-                              EpiSmem& es, uint32_t& bar_phase, int et) {
+                              EpiSmem& es, uint32_t& bar_phase, int et, int l, int cta) {
   const int n = p.n_keys;
   const int lo = q * kItemKeys;
   const int cnt = min(kItemKeys, n - lo);
+  const int items = (n + kItemKeys - 1) / kItemKeys;
   if (et == 0) {
     fence_proxy_async();
     const uint32_t bytes = (uint32_t)((cnt + 3) & ~3) * 4u;  // key rows are padded to 4
     mbar_arrive_expect_tx(&es.bar, bytes);
     bulk_g2s(es.buf, R.keys + lo, bytes, &es.bar);
   }
-  // boundary bin d1 (bits 31..21) of the whole row
-  const uint32_t* h = R.h1;
-  if (!h) {  // block mode: the row is a single item -- histogram it here
+  if (!R.h1) {  // block mode: the row is a single item -- histogram it here
     mbar_wait(&es.bar, bar_phase);
     for (int b = et; b < LYC_BINS; b += kEpiThreads) es.hist[b] = 0u;
     epi_bar();
     for (int i = et; i < cnt; i += kEpiThreads) atomicAdd(&es.hist[es.buf[i] >> 21], 1u);
     epi_bar();
-    h = es.hist;
   }
-  epi_digit(es, h, R.h1 != nullptr, LYC_BINS, (uint32_t)p.k_sel, et);
-  const uint32_t d1 = es.digit;
+  row_prefix(p, R, es, et);
+  const uint32_t P = es.digit;
+  const int shift = (int)es.last;
+  if (R.h16) {  // reset this item's share of the 16-bit histogram, except d1's sub-bins
+    const int b0 = q * (65536 / items), b1 = (q == items - 1) ? 65536 : (q + 1) * (65536 / items);
+    const int keep0 = (int)(P >> 5) * 32, keep1 = keep0 + 32;
+    for (int b = b0 + et; b < b1; b += kEpiThreads)
+      if (b < keep0 || b >= keep1) R.h16[b] = 0u;
+  }
   mbar_wait(&es.bar, bar_phase);
   bar_phase ^= 1u;
   // thread et owns 128 consecutive keys = 4 bitmap words, read as rotated 16-B
@@ -281,9 +337,9 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
       for (int e = 0; e < 4; ++e) {
         const int j = qq * 4 + e;
         const bool ok = k0 + w * 32 + j < cnt;
-        const uint32_t top = kv[e] >> 21;
-        words[w] |= (ok && top > d1) ? (1u << j) : 0u;
-        eqm[w] |= (ok && top == d1) ? (1u << j) : 0u;
+        const uint32_t pre = kv[e] >> shift;
+        words[w] |= (ok && pre > P) ? (1u << j) : 0u;
+        eqm[w] |= (ok && pre == P) ? (1u << j) : 0u;
       }
     }
   }
@@ -309,7 +365,6 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
   epi_bar();
   if (et == 0) {
     __threadfence();
-    const int items = (n + kItemKeys - 1) / kItemKeys;
     const uint32_t old = atomicAdd(R.ctr, 1u);
     es.last = old == epoch1 * (uint32_t)items - 1u;
     if (es.last) __threadfence();  // acquire the other items' writes
@@ -320,21 +375,20 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
 
 // Finish one row after its last item.  One thread bulk-copies the row's bitmap
 // and every item's candidate segment (keys and indices, 16-B aligned) into
-// shared memory -- all copies in flight at once -- then radix passes 2-3 run
-// on the candidates, the selected ones join the bitmap, and the set bits are
-// emitted in ascending order.  Rows whose boundary bin holds more candidates
-// than fit on chip fall back to reading them from L2.
+// shared memory -- all copies in flight at once -- then the radix finishes on
+// the candidates (<= 11 bits per pass), the selected ones join the bitmap, and
+// the set bits are emitted in ascending order.  Rows whose boundary bin holds
+// more candidates than fit on chip read them from L2 instead.
 __device__ void finish_row(const LycStepParams& p, const SelRow& R, int32_t* out, EpiSmem& es,
-                           uint32_t& bar_phase, int et) {
+                           uint32_t& bar_phase, int et, int l, int cta) {
   const int n = p.n_keys;
   const int items = (n + kItemKeys - 1) / kItemKeys;
   const int nwords = (n + 31) / 32;
   const int bm_words = (nwords + 3) & ~3;
-  uint32_t krem = (uint32_t)p.k_sel;
-  // boundary bin again (block mode: es.hist still holds the item histogram)
-  epi_digit(es, R.h1 ? R.h1 : es.hist, R.h1 != nullptr, LYC_BINS, krem, et);
-  const uint32_t d1 = es.digit;
-  krem -= es.above;
+  row_prefix(p, R, es, et);  // block mode: es.hist still holds the item histogram
+  uint32_t P = es.digit;
+  int shift = (int)es.last;
+  uint32_t krem = (uint32_t)p.k_sel - es.above;
   // candidate segments: item q's candidates land at smem [seg[q], seg[q] + cnt[q])
   const uint32_t c_mine = et < items ? __ldcg(R.ccnt + et) : 0u;
   const uint32_t c_pad = (c_mine + 3) & ~3u;
@@ -344,7 +398,7 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int32_t* out
     es.seg[et] = incl - c_pad;
     es.cnt[et] = c_mine;
   }
-  const int cap = (kEpiBufWords - bm_words) / 2;  // candidates that fit next to the bitmap
+  const int cap = ((kEpiBufWords - bm_words) / 2) & ~3;  // candidates that fit next to the bitmap
   const bool on_chip = (int)padded <= cap;
   uint32_t* bmp = es.buf;
   uint32_t* skey = es.buf + bm_words;
@@ -367,6 +421,7 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int32_t* out
   }
   mbar_wait(&es.bar, bar_phase);
   bar_phase ^= 1u;
+  if (et == 0) stamp(p, l, EV_SEL2, cta);
   // i-th padded slot -> (valid?, key, index); slots past a segment's count are padding
   auto slot = [&](int i, uint32_t& key, uint32_t& idx) -> bool {
     int q = 0;
@@ -383,28 +438,25 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int32_t* out
     return true;
   };
   const int ns = (int)padded;
-  // pass 2 (bits 20..10)
-  for (int b = et; b < LYC_BINS; b += kEpiThreads) es.hist[b] = 0u;
-  epi_bar();
-  for (int i = et; i < ns; i += kEpiThreads) {
-    uint32_t key, idx;
-    if (slot(i, key, idx)) atomicAdd(&es.hist[(key >> 10) & 0x7ffu], 1u);
+  // remaining radix passes over the candidates (<= 11 bits each)
+  while (shift > 0) {
+    const int wbits = shift > 11 ? 11 : shift;
+    shift -= wbits;
+    const uint32_t mask = (1u << wbits) - 1u;
+    for (int b = et; b < (1 << wbits); b += kEpiThreads) es.hist[b] = 0u;
+    epi_bar();
+    for (int i = et; i < ns; i += kEpiThreads) {
+      uint32_t key, idx;
+      if (slot(i, key, idx) && (key >> (shift + wbits)) == P)
+        atomicAdd(&es.hist[(key >> shift) & mask], 1u);
+    }
+    epi_bar();
+    epi_digit(es, es.hist, false, 1 << wbits, krem, et);
+    P = (P << wbits) | es.digit;
+    krem -= es.above;
   }
-  epi_bar();
-  epi_digit(es, es.hist, false, LYC_BINS, krem, et);
-  const uint32_t P = (d1 << 11) | es.digit;
-  krem -= es.above;
-  // pass 3 (bits 9..0)
-  for (int b = et; b < 1024; b += kEpiThreads) es.hist[b] = 0u;
-  epi_bar();
-  for (int i = et; i < ns; i += kEpiThreads) {
-    uint32_t key, idx;
-    if (slot(i, key, idx) && (key >> 10) == P) atomicAdd(&es.hist[key & 0x3ffu], 1u);
-  }
-  epi_bar();
-  epi_digit(es, es.hist, false, 1024, krem, et);
-  const uint32_t T = (P << 10) | es.digit;
-  krem -= es.above;  // ties of T to take (lowest indices first)
+  const uint32_t T = P;  // the k-th largest key; krem of its ties are taken
+  if (et == 0) stamp(p, l, EV_SEL0, cta);
   // selected candidates join the (on-chip) bitmap, ties in index order
   uint32_t tie_run = 0;
   for (int b0 = 0; b0 < ns; b0 += kEpiThreads) {
@@ -419,6 +471,7 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int32_t* out
     tie_run += tot;
   }
   epi_bar();
+  if (et == 0) stamp(p, l, EV_SEL1, cta);
   // ascending emission of the set bits
   const int per = (nwords + kEpiThreads - 1) / kEpiThreads;
   const int w0 = min(nwords, et * per), w1 = min(nwords, w0 + per);
@@ -437,6 +490,7 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int32_t* out
   // reset the per-row inputs for their next use
   if (R.h1)
     for (int b = et; b < LYC_BINS; b += kEpiThreads) R.h1[b] = 0u;
+  if (R.h16 && et < 32) R.h16[(T >> 21) * 32u + (uint32_t)et] = 0u;  // d1's sub-bins
   if (p.sel_mode == SEL_BLOCK_KEYS)
     for (int i = et; i < n; i += kEpiThreads) R.keys[i] = 0u;
   epi_bar();
@@ -549,9 +603,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
         for (int it = cta; it < n_items; it += p.n_ctas) {
           const int r = it / items, q = it - r * items;
           const SelRow R = sel_row(p, l, r);
-          if (classify_item(p, R, q, epoch1, es, bar_phase, et)) {
+          if (classify_item(p, R, q, epoch1, es, bar_phase, et, l, cta)) {
             const int row = __ldg(L.sel_rows + r);
-            finish_row(p, R, p.idx + (int64_t)row * p.idx_stride, es, bar_phase, et);
+            finish_row(p, R, p.idx + (int64_t)row * p.idx_stride, es, bar_phase, et, l, cta);
             if (et == 0) {
               if (p.idx_count) p.idx_count[row] = p.k_sel;
               stamp(p, l, EV_SELDONE, cta);
