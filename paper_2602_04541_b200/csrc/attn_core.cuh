@@ -54,7 +54,7 @@ struct AttnCfg {
   // the step kernel's epilogue warps (selection); the step kernel is built for d <= 128 only
   static constexpr int kExtraBytes = D <= 128 ? 58 * 1024 : 0;
   static constexpr int kHistBytes = LYC_BINS * 4;  // per-CTA first-pass selection histogram
-  static constexpr int kFixed = kMergeBytes + kQBytes + 512 + kExtraBytes + kHistBytes;
+  static constexpr int kFixed = kMergeBytes + kQBytes + 512 + kExtraBytes + kHistBytes;  // 512: barriers + 128-B alignment
   static constexpr int kStagesRaw = (kMaxSmem - kFixed) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kSmem = kStages * kStageBytes + kFixed + 1024;
@@ -82,20 +82,33 @@ struct AttnSmem {
   uint8_t* extra;  // kExtraBytes scratch for other warp roles
   uint32_t* hist;  // [LYC_BINS] first radix pass of the unit's selection keys (zero between units)
 
+  // Offsets are applied to the __shared__ array itself (no integer round trip),
+  // so the compiler keeps the shared address space and emits LDS/STS/ATOMS --
+  // generic accesses would queue behind the thread's outstanding global stores.
+  static constexpr int kMoOff = 0;
+  static constexpr int kMlOff = kMoOff + kConsumerWarps * kMaxG * D * 4;
+  static constexpr int kQsOff = kMlOff + kConsumerWarps * kMaxG * 2 * 4;
+  static constexpr int kBarOff = kQsOff + AttnCfg<T, D>::kQBytes;
+  static constexpr int kExtraOff =
+      (kBarOff + 2 * AttnCfg<T, D>::kStages * 8 + 127) & ~127;
+  static constexpr int kHistOff = kExtraOff + AttnCfg<T, D>::kExtraBytes;
+
+  static_assert(kHistOff + AttnCfg<T, D>::kHistBytes + 1024 <= AttnCfg<T, D>::kSmem -
+                    AttnCfg<T, D>::kStages * AttnCfg<T, D>::kStageBytes,
+                "shared-memory carve exceeds the allocation");
   __device__ __forceinline__ static AttnSmem carve(uint8_t* raw) {
     using C = AttnCfg<T, D>;
     AttnSmem s;
-    uint8_t* base = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* base = raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
     s.ring = base;
-    s.mo = reinterpret_cast<float*>(base + C::kStages * C::kStageBytes);
-    s.ml = s.mo + kConsumerWarps * kMaxG * D;
-    s.qs = s.ml + kConsumerWarps * kMaxG * 2;
-    s.full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(s.qs) + C::kQBytes);
+    uint8_t* fx = base + C::kStages * C::kStageBytes;
+    s.mo = reinterpret_cast<float*>(fx + kMoOff);
+    s.ml = reinterpret_cast<float*>(fx + kMlOff);
+    s.qs = reinterpret_cast<float*>(fx + kQsOff);
+    s.full = reinterpret_cast<uint64_t*>(fx + kBarOff);
     s.empty = s.full + C::kStages;
-    s.extra = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(s.empty + C::kStages) + 127) & ~static_cast<uintptr_t>(127));
-    s.hist = reinterpret_cast<uint32_t*>(s.extra + C::kExtraBytes);
+    s.extra = fx + kExtraOff;
+    s.hist = reinterpret_cast<uint32_t*>(fx + kHistOff);
     return s;
   }
 };

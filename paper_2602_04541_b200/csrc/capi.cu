@@ -28,6 +28,7 @@ cudaError_t launch_float_keys(const float* s, uint32_t* keys, int64_t n, cudaStr
 cudaError_t launch_step(const LycStepParams& p, int dtype, int d, cudaStream_t st);
 bool step_supported(int dtype, int d);
 int64_t step_max_keys();
+int64_t step_bitmap_words(int64_t n_keys);
 int step_item_keys();
 }  // namespace lyc
 
@@ -470,7 +471,7 @@ struct lyc_decoder {
   uint32_t* hist16 = nullptr;   // [2][B*H][65536] fused 16-bit-prefix histograms
   int stages = 0;               // attention ring stages in use (0 = all; env LYC_STAGES)
   uint32_t* ctr = nullptr;      // [NL][CTR_PER_LAYER] + 2
-  unsigned long long* trace = nullptr;  // optional step timeline [NL][8][n_ctas]
+  unsigned long long* trace = nullptr;  // optional step timeline [NL][LYC_TRACE_EVENTS][n_ctas]
   float* part_o = nullptr;
   float* part_lse = nullptr;
   size_t part_units = 0;
@@ -910,7 +911,7 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
       cuda_check(cudaMalloc(&d->hist, 2 * rows * LYC_BINS * 4), "cudaMalloc hist");
       cuda_check(cudaMemset(d->hist, 0, 2 * rows * LYC_BINS * 4), "memset");
       if (d->fused && c.select_mode != LYC_SELECT_NONE) {  // pooled-selection scratch
-        d->bitmap_stride = ((d->sel_stride + 31) / 32 + 3) & ~(int64_t)3;
+        d->bitmap_stride = (lyc::step_bitmap_words(d->sel_stride) + 3) & ~(int64_t)3;
         cuda_check(cudaMalloc(&d->sel_bitmap, 2 * rows * d->bitmap_stride * 4), "cudaMalloc bitmap");
         cuda_check(cudaMalloc(&d->sel_cand, 2 * rows * 2 * d->sel_stride * 4), "cudaMalloc cand");
         cuda_check(cudaMalloc(&d->sel_ccnt, 2 * rows * 64 * 4), "cudaMalloc ccnt");
@@ -1104,8 +1105,8 @@ int lyc_decoder_set_trace(lyc_decoder* d, int enable) {
   return (int)guarded([&]() -> int64_t {
     if (!d) fail(LYC_EINVAL, "decoder: null");
     if (enable && !d->trace) {
-      cuda_check(cudaMalloc(&d->trace, (size_t)d->NL * 8 * d->n_ctas() * 8), "cudaMalloc trace");
-      cuda_check(cudaMemset(d->trace, 0, (size_t)d->NL * 8 * d->n_ctas() * 8), "memset trace");
+      cuda_check(cudaMalloc(&d->trace, (size_t)d->NL * LYC_TRACE_EVENTS * d->n_ctas() * 8), "cudaMalloc trace");
+      cuda_check(cudaMemset(d->trace, 0, (size_t)d->NL * LYC_TRACE_EVENTS * d->n_ctas() * 8), "memset trace");
     }
     if (!enable) {
       free_dev(d->trace);
@@ -1119,7 +1120,7 @@ int64_t lyc_decoder_trace(lyc_decoder* d, unsigned long long* out, int64_t cap) 
   return guarded([&]() -> int64_t {
     if (!d) fail(LYC_EINVAL, "decoder: null");
     if (!d->trace) fail(LYC_ESTATE, "decoder: tracing is off");
-    const int64_t n = (int64_t)d->NL * 8 * d->n_ctas();
+    const int64_t n = (int64_t)d->NL * LYC_TRACE_EVENTS * d->n_ctas();
     if (!out) return n;  // size query
     if (cap < n) fail(LYC_EINVAL, "decoder: trace buffer too small");
     cuda_check(cudaMemcpy(out, d->trace, (size_t)n * 8, cudaMemcpyDeviceToHost), "D2H trace");

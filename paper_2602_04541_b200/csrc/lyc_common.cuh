@@ -39,6 +39,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
                : "memory");
 }
 
+// Predicated stores without a branch (a guarded store in a hot unrolled loop
+// otherwise becomes divergent control flow).
+__device__ __forceinline__ void st_shared_pred(uint32_t addr, uint32_t v, bool ok) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u32 [%0], %1;\n\t}" ::"r"(addr),
+               "r"(v), "r"((uint32_t)ok)
+               : "memory");
+}
+__device__ __forceinline__ void st_global_pred(int32_t* ptr, uint32_t v, bool ok) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.global.u32 [%0], %1;\n\t}" ::"l"(ptr),
+               "r"(v), "r"((uint32_t)ok)
+               : "memory");
+}
+
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t phase) {
   uint32_t ok;
   asm volatile(

@@ -17,6 +17,7 @@
 
 #define LYC_TILE 64
 #define LYC_BINS 2048
+#define LYC_TRACE_EVENTS 16  // step-timeline stamps per layer per CTA
 
 enum { ITEM_DENSE = 0, ITEM_BLOCKS = 1, ITEM_TOKENS = 2 };
 

@@ -37,6 +37,7 @@ constexpr int kEpiWarps = 2;
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kStepThreads = (kConsumerWarps + kProducerWarps + kEpiWarps) * 32;
 constexpr int kItemKeys = 8192;  // keys per selection item (32 KB, one TMA bulk copy)
+constexpr int kRankMax = 384;    // boundary-bin candidates resolved by direct ranking
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
@@ -68,12 +69,13 @@ __device__ __forceinline__ void signal(uint32_t* ctr) {
 __device__ __forceinline__ void epi_bar() { group_bar(2, kEpiThreads); }
 
 // Debug timeline: %globaltimer (ns) of event ev of layer l on CTA `cta`.
-enum { EV_CONS_BEGIN = 0, EV_CONS_END, EV_EPI_ATTN, EV_MERGE, EV_SEL0, EV_SEL1, EV_SEL2, EV_SELDONE };
+enum { EV_CONS_BEGIN = 0, EV_CONS_END, EV_EPI_ATTN, EV_MERGE, EV_SEL0, EV_SEL1, EV_SEL2, EV_SELDONE,
+       EV_C_PREFIX, EV_C_KEYS, EV_C_DONE, EV_F_PREFIX, EV_F_SCAN, EV_F_EMIT, EV_X0, EV_X1 };
 __device__ __forceinline__ void stamp(const LycStepParams& p, int l, int ev, int cta) {
   if (p.trace) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.trace[((size_t)l * 8 + ev) * p.n_ctas + cta] = t;
+    p.trace[((size_t)l * LYC_TRACE_EVENTS + ev) * p.n_ctas + cta] = t;
   }
 }
 
@@ -181,6 +183,12 @@ __device__ __forceinline__ void find_digit(const uint32_t* h, int nbins, uint32_
   above = __shfl_sync(0xffffffffu, a, src_lane);
 }
 
+// Selection bitmaps (global and on chip) are stored in 64-word chunks at a
+// 68-word stride: the finisher's thread t reads chunk t as 16-B vectors, and
+// the 4-word skew makes those reads bank-conflict-free.
+__host__ __device__ __forceinline__ int bm_pad(int w) { return w + (w >> 6) * 4; }
+__host__ __device__ __forceinline__ int bm_padded_words(int nwords) { return (nwords + 63) / 64 * 68; }
+
 // Epilogue scratch (inside AttnSmem::extra).
 constexpr int kEpiBufWords = 12288;  // 48 KB
 struct EpiSmem {
@@ -193,6 +201,7 @@ struct EpiSmem {
   uint32_t cnt[72];          // finish: candidates of each item
   uint64_t bar;
   uint32_t digit, above, last, pad;
+  uint32_t pfx, pabove, pshift, pad2;  // the row's boundary prefix (classify -> finish)
 };
 
 // 64-thread inclusive scan (2 warps).
@@ -312,8 +321,14 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
     epi_bar();
   }
   row_prefix(p, R, es, et);
+  if (et == 0) stamp(p, l, EV_C_PREFIX, cta);
   const uint32_t P = es.digit;
   const int shift = (int)es.last;
+  if (et == 0) {  // kept for finish_row (this CTA finishes the row if its item is the last)
+    es.pfx = P;
+    es.pabove = es.above;
+    es.pshift = (uint32_t)shift;
+  }
   if (R.h16) {  // reset this item's share of the 16-bit histogram, except d1's sub-bins
     const int b0 = q * (65536 / items), b1 = (q == items - 1) ? 65536 : (q + 1) * (65536 / items);
     const int keep0 = (int)(P >> 5) * 32, keep1 = keep0 + 32;
@@ -322,6 +337,7 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
   }
   mbar_wait(&es.bar, bar_phase);
   bar_phase ^= 1u;
+  if (et == 0) stamp(p, l, EV_C_KEYS, cta);
   // thread et owns 128 consecutive keys = 4 bitmap words, read as rotated 16-B
   // vectors (conflict-free)
   uint32_t words[4] = {0u, 0u, 0u, 0u}, eqm[4] = {0u, 0u, 0u, 0u};
@@ -345,7 +361,7 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
   }
 #pragma unroll
   for (int w = 0; w < 4; ++w)
-    if (k0 + w * 32 < cnt) R.bitmap[(lo + k0) / 32 + w] = words[w];
+    if (k0 + w * 32 < cnt) R.bitmap[bm_pad((lo + k0) / 32 + w)] = words[w];
   const uint32_t c = __popc(eqm[0]) + __popc(eqm[1]) + __popc(eqm[2]) + __popc(eqm[3]);
   uint32_t total;
   uint32_t pos = epi_scan(c, es.scan, et, total) - c;
@@ -361,9 +377,18 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
       ++pos;
     }
   }
-  if (et == 0) R.ccnt[q] = total;
+  if (et == 0) {
+    R.ccnt[q] = total;
+    // pad the segment to a multiple of 4 with sentinels (index ~0, key 0: never
+    // ranks above a real candidate) so the finisher can scan padded slots blindly
+    for (uint32_t i = total; i < ((total + 3u) & ~3u); ++i) {
+      R.ckey[lo + i] = 0u;
+      R.cidx[lo + i] = 0xFFFFFFFFu;
+    }
+  }
   epi_bar();
   if (et == 0) {
+    stamp(p, l, EV_C_DONE, cta);
     __threadfence();
     const uint32_t old = atomicAdd(R.ctr, 1u);
     es.last = old == epoch1 * (uint32_t)items - 1u;
@@ -384,11 +409,12 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int32_t* out
   const int n = p.n_keys;
   const int items = (n + kItemKeys - 1) / kItemKeys;
   const int nwords = (n + 31) / 32;
-  const int bm_words = (nwords + 3) & ~3;
-  row_prefix(p, R, es, et);  // block mode: es.hist still holds the item histogram
-  uint32_t P = es.digit;
-  int shift = (int)es.last;
-  uint32_t krem = (uint32_t)p.k_sel - es.above;
+  const int bm_words = bm_padded_words(nwords);
+  // the boundary prefix this CTA computed while classifying the row's last item
+  uint32_t P = es.pfx;
+  int shift = (int)es.pshift;
+  uint32_t krem = (uint32_t)p.k_sel - es.pabove;
+  if (et == 0) stamp(p, l, EV_F_PREFIX, cta);
   // candidate segments: item q's candidates land at smem [seg[q], seg[q] + cnt[q])
   const uint32_t c_mine = et < items ? __ldcg(R.ccnt + et) : 0u;
   const uint32_t c_pad = (c_mine + 3) & ~3u;
@@ -405,6 +431,7 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int32_t* out
   uint32_t* sidx = skey + cap;
   epi_bar();
   if (et == 0) {
+    stamp(p, l, EV_F_SCAN, cta);
     fence_proxy_async();
     uint32_t bytes = (uint32_t)bm_words * 4u;
     if (on_chip) bytes += padded * 8u;
@@ -438,59 +465,146 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int32_t* out
     return true;
   };
   const int ns = (int)padded;
-  // remaining radix passes over the candidates (<= 11 bits each)
-  while (shift > 0) {
-    const int wbits = shift > 11 ? 11 : shift;
-    shift -= wbits;
-    const uint32_t mask = (1u << wbits) - 1u;
-    for (int b = et; b < (1 << wbits); b += kEpiThreads) es.hist[b] = 0u;
-    epi_bar();
-    for (int i = et; i < ns; i += kEpiThreads) {
-      uint32_t key, idx;
-      if (slot(i, key, idx) && (key >> (shift + wbits)) == P)
-        atomicAdd(&es.hist[(key >> shift) & mask], 1u);
+  if (on_chip && ns <= kRankMax) {
+    // Few candidates (the usual case: the 16-bit boundary bin of a smooth score
+    // distribution holds ~1e2 keys): exact rank of every candidate among the
+    // others -- greater key, or equal key and lower index (attention.hpp:115-119)
+    // -- with broadcast smem reads; the krem best join the bitmap.
+    for (int i0 = 0; i0 < ns; i0 += kEpiThreads) {
+      const int i = i0 + et;
+      const uint32_t ki = i < ns ? skey[i] : 0u;
+      const uint32_t xi = i < ns ? sidx[i] : 0xFFFFFFFFu;
+      uint32_t rank = 0;
+      for (int j = 0; j < ns; j += 4) {
+        const uint4 kj = *reinterpret_cast<const uint4*>(skey + j);
+        const uint4 xj = *reinterpret_cast<const uint4*>(sidx + j);
+        rank += (kj.x > ki || (kj.x == ki && xj.x < xi)) ? 1u : 0u;
+        rank += (kj.y > ki || (kj.y == ki && xj.y < xi)) ? 1u : 0u;
+        rank += (kj.z > ki || (kj.z == ki && xj.z < xi)) ? 1u : 0u;
+        rank += (kj.w > ki || (kj.w == ki && xj.w < xi)) ? 1u : 0u;
+      }
+      if (xi != 0xFFFFFFFFu && rank < krem) atomicOr(bmp + bm_pad((int)(xi >> 5)), 1u << (xi & 31));
     }
     epi_bar();
-    epi_digit(es, es.hist, false, 1 << wbits, krem, et);
-    P = (P << wbits) | es.digit;
-    krem -= es.above;
+    if (et == 0) {
+      stamp(p, l, EV_SEL0, cta);
+      stamp(p, l, EV_SEL1, cta);
+    }
+  } else {
+    // remaining radix passes over the candidates (<= 11 bits each)
+    while (shift > 0) {
+      const int wbits = shift > 11 ? 11 : shift;
+      shift -= wbits;
+      const uint32_t mask = (1u << wbits) - 1u;
+      for (int b = et; b < (1 << wbits); b += kEpiThreads) es.hist[b] = 0u;
+      epi_bar();
+      for (int i = et; i < ns; i += kEpiThreads) {
+        uint32_t key, idx;
+        if (slot(i, key, idx) && (key >> (shift + wbits)) == P)
+          atomicAdd(&es.hist[(key >> shift) & mask], 1u);
+      }
+      epi_bar();
+      epi_digit(es, es.hist, false, 1 << wbits, krem, et);
+      P = (P << wbits) | es.digit;
+      krem -= es.above;
+    }
+    const uint32_t T = P;  // the k-th largest key; krem of its ties are taken
+    if (et == 0) stamp(p, l, EV_SEL0, cta);
+    // selected candidates join the (on-chip) bitmap, ties in index order
+    uint32_t tie_run = 0;
+    for (int b0 = 0; b0 < ns; b0 += kEpiThreads) {
+      const int i = b0 + et;
+      uint32_t key = 0, idx = 0;
+      const bool ok = i < ns && slot(i, key, idx);
+      const bool is_eq = ok && key == T;
+      uint32_t tot;
+      const uint32_t inc = epi_scan(is_eq ? 1u : 0u, es.scan, et, tot);
+      const uint32_t rank = tie_run + inc - (is_eq ? 1u : 0u);
+      if (ok && (key > T || (is_eq && rank < krem)))
+        atomicOr(bmp + bm_pad((int)(idx >> 5)), 1u << (idx & 31));
+      tie_run += tot;
+    }
+    epi_bar();
+    if (et == 0) stamp(p, l, EV_SEL1, cta);
   }
-  const uint32_t T = P;  // the k-th largest key; krem of its ties are taken
-  if (et == 0) stamp(p, l, EV_SEL0, cta);
-  // selected candidates join the (on-chip) bitmap, ties in index order
-  uint32_t tie_run = 0;
-  for (int b0 = 0; b0 < ns; b0 += kEpiThreads) {
-    const int i = b0 + et;
-    uint32_t key = 0, idx = 0;
-    const bool ok = i < ns && slot(i, key, idx);
-    const bool is_eq = ok && key == T;
+  // ascending emission of the set bits.  Thread t owns a contiguous run of
+  // 64-word chunks, read 16 words at a time into registers (conflict-free
+  // 16-B loads thanks to the padded layout); one 64-thread scan of the
+  // per-thread popcounts gives every thread its output offset.  Indices are
+  // staged on chip and copied out coalesced (or stored directly when the
+  // staging area is too small).
+  {
+    const int nchunks = (nwords + 63) / 64;
+    const int cper = (nchunks + kEpiThreads - 1) / kEpiThreads;
+    const int c0 = min(nchunks, et * cper), c1 = min(nchunks, c0 + cper);
+    auto quarter = [&](int c, int qq, uint32_t (&wv)[16]) {
+      const uint4* src = reinterpret_cast<const uint4*>(bmp + c * 68 + qq * 16);
+      const int lim = nwords - (c * 64 + qq * 16);  // words past the row end are garbage
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const uint4 x = src[v];
+        wv[4 * v] = 4 * v < lim ? x.x : 0u;
+        wv[4 * v + 1] = 4 * v + 1 < lim ? x.y : 0u;
+        wv[4 * v + 2] = 4 * v + 2 < lim ? x.z : 0u;
+        wv[4 * v + 3] = 4 * v + 3 < lim ? x.w : 0u;
+      }
+    };
+    uint32_t cnt = 0;
+    for (int c = c0; c < c1; ++c)
+      for (int qq = 0; qq < 4; ++qq) {
+        uint32_t wv[16];
+        quarter(c, qq, wv);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) cnt += __popc(wv[i]);
+      }
     uint32_t tot;
-    const uint32_t inc = epi_scan(is_eq ? 1u : 0u, es.scan, et, tot);
-    const uint32_t rank = tie_run + inc - (is_eq ? 1u : 0u);
-    if (ok && (key > T || (is_eq && rank < krem))) atomicOr(bmp + (idx >> 5), 1u << (idx & 31));
-    tie_run += tot;
-  }
-  epi_bar();
-  if (et == 0) stamp(p, l, EV_SEL1, cta);
-  // ascending emission of the set bits
-  const int per = (nwords + kEpiThreads - 1) / kEpiThreads;
-  const int w0 = min(nwords, et * per), w1 = min(nwords, w0 + per);
-  uint32_t cnt = 0;
-  for (int w = w0; w < w1; ++w) cnt += __popc(bmp[w]);
-  uint32_t tot;
-  uint32_t pos = epi_scan(cnt, es.scan, et, tot) - cnt;
-  for (int w = w0; w < w1; ++w) {
-    uint32_t m = bmp[w];
-    while (m) {
-      const int j = __ffs(m) - 1;
-      m &= m - 1;
-      out[pos++] = w * 32 + j;
+    const uint32_t pos0 = epi_scan(cnt, es.scan, et, tot) - cnt;
+    if (et == 0) stamp(p, l, EV_X0, cta);
+    const int k_out = p.k_sel;
+    const bool staged = bm_words + k_out <= kEpiBufWords;
+    // Per word: the first four set bits are stored with predicated,
+    // branch-free stores (a divergent per-bit loop costs ~10x more); words
+    // with more bits (rare at top-k densities) finish in a short loop.
+    auto emit = [&](auto store) {
+      uint32_t pos = pos0;
+      for (int c = c0; c < c1; ++c)
+        for (int qq = 0; qq < 4; ++qq) {
+          uint32_t wv[16];
+          quarter(c, qq, wv);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const uint32_t m0 = wv[i];
+            const uint32_t base = (uint32_t)(c * 64 + qq * 16 + i) * 32u;
+            const uint32_t m1 = m0 & (m0 - 1u), m2 = m1 & (m1 - 1u), m3 = m2 & (m2 - 1u);
+            uint32_t m4 = m3 & (m3 - 1u);
+            store(pos, base + (uint32_t)(__ffs(m0) - 1), m0 != 0u);
+            store(pos + 1u, base + (uint32_t)(__ffs(m1) - 1), m1 != 0u);
+            store(pos + 2u, base + (uint32_t)(__ffs(m2) - 1), m2 != 0u);
+            store(pos + 3u, base + (uint32_t)(__ffs(m3) - 1), m3 != 0u);
+            uint32_t p4 = pos + 4u;
+            pos += __popc(m0);
+            while (m4) {
+              store(p4++, base + (uint32_t)(__ffs(m4) - 1), true);
+              m4 &= m4 - 1u;
+            }
+          }
+        }
+    };
+    if (staged) {
+      uint32_t* stg = bmp + bm_words;
+      const uint32_t sb = smem_u32(stg);
+      emit([&](uint32_t i, uint32_t v, bool ok) { st_shared_pred(sb + 4u * i, v, ok); });
+      epi_bar();
+      for (int i = et; i < k_out; i += kEpiThreads) out[i] = (int32_t)stg[i];
+    } else {
+      emit([&](uint32_t i, uint32_t v, bool ok) { st_global_pred(out + i, v, ok); });
     }
   }
+  if (et == 0) stamp(p, l, EV_F_EMIT, cta);
   // reset the per-row inputs for their next use
   if (R.h1)
     for (int b = et; b < LYC_BINS; b += kEpiThreads) R.h1[b] = 0u;
-  if (R.h16 && et < 32) R.h16[(T >> 21) * 32u + (uint32_t)et] = 0u;  // d1's sub-bins
+  if (R.h16 && et < 32) R.h16[(es.pfx >> (21u - es.pshift)) * 32u + (uint32_t)et] = 0u;  // d1's sub-bins
   if (p.sel_mode == SEL_BLOCK_KEYS)
     for (int i = et; i < n; i += kEpiThreads) R.keys[i] = 0u;
   epi_bar();
@@ -663,8 +777,14 @@ cudaError_t launch_step(const LycStepParams& p, int dtype, int d, cudaStream_t s
   return cudaErrorInvalidValue;
 }
 
-// Largest selection row (keys) the fused step supports: <= 64 items per row.
-int64_t step_max_keys() { return (int64_t)64 * kItemKeys; }
+// Largest selection row (keys) the fused step supports.
+int64_t step_max_keys() {
+  // the finisher holds the row's padded bitmap on chip
+  int64_t n = (int64_t)64 * kItemKeys;
+  while (bm_padded_words((int)((n + 31) / 32)) > kEpiBufWords) n -= kItemKeys;
+  return n;
+}
+int64_t step_bitmap_words(int64_t n_keys) { return bm_padded_words((int)((n_keys + 31) / 32)); }
 int step_item_keys() { return kItemKeys; }
 
 bool step_supported(int dtype, int d) {
