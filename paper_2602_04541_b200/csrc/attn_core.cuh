@@ -53,7 +53,7 @@ struct AttnCfg {
   static constexpr int kMaxSmem = 232448 - 1024;   // 227 KB opt-in minus alignment slack
   // the step kernel's epilogue warps (selection); the step kernel is built for d <= 128 only
   static constexpr int kExtraBytes = D <= 128 ? 58 * 1024 : 0;
-  static constexpr int kHistBytes = LYC_BINS * 4;  // per-CTA first-pass selection histogram
+  static constexpr int kHistBytes = LYC_H1_BINS * 4;  // per-CTA first-pass selection histogram
   static constexpr int kFixed = kMergeBytes + kQBytes + 512 + kExtraBytes + kHistBytes;  // 512: barriers + 128-B alignment
   static constexpr int kStagesRaw = (kMaxSmem - kFixed) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
@@ -80,7 +80,7 @@ struct AttnSmem {
   uint64_t* full;
   uint64_t* empty;
   uint8_t* extra;  // kExtraBytes scratch for other warp roles
-  uint32_t* hist;  // [LYC_BINS] first radix pass of the unit's selection keys (zero between units)
+  uint32_t* hist;  // [LYC_H1_BINS] first radix pass of the unit's selection keys (zero between units)
 
   // Offsets are applied to the __shared__ array itself (no integer round trip),
   // so the compiler keeps the shared address space and emits LDS/STS/ATOMS --
@@ -301,14 +301,26 @@ __device__ __forceinline__ void unit_epilogue(const LycView& p, const LycSlot& s
       if (d == 0) p.part_lse[(int64_t)u * G + j] = log2f(L) + M;
     }
   }
-  if (hist_g) {  // flush the unit's first-pass histogram (few non-zero bins) and re-zero it
-    for (int b = tid; b < LYC_BINS; b += kConsumerWarps * 32) {
+  static_assert(kConsumerWarps * 32 * 32 == LYC_H1_BINS && LYC_H1_COARSE * 64 == LYC_H1_BINS,
+                "histogram flush mapping");
+  if (hist_g) {
+    // flush the unit's first-pass histogram and re-zero it: thread t owns 32
+    // consecutive bins (rotated reads, conflict-free); the 64-bin coarse
+    // summary (top 6 bits) that follows the fine bins in the global row gets
+    // one atomic per non-empty coarse bin (thread pairs share one)
+    uint32_t sum = 0;
+#pragma unroll 4
+    for (int i = 0; i < 32; ++i) {
+      const int b = tid * 32 + ((i + tid) & 31);
       const uint32_t c = hist_s[b];
       if (c) {
         atomicAdd(hist_g + b, c);
         hist_s[b] = 0u;
+        sum += c;
       }
     }
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    if ((tid & 1) == 0 && sum) atomicAdd(hist_g + LYC_H1_BINS + (tid >> 1), sum);
   }
   consumer_bar();
 }
@@ -362,8 +374,7 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
 #pragma unroll
     for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = 0.f;
     const bool want_sel = s.sel >= 0 && p.sel_mode != SEL_NONE;
-    uint32_t* hist = (want_sel && p.hist1) ? p.hist1 + (int64_t)s.sel * LYC_BINS : nullptr;
-    uint32_t* hist16 = (want_sel && p.hist16) ? p.hist16 + (int64_t)s.sel * 65536 : nullptr;
+    uint32_t* hist = (want_sel && p.hist1) ? p.hist1 + (int64_t)s.sel * LYC_H1_ROW : nullptr;
 
     for (int it = un.begin; it < un.end; ++it) {
       for (int sub = 0; sub < tpi; ++sub) {
@@ -395,21 +406,19 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
               ps[n][e] = v;
             }
           if (p.sel_mode == SEL_TOKEN_KEYS) {
-            if (lane < 4) {
-              uint32_t* dst = p.sel_keys + (int64_t)s.sel * p.sel_stride + t.lo;
-#pragma unroll
-              for (int n = 0; n < 2; ++n)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                  const int r = t0 + n * 8 + qc + e;
-                  const bool ok = r < t.nvalid;
-                  const uint32_t key = float_key(ps[n][e]);
-                  if (ok) {
-                    dst[r] = key;
-                    if (hist) atomicAdd(sm.hist + (key >> 21), 1u);
-                    if (hist16) atomicAdd(hist16 + (key >> 16), 1u);
-                  }
-                }
+            // lane r < 16 gathers row t0 + r's score (held by lane (r & 7) >> 1
+            // as ps[r >> 3][r & 1]) so the warp's 16 keys go out in one
+            // coalesced 64-B store and one shared-memory atomic
+            const int r = lane & 15, src = (r & 7) >> 1;
+            const float v00 = __shfl_sync(0xffffffffu, ps[0][0], src);
+            const float v01 = __shfl_sync(0xffffffffu, ps[0][1], src);
+            const float v10 = __shfl_sync(0xffffffffu, ps[1][0], src);
+            const float v11 = __shfl_sync(0xffffffffu, ps[1][1], src);
+            const float mine = (r >> 3) ? ((r & 1) ? v11 : v10) : ((r & 1) ? v01 : v00);
+            if (lane < 16 && t0 + r < t.nvalid) {
+              const uint32_t key = float_key(mine);
+              p.sel_keys[(int64_t)s.sel * p.sel_stride + t.lo + t0 + r] = key;
+              if (hist) atomicAdd(sm.hist + (key >> (32 - LYC_H1_BITS)), 1u);
             }
           } else {  // SEL_BLOCK_KEYS: max over valid rows of this block
             uint32_t km = 0u;
@@ -509,8 +518,7 @@ __device__ __forceinline__ void consume_units_f32(const LycView& p, const AttnSm
     const LycSlot s = p.slots[un.slot];
     const int tpi = tiles_per_item(s, p.block_size);
     const bool want_sel = s.sel >= 0 && p.sel_mode != SEL_NONE;
-    uint32_t* hist = (want_sel && p.hist1) ? p.hist1 + (int64_t)s.sel * LYC_BINS : nullptr;
-    uint32_t* hist16 = (want_sel && p.hist16) ? p.hist16 + (int64_t)s.sel * 65536 : nullptr;
+    uint32_t* hist = (want_sel && p.hist1) ? p.hist1 + (int64_t)s.sel * LYC_H1_ROW : nullptr;
     float m[kMaxG], l[kMaxG], o[kMaxG][DC];
 #pragma unroll
     for (int j = 0; j < kMaxG; ++j) {
@@ -560,8 +568,7 @@ __device__ __forceinline__ void consume_units_f32(const LycView& p, const AttnSm
               const uint32_t key = float_key(pooled);
               if (valid) {
                 p.sel_keys[(int64_t)s.sel * p.sel_stride + t.lo + t0 + tr] = key;
-                if (hist) atomicAdd(sm.hist + (key >> 21), 1u);
-                if (hist16) atomicAdd(hist16 + (key >> 16), 1u);
+                if (hist) atomicAdd(sm.hist + (key >> (32 - LYC_H1_BITS)), 1u);
               }
             }
           } else {

@@ -462,13 +462,12 @@ struct lyc_decoder {
   int32_t* idx_count = nullptr;
   uint32_t* sel_keys = nullptr; // [2][B*H][sel_stride]
   int64_t sel_stride = 0;
-  uint32_t* hist = nullptr;     // [2][B*H][LYC_BINS] fused first-pass histograms
+  uint32_t* hist = nullptr;     // [2][B*H][LYC_H1_BINS] fused first-pass histograms
   uint32_t* sel_bitmap = nullptr;  // fused-mode pooled selection scratch (see LycStepParams)
   int64_t bitmap_stride = 0;
   uint32_t* sel_cand = nullptr;
   uint32_t* sel_ccnt = nullptr;
   uint32_t* sel_rowctr = nullptr;
-  uint32_t* hist16 = nullptr;   // [2][B*H][65536] fused 16-bit-prefix histograms
   int stages = 0;               // attention ring stages in use (0 = all; env LYC_STAGES)
   uint32_t* ctr = nullptr;      // [NL][CTR_PER_LAYER] + 2
   unsigned long long* trace = nullptr;  // optional step timeline [NL][LYC_TRACE_EVENTS][n_ctas]
@@ -813,7 +812,6 @@ void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, i
   p.sel_cand = d->sel_cand;
   p.sel_ccnt = d->sel_ccnt;
   p.sel_rowctr = d->sel_rowctr;
-  p.hist16 = d->hist16;
   p.ctr = d->ctr;
   p.idx = d->idx;
   p.idx_stride = d->k_cap;
@@ -908,18 +906,14 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
       cuda_check(cudaMemset(d->idx_count, 0, rows * 4), "memset");
       cuda_check(cudaMalloc(&d->sel_keys, 2 * rows * d->sel_stride * 4), "cudaMalloc keys");
       cuda_check(cudaMemset(d->sel_keys, 0, 2 * rows * d->sel_stride * 4), "memset");
-      cuda_check(cudaMalloc(&d->hist, 2 * rows * LYC_BINS * 4), "cudaMalloc hist");
-      cuda_check(cudaMemset(d->hist, 0, 2 * rows * LYC_BINS * 4), "memset");
+      cuda_check(cudaMalloc(&d->hist, 2 * rows * LYC_H1_ROW * 4), "cudaMalloc hist");
+      cuda_check(cudaMemset(d->hist, 0, 2 * rows * LYC_H1_ROW * 4), "memset");
       if (d->fused && c.select_mode != LYC_SELECT_NONE) {  // pooled-selection scratch
         d->bitmap_stride = (lyc::step_bitmap_words(d->sel_stride) + 3) & ~(int64_t)3;
         cuda_check(cudaMalloc(&d->sel_bitmap, 2 * rows * d->bitmap_stride * 4), "cudaMalloc bitmap");
-        cuda_check(cudaMalloc(&d->sel_cand, 2 * rows * 2 * d->sel_stride * 4), "cudaMalloc cand");
-        cuda_check(cudaMalloc(&d->sel_ccnt, 2 * rows * 64 * 4), "cudaMalloc ccnt");
+        cuda_check(cudaMalloc(&d->sel_cand, 2 * rows * 3 * d->sel_stride * 4), "cudaMalloc cand");
+        cuda_check(cudaMalloc(&d->sel_ccnt, 2 * rows * 192 * 4), "cudaMalloc ccnt");
         cuda_check(cudaMalloc(&d->sel_rowctr, (size_t)d->NL * rows * 16 * 4), "cudaMalloc rowctr");
-        if (c.select_mode == LYC_SELECT_TOKENS) {
-          cuda_check(cudaMalloc(&d->hist16, 2 * rows * 65536 * 4), "cudaMalloc hist16");
-          cuda_check(cudaMemset(d->hist16, 0, 2 * rows * 65536 * 4), "memset");
-        }
         cuda_check(cudaMemset(d->sel_rowctr, 0, (size_t)d->NL * rows * 16 * 4), "memset");
       }
       cuda_check(cudaMalloc(&d->ctr, LYC_CTR_WORDS(d->NL) * 4), "cudaMalloc ctr");
@@ -947,7 +941,6 @@ int lyc_decoder_destroy(lyc_decoder* d) {
   free_dev(d->sel_cand);
   free_dev(d->sel_ccnt);
   free_dev(d->sel_rowctr);
-  free_dev(d->hist16);
   free_dev(d->ctr);
   free_dev(d->trace);
   free_dev(d->part_o);

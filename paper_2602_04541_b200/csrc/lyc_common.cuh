@@ -52,6 +52,10 @@ __device__ __forceinline__ void st_global_pred(int32_t* ptr, uint32_t v, bool ok
                : "memory");
 }
 
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t phase) {
   uint32_t ok;
   asm volatile(

@@ -17,6 +17,12 @@
 
 #define LYC_TILE 64
 #define LYC_BINS 2048
+// First radix pass fused into the attention consumers (per-CTA smem histogram).
+#define LYC_H1_BITS 12
+#define LYC_H1_BINS (1 << LYC_H1_BITS)
+// Global h1 rows carry 64 coarse bins (top 6 bits) after the fine bins.
+#define LYC_H1_COARSE 64
+#define LYC_H1_ROW (LYC_H1_BINS + LYC_H1_COARSE)
 #define LYC_TRACE_EVENTS 16  // step-timeline stamps per layer per CTA
 
 enum { ITEM_DENSE = 0, ITEM_BLOCKS = 1, ITEM_TOKENS = 2 };
@@ -56,8 +62,7 @@ struct LycView {
   float* part_o;            // [n_units][G][d]  normalized partial outputs
   float* part_lse;          // [n_units][G]     base-2 log-sum-exp
   uint32_t* sel_keys;       // [n_sel][sel_stride]
-  uint32_t* hist1;          // optional [n_sel][LYC_BINS]: fused first radix pass
-  uint32_t* hist16;         // optional [n_sel][65536]: fused 16-bit-prefix histogram
+  uint32_t* hist1;          // optional [n_sel][LYC_H1_ROW]: fused first radix pass (+ coarse bins)
   uint32_t* exec_counts;    // optional [n_slots][counts_stride] per item
   int64_t sel_stride;
   int32_t counts_stride;
@@ -151,12 +156,11 @@ struct LycStepParams {
   float* part_lse;
   uint32_t* sel_keys;        // [2 parity][max_sel][sel_stride]
   int64_t sel_stride;
-  uint32_t* hist;            // [2 parity][max_sel][LYC_BINS] fused first-pass histograms
-  uint32_t* hist16;          // [2 parity][max_sel][65536] fused 16-bit-prefix histograms
+  uint32_t* hist;            // [2 parity][max_sel][LYC_H1_ROW] fused first-pass histograms
   uint32_t* sel_bitmap;      // [2 parity][max_sel][bitmap_stride] selected-key bitmaps
   int64_t bitmap_stride;
-  uint32_t* sel_cand;        // [2 parity][max_sel][2][sel_stride] boundary-bin candidates
-  uint32_t* sel_ccnt;        // [2 parity][max_sel][64] candidates per item
+  uint32_t* sel_cand;        // [2 parity][max_sel][3][sel_stride] boundary-bin candidates: keys, indices, selected flags
+  uint32_t* sel_ccnt;        // [2 parity][max_sel][192] per item: candidates, definite keys, output offset
   uint32_t* sel_rowctr;      // [n_layers][max_sel][16] finished items per row (monotonic)
   uint32_t* ctr;             // LYC_CTR counters: [n_layers][CTR_PER_LAYER], then epoch, exits
   int32_t* idx;              // index cache [B*H][idx_stride]

@@ -79,6 +79,12 @@ __device__ __forceinline__ void stamp(const LycStepParams& p, int l, int ev, int
   }
 }
 
+// Every selection item signals CTR_SELDONE once after emitting its share of
+// the index-cache row.
+__device__ __forceinline__ uint32_t seldone_per_step(const LycStepParams& p, int l) {
+  return (uint32_t)p.layers[l].n_sel * (uint32_t)((p.n_keys + kItemKeys - 1) / kItemKeys);
+}
+
 struct StepWaits {
   const LycStepParams* p;
   uint32_t epoch1;
@@ -90,7 +96,7 @@ struct StepWaits {
   }
   __device__ __forceinline__ void unit(const LycSlot& s) const {
     if (s.dep >= 0)  // every retrieval head of layer dep finished its selection
-      wait(LYC_CTR(p->ctr, s.dep, CTR_SELDONE), epoch1 * (uint32_t)p->layers[s.dep].n_sel);
+      wait(LYC_CTR(p->ctr, s.dep, CTR_SELDONE), epoch1 * seldone_per_step(*p, s.dep));
   }
   __device__ __forceinline__ void last_tile() const {
     if (layer > 0) wait(LYC_CTR(p->ctr, layer - 1, CTR_MERGE), epoch1 * (uint32_t)p->n_ctas);
@@ -110,10 +116,8 @@ __device__ __forceinline__ LycView layer_view(const LycStepParams& p, const LycL
   v.part_o = p.part_o;
   v.part_lse = p.part_lse;
   v.sel_keys = p.sel_keys + (int64_t)(l & 1) * p.max_sel * p.sel_stride;
-  v.hist1 = p.sel_mode == SEL_TOKEN_KEYS ? p.hist + (int64_t)(l & 1) * p.max_sel * LYC_BINS
+  v.hist1 = p.sel_mode == SEL_TOKEN_KEYS ? p.hist + (int64_t)(l & 1) * p.max_sel * LYC_H1_ROW
                                          : nullptr;
-  v.hist16 = p.sel_mode == SEL_TOKEN_KEYS ? p.hist16 + (int64_t)(l & 1) * p.max_sel * 65536
-                                          : nullptr;
   v.exec_counts = nullptr;
   v.sel_stride = p.sel_stride;
   v.counts_stride = 0;
@@ -130,57 +134,69 @@ __device__ __forceinline__ LycView layer_view(const LycStepParams& p, const LycL
 
 // ---------------------------------------------------------------- selection
 // Warp-level search of a histogram (from the top bin down) for the bin that
-// holds the krem-th largest candidate.  Returns (digit, count above it).
+// holds the krem-th largest candidate (krem >= 1).  Two levels, no local
+// arrays: every lane sums a contiguous run of nbins/32 bins, a warp scan picks
+// the lane holding the target, then the warp splits that lane's run again.
+// Returns (digit, count strictly above it).  nbins: power of two, 32..4096.
+__device__ __forceinline__ uint32_t ld_bin(const uint32_t* a, bool global) {
+  return global ? __ldcg(a) : *a;
+}
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t n = __shfl_up_sync(0xffffffffu, v, off);
+    if (lane >= off) v += n;
+  }
+  return v;
+}
 __device__ __forceinline__ void find_digit(const uint32_t* h, int nbins, uint32_t krem,
                                            uint32_t& digit, uint32_t& above, int lane,
                                            bool global) {
-  const int per = nbins / 32;  // 64 (11-bit) or 32 (10-bit) bins per lane
-  const int hi = nbins - 1 - lane * per;  // lane owns bins hi, hi-1, ..., hi-per+1
-  uint32_t cnt[64];
+  const int per = nbins / 32;             // bins per lane (1..128)
+  const int hi = nbins - 1 - lane * per;  // lane owns bins (hi - per, hi], highest first
   uint32_t sum = 0;
-  const uint4* src = reinterpret_cast<const uint4*>(h + hi - per + 1);
   if (per >= 4) {
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      if (q * 4 >= per) break;
+    const uint4* src = reinterpret_cast<const uint4*>(h + hi - per + 1);
+#pragma unroll 8
+    for (int q = 0; q < per / 4; ++q) {
       const uint4 v = global ? __ldcg(src + q) : src[q];
-      cnt[4 * q] = v.x;
-      cnt[4 * q + 1] = v.y;
-      cnt[4 * q + 2] = v.z;
-      cnt[4 * q + 3] = v.w;
       sum += v.x + v.y + v.z + v.w;
     }
-  } else {  // small histograms (< 128 bins)
-    for (int i = 0; i < per; ++i) {
-      const uint32_t* a = h + hi - per + 1 + i;
-      cnt[i] = global ? __ldcg(a) : *a;
-      sum += cnt[i];
-    }
+  } else {
+    for (int i = 0; i < per; ++i) sum += ld_bin(h + hi - i, global);
   }
-  uint32_t incl = sum;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const uint32_t n = __shfl_up_sync(0xffffffffu, incl, off);
-    if (lane >= off) incl += n;
+  uint32_t incl = warp_incl_scan(sum, lane);
+  unsigned who = __ballot_sync(0xffffffffu, incl - sum < krem && krem <= incl);
+  const int L = __ffs(who) - 1;
+  uint32_t run = __shfl_sync(0xffffffffu, incl - sum, L);  // keys above lane L's run
+  const int top = nbins - 1 - L * per;                      // lane L's highest bin
+  // second level: lane i takes `sub` consecutive bins of lane L's run, highest first
+  const int sub = per >= 32 ? per / 32 : 1;
+  const bool act = lane * sub < per;
+  uint32_t s2 = 0;
+  if (act) {
+#pragma unroll 4
+    for (int i = 0; i < sub; ++i) s2 += ld_bin(h + top - lane * sub - i, global);
   }
-  const uint32_t excl = incl - sum;
+  incl = warp_incl_scan(s2, lane) + run;
+  who = __ballot_sync(0xffffffffu, act && incl - s2 < krem && krem <= incl);
+  const int M = __ffs(who) - 1;
   uint32_t d = 0, a = 0;
-  const bool mine = excl < krem && krem <= incl;
-  if (mine) {
-    uint32_t run = excl;
-    for (int i = per - 1; i >= 0; --i) {  // cnt[i] is bin hi - per + 1 + i
-      if (krem <= run + cnt[i]) {
-        d = (uint32_t)(hi - per + 1 + i);
-        a = run;
+  if (lane == M) {
+    uint32_t r = incl - s2;
+    for (int i = 0; i < sub; ++i) {
+      const int bin = top - lane * sub - i;
+      const uint32_t c = ld_bin(h + bin, global);
+      if (krem <= r + c) {
+        d = (uint32_t)bin;
+        a = r;
         break;
       }
-      run += cnt[i];
+      r += c;
     }
   }
-  const unsigned who = __ballot_sync(0xffffffffu, mine);
-  const int src_lane = __ffs(who) - 1;
-  digit = __shfl_sync(0xffffffffu, d, src_lane);
-  above = __shfl_sync(0xffffffffu, a, src_lane);
+  digit = __shfl_sync(0xffffffffu, d, M);
+  above = __shfl_sync(0xffffffffu, a, M);
 }
 
 // Selection bitmaps (global and on chip) are stored in 64-word chunks at a
@@ -199,6 +215,7 @@ struct EpiSmem {
   uint32_t scan[64];
   uint32_t seg[72];          // finish: smem start of each item's candidate segment
   uint32_t cnt[72];          // finish: candidates of each item
+  uint32_t selc[72];         // finish: selected candidates of each item
   uint64_t bar;
   uint32_t digit, above, last, pad;
   uint32_t pfx, pabove, pshift, pad2;  // the row's boundary prefix (classify -> finish)
@@ -236,65 +253,53 @@ __device__ __forceinline__ void epi_digit(EpiSmem& es, const uint32_t* h, bool g
 
 struct SelRow {
   uint32_t* keys;     // keys of the row [n]
-  uint32_t* h1;       // fused first-pass histogram (token mode) or nullptr
-  uint32_t* h16;      // fused 16-bit-prefix histogram [65536] (token mode) or nullptr
+  uint32_t* h1;       // fused first-pass (12-bit) histogram (token mode) or nullptr
   uint32_t* bitmap;   // [n_words]
   uint32_t* ckey;     // [n] candidate keys, item q's segment at q*kItemKeys
   uint32_t* cidx;     // [n] candidate indices
-  uint32_t* ccnt;     // [n_items] candidates per item
-  uint32_t* ctr;      // per-row item counter
+  uint32_t* cflag;    // [n] candidate selected (1) or not (0), written by the finisher
+  uint32_t* ccnt;     // [n_items] candidates per item; +64: definite keys per item;
+                      // +128: output offset of each item
+  uint32_t* ctr;      // per-row words: [0] items classified, [4] row resolved (epoch)
 };
 
 __device__ __forceinline__ SelRow sel_row(const LycStepParams& p, int l, int r) {
   const int64_t pr = (int64_t)(l & 1) * p.max_sel + r;
   SelRow s;
   s.keys = p.sel_keys + pr * p.sel_stride;
-  s.h1 = p.sel_mode == SEL_TOKEN_KEYS ? p.hist + pr * LYC_BINS : nullptr;
-  s.h16 = (p.sel_mode == SEL_TOKEN_KEYS && p.hist16) ? p.hist16 + pr * 65536 : nullptr;
+  s.h1 = p.sel_mode == SEL_TOKEN_KEYS ? p.hist + pr * LYC_H1_ROW : nullptr;
   s.bitmap = p.sel_bitmap + pr * p.bitmap_stride;
-  s.ckey = p.sel_cand + pr * 2 * p.sel_stride;
+  s.ckey = p.sel_cand + pr * 3 * p.sel_stride;
   s.cidx = s.ckey + p.sel_stride;
-  s.ccnt = p.sel_ccnt + pr * 64;
+  s.cflag = s.cidx + p.sel_stride;
+  s.ccnt = p.sel_ccnt + pr * 192;
   s.ctr = p.sel_rowctr + ((int64_t)l * p.max_sel + r) * 16;
   return s;
 }
 
-// The boundary prefix of a row.  Token mode: the 11-bit bin d1 from the fused
-// first-pass histogram, refined to 16 bits with the 32 sub-bins of d1 in the
-// fused 16-bit histogram -- the boundary bin then holds ~1e2 keys.  Block mode
-// (one item): the 11-bit bin of the item's own histogram (es.hist).
+// The boundary prefix of a row.  Token mode: the 12-bit bin from the first
+// radix pass the attention consumers fused into scoring (h1); block mode (one
+// item): the 11-bit bin of the item's own histogram (es.hist).
 // Sets es.digit = prefix, es.above = keys strictly above it, es.last = shift.
 __device__ __forceinline__ void row_prefix(const LycStepParams& p, const SelRow& R, EpiSmem& es,
                                            int et) {
-  const uint32_t k = (uint32_t)p.k_sel;
-  epi_digit(es, R.h1 ? R.h1 : es.hist, R.h1 != nullptr, LYC_BINS, k, et);
-  if (!R.h16) {
-    if (et == 0) es.last = 21u;
+  if (R.h1) {
+    // two dependent L2 reads: the 64 coarse bins, then the 64 fine bins of
+    // the chosen coarse bin
+    if (et < 32) {
+      const uint32_t k = (uint32_t)p.k_sel;
+      uint32_t cd, ca, fd, fa;
+      find_digit(R.h1 + LYC_H1_BINS, LYC_H1_COARSE, k, cd, ca, et, true);
+      find_digit(R.h1 + cd * 64, 64, k - ca, fd, fa, et, true);
+      if (et == 0) {
+        es.digit = cd * 64 + fd;
+        es.above = ca + fa;
+      }
+    }
     epi_bar();
-    return;
-  }
-  const uint32_t d1 = es.digit, a1 = es.above;
-  epi_bar();
-  if (et < 32) {
-    // sub-bins of d1, highest first: lane i holds sub-bin 31 - i
-    const uint32_t c = __ldcg(R.h16 + d1 * 32u + (31u - (uint32_t)et));
-    uint32_t incl = c;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t n = __shfl_up_sync(0xffffffffu, incl, off);
-      if (et >= off) incl += n;
-    }
-    const uint32_t krem = k - a1;
-    const bool mine = incl - c < krem && krem <= incl;
-    const unsigned who = __ballot_sync(0xffffffffu, mine);
-    const int src = __ffs(who) - 1;
-    const uint32_t above = __shfl_sync(0xffffffffu, incl - c, src);
-    if (et == 0) {
-      es.digit = (d1 << 5) | (31u - (uint32_t)src);
-      es.above = a1 + above;
-      es.last = 16u;
-    }
-  }
+  } else
+    epi_digit(es, es.hist, false, LYC_BINS, (uint32_t)p.k_sel, et);
+  if (et == 0) es.last = R.h1 ? 32u - LYC_H1_BITS : 21u;
   epi_bar();
 }
 
@@ -328,12 +333,6 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
     es.pfx = P;
     es.pabove = es.above;
     es.pshift = (uint32_t)shift;
-  }
-  if (R.h16) {  // reset this item's share of the 16-bit histogram, except d1's sub-bins
-    const int b0 = q * (65536 / items), b1 = (q == items - 1) ? 65536 : (q + 1) * (65536 / items);
-    const int keep0 = (int)(P >> 5) * 32, keep1 = keep0 + 32;
-    for (int b = b0 + et; b < b1; b += kEpiThreads)
-      if (b < keep0 || b >= keep1) R.h16[b] = 0u;
   }
   mbar_wait(&es.bar, bar_phase);
   bar_phase ^= 1u;
@@ -377,8 +376,14 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
       ++pos;
     }
   }
+  uint32_t ndef = __popc(words[0]) + __popc(words[1]) + __popc(words[2]) + __popc(words[3]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) ndef += __shfl_xor_sync(0xffffffffu, ndef, off);
+  if ((et & 31) == 0) es.scan[32 + (et >> 5)] = ndef;
+  epi_bar();
   if (et == 0) {
     R.ccnt[q] = total;
+    R.ccnt[64 + q] = es.scan[32] + es.scan[33];
     // pad the segment to a multiple of 4 with sentinels (index ~0, key 0: never
     // ranks above a real candidate) so the finisher can scan padded slots blindly
     for (uint32_t i = total; i < ((total + 3u) & ~3u); ++i) {
@@ -398,23 +403,21 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
   return es.last != 0;
 }
 
-// Finish one row after its last item.  One thread bulk-copies the row's bitmap
-// and every item's candidate segment (keys and indices, 16-B aligned) into
-// shared memory -- all copies in flight at once -- then the radix finishes on
-// the candidates (<= 11 bits per pass), the selected ones join the bitmap, and
-// the set bits are emitted in ascending order.  Rows whose boundary bin holds
-// more candidates than fit on chip read them from L2 instead.
-__device__ void finish_row(const LycStepParams& p, const SelRow& R, int32_t* out, EpiSmem& es,
-                           uint32_t& bar_phase, int et, int l, int cta) {
+// Resolve one row after its last item was classified.  One thread bulk-copies
+// every item's boundary-bin candidate segment (keys and indices, 16-B
+// aligned) into shared memory, all copies in flight at once; the krem best
+// candidates (greater key, or equal key and lower index: attention.hpp:115-119)
+// are OR-ed into the row's global bitmap and counted per item; the per-item
+// output offsets are published and the row is released to its items, which
+// emit their own ranges (emit_item).
+__device__ void finish_row(const LycStepParams& p, const SelRow& R, int row, EpiSmem& es,
+                           uint32_t& bar_phase, uint32_t epoch1, int et, int l, int cta) {
   const int n = p.n_keys;
   const int items = (n + kItemKeys - 1) / kItemKeys;
-  const int nwords = (n + 31) / 32;
-  const int bm_words = bm_padded_words(nwords);
   // the boundary prefix this CTA computed while classifying the row's last item
   uint32_t P = es.pfx;
   int shift = (int)es.pshift;
   uint32_t krem = (uint32_t)p.k_sel - es.pabove;
-  if (et == 0) stamp(p, l, EV_F_PREFIX, cta);
   // candidate segments: item q's candidates land at smem [seg[q], seg[q] + cnt[q])
   const uint32_t c_mine = et < items ? __ldcg(R.ccnt + et) : 0u;
   const uint32_t c_pad = (c_mine + 3) & ~3u;
@@ -424,20 +427,17 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int32_t* out
     es.seg[et] = incl - c_pad;
     es.cnt[et] = c_mine;
   }
-  const int cap = ((kEpiBufWords - bm_words) / 2) & ~3;  // candidates that fit next to the bitmap
+  if (et < 72) es.selc[et] = 0u;
+  const int cap = (kEpiBufWords / 2) & ~3;  // candidates that fit on chip
   const bool on_chip = (int)padded <= cap;
-  uint32_t* bmp = es.buf;
-  uint32_t* skey = es.buf + bm_words;
-  uint32_t* sidx = skey + cap;
+  uint32_t* skey = es.buf;
+  uint32_t* sidx = es.buf + cap;
   epi_bar();
   if (et == 0) {
     stamp(p, l, EV_F_SCAN, cta);
-    fence_proxy_async();
-    uint32_t bytes = (uint32_t)bm_words * 4u;
-    if (on_chip) bytes += padded * 8u;
-    mbar_arrive_expect_tx(&es.bar, bytes);
-    bulk_g2s(bmp, R.bitmap, (uint32_t)bm_words * 4u, &es.bar);
-    if (on_chip)
+    if (on_chip && padded > 0) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&es.bar, padded * 8u);
       for (int q = 0; q < items; ++q) {
         const uint32_t b = ((es.cnt[q] + 3) & ~3u) * 4u;
         if (b) {
@@ -445,169 +445,190 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int32_t* out
           bulk_g2s(sidx + es.seg[q], R.cidx + (size_t)q * kItemKeys, b, &es.bar);
         }
       }
+    }
   }
-  mbar_wait(&es.bar, bar_phase);
-  bar_phase ^= 1u;
+  if (on_chip && padded > 0) {
+    mbar_wait(&es.bar, bar_phase);
+    bar_phase ^= 1u;
+  }
   if (et == 0) stamp(p, l, EV_SEL2, cta);
-  // i-th padded slot -> (valid?, key, index); slots past a segment's count are padding
-  auto slot = [&](int i, uint32_t& key, uint32_t& idx) -> bool {
+  const int ns = (int)padded;
+  // i-th padded slot -> (valid?, key, index).  On chip the padding carries
+  // sentinels (index ~0); off chip the segment table is walked in L2.
+  auto get = [&](int i, uint32_t& key, uint32_t& idx) -> bool {
+    if (on_chip) {
+      key = skey[i];
+      idx = sidx[i];
+      return idx != 0xFFFFFFFFu;
+    }
     int q = 0;
     while (q + 1 < items && (uint32_t)i >= es.seg[q + 1]) ++q;
     const uint32_t off = (uint32_t)i - es.seg[q];
     if (off >= es.cnt[q]) return false;
-    if (on_chip) {
-      key = skey[i];
-      idx = sidx[i];
-    } else {
-      key = __ldcg(R.ckey + (size_t)q * kItemKeys + off);
-      idx = __ldcg(R.cidx + (size_t)q * kItemKeys + off);
-    }
+    key = __ldcg(R.ckey + (size_t)q * kItemKeys + off);
+    idx = __ldcg(R.cidx + (size_t)q * kItemKeys + off);
     return true;
   };
-  const int ns = (int)padded;
-  if (on_chip && ns <= kRankMax) {
-    // Few candidates (the usual case: the 16-bit boundary bin of a smooth score
-    // distribution holds ~1e2 keys): exact rank of every candidate among the
-    // others -- greater key, or equal key and lower index (attention.hpp:115-119)
-    // -- with broadcast smem reads; the krem best join the bitmap.
-    for (int i0 = 0; i0 < ns; i0 += kEpiThreads) {
-      const int i = i0 + et;
-      const uint32_t ki = i < ns ? skey[i] : 0u;
-      const uint32_t xi = i < ns ? sidx[i] : 0xFFFFFFFFu;
-      uint32_t rank = 0;
-      for (int j = 0; j < ns; j += 4) {
-        const uint4 kj = *reinterpret_cast<const uint4*>(skey + j);
-        const uint4 xj = *reinterpret_cast<const uint4*>(sidx + j);
-        rank += (kj.x > ki || (kj.x == ki && xj.x < xi)) ? 1u : 0u;
-        rank += (kj.y > ki || (kj.y == ki && xj.y < xi)) ? 1u : 0u;
-        rank += (kj.z > ki || (kj.z == ki && xj.z < xi)) ? 1u : 0u;
-        rank += (kj.w > ki || (kj.w == ki && xj.w < xi)) ? 1u : 0u;
-      }
-      if (xi != 0xFFFFFFFFu && rank < krem) atomicOr(bmp + bm_pad((int)(xi >> 5)), 1u << (xi & 31));
+  // slot i's flag lives next to its candidate in L2 (item q = idx / kItemKeys)
+  auto flag = [&](int i, uint32_t idx, uint32_t v) {
+    const uint32_t q = idx / kItemKeys;
+    R.cflag[(size_t)q * kItemKeys + (uint32_t)i - es.seg[q]] = v;
+    if (v) atomicAdd(&es.selc[q], 1u);
+  };
+  // Narrow with 8-bit radix passes while many candidates share the prefix
+  // (counts only), then one pass takes every candidate above the final
+  // prefix and compacts the survivors, which are ranked exactly.
+  uint32_t live = padded;  // upper bound on candidates matching P
+  while (live > (uint32_t)kRankMax && shift > 0) {
+    const int wbits = shift > 8 ? 8 : shift;
+    shift -= wbits;
+    const uint32_t mask = (1u << wbits) - 1u;
+    epi_bar();
+    for (int b = et; b < (1 << wbits); b += kEpiThreads) es.hist[b] = 0u;
+    epi_bar();
+    for (int i = et; i < ns; i += kEpiThreads) {
+      uint32_t key, idx;
+      if (get(i, key, idx) && (key >> (shift + wbits)) == P)
+        atomicAdd(&es.hist[(key >> shift) & mask], 1u);
     }
     epi_bar();
-    if (et == 0) {
-      stamp(p, l, EV_SEL0, cta);
-      stamp(p, l, EV_SEL1, cta);
-    }
-  } else {
-    // remaining radix passes over the candidates (<= 11 bits each)
-    while (shift > 0) {
-      const int wbits = shift > 11 ? 11 : shift;
-      shift -= wbits;
-      const uint32_t mask = (1u << wbits) - 1u;
-      for (int b = et; b < (1 << wbits); b += kEpiThreads) es.hist[b] = 0u;
-      epi_bar();
-      for (int i = et; i < ns; i += kEpiThreads) {
-        uint32_t key, idx;
-        if (slot(i, key, idx) && (key >> (shift + wbits)) == P)
-          atomicAdd(&es.hist[(key >> shift) & mask], 1u);
+    epi_digit(es, es.hist, false, 1 << wbits, krem, et);
+    P = (P << wbits) | es.digit;
+    krem -= es.above;
+    live = es.hist[es.digit];
+  }
+  uint32_t* lkey = es.hist;
+  uint32_t* lidx = es.hist + kRankMax;
+  uint32_t* lslot = es.hist + 2 * kRankMax;
+  epi_bar();
+  if (et == 0) {
+    es.pad = 0u;
+    stamp(p, l, EV_F_PREFIX, cta);
+  }
+  epi_bar();
+  for (int i = et; i < ns; i += kEpiThreads) {
+    uint32_t key, idx;
+    if (!get(i, key, idx)) continue;
+    const uint32_t pre = key >> shift;  // shift < 32
+    flag(i, idx, pre > P ? 1u : 0u);
+    if (pre == P) {
+      const uint32_t at = atomicAdd(&es.pad, 1u);
+      if (at < (uint32_t)kRankMax) {
+        lkey[at] = key;
+        lidx[at] = idx;
+        lslot[at] = (uint32_t)i;
       }
-      epi_bar();
-      epi_digit(es, es.hist, false, 1 << wbits, krem, et);
-      P = (P << wbits) | es.digit;
-      krem -= es.above;
     }
-    const uint32_t T = P;  // the k-th largest key; krem of its ties are taken
-    if (et == 0) stamp(p, l, EV_SEL0, cta);
-    // selected candidates join the (on-chip) bitmap, ties in index order
+  }
+  epi_bar();
+  const uint32_t m = es.pad;
+  if (et == 0) stamp(p, l, EV_X1, cta);
+  const bool ranked = m <= (uint32_t)kRankMax;
+  if (ranked) {
+    for (uint32_t i = et; i < m; i += kEpiThreads) {
+      const uint32_t ki = lkey[i], xi = lidx[i];
+      uint32_t rank = 0;
+      for (uint32_t j = 0; j < m; ++j) {
+        const uint32_t kj = lkey[j];
+        rank += (kj > ki || (kj == ki && lidx[j] < xi)) ? 1u : 0u;
+      }
+      if (rank < krem) flag((int)lslot[i], xi, 1u);
+    }
+  }
+  if (!ranked) {
+    // (only with shift == 0) all survivors carry the same key T = P: the
+    // first krem in index order
+    // (slot order is index order)
     uint32_t tie_run = 0;
     for (int b0 = 0; b0 < ns; b0 += kEpiThreads) {
       const int i = b0 + et;
       uint32_t key = 0, idx = 0;
-      const bool ok = i < ns && slot(i, key, idx);
-      const bool is_eq = ok && key == T;
+      const bool ok = i < ns && get(i, key, idx);
+      const bool is_eq = ok && key == P;
       uint32_t tot;
       const uint32_t inc = epi_scan(is_eq ? 1u : 0u, es.scan, et, tot);
-      const uint32_t rank = tie_run + inc - (is_eq ? 1u : 0u);
-      if (ok && (key > T || (is_eq && rank < krem)))
-        atomicOr(bmp + bm_pad((int)(idx >> 5)), 1u << (idx & 31));
+      if (is_eq && tie_run + inc - 1u < krem) flag(i, idx, 1u);
       tie_run += tot;
     }
-    epi_bar();
-    if (et == 0) stamp(p, l, EV_SEL1, cta);
   }
-  // ascending emission of the set bits.  Thread t owns a contiguous run of
-  // 64-word chunks, read 16 words at a time into registers (conflict-free
-  // 16-B loads thanks to the padded layout); one 64-thread scan of the
-  // per-thread popcounts gives every thread its output offset.  Indices are
-  // staged on chip and copied out coalesced (or stored directly when the
-  // staging area is too small).
-  {
-    const int nchunks = (nwords + 63) / 64;
-    const int cper = (nchunks + kEpiThreads - 1) / kEpiThreads;
-    const int c0 = min(nchunks, et * cper), c1 = min(nchunks, c0 + cper);
-    auto quarter = [&](int c, int qq, uint32_t (&wv)[16]) {
-      const uint4* src = reinterpret_cast<const uint4*>(bmp + c * 68 + qq * 16);
-      const int lim = nwords - (c * 64 + qq * 16);  // words past the row end are garbage
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const uint4 x = src[v];
-        wv[4 * v] = 4 * v < lim ? x.x : 0u;
-        wv[4 * v + 1] = 4 * v + 1 < lim ? x.y : 0u;
-        wv[4 * v + 2] = 4 * v + 2 < lim ? x.z : 0u;
-        wv[4 * v + 3] = 4 * v + 3 < lim ? x.w : 0u;
-      }
-    };
-    uint32_t cnt = 0;
-    for (int c = c0; c < c1; ++c)
-      for (int qq = 0; qq < 4; ++qq) {
-        uint32_t wv[16];
-        quarter(c, qq, wv);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) cnt += __popc(wv[i]);
-      }
-    uint32_t tot;
-    const uint32_t pos0 = epi_scan(cnt, es.scan, et, tot) - cnt;
-    if (et == 0) stamp(p, l, EV_X0, cta);
-    const int k_out = p.k_sel;
-    const bool staged = bm_words + k_out <= kEpiBufWords;
-    // Per word: the first four set bits are stored with predicated,
-    // branch-free stores (a divergent per-bit loop costs ~10x more); words
-    // with more bits (rare at top-k densities) finish in a short loop.
-    auto emit = [&](auto store) {
-      uint32_t pos = pos0;
-      for (int c = c0; c < c1; ++c)
-        for (int qq = 0; qq < 4; ++qq) {
-          uint32_t wv[16];
-          quarter(c, qq, wv);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const uint32_t m0 = wv[i];
-            const uint32_t base = (uint32_t)(c * 64 + qq * 16 + i) * 32u;
-            const uint32_t m1 = m0 & (m0 - 1u), m2 = m1 & (m1 - 1u), m3 = m2 & (m2 - 1u);
-            uint32_t m4 = m3 & (m3 - 1u);
-            store(pos, base + (uint32_t)(__ffs(m0) - 1), m0 != 0u);
-            store(pos + 1u, base + (uint32_t)(__ffs(m1) - 1), m1 != 0u);
-            store(pos + 2u, base + (uint32_t)(__ffs(m2) - 1), m2 != 0u);
-            store(pos + 3u, base + (uint32_t)(__ffs(m3) - 1), m3 != 0u);
-            uint32_t p4 = pos + 4u;
-            pos += __popc(m0);
-            while (m4) {
-              store(p4++, base + (uint32_t)(__ffs(m4) - 1), true);
-              m4 &= m4 - 1u;
-            }
-          }
-        }
-    };
-    if (staged) {
-      uint32_t* stg = bmp + bm_words;
-      const uint32_t sb = smem_u32(stg);
-      emit([&](uint32_t i, uint32_t v, bool ok) { st_shared_pred(sb + 4u * i, v, ok); });
-      epi_bar();
-      for (int i = et; i < k_out; i += kEpiThreads) out[i] = (int32_t)stg[i];
-    } else {
-      emit([&](uint32_t i, uint32_t v, bool ok) { st_global_pred(out + i, v, ok); });
-    }
-  }
-  if (et == 0) stamp(p, l, EV_F_EMIT, cta);
-  // reset the per-row inputs for their next use
+  epi_bar();
+  if (et == 0) stamp(p, l, EV_SEL0, cta);
+  // per-item output offsets: definite keys + selected candidates, in item order
+  const uint32_t n_q = et < items ? __ldcg(R.ccnt + 64 + et) + es.selc[et] : 0u;
+  uint32_t tot;
+  const uint32_t end_q = epi_scan(n_q, es.scan, et, tot);
+  if (et < items) R.ccnt[128 + et] = end_q - n_q;
+  // reset the row's fused histogram for its next use
   if (R.h1)
-    for (int b = et; b < LYC_BINS; b += kEpiThreads) R.h1[b] = 0u;
-  if (R.h16 && et < 32) R.h16[(es.pfx >> (21u - es.pshift)) * 32u + (uint32_t)et] = 0u;  // d1's sub-bins
+    for (int b = et; b < LYC_H1_ROW; b += kEpiThreads) R.h1[b] = 0u;
   if (p.sel_mode == SEL_BLOCK_KEYS)
     for (int i = et; i < n; i += kEpiThreads) R.keys[i] = 0u;
   epi_bar();
+  if (et == 0) {
+    if (p.idx_count) p.idx_count[row] = p.k_sel;
+    __threadfence();
+    st_release(R.ctr + 4, epoch1);
+    stamp(p, l, EV_SEL1, cta);
+  }
+}
+
+// Emit item q of a resolved row: its 256 bitmap words (one 16-B vector per
+// thread), one scan for the positions, branch-free predicated stores of the
+// first four set bits of every word.
+__device__ void emit_item(const LycStepParams& p, const SelRow& R, int q, int32_t* out,
+                          EpiSmem& es, uint32_t epoch1, int et, int l, int cta) {
+  if (et == 0) {
+    spin_until(R.ctr + 4, epoch1);
+    stamp(p, l, EV_X0, cta);
+  }
+  epi_bar();
+  const int n = p.n_keys;
+  const int lo = q * kItemKeys;
+  const int cnt = min(kItemKeys, n - lo);
+  const int w0 = lo / 32 + et * 4;  // this thread's 4 words (128 keys)
+  uint4 v = make_uint4(0u, 0u, 0u, 0u);
+  if (et * 128 < cnt) v = __ldcg(reinterpret_cast<const uint4*>(R.bitmap + bm_pad(w0)));
+  // the finisher's selected boundary-bin candidates join this item's words
+  uint32_t* ws = es.buf;  // [256] on-chip copy of the item's words
+  reinterpret_cast<uint4*>(ws)[et] = v;
+  epi_bar();
+  const uint32_t ncand = __ldcg(R.ccnt + q);
+  for (uint32_t i = et; i < ncand; i += kEpiThreads)
+    if (__ldcg(R.cflag + lo + i)) {
+      const uint32_t idx = __ldcg(R.cidx + lo + i);
+      atomicOr(ws + ((idx - (uint32_t)lo) >> 5), 1u << (idx & 31));
+    }
+  epi_bar();
+  v = reinterpret_cast<const uint4*>(ws)[et];
+  uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (et * 128 + i * 32 >= cnt) wv[i] = 0u;
+  const uint32_t c = __popc(wv[0]) + __popc(wv[1]) + __popc(wv[2]) + __popc(wv[3]);
+  uint32_t tot;
+  uint32_t pos = epi_scan(c, es.scan, et, tot) - c + __ldcg(R.ccnt + 128 + q);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t m0 = wv[i];
+    const uint32_t base = (uint32_t)(w0 + i) * 32u;
+    const uint32_t m1 = m0 & (m0 - 1u), m2 = m1 & (m1 - 1u), m3 = m2 & (m2 - 1u);
+    uint32_t m4 = m3 & (m3 - 1u);
+    st_global_pred(out + pos, base + (uint32_t)(__ffs(m0) - 1), m0 != 0u);
+    st_global_pred(out + pos + 1, base + (uint32_t)(__ffs(m1) - 1), m1 != 0u);
+    st_global_pred(out + pos + 2, base + (uint32_t)(__ffs(m2) - 1), m2 != 0u);
+    st_global_pred(out + pos + 3, base + (uint32_t)(__ffs(m3) - 1), m3 != 0u);
+    uint32_t p4 = pos + 4u;
+    pos += __popc(m0);
+    while (m4) {
+      out[p4++] = (int32_t)(base + (uint32_t)(__ffs(m4) - 1));
+      m4 &= m4 - 1u;
+    }
+  }
+  epi_bar();
+  if (et == 0) {
+    stamp(p, l, EV_F_EMIT, cta);
+    signal(LYC_CTR(p.ctr, l, CTR_SELDONE));
+  }
 }
 
 // ---------------------------------------------------------------- kernel
@@ -631,7 +652,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
     mbar_init(&es.bar, 1);
     fence_mbar_init();
   }
-  for (int b = threadIdx.x; b < LYC_BINS; b += kStepThreads) sm.hist[b] = 0u;
+  for (int b = threadIdx.x; b < LYC_H1_BINS; b += kStepThreads) sm.hist[b] = 0u;
   __syncthreads();
   const uint32_t epoch1 = s_epoch + 1u;
   const uint32_t t_attn = epoch1 * (uint32_t)p.n_ctas;
@@ -650,8 +671,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
           // key / histogram buffers of this parity are free once layer l-2's
           // selection (if any) finished
           if (l >= 2 && p.layers[l - 2].n_sel > 0 && p.sel_mode != SEL_NONE)
-            spin_until(LYC_CTR(p.ctr, l - 2, CTR_SELDONE),
-                       epoch1 * (uint32_t)p.layers[l - 2].n_sel);
+            spin_until(LYC_CTR(p.ctr, l - 2, CTR_SELDONE), epoch1 * seldone_per_step(p, l - 2));
           __threadfence();
         }
         consumer_bar();
@@ -711,21 +731,21 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
         stamp(p, l, EV_MERGE, cta);
         signal(LYC_CTR(p.ctr, l, CTR_MERGE));
       }
-      // (b) selection items of this layer's retrieval heads
+      // (b) selection items of this layer's retrieval heads: classify every
+      // own item (the CTA completing a row resolves it), then emit them
       if (L.n_sel > 0 && p.sel_mode != SEL_NONE) {
         const int n_items = L.n_sel * items;
         for (int it = cta; it < n_items; it += p.n_ctas) {
           const int r = it / items, q = it - r * items;
           const SelRow R = sel_row(p, l, r);
-          if (classify_item(p, R, q, epoch1, es, bar_phase, et, l, cta)) {
-            const int row = __ldg(L.sel_rows + r);
-            finish_row(p, R, p.idx + (int64_t)row * p.idx_stride, es, bar_phase, et, l, cta);
-            if (et == 0) {
-              if (p.idx_count) p.idx_count[row] = p.k_sel;
-              stamp(p, l, EV_SELDONE, cta);
-              signal(LYC_CTR(p.ctr, l, CTR_SELDONE));
-            }
-          }
+          if (classify_item(p, R, q, epoch1, es, bar_phase, et, l, cta))
+            finish_row(p, R, __ldg(L.sel_rows + r), es, bar_phase, epoch1, et, l, cta);
+        }
+        for (int it = cta; it < n_items; it += p.n_ctas) {
+          const int r = it / items, q = it - r * items;
+          const SelRow R = sel_row(p, l, r);
+          const int row = __ldg(L.sel_rows + r);
+          emit_item(p, R, q, p.idx + (int64_t)row * p.idx_stride, es, epoch1, et, l, cta);
         }
       }
     }

@@ -10,7 +10,9 @@ __global__ void k(const uint32_t* gbm, int nwords, int* out, long long* cyc) {
   __shared__ __align__(16) uint32_t bmp[64 * 68];
   __shared__ uint32_t stg[4096 + 64];
   __shared__ uint32_t scan[64];
+  __shared__ uint32_t tab[32];
   const int et = threadIdx.x, lane = et & 31, ew = et >> 5;
+  if (et < 32) tab[(0x077CB531u << et) >> 27] = et;
   for (int i = et; i < nwords; i += 64) bmp[bm_pad(i)] = gbm[i];
   __syncthreads();
   const long long c0 = clock64();
@@ -72,6 +74,22 @@ __global__ void k(const uint32_t* gbm, int nwords, int* out, long long* cyc) {
             asm volatile("st.shared.u32 [%0], %1;" :: "r"(sb + 4u * p2), "r"(base + (uint32_t)(__ffs(m4) - 1)) : "memory");
             ++p2; m4 &= m4 - 1u;
           }
+        } else if (MODE == 7) {
+          const uint32_t sb = (uint32_t)__cvta_generic_to_shared(stg);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t lb = m & (0u - m);
+            m ^= lb;
+            const uint32_t j = tab[(lb * 0x077CB531u) >> 27];
+            asm volatile("{.reg .pred p; setp.ne.u32 p, %2, 0; @p st.shared.u32 [%0], %1;}" :: "r"(sb + 4u * pos), "r"(base + j), "r"(lb) : "memory");
+            pos += lb != 0u;
+          }
+          while (m) {
+            const uint32_t lb = m & (0u - m);
+            m ^= lb;
+            asm volatile("st.shared.u32 [%0], %1;" :: "r"(sb + 4u * pos), "r"(base + tab[(lb * 0x077CB531u) >> 27]) : "memory");
+            ++pos;
+          }
         } else if (MODE == 5) {
           while (m) { out[pos++] = base + (uint32_t)(__ffs(m) - 1); m &= m - 1; }
         } else if (MODE == 2) {
@@ -102,7 +120,7 @@ int main() {
   uint32_t* d; int* o; long long* cyc;
   cudaMalloc(&d, sizeof(h)); cudaMalloc(&o, 8192 * 4); cudaMalloc(&cyc, 32);
   cudaMemcpy(d, h, sizeof(h), cudaMemcpyHostToDevice);
-  for (int mode = 0; mode < 7; ++mode)
+  for (int mode = 0; mode < 8; ++mode)
     for (int r = 0; r < 2; ++r) {
       switch (mode) {
         case 0: k<0><<<1, 64>>>(d, nwords, o, cyc); break;
@@ -110,6 +128,7 @@ int main() {
         case 2: k<2><<<1, 64>>>(d, nwords, o, cyc); break;
         case 3: k<3><<<1, 64>>>(d, nwords, o, cyc); break;
         case 4: k<4><<<1, 64>>>(d, nwords, o, cyc); break;
+        case 7: k<7><<<1, 64>>>(d, nwords, o, cyc); break;
         case 6: k<6><<<1, 64>>>(d, nwords, o, cyc); break;
         case 5: k<5><<<1, 64>>>(d, nwords, o + 4096, cyc); break;
       }

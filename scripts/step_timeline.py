@@ -52,9 +52,9 @@ def main():
     # selection events in chronological order (max over CTAs; NaN = no selection)
     ev = [("cons_beg", 0, "min"), ("cons_end", 1, "max"), ("merge", 3, "max"),
           ("c_prefix", 8, "max"), ("c_keys", 9, "max"), ("c_done", 10, "max"),
-          ("f_prefix", 11, "max"), ("f_scan", 12, "max"), ("f_loaded", 6, "max"),
-          ("f_radix", 4, "max"), ("f_join", 5, "max"), ("f_count", 14, "max"), ("f_emit", 13, "max"),
-          ("seldone", 7, "max")]
+          ("f_scan", 12, "max"), ("f_loaded", 6, "max"), ("f_narrow", 11, "max"),
+          ("f_compact", 15, "max"), ("f_ranked", 4, "max"), ("f_release", 5, "max"),
+          ("e_wake", 14, "max"), ("e_done", 13, "max")]
     print(f"{'l':>3} {'R':>2} " + " ".join(f"{n:>9}" for n, _, _ in ev))
     for l in range(NL):
         nr = int((roles[l] == 0).sum()) if l else H
@@ -66,9 +66,7 @@ def main():
             else:
                 vals.append(rel[l, e].max() if x.max() > t0 else float("nan"))
         print(f"{l:3d} {nr:2d} " + " ".join(f"{v:9.1f}" for v in vals))
-    x = tr[NL - 1, 15].max()
-    print("last-layer emission: cycles", x >> 32, "max round", (x >> 12) & 0xFFFFF, "stores", x & 0xFFF)
-    print("step span us:", (tr[:, :14].max() - t0) / 1e3)
+    print("step span us:", (tr.max() - t0) / 1e3)
 
 
 if __name__ == "__main__":
