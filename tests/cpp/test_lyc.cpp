@@ -1,0 +1,328 @@
+// test_lyc.cpp -- C++ parity tests of the drop-in host API (include/lyc.hpp)
+// on the B200, written like the reference's own GTest suites
+// (tests/kernel_sim_test.cpp, attention_test.cpp, decode_engine_test.cpp;
+// GTest is not in this image, so a minimal CHECK harness).  The expected
+// values come from plain-loop oracles in this file (the reference's
+// test_util.hpp style: two-pass softmax in double), never from the library.
+//
+//   make -C tests/cpp && build/cpp/test_lyc            (needs a GPU)
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <numeric>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "lyc.hpp"
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(cond)                                                        \
+  do {                                                                     \
+    ++g_checks;                                                            \
+    if (!(cond)) {                                                         \
+      ++g_fail;                                                            \
+      std::printf("  FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);        \
+    }                                                                      \
+  } while (0)
+#define CHECK_THROWS(stmt, Exc)                                            \
+  do {                                                                     \
+    bool thrown_ = false;                                                  \
+    try {                                                                  \
+      stmt;                                                                \
+    } catch (const Exc&) {                                                 \
+      thrown_ = true;                                                      \
+    } catch (...) {                                                        \
+    }                                                                      \
+    CHECK(thrown_ && #Exc);                                                \
+  } while (0)
+
+using lyc::kernel::BlockIndexSet;
+using lyc::kernel::Workload;
+
+// ---------------------------------------------------------------- oracles
+// test_util.hpp naive_attention: two-pass softmax over the listed rows, f64.
+static std::vector<double> naive_attention(const float* q, const float* K, const float* V, int d,
+                                           const std::vector<int>& rows, double scale) {
+  std::vector<double> s(rows.size());
+  double m = -INFINITY;
+  for (size_t i = 0; i < rows.size(); ++i) {
+    double acc = 0;
+    for (int c = 0; c < d; ++c) acc += (double)q[c] * K[(size_t)rows[i] * d + c];
+    s[i] = acc * scale;
+    m = std::max(m, s[i]);
+  }
+  double l = 0;
+  for (double& x : s) l += (x = std::exp(x - m));
+  std::vector<double> o(d, 0.0);
+  for (size_t i = 0; i < rows.size(); ++i)
+    for (int c = 0; c < d; ++c) o[c] += s[i] / l * V[(size_t)rows[i] * d + c];
+  return o;
+}
+
+// attention.hpp:108-123: k largest, ties to the lower index, ascending.
+static std::vector<int> top_k(const std::vector<double>& w, size_t k) {
+  std::vector<int> idx(w.size());
+  std::iota(idx.begin(), idx.end(), 0);
+  const size_t kk = std::min(k, w.size());
+  std::partial_sort(idx.begin(), idx.begin() + kk, idx.end(),
+                    [&](int a, int b) { return w[a] > w[b] || (w[a] == w[b] && a < b); });
+  idx.resize(kk);
+  std::sort(idx.begin(), idx.end());
+  return idx;
+}
+
+static Workload<float> random_workload(std::mt19937_64& rng, int B, int H, int G, int d, int L,
+                                       double sparse_frac) {
+  std::uniform_real_distribution<float> U(-1.f, 1.f);
+  Workload<float> w;
+  w.batch = B;
+  w.n_kv_heads = H;
+  w.group_size = G;
+  w.d_head = d;
+  w.seq_len = L;
+  w.block_size = 64;
+  w.scale = 1.f / std::sqrt((float)d);
+  const int nb = (L + 63) / 64;
+  for (int i = 0; i < B * H; ++i) {
+    lyc::kernel::Matrix<float> k(L, d), v(L, d);
+    for (auto& x : k.data) x = U(rng);
+    for (auto& x : v.data) x = U(rng);
+    w.keys.push_back(std::move(k));
+    w.values.push_back(std::move(v));
+  }
+  for (int h = 0; h < B * H * G; ++h) {
+    std::vector<float> q(d);
+    for (auto& x : q) x = U(rng);
+    w.queries.push_back(std::move(q));
+  }
+  w.blocks.batch = B;
+  w.blocks.n_kv_heads = H;
+  for (int i = 0; i < B * H; ++i) {
+    std::vector<uint32_t> ids;
+    for (int b = 0; b < nb; ++b)
+      if (i % 2 == 0 || std::uniform_real_distribution<double>(0, 1)(rng) < sparse_frac) ids.push_back(b);
+    if (ids.empty()) ids.push_back(0);
+    w.blocks.ids.push_back(ids);
+  }
+  return w;
+}
+
+// kernel_sim_test.cpp:69-88 reference_outputs: sparse attention over the
+// expanded token set of every slot.
+static std::vector<std::vector<double>> expected_outputs(const Workload<float>& w) {
+  std::vector<std::vector<double>> out;
+  for (size_t b = 0; b < w.batch; ++b)
+    for (size_t g = 0; g < w.n_kv_heads; ++g) {
+      const size_t slot = b * w.n_kv_heads + g;
+      std::vector<int> rows;
+      for (uint32_t blk : w.blocks.ids[slot])
+        for (size_t r = blk * 64; r < std::min<size_t>((blk + 1) * 64, w.seq_len); ++r) rows.push_back((int)r);
+      for (size_t j = 0; j < w.group_size; ++j)
+        out.push_back(naive_attention(w.queries[(b * w.n_kv_heads + g) * w.group_size + j].data(),
+                                      w.keys[slot].data.data(), w.values[slot].data.data(),
+                                      (int)w.d_head, rows, w.scale));
+    }
+  return out;
+}
+
+// ---------------------------------------------------------------- tests
+static void test_plan_splits_known() {  // kernel_sim_test.cpp:113-138
+  BlockIndexSet a{1, 1, {{0, 1, 2, 3, 4, 5, 6, 7}}};
+  auto s = lyc::kernel::plan_splits(a, 2);
+  CHECK(s.split_blocks[0] == (std::vector<size_t>{4, 4}));
+  CHECK(s.units[0][0].size() == 1 && s.units[0][1][0].head_local_split == 1);
+  BlockIndexSet b{1, 3, {{}, {}, {}}};
+  for (uint32_t i = 0; i < 16; ++i) b.ids[0].push_back(i);
+  b.ids[1] = {0, 1};
+  b.ids[2] = {0, 1};
+  auto t = lyc::kernel::plan_splits(b, 4);
+  CHECK(t.split_blocks[0] == (std::vector<size_t>{5, 5, 5, 5}));
+  CHECK(t.head_split_count[0] == (std::vector<size_t>{4, 1, 1}));
+  auto r = lyc::kernel::latency_model(t, 1024);
+  CHECK(r.pooled_critical_blocks == 5 && r.naive_critical_blocks == 16 && r.total_blocks == 20);
+  CHECK(r.pooled_critical_bytes == 5 * 1024);
+  CHECK_THROWS(lyc::kernel::plan_splits(a, 0), std::invalid_argument);
+  BlockIndexSet z{1, 2, {{}, {}}};
+  CHECK_THROWS(lyc::kernel::plan_splits(z, 2), std::invalid_argument);
+}
+
+static void test_run_exactness_sweep() {  // acceptance_test.cpp:269-345, kernel_sim_test.cpp:219-239
+  std::mt19937_64 rng(2602);
+  double worst = 0;
+  for (int trial = 0; trial < 6; ++trial) {
+    const int B = 1 + trial % 3, H = 1 + trial % 4, G = 1 + trial % 4, d = trial % 2 ? 64 : 128;
+    const int L = 300 + 700 * trial;
+    auto w = random_workload(rng, B, H, G, d, L, 0.1);
+    auto want = expected_outputs(w);
+    for (size_t splits : {1, 3, 8}) {
+      auto res = lyc::kernel::run(w, splits, 2);
+      CHECK(res.outputs.size() == want.size());
+      for (size_t h = 0; h < want.size(); ++h)
+        for (size_t c = 0; c < w.d_head; ++c)
+          worst = std::max(worst, std::abs((double)res.outputs[h][c] - want[h][c]));
+      // conservation (kernel_sim_test.cpp:241-248): every listed block once
+      CHECK(std::all_of(res.block_exec_counts.begin(), res.block_exec_counts.end(),
+                        [](uint32_t c) { return c == 1; }));
+      size_t listed = 0;
+      for (auto& l : w.blocks.ids) listed += l.size();
+      CHECK(res.block_exec_counts.size() == listed);
+      CHECK(res.schedule.num_splits == splits);
+    }
+  }
+  std::printf("  run: max |gpu - f64 oracle| = %.3g (bar 1e-5)\n", worst);
+  CHECK(worst < 1e-5);
+}
+
+static void test_run_determinism() {  // kernel_sim_test.cpp:250-264
+  std::mt19937_64 rng(7);
+  auto w = random_workload(rng, 2, 4, 4, 64, 2000, 0.3);
+  auto a = lyc::kernel::run(w, 16, 1);
+  auto b = lyc::kernel::run(w, 16, 8);
+  CHECK(a.outputs == b.outputs);
+}
+
+static void test_run_errors() {
+  std::mt19937_64 rng(3);
+  auto w = random_workload(rng, 1, 2, 2, 64, 256, 0.5);
+  auto bad = w;
+  bad.blocks.ids[0] = {2, 1};
+  CHECK_THROWS(lyc::kernel::run(bad, 2), std::invalid_argument);
+  bad = w;
+  bad.blocks.ids[0] = {99};
+  CHECK_THROWS(lyc::kernel::run(bad, 2), std::invalid_argument);
+  bad = w;
+  bad.queries.pop_back();
+  CHECK_THROWS(lyc::kernel::run(bad, 2), std::invalid_argument);
+  CHECK_THROWS(lyc::kernel::run(w, 0), std::invalid_argument);
+}
+
+static void test_args_top_k() {  // attention_test.cpp:110-135
+  std::vector<float> a{0.4f, 0.1f, 0.3f, 0.2f};
+  CHECK(lyc::args_top_k<float>(a, 2).indices == (std::vector<size_t>{0, 2}));
+  std::vector<float> e(5, 1.f);
+  CHECK(lyc::args_top_k<float>(e, 3).indices == (std::vector<size_t>{0, 1, 2}));
+  CHECK(lyc::args_top_k<float>(a, 9).size() == 4);
+  CHECK_THROWS(lyc::args_top_k<float>(a, 0), std::invalid_argument);
+  std::mt19937_64 rng(11);
+  std::uniform_real_distribution<float> U(-1.f, 1.f);
+  std::vector<float> s(32768);
+  for (auto& x : s) x = U(rng);
+  std::vector<double> sd(s.begin(), s.end());
+  auto got = lyc::args_top_k<float>(s, 2048).indices;
+  auto want = top_k(sd, 2048);
+  CHECK(std::equal(got.begin(), got.end(), want.begin(), want.end()));
+}
+
+// decode_engine.hpp:109-151 restated on host in f64 for one step.
+static void test_hybrid_decoder_tiny() {
+  const int NL = 4, H = 2, G = 4, d = 64, L = 4096, K = 256;
+  std::vector<uint8_t> roles(NL * H, 1);
+  roles[0] = roles[1] = 0;  // layer 0 all retrieval
+  roles[2 * H + 1] = 0;     // one retrieval head above
+  std::mt19937_64 rng(1234);
+  std::uniform_real_distribution<float> U(-1.f, 1.f);
+  std::vector<float> q((size_t)NL * H * G * d), k((size_t)NL * H * L * d), v(k.size());
+  for (auto* vec : {&q, &k, &v})
+    for (auto& x : *vec) x = U(rng);
+  lyc::DeviceBuffer dq(q.size() * 4), dk(k.size() * 4), dv(v.size() * 4), dout(q.size() * 4);
+  dq.upload(q.data(), q.size() * 4);
+  dk.upload(k.data(), k.size() * 4);
+  dv.upload(v.data(), v.size() * 4);
+  lyc::HybridDecoder::Config c;
+  c.n_layers = NL;
+  c.batch = 1;
+  c.n_kv_heads = H;
+  c.group_size = G;
+  c.d_head = d;
+  c.dtype = lyc::Dtype::F32;
+  c.seq_cap = L;
+  c.policy = lyc::SparsityPolicy::top_k(K);
+  lyc::HybridDecoder dec(c, roles);
+  dec.decode_step(dq.get(), dk.get(), dv.get(), L, dout.get());
+  std::vector<float> out(q.size());
+  cudaDeviceSynchronize();
+  dout.download(out.data(), out.size() * 4);
+  auto sets = dec.token_sets();
+  // host restatement
+  const double scale = 1.0 / std::sqrt((double)d);
+  std::vector<std::vector<int>> sets_ref(H);
+  double worst = 0, ref_max = 0;
+  std::vector<int> all(L);
+  std::iota(all.begin(), all.end(), 0);
+  for (int l = 0; l < NL; ++l)
+    for (int g = 0; g < H; ++g) {
+      const float* Kl = k.data() + ((size_t)l * H + g) * L * d;
+      const float* Vl = v.data() + ((size_t)l * H + g) * L * d;
+      const bool retrieval = l == 0 || roles[l * H + g] == 0;
+      const std::vector<int>& rows = retrieval ? all : sets_ref[g];
+      for (int j = 0; j < G; ++j) {
+        const float* qh = q.data() + (((size_t)l * H + g) * G + j) * d;
+        auto o = naive_attention(qh, Kl, Vl, d, rows, scale);
+        for (int cc = 0; cc < d; ++cc) {
+          worst = std::max(worst, std::abs((double)out[(((size_t)l * H + g) * G + j) * d + cc] - o[cc]));
+          ref_max = std::max(ref_max, std::abs(o[cc]));
+        }
+      }
+      if (retrieval) {  // pooled-query selection (gqa_pool_queries + dense weights)
+        std::vector<double> pooled(d, 0.0), w(L);
+        for (int j = 0; j < G; ++j)
+          for (int cc = 0; cc < d; ++cc) pooled[cc] += q[(((size_t)l * H + g) * G + j) * d + cc];
+        for (auto& x : pooled) x /= G;
+        for (int t = 0; t < L; ++t) {
+          double acc = 0;
+          for (int cc = 0; cc < d; ++cc) acc += pooled[cc] * Kl[(size_t)t * d + cc];
+          w[t] = acc * scale;
+        }
+        sets_ref[g] = top_k(w, K);
+      }
+    }
+  const double rel = worst / std::max(ref_max, 1e-3);
+  std::printf("  decoder: rel err %.3g (bar 1e-5), sets %s\n", rel,
+              sets[0] == std::vector<int32_t>(sets_ref[0].begin(), sets_ref[0].end()) ? "equal" : "DIFFER");
+  CHECK(rel < 1e-5);
+  for (int g = 0; g < H; ++g) CHECK(sets[g] == std::vector<int32_t>(sets_ref[g].begin(), sets_ref[g].end()));
+}
+
+static void test_hybrid_decoder_errors() {
+  lyc::HybridDecoder::Config c;
+  c.n_layers = 2;
+  c.n_kv_heads = 2;
+  c.group_size = 4;
+  c.d_head = 64;
+  c.seq_cap = 1024;
+  c.policy = lyc::SparsityPolicy::top_k(16);
+  std::vector<uint8_t> bad{1, 0, 0, 0};  // layer 0 must be all retrieval
+  CHECK_THROWS(lyc::HybridDecoder(c, bad), std::invalid_argument);
+  std::vector<uint8_t> ok{0, 0, 1, 1};
+  c.policy = lyc::SparsityPolicy::top_p(0.9);
+  CHECK_THROWS(lyc::HybridDecoder(c, ok), lyc::not_supported);
+  CHECK_THROWS(lyc::SparsityPolicy::top_k(0), std::invalid_argument);
+  CHECK_THROWS(lyc::SparsityPolicy::ratio(1.5), std::invalid_argument);
+  CHECK(lyc::fraction_budget(0.1, 100) == 10);
+}
+
+int main() {
+  const std::pair<const char*, std::function<void()>> tests[] = {
+      {"PlanSplits.KnownAnswersAndErrors", test_plan_splits_known},
+      {"Run.ExactnessSweepF32", test_run_exactness_sweep},
+      {"Run.DeterministicAcrossWorkers", test_run_determinism},
+      {"Run.Errors", test_run_errors},
+      {"ArgsTopK.KnownCasesTiesAndSort", test_args_top_k},
+      {"HybridDecoder.TinyStepMatchesHostLoop", test_hybrid_decoder_tiny},
+      {"HybridDecoder.Errors", test_hybrid_decoder_errors},
+  };
+  for (const auto& [name, fn] : tests) {
+    const int before = g_fail;
+    try {
+      fn();
+    } catch (const std::exception& e) {
+      ++g_fail;
+      std::printf("  FAIL uncaught %s\n", e.what());
+    }
+    std::printf("[%s] %s\n", g_fail == before ? "  OK  " : " FAIL ", name);
+  }
+  std::printf("%d checks, %d failures\n", g_checks, g_fail);
+  return g_fail ? 1 : 0;
+}
