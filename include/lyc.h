@@ -183,6 +183,37 @@ int lyc_decoder_is_fused(lyc_decoder* dec);
 int lyc_decoder_set_trace(lyc_decoder* dec, int enable);
 int64_t lyc_decoder_trace(lyc_decoder* dec, unsigned long long* out, int64_t cap);
 
+/* ---------------------------------------------------------------------------
+ * KV-sequence sharding across GPUs (the inter-GPU form of the
+ * split pooling of kernel_sim.hpp:63-110 with the combine of :205-225).
+ * Rank p of P holds rows [row_begin, row_begin + n_local) of every head's
+ * cache, numbered locally (k, v point at local row 0 of layer 0; seq_cap is
+ * the slab stride).  Per layer, in order:
+ *   1. lyc_shard_layer: local attention partials -- fp32 normalized o
+ *      [B][Hq][d] and base-2 LSE [B][Hq] -- and, for the layer's retrieval
+ *      heads, the exact local top-k of this shard's pooled scores as
+ *      (order-preserving key, GLOBAL token id) rows [B*H][k_cap], ascending,
+ *      padded with key 0 / id -1.  Sparse heads read this rank's filtered
+ *      index-cache rows (written by step 3 of an earlier layer).
+ *   2. the caller all-gathers [part_o | part_lse | cand_key | cand_idx] of all
+ *      ranks in rank order (one packed ncclAllGather).
+ *   3. lyc_shard_merge: identically on every rank, the rank-ordered LSE merge
+ *      into out_l (dtype) and, per retrieval (b, g), the global top-k over the
+ *      gathered candidates (ties to the lower global id) -> global_sets
+ *      [B*H][k_cap] (optional) and this rank's filtered index-cache row.
+ * seq_total = sum of n_local over ranks (the global budget is computed on it).
+ * rank_stride: distance in 4-byte words between consecutive ranks' blocks when
+ * the four fields are packed per rank in that order into one gathered buffer
+ * (one collective); 0 when each field was gathered into its own array.
+ * Token-mode selection only (LYC_ENOTSUP for block mode). */
+int lyc_shard_layer(lyc_decoder* dec, int32_t layer, const void* q_l, const void* k,
+                    const void* v, int64_t n_local, int64_t row_begin, float* part_o,
+                    float* part_lse, uint32_t* cand_key, int32_t* cand_idx, void* stream);
+int lyc_shard_merge(lyc_decoder* dec, int32_t layer, int32_t world, const float* all_o,
+                    const float* all_lse, const uint32_t* all_key, const int32_t* all_idx,
+                    int64_t rank_stride, int64_t n_local, int64_t row_begin, int64_t seq_total,
+                    void* out_l, int32_t* global_sets, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

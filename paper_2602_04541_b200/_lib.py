@@ -23,6 +23,7 @@ SYMBOLS = [
     "lyc_decoder_replay", "lyc_decoder_index_cache", "lyc_decoder_launches_per_step",
     "lyc_decoder_step_bytes", "lyc_decoder_layer_attn_bytes", "lyc_decoder_set_timing",
     "lyc_decoder_attn_ms", "lyc_decoder_is_fused", "lyc_decoder_set_trace", "lyc_decoder_trace",
+    "lyc_shard_layer", "lyc_shard_merge",
 ]
 
 
@@ -122,6 +123,10 @@ def lib() -> C.CDLL:
     L.lyc_decoder_set_trace.argtypes = [vp, C.c_int]
     L.lyc_decoder_trace.restype = i64
     L.lyc_decoder_trace.argtypes = [vp, vp, i64]
+    L.lyc_shard_layer.restype = C.c_int
+    L.lyc_shard_layer.argtypes = [vp, i32, vp, vp, vp, i64, i64, vp, vp, vp, vp, vp]
+    L.lyc_shard_merge.restype = C.c_int
+    L.lyc_shard_merge.argtypes = [vp, i32, i32, vp, vp, vp, vp, i64, i64, i64, i64, vp, vp, vp]
     _lib = L
     return L
 

@@ -52,7 +52,8 @@ __global__ void __launch_bounds__(128) split_merge_kernel(const __grid_constant_
   if (task >= p.n_tasks) return;
   const LycMergeTask tk = p.tasks[task];
   const LycSlot s = p.slots[tk.slot];
-  merge_task<T>(p.part_o, p.part_lse, s, tk.j, chunk, p.group, p.d, p.out, lane);
+  merge_task<T>(p.part_o, p.part_lse, s, tk.j, chunk, p.group, p.d, p.out, lane, p.out_f32,
+                p.out_lse);
 }
 
 // ---------------------------------------------------------------- launchers

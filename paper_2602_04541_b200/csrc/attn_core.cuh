@@ -136,7 +136,8 @@ __device__ __forceinline__ Tile tile_of(const LycSlot& s, int item, int sub, int
   if (s.kind == ITEM_TOKENS) {
     t.ids = s.list + (int64_t)item * LYC_TILE;
     t.lo = 0;
-    t.nvalid = min(LYC_TILE, s.list_len - item * LYC_TILE);
+    const int len = s.count ? min(s.list_len, __ldcg(s.count)) : s.list_len;
+    t.nvalid = min(LYC_TILE, len - item * LYC_TILE);
   } else {
     const int blk = s.kind == ITEM_DENSE ? item : __ldcg(s.list + item);
     const int b0 = blk * bs;
@@ -293,12 +294,17 @@ __device__ __forceinline__ void unit_epilogue(const LycView& p, const LycSlot& s
       L += ml[(w * kMaxG + j) * 2 + 1] * f;
       O += mo[(w * kMaxG + j) * D + d] * f;
     }
-    const float o = O / L;
-    if (direct) {
+    // L == 0: the unit saw no valid row (a shard holding none of a sparse
+    // head's indices) -- an empty partial (o = 0, lse = -inf)
+    const float o = L > 0.f ? O / L : 0.f;
+    if (direct && p.out_f32) {
+      p.out_f32[(int64_t)(s.q_row + j) * D + d] = o;
+      if (d == 0) p.out_lse[s.q_row + j] = L > 0.f ? log2f(L) + M : -INFINITY;
+    } else if (direct) {
       store_out<T>(static_cast<T*>(p.out) + (int64_t)(s.q_row + j) * D + d, o);
     } else {
       p.part_o[((int64_t)u * G + j) * D + d] = o;
-      if (d == 0) p.part_lse[(int64_t)u * G + j] = log2f(L) + M;
+      if (d == 0) p.part_lse[(int64_t)u * G + j] = L > 0.f ? log2f(L) + M : -INFINITY;
     }
   }
   static_assert(kConsumerWarps * 32 * 32 == LYC_H1_BINS && LYC_H1_COARSE * 64 == LYC_H1_BINS,
@@ -653,19 +659,21 @@ __device__ __forceinline__ void consume_units(const LycView& p, const AttnSmem<T
 template <typename T>
 __device__ __forceinline__ void merge_task(const float* part_o, const float* part_lse,
                                            const LycSlot& s, int j, int chunk, int G, int D,
-                                           void* out, int lane) {
+                                           void* out, int lane, float* out_f32 = nullptr,
+                                           float* out_lse = nullptr) {
   float M = -INFINITY;
   for (int i = lane; i < s.n_units; i += 32)
     M = fmaxf(M, __ldcg(part_lse + (int64_t)(s.first_unit + i) * G + j));
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+  const float Mz = M == -INFINITY ? 0.f : M;  // all partials empty: weights 0, output 0
   float den = 0.f;
   float acc[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) acc[c] = 0.f;
   for (int i = lane; i < s.n_units; i += 32) {
     const int64_t u = s.first_unit + i;
-    const float w = exp2f(__ldcg(part_lse + u * G + j) - M);
+    const float w = exp2f(__ldcg(part_lse + u * G + j) - Mz);
     den += w;
     const float4* src = reinterpret_cast<const float4*>(part_o + (u * G + j) * D + chunk * 32);
 #pragma unroll
@@ -693,9 +701,13 @@ __device__ __forceinline__ void merge_task(const float* part_o, const float* par
       acc[c] = keep + __shfl_xor_sync(0xffffffffu, send, half);
     }
   }
-  if (chunk * 32 + lane < D)
-    store_out<T>(static_cast<T*>(out) + (int64_t)(s.q_row + j) * D + chunk * 32 + lane,
-                 acc[0] / den);
+  const float o = den > 0.f ? acc[0] / den : 0.f;
+  if (out_f32) {
+    if (chunk * 32 + lane < D) out_f32[(int64_t)(s.q_row + j) * D + chunk * 32 + lane] = o;
+    if (chunk == 0 && lane == 0) out_lse[s.q_row + j] = den > 0.f ? log2f(den) + Mz : -INFINITY;
+  } else if (chunk * 32 + lane < D) {
+    store_out<T>(static_cast<T*>(out) + (int64_t)(s.q_row + j) * D + chunk * 32 + lane, o);
+  }
 }
 
 }  // namespace lyc

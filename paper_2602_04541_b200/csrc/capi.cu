@@ -28,6 +28,22 @@ cudaError_t launch_float_keys(const float* s, uint32_t* keys, int64_t n, cudaStr
 cudaError_t launch_step(const LycStepParams& p, int dtype, int d, cudaStream_t st);
 bool step_supported(int dtype, int d);
 int64_t step_max_keys();
+cudaError_t launch_shard_candidates(const uint32_t* keys, int64_t key_stride,
+                                    const int32_t* local_ids, const int32_t* cnt,
+                                    const int32_t* sel_rows, int n_sel, int64_t k_cap,
+                                    int64_t row_begin, uint32_t* cand_key, int32_t* cand_idx,
+                                    cudaStream_t st);
+cudaError_t launch_shard_merge(const float* all_o, const float* all_lse, int64_t stride_o,
+                               int64_t stride_lse, int world, int rows, int d, void* out,
+                               int dtype, cudaStream_t st);
+cudaError_t launch_shard_gather(const uint32_t* all_key, const int32_t* all_idx, int64_t stride,
+                                int world, int64_t k_cap, const int32_t* sel_rows, int n_sel,
+                                uint32_t* keys, int32_t* ids, cudaStream_t st);
+cudaError_t launch_shard_finalize(const int32_t* pos, int64_t pos_stride, const int32_t* ids,
+                                  int64_t id_stride, int k, const int32_t* sel_rows, int n_sel,
+                                  int64_t row_begin, int64_t n_local, int32_t* global_sets,
+                                  int64_t global_stride, int32_t* cache, int64_t cache_stride,
+                                  int32_t* cache_count, cudaStream_t st);
 int64_t step_bitmap_words(int64_t n_keys);
 int step_item_keys();
 }  // namespace lyc
@@ -457,6 +473,14 @@ struct lyc_decoder {
   std::vector<uint8_t> roles;
   int B = 0, H = 0, G = 0, Hq = 0, D = 0, NL = 0, S = 0, bs = 64;
   bool fused = false;           // whole step in one persistent launch (step.cu)
+  bool shard = false;           // KV-sequence shard mode (lyc_shard_layer / lyc_shard_merge)
+  int32_t* shard_ids = nullptr; // [B*H][k_cap] local top-k ids
+  int32_t* shard_cnt = nullptr; // [B*H]
+  int32_t* shard_rows = nullptr;// [B*H] identity rows for the candidate top-k
+  uint32_t* shard_ckey = nullptr;  // [B*H][world * k_cap] concatenated candidates
+  int32_t* shard_cidx = nullptr;
+  int32_t* shard_pos = nullptr; // [B*H][k_cap] positions of the global top-k
+  int shard_world = 0;
   int64_t k_cap = 0;
   int32_t* idx = nullptr;       // [B*H][k_cap]
   int32_t* idx_count = nullptr;
@@ -634,6 +658,7 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
           s.kind = blocks ? ITEM_BLOCKS : ITEM_TOKENS;
           s.list = d->idx + (int64_t)(b * H + g) * d->k_cap;
           s.list_len = (int32_t)kb;
+          if (d->shard) s.count = d->idx_count + (b * H + g);  // this rank's filtered set
           s.n_items = blocks ? (int32_t)kb : (int32_t)((kb + LYC_TILE - 1) / LYC_TILE);
           s.dep = last_r[(size_t)g];
         }
@@ -765,6 +790,10 @@ void decoder_layer(lyc_decoder* d, int l, const void* q_l, const void* k, const 
   ly.ap.v.v = v;
   ly.ap.v.q = q_l;
   ly.ap.v.out = out_l;
+  ly.ap.v.out_f32 = nullptr;
+  ly.ap.v.out_lse = nullptr;
+  ly.mp.out_f32 = nullptr;
+  ly.mp.out_lse = nullptr;
   record(d, d->ev_pre, (size_t)l, st);
   cuda_check(lyc::launch_attn(ly.ap, d->cfg.dtype, d->D, d->B, st), "attention launch");
   record(d, d->ev_post, (size_t)l, st);
@@ -946,6 +975,12 @@ int lyc_decoder_destroy(lyc_decoder* d) {
   free_dev(d->part_o);
   free_dev(d->part_lse);
   free_dev(d->blob);
+  free_dev(d->shard_ids);
+  free_dev(d->shard_cnt);
+  free_dev(d->shard_rows);
+  free_dev(d->shard_ckey);
+  free_dev(d->shard_cidx);
+  free_dev(d->shard_pos);
   delete d;
   return LYC_OK;
 }
@@ -971,6 +1006,140 @@ int lyc_decoder_layer(lyc_decoder* d, int32_t layer, const void* q_l, const void
     }
     decoder_plan(d, seq_len);
     decoder_layer(d, layer, q_l, k, v, out_l, (cudaStream_t)stream);
+    return LYC_OK;
+  });
+}
+
+// ------------------------------------------------------------ shard mode
+namespace {
+void shard_enter(lyc_decoder* d) {
+  if (d->cfg.select_mode == LYC_SELECT_BLOCKS)
+    fail(LYC_ENOTSUP, "shard: sequence sharding supports token-mode selection only");
+  if (d->fused || !d->shard) {
+    d->fused = false;  // per-layer kernels: the collective sits between layers
+    d->shard = true;   // sparse slots read device counts of the filtered sets
+    d->planned_seq = -1;
+  }
+  const size_t rows = (size_t)d->B * d->H;
+  if (!d->shard_ids) {
+    cuda_check(cudaMalloc(&d->shard_ids, rows * d->k_cap * 4), "cudaMalloc shard ids");
+    cuda_check(cudaMalloc(&d->shard_cnt, rows * 4), "cudaMalloc shard cnt");
+    cuda_check(cudaMalloc(&d->shard_rows, rows * 4), "cudaMalloc shard rows");
+    cuda_check(cudaMalloc(&d->shard_pos, rows * d->k_cap * 4), "cudaMalloc shard pos");
+    std::vector<int32_t> iota(rows);
+    for (size_t i = 0; i < rows; ++i) iota[i] = (int32_t)i;
+    cuda_check(cudaMemcpy(d->shard_rows, iota.data(), rows * 4, cudaMemcpyHostToDevice), "H2D");
+  }
+}
+}  // namespace
+
+int lyc_shard_layer(lyc_decoder* d, int32_t layer, const void* q_l, const void* k, const void* v,
+                    int64_t n_local, int64_t row_begin, float* part_o, float* part_lse,
+                    uint32_t* cand_key, int32_t* cand_idx, void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    if (layer < 0 || layer >= d->NL) fail(LYC_EINVAL, "decoder: layer out of range");
+    if (!part_o || !part_lse || !cand_key || !cand_idx) fail(LYC_EINVAL, "shard: null output");
+    if (row_begin < 0) fail(LYC_EINVAL, "shard: row_begin must be >= 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    shard_enter(d);
+    decoder_plan(d, n_local);
+    lyc_decoder::Layer& ly = d->layers[(size_t)layer];
+    ensure_maps(d, k, v);
+    ly.ap.tmap_k = d->maps.tmap_k;
+    ly.ap.tmap_v = d->maps.tmap_v;
+    ly.ap.v.k = k;
+    ly.ap.v.v = v;
+    ly.ap.v.q = q_l;
+    ly.ap.v.out = nullptr;
+    ly.ap.v.out_f32 = part_o;
+    ly.ap.v.out_lse = part_lse;
+    cuda_check(lyc::launch_attn(ly.ap, d->cfg.dtype, d->D, d->B, st), "attention launch");
+    ++g_launches;
+    if (ly.n_merges) {
+      ly.mp.out = nullptr;
+      ly.mp.out_f32 = part_o;
+      ly.mp.out_lse = part_lse;
+      cuda_check(lyc::launch_merge(ly.mp, d->cfg.dtype, st), "merge launch");
+      ++g_launches;
+    }
+    if (ly.n_sel) {  // local top-k of this shard's pooled scores -> (key, global id)
+      LycTopkParams tp = ly.tp;
+      tp.out = d->shard_ids;
+      tp.out_count = d->shard_cnt;
+      cuda_check(lyc::launch_topk(tp, ly.n_sel, ly.cluster, st), "topk launch");
+      cuda_check(lyc::launch_shard_candidates(tp.keys, tp.key_stride, d->shard_ids, d->shard_cnt,
+                                              tp.out_row, ly.n_sel, d->k_cap, row_begin, cand_key,
+                                              cand_idx, st),
+                 "shard candidates");
+      g_launches += 2;
+    }
+    return LYC_OK;
+  });
+}
+
+int lyc_shard_merge(lyc_decoder* d, int32_t layer, int32_t world, const float* all_o,
+                    const float* all_lse, const uint32_t* all_key, const int32_t* all_idx,
+                    int64_t rank_stride, int64_t n_local, int64_t row_begin, int64_t seq_total,
+                    void* out_l, int32_t* global_sets, void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    if (layer < 0 || layer >= d->NL) fail(LYC_EINVAL, "decoder: layer out of range");
+    if (world < 1) fail(LYC_EINVAL, "shard: world must be >= 1");
+    if (seq_total < n_local) fail(LYC_EINVAL, "shard: seq_total < n_local");
+    cudaStream_t st = (cudaStream_t)stream;
+    shard_enter(d);
+    decoder_plan(d, n_local);
+    lyc_decoder::Layer& ly = d->layers[(size_t)layer];
+    const int rows = d->B * d->Hq;
+    const size_t brows0 = (size_t)d->B * d->H;
+    // per-rank strides in 4-byte words: one packed block per rank, or the
+    // natural stride of each separately gathered array
+    const int64_t so = rank_stride ? rank_stride : (int64_t)rows * d->D;
+    const int64_t sl = rank_stride ? rank_stride : (int64_t)rows;
+    const int64_t sc = rank_stride ? rank_stride : (int64_t)brows0 * d->k_cap;
+    cuda_check(lyc::launch_shard_merge(all_o, all_lse, so, sl, world, rows, d->D, out_l,
+                                       d->cfg.dtype, st),
+               "shard merge");
+    ++g_launches;
+    if (ly.n_sel) {
+      const int64_t kg = d->budget(seq_total);  // global budget (TopK / Ratio on the full length)
+      if (kg > d->k_cap) fail(LYC_ENOTSUP, "shard: global budget exceeds the index-cache capacity");
+      const size_t brows = (size_t)d->B * d->H;
+      const int64_t n = (int64_t)world * d->k_cap;
+      if (world > d->shard_world) {
+        free_dev(d->shard_ckey);
+        free_dev(d->shard_cidx);
+        d->shard_ckey = nullptr;
+        d->shard_cidx = nullptr;
+        cuda_check(cudaMalloc(&d->shard_ckey, brows * n * 4), "cudaMalloc shard cand");
+        cuda_check(cudaMalloc(&d->shard_cidx, brows * n * 4), "cudaMalloc shard cand");
+        d->shard_world = world;
+      }
+      cuda_check(lyc::launch_shard_gather(all_key, all_idx, sc, world, d->k_cap, ly.tp.out_row,
+                                          ly.n_sel, d->shard_ckey, d->shard_cidx, st),
+                 "shard gather");
+      LycTopkParams tp;
+      std::memset(&tp, 0, sizeof(tp));
+      tp.keys = d->shard_ckey;
+      tp.key_stride = n;
+      tp.n = (int32_t)n;
+      tp.k = (int32_t)kg;
+      tp.out = d->shard_pos;
+      tp.out_row = d->shard_rows;
+      tp.out_stride = d->k_cap;
+      tp.out_count = nullptr;
+      const int cluster = lyc::topk_cluster_size((int)n, 16384);
+      tp.slice = (int32_t)((n + cluster - 1) / cluster);
+      tp.clear_keys = 0;
+      cuda_check(lyc::launch_topk(tp, ly.n_sel, cluster, st), "shard topk");
+      cuda_check(lyc::launch_shard_finalize(d->shard_pos, d->k_cap, d->shard_cidx, n, (int)kg,
+                                            ly.tp.out_row, ly.n_sel, row_begin, n_local,
+                                            global_sets, d->k_cap, d->idx, d->k_cap, d->idx_count,
+                                            st),
+                 "shard finalize");
+      g_launches += 3;
+    }
     return LYC_OK;
   });
 }

@@ -38,6 +38,7 @@ struct LycSlot {
   int32_t q_row;         // first query/output row: b*Hq + g*G
   int32_t sel;           // selection output row (-1: none)
   int32_t dep;           // layer whose selection wrote `list` (-1: none / already complete)
+  const int32_t* count;  // ITEM_TOKENS: device count of valid ids (<= list_len), or nullptr
 };
 
 struct LycUnit {
@@ -64,6 +65,8 @@ struct LycView {
   uint32_t* sel_keys;       // [n_sel][sel_stride]
   uint32_t* hist1;          // optional [n_sel][LYC_H1_ROW]: fused first radix pass (+ coarse bins)
   uint32_t* exec_counts;    // optional [n_slots][counts_stride] per item
+  float* out_f32;           // optional: fp32 outputs [rows][d] instead of `out` (shard partials)
+  float* out_lse;           // optional with out_f32: base-2 LSE per output row
   int64_t sel_stride;
   int32_t counts_stride;
   int32_t n_splits;         // splits per batch item (grid.x)
@@ -96,6 +99,8 @@ struct LycMergeParams {
   const LycSlot* slots;
   const LycMergeTask* tasks;
   void* out;
+  float* out_f32;           // optional: fp32 outputs + base-2 LSE (shard partials)
+  float* out_lse;
   int32_t n_tasks;
   int32_t group;
   int32_t chunks;           // ceil(d / 32)
