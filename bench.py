@@ -50,6 +50,7 @@ WORKLOADS = {
     "llama3-8b-32k": dict(NL=32, H=8, G=4, d=128, L=32768, k=2048, B=1, dtype="bf16"),
     "qwen3-8b-128k": dict(NL=36, H=8, G=4, d=128, L=131072, k=4096, B=1, dtype="bf16"),
     "llama3-8b-64k-b16": dict(NL=32, H=8, G=4, d=128, L=65536, k=2048, B=16, dtype="bf16"),
+    "llama3-8b-256k-b4": dict(NL=32, H=8, G=4, d=128, L=262144, k=2048, B=4, dtype="bf16"),
     "tiny": dict(NL=4, H=2, G=4, d=64, L=4096, k=256, B=1, dtype="f32"),
 }
 
@@ -133,6 +134,16 @@ class ClockSampler:
                 "samples": len(self.samples), "reasons": sorted(self.reasons)}
 
 
+def ncu_traffic(workload):
+    """dram read+write bytes per launch of the step kernel from the committed
+    `ncu --set full` capture (profiles/ncu_traffic.json), or None."""
+    try:
+        t = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())[workload]
+        return float(t["dram_bytes_read"] + t["dram_bytes_write"])
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
@@ -177,12 +188,29 @@ def cpu_sample(wl, roles, K_host=None, V_host=None, q_host=None, reps=1, want_ou
                        scale=1 / np.sqrt(d), num_splits=splits, dtype=np.float32)
         best = time.perf_counter() - t0
     us = best * 1e6 * total_blocks / sample_blocks
+    # selection pass of one retrieval head (decode_engine.hpp:129-132): pooled
+    # query (gqa_pool_queries), dense_attention weights, select_tokens TopK --
+    # the reference runs it serially per retrieval (layer, head); scaled by the
+    # step's retrieval slot count
+    n_ret = B * int(sum(1 for l in range(NL) for g in range(H) if roles[l, g] == 0))
+    t_sel = 0.0
+    if kind == "reference":
+        pooled = lib.gqa_pool_queries(q_host[:G], G)[0]
+        Kd, Vd = K_host[0].astype(np.float64), V_host[0].astype(np.float64)
+        t0 = time.perf_counter()
+        _, w = lib.dense_attention(pooled, Kd, Vd, 1 / np.sqrt(d))
+        lib.select_tokens("topk", w, k=min(k, L))
+        t_sel = time.perf_counter() - t0
+        us += t_sel * 1e6 * n_ret
     info = {"kind": kind, "cores": cores,
             "sample": (f"hh::kernel::run<float> one layer: 1 retrieval head ({nb} blocks) + "
                        f"{H - 1} sparse heads ({nblk} blocks), L={L}, d={d}, G={G}, "
                        f"{splits} splits, {cores} workers; {best * 1e3:.1f} ms, scaled x"
-                       f"{total_blocks / sample_blocks:.2f} by block count to one decode step "
-                       f"(selection pass not included)")}
+                       f"{total_blocks / sample_blocks:.2f} by block count to one decode step"
+                       + (f"; plus the selection pass of one retrieval head (gqa_pool_queries + "
+                          f"dense_attention f64 weights + select_tokens TopK, 1 thread, "
+                          f"{t_sel * 1e3:.1f} ms) x {n_ret} retrieval slots" if t_sel else
+                          " (selection pass not included)"))}
     return us, info
 
 
@@ -222,12 +250,80 @@ def config_of(args, wl):
     c = {"workload": args.workload, "layers": wl["NL"], "q_heads": wl["H"] * wl["G"],
          "kv_heads": wl["H"], "head_dim": wl["d"], "context": wl["L"], "top_k": wl["k"],
          "batch": wl["B"], "retrieval_fraction": args.retrieval_frac, "select": args.select,
-         "parallelism": f"head-sharded x{args.gpus}" if args.gpus > 1 else "single GPU",
+         "parallelism": (f"{args.shard}-sharded x{args.gpus}" if args.gpus > 1 else "single GPU"),
          "l2": "inputs larger than L2 (KV caches >> 126 MB), no flush"}
     return c
 
 
 # ----------------------------------------------------------------------- GPU
+def run_seq_sharded(args, wl, roles, rank, world, local):
+    """KV-sequence sharding: every rank holds L/N rows of every
+    head; per layer one packed NCCL all-gather of [partials | top-k candidates]
+    (paper_2602_04541_b200/sharded.py).  Total work fixed: strong scaling."""
+    import torch
+    import torch.distributed as dist
+    import paper_2602_04541_b200 as P
+    from paper_2602_04541_b200.sharded import ShardedDecoder, shard_rows
+    NL, H, G, d, L, k, B = (wl[x] for x in ("NL", "H", "G", "d", "L", "k", "B"))
+    dev = torch.device("cuda", local)
+    dt = torch.bfloat16 if wl["dtype"] == "bf16" else torch.float32
+    rb, nl = shard_rows(L, world, rank)
+    gen = torch.Generator(device=dev).manual_seed(args.seed + 17 * rank)
+    K = torch.empty((NL, B, H, nl, d), dtype=dt, device=dev)
+    V = torch.empty_like(K)
+    for t in (K, V):
+        for l in range(NL):
+            t[l].uniform_(-1, 1, generator=gen)
+    qgen = torch.Generator(device=dev).manual_seed(args.seed)  # q identical on every rank
+    q = torch.empty((NL, B, H * G, d), dtype=dt, device=dev).uniform_(-1, 1, generator=qgen)
+    out = torch.empty_like(q)
+    sd = ShardedDecoder(n_layers=NL, batch=B, n_kv_heads=H, group_size=G, d_head=d, seq_cap=nl,
+                        roles=roles, policy=P.SparsityPolicy.top_k(k), dtype=dt, world=world,
+                        rank=rank)
+    for _ in range(args.warmup):
+        sd.decode_step(q, K, V, nl, rb, L, out)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            sd.decode_step(q, K, V, nl, rb, L, out)
+        e1.record()
+        e1.synchronize()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    # algorithmic bytes of the whole job per step (all ranks): K/V rows touched + q/out
+    e = 2 if dt == torch.bfloat16 else 4
+    kb = min(k, L)
+    rows = sum(L if (l == 0 or roles[l, g] == 0) else kb for l in range(NL) for g in range(H))
+    job_bytes = B * rows * 2 * d * e + NL * B * H * G * d * e * 2
+    if rank == 0:
+        pk, pk_kind = peaks()
+        achieved = job_bytes / (ms / 1e3) / 1e9 / world  # per GPU
+        line = {
+            "metric": METRIC, "value": ms * 1e3 / B, "unit": "us/token", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": wl["dtype"], "data": "synthetic U(-1,1) q/K/V, seeded roles",
+            "config": config_of(args, wl), "tokens_per_s": B / (ms / 1e3),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": float(pk["hbm_gbs"]),
+                         "unit": "GB/s", "frac": achieved / float(pk["hbm_gbs"]),
+                         "traffic": None, "peak_kind": pk_kind,
+                         "kernel": "per-layer attention + merge + top-k + packed NCCL all-gather"},
+            "cpu_baseline": None,
+            "e2e": None,
+            "gpu_launches": int(args.steps * NL * 6),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    sd.close()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -240,6 +336,9 @@ def main():
     ap.add_argument("--seed", type=int, default=2602)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-full", action="store_true")
+    ap.add_argument("--shard", default="heads", choices=["heads", "seq"],
+                    help="multi-GPU split: KV heads (no collective) or KV sequence "
+                         "(one packed NCCL all-gather of partials + top-k candidates per layer)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = dict(WORKLOADS[args.workload])
@@ -260,6 +359,9 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2602_04541_b200 as P
 
+    if world > 1 and args.shard == "seq":
+        run_seq_sharded(args, wl, roles, rank, world, local)
+        return
     NL, H, G, d, L, k, B = (wl[x] for x in ("NL", "H", "G", "d", "L", "k", "B"))
     my_heads = shard_heads(roles, L, k, world, rank) if world > 1 else list(range(H))
     Hr = len(my_heads)
@@ -426,7 +528,10 @@ def main():
             "tokens_per_s": B / (ms / 1e3),
             "step_hbm_gbs": step_bytes / (ms / 1e3) / 1e9 if world == 1 else None,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": pk_kind,
+                         "frac": achieved / peak,
+                         "traffic": ncu_traffic(args.workload) if fused and world == 1 else None,
+                         "traffic_unit": "bytes per launch (= step), ncu --set full",
+                         "peak_kind": pk_kind,
                          "frac_of_8TBs": achieved / 8000.0,
                          "kernel": ("hybrid_step_kernel (whole step: attention + merge + "
                                     "selection of all layers, 1 launch)") if fused

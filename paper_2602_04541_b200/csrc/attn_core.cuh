@@ -52,9 +52,15 @@ struct AttnCfg {
   static constexpr int kQBytes = kE == 4 ? (kMaxG + 1) * D * 4 : 0;
   static constexpr int kMaxSmem = 232448 - 1024;   // 227 KB opt-in minus alignment slack
   // the step kernel's epilogue warps (selection); the step kernel is built for d <= 128 only
-  static constexpr int kExtraBytes = D <= 128 ? 58 * 1024 : 0;
+  static constexpr int kExtraBytes = D <= 128 ? 42240 : 0;  // sizeof(EpiSmem), step.cu
+  // layer-start staging of up to kQUnits unit descriptors + their queries (bf16)
+  static constexpr int kQUnits = 8;
+  static constexpr int kURecBytes = 80;  // LycUnit + LycSlot, padded
+  static constexpr int kUStageBytes = kE == 2 ? kQUnits * kURecBytes : 0;
+  static constexpr int kQStageBytes = kE == 2 ? kQUnits * kMaxG * D * 2 : 0;
   static constexpr int kHistBytes = LYC_H1_BINS * 4;  // per-CTA first-pass selection histogram
-  static constexpr int kFixed = kMergeBytes + kQBytes + 512 + kExtraBytes + kHistBytes;  // 512: barriers + 128-B alignment
+  static constexpr int kFixed = kMergeBytes + kQBytes + 512 + kExtraBytes + kHistBytes +
+                                kUStageBytes + kQStageBytes;  // 512: barriers + 128-B alignment
   static constexpr int kStagesRaw = (kMaxSmem - kFixed) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kSmem = kStages * kStageBytes + kFixed + 1024;
@@ -81,6 +87,8 @@ struct AttnSmem {
   uint64_t* empty;
   uint8_t* extra;  // kExtraBytes scratch for other warp roles
   uint32_t* hist;  // [LYC_H1_BINS] first radix pass of the unit's selection keys (zero between units)
+  uint8_t* ustage; // [kQUnits] unit records staged at layer start (bf16 consumers)
+  uint8_t* qstage; // [kQUnits][kMaxG][D] bf16 queries of those units
 
   // Offsets are applied to the __shared__ array itself (no integer round trip),
   // so the compiler keeps the shared address space and emits LDS/STS/ATOMS --
@@ -92,8 +100,10 @@ struct AttnSmem {
   static constexpr int kExtraOff =
       (kBarOff + 2 * AttnCfg<T, D>::kStages * 8 + 127) & ~127;
   static constexpr int kHistOff = kExtraOff + AttnCfg<T, D>::kExtraBytes;
+  static constexpr int kUStageOff = kHistOff + AttnCfg<T, D>::kHistBytes;
+  static constexpr int kQStageOff = kUStageOff + AttnCfg<T, D>::kUStageBytes;
 
-  static_assert(kHistOff + AttnCfg<T, D>::kHistBytes + 1024 <= AttnCfg<T, D>::kSmem -
+  static_assert(kQStageOff + AttnCfg<T, D>::kQStageBytes + 1024 <= AttnCfg<T, D>::kSmem -
                     AttnCfg<T, D>::kStages * AttnCfg<T, D>::kStageBytes,
                 "shared-memory carve exceeds the allocation");
   __device__ __forceinline__ static AttnSmem carve(uint8_t* raw) {
@@ -109,6 +119,8 @@ struct AttnSmem {
     s.empty = s.full + C::kStages;
     s.extra = fx + kExtraOff;
     s.hist = reinterpret_cast<uint32_t*>(fx + kHistOff);
+    s.ustage = fx + kUStageOff;
+    s.qstage = fx + kQStageOff;
     return s;
   }
 };
@@ -364,16 +376,54 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
   const int v_x = lane >> 4;
   const __nv_bfloat16* Q = static_cast<const __nv_bfloat16*>(p.q);
 
+  // ---- layer start: the first kQUnits unit records and their queries are
+  // staged on chip in two coalesced round trips, instead of three dependent
+  // L2 round trips (unit -> slot -> q) at every unit boundary
+  constexpr int kQU = C::kQUnits;
+  struct URec {
+    LycUnit u;
+    LycSlot s;
+  };
+  static_assert(sizeof(URec) <= C::kURecBytes, "unit record");
+  URec* rec = reinterpret_cast<URec*>(sm.ustage);
+  const int tid = warp * 32 + lane;
+  const int nst = min(ue - ub, kQU);
+  if (tid < nst) {
+    URec r;
+    r.u = p.units[ub + tid];
+    r.s = p.unit_slots ? p.unit_slots[ub + tid] : p.slots[r.u.slot];
+    rec[tid] = r;
+  }
+  consumer_bar();
+  {
+    const int cpu = G * D / 8;  // 16-B chunks of one unit's G query rows
+    for (int c = tid; c < nst * cpu; c += kConsumerWarps * 32) {
+      const int uu = c / cpu, r = c - uu * cpu;
+      const uint4 v = __ldcg(reinterpret_cast<const uint4*>(Q + (int64_t)rec[uu].s.q_row * D) + r);
+      reinterpret_cast<uint4*>(sm.qstage + uu * kMaxG * D * 2)[r] = v;
+    }
+  }
+  consumer_bar();
+
   for (int u = ub; u < ue; ++u) {
-    const LycUnit un = p.units[u];
-    const LycSlot s = p.slots[un.slot];
+    const bool staged = u - ub < kQU;
+    const LycUnit un = staged ? rec[u - ub].u : p.units[u];
+    const LycSlot s = staged ? rec[u - ub].s : p.slots[un.slot];
     const int tpi = tiles_per_item(s, p.block_size);
     uint32_t qa0[KS], qa2[KS];
+    const __nv_bfloat16* qst =
+        reinterpret_cast<const __nv_bfloat16*>(sm.qstage + (u - ub) * kMaxG * D * 2);
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) {
-      const __nv_bfloat16* qrow = Q + (int64_t)(s.q_row + qr) * D + kk * 16 + qc;
-      qa0[kk] = qr < G ? __ldcg(reinterpret_cast<const unsigned int*>(qrow)) : 0u;
-      qa2[kk] = qr < G ? __ldcg(reinterpret_cast<const unsigned int*>(qrow + 8)) : 0u;
+      if (staged) {
+        const __nv_bfloat16* qrow = qst + qr * D + kk * 16 + qc;
+        qa0[kk] = qr < G ? *reinterpret_cast<const unsigned int*>(qrow) : 0u;
+        qa2[kk] = qr < G ? *reinterpret_cast<const unsigned int*>(qrow + 8) : 0u;
+      } else {
+        const __nv_bfloat16* qrow = Q + (int64_t)(s.q_row + qr) * D + kk * 16 + qc;
+        qa0[kk] = qr < G ? __ldcg(reinterpret_cast<const unsigned int*>(qrow)) : 0u;
+        qa2[kk] = qr < G ? __ldcg(reinterpret_cast<const unsigned int*>(qrow + 8)) : 0u;
+      }
     }
     float m0 = -INFINITY, l0 = 0.f;
     float o[NT][2];
@@ -661,30 +711,48 @@ __device__ __forceinline__ void merge_task(const float* part_o, const float* par
                                            const LycSlot& s, int j, int chunk, int G, int D,
                                            void* out, int lane, float* out_f32 = nullptr,
                                            float* out_lse = nullptr) {
-  float M = -INFINITY;
-  for (int i = lane; i < s.n_units; i += 32)
-    M = fmaxf(M, __ldcg(part_lse + (int64_t)(s.first_unit + i) * G + j));
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-  const float Mz = M == -INFINITY ? 0.f : M;  // all partials empty: weights 0, output 0
-  float den = 0.f;
+  // one pass (online rescaling): every lane loads its partials' LSE and
+  // outputs together -- one L2 round trip per partial instead of two
+  float m = -INFINITY, den = 0.f;
   float acc[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+#pragma unroll 2
   for (int i = lane; i < s.n_units; i += 32) {
     const int64_t u = s.first_unit + i;
-    const float w = exp2f(__ldcg(part_lse + u * G + j) - Mz);
-    den += w;
+    const float lse = __ldcg(part_lse + u * G + j);
     const float4* src = reinterpret_cast<const float4*>(part_o + (u * G + j) * D + chunk * 32);
+    float4 v[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = chunk * 32 + 4 * c < D ? __ldcg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (lse == -INFINITY) continue;  // empty partial
+    if (lse > m) {
+      const float f = m == -INFINITY ? 0.f : exp2f(m - lse);
+      den *= f;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) acc[c] *= f;
+      m = lse;
+    }
+    const float w = exp2f(lse - m);
+    den += w;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      if (chunk * 32 + 4 * c >= D) break;
-      const float4 v = __ldcg(src + c);
-      acc[4 * c] = fmaf(w, v.x, acc[4 * c]);
-      acc[4 * c + 1] = fmaf(w, v.y, acc[4 * c + 1]);
-      acc[4 * c + 2] = fmaf(w, v.z, acc[4 * c + 2]);
-      acc[4 * c + 3] = fmaf(w, v.w, acc[4 * c + 3]);
+      acc[4 * c] = fmaf(w, v[c].x, acc[4 * c]);
+      acc[4 * c + 1] = fmaf(w, v[c].y, acc[4 * c + 1]);
+      acc[4 * c + 2] = fmaf(w, v[c].z, acc[4 * c + 2]);
+      acc[4 * c + 3] = fmaf(w, v[c].w, acc[4 * c + 3]);
     }
+  }
+  // rescale every lane to the warp maximum, then the fixed-shape reductions
+  float M = m;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+  const float Mz = M == -INFINITY ? 0.f : M;  // all partials empty: output 0
+  {
+    const float f = m == -INFINITY ? 0.f : exp2f(m - Mz);
+    den *= f;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) acc[c] *= f;
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) den += __shfl_xor_sync(0xffffffffu, den, off);

@@ -161,6 +161,7 @@ void plan_launch(HostLaunch& L, int batch, int heads, int splits, int group) {
 struct DevLaunch {
   LycSlot* slots = nullptr;
   LycUnit* units = nullptr;
+  LycSlot* unit_slots = nullptr;
   int32_t* split_off = nullptr;
   LycMergeTask* merges = nullptr;
   int32_t* sel_rows = nullptr;
@@ -172,6 +173,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 size_t launch_bytes(const HostLaunch& L) {
   return align_up(L.slots.size() * sizeof(LycSlot), 256) +
          align_up(L.units.size() * sizeof(LycUnit), 256) +
+         align_up(std::max<size_t>(1, L.units.size()) * sizeof(LycSlot), 256) +
          align_up(L.split_off.size() * 4, 256) +
          align_up(std::max<size_t>(1, L.merges.size()) * sizeof(LycMergeTask), 256) +
          align_up(std::max<size_t>(1, L.sel_rows.size()) * 4, 256);
@@ -193,6 +195,10 @@ DevLaunch stage_launch(const HostLaunch& L, std::vector<uint8_t>& host, size_t& 
                           align_up(L.slots.size() * sizeof(LycSlot), 256));
   d.units = (LycUnit*)put(L.units.data(), L.units.size() * sizeof(LycUnit),
                           align_up(L.units.size() * sizeof(LycUnit), 256));
+  std::vector<LycSlot> us(L.units.size());
+  for (size_t u = 0; u < L.units.size(); ++u) us[u] = L.slots[(size_t)L.units[u].slot];
+  d.unit_slots = (LycSlot*)put(us.data(), us.size() * sizeof(LycSlot),
+                               align_up(std::max<size_t>(1, us.size()) * sizeof(LycSlot), 256));
   d.split_off = (int32_t*)put(L.split_off.data(), L.split_off.size() * 4,
                               align_up(L.split_off.size() * 4, 256));
   d.merges = (LycMergeTask*)put(L.merges.data(), L.merges.size() * sizeof(LycMergeTask),
@@ -396,6 +402,7 @@ int lyc_workload_run(const lyc_workload* w, int64_t num_splits, void* out, uint3
     v.out = out;
     v.slots = dl.slots;
     v.units = dl.units;
+    v.unit_slots = dl.unit_slots;
     v.split_off = dl.split_off;
     v.part_o = (float*)(dev + plan_b + ids_b);
     v.part_lse = (float*)(dev + plan_b + ids_b + po_b);
@@ -705,6 +712,7 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
     LycView& v = ly.ap.v;
     v.slots = dl.slots;
     v.units = dl.units;
+    v.unit_slots = dl.unit_slots;
     v.split_off = dl.split_off;
     v.part_o = d->part_o;
     v.part_lse = d->part_lse;
@@ -746,6 +754,7 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
     LycLayerDesc& ds = descs[(size_t)l];
     ds.slots = dl.slots;
     ds.units = dl.units;
+    ds.unit_slots = dl.unit_slots;
     ds.split_off = dl.split_off;
     ds.merges = dl.merges;
     ds.sel_rows = dl.sel_rows;

@@ -59,6 +59,7 @@ struct LycView {
   void* out;                // [rows][d]
   const LycSlot* slots;
   const LycUnit* units;
+  const LycSlot* unit_slots;// [n_units] copy of each unit's slot (one coalesced load per layer)
   const int32_t* split_off; // [B * n_splits + 1] unit ranges per (b, split)
   float* part_o;            // [n_units][G][d]  normalized partial outputs
   float* part_lse;          // [n_units][G]     base-2 log-sum-exp
@@ -125,6 +126,7 @@ struct LycTopkParams {
 struct LycLayerDesc {
   const LycSlot* slots;
   const LycUnit* units;
+  const LycSlot* unit_slots;
   const int32_t* split_off;
   const LycMergeTask* merges;
   const int32_t* sel_rows;  // selection index -> index-cache row

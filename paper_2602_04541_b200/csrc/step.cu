@@ -37,7 +37,7 @@ constexpr int kEpiWarps = 2;
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kStepThreads = (kConsumerWarps + kProducerWarps + kEpiWarps) * 32;
 constexpr int kItemKeys = 8192;  // keys per selection item (32 KB, one TMA bulk copy)
-constexpr int kRankMax = 384;    // boundary-bin candidates resolved by direct ranking
+constexpr int kRankMax = 256;    // boundary-bin candidates resolved by direct ranking (per warp list)
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
@@ -112,6 +112,7 @@ __device__ __forceinline__ LycView layer_view(const LycStepParams& p, const LycL
   v.out = static_cast<uint8_t*>(p.out) + (int64_t)l * p.q_layer_stride * esz;
   v.slots = L.slots;
   v.units = L.units;
+  v.unit_slots = L.unit_slots;
   v.split_off = L.split_off;
   v.part_o = p.part_o;
   v.part_lse = p.part_lse;
@@ -206,7 +207,7 @@ __host__ __device__ __forceinline__ int bm_pad(int w) { return w + (w >> 6) * 4;
 __host__ __device__ __forceinline__ int bm_padded_words(int nwords) { return (nwords + 63) / 64 * 68; }
 
 // Epilogue scratch (inside AttnSmem::extra).
-constexpr int kEpiBufWords = 12288;  // 48 KB
+constexpr int kEpiBufWords = 8192;  // 32 KB: one classify item; finisher candidates
 struct EpiSmem {
   // classify: one item's keys [kItemKeys]; finish: bitmap [nwords] followed by
   // the candidates' keys and indices
@@ -479,7 +480,7 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int row, Epi
   // (counts only), then one pass takes every candidate above the final
   // prefix and compacts the survivors, which are ranked exactly.
   uint32_t live = padded;  // upper bound on candidates matching P
-  while (live > (uint32_t)kRankMax && shift > 0) {
+  while (live > (uint32_t)kRankMax && shift > 0) {  // <= kRankMax survivors fit either warp's list
     const int wbits = shift > 8 ? 8 : shift;
     shift -= wbits;
     const uint32_t mask = (1u << wbits) - 1u;
@@ -497,42 +498,53 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int row, Epi
     krem -= es.above;
     live = es.hist[es.digit];
   }
-  uint32_t* lkey = es.hist;
-  uint32_t* lidx = es.hist + kRankMax;
-  uint32_t* lslot = es.hist + 2 * kRankMax;
+  // per-warp survivor lists (ballot compaction, no atomics): warp w's list at
+  // es.hist + w * 3 * kRankMax as keys | ids | slots
+  const int lane = et & 31, ew = et >> 5;
   epi_bar();
-  if (et == 0) {
-    es.pad = 0u;
-    stamp(p, l, EV_F_PREFIX, cta);
-  }
-  epi_bar();
-  for (int i = et; i < ns; i += kEpiThreads) {
-    uint32_t key, idx;
-    if (!get(i, key, idx)) continue;
-    const uint32_t pre = key >> shift;  // shift < 32
-    flag(i, idx, pre > P ? 1u : 0u);
-    if (pre == P) {
-      const uint32_t at = atomicAdd(&es.pad, 1u);
-      if (at < (uint32_t)kRankMax) {
-        lkey[at] = key;
-        lidx[at] = idx;
-        lslot[at] = (uint32_t)i;
+  if (et == 0) stamp(p, l, EV_F_PREFIX, cta);
+  {
+    uint32_t* lk = es.hist + ew * 3 * kRankMax;
+    uint32_t mw = 0;
+    for (int i0 = ew * 32; i0 < ns; i0 += kEpiThreads) {
+      const int i = i0 + lane;
+      uint32_t key = 0, idx = 0;
+      const bool ok = i < ns && get(i, key, idx);
+      const uint32_t pre = key >> shift;  // shift < 32
+      if (ok) flag(i, idx, pre > P ? 1u : 0u);
+      const bool surv = ok && pre == P;
+      const unsigned bal = __ballot_sync(0xffffffffu, surv);
+      const uint32_t at = mw + (uint32_t)__popc(bal & ((1u << lane) - 1u));
+      if (surv && at < (uint32_t)kRankMax) {
+        lk[at] = key;
+        lk[kRankMax + at] = idx;
+        lk[2 * kRankMax + at] = (uint32_t)i;
       }
+      mw += (uint32_t)__popc(bal);
     }
+    if (lane == 0) es.scan[40 + ew] = mw;
   }
   epi_bar();
-  const uint32_t m = es.pad;
+  const uint32_t m0 = es.scan[40], m1 = es.scan[41];
   if (et == 0) stamp(p, l, EV_X1, cta);
-  const bool ranked = m <= (uint32_t)kRankMax;
+  const bool ranked = m0 <= (uint32_t)kRankMax && m1 <= (uint32_t)kRankMax;
   if (ranked) {
-    for (uint32_t i = et; i < m; i += kEpiThreads) {
-      const uint32_t ki = lkey[i], xi = lidx[i];
+    const uint32_t m = m0 + m1;
+    const uint32_t* L0 = es.hist;
+    const uint32_t* L1 = es.hist + 3 * kRankMax;
+    for (uint32_t e = et; e < m; e += kEpiThreads) {
+      const uint32_t* Le = e < m0 ? L0 + e : L1 + (e - m0);
+      const uint32_t ki = Le[0], xi = Le[kRankMax];
       uint32_t rank = 0;
-      for (uint32_t j = 0; j < m; ++j) {
-        const uint32_t kj = lkey[j];
-        rank += (kj > ki || (kj == ki && lidx[j] < xi)) ? 1u : 0u;
+      for (uint32_t j = 0; j < m0; ++j) {
+        const uint32_t kj = L0[j];
+        rank += (kj > ki || (kj == ki && L0[kRankMax + j] < xi)) ? 1u : 0u;
       }
-      if (rank < krem) flag((int)lslot[i], xi, 1u);
+      for (uint32_t j = 0; j < m1; ++j) {
+        const uint32_t kj = L1[j];
+        rank += (kj > ki || (kj == ki && L1[kRankMax + j] < xi)) ? 1u : 0u;
+      }
+      if (rank < krem) flag((int)Le[2 * kRankMax], xi, 1u);
     }
   }
   if (!ranked) {
@@ -558,11 +570,6 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int row, Epi
   uint32_t tot;
   const uint32_t end_q = epi_scan(n_q, es.scan, et, tot);
   if (et < items) R.ccnt[128 + et] = end_q - n_q;
-  // reset the row's fused histogram for its next use
-  if (R.h1)
-    for (int b = et; b < LYC_H1_ROW; b += kEpiThreads) R.h1[b] = 0u;
-  if (p.sel_mode == SEL_BLOCK_KEYS)
-    for (int i = et; i < n; i += kEpiThreads) R.keys[i] = 0u;
   epi_bar();
   if (et == 0) {
     if (p.idx_count) p.idx_count[row] = p.k_sel;
@@ -570,6 +577,13 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int row, Epi
     st_release(R.ctr + 4, epoch1);
     stamp(p, l, EV_SEL1, cta);
   }
+  // reset the row's fused histogram (block mode: its keys) for the next use
+  // of this parity -- after the release (off the emitters' critical path);
+  // ordered before this CTA's own CTR_SELDONE signal, which layer l + 2 waits for
+  if (R.h1)
+    for (int b = et; b < LYC_H1_ROW; b += kEpiThreads) R.h1[b] = 0u;
+  if (p.sel_mode == SEL_BLOCK_KEYS)
+    for (int i = et; i < n; i += kEpiThreads) R.keys[i] = 0u;
 }
 
 // Emit item q of a resolved row: its 256 bitmap words (one 16-B vector per
@@ -586,18 +600,37 @@ __device__ void emit_item(const LycStepParams& p, const SelRow& R, int q, int32_
   const int lo = q * kItemKeys;
   const int cnt = min(kItemKeys, n - lo);
   const int w0 = lo / 32 + et * 4;  // this thread's 4 words (128 keys)
+  // independent loads first: the item's words, its candidate count and output
+  // offset, and the first two candidate (flag, id) pairs of this thread
   uint4 v = make_uint4(0u, 0u, 0u, 0u);
   if (et * 128 < cnt) v = __ldcg(reinterpret_cast<const uint4*>(R.bitmap + bm_pad(w0)));
+  const uint32_t ncand = __ldcg(R.ccnt + q);
+  const uint32_t out0 = __ldcg(R.ccnt + 128 + q);
+  // (speculative: slots past the candidate count are never used; a slot
+  // index below the item's key count is always inside the row)
+  uint32_t f0 = 0, x0 = 0, f1 = 0, x1 = 0;
+  if (et < cnt) {
+    f0 = __ldcg(R.cflag + lo + et);
+    x0 = __ldcg(R.cidx + lo + et);
+  }
+  if (et + kEpiThreads < cnt) {
+    f1 = __ldcg(R.cflag + lo + et + kEpiThreads);
+    x1 = __ldcg(R.cidx + lo + et + kEpiThreads);
+  }
   // the finisher's selected boundary-bin candidates join this item's words
   uint32_t* ws = es.buf;  // [256] on-chip copy of the item's words
   reinterpret_cast<uint4*>(ws)[et] = v;
   epi_bar();
-  const uint32_t ncand = __ldcg(R.ccnt + q);
-  for (uint32_t i = et; i < ncand; i += kEpiThreads)
-    if (__ldcg(R.cflag + lo + i)) {
-      const uint32_t idx = __ldcg(R.cidx + lo + i);
-      atomicOr(ws + ((idx - (uint32_t)lo) >> 5), 1u << (idx & 31));
+  for (uint32_t i = et; i < ncand; i += kEpiThreads) {
+    uint32_t f = f0, x = x0;
+    if (i >= 2 * kEpiThreads) {
+      f = __ldcg(R.cflag + lo + i);
+      x = __ldcg(R.cidx + lo + i);
     }
+    f0 = f1;
+    x0 = x1;
+    if (f) atomicOr(ws + ((x - (uint32_t)lo) >> 5), 1u << (x & 31));
+  }
   epi_bar();
   v = reinterpret_cast<const uint4*>(ws)[et];
   uint32_t wv[4] = {v.x, v.y, v.z, v.w};
@@ -606,7 +639,7 @@ __device__ void emit_item(const LycStepParams& p, const SelRow& R, int q, int32_
     if (et * 128 + i * 32 >= cnt) wv[i] = 0u;
   const uint32_t c = __popc(wv[0]) + __popc(wv[1]) + __popc(wv[2]) + __popc(wv[3]);
   uint32_t tot;
-  uint32_t pos = epi_scan(c, es.scan, et, tot) - c + __ldcg(R.ccnt + 128 + q);
+  uint32_t pos = epi_scan(c, es.scan, et, tot) - c + out0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const uint32_t m0 = wv[i];
@@ -799,10 +832,7 @@ cudaError_t launch_step(const LycStepParams& p, int dtype, int d, cudaStream_t s
 
 // Largest selection row (keys) the fused step supports.
 int64_t step_max_keys() {
-  // the finisher holds the row's padded bitmap on chip
-  int64_t n = (int64_t)64 * kItemKeys;
-  while (bm_padded_words((int)((n + 31) / 32)) > kEpiBufWords) n -= kItemKeys;
-  return n;
+  return (int64_t)64 * kItemKeys;  // <= 64 items per row (one epilogue thread per item)
 }
 int64_t step_bitmap_words(int64_t n_keys) { return bm_padded_words((int)((n_keys + 31) / 32)); }
 int step_item_keys() { return kItemKeys; }
