@@ -51,9 +51,7 @@ __global__ void __launch_bounds__(128) split_merge_kernel(const __grid_constant_
   const int task = gw / p.chunks, chunk = gw - task * p.chunks;
   if (task >= p.n_tasks) return;
   const LycMergeTask tk = p.tasks[task];
-  const LycSlot s = p.slots[tk.slot];
-  merge_task<T>(p.part_o, p.part_lse, s, tk.j, chunk, p.group, p.d, p.out, lane, p.out_f32,
-                p.out_lse);
+  merge_task<T>(p.part_o, p.part_lse, tk, chunk, p.group, p.d, p.out, lane, p.out_f32, p.out_lse);
 }
 
 // ---------------------------------------------------------------- launchers

@@ -52,7 +52,7 @@ struct AttnCfg {
   static constexpr int kQBytes = kE == 4 ? (kMaxG + 1) * D * 4 : 0;
   static constexpr int kMaxSmem = 232448 - 1024;   // 227 KB opt-in minus alignment slack
   // the step kernel's epilogue warps (selection); the step kernel is built for d <= 128 only
-  static constexpr int kExtraBytes = D <= 128 ? 42240 : 0;  // sizeof(EpiSmem), step.cu
+  static constexpr int kExtraBytes = D <= 128 ? 43008 : 0;  // >= sizeof(EpiSmem), step.cu
   // layer-start staging of up to kQUnits unit descriptors + their queries (bf16)
   static constexpr int kQUnits = 8;
   static constexpr int kURecBytes = 80;  // LycUnit + LycSlot, padded
@@ -708,9 +708,10 @@ __device__ __forceinline__ void consume_units(const LycView& p, const AttnSmem<T
 // fixed-shape butterfly reduces across lanes -> bitwise deterministic.
 template <typename T>
 __device__ __forceinline__ void merge_task(const float* part_o, const float* part_lse,
-                                           const LycSlot& s, int j, int chunk, int G, int D,
+                                           const LycMergeTask& s, int chunk, int G, int D,
                                            void* out, int lane, float* out_f32 = nullptr,
                                            float* out_lse = nullptr) {
+  const int j = s.j;
   // one pass (online rescaling): every lane loads its partials' LSE and
   // outputs together -- one L2 round trip per partial instead of two
   float m = -INFINITY, den = 0.f;

@@ -154,7 +154,9 @@ void plan_launch(HostLaunch& L, int batch, int heads, int splits, int group) {
   L.split_off[(size_t)batch * splits] = (int32_t)L.units.size();
   for (size_t i = 0; i < L.slots.size(); ++i)
     if (L.slots[i].n_units > 1)
-      for (int j = 0; j < group; ++j) L.merges.push_back(LycMergeTask{(int32_t)i, j});
+      for (int j = 0; j < group; ++j)
+        L.merges.push_back(LycMergeTask{(int32_t)i, j, L.slots[i].first_unit, L.slots[i].n_units,
+                                        L.slots[i].q_row, 0});
 }
 
 // Device copy of one HostLaunch; returns the device pointers inside `blob`.
@@ -498,6 +500,7 @@ struct lyc_decoder {
   int64_t bitmap_stride = 0;
   uint32_t* sel_cand = nullptr;
   uint32_t* sel_ccnt = nullptr;
+  uint32_t* sel_csub = nullptr;
   uint32_t* sel_rowctr = nullptr;
   int stages = 0;               // attention ring stages in use (0 = all; env LYC_STAGES)
   uint32_t* ctr = nullptr;      // [NL][CTR_PER_LAYER] + 2
@@ -613,7 +616,9 @@ void plan_step_launch(HostLaunch& L, int batch, int heads, int splits, int group
   }
   for (size_t i = 0; i < L.slots.size(); ++i)
     if (L.slots[i].n_units > 1)
-      for (int j = 0; j < group; ++j) L.merges.push_back(LycMergeTask{(int32_t)i, j});
+      for (int j = 0; j < group; ++j)
+        L.merges.push_back(LycMergeTask{(int32_t)i, j, L.slots[i].first_unit, L.slots[i].n_units,
+                                        L.slots[i].q_row, 0});
 }
 
 void free_dev(void* p) {
@@ -849,6 +854,7 @@ void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, i
   p.bitmap_stride = d->bitmap_stride;
   p.sel_cand = d->sel_cand;
   p.sel_ccnt = d->sel_ccnt;
+  p.sel_csub = d->sel_csub;
   p.sel_rowctr = d->sel_rowctr;
   p.ctr = d->ctr;
   p.idx = d->idx;
@@ -950,7 +956,9 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
         d->bitmap_stride = (lyc::step_bitmap_words(d->sel_stride) + 3) & ~(int64_t)3;
         cuda_check(cudaMalloc(&d->sel_bitmap, 2 * rows * d->bitmap_stride * 4), "cudaMalloc bitmap");
         cuda_check(cudaMalloc(&d->sel_cand, 2 * rows * 3 * d->sel_stride * 4), "cudaMalloc cand");
-        cuda_check(cudaMalloc(&d->sel_ccnt, 2 * rows * 192 * 4), "cudaMalloc ccnt");
+        cuda_check(cudaMalloc(&d->sel_ccnt, 2 * rows * 256 * 4), "cudaMalloc ccnt");
+        cuda_check(cudaMalloc(&d->sel_csub, 2 * rows * 256 * 4), "cudaMalloc csub");
+        cuda_check(cudaMemset(d->sel_csub, 0, 2 * rows * 256 * 4), "memset");
         cuda_check(cudaMalloc(&d->sel_rowctr, (size_t)d->NL * rows * 16 * 4), "cudaMalloc rowctr");
         cuda_check(cudaMemset(d->sel_rowctr, 0, (size_t)d->NL * rows * 16 * 4), "memset");
       }
@@ -978,6 +986,7 @@ int lyc_decoder_destroy(lyc_decoder* d) {
   free_dev(d->sel_bitmap);
   free_dev(d->sel_cand);
   free_dev(d->sel_ccnt);
+  free_dev(d->sel_csub);
   free_dev(d->sel_rowctr);
   free_dev(d->ctr);
   free_dev(d->trace);

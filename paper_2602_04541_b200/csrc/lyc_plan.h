@@ -92,6 +92,10 @@ struct LycAttnParams {
 struct LycMergeTask {       // one (slot, q head j) pair needing a split-KV merge
   int32_t slot;
   int32_t j;
+  int32_t first_unit;       // the slot's partials (copied from LycSlot: one load per task)
+  int32_t n_units;
+  int32_t q_row;
+  int32_t pad;
 };
 
 struct LycMergeParams {
@@ -167,7 +171,8 @@ struct LycStepParams {
   uint32_t* sel_bitmap;      // [2 parity][max_sel][bitmap_stride] selected-key bitmaps
   int64_t bitmap_stride;
   uint32_t* sel_cand;        // [2 parity][max_sel][3][sel_stride] boundary-bin candidates: keys, indices, selected flags
-  uint32_t* sel_ccnt;        // [2 parity][max_sel][192] per item: candidates, definite keys, output offset
+  uint32_t* sel_ccnt;        // [2 parity][max_sel][256] per item: candidates [0,64), definite keys [64,128); row prefix [192,195)
+  uint32_t* sel_csub;        // [2 parity][max_sel][256] boundary-bin sub-histograms (zero between uses)
   uint32_t* sel_rowctr;      // [n_layers][max_sel][16] finished items per row (monotonic)
   uint32_t* ctr;             // LYC_CTR counters: [n_layers][CTR_PER_LAYER], then epoch, exits
   int32_t* idx;              // index cache [B*H][idx_stride]

@@ -45,25 +45,40 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   return v;
 }
 
-// Grid-level wait on a monotonic counter; traps after ~20 s (a lost signal is
-// a bug -- fail the launch instead of hanging the GPU).
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid-level wait on a monotonic counter: relaxed polls (no L1 invalidation
+// per poll), one acquire fence once the target is reached.  Traps after ~20 s
+// (a lost signal is a bug -- fail the launch instead of hanging the GPU).
 __device__ __forceinline__ void spin_until(const uint32_t* ctr, uint32_t target) {
-  if ((int)(ld_acquire(ctr) - target) >= 0) return;
-  const long long t0 = clock64();
-  while ((int)(ld_acquire(ctr) - target) < 0) {
-    __nanosleep(128);
-    if (clock64() - t0 > 40000000000LL) __trap();
+  if ((int)(ld_relaxed(ctr) - target) < 0) {
+    const long long t0 = clock64();
+    while ((int)(ld_relaxed(ctr) - target) < 0) {
+      __nanosleep(64);
+      if (clock64() - t0 > 40000000000LL) __trap();
+    }
   }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
 __device__ __forceinline__ void group_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// One thread of a warp group signals after the group's global writes.
+// One thread of a warp group signals after the group's global writes (the
+// group synchronised with bar.sync first; the release is cumulative).
 __device__ __forceinline__ void signal(uint32_t* ctr) {
-  __threadfence();
-  atomicAdd(ctr, 1u);
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+}
+
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* ctr, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(ctr), "r"(v) : "memory");
+  return old;
 }
 
 __device__ __forceinline__ void epi_bar() { group_bar(2, kEpiThreads); }
@@ -216,7 +231,8 @@ struct EpiSmem {
   uint32_t scan[64];
   uint32_t seg[72];          // finish: smem start of each item's candidate segment
   uint32_t cnt[72];          // finish: candidates of each item
-  uint32_t selc[72];         // finish: selected candidates of each item
+  uint32_t selc[72];         // resolve: selected candidates of each item
+  uint32_t defc[72];         // resolve: definite keys of each item
   uint64_t bar;
   uint32_t digit, above, last, pad;
   uint32_t pfx, pabove, pshift, pad2;  // the row's boundary prefix (classify -> finish)
@@ -258,10 +274,11 @@ struct SelRow {
   uint32_t* bitmap;   // [n_words]
   uint32_t* ckey;     // [n] candidate keys, item q's segment at q*kItemKeys
   uint32_t* cidx;     // [n] candidate indices
-  uint32_t* cflag;    // [n] candidate selected (1) or not (0), written by the finisher
+  uint32_t* cflag;    // [n] (unused)
+  uint32_t* csub;     // [256] row sub-histogram of the boundary-bin candidates
   uint32_t* ccnt;     // [n_items] candidates per item; +64: definite keys per item;
                       // +128: output offset of each item
-  uint32_t* ctr;      // per-row words: [0] items classified, [4] row resolved (epoch)
+  uint32_t* ctr;      // per-row words: [0] items classified, [8] items holding their copies
 };
 
 __device__ __forceinline__ SelRow sel_row(const LycStepParams& p, int l, int r) {
@@ -273,7 +290,8 @@ __device__ __forceinline__ SelRow sel_row(const LycStepParams& p, int l, int r) 
   s.ckey = p.sel_cand + pr * 3 * p.sel_stride;
   s.cidx = s.ckey + p.sel_stride;
   s.cflag = s.cidx + p.sel_stride;
-  s.ccnt = p.sel_ccnt + pr * 192;
+  s.csub = p.sel_csub + pr * 256;
+  s.ccnt = p.sel_ccnt + pr * 256;
   s.ctr = p.sel_rowctr + ((int64_t)l * p.max_sel + r) * 16;
   return s;
 }
@@ -304,15 +322,14 @@ __device__ __forceinline__ void row_prefix(const LycStepParams& p, const SelRow&
   epi_bar();
 }
 
-// Classify item q of one row: keys above the boundary prefix set bitmap bits,
-// keys inside it become candidates (index order).  Returns true to the whole
-// group if this was the row's last item (the caller then finishes the row).
-__device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, uint32_t epoch1,
-                              EpiSmem& es, uint32_t& bar_phase, int et, int l, int cta) {
+// Classify item q of one row: keys above the row's boundary prefix set bitmap
+// bits, keys inside it become candidates (index order) and are histogrammed by
+// their next 8 bits into the row's 256-bin sub-histogram (global, atomics).
+__device__ void classify_item(const LycStepParams& p, const SelRow& R, int q, EpiSmem& es,
+                              uint32_t& bar_phase, int et, int l, int cta) {
   const int n = p.n_keys;
   const int lo = q * kItemKeys;
   const int cnt = min(kItemKeys, n - lo);
-  const int items = (n + kItemKeys - 1) / kItemKeys;
   if (et == 0) {
     fence_proxy_async();
     const uint32_t bytes = (uint32_t)((cnt + 3) & ~3) * 4u;  // key rows are padded to 4
@@ -329,12 +346,10 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
   row_prefix(p, R, es, et);
   if (et == 0) stamp(p, l, EV_C_PREFIX, cta);
   const uint32_t P = es.digit;
+  const uint32_t above = es.above;
   const int shift = (int)es.last;
-  if (et == 0) {  // kept for finish_row (this CTA finishes the row if its item is the last)
-    es.pfx = P;
-    es.pabove = es.above;
-    es.pshift = (uint32_t)shift;
-  }
+  epi_bar();
+  for (int b = et; b < 256; b += kEpiThreads) es.hist[b] = 0u;  // item sub-histogram
   mbar_wait(&es.bar, bar_phase);
   bar_phase ^= 1u;
   if (et == 0) stamp(p, l, EV_C_KEYS, cta);
@@ -372,8 +387,10 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
       const int j = __ffs(m) - 1;
       m &= m - 1;
       const int i = k0 + w * 32 + j;
-      R.ckey[lo + pos] = es.buf[i];
+      const uint32_t key = es.buf[i];
+      R.ckey[lo + pos] = key;
       R.cidx[lo + pos] = (uint32_t)(lo + i);
+      atomicAdd(&es.hist[(key >> (shift - 8)) & 255u], 1u);
       ++pos;
     }
   }
@@ -382,11 +399,19 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
   for (int off = 16; off > 0; off >>= 1) ndef += __shfl_xor_sync(0xffffffffu, ndef, off);
   if ((et & 31) == 0) es.scan[32 + (et >> 5)] = ndef;
   epi_bar();
+  for (int b = et; b < 256; b += kEpiThreads) {
+    const uint32_t h = es.hist[b];
+    if (h) atomicAdd(R.csub + b, h);
+  }
   if (et == 0) {
     R.ccnt[q] = total;
     R.ccnt[64 + q] = es.scan[32] + es.scan[33];
+    // the row's boundary prefix (identical from every item) for the resolvers
+    R.ccnt[192] = P;
+    R.ccnt[193] = above;
+    R.ccnt[194] = (uint32_t)shift;
     // pad the segment to a multiple of 4 with sentinels (index ~0, key 0: never
-    // ranks above a real candidate) so the finisher can scan padded slots blindly
+    // ranks above a real candidate) so resolvers can scan padded slots blindly
     for (uint32_t i = total; i < ((total + 3u) & ~3u); ++i) {
       R.ckey[lo + i] = 0u;
       R.cidx[lo + i] = 0xFFFFFFFFu;
@@ -395,92 +420,113 @@ __device__ bool classify_item(const LycStepParams& p, const SelRow& R, int q, ui
   epi_bar();
   if (et == 0) {
     stamp(p, l, EV_C_DONE, cta);
-    __threadfence();
-    const uint32_t old = atomicAdd(R.ctr, 1u);
-    es.last = old == epoch1 * (uint32_t)items - 1u;
-    if (es.last) __threadfence();  // acquire the other items' writes
+    signal(R.ctr);  // release this item's writes
   }
-  epi_bar();
-  return es.last != 0;
 }
 
-// Resolve one row after its last item was classified.  One thread bulk-copies
-// every item's boundary-bin candidate segment (keys and indices, 16-B
-// aligned) into shared memory, all copies in flight at once; the krem best
-// candidates (greater key, or equal key and lower index: attention.hpp:115-119)
-// are OR-ed into the row's global bitmap and counted per item; the per-item
-// output offsets are published and the row is released to its items, which
-// emit their own ranges (emit_item).
-__device__ void finish_row(const LycStepParams& p, const SelRow& R, int row, EpiSmem& es,
-                           uint32_t& bar_phase, uint32_t epoch1, int et, int l, int cta) {
+// Resolve the row and emit item q's share of the index-cache row.  Every item
+// of the row resolves it redundantly (no hand-off to a finisher and back):
+// once all items are classified, bulk-load the boundary-bin candidates (about
+// k/4 keys) and the row's 256-bin sub-histogram; the sub-histogram narrows the
+// boundary by 8 more bits, one scan takes everything above it and compacts the
+// few survivors, which are ranked exactly (greater key, or equal key and lower
+// index: attention.hpp:115-119).  Per-item selected counts give this item's
+// output offset; its own words (definite keys + its selected candidates) are
+// emitted with branch-free predicated stores.
+__device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q, int row,
+                                  int32_t* out, EpiSmem& es, uint32_t& bar_phase,
+                                  uint32_t epoch1, int et, int l, int cta) {
   const int n = p.n_keys;
   const int items = (n + kItemKeys - 1) / kItemKeys;
-  // the boundary prefix this CTA computed while classifying the row's last item
-  uint32_t P = es.pfx;
-  int shift = (int)es.pshift;
-  uint32_t krem = (uint32_t)p.k_sel - es.pabove;
-  // candidate segments: item q's candidates land at smem [seg[q], seg[q] + cnt[q])
+  const int lo = q * kItemKeys;
+  const int cnt = min(kItemKeys, n - lo);
+  const int lane = et & 31, ew = et >> 5;
+  if (et == 0) spin_until(R.ctr, epoch1 * (uint32_t)items);  // every item classified
+  epi_bar();
+  if (et == 0) stamp(p, l, EV_F_SCAN, cta);
+  // round 1: the row prefix, counts, this item's definite words
+  uint32_t P = __ldcg(R.ccnt + 192);
+  int shift = (int)__ldcg(R.ccnt + 194);
+  uint32_t krem = (uint32_t)p.k_sel - __ldcg(R.ccnt + 193);
   const uint32_t c_mine = et < items ? __ldcg(R.ccnt + et) : 0u;
+  const uint32_t d_mine = et < items ? __ldcg(R.ccnt + 64 + et) : 0u;
+  const int w0 = lo / 32 + et * 4;  // this thread's 4 words (128 keys)
+  uint4 wv4 = make_uint4(0u, 0u, 0u, 0u);
+  if (et * 128 < cnt) wv4 = __ldcg(reinterpret_cast<const uint4*>(R.bitmap + bm_pad(w0)));
+  uint32_t* ws = es.hist + 1792;  // [256] this item's words on chip
+  reinterpret_cast<uint4*>(ws)[et] = wv4;
   const uint32_t c_pad = (c_mine + 3) & ~3u;
   uint32_t padded;
   const uint32_t incl = epi_scan(c_pad, es.scan, et, padded);
   if (et < items) {
     es.seg[et] = incl - c_pad;
     es.cnt[et] = c_mine;
+    es.defc[et] = d_mine;
   }
-  if (et < 72) es.selc[et] = 0u;
+  if (et < 64) es.selc[et] = 0u;
   const int cap = (kEpiBufWords / 2) & ~3;  // candidates that fit on chip
   const bool on_chip = (int)padded <= cap;
   uint32_t* skey = es.buf;
   uint32_t* sidx = es.buf + cap;
   epi_bar();
+  // round 2: candidates and the 256-bin sub-histogram, all copies in flight at once
   if (et == 0) {
-    stamp(p, l, EV_F_SCAN, cta);
-    if (on_chip && padded > 0) {
-      fence_proxy_async();
-      mbar_arrive_expect_tx(&es.bar, padded * 8u);
-      for (int q = 0; q < items; ++q) {
-        const uint32_t b = ((es.cnt[q] + 3) & ~3u) * 4u;
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&es.bar, 1024u + (on_chip ? padded * 8u : 0u));
+    bulk_g2s(es.hist, R.csub, 1024u, &es.bar);
+    if (on_chip)
+      for (int qq = 0; qq < items; ++qq) {
+        const uint32_t b = ((es.cnt[qq] + 3) & ~3u) * 4u;
         if (b) {
-          bulk_g2s(skey + es.seg[q], R.ckey + (size_t)q * kItemKeys, b, &es.bar);
-          bulk_g2s(sidx + es.seg[q], R.cidx + (size_t)q * kItemKeys, b, &es.bar);
+          bulk_g2s(skey + es.seg[qq], R.ckey + (size_t)qq * kItemKeys, b, &es.bar);
+          bulk_g2s(sidx + es.seg[qq], R.cidx + (size_t)qq * kItemKeys, b, &es.bar);
         }
       }
-    }
   }
-  if (on_chip && padded > 0) {
-    mbar_wait(&es.bar, bar_phase);
-    bar_phase ^= 1u;
+  mbar_wait(&es.bar, bar_phase);
+  bar_phase ^= 1u;
+  if (et == 0) {
+    stamp(p, l, EV_SEL2, cta);
+    // the last item to take its copy of the shared row state resets it for
+    // the next use of this parity (h1, the sub-histogram; block mode: keys);
+    // ordered before this CTA's CTR_SELDONE signal, which layer l + 2 waits for
+    const uint32_t old = atom_add_acq_rel(R.ctr + 8, 1u);
+    es.last = old == epoch1 * (uint32_t)items - 1u;
   }
-  if (et == 0) stamp(p, l, EV_SEL2, cta);
   const int ns = (int)padded;
-  // i-th padded slot -> (valid?, key, index).  On chip the padding carries
-  // sentinels (index ~0); off chip the segment table is walked in L2.
   auto get = [&](int i, uint32_t& key, uint32_t& idx) -> bool {
     if (on_chip) {
       key = skey[i];
       idx = sidx[i];
       return idx != 0xFFFFFFFFu;
     }
-    int q = 0;
-    while (q + 1 < items && (uint32_t)i >= es.seg[q + 1]) ++q;
-    const uint32_t off = (uint32_t)i - es.seg[q];
-    if (off >= es.cnt[q]) return false;
-    key = __ldcg(R.ckey + (size_t)q * kItemKeys + off);
-    idx = __ldcg(R.cidx + (size_t)q * kItemKeys + off);
+    int qq = 0;
+    while (qq + 1 < items && (uint32_t)i >= es.seg[qq + 1]) ++qq;
+    const uint32_t off = (uint32_t)i - es.seg[qq];
+    if (off >= es.cnt[qq]) return false;
+    key = __ldcg(R.ckey + (size_t)qq * kItemKeys + off);
+    idx = __ldcg(R.cidx + (size_t)qq * kItemKeys + off);
     return true;
   };
-  // slot i's flag lives next to its candidate in L2 (item q = idx / kItemKeys)
-  auto flag = [&](int i, uint32_t idx, uint32_t v) {
-    const uint32_t q = idx / kItemKeys;
-    R.cflag[(size_t)q * kItemKeys + (uint32_t)i - es.seg[q]] = v;
-    if (v) atomicAdd(&es.selc[q], 1u);
+  auto take = [&](uint32_t idx) {
+    atomicAdd(&es.selc[idx / kItemKeys], 1u);
+    if ((int)idx >= lo && (int)idx < lo + cnt) atomicOr(ws + ((idx - (uint32_t)lo) >> 5), 1u << (idx & 31));
   };
-  // Narrow with 8-bit radix passes while many candidates share the prefix
-  // (counts only), then one pass takes every candidate above the final
-  // prefix and compacts the survivors, which are ranked exactly.
-  uint32_t live = padded;  // upper bound on candidates matching P
-  while (live > (uint32_t)kRankMax && shift > 0) {  // <= kRankMax survivors fit either warp's list
+  epi_digit(es, es.hist, false, 256, krem, et);  // ends with epi_bar: es.last visible
+  if (es.last) {
+    if (R.h1)
+      for (int b = et; b < LYC_H1_ROW; b += kEpiThreads) R.h1[b] = 0u;
+    for (int b = et; b < 256; b += kEpiThreads) R.csub[b] = 0u;
+    if (p.sel_mode == SEL_BLOCK_KEYS)
+      for (int i = et; i < n; i += kEpiThreads) R.keys[i] = 0u;
+  }
+  P = (P << 8) | es.digit;
+  shift -= 8;
+  krem -= es.above;
+  uint32_t live = es.hist[es.digit];
+  if (et == 0) stamp(p, l, EV_F_PREFIX, cta);
+  // (rare) keep narrowing while too many candidates share the prefix
+  while (live > (uint32_t)kRankMax && shift > 0) {
     const int wbits = shift > 8 ? 8 : shift;
     shift -= wbits;
     const uint32_t mask = (1u << wbits) - 1u;
@@ -498,27 +544,24 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int row, Epi
     krem -= es.above;
     live = es.hist[es.digit];
   }
-  // per-warp survivor lists (ballot compaction, no atomics): warp w's list at
-  // es.hist + w * 3 * kRankMax as keys | ids | slots
-  const int lane = et & 31, ew = et >> 5;
   epi_bar();
-  if (et == 0) stamp(p, l, EV_F_PREFIX, cta);
+  // one scan: take everything above the prefix, compact the survivors (per-warp
+  // ballot lists at es.hist + 256 + w * 3 * kRankMax: keys | ids)
   {
-    uint32_t* lk = es.hist + ew * 3 * kRankMax;
+    uint32_t* lk = es.hist + 256 + ew * 3 * kRankMax;
     uint32_t mw = 0;
     for (int i0 = ew * 32; i0 < ns; i0 += kEpiThreads) {
       const int i = i0 + lane;
       uint32_t key = 0, idx = 0;
       const bool ok = i < ns && get(i, key, idx);
       const uint32_t pre = key >> shift;  // shift < 32
-      if (ok) flag(i, idx, pre > P ? 1u : 0u);
+      if (ok && pre > P) take(idx);
       const bool surv = ok && pre == P;
       const unsigned bal = __ballot_sync(0xffffffffu, surv);
       const uint32_t at = mw + (uint32_t)__popc(bal & ((1u << lane) - 1u));
       if (surv && at < (uint32_t)kRankMax) {
         lk[at] = key;
         lk[kRankMax + at] = idx;
-        lk[2 * kRankMax + at] = (uint32_t)i;
       }
       mw += (uint32_t)__popc(bal);
     }
@@ -527,11 +570,10 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int row, Epi
   epi_bar();
   const uint32_t m0 = es.scan[40], m1 = es.scan[41];
   if (et == 0) stamp(p, l, EV_X1, cta);
-  const bool ranked = m0 <= (uint32_t)kRankMax && m1 <= (uint32_t)kRankMax;
-  if (ranked) {
+  if (m0 <= (uint32_t)kRankMax && m1 <= (uint32_t)kRankMax) {
     const uint32_t m = m0 + m1;
-    const uint32_t* L0 = es.hist;
-    const uint32_t* L1 = es.hist + 3 * kRankMax;
+    const uint32_t* L0 = es.hist + 256;
+    const uint32_t* L1 = es.hist + 256 + 3 * kRankMax;
     for (uint32_t e = et; e < m; e += kEpiThreads) {
       const uint32_t* Le = e < m0 ? L0 + e : L1 + (e - m0);
       const uint32_t ki = Le[0], xi = Le[kRankMax];
@@ -544,13 +586,11 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int row, Epi
         const uint32_t kj = L1[j];
         rank += (kj > ki || (kj == ki && L1[kRankMax + j] < xi)) ? 1u : 0u;
       }
-      if (rank < krem) flag((int)Le[2 * kRankMax], xi, 1u);
+      if (rank < krem) take(xi);
     }
-  }
-  if (!ranked) {
-    // (only with shift == 0) all survivors carry the same key T = P: the
-    // first krem in index order
-    // (slot order is index order)
+  } else {
+    // (only with shift == 0) more than kRankMax copies of one key: the first
+    // krem in index order (slot order is index order)
     uint32_t tie_run = 0;
     for (int b0 = 0; b0 < ns; b0 += kEpiThreads) {
       const int i = b0 + et;
@@ -559,104 +599,46 @@ __device__ void finish_row(const LycStepParams& p, const SelRow& R, int row, Epi
       const bool is_eq = ok && key == P;
       uint32_t tot;
       const uint32_t inc = epi_scan(is_eq ? 1u : 0u, es.scan, et, tot);
-      if (is_eq && tie_run + inc - 1u < krem) flag(i, idx, 1u);
+      if (is_eq && tie_run + inc - 1u < krem) take(idx);
       tie_run += tot;
     }
   }
   epi_bar();
   if (et == 0) stamp(p, l, EV_SEL0, cta);
-  // per-item output offsets: definite keys + selected candidates, in item order
-  const uint32_t n_q = et < items ? __ldcg(R.ccnt + 64 + et) + es.selc[et] : 0u;
+  // this item's output offset: definite keys + selected candidates of the
+  // items before it
+  const uint32_t n_q = et < items ? es.defc[et] + es.selc[et] : 0u;
   uint32_t tot;
   const uint32_t end_q = epi_scan(n_q, es.scan, et, tot);
-  if (et < items) R.ccnt[128 + et] = end_q - n_q;
+  if (et == q) es.pad = end_q - n_q;
   epi_bar();
-  if (et == 0) {
-    if (p.idx_count) p.idx_count[row] = p.k_sel;
-    __threadfence();
-    st_release(R.ctr + 4, epoch1);
-    stamp(p, l, EV_SEL1, cta);
-  }
-  // reset the row's fused histogram (block mode: its keys) for the next use
-  // of this parity -- after the release (off the emitters' critical path);
-  // ordered before this CTA's own CTR_SELDONE signal, which layer l + 2 waits for
-  if (R.h1)
-    for (int b = et; b < LYC_H1_ROW; b += kEpiThreads) R.h1[b] = 0u;
-  if (p.sel_mode == SEL_BLOCK_KEYS)
-    for (int i = et; i < n; i += kEpiThreads) R.keys[i] = 0u;
-}
-
-// Emit item q of a resolved row: its 256 bitmap words (one 16-B vector per
-// thread), one scan for the positions, branch-free predicated stores of the
-// first four set bits of every word.
-__device__ void emit_item(const LycStepParams& p, const SelRow& R, int q, int32_t* out,
-                          EpiSmem& es, uint32_t epoch1, int et, int l, int cta) {
-  if (et == 0) {
-    spin_until(R.ctr + 4, epoch1);
-    stamp(p, l, EV_X0, cta);
-  }
-  epi_bar();
-  const int n = p.n_keys;
-  const int lo = q * kItemKeys;
-  const int cnt = min(kItemKeys, n - lo);
-  const int w0 = lo / 32 + et * 4;  // this thread's 4 words (128 keys)
-  // independent loads first: the item's words, its candidate count and output
-  // offset, and the first two candidate (flag, id) pairs of this thread
-  uint4 v = make_uint4(0u, 0u, 0u, 0u);
-  if (et * 128 < cnt) v = __ldcg(reinterpret_cast<const uint4*>(R.bitmap + bm_pad(w0)));
-  const uint32_t ncand = __ldcg(R.ccnt + q);
-  const uint32_t out0 = __ldcg(R.ccnt + 128 + q);
-  // (speculative: slots past the candidate count are never used; a slot
-  // index below the item's key count is always inside the row)
-  uint32_t f0 = 0, x0 = 0, f1 = 0, x1 = 0;
-  if (et < cnt) {
-    f0 = __ldcg(R.cflag + lo + et);
-    x0 = __ldcg(R.cidx + lo + et);
-  }
-  if (et + kEpiThreads < cnt) {
-    f1 = __ldcg(R.cflag + lo + et + kEpiThreads);
-    x1 = __ldcg(R.cidx + lo + et + kEpiThreads);
-  }
-  // the finisher's selected boundary-bin candidates join this item's words
-  uint32_t* ws = es.buf;  // [256] on-chip copy of the item's words
-  reinterpret_cast<uint4*>(ws)[et] = v;
-  epi_bar();
-  for (uint32_t i = et; i < ncand; i += kEpiThreads) {
-    uint32_t f = f0, x = x0;
-    if (i >= 2 * kEpiThreads) {
-      f = __ldcg(R.cflag + lo + i);
-      x = __ldcg(R.cidx + lo + i);
-    }
-    f0 = f1;
-    x0 = x1;
-    if (f) atomicOr(ws + ((x - (uint32_t)lo) >> 5), 1u << (x & 31));
-  }
-  epi_bar();
-  v = reinterpret_cast<const uint4*>(ws)[et];
+  const uint32_t out0 = es.pad;
+  const uint4 v = reinterpret_cast<const uint4*>(ws)[et];
   uint32_t wv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
   for (int i = 0; i < 4; ++i)
     if (et * 128 + i * 32 >= cnt) wv[i] = 0u;
   const uint32_t c = __popc(wv[0]) + __popc(wv[1]) + __popc(wv[2]) + __popc(wv[3]);
-  uint32_t tot;
   uint32_t pos = epi_scan(c, es.scan, et, tot) - c + out0;
+  if (et == 0) stamp(p, l, EV_X0, cta);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const uint32_t m0 = wv[i];
+    const uint32_t m0w = wv[i];
     const uint32_t base = (uint32_t)(w0 + i) * 32u;
-    const uint32_t m1 = m0 & (m0 - 1u), m2 = m1 & (m1 - 1u), m3 = m2 & (m2 - 1u);
-    uint32_t m4 = m3 & (m3 - 1u);
-    st_global_pred(out + pos, base + (uint32_t)(__ffs(m0) - 1), m0 != 0u);
-    st_global_pred(out + pos + 1, base + (uint32_t)(__ffs(m1) - 1), m1 != 0u);
-    st_global_pred(out + pos + 2, base + (uint32_t)(__ffs(m2) - 1), m2 != 0u);
-    st_global_pred(out + pos + 3, base + (uint32_t)(__ffs(m3) - 1), m3 != 0u);
+    const uint32_t m1w = m0w & (m0w - 1u), m2w = m1w & (m1w - 1u), m3w = m2w & (m2w - 1u);
+    uint32_t m4w = m3w & (m3w - 1u);
+    st_global_pred(out + pos, base + (uint32_t)(__ffs(m0w) - 1), m0w != 0u);
+    st_global_pred(out + pos + 1, base + (uint32_t)(__ffs(m1w) - 1), m1w != 0u);
+    st_global_pred(out + pos + 2, base + (uint32_t)(__ffs(m2w) - 1), m2w != 0u);
+    st_global_pred(out + pos + 3, base + (uint32_t)(__ffs(m3w) - 1), m3w != 0u);
     uint32_t p4 = pos + 4u;
-    pos += __popc(m0);
-    while (m4) {
-      out[p4++] = (int32_t)(base + (uint32_t)(__ffs(m4) - 1));
-      m4 &= m4 - 1u;
+    pos += __popc(m0w);
+    while (m4w) {
+      out[p4++] = (int32_t)(base + (uint32_t)(__ffs(m4w) - 1));
+      m4w &= m4w - 1u;
     }
   }
+  if (q == 0 && et == 0 && p.idx_count) p.idx_count[row] = p.k_sel;
   epi_bar();
   if (et == 0) {
     stamp(p, l, EV_F_EMIT, cta);
@@ -705,7 +687,6 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
           // selection (if any) finished
           if (l >= 2 && p.layers[l - 2].n_sel > 0 && p.sel_mode != SEL_NONE)
             spin_until(LYC_CTR(p.ctr, l - 2, CTR_SELDONE), epoch1 * seldone_per_step(p, l - 2));
-          __threadfence();
         }
         consumer_bar();
       }
@@ -747,38 +728,43 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
       const LycLayerDesc L = p.layers[l];
       if (et == 0) {
         spin_until(LYC_CTR(p.ctr, l, CTR_ATTN), t_attn);
-        __threadfence();
         stamp(p, l, EV_EPI_ATTN, cta);
       }
       epi_bar();
+      // Roles of this layer's epilogue: when the selection items fit in half
+      // the grid they go to the LAST n_items CTAs, which classify at once,
+      // while the other CTAs merge (the selection no longer queues behind the
+      // merge); otherwise every CTA merges, then classifies.
+      const int n_items = (L.n_sel > 0 && p.sel_mode != SEL_NONE) ? L.n_sel * items : 0;
+      const bool split_roles = n_items > 0 && 2 * n_items <= p.n_ctas;
+      const int item_base = split_roles ? p.n_ctas - n_items : 0;
+      const int merge_ctas = split_roles ? item_base : p.n_ctas;
       // (a) split-KV merge
       const int total = L.n_merges * chunks;
       uint8_t* outl = static_cast<uint8_t*>(p.out) + (int64_t)l * p.q_layer_stride * esz;
-      for (int t = cta * kEpiWarps + ew; t < total; t += p.n_ctas * kEpiWarps) {
-        const LycMergeTask tk = L.merges[t / chunks];
-        const LycSlot s = L.slots[tk.slot];
-        merge_task<T>(p.part_o, p.part_lse, s, tk.j, t % chunks, p.group, D, outl, lane);
-      }
+      if (cta < merge_ctas)
+        for (int t = cta * kEpiWarps + ew; t < total; t += merge_ctas * kEpiWarps) {
+          const LycMergeTask tk = L.merges[t / chunks];
+          merge_task<T>(p.part_o, p.part_lse, tk, t % chunks, p.group, D, outl, lane);
+        }
       epi_bar();
       if (et == 0) {
         stamp(p, l, EV_MERGE, cta);
         signal(LYC_CTR(p.ctr, l, CTR_MERGE));
       }
       // (b) selection items of this layer's retrieval heads: classify every
-      // own item (the CTA completing a row resolves it), then emit them
-      if (L.n_sel > 0 && p.sel_mode != SEL_NONE) {
-        const int n_items = L.n_sel * items;
-        for (int it = cta; it < n_items; it += p.n_ctas) {
+      // own item, then resolve the rows and emit the items
+      if (n_items > 0 && cta >= item_base) {
+        const int i0 = cta - item_base, istep = split_roles ? n_items : p.n_ctas;
+        for (int it = i0; it < n_items; it += istep) {
           const int r = it / items, q = it - r * items;
-          const SelRow R = sel_row(p, l, r);
-          if (classify_item(p, R, q, epoch1, es, bar_phase, et, l, cta))
-            finish_row(p, R, __ldg(L.sel_rows + r), es, bar_phase, epoch1, et, l, cta);
+          classify_item(p, sel_row(p, l, r), q, es, bar_phase, et, l, cta);
         }
-        for (int it = cta; it < n_items; it += p.n_ctas) {
+        for (int it = i0; it < n_items; it += istep) {
           const int r = it / items, q = it - r * items;
-          const SelRow R = sel_row(p, l, r);
           const int row = __ldg(L.sel_rows + r);
-          emit_item(p, R, q, p.idx + (int64_t)row * p.idx_stride, es, epoch1, et, l, cta);
+          resolve_emit_item(p, sel_row(p, l, r), q, row, p.idx + (int64_t)row * p.idx_stride, es,
+                            bar_phase, epoch1, et, l, cta);
         }
       }
     }

@@ -50,11 +50,11 @@ def main():
     t0 = tr[0, 0].min()
     rel = (tr - t0) / 1e3
     # selection events in chronological order (max over CTAs; NaN = no selection)
-    ev = [("cons_beg", 0, "min"), ("cons_end", 1, "max"), ("merge", 3, "max"),
-          ("c_prefix", 8, "max"), ("c_keys", 9, "max"), ("c_done", 10, "max"),
-          ("f_scan", 12, "max"), ("f_loaded", 6, "max"), ("f_narrow", 11, "max"),
-          ("f_compact", 15, "max"), ("f_ranked", 4, "max"), ("f_release", 5, "max"),
-          ("e_wake", 14, "max"), ("e_done", 13, "max")]
+    ev = [("cons_beg", 0, "min"), ("cons_end", 1, "max"), ("epi_wake", 2, "max"),
+          ("merge", 3, "max"), ("c_prefix", 8, "max"), ("c_keys", 9, "max"),
+          ("c_done", 10, "max"), ("r_wake", 12, "max"), ("r_loaded", 6, "max"),
+          ("r_digit", 11, "max"), ("r_scan", 15, "max"), ("r_ranked", 4, "max"),
+          ("e_scan", 14, "max"), ("e_done", 13, "max")]
     print(f"{'l':>3} {'R':>2} " + " ".join(f"{n:>9}" for n, _, _ in ev))
     for l in range(NL):
         nr = int((roles[l] == 0).sum()) if l else H
