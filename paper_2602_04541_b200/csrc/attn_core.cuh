@@ -712,36 +712,47 @@ __device__ __forceinline__ void merge_task(const float* part_o, const float* par
                                            void* out, int lane, float* out_f32 = nullptr,
                                            float* out_lse = nullptr) {
   const int j = s.j;
-  // one pass (online rescaling): every lane loads its partials' LSE and
-  // outputs together -- one L2 round trip per partial instead of two
+  // one pass (online rescaling) in batches of kB partials per lane: all of a
+  // batch's LSE and output loads are issued before any is used -- a slot with
+  // <= 32 * kB partials merges in ONE L2 round trip
+  constexpr int kB = 4;
   float m = -INFINITY, den = 0.f;
   float acc[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) acc[c] = 0.f;
-#pragma unroll 2
-  for (int i = lane; i < s.n_units; i += 32) {
-    const int64_t u = s.first_unit + i;
-    const float lse = __ldcg(part_lse + u * G + j);
-    const float4* src = reinterpret_cast<const float4*>(part_o + (u * G + j) * D + chunk * 32);
-    float4 v[8];
+  for (int base = 0; base < s.n_units; base += 32 * kB) {
+    float lse[kB];
+    float4 v[kB][8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) v[c] = chunk * 32 + 4 * c < D ? __ldcg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-    if (lse == -INFINITY) continue;  // empty partial
-    if (lse > m) {
-      const float f = m == -INFINITY ? 0.f : exp2f(m - lse);
-      den *= f;
+    for (int b = 0; b < kB; ++b) {
+      const int i = base + b * 32 + lane;
+      const bool ok = i < s.n_units;
+      const int64_t u = s.first_unit + (ok ? i : 0);
+      lse[b] = ok ? __ldcg(part_lse + u * G + j) : -INFINITY;
+      const float4* src = reinterpret_cast<const float4*>(part_o + (u * G + j) * D + chunk * 32);
 #pragma unroll
-      for (int c = 0; c < 32; ++c) acc[c] *= f;
-      m = lse;
+      for (int c = 0; c < 8; ++c)
+        v[b][c] = (ok && chunk * 32 + 4 * c < D) ? __ldcg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    const float w = exp2f(lse - m);
-    den += w;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      acc[4 * c] = fmaf(w, v[c].x, acc[4 * c]);
-      acc[4 * c + 1] = fmaf(w, v[c].y, acc[4 * c + 1]);
-      acc[4 * c + 2] = fmaf(w, v[c].z, acc[4 * c + 2]);
-      acc[4 * c + 3] = fmaf(w, v[c].w, acc[4 * c + 3]);
+    for (int b = 0; b < kB; ++b) {
+      if (lse[b] == -INFINITY) continue;  // empty or absent partial
+      if (lse[b] > m) {
+        const float f = m == -INFINITY ? 0.f : exp2f(m - lse[b]);
+        den *= f;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) acc[c] *= f;
+        m = lse[b];
+      }
+      const float w = exp2f(lse[b] - m);
+      den += w;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        acc[4 * c] = fmaf(w, v[b][c].x, acc[4 * c]);
+        acc[4 * c + 1] = fmaf(w, v[b][c].y, acc[4 * c + 1]);
+        acc[4 * c + 2] = fmaf(w, v[b][c].z, acc[4 * c + 2]);
+        acc[4 * c + 3] = fmaf(w, v[b][c].w, acc[4 * c + 3]);
+      }
     }
   }
   // rescale every lane to the warp maximum, then the fixed-shape reductions
