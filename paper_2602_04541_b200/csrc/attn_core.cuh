@@ -56,7 +56,7 @@ struct AttnCfg {
   // layer-start staging of up to kQUnits unit descriptors + their queries (bf16)
   static constexpr int kQUnits = 8;
   static constexpr int kURecBytes = 80;  // LycUnit + LycSlot, padded
-  static constexpr int kUStageBytes = kE == 2 ? kQUnits * kURecBytes : 0;
+  static constexpr int kUStageBytes = kE == 2 ? 2 * kQUnits * kURecBytes : 0;  // double-buffered
   static constexpr int kQStageBytes = kE == 2 ? kQUnits * kMaxG * D * 2 : 0;
   static constexpr int kHistBytes = LYC_H1_BINS * 4;  // per-CTA first-pass selection histogram
   static constexpr int kFixed = kMergeBytes + kQBytes + 512 + kExtraBytes + kHistBytes +
@@ -356,10 +356,27 @@ __device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t bin, bool ok, 
 // Consumer warp w handles rows [16w, 16w+16) of each 64-row tile.  Query rows
 // j < G <= 8 sit in A-fragment rows 0..7; rows 8..15 are zero, so only the
 // c0/c1 halves of the score / output fragments carry data.
+struct UnitRec {
+  LycUnit u;
+  LycSlot s;
+};
+
+// Unit records [ub, ub + n) (n <= cap) of one layer into shared memory, by the
+// first n threads of the caller's group.
+__device__ __forceinline__ void stage_unit_records(const LycView& p, UnitRec* rec, int ub, int ue,
+                                                   int tid, int cap) {
+  if (tid < min(ue - ub, cap)) {
+    UnitRec r;
+    r.u = p.units[ub + tid];
+    r.s = p.unit_slots ? p.unit_slots[ub + tid] : p.slots[r.u.slot];
+    rec[tid] = r;
+  }
+}
+
 template <int D>
 __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnSmem<__nv_bfloat16, D>& sm,
                                                    int ub, int ue, int warp, int lane, int& stage,
-                                                   uint32_t& phase) {
+                                                   uint32_t& phase, int rec_buf = -1) {
   using C = AttnCfg<__nv_bfloat16, D>;
   constexpr int KS = D / 16;  // k-steps over d for QK^T
   constexpr int NT = D / 8;   // n-tiles over d for PV
@@ -377,24 +394,19 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
   const __nv_bfloat16* Q = static_cast<const __nv_bfloat16*>(p.q);
 
   // ---- layer start: the first kQUnits unit records and their queries are
-  // staged on chip in two coalesced round trips, instead of three dependent
-  // L2 round trips (unit -> slot -> q) at every unit boundary
+  // staged on chip (records possibly pre-staged by the caller while it waited
+  // for the previous layer -- rec_buf >= 0), instead of three dependent L2
+  // round trips (unit -> slot -> q) at every unit boundary
   constexpr int kQU = C::kQUnits;
-  struct URec {
-    LycUnit u;
-    LycSlot s;
-  };
+  using URec = UnitRec;
   static_assert(sizeof(URec) <= C::kURecBytes, "unit record");
-  URec* rec = reinterpret_cast<URec*>(sm.ustage);
   const int tid = warp * 32 + lane;
   const int nst = min(ue - ub, kQU);
-  if (tid < nst) {
-    URec r;
-    r.u = p.units[ub + tid];
-    r.s = p.unit_slots ? p.unit_slots[ub + tid] : p.slots[r.u.slot];
-    rec[tid] = r;
+  URec* rec = reinterpret_cast<URec*>(sm.ustage) + (rec_buf > 0 ? kQU : 0);
+  if (rec_buf < 0) {
+    stage_unit_records(p, rec, ub, ue, tid, kQU);
+    consumer_bar();
   }
-  consumer_bar();
   {
     const int cpu = G * D / 8;  // 16-B chunks of one unit's G query rows
     for (int c = tid; c < nst * cpu; c += kConsumerWarps * 32) {
@@ -695,9 +707,9 @@ __device__ __forceinline__ void consume_units_f32(const LycView& p, const AttnSm
 template <typename T, int D>
 __device__ __forceinline__ void consume_units(const LycView& p, const AttnSmem<T, D>& sm, int ub,
                                               int ue, int warp, int lane, int& stage,
-                                              uint32_t& phase) {
+                                              uint32_t& phase, int rec_buf = -1) {
   if constexpr (sizeof(T) == 2)
-    consume_units_bf16<D>(p, sm, ub, ue, warp, lane, stage, phase);
+    consume_units_bf16<D>(p, sm, ub, ue, warp, lane, stage, phase, rec_buf);
   else
     consume_units_f32<D>(p, sm, ub, ue, warp, lane, stage, phase);
 }

@@ -694,11 +694,21 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
       const LycLayerDesc L = p.layers[l];
       const LycView v = layer_view(p, L, l, esz);
       consume_units<T, D>(v, sm, L.split_off[cell], L.split_off[cell + 1], warp, lane, stage,
-                          phase);
+                          phase, l > 0 ? (l & 1) : -1);
       consumer_bar();
       if (tid == 0) {
         stamp(p, l, EV_CONS_END, cta);
         signal(LYC_CTR(p.ctr, l, CTR_ATTN));
+      }
+      // while the grid finishes layer l: stage layer l + 1's unit records
+      // (static plan data) into the other record buffer
+      if constexpr (sizeof(T) == 2) {
+        if (l + 1 < p.n_layers) {
+          const LycLayerDesc Ln = p.layers[l + 1];
+          const LycView vn = layer_view(p, Ln, l + 1, esz);
+          UnitRec* rec = reinterpret_cast<UnitRec*>(sm.ustage) + ((l + 1) & 1) * C::kQUnits;
+          stage_unit_records(vn, rec, Ln.split_off[cell], Ln.split_off[cell + 1], tid, C::kQUnits);
+        }
       }
     }
   } else if (warp < kConsumerWarps + kProducerWarps) {
