@@ -333,6 +333,7 @@ def main():
     ap.add_argument("--workload", default="llama3-8b-128k", choices=list(WORKLOADS))
     ap.add_argument("--select", default="tokens", choices=["tokens", "blocks"])
     ap.add_argument("--retrieval-frac", type=float, default=0.125)
+    ap.add_argument("--top-k", type=int, default=0, help="override the workload's top-k budget")
     ap.add_argument("--seed", type=int, default=2602)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-full", action="store_true")
@@ -342,6 +343,8 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = dict(WORKLOADS[args.workload])
+    if args.top_k:
+        wl["k"] = args.top_k
     roles = make_roles(wl["NL"], wl["H"], args.retrieval_frac, args.seed)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))

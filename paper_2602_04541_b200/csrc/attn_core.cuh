@@ -163,6 +163,7 @@ __device__ __forceinline__ Tile tile_of(const LycSlot& s, int item, int sub, int
 
 struct NoWaits {
   __device__ __forceinline__ void unit(const LycSlot&) const {}
+  __device__ __forceinline__ bool needed() const { return false; }
   __device__ __forceinline__ void last_tile() const {}
 };
 
@@ -217,7 +218,19 @@ __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMa
         load_rows(tn, rows_n);
       }
       {
-        if (it == s.n_items - 1 && sub == tpi - 1) waits.last_tile();
+        // the current token's K/V row is produced after the previous layer:
+        // only a tile that holds it waits (dense: the last tile always; a
+        // selected set: iff its largest id is the current token)
+        if (it == s.n_items - 1 && sub == tpi - 1 && waits.needed()) {
+          bool has_cur = true;
+          if (s.kind == ITEM_TOKENS) {
+            const int len = s.count ? min(s.list_len, __ldcg(s.count)) : s.list_len;
+            has_cur = len > 0 && __ldcg(s.list + len - 1) == p.seq_len - 1;
+          } else if (s.kind == ITEM_BLOCKS) {
+            has_cur = __ldcg(s.list + s.n_items - 1) == (p.seq_len - 1) / p.block_size;
+          }
+          if (has_cur) waits.last_tile();
+        }
         uint8_t* kd = ring + stage * C::kStageBytes;
         uint8_t* vd = kd + C::kTileBytes;
         if (t.ids == nullptr && t.nvalid == LYC_TILE) {

@@ -113,6 +113,7 @@ struct StepWaits {
     if (s.dep >= 0)  // every retrieval head of layer dep finished its selection
       wait(LYC_CTR(p->ctr, s.dep, CTR_SELDONE), epoch1 * seldone_per_step(*p, s.dep));
   }
+  __device__ __forceinline__ bool needed() const { return layer > 0; }
   __device__ __forceinline__ void last_tile() const {
     if (layer > 0) wait(LYC_CTR(p->ctr, layer - 1, CTR_MERGE), epoch1 * (uint32_t)p->n_ctas);
   }
