@@ -48,7 +48,7 @@ struct AttnCfg {
   static constexpr int kTileBytes = LYC_TILE * kRowBytes;
   static constexpr int kStageBytes = 2 * kTileBytes;  // K tile then V tile
   static constexpr int kChunksPerRow = kRowBytes / 16;
-  static constexpr int kMergeBytes = kConsumerWarps * kMaxG * (D + 2) * 4;
+  static constexpr int kMergeBytes = kConsumerWarps * kMaxG * (D + 3) * 4;  // mo, ml, coef
   static constexpr int kQBytes = kE == 4 ? (kMaxG + 1) * D * 4 : 0;
   static constexpr int kMaxSmem = 232448 - 1024;   // 227 KB opt-in minus alignment slack
   // the step kernel's epilogue warps (selection); the step kernel is built for d <= 128 only
@@ -95,7 +95,7 @@ struct AttnSmem {
   // generic accesses would queue behind the thread's outstanding global stores.
   static constexpr int kMoOff = 0;
   static constexpr int kMlOff = kMoOff + kConsumerWarps * kMaxG * D * 4;
-  static constexpr int kQsOff = kMlOff + kConsumerWarps * kMaxG * 2 * 4;
+  static constexpr int kQsOff = kMlOff + kConsumerWarps * kMaxG * 3 * 4;  // ml + coef
   static constexpr int kBarOff = kQsOff + AttnCfg<T, D>::kQBytes;
   static constexpr int kExtraOff =
       (kBarOff + 2 * AttnCfg<T, D>::kStages * 8 + 127) & ~127;
@@ -298,40 +298,67 @@ __device__ __forceinline__ void store_out<__nv_bfloat16>(__nv_bfloat16* dst, flo
   *dst = __float2bfloat16_rn(v);
 }
 
+// Consumer-side timeline stamps (events 16..23 of the step timeline).
+__device__ __forceinline__ void cstamp(const LycView& p, int ev, int tid) {
+  if (p.trace_l && tid == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace_l[(size_t)ev * p.trace_ctas + blockIdx.x] = t;
+  }
+}
+
 // Merge the consumer warps' (m, l, o) for one unit and emit partial / output.
 template <typename T, int D>
 __device__ __forceinline__ void unit_epilogue(const LycView& p, const LycSlot& s, int u,
                                               float* mo, float* ml, int tid, uint32_t* hist_s,
                                               uint32_t* hist_g) {
   const int G = p.group;
+  cstamp(p, 20, tid);
   consumer_bar();
+  cstamp(p, 21, tid);
   const bool direct = s.n_units == 1;
-  for (int idx = tid; idx < G * D; idx += kConsumerWarps * 32) {
-    const int j = idx / D, d = idx - j * D;
+  // per query head j (one thread each): the warps' rescale coefficients
+  // f_w / L and the unit's LSE -- computed once, not once per column
+  float* coef = ml + kConsumerWarps * kMaxG * 2;  // [kMaxG][kConsumerWarps]
+  if (tid < G) {
+    const int j = tid;
     float M = -INFINITY;
 #pragma unroll
     for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, ml[(w * kMaxG + j) * 2]);
-    float L = 0.f, O = 0.f;
+    float f[kConsumerWarps], L = 0.f;
 #pragma unroll
     for (int w = 0; w < kConsumerWarps; ++w) {
       const float mw = ml[(w * kMaxG + j) * 2];
-      const float f = mw == -INFINITY ? 0.f : exp2f(mw - M);
-      L += ml[(w * kMaxG + j) * 2 + 1] * f;
-      O += mo[(w * kMaxG + j) * D + d] * f;
+      f[w] = mw == -INFINITY ? 0.f : exp2f(mw - M);
+      L += ml[(w * kMaxG + j) * 2 + 1] * f[w];
     }
     // L == 0: the unit saw no valid row (a shard holding none of a sparse
     // head's indices) -- an empty partial (o = 0, lse = -inf)
-    const float o = L > 0.f ? O / L : 0.f;
-    if (direct && p.out_f32) {
-      p.out_f32[(int64_t)(s.q_row + j) * D + d] = o;
-      if (d == 0) p.out_lse[s.q_row + j] = L > 0.f ? log2f(L) + M : -INFINITY;
-    } else if (direct) {
-      store_out<T>(static_cast<T*>(p.out) + (int64_t)(s.q_row + j) * D + d, o);
-    } else {
-      p.part_o[((int64_t)u * G + j) * D + d] = o;
-      if (d == 0) p.part_lse[(int64_t)u * G + j] = L > 0.f ? log2f(L) + M : -INFINITY;
-    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) coef[j * kConsumerWarps + w] = f[w] * inv;
+    const float lse = L > 0.f ? log2f(L) + M : -INFINITY;
+    if (direct && p.out_f32)
+      p.out_lse[s.q_row + j] = lse;
+    else if (!direct)
+      p.part_lse[(int64_t)u * G + j] = lse;
   }
+  consumer_bar();
+#pragma unroll 4
+  for (int idx = tid; idx < G * D; idx += kConsumerWarps * 32) {
+    const int j = idx / D, d = idx - j * D;
+    float o = 0.f;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w)
+      o = fmaf(mo[(w * kMaxG + j) * D + d], coef[j * kConsumerWarps + w], o);
+    if (direct && p.out_f32)
+      p.out_f32[(int64_t)(s.q_row + j) * D + d] = o;
+    else if (direct)
+      store_out<T>(static_cast<T*>(p.out) + (int64_t)(s.q_row + j) * D + d, o);
+    else
+      p.part_o[((int64_t)u * G + j) * D + d] = o;
+  }
+  cstamp(p, 22, tid);
   static_assert(kConsumerWarps * 32 * 32 == LYC_H1_BINS && LYC_H1_COARSE * 64 == LYC_H1_BINS,
                 "histogram flush mapping");
   if (hist_g) {
@@ -429,6 +456,8 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
     }
   }
   consumer_bar();
+  cstamp(p, 16, tid);
+  bool first_tile = true;
 
   for (int u = ub; u < ue; ++u) {
     const bool staged = u - ub < kQU;
@@ -461,18 +490,31 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
       for (int sub = 0; sub < tpi; ++sub) {
         const Tile t = tile_of(s, it, sub, p.seq_len, p.block_size);
         mbar_wait(&sm.full[stage], phase);
+        if (first_tile) {
+          cstamp(p, 17, tid);
+          first_tile = false;
+        }
+        cstamp(p, 19, tid);
         const uint8_t* ks = sm.ring + stage * C::kStageBytes;
         const uint8_t* vs = ks + C::kTileBytes;
         // ---- S = Q K^T for this warp's 16 rows (two n-tiles of 8)
+        // two independent accumulator chains (even / odd k-steps) halve the
+        // dependent-MMA latency of a tile; summed once at the end
         float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        float sd[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) {
           uint32_t b0, b1, b2, b3;
           const int c = 2 * (kk & 3) + k_x;
           ldsm_x4(b0, b1, b2, b3, ks + (kk >> 2) * C::kPanelBytes + k_row + ((c ^ sw) << 4));
-          mma_bf16(sc[0], qa0[kk], 0u, qa2[kk], 0u, b0, b1);
-          mma_bf16(sc[1], qa0[kk], 0u, qa2[kk], 0u, b2, b3);
+          float (&acc)[2][4] = (kk & 1) ? sd : sc;
+          mma_bf16(acc[0], qa0[kk], 0u, qa2[kk], 0u, b0, b1);
+          mma_bf16(acc[1], qa0[kk], 0u, qa2[kk], 0u, b2, b3);
         }
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) sc[n][e] += sd[n][e];
         // ---- fused selection score: sum over packed rows (rows >= G are 0)
         if (want_sel) {
           float ps[2][2];
@@ -574,6 +616,7 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
     }
     unit_epilogue<__nv_bfloat16, D>(p, s, s.first_unit + un.hls, sm.mo, sm.ml, warp * 32 + lane,
                                     sm.hist, hist);
+    if (u == ub) cstamp(p, 18, tid);
   }
 }
 

@@ -23,7 +23,7 @@
 // Global h1 rows carry 64 coarse bins (top 6 bits) after the fine bins.
 #define LYC_H1_COARSE 64
 #define LYC_H1_ROW (LYC_H1_BINS + LYC_H1_COARSE)
-#define LYC_TRACE_EVENTS 16  // step-timeline stamps per layer per CTA
+#define LYC_TRACE_EVENTS 24  // step-timeline stamps per layer per CTA
 
 enum { ITEM_DENSE = 0, ITEM_BLOCKS = 1, ITEM_TOKENS = 2 };
 
@@ -68,6 +68,8 @@ struct LycView {
   uint32_t* exec_counts;    // optional [n_slots][counts_stride] per item
   float* out_f32;           // optional: fp32 outputs [rows][d] instead of `out` (shard partials)
   float* out_lse;           // optional with out_f32: base-2 LSE per output row
+  unsigned long long* trace_l;  // optional step timeline of this layer [LYC_TRACE_EVENTS][n_ctas]
+  int32_t trace_ctas;
   int64_t sel_stride;
   int32_t counts_stride;
   int32_t n_splits;         // splits per batch item (grid.x)

@@ -201,11 +201,11 @@ class HybridDecoder:
         check(lib().lyc_decoder_set_trace(self._h, int(bool(enable))))
 
     def trace(self) -> np.ndarray:
-        """[n_layers][16 events][n_ctas] ns stamps of the last traced step."""
+        """[n_layers][24 events][n_ctas] ns stamps of the last traced step."""
         n = check(lib().lyc_decoder_trace(self._h, None, 0))
         buf = np.zeros(n, dtype=np.uint64)
         check(lib().lyc_decoder_trace(self._h, buf.ctypes.data, n))
-        return buf.reshape(self.n_layers, 16, -1)
+        return buf.reshape(self.n_layers, 24, -1)
 
     def set_timing(self, enable: bool = True):
         """CUDA events around every attention-kernel launch (graph-capturable)."""

@@ -33,6 +33,9 @@ for l in range(NL):
     nr = int((roles[l] == 0).sum()) if l else H
     b, e = rel[l, 0], rel[l, 1]
     span = e - b
-    print(f"l{l:2d} R{nr} begin min/max {b.min():7.1f}/{b.max():7.1f}  end p10/p50/p90/max "
-          f"{np.percentile(e,10):7.1f}/{np.percentile(e,50):7.1f}/{np.percentile(e,90):7.1f}/{e.max():7.1f}"
-          f"  span p50 {np.percentile(span,50):5.1f}")
+    qs, t1, u1, tl = rel[l, 16] - b, rel[l, 17] - b, rel[l, 18] - b, rel[l, 19] - b
+    print(f"l{l:2d} R{nr} begin max {b.max():7.1f} end p50/max {np.percentile(e,50):7.1f}/{e.max():7.1f}"
+          f"  span p50 {np.percentile(span,50):5.1f} | q_staged p50 {np.percentile(qs,50):4.1f} "
+          f"first_tile p50 {np.percentile(t1,50):4.1f} first_unit_done p50 {np.percentile(u1,50):5.1f} "
+          f"last_tile p50 {np.percentile(tl,50):5.1f} | ue_enter {np.percentile(rel[l,20]-b,50):5.1f} "
+          f"ue_bar {np.percentile(rel[l,21]-b,50):5.1f} ue_stored {np.percentile(rel[l,22]-b,50):5.1f}")
