@@ -617,6 +617,11 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
     unit_epilogue<__nv_bfloat16, D>(p, s, s.first_unit + un.hls, sm.mo, sm.ml, warp * 32 + lane,
                                     sm.hist, hist);
     if (u == ub) cstamp(p, 18, tid);
+    // one more finished unit of a selection slot: its keys and histogram
+    // counts are published (unit_epilogue ended with a consumer barrier)
+    if (want_sel && p.sel_ctr && tid == 0)
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.sel_ctr + (int64_t)s.sel * 16 + 12)
+                   : "memory");
   }
 }
 
@@ -757,6 +762,9 @@ __device__ __forceinline__ void consume_units_f32(const LycView& p, const AttnSm
     }
     unit_epilogue<float, D>(p, s, s.first_unit + un.hls, sm.mo, sm.ml, warp * 32 + lane, sm.hist,
                             hist);
+    if (want_sel && p.sel_ctr && warp * 32 + lane == 0)
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.sel_ctr + (int64_t)s.sel * 16 + 12)
+                   : "memory");
   }
 }
 

@@ -546,10 +546,13 @@ struct lyc_decoder {
 
 namespace {
 
-// The step kernel's split order: per batch item, slots whose index list is
-// produced by the immediately preceding layer's selection (pool B) are placed
-// after everything else (pool A) inside every split, so each CTA streams its
-// independent tiles while that selection is still running.
+// The step kernel's split order: per batch item, three pools are each cut
+// evenly across all splits and concatenated per split in this order --
+// retrieval slots (so every CTA finishes its share of the retrieval heads
+// first and their selection can start before the layer ends), sparse slots
+// with an older index list, and last the sparse slots whose list the
+// immediately preceding layer's selection produces (streamed while that
+// selection is still running).
 void plan_step_launch(HostLaunch& L, int batch, int heads, int splits, int group, int layer) {
   L.batch = batch;
   L.heads = heads;
@@ -567,13 +570,14 @@ void plan_step_launch(HostLaunch& L, int batch, int heads, int splits, int group
       total += s.n_items;
     }
     if (total == 0) fail(LYC_EINVAL, "plan_splits: batch item has zero blocks");
-    for (int pool = 0; pool < 2; ++pool) {
+    for (int pool = 0; pool < 3; ++pool) {
       std::vector<int> hs;
       int64_t tot = 0;
       for (int g = 0; g < heads; ++g) {
         const LycSlot& s = L.slots[(size_t)b * heads + g];
         const bool late = s.dep >= 0 && s.dep == layer - 1;
-        if ((pool == 1) == late && s.n_items > 0) {
+        const int my_pool = s.kind == ITEM_DENSE ? 0 : late ? 2 : 1;
+        if (my_pool == pool && s.n_items > 0) {
           hs.push_back(g);
           tot += s.n_items;
         }

@@ -68,6 +68,7 @@ struct LycView {
   uint32_t* exec_counts;    // optional [n_slots][counts_stride] per item
   float* out_f32;           // optional: fp32 outputs [rows][d] instead of `out` (shard partials)
   float* out_lse;           // optional with out_f32: base-2 LSE per output row
+  uint32_t* sel_ctr;        // optional [n_sel][16]: word 12 counts finished units of the row's slot
   unsigned long long* trace_l;  // optional step timeline of this layer [LYC_TRACE_EVENTS][n_ctas]
   int32_t trace_ctas;
   int64_t sel_stride;

@@ -147,6 +147,7 @@ __device__ __forceinline__ LycView layer_view(const LycStepParams& p, const LycL
   v.scale_log2 = p.scale_log2;
   v.stages = p.stages;
   v.trace_l = p.trace ? p.trace + (size_t)l * LYC_TRACE_EVENTS * p.n_ctas : nullptr;
+  v.sel_ctr = p.sel_rowctr + (size_t)l * p.max_sel * 16;
   v.trace_ctas = p.n_ctas;
   return v;
 }
@@ -739,19 +740,22 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
     uint32_t bar_phase = 0;
     for (int l = 0; l < p.n_layers; ++l) {
       const LycLayerDesc L = p.layers[l];
-      if (et == 0) {
-        spin_until(LYC_CTR(p.ctr, l, CTR_ATTN), t_attn);
-        stamp(p, l, EV_EPI_ATTN, cta);
-      }
-      epi_bar();
       // Roles of this layer's epilogue: when the selection items fit in half
-      // the grid they go to the LAST n_items CTAs, which classify at once,
-      // while the other CTAs merge (the selection no longer queues behind the
-      // merge); otherwise every CTA merges, then classifies.
+      // the grid they go to the LAST n_items CTAs, which start classifying a
+      // row as soon as its retrieval slot's units are all done (per-row unit
+      // counter; retrieval units come first in every split) -- without waiting
+      // for the rest of the layer -- while the other CTAs merge; otherwise
+      // every CTA merges, then classifies.
       const int n_items = (L.n_sel > 0 && p.sel_mode != SEL_NONE) ? L.n_sel * items : 0;
       const bool split_roles = n_items > 0 && 2 * n_items <= p.n_ctas;
       const int item_base = split_roles ? p.n_ctas - n_items : 0;
       const int merge_ctas = split_roles ? item_base : p.n_ctas;
+      const bool early_items = split_roles && cta >= item_base;
+      if (et == 0 && !early_items) {
+        spin_until(LYC_CTR(p.ctr, l, CTR_ATTN), t_attn);
+        stamp(p, l, EV_EPI_ATTN, cta);
+      }
+      epi_bar();
       // (a) split-KV merge
       const int total = L.n_merges * chunks;
       uint8_t* outl = static_cast<uint8_t*>(p.out) + (int64_t)l * p.q_layer_stride * esz;
@@ -771,6 +775,13 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
         const int i0 = cta - item_base, istep = split_roles ? n_items : p.n_ctas;
         for (int it = i0; it < n_items; it += istep) {
           const int r = it / items, q = it - r * items;
+          if (early_items && et == 0) {  // the row's retrieval slot is complete
+            const int slot = __ldg(L.sel_rows + r);
+            spin_until(p.sel_rowctr + ((size_t)l * p.max_sel + r) * 16 + 12,
+                       epoch1 * (uint32_t)L.slots[slot].n_units);
+            stamp(p, l, EV_EPI_ATTN, cta);
+          }
+          epi_bar();
           classify_item(p, sel_row(p, l, r), q, es, bar_phase, et, l, cta);
         }
         for (int it = i0; it < n_items; it += istep) {
