@@ -617,10 +617,11 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
     unit_epilogue<__nv_bfloat16, D>(p, s, s.first_unit + un.hls, sm.mo, sm.ml, warp * 32 + lane,
                                     sm.hist, hist);
     if (u == ub) cstamp(p, 18, tid);
-    // one more finished unit of a selection slot: its keys and histogram
-    // counts are published (unit_epilogue ended with a consumer barrier)
-    if (want_sel && p.sel_ctr && tid == 0)
-      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.sel_ctr + (int64_t)s.sel * 16 + 12)
+    // one more finished unit of a slot that is merged or selected: its
+    // partial, keys and histogram counts are published (unit_epilogue ended
+    // with a consumer barrier)
+    if ((want_sel || s.n_units > 1) && p.slot_ctr && tid == 0)
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.slot_ctr + (int64_t)un.slot * 16 + 12)
                    : "memory");
   }
 }
@@ -762,8 +763,8 @@ __device__ __forceinline__ void consume_units_f32(const LycView& p, const AttnSm
     }
     unit_epilogue<float, D>(p, s, s.first_unit + un.hls, sm.mo, sm.ml, warp * 32 + lane, sm.hist,
                             hist);
-    if (want_sel && p.sel_ctr && warp * 32 + lane == 0)
-      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.sel_ctr + (int64_t)s.sel * 16 + 12)
+    if ((want_sel || s.n_units > 1) && p.slot_ctr && warp * 32 + lane == 0)
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.slot_ctr + (int64_t)un.slot * 16 + 12)
                    : "memory");
   }
 }

@@ -963,6 +963,8 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
         cuda_check(cudaMalloc(&d->sel_ccnt, 2 * rows * 256 * 4), "cudaMalloc ccnt");
         cuda_check(cudaMalloc(&d->sel_csub, 2 * rows * 256 * 4), "cudaMalloc csub");
         cuda_check(cudaMemset(d->sel_csub, 0, 2 * rows * 256 * 4), "memset");
+      }
+      if (d->fused) {  // per-(layer, row / slot) counters of the step kernel
         cuda_check(cudaMalloc(&d->sel_rowctr, (size_t)d->NL * rows * 16 * 4), "cudaMalloc rowctr");
         cuda_check(cudaMemset(d->sel_rowctr, 0, (size_t)d->NL * rows * 16 * 4), "memset");
       }

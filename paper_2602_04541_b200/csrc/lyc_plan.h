@@ -68,7 +68,7 @@ struct LycView {
   uint32_t* exec_counts;    // optional [n_slots][counts_stride] per item
   float* out_f32;           // optional: fp32 outputs [rows][d] instead of `out` (shard partials)
   float* out_lse;           // optional with out_f32: base-2 LSE per output row
-  uint32_t* sel_ctr;        // optional [n_sel][16]: word 12 counts finished units of the row's slot
+  uint32_t* slot_ctr;       // optional [slots][16]: word 12 counts the slot's finished units
   unsigned long long* trace_l;  // optional step timeline of this layer [LYC_TRACE_EVENTS][n_ctas]
   int32_t trace_ctas;
   int64_t sel_stride;
@@ -176,7 +176,8 @@ struct LycStepParams {
   uint32_t* sel_cand;        // [2 parity][max_sel][3][sel_stride] boundary-bin candidates: keys, indices, selected flags
   uint32_t* sel_ccnt;        // [2 parity][max_sel][256] per item: candidates [0,64), definite keys [64,128); row prefix [192,195)
   uint32_t* sel_csub;        // [2 parity][max_sel][256] boundary-bin sub-histograms (zero between uses)
-  uint32_t* sel_rowctr;      // [n_layers][max_sel][16] finished items per row (monotonic)
+  uint32_t* sel_rowctr;      // [n_layers][max_sel][16] monotonic: per selection row words 0 / 8
+                             // (items classified / holding copies); per SLOT word 12 (units done)
   uint32_t* ctr;             // LYC_CTR counters: [n_layers][CTR_PER_LAYER], then epoch, exits
   int32_t* idx;              // index cache [B*H][idx_stride]
   int64_t idx_stride;

@@ -147,7 +147,7 @@ __device__ __forceinline__ LycView layer_view(const LycStepParams& p, const LycL
   v.scale_log2 = p.scale_log2;
   v.stages = p.stages;
   v.trace_l = p.trace ? p.trace + (size_t)l * LYC_TRACE_EVENTS * p.n_ctas : nullptr;
-  v.sel_ctr = p.sel_rowctr + (size_t)l * p.max_sel * 16;
+  v.slot_ctr = p.sel_rowctr + (size_t)l * p.max_sel * 16;
   v.trace_ctas = p.n_ctas;
   return v;
 }
@@ -750,18 +750,17 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
       const bool split_roles = n_items > 0 && 2 * n_items <= p.n_ctas;
       const int item_base = split_roles ? p.n_ctas - n_items : 0;
       const int merge_ctas = split_roles ? item_base : p.n_ctas;
-      const bool early_items = split_roles && cta >= item_base;
-      if (et == 0 && !early_items) {
-        spin_until(LYC_CTR(p.ctr, l, CTR_ATTN), t_attn);
-        stamp(p, l, EV_EPI_ATTN, cta);
-      }
-      epi_bar();
+      // no layer barrier: every merge task waits for its own slot's units,
+      // every selection item for its row's retrieval slot (per-slot counters)
+      uint32_t* slot_ctr = p.sel_rowctr + (size_t)l * p.max_sel * 16 + 12;
       // (a) split-KV merge
       const int total = L.n_merges * chunks;
       uint8_t* outl = static_cast<uint8_t*>(p.out) + (int64_t)l * p.q_layer_stride * esz;
       if (cta < merge_ctas)
         for (int t = cta * kEpiWarps + ew; t < total; t += merge_ctas * kEpiWarps) {
           const LycMergeTask tk = L.merges[t / chunks];
+          if (lane == 0) spin_until(slot_ctr + (size_t)tk.slot * 16, epoch1 * (uint32_t)tk.n_units);
+          __syncwarp();
           merge_task<T>(p.part_o, p.part_lse, tk, t % chunks, p.group, D, outl, lane);
         }
       epi_bar();
@@ -775,10 +774,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
         const int i0 = cta - item_base, istep = split_roles ? n_items : p.n_ctas;
         for (int it = i0; it < n_items; it += istep) {
           const int r = it / items, q = it - r * items;
-          if (early_items && et == 0) {  // the row's retrieval slot is complete
+          if (et == 0) {  // the row's retrieval slot is complete
             const int slot = __ldg(L.sel_rows + r);
-            spin_until(p.sel_rowctr + ((size_t)l * p.max_sel + r) * 16 + 12,
-                       epoch1 * (uint32_t)L.slots[slot].n_units);
+            spin_until(slot_ctr + (size_t)slot * 16, epoch1 * (uint32_t)L.slots[slot].n_units);
             stamp(p, l, EV_EPI_ATTN, cta);
           }
           epi_bar();
