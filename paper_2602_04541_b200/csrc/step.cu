@@ -157,7 +157,7 @@ __device__ __forceinline__ LycView layer_view(const LycStepParams& p, const LycL
 // holds the krem-th largest candidate (krem >= 1).  Two levels, no local
 // arrays: every lane sums a contiguous run of nbins/32 bins, a warp scan picks
 // the lane holding the target, then the warp splits that lane's run again.
-// Returns (digit, count strictly above it).  nbins: power of two, 32..4096.
+// Returns (digit, count strictly above it).  nbins: power of two, 2..4096.
 __device__ __forceinline__ uint32_t ld_bin(const uint32_t* a, bool global) {
   return global ? __ldcg(a) : *a;
 }
@@ -172,10 +172,14 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 __device__ __forceinline__ void find_digit(const uint32_t* h, int nbins, uint32_t krem,
                                            uint32_t& digit, uint32_t& above, int lane,
                                            bool global) {
-  const int per = nbins / 32;             // bins per lane (1..128)
+  // bins per lane (1..128); histograms smaller than 32 bins: one bin per lane
+  // for the first nbins lanes, none for the rest
+  const int per = nbins >= 32 ? nbins / 32 : 1;
   const int hi = nbins - 1 - lane * per;  // lane owns bins (hi - per, hi], highest first
   uint32_t sum = 0;
-  if (per >= 4) {
+  if (hi < 0) {
+    // no bins
+  } else if (per >= 4) {
     const uint4* src = reinterpret_cast<const uint4*>(h + hi - per + 1);
 #pragma unroll 8
     for (int q = 0; q < per / 4; ++q) {

@@ -307,3 +307,36 @@ def test_fused_step_repeated_and_replanned(orc):
                         V[:, 0].float().cpu().numpy(), roles, seq=2999, scale=1 / np.sqrt(d),
                         kind="topk", k=200)
     assert rel_err(c[:, 0].float().cpu().numpy(), r["out"]) < BF16_TOL
+
+
+@pytest.mark.parametrize("n_ties", [2000, 6000])
+def test_fused_step_exact_ties_lowest_index(orc, n_ties):
+    """Exact score ties at the top-k boundary (attention.hpp:117-118: ties go
+    to the lower index).  Rows are built so the pooled scores take three values:
+    800 rows at 2|qbar|^2, n_ties identical rows at |qbar|^2 straddling the
+    boundary, the rest 0 -- the fused selection's tie path (and, with 6000 ties,
+    its off-chip candidate path) must take exactly the lowest-index ties."""
+    import paper_2602_04541_b200 as P
+    NL, B, H, G, d, seq, k = 2, 1, 2, 4, 64, 20000, 1000
+    roles = roles_for(NL, H, [])
+    q, K, V = synth(11, NL, B, H, G, d, seq, seq, torch.float32)
+    rng = np.random.default_rng(5)
+    for l in range(NL):
+        for g in range(H):
+            qbar = q[l, 0, g * G:(g + 1) * G].double().mean(0)
+            rows = rng.permutation(seq)
+            Kl = torch.zeros(seq, d, dtype=torch.float64)
+            Kl[rows[:800]] = 2 * qbar
+            Kl[rows[800:800 + n_ties]] = qbar
+            K[l, 0, g] = Kl.float()
+    dec = P.HybridDecoder(n_layers=NL, batch=B, n_kv_heads=H, group_size=G, d_head=d, seq_cap=seq,
+                          roles=roles, policy=P.SparsityPolicy.top_k(k), dtype=torch.float32)
+    assert dec.fused
+    out = dec.decode_step(q.cuda(), K.cuda(), V.cuda(), seq)
+    torch.cuda.synchronize()
+    sets = dec.token_sets()[0]
+    r = orc.decode_step(q[:, 0].numpy(), K[:, 0].numpy(), V[:, 0].numpy(), roles, seq=seq,
+                        scale=1 / np.sqrt(d), kind="topk", k=k)
+    for g in range(H):
+        np.testing.assert_array_equal(sets[g], r["sets"][g])
+    assert rel_err(out[:, 0].cpu().numpy(), r["out"]) < FP32_TOL
