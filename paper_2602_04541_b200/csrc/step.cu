@@ -563,16 +563,10 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
       uint32_t key = 0, idx = 0;
       const bool ok = i < ns && get(i, key, idx);
       const uint32_t pre = key >> shift;  // shift < 32
-      // taken candidates: OR the own-range ones into this item's words; count
-      // per item with one shared atomic per (warp, item) group -- consecutive
-      // slots mostly share an item, and a same-address atomic from 32 lanes
-      // would serialise
+      // taken candidates: counted per item (shared atomic) and OR-ed into this
+      // item's words when in its range
       const bool tk = ok && pre > P;
-      if (tk && (int)idx >= lo && (int)idx < lo + cnt)
-        atomicOr(ws + ((idx - (uint32_t)lo) >> 5), 1u << (idx & 31));
-      const uint32_t titem = tk ? idx / kItemKeys : 0xFFFFFFFFu;
-      const unsigned grp = __match_any_sync(0xffffffffu, titem);
-      if (tk && lane == __ffs(grp) - 1) atomicAdd(&es.selc[titem], (uint32_t)__popc(grp));
+      if (tk) take(idx);
       const bool surv = ok && pre == P;
       const unsigned bal = __ballot_sync(0xffffffffu, surv);
       const uint32_t at = mw + (uint32_t)__popc(bal & ((1u << lane) - 1u));
