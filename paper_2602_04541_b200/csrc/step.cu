@@ -37,6 +37,7 @@ constexpr int kEpiWarps = 2;
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kStepThreads = (kConsumerWarps + kProducerWarps + kEpiWarps) * 32;
 constexpr int kItemKeys = 8192;  // keys per selection item (32 KB, one TMA bulk copy)
+constexpr int kSpec = 2048;     // candidates a resolver loads before it knows the count
 constexpr int kRankMax = 256;    // boundary-bin candidates resolved by direct ranking (per warp list)
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
@@ -339,7 +340,8 @@ __device__ void classify_item(const LycStepParams& p, const SelRow& R, int q, Ep
   const int lo = q * kItemKeys;
   const int cnt = min(kItemKeys, n - lo);
   if (et == 0) {
-    fence_proxy_async();
+    fence_proxy_async();         // earlier generic use of es.buf -> TMA write
+    fence_proxy_async_global();  // consumers' key stores (acquired) -> TMA read
     const uint32_t bytes = (uint32_t)((cnt + 3) & ~3) * 4u;  // key rows are padded to 4
     mbar_arrive_expect_tx(&es.bar, bytes);
     bulk_g2s(es.buf, R.keys + lo, bytes, &es.bar);
@@ -388,6 +390,11 @@ __device__ void classify_item(const LycStepParams& p, const SelRow& R, int q, Ep
   const uint32_t c = __popc(eqm[0]) + __popc(eqm[1]) + __popc(eqm[2]) + __popc(eqm[3]);
   uint32_t total;
   uint32_t pos = epi_scan(c, es.scan, et, total) - c;
+  // this item's block of the row's contiguous candidate array (per-step
+  // counter, reset by the row's last resolver)
+  if (et == 0) es.pad = atomicAdd(R.ctr + 4, total);
+  epi_bar();
+  pos += es.pad;
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
     uint32_t m = eqm[w];
@@ -396,8 +403,8 @@ __device__ void classify_item(const LycStepParams& p, const SelRow& R, int q, Ep
       m &= m - 1;
       const int i = k0 + w * 32 + j;
       const uint32_t key = es.buf[i];
-      R.ckey[lo + pos] = key;
-      R.cidx[lo + pos] = (uint32_t)(lo + i);
+      R.ckey[pos] = key;
+      R.cidx[pos] = (uint32_t)(lo + i);
       atomicAdd(&es.hist[(key >> (shift - 8)) & 255u], 1u);
       ++pos;
     }
@@ -418,12 +425,6 @@ __device__ void classify_item(const LycStepParams& p, const SelRow& R, int q, Ep
     R.ccnt[192] = P;
     R.ccnt[193] = above;
     R.ccnt[194] = (uint32_t)shift;
-    // pad the segment to a multiple of 4 with sentinels (index ~0, key 0: never
-    // ranks above a real candidate) so resolvers can scan padded slots blindly
-    for (uint32_t i = total; i < ((total + 3u) & ~3u); ++i) {
-      R.ckey[lo + i] = 0u;
-      R.cidx[lo + i] = 0xFFFFFFFFu;
-    }
   }
   epi_bar();
   if (et == 0) {
@@ -452,68 +453,63 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
   if (et == 0) spin_until(R.ctr, epoch1 * (uint32_t)items);  // every item classified
   epi_bar();
   if (et == 0) stamp(p, l, EV_F_SCAN, cta);
-  // round 1: the row prefix, counts, this item's definite words
+  // one round: the row prefix and counts, this item's definite words, the
+  // row's sub-histogram and (speculatively) the first kSpec candidates
+  const int cap = (kEpiBufWords / 2) & ~3;  // candidates that fit on chip
+  const int spec = min(kSpec, (int)(p.sel_stride & ~(int64_t)3));
+  uint32_t* skey = es.buf;
+  uint32_t* sidx = es.buf + cap;
+  if (et == 0) {
+    fence_proxy_async();         // earlier generic use of es.buf / es.hist -> TMA write
+    fence_proxy_async_global();  // other CTAs' generic writes -> this TMA read
+    mbar_arrive_expect_tx(&es.bar, 1024u + 8u * (uint32_t)spec);
+    bulk_g2s(es.hist, R.csub, 1024u, &es.bar);
+    bulk_g2s(skey, R.ckey, 4u * (uint32_t)spec, &es.bar);
+    bulk_g2s(sidx, R.cidx, 4u * (uint32_t)spec, &es.bar);
+  }
   uint32_t P = __ldcg(R.ccnt + 192);
   int shift = (int)__ldcg(R.ccnt + 194);
   uint32_t krem = (uint32_t)p.k_sel - __ldcg(R.ccnt + 193);
-  const uint32_t c_mine = et < items ? __ldcg(R.ccnt + et) : 0u;
+  const int ns = (int)__ldcg(R.ctr + 4);  // candidates of the row
   const uint32_t d_mine = et < items ? __ldcg(R.ccnt + 64 + et) : 0u;
   const int w0 = lo / 32 + et * 4;  // this thread's 4 words (128 keys)
   uint4 wv4 = make_uint4(0u, 0u, 0u, 0u);
   if (et * 128 < cnt) wv4 = __ldcg(reinterpret_cast<const uint4*>(R.bitmap + bm_pad(w0)));
   uint32_t* ws = es.hist + 1792;  // [256] this item's words on chip
   reinterpret_cast<uint4*>(ws)[et] = wv4;
-  const uint32_t c_pad = (c_mine + 3) & ~3u;
-  uint32_t padded;
-  const uint32_t incl = epi_scan(c_pad, es.scan, et, padded);
-  if (et < items) {
-    es.seg[et] = incl - c_pad;
-    es.cnt[et] = c_mine;
-    es.defc[et] = d_mine;
-  }
+  if (et < items) es.defc[et] = d_mine;
   if (et < 64) es.selc[et] = 0u;
-  const int cap = (kEpiBufWords / 2) & ~3;  // candidates that fit on chip
-  const bool on_chip = (int)padded <= cap;
-  uint32_t* skey = es.buf;
-  uint32_t* sidx = es.buf + cap;
-  epi_bar();
-  // round 2: candidates and the 256-bin sub-histogram, all copies in flight at once
-  if (et == 0) {
-    fence_proxy_async();
-    mbar_arrive_expect_tx(&es.bar, 1024u + (on_chip ? padded * 8u : 0u));
-    bulk_g2s(es.hist, R.csub, 1024u, &es.bar);
-    if (on_chip)
-      for (int qq = 0; qq < items; ++qq) {
-        const uint32_t b = ((es.cnt[qq] + 3) & ~3u) * 4u;
-        if (b) {
-          bulk_g2s(skey + es.seg[qq], R.ckey + (size_t)qq * kItemKeys, b, &es.bar);
-          bulk_g2s(sidx + es.seg[qq], R.cidx + (size_t)qq * kItemKeys, b, &es.bar);
-        }
-      }
-  }
+  const bool on_chip = ns <= cap;
   mbar_wait(&es.bar, bar_phase);
   bar_phase ^= 1u;
+  if (on_chip && ns > spec) {  // the rest of the candidates
+    epi_bar();
+    if (et == 0) {
+      const uint32_t rest = (uint32_t)(((ns + 3) & ~3) - spec) * 4u;
+      mbar_arrive_expect_tx(&es.bar, 2u * rest);
+      bulk_g2s(skey + spec, R.ckey + spec, rest, &es.bar);
+      bulk_g2s(sidx + spec, R.cidx + spec, rest, &es.bar);
+    }
+    mbar_wait(&es.bar, bar_phase);
+    bar_phase ^= 1u;
+  }
   if (et == 0) {
     stamp(p, l, EV_SEL2, cta);
     // the last item to take its copy of the shared row state resets it for
-    // the next use of this parity (h1, the sub-histogram; block mode: keys);
-    // ordered before this CTA's CTR_SELDONE signal, which layer l + 2 waits for
+    // the next use (h1, the sub-histogram, the candidate counter; block mode:
+    // keys); ordered before this CTA's CTR_SELDONE signal
     const uint32_t old = atom_add_acq_rel(R.ctr + 8, 1u);
     es.last = old == epoch1 * (uint32_t)items - 1u;
   }
-  const int ns = (int)padded;
   auto get = [&](int i, uint32_t& key, uint32_t& idx) -> bool {
+    if (i >= ns) return false;
     if (on_chip) {
       key = skey[i];
       idx = sidx[i];
-      return idx != 0xFFFFFFFFu;
+    } else {
+      key = __ldcg(R.ckey + i);
+      idx = __ldcg(R.cidx + i);
     }
-    int qq = 0;
-    while (qq + 1 < items && (uint32_t)i >= es.seg[qq + 1]) ++qq;
-    const uint32_t off = (uint32_t)i - es.seg[qq];
-    if (off >= es.cnt[qq]) return false;
-    key = __ldcg(R.ckey + (size_t)qq * kItemKeys + off);
-    idx = __ldcg(R.cidx + (size_t)qq * kItemKeys + off);
     return true;
   };
   auto take = [&](uint32_t idx) {
@@ -525,6 +521,7 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
     if (R.h1)
       for (int b = et; b < LYC_H1_ROW; b += kEpiThreads) R.h1[b] = 0u;
     for (int b = et; b < 256; b += kEpiThreads) R.csub[b] = 0u;
+    if (et == 0) R.ctr[4] = 0u;
     if (p.sel_mode == SEL_BLOCK_KEYS)
       for (int i = et; i < n; i += kEpiThreads) R.keys[i] = 0u;
   }
@@ -600,18 +597,33 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
       if (rank < krem) take(xi);
     }
   } else {
-    // (only with shift == 0) more than kRankMax copies of one key: the first
-    // krem in index order (slot order is index order)
-    uint32_t tie_run = 0;
-    for (int b0 = 0; b0 < ns; b0 += kEpiThreads) {
-      const int i = b0 + et;
-      uint32_t key = 0, idx = 0;
-      const bool ok = i < ns && get(i, key, idx);
-      const bool is_eq = ok && key == P;
-      uint32_t tot;
-      const uint32_t inc = epi_scan(is_eq ? 1u : 0u, es.scan, et, tot);
-      if (is_eq && tie_run + inc - 1u < krem) take(idx);
-      tie_run += tot;
+    // (only with shift == 0) more than kRankMax copies of one key: the krem
+    // LOWEST indices among them (attention.hpp:117-118), by a radix select on
+    // kp = 0xFFFFF - idx (largest kp = smallest index; idx < 2^20)
+    uint32_t Pi = 0, kr = krem;
+    int sh = 20;
+    while (sh > 0) {
+      const int wbits = sh > 8 ? 8 : sh;
+      sh -= wbits;
+      const uint32_t mask = (1u << wbits) - 1u;
+      epi_bar();
+      for (int b = et; b < (1 << wbits); b += kEpiThreads) es.hist[b] = 0u;
+      epi_bar();
+      for (int i = et; i < ns; i += kEpiThreads) {
+        uint32_t key, idx;
+        if (get(i, key, idx) && key == P) {
+          const uint32_t kp = 0xFFFFFu - idx;
+          if ((kp >> (sh + wbits)) == Pi) atomicAdd(&es.hist[(kp >> sh) & mask], 1u);
+        }
+      }
+      epi_bar();
+      epi_digit(es, es.hist, false, 1 << wbits, kr, et);
+      Pi = (Pi << wbits) | es.digit;
+      kr -= es.above;
+    }
+    for (int i = et; i < ns; i += kEpiThreads) {
+      uint32_t key, idx;
+      if (get(i, key, idx) && key == P && 0xFFFFFu - idx >= Pi) take(idx);
     }
   }
   epi_bar();
