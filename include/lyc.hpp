@@ -36,6 +36,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -546,6 +547,82 @@ class HybridDecoder {
  private:
   Config cfg_;
   lyc_decoder* d_ = nullptr;
+};
+
+// KV-sequence sharding across GPUs (lyc_shard_layer / lyc_shard_merge): this
+// rank holds rows [row_begin, row_begin + n_local) of every head's cache.
+// Per layer: local partials + local top-k candidates into this rank's packed
+// block, the caller's all-gather of every rank's block (rank order; e.g. one
+// ncclAllGather), then the identical rank-ordered merge + global top-k.
+class ShardedDecoder {
+ public:
+  // exchange(send, recv, words): gather `words` 4-byte words from every rank
+  // into recv[rank * words ...] (device pointers, stream ordered)
+  using Exchange = std::function<void(const float* send, float* recv, std::size_t words)>;
+
+  ShardedDecoder(const HybridDecoder::Config& c, std::span<const std::uint8_t> roles, int world,
+                 int rank, Exchange exchange)
+      : dec_(c, roles), cfg_(c), world_(world), rank_(rank), exchange_(std::move(exchange)) {
+    if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("shard: bad world/rank");
+    int32_t *ids = nullptr, *counts = nullptr;
+    check(lyc_decoder_index_cache(dec_.handle(), &ids, &counts, &k_cap_));
+    rows_ = (std::size_t)c.batch * c.n_kv_heads * c.group_size;
+    bh_ = (std::size_t)c.batch * c.n_kv_heads;
+    off_lse_ = rows_ * c.d_head;
+    off_key_ = off_lse_ + rows_;
+    off_idx_ = off_key_ + bh_ * (std::size_t)k_cap_;
+    words_ = (off_idx_ + bh_ * (std::size_t)k_cap_ + 3) / 4 * 4;
+    send_ = DeviceBuffer(words_ * 4);
+    recv_ = DeviceBuffer(words_ * 4 * (std::size_t)world);
+  }
+
+  // Step 1 of a layer: this rank's partials + local top-k candidates into its
+  // packed send block (send(), block_words() 4-byte words).
+  void layer_local(int l, const void* q_l, const void* k, const void* v, std::size_t n_local,
+                   std::size_t row_begin, cudaStream_t st = nullptr) {
+    float* sb = send_.as<float>();
+    check(lyc_shard_layer(dec_.handle(), l, q_l, k, v, (int64_t)n_local, (int64_t)row_begin, sb,
+                          sb + off_lse_, reinterpret_cast<uint32_t*>(sb + off_key_),
+                          reinterpret_cast<int32_t*>(sb + off_idx_), st));
+  }
+  // Step 3 of a layer (after the all-gather of every rank's block into
+  // `gathered`, rank order): identical on every rank.
+  void layer_combine(int l, const float* gathered, std::size_t n_local, std::size_t row_begin,
+                     std::size_t seq_total, void* out_l, int32_t* global_sets = nullptr,
+                     cudaStream_t st = nullptr) {
+    check(lyc_shard_merge(dec_.handle(), l, world_, gathered, gathered + off_lse_,
+                          reinterpret_cast<const uint32_t*>(gathered + off_key_),
+                          reinterpret_cast<const int32_t*>(gathered + off_idx_), (int64_t)words_,
+                          (int64_t)n_local, (int64_t)row_begin, (int64_t)seq_total, out_l,
+                          global_sets, st));
+  }
+
+  // One decode step: q/out [L][B][Hq][d] (identical q on every rank), k/v this
+  // rank's [L][B][H][seq_cap][d] with local row 0 = global row row_begin.
+  void decode_step(const void* q, const void* k, const void* v, std::size_t n_local,
+                   std::size_t row_begin, std::size_t seq_total, void* out, cudaStream_t st = nullptr) {
+    const std::size_t esz = cfg_.dtype == Dtype::BF16 ? 2 : 4;
+    const std::size_t qstride = rows_ * cfg_.d_head * esz;
+    for (int l = 0; l < cfg_.n_layers; ++l) {
+      layer_local(l, static_cast<const char*>(q) + l * qstride, k, v, n_local, row_begin, st);
+      exchange_(send_.as<float>(), recv_.as<float>(), words_);
+      layer_combine(l, recv_.as<float>(), n_local, row_begin, seq_total,
+                    static_cast<char*>(out) + l * qstride, nullptr, st);
+    }
+  }
+
+  const float* send() const { return send_.as<float>(); }
+  HybridDecoder& local() { return dec_; }
+  std::size_t block_words() const { return words_; }
+
+ private:
+  HybridDecoder dec_;
+  HybridDecoder::Config cfg_;
+  int world_, rank_;
+  Exchange exchange_;
+  int64_t k_cap_ = 0;
+  std::size_t rows_ = 0, bh_ = 0, off_lse_ = 0, off_key_ = 0, off_idx_ = 0, words_ = 0;
+  DeviceBuffer send_, recv_;
 };
 
 }  // namespace lyc

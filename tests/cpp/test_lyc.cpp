@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <functional>
+#include <memory>
 #include <numeric>
 #include <random>
 #include <string>
@@ -303,6 +304,71 @@ static void test_hybrid_decoder_errors() {
   CHECK(lyc::fraction_budget(0.1, 100) == 10);
 }
 
+// Sequence sharding over P = 2 ranks emulated on one GPU: each rank's
+// exchange copies its block into a shared gathered buffer; the step runs rank
+// by rank per layer (local work of both ranks, then both combines), so the
+// result must equal the unsharded decoder.
+static void test_sharded_decoder_two_ranks() {
+  const int NL = 2, H = 2, G = 4, d = 64, L = 3000, K = 128, P = 2;
+  std::vector<uint8_t> roles{0, 0, 1, 0};
+  std::mt19937_64 rng(99);
+  std::uniform_real_distribution<float> U(-1.f, 1.f);
+  std::vector<float> q((size_t)NL * H * G * d), k((size_t)NL * H * L * d), v(k.size());
+  for (auto* vec : {&q, &k, &v})
+    for (auto& x : *vec) x = U(rng);
+  lyc::DeviceBuffer dq(q.size() * 4), dk(k.size() * 4), dv(v.size() * 4), dref(q.size() * 4);
+  dq.upload(q.data(), q.size() * 4);
+  dk.upload(k.data(), k.size() * 4);
+  dv.upload(v.data(), v.size() * 4);
+  lyc::HybridDecoder::Config c;
+  c.n_layers = NL;
+  c.n_kv_heads = H;
+  c.group_size = G;
+  c.d_head = d;
+  c.dtype = lyc::Dtype::F32;
+  c.seq_cap = L;
+  c.policy = lyc::SparsityPolicy::top_k(K);
+  lyc::HybridDecoder full(c, roles);
+  full.decode_step(dq.get(), dk.get(), dv.get(), L, dref.get());
+  std::vector<float> ref(q.size());
+  cudaDeviceSynchronize();
+  dref.download(ref.data(), ref.size() * 4);
+  // two ranks, rows [0, 1500) and [1500, 3000): their caches are views of the
+  // full cache at the same slab stride (seq_cap = L); one shared gathered
+  // buffer stands in for the all-gather
+  const size_t half = L / 2;
+  std::vector<std::unique_ptr<lyc::ShardedDecoder>> ranks;
+  for (int r = 0; r < P; ++r)
+    ranks.push_back(std::make_unique<lyc::ShardedDecoder>(c, roles, P, r, nullptr));
+  const size_t words = ranks[0]->block_words();
+  lyc::DeviceBuffer gathered(words * 4 * P), d0(q.size() * 4), d1(q.size() * 4);
+  const size_t qstride = (size_t)H * G * d;
+  for (int l = 0; l < NL; ++l) {
+    for (int r = 0; r < P; ++r) {
+      const float* kr = dk.as<float>() + r * half * d;
+      const float* vr = dv.as<float>() + r * half * d;
+      ranks[r]->layer_local(l, dq.as<float>() + l * qstride, kr, vr, half, r * half);
+      cudaMemcpy(gathered.as<float>() + r * words, ranks[r]->send(), words * 4, cudaMemcpyDeviceToDevice);
+    }
+    for (int r = 0; r < P; ++r)
+      ranks[r]->layer_combine(l, gathered.as<float>(), half, r * half, L,
+                              (r ? d1 : d0).as<float>() + l * qstride);
+  }
+  std::vector<float> o0(q.size()), o1(q.size());
+  cudaDeviceSynchronize();
+  d0.download(o0.data(), o0.size() * 4);
+  d1.download(o1.data(), o1.size() * 4);
+  double worst = 0, mx = 0;
+  for (size_t i = 0; i < ref.size(); ++i) {
+    worst = std::max(worst, (double)std::abs(o0[i] - ref[i]));
+    mx = std::max(mx, (double)std::abs(ref[i]));
+  }
+  std::printf("  sharded x2: rel err vs unsharded %.3g (bar 1e-5), ranks bitwise equal: %s\n",
+              worst / std::max(mx, 1e-3), o0 == o1 ? "yes" : "NO");
+  CHECK(worst / std::max(mx, 1e-3) < 1e-5);
+  CHECK(o0 == o1);
+}
+
 int main() {
   const std::pair<const char*, std::function<void()>> tests[] = {
       {"PlanSplits.KnownAnswersAndErrors", test_plan_splits_known},
@@ -312,6 +378,7 @@ int main() {
       {"ArgsTopK.KnownCasesTiesAndSort", test_args_top_k},
       {"HybridDecoder.TinyStepMatchesHostLoop", test_hybrid_decoder_tiny},
       {"HybridDecoder.Errors", test_hybrid_decoder_errors},
+      {"ShardedDecoder.TwoRanksEqualUnsharded", test_sharded_decoder_two_ranks},
   };
   for (const auto& [name, fn] : tests) {
     const int before = g_fail;
