@@ -363,19 +363,25 @@ __device__ __forceinline__ void unit_epilogue(const LycView& p, const LycSlot& s
                 "histogram flush mapping");
   if (hist_g) {
     // flush the unit's first-pass histogram and re-zero it: thread t owns 32
-    // consecutive bins (rotated reads, conflict-free); the 64-bin coarse
-    // summary (top 6 bits) that follows the fine bins in the global row gets
-    // one atomic per non-empty coarse bin (thread pairs share one)
+    // consecutive bins, read and re-zeroed as eight 16-B vectors in a rotated
+    // order (conflict-free), then one predicated global atomic per non-empty
+    // bin; the 64-bin coarse summary (top 6 bits) after the fine bins gets one
+    // atomic per non-empty coarse bin (thread pairs share one)
+    uint4* hv = reinterpret_cast<uint4*>(hist_s + tid * 32);
+    uint4 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = hv[(j + tid) & 7];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) hv[(j + tid) & 7] = make_uint4(0u, 0u, 0u, 0u);
     uint32_t sum = 0;
-#pragma unroll 4
-    for (int i = 0; i < 32; ++i) {
-      const int b = tid * 32 + ((i + tid) & 31);
-      const uint32_t c = hist_s[b];
-      if (c) {
-        atomicAdd(hist_g + b, c);
-        hist_s[b] = 0u;
-        sum += c;
-      }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t* g = hist_g + tid * 32 + ((j + tid) & 7) * 4;
+      if (v[j].x) atomicAdd(g, v[j].x);
+      if (v[j].y) atomicAdd(g + 1, v[j].y);
+      if (v[j].z) atomicAdd(g + 2, v[j].z);
+      if (v[j].w) atomicAdd(g + 3, v[j].w);
+      sum += v[j].x + v[j].y + v[j].z + v[j].w;
     }
     sum += __shfl_xor_sync(0xffffffffu, sum, 1);
     if ((tid & 1) == 0 && sum) atomicAdd(hist_g + LYC_H1_BINS + (tid >> 1), sum);
@@ -480,9 +486,11 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
       }
     }
     float m0 = -INFINITY, l0 = 0.f;
-    float o[NT][2];
+    // full m16n8 C fragments, accumulated in place: entries [2], [3] (rows
+    // 8..15 of the A operand, which are zero) stay 0 and are never read
+    float o[NT][4];
 #pragma unroll
-    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = 0.f;
+    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
     const bool want_sel = s.sel >= 0 && p.sel_mode != SEL_NONE;
     uint32_t* hist = (want_sel && p.hist1) ? p.hist1 + (int64_t)s.sel * LYC_H1_ROW : nullptr;
 
@@ -584,14 +592,8 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
           uint32_t b0, b1, b2, b3;
           const int c = 2 * (n2 & 3) + v_x;
           ldsm_x4_t(b0, b1, b2, b3, vs + (n2 >> 2) * C::kPanelBytes + v_row + ((c ^ sw) << 4));
-          float c0[4] = {o[2 * n2][0], o[2 * n2][1], 0.f, 0.f};
-          float c1[4] = {o[2 * n2 + 1][0], o[2 * n2 + 1][1], 0.f, 0.f};
-          mma_bf16(c0, pa0, 0u, pa2, 0u, b0, b1);
-          mma_bf16(c1, pa0, 0u, pa2, 0u, b2, b3);
-          o[2 * n2][0] = c0[0];
-          o[2 * n2][1] = c0[1];
-          o[2 * n2 + 1][0] = c1[0];
-          o[2 * n2 + 1][1] = c1[1];
+          mma_bf16(o[2 * n2], pa0, 0u, pa2, 0u, b0, b1);
+          mma_bf16(o[2 * n2 + 1], pa0, 0u, pa2, 0u, b2, b3);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[stage]);
