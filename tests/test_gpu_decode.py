@@ -340,3 +340,25 @@ def test_fused_step_exact_ties_lowest_index(orc, n_ties):
     for g in range(H):
         np.testing.assert_array_equal(sets[g], r["sets"][g])
     assert rel_err(out[:, 0].cpu().numpy(), r["out"]) < FP32_TOL
+
+
+def test_fused_step_batch4_many_items_per_cta(orc):
+    """Batch 4 x 8 KV heads, 40K context: layer 0 has 32 selection rows x 5
+    items = 160 items for 148 CTAs (several items per CTA, no role split);
+    later layers use the split roles.  Every batch item against the oracle."""
+    import paper_2602_04541_b200 as P
+    NL, B, H, G, d, seq, k = 3, 4, 8, 4, 128, 40000, 2048
+    roles = roles_for(NL, H, [(1, 2), (2, 5), (2, 7)])
+    dec, q, K, V, out, _ = run_case(orc, NL=NL, B=B, H=H, G=G, d=d, seq=seq, seq_cap=seq,
+                                    dtype=torch.bfloat16, roles=roles,
+                                    policy=P.SparsityPolicy.top_k(k), seed=31)
+    assert dec.fused
+    sets = dec.token_sets()
+    for b in range(B):
+        r = orc.decode_step(q[:, b], K[:, b], V[:, b], roles, seq=seq, scale=1 / np.sqrt(d),
+                            kind="topk", k=k)
+        assert rel_err(out[:, b], r["out"]) < BF16_TOL
+        for g in range(H):
+            src = max(l for l in range(NL) if roles[l, g] == 0)
+            sc = pooled_scores(q[src, b], K[src, b, g], G, g, seq)
+            check_set(sets[b][g], r["sets"][g], sc, k)
