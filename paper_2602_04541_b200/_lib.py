@@ -6,9 +6,13 @@ shared object is missing the import fails loudly with the build command.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "liblyc.so"
+# A/B measurement of an alternative in-tree build (debug scripts only)
+if os.environ.get("LYC_LIB_VARIANT"):
+    LIB_PATH = LIB_PATH.with_name("liblyc_" + os.environ["LYC_LIB_VARIANT"] + ".so")
 
 LYC_OK, LYC_EINVAL, LYC_ESTATE, LYC_ECUDA, LYC_ENOTSUP, LYC_ENCCL = 0, -1, -2, -3, -4, -5
 DTYPE_F32, DTYPE_BF16 = 0, 1

@@ -312,16 +312,31 @@ __device__ __forceinline__ SelRow sel_row(const LycStepParams& p, int l, int r) 
 __device__ __forceinline__ void row_prefix(const LycStepParams& p, const SelRow& R, EpiSmem& es,
                                            int et) {
   if (R.h1) {
-    // two dependent L2 reads: the 64 coarse bins, then the 64 fine bins of
-    // the chosen coarse bin
+    // two coalesced L2 reads by warp 0: the 64 coarse bins, then the 64 fine
+    // bins of the chosen coarse bin (lane i holds bins 2(31-i), 2(31-i)+1)
     if (et < 32) {
-      const uint32_t k = (uint32_t)p.k_sel;
-      uint32_t cd, ca, fd, fa;
-      find_digit(R.h1 + LYC_H1_BINS, LYC_H1_COARSE, k, cd, ca, et, true);
-      find_digit(R.h1 + cd * 64, 64, k - ca, fd, fa, et, true);
+      uint32_t k = (uint32_t)p.k_sel, base = 0, above = 0;
+      const uint32_t* h = R.h1 + LYC_H1_BINS;
+#pragma unroll
+      for (int level = 0; level < 2; ++level) {
+        const uint2 v = __ldcg(reinterpret_cast<const uint2*>(h) + (31 - et));
+        const uint32_t sum = v.x + v.y;
+        const uint32_t incl = warp_incl_scan(sum, et);
+        const unsigned who = __ballot_sync(0xffffffffu, incl - sum < k && k <= incl);
+        const int L = who ? __ffs(who) - 1 : 31;
+        const uint32_t ex = __shfl_sync(0xffffffffu, incl - sum, L);
+        const uint32_t hi = __shfl_sync(0xffffffffu, v.y, L);
+        const bool upper = k <= ex + hi;
+        const uint32_t bin = 2u * (31u - (uint32_t)L) + (upper ? 1u : 0u);
+        const uint32_t a = upper ? ex : ex + hi;
+        above += a;
+        k -= a;
+        base = level == 0 ? bin * 64u : base + bin;
+        h = R.h1 + bin * 64u;
+      }
       if (et == 0) {
-        es.digit = cd * 64 + fd;
-        es.above = ca + fa;
+        es.digit = base;
+        es.above = above;
       }
     }
     epi_bar();
@@ -467,6 +482,11 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
     bulk_g2s(skey, R.ckey, 4u * (uint32_t)spec, &es.bar);
     bulk_g2s(sidx, R.cidx, 4u * (uint32_t)spec, &es.bar);
   }
+  if (R.h1) {  // every item has read the row's first-pass histogram: item q re-zeroes its share
+    const int per = (LYC_H1_ROW + items - 1) / items;
+    const int b1 = min(LYC_H1_ROW, (q + 1) * per);
+    for (int b = q * per + et; b < b1; b += kEpiThreads) R.h1[b] = 0u;
+  }
   uint32_t P = __ldcg(R.ccnt + 192);
   int shift = (int)__ldcg(R.ccnt + 194);
   uint32_t krem = (uint32_t)p.k_sel - __ldcg(R.ccnt + 193);
@@ -478,7 +498,7 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
   uint32_t* ws = es.hist + 1792;  // [256] this item's words on chip
   reinterpret_cast<uint4*>(ws)[et] = wv4;
   if (et < items) es.defc[et] = d_mine;
-  if (et < 64) es.selc[et] = 0u;
+  if (et == 0) es.scan[46] = 0u;
   const bool on_chip = ns <= cap;
   mbar_wait(&es.bar, bar_phase);
   bar_phase ^= 1u;
@@ -512,14 +532,14 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
     }
     return true;
   };
+  // a selected candidate: counted when it precedes this item (output offset),
+  // OR-ed into this item's words when inside it
   auto take = [&](uint32_t idx) {
-    atomicAdd(&es.selc[idx / kItemKeys], 1u);
-    if ((int)idx >= lo && (int)idx < lo + cnt) atomicOr(ws + ((idx - (uint32_t)lo) >> 5), 1u << (idx & 31));
+    if ((int)idx < lo) atomicAdd(&es.scan[46], 1u);
+    else if ((int)idx < lo + cnt) atomicOr(ws + ((idx - (uint32_t)lo) >> 5), 1u << (idx & 31));
   };
   epi_digit(es, es.hist, false, 256, krem, et);  // ends with epi_bar: es.last visible
   if (es.last) {
-    if (R.h1)
-      for (int b = et; b < LYC_H1_ROW; b += kEpiThreads) R.h1[b] = 0u;
     for (int b = et; b < 256; b += kEpiThreads) R.csub[b] = 0u;
     if (et == 0) R.ctr[4] = 0u;
     if (p.sel_mode == SEL_BLOCK_KEYS)
@@ -550,30 +570,43 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
     live = es.hist[es.digit];
   }
   epi_bar();
-  // one scan: take everything above the prefix, compact the survivors (per-warp
-  // ballot lists at es.hist + 256 + w * 3 * kRankMax: keys | ids)
+  // one scan: take everything above the prefix (count the ones before this
+  // item, OR in its own), compact the survivors (per-warp ballot lists at
+  // es.hist + 256 + w * 3 * kRankMax: keys | ids); four loads in flight
   {
     uint32_t* lk = es.hist + 256 + ew * 3 * kRankMax;
-    uint32_t mw = 0;
-    for (int i0 = ew * 32; i0 < ns; i0 += kEpiThreads) {
-      const int i = i0 + lane;
-      uint32_t key = 0, idx = 0;
-      const bool ok = i < ns && get(i, key, idx);
-      const uint32_t pre = key >> shift;  // shift < 32
-      // taken candidates: counted per item (shared atomic) and OR-ed into this
-      // item's words when in its range
-      const bool tk = ok && pre > P;
-      if (tk) take(idx);
-      const bool surv = ok && pre == P;
-      const unsigned bal = __ballot_sync(0xffffffffu, surv);
-      const uint32_t at = mw + (uint32_t)__popc(bal & ((1u << lane) - 1u));
-      if (surv && at < (uint32_t)kRankMax) {
-        lk[at] = key;
-        lk[kRankMax + at] = idx;
+    uint32_t mw = 0, before = 0;
+    constexpr int U = 4;
+    for (int i0 = ew * 32; i0 < ns; i0 += kEpiThreads * U) {
+      uint32_t key[U], idx[U];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        key[u] = 0u;
+        idx[u] = 0u;
+        ok[u] = get(i0 + u * kEpiThreads + lane, key[u], idx[u]);
       }
-      mw += (uint32_t)__popc(bal);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t pre = key[u] >> shift;  // shift < 32
+        const bool tk = ok[u] && pre > P;
+        before += (uint32_t)__popc(__ballot_sync(0xffffffffu, tk && (int)idx[u] < lo));
+        if (tk && (int)idx[u] >= lo && (int)idx[u] < lo + cnt)
+          atomicOr(ws + ((idx[u] - (uint32_t)lo) >> 5), 1u << (idx[u] & 31));
+        const bool surv = ok[u] && pre == P;
+        const unsigned bal = __ballot_sync(0xffffffffu, surv);
+        const uint32_t at = mw + (uint32_t)__popc(bal & ((1u << lane) - 1u));
+        if (surv && at < (uint32_t)kRankMax) {
+          lk[at] = key[u];
+          lk[kRankMax + at] = idx[u];
+        }
+        mw += (uint32_t)__popc(bal);
+      }
     }
-    if (lane == 0) es.scan[40 + ew] = mw;
+    if (lane == 0) {
+      es.scan[40 + ew] = mw;
+      es.scan[44 + ew] = before;
+    }
   }
   epi_bar();
   const uint32_t m0 = es.scan[40], m1 = es.scan[41];
@@ -630,12 +663,13 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
   if (et == 0) stamp(p, l, EV_SEL0, cta);
   // this item's output offset: definite keys + selected candidates of the
   // items before it
-  const uint32_t n_q = et < items ? es.defc[et] + es.selc[et] : 0u;
+  const uint32_t n_q = et < items ? es.defc[et] : 0u;
+  const uint32_t taken_before = es.scan[44] + es.scan[45] + es.scan[46];
   uint32_t tot;
   const uint32_t end_q = epi_scan(n_q, es.scan, et, tot);
   if (et == q) es.pad = end_q - n_q;
   epi_bar();
-  const uint32_t out0 = es.pad;
+  const uint32_t out0 = es.pad + taken_before;
   const uint4 v = reinterpret_cast<const uint4*>(ws)[et];
   uint32_t wv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
