@@ -379,25 +379,33 @@ __device__ void classify_item(const LycStepParams& p, const SelRow& R, int q, Ep
   bar_phase ^= 1u;
   if (et == 0) stamp(p, l, EV_C_KEYS, cta);
   // thread et owns 128 consecutive keys = 4 bitmap words, read as rotated 16-B
-  // vectors (conflict-free)
-  uint32_t words[4] = {0u, 0u, 0u, 0u}, eqm[4] = {0u, 0u, 0u, 0u};
+  // vectors (conflict-free).  Threshold compares against the prefix's key
+  // range [T0, T1m]; bits are set at static positions (predicated ORs) and the
+  // words rotated once at the end; the tail item's words are masked after.
+  const uint32_t T0 = P << shift;
+  const uint32_t T1m = T0 | ((1u << shift) - 1u);  // largest key with prefix P
+  uint32_t words[4], eqm[4];
   const int k0 = et * 128;
+  const int rot = 4 * (et & 7);
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
+    uint32_t ta = 0u, tg = 0u;
 #pragma unroll
     for (int qv = 0; qv < 8; ++qv) {
-      const int qq = (qv + et) & 7;
-      const uint4 v = reinterpret_cast<const uint4*>(es.buf + k0 + w * 32)[qq];
+      const uint4 v = reinterpret_cast<const uint4*>(es.buf + k0 + w * 32)[(qv + et) & 7];
       const uint32_t kv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int j = qq * 4 + e;
-        const bool ok = k0 + w * 32 + j < cnt;
-        const uint32_t pre = kv[e] >> shift;
-        words[w] |= (ok && pre > P) ? (1u << j) : 0u;
-        eqm[w] |= (ok && pre == P) ? (1u << j) : 0u;
+        if (kv[e] > T1m) ta |= 1u << (qv * 4 + e);
+        if (kv[e] >= T0) tg |= 1u << (qv * 4 + e);
       }
     }
+    ta = __funnelshift_l(ta, ta, rot);
+    tg = __funnelshift_l(tg, tg, rot);
+    const int valid = cnt - (k0 + w * 32);
+    const uint32_t vm = valid >= 32 ? 0xffffffffu : valid <= 0 ? 0u : (1u << valid) - 1u;
+    words[w] = ta & vm;
+    eqm[w] = tg & ~ta & vm;
   }
 #pragma unroll
   for (int w = 0; w < 4; ++w)
@@ -515,11 +523,6 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
   }
   if (et == 0) {
     stamp(p, l, EV_SEL2, cta);
-    // the last item to take its copy of the shared row state resets it for
-    // the next use (h1, the sub-histogram, the candidate counter; block mode:
-    // keys); ordered before this CTA's CTR_SELDONE signal
-    const uint32_t old = atom_add_acq_rel(R.ctr + 8, 1u);
-    es.last = old == epoch1 * (uint32_t)items - 1u;
   }
   auto get = [&](int i, uint32_t& key, uint32_t& idx) -> bool {
     if (i >= ns) return false;
@@ -538,13 +541,14 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
     if ((int)idx < lo) atomicAdd(&es.scan[46], 1u);
     else if ((int)idx < lo + cnt) atomicOr(ws + ((idx - (uint32_t)lo) >> 5), 1u << (idx & 31));
   };
-  epi_digit(es, es.hist, false, 256, krem, et);  // ends with epi_bar: es.last visible
-  if (es.last) {
-    for (int b = et; b < 256; b += kEpiThreads) R.csub[b] = 0u;
-    if (et == 0) R.ctr[4] = 0u;
-    if (p.sel_mode == SEL_BLOCK_KEYS)
-      for (int i = et; i < n; i += kEpiThreads) R.keys[i] = 0u;
-  }
+  epi_digit(es, es.hist, false, 256, krem, et);
+  // every thread's reads of the shared row state (count, sub-histogram; bulk
+  // copies complete) are performed (barrier above): count this item's copy
+  // taken.  The last item resets the state for the next use at the end
+  // (before this CTA's CTR_SELDONE signal); the atomic's round trip overlaps
+  // the scan.
+  uint32_t copies = 0;
+  if (et == 0) copies = atomicAdd(R.ctr + 8, 1u);
   P = (P << 8) | es.digit;
   shift -= 8;
   krem -= es.above;
@@ -659,6 +663,7 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
       if (get(i, key, idx) && key == P && 0xFFFFFu - idx >= Pi) take(idx);
     }
   }
+  if (et == 0) es.last = copies == epoch1 * (uint32_t)items - 1u;
   epi_bar();
   if (et == 0) stamp(p, l, EV_SEL0, cta);
   // this item's output offset: definite keys + selected candidates of the
@@ -696,6 +701,12 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
     }
   }
   if (q == 0 && et == 0 && p.idx_count) p.idx_count[row] = p.k_sel;
+  if (es.last) {
+    for (int b = et; b < 256; b += kEpiThreads) R.csub[b] = 0u;
+    if (et == 0) R.ctr[4] = 0u;
+    if (p.sel_mode == SEL_BLOCK_KEYS)
+      for (int i = et; i < n; i += kEpiThreads) R.keys[i] = 0u;
+  }
   epi_bar();
   if (et == 0) {
     stamp(p, l, EV_F_EMIT, cta);
