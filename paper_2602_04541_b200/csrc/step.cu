@@ -821,7 +821,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
       const int total = L.n_merges * chunks;
       uint8_t* outl = static_cast<uint8_t*>(p.out) + (int64_t)l * p.q_layer_stride * esz;
       if (cta < merge_ctas)
-        for (int t = cta * kEpiWarps + ew; t < total; t += merge_ctas * kEpiWarps) {
+        for (int t = ew * merge_ctas + cta; t < total; t += merge_ctas * kEpiWarps) {
           const LycMergeTask tk = L.merges[t / chunks];
           if (lane == 0) spin_until(slot_ctr + (size_t)tk.slot * 16, epoch1 * (uint32_t)tk.n_units);
           __syncwarp();
