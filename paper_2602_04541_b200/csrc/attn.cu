@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) hybrid_attn_kernel(const __gr
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&sm.full[s], kProducerThreads);
+      mbar_init(&sm.full[s], kProducerThreads + 1);  // + the tile-info arrival
       mbar_init(&sm.empty[s], kConsumerWarps);
     }
     fence_mbar_init();
@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) hybrid_attn_kernel(const __gr
       prefetch_tensormap(&p.tmap_k);
       prefetch_tensormap(&p.tmap_v);
     }
-    produce_units<T, D>(p.v, &p.tmap_k, &p.tmap_v, sm.ring, sm.full, sm.empty, ub, ue, pt, stage,
+    produce_units<T, D>(p.v, &p.tmap_k, &p.tmap_v, sm.ring, sm.full, sm.empty, sm.tinfo, ub, ue, pt, stage,
                         phase, NoWaits{});
   } else {
     consume_units<T, D>(p.v, sm, ub, ue, warp, lane, stage, phase);

@@ -85,6 +85,7 @@ struct AttnSmem {
   float* qs;       // fp32 path: staged queries [kMaxG + 1][D]
   uint64_t* full;
   uint64_t* empty;
+  int2* tinfo;     // [kStages] (first row, valid rows) of the tile in each stage, from the producer
   uint8_t* extra;  // kExtraBytes scratch for other warp roles
   uint32_t* hist;  // [LYC_H1_BINS] first radix pass of the unit's selection keys (zero between units)
   uint8_t* ustage; // [kQUnits] unit records staged at layer start (bf16 consumers)
@@ -97,8 +98,8 @@ struct AttnSmem {
   static constexpr int kMlOff = kMoOff + kConsumerWarps * kMaxG * D * 4;
   static constexpr int kQsOff = kMlOff + kConsumerWarps * kMaxG * 3 * 4;  // ml + coef
   static constexpr int kBarOff = kQsOff + AttnCfg<T, D>::kQBytes;
-  static constexpr int kExtraOff =
-      (kBarOff + 2 * AttnCfg<T, D>::kStages * 8 + 127) & ~127;
+  static constexpr int kTinfoOff = kBarOff + 2 * AttnCfg<T, D>::kStages * 8;
+  static constexpr int kExtraOff = (kTinfoOff + AttnCfg<T, D>::kStages * 8 + 127) & ~127;
   static constexpr int kHistOff = kExtraOff + AttnCfg<T, D>::kExtraBytes;
   static constexpr int kUStageOff = kHistOff + AttnCfg<T, D>::kHistBytes;
   static constexpr int kQStageOff = kUStageOff + AttnCfg<T, D>::kUStageBytes;
@@ -117,6 +118,7 @@ struct AttnSmem {
     s.qs = reinterpret_cast<float*>(fx + kQsOff);
     s.full = reinterpret_cast<uint64_t*>(fx + kBarOff);
     s.empty = s.full + C::kStages;
+    s.tinfo = reinterpret_cast<int2*>(fx + kTinfoOff);
     s.extra = fx + kExtraOff;
     s.hist = reinterpret_cast<uint32_t*>(fx + kHistOff);
     s.ustage = fx + kUStageOff;
@@ -137,6 +139,7 @@ struct Tile {
   int32_t lo;            // first row (contiguous tiles)
   int32_t nvalid;        // valid rows in this tile
   const int32_t* ids;    // token ids (gathered tiles) or nullptr
+  int32_t cap;           // gathered tiles: ids readable (list capacity) from ids
 };
 
 __device__ __forceinline__ int tiles_per_item(const LycSlot& s, int bs) {
@@ -148,6 +151,7 @@ __device__ __forceinline__ Tile tile_of(const LycSlot& s, int item, int sub, int
   if (s.kind == ITEM_TOKENS) {
     t.ids = s.list + (int64_t)item * LYC_TILE;
     t.lo = 0;
+    t.cap = s.list_len - item * LYC_TILE;
     const int len = s.count ? min(s.list_len, __ldcg(s.count)) : s.list_len;
     t.nvalid = min(LYC_TILE, len - item * LYC_TILE);
   } else {
@@ -155,6 +159,7 @@ __device__ __forceinline__ Tile tile_of(const LycSlot& s, int item, int sub, int
     const int b0 = blk * bs;
     const int hi = min(b0 + bs, seq);
     t.ids = nullptr;
+    t.cap = 0;
     t.lo = b0 + sub * LYC_TILE;
     t.nvalid = max(0, min(LYC_TILE, hi - t.lo));
   }
@@ -173,7 +178,8 @@ struct NoWaits {
 template <typename T, int D, typename Waits>
 __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMap* tmk,
                                               const CUtensorMap* tmv, uint8_t* ring,
-                                              uint64_t* full, uint64_t* empty, int ub, int ue,
+                                              uint64_t* full, uint64_t* empty, int2* tinfo,
+                                              int ub, int ue,
                                               int pt, int& stage, uint32_t& phase,
                                               const Waits& waits) {
   using C = AttnCfg<T, D>;
@@ -189,13 +195,18 @@ __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMa
   // Row indices (gathered tiles) and block ids (block lists) of the NEXT tile
   // are loaded while the current tile is issued: one L2 round trip per unit
   // instead of one per tile.
+  // (token lists: the id loads are predicated on the list capacity only, so
+  // they overlap the device count's load; rows past the count are masked after)
   auto load_rows = [&](const Tile& t, int* rows) {
     if (t.ids == nullptr && t.nvalid == LYC_TILE) return;
 #pragma unroll
     for (int i = 0; i < kRounds; ++i) {
       const int r = my_r0 + i * kRowsPerRound;
-      rows[i] = r < t.nvalid ? (t.ids ? __ldcg(t.ids + r) : t.lo + r) : -1;
+      rows[i] = t.ids ? (r < t.cap ? __ldcg(t.ids + r) : -1) : t.lo + r;
     }
+#pragma unroll
+    for (int i = 0; i < kRounds; ++i)
+      if (my_r0 + i * kRowsPerRound >= t.nvalid) rows[i] = -1;
   };
   for (int u = ub; u < ue; ++u) {
     const LycUnit un = p.units[u];
@@ -236,6 +247,10 @@ __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMa
         if (t.ids == nullptr && t.nvalid == LYC_TILE) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (pt == 0) {
+            // the tile's rows for the consumers (no global loads on their side);
+            // released by this thread's extra arrival
+            tinfo[stage] = make_int2(t.lo, t.nvalid);
+            mbar_arrive(&full[stage]);
             mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
             if constexpr (C::kSwizzle) {
 #pragma unroll
@@ -255,6 +270,10 @@ __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMa
         } else {
           // gathered / ragged tile: coalesced 16-B cp.async, masked rows zero-filled
           mbar_wait(&empty[stage], phase ^ 1);
+          if (pt == 0) {
+            tinfo[stage] = make_int2(t.lo, t.nvalid);
+            mbar_arrive(&full[stage]);
+          }
 #pragma unroll
           for (int i = 0; i < kRounds; ++i) {
             const int r = my_r0 + i * kRowsPerRound;
@@ -496,8 +515,8 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
 
     for (int it = un.begin; it < un.end; ++it) {
       for (int sub = 0; sub < tpi; ++sub) {
-        const Tile t = tile_of(s, it, sub, p.seq_len, p.block_size);
         mbar_wait(&sm.full[stage], phase);
+        const int2 t = sm.tinfo[stage];  // (first row, valid rows)
         if (first_tile) {
           cstamp(p, 17, tid);
           first_tile = false;
@@ -546,9 +565,9 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
             const float v10 = __shfl_sync(0xffffffffu, ps[1][0], src);
             const float v11 = __shfl_sync(0xffffffffu, ps[1][1], src);
             const float mine = (r >> 3) ? ((r & 1) ? v11 : v10) : ((r & 1) ? v01 : v00);
-            if (lane < 16 && t0 + r < t.nvalid) {
+            if (lane < 16 && t0 + r < t.y) {
               const uint32_t key = float_key(mine);
-              p.sel_keys[(int64_t)s.sel * p.sel_stride + t.lo + t0 + r] = key;
+              p.sel_keys[(int64_t)s.sel * p.sel_stride + t.x + t0 + r] = key;
               if (hist) atomicAdd(sm.hist + (key >> (32 - LYC_H1_BITS)), 1u);
             }
           } else {  // SEL_BLOCK_KEYS: max over valid rows of this block
@@ -557,7 +576,7 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
             for (int n = 0; n < 2; ++n)
 #pragma unroll
               for (int e = 0; e < 2; ++e)
-                if (t0 + n * 8 + qc + e < t.nvalid) km = max(km, float_key(ps[n][e]));
+                if (t0 + n * 8 + qc + e < t.y) km = max(km, float_key(ps[n][e]));
             km = max(km, __shfl_xor_sync(0xffffffffu, km, 1));
             km = max(km, __shfl_xor_sync(0xffffffffu, km, 2));
             if (lane == 0 && km != 0u)
@@ -570,7 +589,7 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
         for (int n = 0; n < 2; ++n)
 #pragma unroll
           for (int e = 0; e < 2; ++e)
-            x[n][e] = t0 + n * 8 + qc + e < t.nvalid ? sc[n][e] * p.scale_log2 : -INFINITY;
+            x[n][e] = t0 + n * 8 + qc + e < t.y ? sc[n][e] * p.scale_log2 : -INFINITY;
         const float mx = warp_max4(fmaxf(fmaxf(x[0][0], x[0][1]), fmaxf(x[1][0], x[1][1])));
         const float mn = fmaxf(m0, mx);
         const float rs = m0 == -INFINITY ? 0.f : fast_exp2(m0 - mn);
@@ -674,8 +693,8 @@ __device__ __forceinline__ void consume_units_f32(const LycView& p, const AttnSm
     consumer_bar();
     for (int it = un.begin; it < un.end; ++it) {
       for (int sub = 0; sub < tpi; ++sub) {
-        const Tile t = tile_of(s, it, sub, p.seq_len, p.block_size);
         mbar_wait(&sm.full[stage], phase);
+        const int2 t = sm.tinfo[stage];  // (first row, valid rows)
         const uint8_t* ks = sm.ring + stage * C::kStageBytes;
         const float* krow = reinterpret_cast<const float*>(ks + (t0 + tr) * C::kRowBytes);
         const uint8_t* vs = ks + C::kTileBytes;
@@ -692,14 +711,14 @@ __device__ __forceinline__ void consume_units_f32(const LycView& p, const AttnSm
         }
 #pragma unroll
         for (int j = 0; j < kMaxG; ++j) sc[j] += __shfl_xor_sync(0xffffffffu, sc[j], 16);
-        const bool valid = t0 + tr < t.nvalid;
+        const bool valid = t0 + tr < t.y;
         if (want_sel) {
           pooled += __shfl_xor_sync(0xffffffffu, pooled, 16);
           if (p.sel_mode == SEL_TOKEN_KEYS) {
             if (half == 0) {
               const uint32_t key = float_key(pooled);
               if (valid) {
-                p.sel_keys[(int64_t)s.sel * p.sel_stride + t.lo + t0 + tr] = key;
+                p.sel_keys[(int64_t)s.sel * p.sel_stride + t.x + t0 + tr] = key;
                 if (hist) atomicAdd(sm.hist + (key >> (32 - LYC_H1_BITS)), 1u);
               }
             }

@@ -729,7 +729,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
   if (threadIdx.x == 0) {
     s_epoch = ld_acquire(ctrl);
     for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&sm.full[s], kProducerThreads);
+      mbar_init(&sm.full[s], kProducerThreads + 1);  // + the tile-info arrival
       mbar_init(&sm.empty[s], kConsumerWarps);
     }
     mbar_init(&es.bar, 1);
@@ -792,7 +792,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
       const LycLayerDesc L = p.layers[l];
       const LycView v = layer_view(p, L, l, esz);
       StepWaits waits{&p, epoch1, l, pt};
-      produce_units<T, D>(v, &p.tmap_k, &p.tmap_v, sm.ring, sm.full, sm.empty,
+      produce_units<T, D>(v, &p.tmap_k, &p.tmap_v, sm.ring, sm.full, sm.empty, sm.tinfo,
                           L.split_off[cell], L.split_off[cell + 1], pt, stage, phase, waits);
     }
   } else {
