@@ -208,9 +208,21 @@ __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMa
     for (int i = 0; i < kRounds; ++i)
       if (my_r0 + i * kRowsPerRound >= t.nvalid) rows[i] = -1;
   };
+  // unit records are prefetched one unit ahead (two dependent loads that
+  // would otherwise stall the ring at every unit start)
+  LycUnit un_next;
+  LycSlot s_next;
+  if (ub < ue) {
+    un_next = p.units[ub];
+    s_next = p.slots[un_next.slot];
+  }
   for (int u = ub; u < ue; ++u) {
-    const LycUnit un = p.units[u];
-    const LycSlot s = p.slots[un.slot];
+    const LycUnit un = un_next;
+    const LycSlot s = s_next;
+    if (u + 1 < ue) {
+      un_next = p.units[u + 1];
+      s_next = p.slots[un_next.slot];
+    }
     waits.unit(s);
     const int tpi = tiles_per_item(s, p.block_size);
     const int row0 = (int)(s.kv_off / D);  // tensor-map row of the slab's row 0
