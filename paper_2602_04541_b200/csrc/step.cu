@@ -52,18 +52,18 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   return v;
 }
 
-// Grid-level wait on a monotonic counter: relaxed polls (no L1 invalidation
-// per poll), one acquire fence once the target is reached.  Traps after ~20 s
+// Grid-level wait on a monotonic counter (acquire loads).  Traps after ~20 s
 // (a lost signal is a bug -- fail the launch instead of hanging the GPU).
 __device__ __forceinline__ void spin_until(const uint32_t* ctr, uint32_t target) {
-  if ((int)(ld_relaxed(ctr) - target) < 0) {
+  // acquire polls: no trailing fence (a fence would also wait for this
+  // thread's own outstanding stores and copies)
+  if ((int)(ld_acquire(ctr) - target) < 0) {
     const long long t0 = clock64();
-    while ((int)(ld_relaxed(ctr) - target) < 0) {
+    while ((int)(ld_acquire(ctr) - target) < 0) {
       __nanosleep(64);
       if (clock64() - t0 > 40000000000LL) __trap();
     }
   }
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
 __device__ __forceinline__ void group_bar(int id, int n) {
