@@ -86,6 +86,7 @@ struct AttnSmem {
   uint64_t* full;
   uint64_t* empty;
   int2* tinfo;     // [kStages] (first row, valid rows) of the tile in each stage, from the producer
+  uint32_t* clayer;  // step kernel: 1 + the layer the consumers have started (they passed its wait)
   uint8_t* extra;  // kExtraBytes scratch for other warp roles
   uint32_t* hist;  // [LYC_H1_BINS] first radix pass of the unit's selection keys (zero between units)
   uint8_t* ustage; // [kQUnits] unit records staged at layer start (bf16 consumers)
@@ -99,7 +100,8 @@ struct AttnSmem {
   static constexpr int kQsOff = kMlOff + kConsumerWarps * kMaxG * 3 * 4;  // ml + coef
   static constexpr int kBarOff = kQsOff + AttnCfg<T, D>::kQBytes;
   static constexpr int kTinfoOff = kBarOff + 2 * AttnCfg<T, D>::kStages * 8;
-  static constexpr int kExtraOff = (kTinfoOff + AttnCfg<T, D>::kStages * 8 + 127) & ~127;
+  static constexpr int kCLayerOff = kTinfoOff + AttnCfg<T, D>::kStages * 8;
+  static constexpr int kExtraOff = (kCLayerOff + 16 + 127) & ~127;
   static constexpr int kHistOff = kExtraOff + AttnCfg<T, D>::kExtraBytes;
   static constexpr int kUStageOff = kHistOff + AttnCfg<T, D>::kHistBytes;
   static constexpr int kQStageOff = kUStageOff + AttnCfg<T, D>::kUStageBytes;
@@ -119,6 +121,7 @@ struct AttnSmem {
     s.full = reinterpret_cast<uint64_t*>(fx + kBarOff);
     s.empty = s.full + C::kStages;
     s.tinfo = reinterpret_cast<int2*>(fx + kTinfoOff);
+    s.clayer = reinterpret_cast<uint32_t*>(fx + kCLayerOff);
     s.extra = fx + kExtraOff;
     s.hist = reinterpret_cast<uint32_t*>(fx + kHistOff);
     s.ustage = fx + kUStageOff;
@@ -169,6 +172,7 @@ __device__ __forceinline__ Tile tile_of(const LycSlot& s, int item, int sub, int
 struct NoWaits {
   __device__ __forceinline__ void unit(const LycSlot&) const {}
   __device__ __forceinline__ bool needed() const { return false; }
+  __device__ __forceinline__ bool any(bool) const { return false; }
   __device__ __forceinline__ void last_tile() const {}
 };
 
@@ -244,15 +248,17 @@ __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMa
         // the current token's K/V row is produced after the previous layer:
         // only a tile that holds it waits (dense: the last tile always; a
         // selected set: iff its largest id is the current token)
-        if (it == s.n_items - 1 && sub == tpi - 1 && waits.needed()) {
-          bool has_cur = true;
-          if (s.kind == ITEM_TOKENS) {
-            const int len = s.count ? min(s.list_len, __ldcg(s.count)) : s.list_len;
-            has_cur = len > 0 && __ldcg(s.list + len - 1) == p.seq_len - 1;
-          } else if (s.kind == ITEM_BLOCKS) {
-            has_cur = __ldcg(s.list + s.n_items - 1) == (p.seq_len - 1) / p.block_size;
+        // (from the tile's own rows -- no extra loads: contiguous tiles by
+        // their range, gathered tiles by the ids already loaded)
+        if (it == s.n_items - 1 && waits.needed()) {
+          bool mine = false;
+          if (t.ids) {
+#pragma unroll
+            for (int i = 0; i < kRounds; ++i) mine |= rows[i] == p.seq_len - 1;
+          } else {
+            mine = t.nvalid > 0 && t.lo + t.nvalid == p.seq_len;
           }
-          if (has_cur) waits.last_tile();
+          if (waits.any(mine)) waits.last_tile();
         }
         uint8_t* kd = ring + stage * C::kStageBytes;
         uint8_t* vd = kd + C::kTileBytes;

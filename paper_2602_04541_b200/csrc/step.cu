@@ -114,9 +114,26 @@ struct StepWaits {
     if (s.dep >= 0)  // every retrieval head of layer dep finished its selection
       wait(LYC_CTR(p->ctr, s.dep, CTR_SELDONE), epoch1 * seldone_per_step(*p, s.dep));
   }
+  const uint32_t* clayer;  // shared: 1 + the layer this CTA's consumers started
   __device__ __forceinline__ bool needed() const { return layer > 0; }
+  // OR over the producer threads (barrier with reduction)
+  __device__ __forceinline__ bool any(bool v) const {
+    uint32_t r;
+    asm volatile(
+        "{\n .reg .pred p, q;\n setp.ne.u32 p, %1, 0;\n bar.red.or.pred q, 3, %2, p;\n"
+        " selp.u32 %0, 1, 0, q;\n}"
+        : "=r"(r)
+        : "r"((uint32_t)v), "n"(kProducerThreads)
+        : "memory");
+    return r != 0;
+  }
+  // the previous layer's outputs are final once this CTA's consumers have
+  // started this layer (they waited for it); otherwise wait for it here
   __device__ __forceinline__ void last_tile() const {
-    if (layer > 0) wait(LYC_CTR(p->ctr, layer - 1, CTR_MERGE), epoch1 * (uint32_t)p->n_ctas);
+    if (layer == 0) return;
+    if (pt == 0 && (int)(ld_acquire_cta_shared(clayer) - (uint32_t)(layer + 1)) < 0)
+      spin_until(LYC_CTR(p->ctr, layer - 1, CTR_MERGE), epoch1 * (uint32_t)p->n_ctas);
+    group_bar(3, kProducerThreads);
   }
 };
 
@@ -734,6 +751,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
     }
     mbar_init(&es.bar, 1);
     fence_mbar_init();
+    *sm.clayer = 0u;
   }
   for (int b = threadIdx.x; b < LYC_H1_BINS; b += kStepThreads) sm.hist[b] = 0u;
   __syncthreads();
@@ -758,7 +776,10 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
         }
         consumer_bar();
       }
-      if (tid == 0) stamp(p, l, EV_CONS_BEGIN, cta);
+      if (tid == 0) {
+        st_release_cta_shared(sm.clayer, (uint32_t)(l + 1));
+        stamp(p, l, EV_CONS_BEGIN, cta);
+      }
       const LycLayerDesc L = p.layers[l];
       const LycView v = layer_view(p, L, l, esz);
       consume_units<T, D>(v, sm, L.split_off[cell], L.split_off[cell + 1], warp, lane, stage,
@@ -791,7 +812,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
     for (int l = 0; l < p.n_layers; ++l) {
       const LycLayerDesc L = p.layers[l];
       const LycView v = layer_view(p, L, l, esz);
-      StepWaits waits{&p, epoch1, l, pt};
+      StepWaits waits{&p, epoch1, l, pt, sm.clayer};
       produce_units<T, D>(v, &p.tmap_k, &p.tmap_v, sm.ring, sm.full, sm.empty, sm.tinfo,
                           L.split_off[cell], L.split_off[cell + 1], pt, stage, phase, waits);
     }
