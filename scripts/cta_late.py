@@ -49,8 +49,8 @@ for l in range(NL):
     print(f"l{l:2d} R{nr} prevR{pr} span p50 {np.median(span):5.1f} max {span.max():5.1f} "
           f"end-rel p50 {np.median(end_rel):5.1f} max {end_rel.max():5.1f} late {list(late)}{msg}")
 # consumer events of the latest CTA vs the median CTA (first rep)
-names = ["q_staged", "first_tile", "unit1_done", "last_tile", "ue_enter", "ue_bar", "ue_stored"]
-for l in (7, 12, 13, 17, 20):
+names = ["q_staged", "first_tile", "unit1_done", "last_tile", "ue_enter", "ue_bar", "ue_stored", "u1_signalled"]
+for l in (5, 6, 7, 12, 13, 17, 20):
     b = rel[:, l, 0]
     e = rel[:, l, 1]
     end_rel = (e - b.max(1, keepdims=True)).mean(0)
