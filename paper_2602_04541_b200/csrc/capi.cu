@@ -937,6 +937,8 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
     if (const char* env_st = std::getenv("LYC_STAGES")) d->stages = std::max(0, std::atoi(env_st));
     d->S = c.num_splits > 0 ? c.num_splits : std::max(1, sms / d->B);
     if (d->fused && d->S * d->B > sms) d->fused = false;
+    // the step kernel's selection handles up to 64 items of 8192 keys per row
+    if (d->fused && c.seq_cap > (int64_t)64 * 8192) d->fused = false;
     const int64_t nb_cap = (c.seq_cap + d->bs - 1) / d->bs;
     if (c.select_mode == LYC_SELECT_BLOCKS) {
       d->k_cap = c.policy_kind == LYC_POLICY_RATIO ? nb_cap
@@ -961,8 +963,9 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
         cuda_check(cudaMalloc(&d->sel_bitmap, 2 * rows * d->bitmap_stride * 4), "cudaMalloc bitmap");
         cuda_check(cudaMalloc(&d->sel_cand, 2 * rows * 3 * d->sel_stride * 4), "cudaMalloc cand");
         cuda_check(cudaMalloc(&d->sel_ccnt, 2 * rows * 256 * 4), "cudaMalloc ccnt");
-        cuda_check(cudaMalloc(&d->sel_csub, 2 * rows * 256 * 4), "cudaMalloc csub");
-        cuda_check(cudaMemset(d->sel_csub, 0, 2 * rows * 256 * 4), "memset");
+        // per row: 64 selection items x 256 u16 bucket starts
+        cuda_check(cudaMalloc(&d->sel_csub, 2 * rows * 64 * 128 * 4), "cudaMalloc csub");
+        cuda_check(cudaMemset(d->sel_csub, 0, 2 * rows * 64 * 128 * 4), "memset");
       }
       if (d->fused) {  // per-(layer, row / slot) counters of the step kernel
         cuda_check(cudaMalloc(&d->sel_rowctr, (size_t)d->NL * rows * 16 * 4), "cudaMalloc rowctr");

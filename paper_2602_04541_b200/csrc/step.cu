@@ -301,7 +301,8 @@ struct SelRow {
   uint32_t* ckey;     // [n] candidate keys, item q's segment at q*kItemKeys
   uint32_t* cidx;     // [n] candidate indices
   uint32_t* cflag;    // [n] (unused)
-  uint32_t* csub;     // [256] row sub-histogram of the boundary-bin candidates
+  uint32_t* csub;     // [64 items][256] u16: each item's bucket starts of its boundary-bin
+                      // candidates by their next 8 bits (descending: start[b] = #above b)
   uint32_t* ccnt;     // [n_items] candidates per item; +64: definite keys per item;
                       // +128: output offset of each item
   uint32_t* ctr;      // per-row words: [0] items classified, [8] items holding their copies
@@ -316,7 +317,7 @@ __device__ __forceinline__ SelRow sel_row(const LycStepParams& p, int l, int r) 
   s.ckey = p.sel_cand + pr * 3 * p.sel_stride;
   s.cidx = s.ckey + p.sel_stride;
   s.cflag = s.cidx + p.sel_stride;
-  s.csub = p.sel_csub + pr * 256;
+  s.csub = p.sel_csub + pr * (64 * 128);
   s.ccnt = p.sel_ccnt + pr * 256;
   s.ctr = p.sel_rowctr + ((int64_t)l * p.max_sel + r) * 16;
   return s;
@@ -429,24 +430,18 @@ __device__ void classify_item(const LycStepParams& p, const SelRow& R, int q, Ep
     if (k0 + w * 32 < cnt) R.bitmap[bm_pad((lo + k0) / 32 + w)] = words[w];
   const uint32_t c = __popc(eqm[0]) + __popc(eqm[1]) + __popc(eqm[2]) + __popc(eqm[3]);
   uint32_t total;
-  uint32_t pos = epi_scan(c, es.scan, et, total) - c;
+  epi_scan(c, es.scan, et, total);
   // this item's block of the row's contiguous candidate array (per-step
-  // counter, reset by the row's last resolver)
+  // counter, reset by the row's last resolver); the reservation's round trip
+  // overlaps the sub-histogram
   if (et == 0) es.pad = atomicAdd(R.ctr + 4, total);
-  epi_bar();
-  pos += es.pad;
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
     uint32_t m = eqm[w];
     while (m) {
       const int j = __ffs(m) - 1;
       m &= m - 1;
-      const int i = k0 + w * 32 + j;
-      const uint32_t key = es.buf[i];
-      R.ckey[pos] = key;
-      R.cidx[pos] = (uint32_t)(lo + i);
-      atomicAdd(&es.hist[(key >> (shift - 8)) & 255u], 1u);
-      ++pos;
+      atomicAdd(&es.hist[(es.buf[k0 + w * 32 + j] >> (shift - 8)) & 255u], 1u);
     }
   }
   uint32_t ndef = __popc(words[0]) + __popc(words[1]) + __popc(words[2]) + __popc(words[3]);
@@ -454,13 +449,51 @@ __device__ void classify_item(const LycStepParams& p, const SelRow& R, int q, Ep
   for (int off = 16; off > 0; off >>= 1) ndef += __shfl_xor_sync(0xffffffffu, ndef, off);
   if ((et & 31) == 0) es.scan[32 + (et >> 5)] = ndef;
   epi_bar();
-  for (int b = et; b < 256; b += kEpiThreads) {
-    const uint32_t h = es.hist[b];
-    if (h) atomicAdd(R.csub + b, h);
+  // descending bucket starts (thread et: bins 255-4et .. 252-4et): published
+  // for the resolvers (u16) and used as scatter cursors here
+  {
+    uint32_t h4[4], hs = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      h4[j] = es.hist[255 - 4 * et - j];
+      hs += h4[j];
+    }
+    uint32_t tot2;
+    uint32_t run = epi_scan(hs, es.scan, et, tot2) - hs;
+    uint32_t st[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      st[j] = run;
+      es.hist[256 + 255 - 4 * et - j] = run;
+      run += h4[j];
+    }
+    // u16 bins 252-4et .. 255-4et (ascending in memory)
+    reinterpret_cast<uint2*>(R.csub + q * 128)[63 - et] =
+        make_uint2(st[3] | (st[2] << 16), st[1] | (st[0] << 16));
+  }
+  epi_bar();
+  // candidates scattered by bucket (order inside a bucket is free: survivors
+  // are ranked by (key, index))
+  {
+    const uint32_t base = es.pad;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      uint32_t m = eqm[w];
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const int i = k0 + w * 32 + j;
+        const uint32_t key = es.buf[i];
+        const uint32_t pos = base + atomicAdd(&es.hist[256 + ((key >> (shift - 8)) & 255u)], 1u);
+        R.ckey[pos] = key;
+        R.cidx[pos] = (uint32_t)(lo + i);
+      }
+    }
   }
   if (et == 0) {
     R.ccnt[q] = total;
     R.ccnt[64 + q] = es.scan[32] + es.scan[33];
+    R.ccnt[128 + q] = es.pad;
     // the row's boundary prefix (identical from every item) for the resolvers
     R.ccnt[192] = P;
     R.ccnt[193] = above;
@@ -493,19 +526,23 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
   if (et == 0) spin_until(R.ctr, epoch1 * (uint32_t)items);  // every item classified
   epi_bar();
   if (et == 0) stamp(p, l, EV_F_SCAN, cta);
-  // one round: the row prefix and counts, this item's definite words, the
-  // row's sub-histogram and (speculatively) the first kSpec candidates
-  const int cap = (kEpiBufWords / 2) & ~3;  // candidates that fit on chip
-  const int spec = min(kSpec, (int)(p.sel_stride & ~(int64_t)3));
-  uint32_t* skey = es.buf;
-  uint32_t* sidx = es.buf + cap;
+  // one round: the row prefix and counts, this item's definite words, every
+  // item's bucket starts and (speculatively) the first kSpec candidates
+  const int bsw = items * 128;  // words of the items' u16 bucket starts
+  const int cap = ((kEpiBufWords - bsw) / 2) & ~3;  // candidates that fit on chip
+  const int spec = max(0, min(min(kSpec, cap), (int)(p.sel_stride & ~(int64_t)3)));
+  const uint16_t* bs16 = reinterpret_cast<const uint16_t*>(es.buf);  // [items][256]
+  uint32_t* skey = es.buf + bsw;
+  uint32_t* sidx = skey + cap;
   if (et == 0) {
     fence_proxy_async();         // earlier generic use of es.buf / es.hist -> TMA write
     fence_proxy_async_global();  // other CTAs' generic writes -> this TMA read
-    mbar_arrive_expect_tx(&es.bar, 1024u + 8u * (uint32_t)spec);
-    bulk_g2s(es.hist, R.csub, 1024u, &es.bar);
-    bulk_g2s(skey, R.ckey, 4u * (uint32_t)spec, &es.bar);
-    bulk_g2s(sidx, R.cidx, 4u * (uint32_t)spec, &es.bar);
+    mbar_arrive_expect_tx(&es.bar, 4u * (uint32_t)bsw + 8u * (uint32_t)spec);
+    bulk_g2s(es.buf, R.csub, 4u * (uint32_t)bsw, &es.bar);
+    if (spec > 0) {
+      bulk_g2s(skey, R.ckey, 4u * (uint32_t)spec, &es.bar);
+      bulk_g2s(sidx, R.cidx, 4u * (uint32_t)spec, &es.bar);
+    }
   }
   if (R.h1) {  // every item has read the row's first-pass histogram: item q re-zeroes its share
     const int per = (LYC_H1_ROW + items - 1) / items;
@@ -517,13 +554,21 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
   uint32_t krem = (uint32_t)p.k_sel - __ldcg(R.ccnt + 193);
   const int ns = (int)__ldcg(R.ctr + 4);  // candidates of the row
   const uint32_t d_mine = et < items ? __ldcg(R.ccnt + 64 + et) : 0u;
+  if (et < items) {
+    es.cnt[et] = __ldcg(R.ccnt + et);
+    es.seg[et] = __ldcg(R.ccnt + 128 + et);
+  }
   const int w0 = lo / 32 + et * 4;  // this thread's 4 words (128 keys)
   uint4 wv4 = make_uint4(0u, 0u, 0u, 0u);
   if (et * 128 < cnt) wv4 = __ldcg(reinterpret_cast<const uint4*>(R.bitmap + bm_pad(w0)));
   uint32_t* ws = es.hist + 1792;  // [256] this item's words on chip
   reinterpret_cast<uint4*>(ws)[et] = wv4;
   if (et < items) es.defc[et] = d_mine;
-  if (et == 0) es.scan[46] = 0u;
+  if (et == 0) {
+    es.scan[44] = 0u;
+    es.scan[45] = 0u;
+    es.scan[46] = 0u;
+  }
   const bool on_chip = ns <= cap;
   mbar_wait(&es.bar, bar_phase);
   bar_phase ^= 1u;
@@ -558,6 +603,23 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
     if ((int)idx < lo) atomicAdd(&es.scan[46], 1u);
     else if ((int)idx < lo + cnt) atomicOr(ws + ((idx - (uint32_t)lo) >> 5), 1u << (idx & 31));
   };
+  // the row's sub-histogram from the items' bucket starts:
+  // count[b] = start[b - 1] - start[b] (start[-1] = the item's candidates)
+  epi_bar();
+  {  // thread et: bins 4et .. 4et+3 (one 8-B load + the bin below per item)
+    uint32_t h0 = 0, h1 = 0, h2 = 0, h3 = 0;
+    for (int i = 0; i < items; ++i) {
+      const uint2 v = reinterpret_cast<const uint2*>(bs16 + i * 256)[et];
+      const uint32_t prev = et ? (uint32_t)bs16[i * 256 + 4 * et - 1] : es.cnt[i];
+      const uint32_t s0 = v.x & 0xffffu, s1 = v.x >> 16, s2 = v.y & 0xffffu, s3 = v.y >> 16;
+      h0 += prev - s0;
+      h1 += s0 - s1;
+      h2 += s1 - s2;
+      h3 += s2 - s3;
+    }
+    reinterpret_cast<uint4*>(es.hist)[et] = make_uint4(h0, h1, h2, h3);
+  }
+  epi_bar();
   epi_digit(es, es.hist, false, 256, krem, et);
   // every thread's reads of the shared row state (count, sub-histogram; bulk
   // copies complete) are performed (barrier above): count this item's copy
@@ -571,6 +633,47 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
   krem -= es.above;
   uint32_t live = es.hist[es.digit];
   if (et == 0) stamp(p, l, EV_F_PREFIX, cta);
+  if (live <= (uint32_t)kRankMax) {
+    // ---- fast path: the buckets above the digit are taken whole; the digit's
+    // bucket of every item (the survivors, contiguous) is ranked exactly
+    const uint32_t d = es.digit;
+    uint32_t n_i = 0, off_i = 0;
+    if (et < items) {
+      const uint32_t above_i = bs16[et * 256 + d];
+      n_i = (d ? (uint32_t)bs16[et * 256 + d - 1] : es.cnt[et]) - above_i;
+      off_i = es.seg[et] + above_i;
+      if (et < q) atomicAdd(&es.scan[44], above_i);  // taken above the bucket, before this item
+    }
+    uint32_t m;
+    const uint32_t base_i = epi_scan(n_i, es.scan, et, m) - n_i;
+    uint32_t* lk = es.hist + 256;  // survivors: keys [kRankMax] | ids [kRankMax]
+    for (uint32_t j = 0; j < n_i; ++j) {
+      uint32_t key = 0, idx = 0;
+      get((int)(off_i + j), key, idx);
+      lk[base_i + j] = key;
+      lk[kRankMax + base_i + j] = idx;
+    }
+    {  // this item's candidates above the bucket
+      const uint32_t a_q = bs16[q * 256 + d];
+      const int s_q = (int)es.seg[q];
+      for (int j = et; j < (int)a_q; j += kEpiThreads) {
+        uint32_t key = 0, idx = 0;
+        get(s_q + j, key, idx);
+        atomicOr(ws + ((idx - (uint32_t)lo) >> 5), 1u << (idx & 31));
+      }
+    }
+    epi_bar();
+    if (et == 0) stamp(p, l, EV_X1, cta);
+    for (uint32_t e = et; e < m; e += kEpiThreads) {
+      const uint32_t ki = lk[e], xi = lk[kRankMax + e];
+      uint32_t rank = 0;
+      for (uint32_t j = 0; j < m; ++j) {
+        const uint32_t kj = lk[j];
+        rank += (kj > ki || (kj == ki && lk[kRankMax + j] < xi)) ? 1u : 0u;
+      }
+      if (rank < krem) take(xi);
+    }
+  } else {
   // (rare) keep narrowing while too many candidates share the prefix
   while (live > (uint32_t)kRankMax && shift > 0) {
     const int wbits = shift > 8 ? 8 : shift;
@@ -680,6 +783,7 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
       if (get(i, key, idx) && key == P && 0xFFFFFu - idx >= Pi) take(idx);
     }
   }
+  }  // narrowing / scan path
   if (et == 0) es.last = copies == epoch1 * (uint32_t)items - 1u;
   epi_bar();
   if (et == 0) stamp(p, l, EV_SEL0, cta);
@@ -719,7 +823,6 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
   }
   if (q == 0 && et == 0 && p.idx_count) p.idx_count[row] = p.k_sel;
   if (es.last) {
-    for (int b = et; b < 256; b += kEpiThreads) R.csub[b] = 0u;
     if (et == 0) R.ctr[4] = 0u;
     if (p.sel_mode == SEL_BLOCK_KEYS)
       for (int i = et; i < n; i += kEpiThreads) R.keys[i] = 0u;
