@@ -113,10 +113,11 @@ typedef struct lyc_decode_config {
   int32_t n_layers, batch, n_kv_heads, group_size, d_head;
   int32_t dtype;         /* LYC_DTYPE_* */
   int64_t seq_cap;       /* KV rows allocated per (layer, b, g) slab */
-  int32_t policy_kind;   /* LYC_POLICY_TOPK or LYC_POLICY_RATIO */
+  int32_t policy_kind;   /* LYC_POLICY_*: TopK / Ratio (step kernel), TopP / Threshold
+                            (per-layer kernels, token selection only) */
   int32_t select_mode;   /* LYC_SELECT_TOKENS or LYC_SELECT_BLOCKS */
   int64_t top_k;         /* TopK budget in tokens (blocks mode: ceil(k / block_size) blocks) */
-  double ratio;          /* Ratio theta in (0, 1) */
+  double ratio;          /* Ratio theta in (0, 1); TopP p in (0, 1]; Threshold tau > 0 */
   int32_t block_size;    /* 64 (tile) */
   int32_t num_splits;    /* splits per batch item; 0 = one CTA per SM */
   float scale;           /* softmax scale; 0 -> 1/sqrt(d_head) */

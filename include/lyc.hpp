@@ -426,8 +426,9 @@ inline std::size_t fraction_budget(double frac, std::size_t n) {
   return (std::size_t)lyc_fraction_budget(frac, (int64_t)n);
 }
 
-// policy.hpp:20-53 (TopK and Ratio run on the device; TopP / Threshold are
-// rejected by HybridDecoder with not_supported).
+// policy.hpp:20-53.  All four kinds run on the device: TopK and Ratio in the
+// persistent step kernel, TopP and Threshold (data-dependent set sizes) with
+// per-layer kernels (csrc/policy.cu).
 struct SparsityPolicy {
   enum class Kind { TopK, TopP, Threshold, Ratio };
   Kind kind = Kind::TopK;
@@ -447,7 +448,7 @@ struct SparsityPolicy {
     return {Kind::TopP, 0, p};
   }
   static SparsityPolicy threshold(double tau) {
-    if (!(tau >= 0.0 && tau <= 1.0)) throw std::invalid_argument("threshold: tau must lie in [0,1]");
+    if (!(tau > 0.0)) throw std::invalid_argument("threshold: tau must be positive");
     return {Kind::Threshold, 0, tau};
   }
 };
@@ -478,8 +479,6 @@ class HybridDecoder {
   HybridDecoder(const Config& c, std::span<const std::uint8_t> roles) : cfg_(c) {
     if (roles.size() != (std::size_t)c.n_layers * c.n_kv_heads)
       throw std::invalid_argument("RoleMap: role count mismatch");
-    if (c.policy.kind == SparsityPolicy::Kind::TopP || c.policy.kind == SparsityPolicy::Kind::Threshold)
-      throw not_supported("decoder: TopP/Threshold selection is not implemented on device");
     lyc_decode_config lc{};
     lc.n_layers = c.n_layers;
     lc.batch = c.batch;
@@ -488,7 +487,12 @@ class HybridDecoder {
     lc.d_head = c.d_head;
     lc.dtype = (int32_t)c.dtype;
     lc.seq_cap = (int64_t)c.seq_cap;
-    lc.policy_kind = c.policy.kind == SparsityPolicy::Kind::Ratio ? LYC_POLICY_RATIO : LYC_POLICY_TOPK;
+    switch (c.policy.kind) {
+      case SparsityPolicy::Kind::TopK: lc.policy_kind = LYC_POLICY_TOPK; break;
+      case SparsityPolicy::Kind::TopP: lc.policy_kind = LYC_POLICY_TOPP; break;
+      case SparsityPolicy::Kind::Threshold: lc.policy_kind = LYC_POLICY_THRESHOLD; break;
+      case SparsityPolicy::Kind::Ratio: lc.policy_kind = LYC_POLICY_RATIO; break;
+    }
     lc.select_mode = (int32_t)c.select;
     lc.top_k = (int64_t)c.policy.k;
     lc.ratio = c.policy.value;

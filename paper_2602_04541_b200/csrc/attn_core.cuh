@@ -262,6 +262,21 @@ __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMa
         }
         uint8_t* kd = ring + stage * C::kStageBytes;
         uint8_t* vd = kd + C::kTileBytes;
+        if (t.nvalid <= 0) {
+          // a variable-size set (device count) ended inside this unit: one
+          // empty tile tells the consumers, both sides leave the unit
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (pt == 0) {
+            tinfo[stage] = make_int2(t.lo, 0);
+            mbar_arrive(&full[stage]);
+          }
+          mbar_arrive(&full[stage]);
+          if (++stage == ring_stages<C>(p)) {
+            stage = 0;
+            phase ^= 1;
+          }
+          break;
+        }
         if (t.ids == nullptr && t.nvalid == LYC_TILE) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (pt == 0) {
@@ -535,6 +550,16 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
       for (int sub = 0; sub < tpi; ++sub) {
         mbar_wait(&sm.full[stage], phase);
         const int2 t = sm.tinfo[stage];  // (first row, valid rows)
+        if (t.y <= 0) {  // the unit's set ended (variable-size set): leave the unit
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.empty[stage]);
+          if (++stage == ring_stages<C>(p)) {
+            stage = 0;
+            phase ^= 1;
+          }
+          it = un.end;
+          break;
+        }
         if (first_tile) {
           cstamp(p, 17, tid);
           first_tile = false;
@@ -713,6 +738,16 @@ __device__ __forceinline__ void consume_units_f32(const LycView& p, const AttnSm
       for (int sub = 0; sub < tpi; ++sub) {
         mbar_wait(&sm.full[stage], phase);
         const int2 t = sm.tinfo[stage];  // (first row, valid rows)
+        if (t.y <= 0) {  // the unit's set ended (variable-size set): leave the unit
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.empty[stage]);
+          if (++stage == ring_stages<C>(p)) {
+            stage = 0;
+            phase ^= 1;
+          }
+          it = un.end;
+          break;
+        }
         const uint8_t* ks = sm.ring + stage * C::kStageBytes;
         const float* krow = reinterpret_cast<const float*>(ks + (t0 + tr) * C::kRowBytes);
         const uint8_t* vs = ks + C::kTileBytes;

@@ -22,6 +22,7 @@ cudaError_t launch_attn(const LycAttnParams& p, int dtype, int d, int batch, cud
 int attn_stages(int dtype, int d);
 cudaError_t launch_merge(const LycMergeParams& p, int dtype, cudaStream_t st);
 cudaError_t launch_topk(const LycTopkParams& p, int rows, int cluster, cudaStream_t st);
+cudaError_t launch_policy(const LycPolicyParams& p, int rows, cudaStream_t st);
 int topk_cluster_size(int n, int max_slice);
 size_t topk_smem_bytes(int slice);
 cudaError_t launch_float_keys(const float* s, uint32_t* keys, int64_t n, cudaStream_t st);
@@ -518,6 +519,7 @@ struct lyc_decoder {
     LycAttnParams ap;           // per-layer kernel path
     LycMergeParams mp;
     LycTopkParams tp;
+    LycPolicyParams pp;         // TopP / Threshold selection (per-layer path)
     LycLayerDesc desc;          // step kernel path
     int n_sel = 0, cluster = 1, n_merges = 0;
   };
@@ -540,7 +542,12 @@ struct lyc_decoder {
       return std::min<int64_t>((cfg.top_k + bs - 1) / bs, nb);
     }
     if (cfg.policy_kind == LYC_POLICY_RATIO) return lyc_fraction_budget(1.0 - cfg.ratio, seq);
+    if (variable_sets()) return seq;  // capacity; the set size is a device count
     return std::min<int64_t>(cfg.top_k, seq);
+  }
+  // TopP / Threshold: data-dependent set sizes (device counts)
+  bool variable_sets() const {
+    return cfg.policy_kind == LYC_POLICY_TOPP || cfg.policy_kind == LYC_POLICY_THRESHOLD;
   }
 };
 
@@ -674,7 +681,8 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
           s.kind = blocks ? ITEM_BLOCKS : ITEM_TOKENS;
           s.list = d->idx + (int64_t)(b * H + g) * d->k_cap;
           s.list_len = (int32_t)kb;
-          if (d->shard) s.count = d->idx_count + (b * H + g);  // this rank's filtered set
+          if (d->shard || d->variable_sets())  // this rank's filtered set / a variable-size set
+            s.count = d->idx_count + (b * H + g);
           s.n_items = blocks ? (int32_t)kb : (int32_t)((kb + LYC_TILE - 1) / LYC_TILE);
           s.dep = last_r[(size_t)g];
         }
@@ -758,6 +766,19 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
     tp.out_count = d->idx_count;
     tp.slice = (int32_t)((sel_n + cluster - 1) / cluster);
     tp.clear_keys = blocks ? 1 : 0;
+    LycPolicyParams& pp = ly.pp;
+    std::memset(&pp, 0, sizeof(pp));
+    pp.keys = d->sel_keys;
+    pp.key_stride = d->sel_stride;
+    pp.n = (int32_t)sel_n;
+    pp.kind = d->cfg.policy_kind;
+    pp.value = d->cfg.ratio;
+    // the consumers' key value: bf16 sum_j q_j.k (= G * pooled_q.k), fp32 pooled_q.k
+    pp.score_scale = d->cfg.dtype == LYC_DTYPE_BF16 ? d->cfg.scale / (float)G : d->cfg.scale;
+    pp.out = d->idx;
+    pp.out_row = dl.sel_rows;
+    pp.out_stride = d->k_cap;
+    pp.out_count = d->idx_count;
     ly.n_sel = dl.n_sel;
     ly.cluster = cluster;
     LycLayerDesc& ds = descs[(size_t)l];
@@ -822,7 +843,10 @@ void decoder_layer(lyc_decoder* d, int l, const void* q_l, const void* k, const 
     ++g_launches;
   }
   if (ly.n_sel) {
-    cuda_check(lyc::launch_topk(ly.tp, ly.n_sel, ly.cluster, st), "topk launch");
+    if (d->variable_sets())
+      cuda_check(lyc::launch_policy(ly.pp, ly.n_sel, st), "policy launch");
+    else
+      cuda_check(lyc::launch_topk(ly.tp, ly.n_sel, ly.cluster, st), "topk launch");
     ++g_launches;
   }
 }
@@ -903,8 +927,12 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
       if (c.top_k < 1) fail(LYC_EINVAL, "top_k: k must be >= 1");
     } else if (c.policy_kind == LYC_POLICY_RATIO) {
       if (!(c.ratio > 0.0 && c.ratio < 1.0)) fail(LYC_EINVAL, "ratio: theta must lie in (0,1)");
-    } else if (c.policy_kind == LYC_POLICY_TOPP || c.policy_kind == LYC_POLICY_THRESHOLD) {
-      fail(LYC_ENOTSUP, "decoder: TopP/Threshold selection is not implemented on device");
+    } else if (c.policy_kind == LYC_POLICY_TOPP) {
+      if (!(c.ratio > 0.0 && c.ratio <= 1.0)) fail(LYC_EINVAL, "top_p: p must lie in (0,1]");
+      if (c.select_mode != LYC_SELECT_TOKENS) fail(LYC_ENOTSUP, "decoder: TopP selects tokens only");
+    } else if (c.policy_kind == LYC_POLICY_THRESHOLD) {
+      if (!(c.ratio > 0.0)) fail(LYC_EINVAL, "threshold: tau must be positive");
+      if (c.select_mode != LYC_SELECT_TOKENS) fail(LYC_ENOTSUP, "decoder: Threshold selects tokens only");
     } else {
       fail(LYC_EINVAL, "decoder: unknown policy");
     }
@@ -933,7 +961,8 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
     const int sms = num_sms();
     // The persistent step kernel needs every CTA co-resident: 1 CTA per SM,
     // S*B <= #SMs.
-    d->fused = lyc::step_supported(c.dtype, c.d_head) && std::getenv("LYC_NO_FUSED_STEP") == nullptr;
+    d->fused = lyc::step_supported(c.dtype, c.d_head) && std::getenv("LYC_NO_FUSED_STEP") == nullptr &&
+               !d->variable_sets();  // TopP / Threshold: per-layer kernels
     if (const char* env_st = std::getenv("LYC_STAGES")) d->stages = std::max(0, std::atoi(env_st));
     d->S = c.num_splits > 0 ? c.num_splits : std::max(1, sms / d->B);
     if (d->fused && d->S * d->B > sms) d->fused = false;
@@ -945,7 +974,9 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
                                                    : std::min<int64_t>((c.top_k + 63) / 64, nb_cap);
       d->sel_stride = (nb_cap + 3) & ~(int64_t)3;  // 16-B aligned key rows
     } else {
-      d->k_cap = c.policy_kind == LYC_POLICY_RATIO ? c.seq_cap : std::min<int64_t>(c.top_k, c.seq_cap);
+      d->k_cap = (c.policy_kind == LYC_POLICY_RATIO || d->variable_sets())
+                     ? c.seq_cap
+                     : std::min<int64_t>(c.top_k, c.seq_cap);
       d->sel_stride = (c.seq_cap + 3) & ~(int64_t)3;
     }
     try {
@@ -1042,6 +1073,8 @@ namespace {
 void shard_enter(lyc_decoder* d) {
   if (d->cfg.select_mode == LYC_SELECT_BLOCKS)
     fail(LYC_ENOTSUP, "shard: sequence sharding supports token-mode selection only");
+  if (d->variable_sets())
+    fail(LYC_ENOTSUP, "shard: sequence sharding supports TopK / Ratio selection only");
   if (d->fused || !d->shard) {
     d->fused = false;  // per-layer kernels: the collective sits between layers
     d->shard = true;   // sparse slots read device counts of the filtered sets

@@ -128,6 +128,23 @@ struct LycTopkParams {
   int32_t clear_keys;       // zero keys after use (block-max keys are atomicMax'ed)
 };
 
+// TopP / Threshold selection (policy.cu): one CTA per selection row.
+#define LYC_POLICY_KIND_TOPP 1       // = LYC_POLICY_TOPP (include/lyc.h)
+#define LYC_POLICY_KIND_THRESHOLD 2  // = LYC_POLICY_THRESHOLD
+struct LycPolicyParams {
+  const uint32_t* keys;     // [n_sel][key_stride] order-preserving keys of sum_j q_j.k
+  int64_t key_stride;
+  int32_t n;                // tokens per selection row (seq_len)
+  int32_t kind;             // LYC_POLICY_KIND_*
+  double value;             // p (TopP) or tau (Threshold)
+  float score_scale;        // key value -> the reference's scaled pooled score (bf16 keys: scale / G)
+  int32_t pad;
+  int32_t* out;             // index cache base
+  const int32_t* out_row;   // [n_sel] -> row in the index cache
+  int64_t out_stride;       // index cache row stride (k_cap)
+  int32_t* out_count;       // [cache rows] size of each set
+};
+
 // ---------------------------------------------------------------------------
 // Persistent decode-step kernel (step.cu): one launch runs every layer.
 struct LycLayerDesc {

@@ -1,7 +1,7 @@
 """Mirror of the reference decode-step attention loop and its selection API.
 
-* ``SparsityPolicy`` / ``fraction_budget`` -- policy.hpp:20-62 (TopK and Ratio
-  run on the device; TopP / Threshold raise ``NotSupported``).
+* ``SparsityPolicy`` / ``fraction_budget`` -- policy.hpp:20-62 (all four kinds
+  run on the device; TopP / Threshold through per-layer kernels, csrc/policy.cu).
 * ``args_top_k``   -- attention.hpp:108-123 on a device score vector.
 * ``HybridDecoder`` -- decode_engine.hpp:109-151: per layer, retrieval heads
   (layer 0, or role R in the RoleMap, rolemap.hpp:33-35) run dense split-KV
@@ -105,8 +105,6 @@ class HybridDecoder:
         self.select = select
         r = np.ascontiguousarray(np.asarray(roles, dtype=np.uint8).reshape(n_layers, n_kv_heads))
         self.roles = r
-        if policy.kind in ("topp", "threshold"):
-            raise NotSupported(f"{policy.kind}: not implemented on device")
         cfg = _lib.lyc_decode_config(
             n_layers=n_layers, batch=batch, n_kv_heads=n_kv_heads, group_size=group_size,
             d_head=d_head,

@@ -298,7 +298,10 @@ static void test_hybrid_decoder_errors() {
   CHECK_THROWS(lyc::HybridDecoder(c, bad), std::invalid_argument);
   std::vector<uint8_t> ok{0, 0, 1, 1};
   c.policy = lyc::SparsityPolicy::top_p(0.9);
+  c.select = lyc::Select::Blocks;  // TopP selects tokens only
   CHECK_THROWS(lyc::HybridDecoder(c, ok), lyc::not_supported);
+  c.select = lyc::Select::Tokens;
+  CHECK_THROWS(lyc::SparsityPolicy::threshold(0.0), std::invalid_argument);
   CHECK_THROWS(lyc::SparsityPolicy::top_k(0), std::invalid_argument);
   CHECK_THROWS(lyc::SparsityPolicy::ratio(1.5), std::invalid_argument);
   CHECK(lyc::fraction_budget(0.1, 100) == 10);

@@ -226,9 +226,9 @@ def test_decoder_errors():
                         roles=bad, policy=P.SparsityPolicy.top_k(4))
     with pytest.raises(P.InvalidArgument):
         P.SparsityPolicy.top_k(0)
-    with pytest.raises(P.NotSupported):
+    with pytest.raises(P.NotSupported):  # TopP selects tokens only
         P.HybridDecoder(n_layers=2, batch=1, n_kv_heads=2, group_size=2, d_head=64, seq_cap=128,
-                        roles=np.zeros((2, 2)), policy=P.SparsityPolicy.top_p(0.9))
+                        roles=np.zeros((2, 2)), policy=P.SparsityPolicy.top_p(0.9), select="blocks")
     dec = P.HybridDecoder(n_layers=2, batch=1, n_kv_heads=2, group_size=2, d_head=64, seq_cap=128,
                           roles=np.zeros((2, 2)), policy=P.SparsityPolicy.top_k(4))
     q = torch.zeros((2, 1, 4, 64), dtype=torch.bfloat16, device="cuda")
@@ -362,3 +362,87 @@ def test_fused_step_batch4_many_items_per_cta(orc):
             src = max(l for l in range(NL) if roles[l, g] == 0)
             sc = pooled_scores(q[src, b], K[src, b, g], G, g, seq)
             check_set(sets[b][g], r["sets"][g], sc, k)
+
+
+def _policy_weights(q_l, K_lg, group, g, seq, scale):
+    s = pooled_scores(q_l, K_lg, group, g, seq) * scale
+    w = np.exp(s - s.max())
+    return w / w.sum()
+
+
+def check_policy_set(got, ref, w, kind, value, rel_band=1e-6):
+    """TopP / Threshold sets: exact, or differences confined to weights within
+    rel_band of the cut (tau, or the weight where the cumulative mass crosses p)."""
+    got, ref = set(got.tolist()), set(ref.tolist())
+    if got == ref:
+        return 0
+    if kind == "threshold":
+        cut = value
+    else:
+        order = sorted(range(len(w)), key=lambda t: (-w[t], t))
+        cut = w[order[len(ref) - 1]]
+        assert abs(len(got) - len(ref)) <= 1
+    for t in got ^ ref:
+        assert abs(w[t] - cut) <= rel_band * cut, (kind, t, w[t], cut)
+    return len(got ^ ref)
+
+
+@pytest.mark.parametrize("kind,value", [("topp", 0.5), ("topp", 0.9), ("topp", 1.0),
+                                        ("threshold", 1.3 / 4096), ("threshold", 0.5)])
+def test_topp_threshold_policies_vs_oracle(orc, kind, value):
+    """policy.hpp:73-101 on the device (csrc/policy.cu): TopP (cumulative mass,
+    stable descending order) and Threshold (w > tau, argmax fallback) from the
+    pooled-query weights; sparse heads consume the variable-size sets through
+    their device counts.  Tiny fp32 config, per-layer sets vs the oracle."""
+    import paper_2602_04541_b200 as P
+    NL, B, H, G, d, seq = 4, 1, 2, 4, 64, 4096
+    roles = roles_for(NL, H, [(2, 1)])
+    policy = P.SparsityPolicy.top_p(value) if kind == "topp" else P.SparsityPolicy.threshold(value)
+    dec, q, K, V, out, traces = run_case(orc, NL=NL, B=B, H=H, G=G, d=d, seq=seq, seq_cap=seq,
+                                         dtype=torch.float32, roles=roles, policy=policy, seed=5,
+                                         layerwise=True)
+    scale = 1 / np.sqrt(d)
+    r = orc.decode_step(q[:, 0], K[:, 0], V[:, 0], roles, seq=seq, scale=scale, kind=kind,
+                        value=value, trace=True)
+    diffs = 0
+    for l in range(NL):
+        for g in range(H):
+            src = max(ll for ll in range(l + 1) if roles[ll, g] == 0 or ll == 0)
+            w = _policy_weights(q[src, 0], K[src, 0, g], G, g, seq, scale)
+            diffs += check_policy_set(traces[l][0][g], r["trace"][l][g], w, kind, value)
+    if diffs == 0:
+        assert rel_err(out[:, 0], r["out"]) < FP32_TOL
+    if kind == "threshold" and value == 0.5:  # nothing clears the bar: the argmax alone
+        assert all(len(traces[l][0][g]) == 1 for l in range(NL) for g in range(H))
+
+
+def test_topp_bf16_llama_heads_graph_replay(orc):
+    """TopP at Llama head shapes in bf16, through the eager step and a CUDA-graph
+    replay (variable-size sets are device counts, so the graph is reusable)."""
+    import paper_2602_04541_b200 as P
+    NL, B, H, G, d, seq = 3, 1, 8, 4, 128, 8192
+    roles = roles_for(NL, H, [(1, 3), (2, 5)])
+    q, K, V = synth(7, NL, B, H, G, d, seq, seq, torch.bfloat16)
+    dec = P.HybridDecoder(n_layers=NL, batch=B, n_kv_heads=H, group_size=G, d_head=d, seq_cap=seq,
+                          roles=roles, policy=P.SparsityPolicy.top_p(0.3), dtype=torch.bfloat16)
+    qd, Kd, Vd = q.cuda(), K.cuda(), V.cuda()
+    out = dec.decode_step(qd, Kd, Vd, seq)
+    sets = dec.token_sets()
+    torch.cuda.synchronize()
+    scale = 1 / np.sqrt(d)
+    qf, Kf, Vf = q.float().numpy(), K.float().numpy(), V.float().numpy()
+    r = orc.decode_step(qf[:, 0], Kf[:, 0], Vf[:, 0], roles, seq=seq, scale=scale, kind="topp",
+                        value=0.3, trace=True)
+    assert rel_err(out.float().cpu().numpy()[:, 0], r["out"]) < BF16_TOL
+    for g in range(H):
+        src = max(ll for ll in range(NL) if roles[ll, g] == 0)
+        w = _policy_weights(qf[src, 0], Kf[src, 0, g], G, g, seq, scale)
+        check_policy_set(sets[0][g], r["sets"][g], w, "topp", 0.3)
+    out2 = torch.empty_like(out)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        dec.capture(qd, Kd, Vd, seq, out2, stream=st)
+        dec.replay(stream=st)
+    st.synchronize()
+    assert torch.equal(out2, out)
+    assert all(np.array_equal(a, b) for a, b in zip(dec.token_sets()[0], sets[0]))
