@@ -12,7 +12,7 @@ namespace lyc {
 
 constexpr int kAttnThreads = (kConsumerWarps + kProducerWarps) * 32;
 
-template <typename T, int D>
+template <typename T, int D, bool kEarlyExit>
 __global__ void __launch_bounds__(kAttnThreads, 1) hybrid_attn_kernel(const __grid_constant__ LycAttnParams p) {
   using C = AttnCfg<T, D>;
   extern __shared__ uint8_t smem_raw[];
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) hybrid_attn_kernel(const __gr
     produce_units<T, D>(p.v, &p.tmap_k, &p.tmap_v, sm.ring, sm.full, sm.empty, sm.tinfo, ub, ue, pt, stage,
                         phase, NoWaits{});
   } else {
-    consume_units<T, D>(p.v, sm, ub, ue, warp, lane, stage, phase);
+    consume_units<T, D, kEarlyExit>(p.v, sm, ub, ue, warp, lane, stage, phase);
   }
 }
 
@@ -55,19 +55,25 @@ __global__ void __launch_bounds__(128) split_merge_kernel(const __grid_constant_
 }
 
 // ---------------------------------------------------------------- launchers
-template <typename T, int D>
-static cudaError_t launch_attn_t(const LycAttnParams& p, int batch, cudaStream_t st) {
+template <typename T, int D, bool kEarlyExit>
+static cudaError_t launch_attn_tt(const LycAttnParams& p, int batch, cudaStream_t st) {
   using C = AttnCfg<T, D>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(hybrid_attn_kernel<T, D>,
+    cudaError_t e = cudaFuncSetAttribute(hybrid_attn_kernel<T, D, kEarlyExit>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   dim3 grid(p.v.n_splits, batch);
-  hybrid_attn_kernel<T, D><<<grid, kAttnThreads, C::kSmem, st>>>(p);
+  hybrid_attn_kernel<T, D, kEarlyExit><<<grid, kAttnThreads, C::kSmem, st>>>(p);
   return cudaGetLastError();
+}
+
+template <typename T, int D>
+static cudaError_t launch_attn_t(const LycAttnParams& p, int batch, cudaStream_t st) {
+  return p.v.early_exit ? launch_attn_tt<T, D, true>(p, batch, st)
+                        : launch_attn_tt<T, D, false>(p, batch, st);
 }
 
 cudaError_t launch_attn(const LycAttnParams& p, int dtype, int d, int batch, cudaStream_t st) {

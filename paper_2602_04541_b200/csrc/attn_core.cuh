@@ -179,7 +179,7 @@ struct NoWaits {
 // ---------------------------------------------------------------- producer
 // Streams the tiles of units [ub, ue) of one layer.  `stage`/`phase` persist
 // across calls (the persistent kernel keeps one ring across layers).
-template <typename T, int D, typename Waits>
+template <typename T, int D, typename Waits, bool kEarlyExit = false>
 __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMap* tmk,
                                               const CUtensorMap* tmv, uint8_t* ring,
                                               uint64_t* full, uint64_t* empty, int2* tinfo,
@@ -262,22 +262,16 @@ __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMa
         }
         uint8_t* kd = ring + stage * C::kStageBytes;
         uint8_t* vd = kd + C::kTileBytes;
-        if (t.nvalid <= 0) {
-          // a variable-size set (device count) ended inside this unit: one
-          // empty tile tells the consumers, both sides leave the unit
+        if (kEarlyExit && t.nvalid <= 0) {
+          // past the end of a variable-size set (device count): an empty tile,
+          // no copies; the consumers skip it
           mbar_wait(&empty[stage], phase ^ 1);
           if (pt == 0) {
             tinfo[stage] = make_int2(t.lo, 0);
             mbar_arrive(&full[stage]);
           }
           mbar_arrive(&full[stage]);
-          if (++stage == ring_stages<C>(p)) {
-            stage = 0;
-            phase ^= 1;
-          }
-          break;
-        }
-        if (t.ids == nullptr && t.nvalid == LYC_TILE) {
+        } else if (t.ids == nullptr && t.nvalid == LYC_TILE) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (pt == 0) {
             // the tile's rows for the consumers (no global loads on their side);
@@ -471,7 +465,7 @@ __device__ __forceinline__ void stage_unit_records(const LycView& p, UnitRec* re
   }
 }
 
-template <int D>
+template <int D, bool kEarlyExit = false>
 __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnSmem<__nv_bfloat16, D>& sm,
                                                    int ub, int ue, int warp, int lane, int& stage,
                                                    uint32_t& phase, int rec_buf = -1) {
@@ -550,15 +544,14 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
       for (int sub = 0; sub < tpi; ++sub) {
         mbar_wait(&sm.full[stage], phase);
         const int2 t = sm.tinfo[stage];  // (first row, valid rows)
-        if (t.y <= 0) {  // the unit's set ended (variable-size set): leave the unit
+        if (kEarlyExit && t.y <= 0) {  // past the end of a variable-size set: skip
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.empty[stage]);
           if (++stage == ring_stages<C>(p)) {
             stage = 0;
             phase ^= 1;
           }
-          it = un.end;
-          break;
+          continue;
         }
         if (first_tile) {
           cstamp(p, 17, tid);
@@ -694,7 +687,7 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
 // CUDA-core FP32 (exact fp32 products); used for the fp32 parity configs.
 // Lane l of warp w owns row t0 + (l & 15) for the scores (half h = l >> 4 of
 // the d range), and d columns l, l+32, ... for PV.  Tiles are unswizzled.
-template <int D>
+template <int D, bool kEarlyExit = false>
 __device__ __forceinline__ void consume_units_f32(const LycView& p, const AttnSmem<float, D>& sm,
                                                   int ub, int ue, int warp, int lane, int& stage,
                                                   uint32_t& phase) {
@@ -738,15 +731,14 @@ __device__ __forceinline__ void consume_units_f32(const LycView& p, const AttnSm
       for (int sub = 0; sub < tpi; ++sub) {
         mbar_wait(&sm.full[stage], phase);
         const int2 t = sm.tinfo[stage];  // (first row, valid rows)
-        if (t.y <= 0) {  // the unit's set ended (variable-size set): leave the unit
+        if (kEarlyExit && t.y <= 0) {  // past the end of a variable-size set: skip
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.empty[stage]);
           if (++stage == ring_stages<C>(p)) {
             stage = 0;
             phase ^= 1;
           }
-          it = un.end;
-          break;
+          continue;
         }
         const uint8_t* ks = sm.ring + stage * C::kStageBytes;
         const float* krow = reinterpret_cast<const float*>(ks + (t0 + tr) * C::kRowBytes);
@@ -843,14 +835,17 @@ __device__ __forceinline__ void consume_units_f32(const LycView& p, const AttnSm
   }
 }
 
-template <typename T, int D>
+// kEarlyExit: units may end early (variable-size sets with device counts:
+// TopP / Threshold, sequence shards); compiled out of the step kernel, whose
+// tile loop is sensitive to the extra exit path.
+template <typename T, int D, bool kEarlyExit = false>
 __device__ __forceinline__ void consume_units(const LycView& p, const AttnSmem<T, D>& sm, int ub,
                                               int ue, int warp, int lane, int& stage,
                                               uint32_t& phase, int rec_buf = -1) {
   if constexpr (sizeof(T) == 2)
-    consume_units_bf16<D>(p, sm, ub, ue, warp, lane, stage, phase, rec_buf);
+    consume_units_bf16<D, kEarlyExit>(p, sm, ub, ue, warp, lane, stage, phase, rec_buf);
   else
-    consume_units_f32<D>(p, sm, ub, ue, warp, lane, stage, phase);
+    consume_units_f32<D, kEarlyExit>(p, sm, ub, ue, warp, lane, stage, phase);
 }
 
 // ---------------------------------------------------------------- merge

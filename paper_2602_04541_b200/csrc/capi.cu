@@ -743,6 +743,7 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
     v.scale = d->cfg.scale;
     v.scale_log2 = d->cfg.scale * 1.4426950408889634f;
     v.stages = d->stages;
+    v.early_exit = (d->variable_sets() || d->shard) ? 1 : 0;
     LycMergeParams& mp = ly.mp;
     std::memset(&mp, 0, sizeof(mp));
     mp.part_o = d->part_o;

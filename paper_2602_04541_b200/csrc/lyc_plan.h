@@ -81,6 +81,7 @@ struct LycView {
   float scale;              // softmax scale (1/sqrt(d))
   float scale_log2;         // scale * log2(e)
   int32_t stages;           // ring stages in use (<= the kernel's capacity; 0 = all)
+  int32_t early_exit;       // per-layer kernel: units may end early (device-count sets)
 };
 
 struct LycAttnParams {

@@ -164,6 +164,7 @@ __device__ __forceinline__ LycView layer_view(const LycStepParams& p, const LycL
   v.scale = p.scale;
   v.scale_log2 = p.scale_log2;
   v.stages = p.stages;
+  v.early_exit = 0;
   v.trace_l = p.trace ? p.trace + (size_t)l * LYC_TRACE_EVENTS * p.n_ctas : nullptr;
   v.slot_ctr = p.sel_rowctr + (size_t)l * p.max_sel * 16;
   v.trace_ctas = p.n_ctas;
