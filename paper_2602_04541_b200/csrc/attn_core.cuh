@@ -29,6 +29,8 @@
 //     a normalized partial + base-2 LSE (kernel_sim.hpp:195-198), or as the
 //     final output when the slot has a single unit.
 #pragma once
+#include <type_traits>
+
 #include "lyc_common.cuh"
 #include "lyc_plan.h"
 
@@ -540,124 +542,133 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
     const bool want_sel = s.sel >= 0 && p.sel_mode != SEL_NONE;
     uint32_t* hist = (want_sel && p.hist1) ? p.hist1 + (int64_t)s.sel * LYC_H1_ROW : nullptr;
 
-    for (int it = un.begin; it < un.end; ++it) {
-      for (int sub = 0; sub < tpi; ++sub) {
-        mbar_wait(&sm.full[stage], phase);
-        const int2 t = sm.tinfo[stage];  // (first row, valid rows)
-        if (kEarlyExit && t.y <= 0) {  // past the end of a variable-size set: skip
+    // the tile loop in two copies: with the fused selection scoring
+    // (retrieval units) and without it -- no per-tile branch on it
+    auto tiles = [&](auto sel_c) {
+      constexpr bool kSel = decltype(sel_c)::value;
+      for (int it = un.begin; it < un.end; ++it) {
+        for (int sub = 0; sub < tpi; ++sub) {
+          mbar_wait(&sm.full[stage], phase);
+          const int2 t = sm.tinfo[stage];  // (first row, valid rows)
+          if (kEarlyExit && t.y <= 0) {  // past the end of a variable-size set: skip
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.empty[stage]);
+            if (++stage == ring_stages<C>(p)) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
+          if (first_tile) {
+            cstamp(p, 17, tid);
+            first_tile = false;
+          }
+          cstamp(p, 19, tid);
+          const uint8_t* ks = sm.ring + stage * C::kStageBytes;
+          const uint8_t* vs = ks + C::kTileBytes;
+          // ---- S = Q K^T for this warp's 16 rows (two n-tiles of 8)
+          // two independent accumulator chains (even / odd k-steps) halve the
+          // dependent-MMA latency of a tile; summed once at the end
+          float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+          float sd[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+  #pragma unroll
+          for (int kk = 0; kk < KS; ++kk) {
+            uint32_t b0, b1, b2, b3;
+            const int c = 2 * (kk & 3) + k_x;
+            ldsm_x4(b0, b1, b2, b3, ks + (kk >> 2) * C::kPanelBytes + k_row + ((c ^ sw) << 4));
+            float (&acc)[2][4] = (kk & 1) ? sd : sc;
+            mma_bf16(acc[0], qa0[kk], 0u, qa2[kk], 0u, b0, b1);
+            mma_bf16(acc[1], qa0[kk], 0u, qa2[kk], 0u, b2, b3);
+          }
+  #pragma unroll
+          for (int n = 0; n < 2; ++n)
+  #pragma unroll
+            for (int e = 0; e < 4; ++e) sc[n][e] += sd[n][e];
+          // ---- fused selection score: sum over packed rows (rows >= G are 0)
+          if constexpr (kSel) {
+            float ps[2][2];
+  #pragma unroll
+            for (int n = 0; n < 2; ++n)
+  #pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                float v = sc[n][e];
+                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                v += __shfl_xor_sync(0xffffffffu, v, 8);
+                v += __shfl_xor_sync(0xffffffffu, v, 16);
+                ps[n][e] = v;
+              }
+            if (p.sel_mode == SEL_TOKEN_KEYS) {
+              // lane r < 16 gathers row t0 + r's score (held by lane (r & 7) >> 1
+              // as ps[r >> 3][r & 1]) so the warp's 16 keys go out in one
+              // coalesced 64-B store and one shared-memory atomic
+              const int r = lane & 15, src = (r & 7) >> 1;
+              const float v00 = __shfl_sync(0xffffffffu, ps[0][0], src);
+              const float v01 = __shfl_sync(0xffffffffu, ps[0][1], src);
+              const float v10 = __shfl_sync(0xffffffffu, ps[1][0], src);
+              const float v11 = __shfl_sync(0xffffffffu, ps[1][1], src);
+              const float mine = (r >> 3) ? ((r & 1) ? v11 : v10) : ((r & 1) ? v01 : v00);
+              if (lane < 16 && t0 + r < t.y) {
+                const uint32_t key = float_key(mine);
+                p.sel_keys[(int64_t)s.sel * p.sel_stride + t.x + t0 + r] = key;
+                if (hist) atomicAdd(sm.hist + (key >> (32 - LYC_H1_BITS)), 1u);
+              }
+            } else {  // SEL_BLOCK_KEYS: max over valid rows of this block
+              uint32_t km = 0u;
+  #pragma unroll
+              for (int n = 0; n < 2; ++n)
+  #pragma unroll
+                for (int e = 0; e < 2; ++e)
+                  if (t0 + n * 8 + qc + e < t.y) km = max(km, float_key(ps[n][e]));
+              km = max(km, __shfl_xor_sync(0xffffffffu, km, 1));
+              km = max(km, __shfl_xor_sync(0xffffffffu, km, 2));
+              if (lane == 0 && km != 0u)
+                atomicMax(p.sel_keys + (int64_t)s.sel * p.sel_stride + it, km);
+            }
+          }
+          // ---- online softmax (exp2 domain) for row qr
+          float x[2][2];
+  #pragma unroll
+          for (int n = 0; n < 2; ++n)
+  #pragma unroll
+            for (int e = 0; e < 2; ++e)
+              x[n][e] = t0 + n * 8 + qc + e < t.y ? sc[n][e] * p.scale_log2 : -INFINITY;
+          const float mx = warp_max4(fmaxf(fmaxf(x[0][0], x[0][1]), fmaxf(x[1][0], x[1][1])));
+          const float mn = fmaxf(m0, mx);
+          const float rs = m0 == -INFINITY ? 0.f : fast_exp2(m0 - mn);
+          const float mu = mn == -INFINITY ? 0.f : mn;
+          const float p00 = fast_exp2(x[0][0] - mu), p01 = fast_exp2(x[0][1] - mu);
+          const float p10 = fast_exp2(x[1][0] - mu), p11 = fast_exp2(x[1][1] - mu);
+          l0 = l0 * rs + p00 + p01 + p10 + p11;
+          m0 = mn;
+  #pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            o[n][0] *= rs;
+            o[n][1] *= rs;
+          }
+          // ---- O += P V ; P (C layout) -> A fragment without a smem round trip
+          const uint32_t pa0 = pack_bf16(p00, p01);
+          const uint32_t pa2 = pack_bf16(p10, p11);
+  #pragma unroll
+          for (int n2 = 0; n2 < D / 16; ++n2) {
+            uint32_t b0, b1, b2, b3;
+            const int c = 2 * (n2 & 3) + v_x;
+            ldsm_x4_t(b0, b1, b2, b3, vs + (n2 >> 2) * C::kPanelBytes + v_row + ((c ^ sw) << 4));
+            mma_bf16(o[2 * n2], pa0, 0u, pa2, 0u, b0, b1);
+            mma_bf16(o[2 * n2 + 1], pa0, 0u, pa2, 0u, b2, b3);
+          }
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.empty[stage]);
           if (++stage == ring_stages<C>(p)) {
             stage = 0;
             phase ^= 1;
           }
-          continue;
-        }
-        if (first_tile) {
-          cstamp(p, 17, tid);
-          first_tile = false;
-        }
-        cstamp(p, 19, tid);
-        const uint8_t* ks = sm.ring + stage * C::kStageBytes;
-        const uint8_t* vs = ks + C::kTileBytes;
-        // ---- S = Q K^T for this warp's 16 rows (two n-tiles of 8)
-        // two independent accumulator chains (even / odd k-steps) halve the
-        // dependent-MMA latency of a tile; summed once at the end
-        float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-        float sd[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-#pragma unroll
-        for (int kk = 0; kk < KS; ++kk) {
-          uint32_t b0, b1, b2, b3;
-          const int c = 2 * (kk & 3) + k_x;
-          ldsm_x4(b0, b1, b2, b3, ks + (kk >> 2) * C::kPanelBytes + k_row + ((c ^ sw) << 4));
-          float (&acc)[2][4] = (kk & 1) ? sd : sc;
-          mma_bf16(acc[0], qa0[kk], 0u, qa2[kk], 0u, b0, b1);
-          mma_bf16(acc[1], qa0[kk], 0u, qa2[kk], 0u, b2, b3);
-        }
-#pragma unroll
-        for (int n = 0; n < 2; ++n)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) sc[n][e] += sd[n][e];
-        // ---- fused selection score: sum over packed rows (rows >= G are 0)
-        if (want_sel) {
-          float ps[2][2];
-#pragma unroll
-          for (int n = 0; n < 2; ++n)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              float v = sc[n][e];
-              v += __shfl_xor_sync(0xffffffffu, v, 4);
-              v += __shfl_xor_sync(0xffffffffu, v, 8);
-              v += __shfl_xor_sync(0xffffffffu, v, 16);
-              ps[n][e] = v;
-            }
-          if (p.sel_mode == SEL_TOKEN_KEYS) {
-            // lane r < 16 gathers row t0 + r's score (held by lane (r & 7) >> 1
-            // as ps[r >> 3][r & 1]) so the warp's 16 keys go out in one
-            // coalesced 64-B store and one shared-memory atomic
-            const int r = lane & 15, src = (r & 7) >> 1;
-            const float v00 = __shfl_sync(0xffffffffu, ps[0][0], src);
-            const float v01 = __shfl_sync(0xffffffffu, ps[0][1], src);
-            const float v10 = __shfl_sync(0xffffffffu, ps[1][0], src);
-            const float v11 = __shfl_sync(0xffffffffu, ps[1][1], src);
-            const float mine = (r >> 3) ? ((r & 1) ? v11 : v10) : ((r & 1) ? v01 : v00);
-            if (lane < 16 && t0 + r < t.y) {
-              const uint32_t key = float_key(mine);
-              p.sel_keys[(int64_t)s.sel * p.sel_stride + t.x + t0 + r] = key;
-              if (hist) atomicAdd(sm.hist + (key >> (32 - LYC_H1_BITS)), 1u);
-            }
-          } else {  // SEL_BLOCK_KEYS: max over valid rows of this block
-            uint32_t km = 0u;
-#pragma unroll
-            for (int n = 0; n < 2; ++n)
-#pragma unroll
-              for (int e = 0; e < 2; ++e)
-                if (t0 + n * 8 + qc + e < t.y) km = max(km, float_key(ps[n][e]));
-            km = max(km, __shfl_xor_sync(0xffffffffu, km, 1));
-            km = max(km, __shfl_xor_sync(0xffffffffu, km, 2));
-            if (lane == 0 && km != 0u)
-              atomicMax(p.sel_keys + (int64_t)s.sel * p.sel_stride + it, km);
-          }
-        }
-        // ---- online softmax (exp2 domain) for row qr
-        float x[2][2];
-#pragma unroll
-        for (int n = 0; n < 2; ++n)
-#pragma unroll
-          for (int e = 0; e < 2; ++e)
-            x[n][e] = t0 + n * 8 + qc + e < t.y ? sc[n][e] * p.scale_log2 : -INFINITY;
-        const float mx = warp_max4(fmaxf(fmaxf(x[0][0], x[0][1]), fmaxf(x[1][0], x[1][1])));
-        const float mn = fmaxf(m0, mx);
-        const float rs = m0 == -INFINITY ? 0.f : fast_exp2(m0 - mn);
-        const float mu = mn == -INFINITY ? 0.f : mn;
-        const float p00 = fast_exp2(x[0][0] - mu), p01 = fast_exp2(x[0][1] - mu);
-        const float p10 = fast_exp2(x[1][0] - mu), p11 = fast_exp2(x[1][1] - mu);
-        l0 = l0 * rs + p00 + p01 + p10 + p11;
-        m0 = mn;
-#pragma unroll
-        for (int n = 0; n < NT; ++n) {
-          o[n][0] *= rs;
-          o[n][1] *= rs;
-        }
-        // ---- O += P V ; P (C layout) -> A fragment without a smem round trip
-        const uint32_t pa0 = pack_bf16(p00, p01);
-        const uint32_t pa2 = pack_bf16(p10, p11);
-#pragma unroll
-        for (int n2 = 0; n2 < D / 16; ++n2) {
-          uint32_t b0, b1, b2, b3;
-          const int c = 2 * (n2 & 3) + v_x;
-          ldsm_x4_t(b0, b1, b2, b3, vs + (n2 >> 2) * C::kPanelBytes + v_row + ((c ^ sw) << 4));
-          mma_bf16(o[2 * n2], pa0, 0u, pa2, 0u, b0, b1);
-          mma_bf16(o[2 * n2 + 1], pa0, 0u, pa2, 0u, b2, b3);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.empty[stage]);
-        if (++stage == ring_stages<C>(p)) {
-          stage = 0;
-          phase ^= 1;
         }
       }
-    }
+    };
+    if (want_sel)
+      tiles(std::true_type{});
+    else
+      tiles(std::false_type{});
     // ---- per-warp state -> smem, then cross-warp merge
     l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
     l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
