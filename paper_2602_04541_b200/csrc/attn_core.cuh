@@ -511,7 +511,6 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
   }
   consumer_bar();
   cstamp(p, 16, tid);
-  bool first_tile = true;
 
   for (int u = ub; u < ue; ++u) {
     const bool staged = u - ub < kQU;
@@ -545,7 +544,7 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
     // the tile loop in two copies: with the fused selection scoring
     // (retrieval units) and without it -- no per-tile branch on it
     auto tiles = [&](auto sel_c) {
-      constexpr bool kSel = decltype(sel_c)::value;
+      constexpr int kSel = decltype(sel_c)::value;  // 0 none, 1 token keys, 2 block keys
       for (int it = un.begin; it < un.end; ++it) {
         for (int sub = 0; sub < tpi; ++sub) {
           mbar_wait(&sm.full[stage], phase);
@@ -559,11 +558,6 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
             }
             continue;
           }
-          if (first_tile) {
-            cstamp(p, 17, tid);
-            first_tile = false;
-          }
-          cstamp(p, 19, tid);
           const uint8_t* ks = sm.ring + stage * C::kStageBytes;
           const uint8_t* vs = ks + C::kTileBytes;
           // ---- S = Q K^T for this warp's 16 rows (two n-tiles of 8)
@@ -585,7 +579,7 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
   #pragma unroll
             for (int e = 0; e < 4; ++e) sc[n][e] += sd[n][e];
           // ---- fused selection score: sum over packed rows (rows >= G are 0)
-          if constexpr (kSel) {
+          if constexpr (kSel != 0) {
             float ps[2][2];
   #pragma unroll
             for (int n = 0; n < 2; ++n)
@@ -597,7 +591,7 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
                 v += __shfl_xor_sync(0xffffffffu, v, 16);
                 ps[n][e] = v;
               }
-            if (p.sel_mode == SEL_TOKEN_KEYS) {
+            if constexpr (kSel == 1) {
               // lane r < 16 gathers row t0 + r's score (held by lane (r & 7) >> 1
               // as ps[r >> 3][r & 1]) so the warp's 16 keys go out in one
               // coalesced 64-B store and one shared-memory atomic
@@ -665,10 +659,12 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
         }
       }
     };
-    if (want_sel)
-      tiles(std::true_type{});
+    if (!want_sel)
+      tiles(std::integral_constant<int, 0>{});
+    else if (p.sel_mode == SEL_TOKEN_KEYS)
+      tiles(std::integral_constant<int, 1>{});
     else
-      tiles(std::false_type{});
+      tiles(std::integral_constant<int, 2>{});
     // ---- per-warp state -> smem, then cross-warp merge
     l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
     l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
