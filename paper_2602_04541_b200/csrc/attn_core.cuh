@@ -545,8 +545,11 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
     // (retrieval units) and without it -- no per-tile branch on it
     auto tiles = [&](auto sel_c) {
       constexpr int kSel = decltype(sel_c)::value;  // 0 none, 1 token keys, 2 block keys
-      for (int it = un.begin; it < un.end; ++it) {
-        for (int sub = 0; sub < tpi; ++sub) {
+      // one flat loop over the unit's tiles (item it, sub-tile sub)
+      const int nt = (un.end - un.begin) * tpi;
+      int it = un.begin, sub = 0;
+      for (int f = 0; f < nt; ++f) {
+        {
           mbar_wait(&sm.full[stage], phase);
           const int2 t = sm.tinfo[stage];  // (first row, valid rows)
           if (kEarlyExit && t.y <= 0) {  // past the end of a variable-size set: skip
@@ -555,6 +558,10 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
             if (++stage == ring_stages<C>(p)) {
               stage = 0;
               phase ^= 1;
+            }
+            if (++sub == tpi) {
+              sub = 0;
+              ++it;
             }
             continue;
           }
@@ -656,6 +663,10 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
             stage = 0;
             phase ^= 1;
           }
+        }
+        if (++sub == tpi) {
+          sub = 0;
+          ++it;
         }
       }
     };
