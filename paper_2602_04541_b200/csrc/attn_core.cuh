@@ -539,7 +539,9 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
 #pragma unroll
     for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
     const bool want_sel = s.sel >= 0 && p.sel_mode != SEL_NONE;
-    uint32_t* hist = (want_sel && p.hist1) ? p.hist1 + (int64_t)s.sel * LYC_H1_ROW : nullptr;
+    uint32_t* hist = (want_sel && p.hist1) ? p.hist1 + (int64_t)s.sel * LYC_H1_STRIDE +
+                                                 (blockIdx.x % LYC_H1_COPIES) * LYC_H1_ROW
+                                           : nullptr;
 
     // the tile loop in two copies: with the fused selection scoring
     // (retrieval units) and without it -- no per-tile branch on it
@@ -723,7 +725,9 @@ __device__ __forceinline__ void consume_units_f32(const LycView& p, const AttnSm
     const LycSlot s = p.slots[un.slot];
     const int tpi = tiles_per_item(s, p.block_size);
     const bool want_sel = s.sel >= 0 && p.sel_mode != SEL_NONE;
-    uint32_t* hist = (want_sel && p.hist1) ? p.hist1 + (int64_t)s.sel * LYC_H1_ROW : nullptr;
+    uint32_t* hist = (want_sel && p.hist1) ? p.hist1 + (int64_t)s.sel * LYC_H1_STRIDE +
+                                                 (blockIdx.x % LYC_H1_COPIES) * LYC_H1_ROW
+                                           : nullptr;
     float m[kMaxG], l[kMaxG], o[kMaxG][DC];
 #pragma unroll
     for (int j = 0; j < kMaxG; ++j) {

@@ -988,8 +988,8 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
       cuda_check(cudaMemset(d->idx_count, 0, rows * 4), "memset");
       cuda_check(cudaMalloc(&d->sel_keys, 2 * rows * d->sel_stride * 4), "cudaMalloc keys");
       cuda_check(cudaMemset(d->sel_keys, 0, 2 * rows * d->sel_stride * 4), "memset");
-      cuda_check(cudaMalloc(&d->hist, 2 * rows * LYC_H1_ROW * 4), "cudaMalloc hist");
-      cuda_check(cudaMemset(d->hist, 0, 2 * rows * LYC_H1_ROW * 4), "memset");
+      cuda_check(cudaMalloc(&d->hist, 2 * rows * LYC_H1_STRIDE * 4), "cudaMalloc hist");
+      cuda_check(cudaMemset(d->hist, 0, 2 * rows * LYC_H1_STRIDE * 4), "memset");
       if (d->fused && c.select_mode != LYC_SELECT_NONE) {  // pooled-selection scratch
         d->bitmap_stride = (lyc::step_bitmap_words(d->sel_stride) + 3) & ~(int64_t)3;
         cuda_check(cudaMalloc(&d->sel_bitmap, 2 * rows * d->bitmap_stride * 4), "cudaMalloc bitmap");

@@ -23,6 +23,11 @@
 // Global h1 rows carry 64 coarse bins (top 6 bits) after the fine bins.
 #define LYC_H1_COARSE 64
 #define LYC_H1_ROW (LYC_H1_BINS + LYC_H1_COARSE)
+// Each selection row keeps LYC_H1_COPIES copies of its first-pass histogram;
+// CTA c flushes into copy c % LYC_H1_COPIES (fewer same-address reductions in
+// L2 -- the release that publishes a unit waits for them); readers sum them.
+#define LYC_H1_COPIES 8
+#define LYC_H1_STRIDE (LYC_H1_COPIES * LYC_H1_ROW)
 #define LYC_TRACE_EVENTS 24  // step-timeline stamps per layer per CTA
 
 enum { ITEM_DENSE = 0, ITEM_BLOCKS = 1, ITEM_TOKENS = 2 };

@@ -151,7 +151,7 @@ __device__ __forceinline__ LycView layer_view(const LycStepParams& p, const LycL
   v.part_o = p.part_o;
   v.part_lse = p.part_lse;
   v.sel_keys = p.sel_keys + (int64_t)(l & 1) * p.max_sel * p.sel_stride;
-  v.hist1 = p.sel_mode == SEL_TOKEN_KEYS ? p.hist + (int64_t)(l & 1) * p.max_sel * LYC_H1_ROW
+  v.hist1 = p.sel_mode == SEL_TOKEN_KEYS ? p.hist + (int64_t)(l & 1) * p.max_sel * LYC_H1_STRIDE
                                          : nullptr;
   v.exec_counts = nullptr;
   v.sel_stride = p.sel_stride;
@@ -313,7 +313,7 @@ __device__ __forceinline__ SelRow sel_row(const LycStepParams& p, int l, int r) 
   const int64_t pr = (int64_t)(l & 1) * p.max_sel + r;
   SelRow s;
   s.keys = p.sel_keys + pr * p.sel_stride;
-  s.h1 = p.sel_mode == SEL_TOKEN_KEYS ? p.hist + pr * LYC_H1_ROW : nullptr;
+  s.h1 = p.sel_mode == SEL_TOKEN_KEYS ? p.hist + pr * LYC_H1_STRIDE : nullptr;
   s.bitmap = p.sel_bitmap + pr * p.bitmap_stride;
   s.ckey = p.sel_cand + pr * 3 * p.sel_stride;
   s.cidx = s.ckey + p.sel_stride;
@@ -338,7 +338,13 @@ __device__ __forceinline__ void row_prefix(const LycStepParams& p, const SelRow&
       const uint32_t* h = R.h1 + LYC_H1_BINS;
 #pragma unroll
       for (int level = 0; level < 2; ++level) {
-        const uint2 v = __ldcg(reinterpret_cast<const uint2*>(h) + (31 - et));
+        uint2 v = make_uint2(0u, 0u);
+#pragma unroll
+        for (int c = 0; c < LYC_H1_COPIES; ++c) {
+          const uint2 w = __ldcg(reinterpret_cast<const uint2*>(h + c * LYC_H1_ROW) + (31 - et));
+          v.x += w.x;
+          v.y += w.y;
+        }
         const uint32_t sum = v.x + v.y;
         const uint32_t incl = warp_incl_scan(sum, et);
         const unsigned who = __ballot_sync(0xffffffffu, incl - sum < k && k <= incl);
@@ -545,10 +551,12 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
       bulk_g2s(sidx, R.cidx, 4u * (uint32_t)spec, &es.bar);
     }
   }
-  if (R.h1) {  // every item has read the row's first-pass histogram: item q re-zeroes its share
-    const int per = (LYC_H1_ROW + items - 1) / items;
-    const int b1 = min(LYC_H1_ROW, (q + 1) * per);
-    for (int b = q * per + et; b < b1; b += kEpiThreads) R.h1[b] = 0u;
+  if (R.h1) {  // every item has read the row's first-pass histograms: item q re-zeroes its share
+    constexpr int kVec = LYC_H1_STRIDE / 4;
+    const int per = (kVec + items - 1) / items;
+    const int b1 = min(kVec, (q + 1) * per);
+    for (int b = q * per + et; b < b1; b += kEpiThreads)
+      reinterpret_cast<uint4*>(R.h1)[b] = make_uint4(0u, 0u, 0u, 0u);
   }
   uint32_t P = __ldcg(R.ccnt + 192);
   int shift = (int)__ldcg(R.ccnt + 194);
