@@ -590,11 +590,31 @@ void plan_step_launch(HostLaunch& L, int batch, int heads, int splits, int group
         }
       }
       if (tot == 0) continue;
+      // even cut points, then snapped onto a head boundary within one item:
+      // a split that would hold the end of one head and the start of the next
+      // (two units: an extra unit epilogue and signal) gets one item more or
+      // less instead
       const int64_t base = tot / splits, rem = tot % splits;
+      std::vector<int64_t> cut((size_t)splits + 1);
+      for (int sp = 0; sp <= splits; ++sp) cut[(size_t)sp] = sp * base + std::min<int64_t>(sp, rem);
+      {
+        int64_t hb = 0;
+        for (size_t h = 0; h + 1 < hs.size(); ++h) {
+          hb += L.slots[(size_t)b * heads + hs[h]].n_items;
+          // the cut nearest to the boundary hb
+          int sp = (int)std::min<int64_t>(splits - 1, std::max<int64_t>(1, hb / std::max<int64_t>(base, 1)));
+          while (sp > 1 && cut[(size_t)sp] > hb) --sp;
+          while (sp < splits - 1 && cut[(size_t)sp + 1] <= hb) ++sp;
+          for (int c = sp; c <= sp + 1 && c < splits; ++c)
+            if (c >= 1 && std::llabs(cut[(size_t)c] - hb) <= 1 && cut[(size_t)c - 1] < hb &&
+                hb < cut[(size_t)c + 1])
+              cut[(size_t)c] = hb;
+        }
+      }
       size_t hi = 0;
       int64_t offset = 0;
       for (int sp = 0; sp < splits; ++sp) {
-        int64_t want = base + (sp < rem ? 1 : 0);
+        int64_t want = cut[(size_t)sp + 1] - cut[(size_t)sp];
         while (want > 0) {
           while (L.slots[(size_t)b * heads + hs[hi]].n_items == offset) {
             ++hi;
