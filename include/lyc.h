@@ -215,6 +215,27 @@ int lyc_shard_merge(lyc_decoder* dec, int32_t layer, int32_t world, const float*
                     int64_t rank_stride, int64_t n_local, int64_t row_begin, int64_t seq_total,
                     void* out_l, int32_t* global_sets, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Device KV write path (kv_cache.hpp:14-69).  The device
+ * cache is the decoder's layout [n_layers][B][H][seq_cap][d] (dtype elements),
+ * one K and one V allocation.  lyc_kv_write copies n_rows rows per (b, g) of
+ * one layer, from src [B][H][n_rows][d] (same dtype, contiguous) to cache rows
+ * [pos, pos + n_rows):
+ *   KvCache::append (23-29) + commit_row (32): n_rows = 1 at pos = length,
+ *     every head of the layer at once (the caller advances the length);
+ *   KvCache::overwrite (34-42): n_rows = 1 at any pos < length, or a window
+ *     (cache correction rewrites the trailing W rows).
+ * LYC_EINVAL when pos + n_rows > seq_cap or the layer is out of range.
+ * Stream-ordered, graph-capturable, no allocation. */
+typedef struct lyc_kv_layout {
+  int32_t n_layers, batch, n_kv_heads, d_head;
+  int32_t dtype;         /* LYC_DTYPE_* */
+  int32_t pad;
+  int64_t seq_cap;
+} lyc_kv_layout;
+int lyc_kv_write(void* k_cache, void* v_cache, const lyc_kv_layout* layout, int32_t layer,
+                 int64_t pos, int64_t n_rows, const void* k_src, const void* v_src, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

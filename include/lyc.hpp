@@ -456,6 +456,43 @@ struct SparsityPolicy {
 enum class Dtype { F32 = LYC_DTYPE_F32, BF16 = LYC_DTYPE_BF16 };
 enum class Select { Tokens = LYC_SELECT_TOKENS, Blocks = LYC_SELECT_BLOCKS, None = LYC_SELECT_NONE };
 
+// Device KV cache write path (kv_cache.hpp:14-69) over caller-owned device
+// caches in the decoder layout [n_layers][B][H][seq_cap][d]: append writes one
+// row per (b, g) of a layer at length() (KvCache::append, 23-29), commit_row
+// advances the shared length (32), overwrite rewrites rows below it (34-42;
+// n_rows > 1 for the cache-correction window).  Rows are [B][H][n_rows][d] in
+// the cache dtype.
+class KvCache {
+ public:
+  KvCache(int n_layers, int batch, int n_kv_heads, int d_head, std::size_t seq_cap, Dtype dtype,
+          void* k_cache, void* v_cache)
+      : k_(k_cache), v_(v_cache) {
+    lay_.n_layers = n_layers;
+    lay_.batch = batch;
+    lay_.n_kv_heads = n_kv_heads;
+    lay_.d_head = d_head;
+    lay_.dtype = (int32_t)dtype;
+    lay_.pad = 0;
+    lay_.seq_cap = (int64_t)seq_cap;
+  }
+  std::size_t length() const { return length_; }
+  void append(int layer, const void* k_rows, const void* v_rows, void* stream = nullptr) {
+    check(lyc_kv_write(k_, v_, &lay_, layer, (int64_t)length_, 1, k_rows, v_rows, stream));
+  }
+  void commit_row() { ++length_; }
+  void overwrite(int layer, std::size_t pos, std::size_t n_rows, const void* k_rows,
+                 const void* v_rows, void* stream = nullptr) {
+    if (pos + n_rows > length_) throw std::invalid_argument("KvCache: overwrite beyond the committed length");
+    check(lyc_kv_write(k_, v_, &lay_, layer, (int64_t)pos, (int64_t)n_rows, k_rows, v_rows, stream));
+  }
+
+ private:
+  void* k_;
+  void* v_;
+  lyc_kv_layout lay_{};
+  std::size_t length_ = 0;
+};
+
 // The decode-step attention loop of DecodeEngine (decode_engine.hpp:109-151)
 // over device-resident caches: per layer, retrieval heads (layer 0, or role
 // Retrieval in the role map; rolemap.hpp:33-35) run dense split-KV attention

@@ -27,7 +27,7 @@ SYMBOLS = [
     "lyc_decoder_replay", "lyc_decoder_index_cache", "lyc_decoder_launches_per_step",
     "lyc_decoder_step_bytes", "lyc_decoder_layer_attn_bytes", "lyc_decoder_set_timing",
     "lyc_decoder_attn_ms", "lyc_decoder_is_fused", "lyc_decoder_set_trace", "lyc_decoder_trace",
-    "lyc_shard_layer", "lyc_shard_merge",
+    "lyc_shard_layer", "lyc_shard_merge", "lyc_kv_write",
 ]
 
 
@@ -68,6 +68,13 @@ class lyc_decode_config(C.Structure):
         ("seq_cap", C.c_int64), ("policy_kind", C.c_int32), ("select_mode", C.c_int32),
         ("top_k", C.c_int64), ("ratio", C.c_double), ("block_size", C.c_int32),
         ("num_splits", C.c_int32), ("scale", C.c_float), ("roles", C.c_void_p),
+    ]
+
+
+class lyc_kv_layout(C.Structure):
+    _fields_ = [
+        ("n_layers", C.c_int32), ("batch", C.c_int32), ("n_kv_heads", C.c_int32),
+        ("d_head", C.c_int32), ("dtype", C.c_int32), ("pad", C.c_int32), ("seq_cap", C.c_int64),
     ]
 
 
@@ -131,6 +138,8 @@ def lib() -> C.CDLL:
     L.lyc_shard_layer.argtypes = [vp, i32, vp, vp, vp, i64, i64, vp, vp, vp, vp, vp]
     L.lyc_shard_merge.restype = C.c_int
     L.lyc_shard_merge.argtypes = [vp, i32, i32, vp, vp, vp, vp, i64, i64, i64, i64, vp, vp, vp]
+    L.lyc_kv_write.restype = C.c_int
+    L.lyc_kv_write.argtypes = [vp, vp, C.POINTER(lyc_kv_layout), i32, i64, i64, vp, vp, vp]
     _lib = L
     return L
 

@@ -1373,3 +1373,54 @@ int64_t lyc_decoder_trace(lyc_decoder* d, unsigned long long* out, int64_t cap) 
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ KV write path
+namespace {
+// One 16-B chunk per thread: (b, g, row, chunk) flattened; src rows are
+// contiguous per (b, g), cache rows are contiguous per slab.
+__global__ void kv_write_kernel(uint4* __restrict__ kc, uint4* __restrict__ vc,
+                                const uint4* __restrict__ ks, const uint4* __restrict__ vs,
+                                int64_t slabs, int64_t n_rows, int64_t chunks, int64_t slab_chunks,
+                                int64_t dst0) {
+  const int64_t total = slabs * n_rows * chunks;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i % chunks, rs = i / chunks;
+    const int64_t r = rs % n_rows, sl = rs / n_rows;
+    const int64_t dst = dst0 + sl * slab_chunks + r * chunks + c;
+    kc[dst] = ks[i];
+    vc[dst] = vs[i];
+  }
+}
+}  // namespace
+
+int lyc_kv_write(void* k_cache, void* v_cache, const lyc_kv_layout* lay, int32_t layer,
+                 int64_t pos, int64_t n_rows, const void* k_src, const void* v_src, void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    if (!lay) fail(LYC_EINVAL, "KvCache: null layout");
+    if (!k_cache || !v_cache || !k_src || !v_src) fail(LYC_EINVAL, "KvCache: null buffer");
+    if (lay->n_layers < 1 || lay->batch < 1 || lay->n_kv_heads < 1 || lay->d_head < 1 ||
+        lay->seq_cap < 1)
+      fail(LYC_EINVAL, "KvCache: all dimensions must be >= 1");
+    if (lay->dtype != LYC_DTYPE_F32 && lay->dtype != LYC_DTYPE_BF16) fail(LYC_EINVAL, "KvCache: dtype");
+    if (layer < 0 || layer >= lay->n_layers) fail(LYC_EINVAL, "KvCache: layer out of range");
+    if (pos < 0 || n_rows < 0 || pos + n_rows > lay->seq_cap)
+      fail(LYC_EINVAL, "KvCache: rows beyond seq_cap");
+    const int64_t row_bytes = (int64_t)lay->d_head * (lay->dtype == LYC_DTYPE_BF16 ? 2 : 4);
+    if (row_bytes % 16) fail(LYC_ENOTSUP, "KvCache: rows must be a multiple of 16 bytes");
+    if (n_rows == 0) return LYC_OK;
+    const int64_t chunks = row_bytes / 16;
+    const int64_t slabs = (int64_t)lay->batch * lay->n_kv_heads;
+    const int64_t slab_chunks = lay->seq_cap * chunks;
+    const int64_t dst0 = ((int64_t)layer * slabs) * slab_chunks + pos * chunks;
+    const int64_t total = slabs * n_rows * chunks;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+    kv_write_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        static_cast<uint4*>(k_cache), static_cast<uint4*>(v_cache),
+        static_cast<const uint4*>(k_src), static_cast<const uint4*>(v_src), slabs, n_rows, chunks,
+        slab_chunks, dst0);
+    cuda_check(cudaGetLastError(), "kv write launch");
+    ++g_launches;
+    return LYC_OK;
+  });
+}

@@ -1,0 +1,107 @@
+"""Device KV write path (kv_cache.hpp:14-69) through the C-ABI lyc_kv_write:
+append + commit_row row by row, window overwrite, errors, and a decode step
+over the appended cache equal (bitwise) to one over the same rows written by
+torch."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2602_04541_b200  # noqa: F401
+    torch.cuda.set_device(0)
+
+
+@pytest.mark.parametrize("dtype,d", [(torch.bfloat16, 128), (torch.float32, 64)])
+def test_append_commit_overwrite(dtype, d):
+    import paper_2602_04541_b200 as P
+    NL, B, H, cap, T = 3, 2, 4, 96, 80
+    kv = P.KvCache(n_layers=NL, batch=B, n_kv_heads=H, d_head=d, seq_cap=cap, dtype=dtype)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    K = torch.rand((T, NL, B, H, d), generator=g, device="cuda").to(dtype)
+    V = torch.rand((T, NL, B, H, d), generator=g, device="cuda").to(dtype)
+    for t in range(T):  # decode order: every layer appends, then the row commits
+        for l in range(NL):
+            kv.append(l, K[t, l], V[t, l])
+        kv.commit_row()
+    assert kv.length == T
+    ref_k = torch.zeros_like(kv.k)
+    ref_v = torch.zeros_like(kv.v)
+    ref_k[:, :, :, :T] = K.permute(1, 2, 3, 0, 4)
+    ref_v[:, :, :, :T] = V.permute(1, 2, 3, 0, 4)
+    torch.cuda.synchronize()
+    assert torch.equal(kv.k, ref_k) and torch.equal(kv.v, ref_v)
+    # cache correction: rewrite the trailing W rows of layer 1 (kv_cache.hpp:34-42)
+    W = 16
+    wk = torch.rand((B, H, W, d), generator=g, device="cuda").to(dtype)
+    wv = torch.rand((B, H, W, d), generator=g, device="cuda").to(dtype)
+    kv.overwrite(1, T - W, wk, wv)
+    ref_k[1, :, :, T - W:T] = wk
+    ref_v[1, :, :, T - W:T] = wv
+    # single-row overwrite
+    kv.overwrite(2, 5, K[0, 0], V[0, 0])
+    ref_k[2, :, :, 5] = K[0, 0]
+    ref_v[2, :, :, 5] = V[0, 0]
+    torch.cuda.synchronize()
+    assert torch.equal(kv.k, ref_k) and torch.equal(kv.v, ref_v)
+    with pytest.raises(P.InvalidArgument):
+        kv.overwrite(0, T - 2, wk, wv)  # beyond the committed length
+
+
+def test_write_errors():
+    import paper_2602_04541_b200 as P
+    from paper_2602_04541_b200 import _lib
+    import ctypes as C
+    kv = P.KvCache(n_layers=2, batch=1, n_kv_heads=2, d_head=64, seq_cap=8, dtype=torch.bfloat16)
+    rows = torch.zeros((1, 2, 64), dtype=torch.bfloat16, device="cuda")
+    lib = _lib.lib()
+    with pytest.raises(P.InvalidArgument):  # layer out of range
+        _lib.check(lib.lyc_kv_write(kv.k.data_ptr(), kv.v.data_ptr(), C.byref(kv._lay), 2, 0, 1,
+                                    rows.data_ptr(), rows.data_ptr(), None))
+    with pytest.raises(P.InvalidArgument):  # beyond seq_cap
+        _lib.check(lib.lyc_kv_write(kv.k.data_ptr(), kv.v.data_ptr(), C.byref(kv._lay), 0, 8, 1,
+                                    rows.data_ptr(), rows.data_ptr(), None))
+    for _ in range(8):
+        for l in range(2):
+            kv.append(l, rows, rows)
+        kv.commit_row()
+    with pytest.raises(P.InvalidArgument):  # full
+        kv.append(0, rows, rows)
+
+
+def test_decode_over_appended_cache_matches_prefilled():
+    """The decoder reads the cache the write path built: same outputs and
+    sets as over a cache filled by torch (bitwise)."""
+    import paper_2602_04541_b200 as P
+    NL, B, H, G, d, seq = 2, 1, 8, 4, 128, 4096
+    roles = np.ones((NL, H), dtype=np.uint8)
+    roles[0] = 0
+    roles[1, 2] = 0
+    g = torch.Generator(device="cuda").manual_seed(7)
+    K = (torch.rand((NL, B, H, seq, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    V = (torch.rand((NL, B, H, seq, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    q = (torch.rand((NL, B, H * G, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    kv = P.KvCache(n_layers=NL, batch=B, n_kv_heads=H, d_head=d, seq_cap=seq, dtype=torch.bfloat16)
+    # a prompt cache adopted in one window write per layer, then 3 decoded rows
+    for l in range(NL):
+        kv._write(l, 0, K[l, :, :, : seq - 3], V[l, :, :, : seq - 3])
+    kv.length = seq - 3
+    for t in range(seq - 3, seq):
+        for l in range(NL):
+            kv.append(l, K[l, :, :, t], V[l, :, :, t])
+        kv.commit_row()
+    dec = P.HybridDecoder(n_layers=NL, batch=B, n_kv_heads=H, group_size=G, d_head=d,
+                          seq_cap=seq, roles=roles, policy=P.SparsityPolicy.top_k(256),
+                          dtype=torch.bfloat16)
+    out_a = dec.decode_step(q, kv.k, kv.v, seq)
+    sets_a = dec.token_sets()
+    out_b = dec.decode_step(q, K, V, seq)
+    sets_b = dec.token_sets()
+    torch.cuda.synchronize()
+    assert torch.equal(out_a, out_b)
+    assert all(np.array_equal(a, b) for a, b in zip(sets_a[0], sets_b[0]))
