@@ -66,6 +66,24 @@ __device__ __forceinline__ void spin_until(const uint32_t* ctr, uint32_t target)
   }
 }
 
+// spin_until on two counters at once (c2 may be null): both loads in flight
+// per poll, so an already-reached second target costs no extra round trip.
+__device__ __forceinline__ void spin_until2(const uint32_t* c1, uint32_t t1, const uint32_t* c2,
+                                            uint32_t t2) {
+  auto done = [&]() {
+    const uint32_t a = ld_acquire(c1);
+    const uint32_t b = c2 ? ld_acquire(c2) : t2;
+    return (int)(a - t1) >= 0 && (int)(b - t2) >= 0;
+  };
+  if (!done()) {
+    const long long t0 = clock64();
+    while (!done()) {
+      __nanosleep(64);
+      if (clock64() - t0 > 40000000000LL) __trap();
+    }
+  }
+}
+
 __device__ __forceinline__ void group_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -880,11 +898,13 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
     for (int l = 0; l < p.n_layers; ++l) {
       if (l > 0) {
         if (tid == 0) {
-          spin_until(LYC_CTR(p.ctr, l - 1, CTR_MERGE), t_attn);
-          // key / histogram buffers of this parity are free once layer l-2's
-          // selection (if any) finished
-          if (l >= 2 && p.layers[l - 2].n_sel > 0 && p.sel_mode != SEL_NONE)
-            spin_until(LYC_CTR(p.ctr, l - 2, CTR_SELDONE), epoch1 * seldone_per_step(p, l - 2));
+          // the previous layer's outputs are final, and the key / histogram
+          // buffers of this parity are free once layer l-2's selection (if
+          // any) finished: both counters polled together (one round trip)
+          const bool sel2 = l >= 2 && p.layers[l - 2].n_sel > 0 && p.sel_mode != SEL_NONE;
+          spin_until2(LYC_CTR(p.ctr, l - 1, CTR_MERGE), t_attn,
+                      sel2 ? LYC_CTR(p.ctr, l - 2, CTR_SELDONE) : nullptr,
+                      sel2 ? epoch1 * seldone_per_step(p, l - 2) : 0u);
         }
         consumer_bar();
       }
