@@ -236,6 +236,22 @@ typedef struct lyc_kv_layout {
 int lyc_kv_write(void* k_cache, void* v_cache, const lyc_kv_layout* layout, int32_t layer,
                  int64_t pos, int64_t n_rows, const void* k_src, const void* v_src, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Cache-correction attention (decode_engine.hpp:164-204):
+ * after the K/V rows of the last `window` positions [start, start + window)
+ * were rewritten (lyc_kv_write), window position i (p = start + i) attends
+ * keys [0, p] of layer `layer` -- all window x Hq query rows of a KV head in
+ * one prefill-style pass over the cache (bf16, d 64 or 128).
+ *   q, out: device [B][window][Hq][d] bf16 (Hq = n_kv_heads * group_size);
+ *   workspace: device, >= lyc_window_workspace(...) bytes.
+ * The surrounding per-position projections (compute_qkv, attn_project_residual,
+ * ffn_residual) are the model's, not this library's. */
+int64_t lyc_window_workspace(const lyc_kv_layout* layout, int32_t group_size, int32_t window);
+int lyc_window_attention(const lyc_kv_layout* layout, int32_t layer, const void* k_cache,
+                         const void* v_cache, int32_t group_size, float scale, int64_t start,
+                         int32_t window, const void* q, void* out, void* workspace,
+                         int64_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

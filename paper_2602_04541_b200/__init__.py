@@ -11,7 +11,7 @@ the built library raises ImportError.
 """
 from ._lib import (CudaError, InvalidArgument, LogicError, LycError, NotSupported, lib)
 from .decode import HybridDecoder, SparsityPolicy, args_top_k, fraction_budget
-from .kvcache import KvCache
+from .kvcache import KvCache, correction_attention
 from .kernel import (BlockIndexSet, CostReport, RunResult, SplitSchedule, WorkUnit, Workload,
                      latency_model, plan_splits, run)
 
@@ -21,5 +21,6 @@ __all__ = [
     "BlockIndexSet", "CostReport", "CudaError", "HybridDecoder", "InvalidArgument", "KvCache",
     "LogicError",
     "LycError", "NotSupported", "RunResult", "SparsityPolicy", "SplitSchedule", "WorkUnit",
-    "Workload", "args_top_k", "fraction_budget", "latency_model", "plan_splits", "run",
+    "Workload", "args_top_k", "correction_attention", "fraction_budget", "latency_model",
+    "plan_splits", "run",
 ]

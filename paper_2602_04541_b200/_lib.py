@@ -27,7 +27,8 @@ SYMBOLS = [
     "lyc_decoder_replay", "lyc_decoder_index_cache", "lyc_decoder_launches_per_step",
     "lyc_decoder_step_bytes", "lyc_decoder_layer_attn_bytes", "lyc_decoder_set_timing",
     "lyc_decoder_attn_ms", "lyc_decoder_is_fused", "lyc_decoder_set_trace", "lyc_decoder_trace",
-    "lyc_shard_layer", "lyc_shard_merge", "lyc_kv_write",
+    "lyc_shard_layer", "lyc_shard_merge", "lyc_kv_write", "lyc_window_workspace",
+    "lyc_window_attention",
 ]
 
 
@@ -140,6 +141,11 @@ def lib() -> C.CDLL:
     L.lyc_shard_merge.argtypes = [vp, i32, i32, vp, vp, vp, vp, i64, i64, i64, i64, vp, vp, vp]
     L.lyc_kv_write.restype = C.c_int
     L.lyc_kv_write.argtypes = [vp, vp, C.POINTER(lyc_kv_layout), i32, i64, i64, vp, vp, vp]
+    L.lyc_window_workspace.restype = C.c_int64
+    L.lyc_window_workspace.argtypes = [C.POINTER(lyc_kv_layout), i32, i32]
+    L.lyc_window_attention.restype = C.c_int
+    L.lyc_window_attention.argtypes = [C.POINTER(lyc_kv_layout), i32, vp, vp, i32, C.c_float, i64,
+                                       i32, vp, vp, vp, i64, vp]
     _lib = L
     return L
 

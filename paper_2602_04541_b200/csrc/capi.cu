@@ -23,6 +23,10 @@ int attn_stages(int dtype, int d);
 cudaError_t launch_merge(const LycMergeParams& p, int dtype, cudaStream_t st);
 cudaError_t launch_topk(const LycTopkParams& p, int rows, int cluster, cudaStream_t st);
 cudaError_t launch_policy(const LycPolicyParams& p, int rows, cudaStream_t st);
+int64_t window_workspace_bytes(int B, int H, int G, int W, int n_split);
+cudaError_t launch_window(const void* q, const void* k, const void* v, int L, int layer, int B,
+                          int H, int G, int d, int64_t cap, int64_t start, int W, float scale,
+                          float* workspace, int n_split, void* out, cudaStream_t st);
 int topk_cluster_size(int n, int max_slice);
 size_t topk_smem_bytes(int slice);
 cudaError_t launch_float_keys(const float* s, uint32_t* keys, int64_t n, cudaStream_t st);
@@ -1421,6 +1425,55 @@ int lyc_kv_write(void* k_cache, void* v_cache, const lyc_kv_layout* lay, int32_t
         slab_chunks, dst0);
     cuda_check(cudaGetLastError(), "kv write launch");
     ++g_launches;
+    return LYC_OK;
+  });
+}
+
+// ------------------------------------------------------------ cache correction
+namespace {
+int window_splits(const lyc_kv_layout* lay, int32_t group_size, int32_t window) {
+  const int rows = window * group_size, rb = (rows + 127) / 128;
+  const int ctas = lay->batch * lay->n_kv_heads * rb;
+  return std::max(1, (2 * num_sms() + ctas - 1) / ctas);
+}
+void window_validate(const lyc_kv_layout* lay, int32_t group_size, int32_t window) {
+  if (!lay) fail(LYC_EINVAL, "window: null layout");
+  if (lay->n_layers < 1 || lay->batch < 1 || lay->n_kv_heads < 1 || lay->seq_cap < 1)
+    fail(LYC_EINVAL, "window: all dimensions must be >= 1");
+  if (group_size < 1 || window < 1) fail(LYC_EINVAL, "window: group_size and window must be >= 1");
+  if (lay->dtype != LYC_DTYPE_BF16 || (lay->d_head != 64 && lay->d_head != 128))
+    fail(LYC_ENOTSUP, "window: bf16 caches with d_head 64 or 128");
+}
+}  // namespace
+
+int64_t lyc_window_workspace(const lyc_kv_layout* lay, int32_t group_size, int32_t window) {
+  return guarded([&]() -> int64_t {
+    window_validate(lay, group_size, window);
+    return lyc::window_workspace_bytes(lay->batch, lay->n_kv_heads, group_size, window,
+                                       window_splits(lay, group_size, window));
+  });
+}
+
+int lyc_window_attention(const lyc_kv_layout* lay, int32_t layer, const void* k_cache,
+                         const void* v_cache, int32_t group_size, float scale, int64_t start,
+                         int32_t window, const void* q, void* out, void* workspace,
+                         int64_t workspace_bytes, void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    window_validate(lay, group_size, window);
+    if (layer < 0 || layer >= lay->n_layers) fail(LYC_EINVAL, "window: layer out of range");
+    if (start < 0 || start + window > lay->seq_cap) fail(LYC_EINVAL, "window: rows beyond seq_cap");
+    if (!k_cache || !v_cache || !q || !out || !workspace) fail(LYC_EINVAL, "window: null buffer");
+    const int ns = window_splits(lay, group_size, window);
+    if (workspace_bytes < lyc::window_workspace_bytes(lay->batch, lay->n_kv_heads, group_size,
+                                                       window, ns))
+      fail(LYC_EINVAL, "window: workspace too small");
+    const float sc = scale != 0.f ? scale : (float)(1.0 / std::sqrt((double)lay->d_head));
+    cuda_check(lyc::launch_window(q, k_cache, v_cache, lay->n_layers, layer, lay->batch,
+                                  lay->n_kv_heads, group_size, lay->d_head, lay->seq_cap, start,
+                                  window, sc, static_cast<float*>(workspace), ns, out,
+                                  (cudaStream_t)stream),
+               "window launch");
+    g_launches += 2;
     return LYC_OK;
   });
 }

@@ -60,4 +60,30 @@ class KvCache:
         self._write(layer, pos, k_rows, v_rows, stream)
 
 
-__all__ = ["KvCache"]
+def correction_attention(k_cache: torch.Tensor, v_cache: torch.Tensor, layer: int,
+                         q_window: torch.Tensor, start: int, *, scale: float = 0.0,
+                         stream=None) -> torch.Tensor:
+    """Cache-correction attention (decode_engine.hpp:164-204): window position
+    i (p = start + i) of q_window [B][W][Hq][d] attends keys [0, p] of `layer`
+    of the cache [L][B][H][cap][d] (bf16), after the window's K/V rows were
+    rewritten (KvCache.overwrite).  Returns [B][W][Hq][d] bf16."""
+    L, B, H, cap, d = k_cache.shape
+    Bq, W, Hq, dq = q_window.shape
+    if Bq != B or dq != d or Hq % H:
+        raise InvalidArgument("correction_attention: shape mismatch")
+    G = Hq // H
+    lay = _lib.lyc_kv_layout(n_layers=L, batch=B, n_kv_heads=H, d_head=d,
+                             dtype=_lib.DTYPE_BF16 if k_cache.dtype == torch.bfloat16 else _lib.DTYPE_F32,
+                             pad=0, seq_cap=cap)
+    need = check(lib().lyc_window_workspace(C.byref(lay), G, W))
+    ws = torch.empty(need // 4 + 1, dtype=torch.float32, device=k_cache.device)
+    q = q_window.contiguous()
+    out = torch.empty_like(q)
+    st = stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    check(lib().lyc_window_attention(C.byref(lay), layer, k_cache.data_ptr(), v_cache.data_ptr(), G,
+                                     scale, start, W, q.data_ptr(), out.data_ptr(), ws.data_ptr(),
+                                     ws.numel() * 4, st))
+    return out
+
+
+__all__ = ["KvCache", "correction_attention"]

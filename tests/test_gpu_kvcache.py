@@ -105,3 +105,39 @@ def test_decode_over_appended_cache_matches_prefilled():
     torch.cuda.synchronize()
     assert torch.equal(out_a, out_b)
     assert all(np.array_equal(a, b) for a, b in zip(sets_a[0], sets_b[0]))
+
+
+@pytest.mark.parametrize("d,G,W,start", [(128, 4, 32, 3000), (64, 8, 16, 1000), (128, 4, 5, 70)])
+def test_correction_attention_vs_oracle(orc, d, G, W, start):
+    """decode_engine.hpp:164-204 attention part: after the window's rows are
+    rewritten, window position i attends keys [0, start + i] (dense,
+    attention.hpp:50-75) -- checked per (b, position, q head) against the
+    oracle's f64 dense_attention; bf16 tolerance 2e-2."""
+    import paper_2602_04541_b200 as P
+    NL, B, H, cap = 2, 2, 2, 4096
+    Hq = H * G
+    g = torch.Generator(device="cuda").manual_seed(11)
+    kv = P.KvCache(n_layers=NL, batch=B, n_kv_heads=H, d_head=d, seq_cap=cap, dtype=torch.bfloat16)
+    kv.k.uniform_(-1, 1, generator=g)
+    kv.v.uniform_(-1, 1, generator=g)
+    kv.length = start + W
+    wk = (torch.rand((B, H, W, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    wv = (torch.rand((B, H, W, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    kv.overwrite(1, start, wk, wv)  # the rewritten window rows (kv_cache.hpp:34-42)
+    q = (torch.rand((B, W, Hq, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    out = P.correction_attention(kv.k, kv.v, 1, q, start)
+    torch.cuda.synchronize()
+    Kn = kv.k[1].float().cpu().numpy()
+    Vn = kv.v[1].float().cpu().numpy()
+    qn = q.float().cpu().numpy()
+    on = out.float().cpu().numpy()
+    scale = 1 / np.sqrt(d)
+    worst = 0.0
+    for b in range(B):
+        for i in range(W):
+            p = start + i
+            for hd in range(Hq):
+                ref, _ = orc.dense_attention(qn[b, i, hd], Kn[b, hd // G, : p + 1],
+                                             Vn[b, hd // G, : p + 1], scale)
+                worst = max(worst, np.abs(on[b, i, hd] - ref).max() / max(np.abs(ref).max(), 1e-3))
+    assert worst < 2e-2, worst
