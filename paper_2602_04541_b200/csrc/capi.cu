@@ -564,7 +564,8 @@ namespace {
 // with an older index list, and last the sparse slots whose list the
 // immediately preceding layer's selection produces (streamed while that
 // selection is still running).
-void plan_step_launch(HostLaunch& L, int batch, int heads, int splits, int group, int layer) {
+void plan_step_launch(HostLaunch& L, int batch, int heads, int splits, int group, int layer,
+                      int free_from) {
   L.batch = batch;
   L.heads = heads;
   L.splits = splits;
@@ -594,23 +595,29 @@ void plan_step_launch(HostLaunch& L, int batch, int heads, int splits, int group
         }
       }
       if (tot == 0) continue;
+      // the sparse pools skip the CTAs that run this layer's selection items
+      // (cells >= free_from): their epilogue classifies while the others
+      // stream, without sharing issue slots with busy consumers
+      int ns = splits;
+      if (pool >= 1) ns = std::max(1, std::min(splits, free_from - b * splits));
       // even cut points, then snapped onto a head boundary within one item:
       // a split that would hold the end of one head and the start of the next
       // (two units: an extra unit epilogue and signal) gets one item more or
       // less instead
-      const int64_t base = tot / splits, rem = tot % splits;
+      const int64_t base = tot / ns, rem = tot % ns;
       constexpr int64_t kSnap = 1;  // items (measured: 1 beats 2 and 3)
       std::vector<int64_t> cut((size_t)splits + 1);
-      for (int sp = 0; sp <= splits; ++sp) cut[(size_t)sp] = sp * base + std::min<int64_t>(sp, rem);
+      for (int sp = 0; sp <= splits; ++sp)
+        cut[(size_t)sp] = sp <= ns ? sp * base + std::min<int64_t>(sp, rem) : tot;
       {
         int64_t hb = 0;
         for (size_t h = 0; h + 1 < hs.size(); ++h) {
           hb += L.slots[(size_t)b * heads + hs[h]].n_items;
           // the cut nearest to the boundary hb
-          int sp = (int)std::min<int64_t>(splits - 1, std::max<int64_t>(1, hb / std::max<int64_t>(base, 1)));
+          int sp = (int)std::min<int64_t>(ns - 1, std::max<int64_t>(1, hb / std::max<int64_t>(base, 1)));
           while (sp > 1 && cut[(size_t)sp] > hb) --sp;
-          while (sp < splits - 1 && cut[(size_t)sp + 1] <= hb) ++sp;
-          for (int c = sp; c <= sp + 1 && c < splits; ++c)
+          while (sp < ns - 1 && cut[(size_t)sp + 1] <= hb) ++sp;
+          for (int c = sp; c <= sp + 1 && c < ns; ++c)
             if (c >= 1 && std::llabs(cut[(size_t)c] - hb) <= kSnap && cut[(size_t)c - 1] < hb &&
                 hb < cut[(size_t)c + 1])
               cut[(size_t)c] = hb;
@@ -715,7 +722,18 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
     for (int g = 0; g < H; ++g)
       if (d->retrieval(l, g)) last_r[(size_t)g] = l;
     if (d->fused)
-      plan_step_launch(L, B, H, d->S, G, l);
+    {
+      // this layer's selection items run on the last n_items CTAs when they
+      // fit in half the grid (step.cu split roles)
+      int free_from = d->S * B;
+      if (!none) {
+        const int64_t nk = blocks ? nb : seq;
+        const int64_t items = (nk + lyc::step_item_keys() - 1) / lyc::step_item_keys();
+        const int64_t n_items = (int64_t)L.sel_rows.size() * items;
+        if (n_items > 0 && 2 * n_items <= (int64_t)d->S * B) free_from = d->S * B - (int)n_items;
+      }
+      plan_step_launch(L, B, H, d->S, G, l, free_from);
+    }
     else
       plan_launch(L, B, H, d->S, G);
     total += launch_bytes(L);
