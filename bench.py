@@ -470,22 +470,31 @@ def main():
                 "speedup_hybrid_vs_full": fms / ms}
         fdec.close()
 
-    # ---- e2e through the public API with host buffers
-    q_h = torch.empty(q.shape, dtype=dt, pin_memory=True)
-    q_h.copy_(q.cpu())
-    kv_new_h = torch.empty((2, NL, B, Hr, d), dtype=dt, pin_memory=True)
-    kv_new_h[0].copy_(K[:, :, :, L - 1].cpu())
-    kv_new_h[1].copy_(V[:, :, :, L - 1].cpu())
-    kv_new_d = torch.empty(kv_new_h.shape, dtype=dt, device=dev)
+    # ---- e2e through the public API with host buffers: one packed pinned
+    # upload per step (q of every layer + the new token's K/V rows), the rows
+    # appended to the cache by the KV write path (lyc_kv_write, all layers in
+    # one launch), the step, and the output read back
+    import ctypes as C
+    from paper_2602_04541_b200 import _lib as LL
+    nq, nkv = q.numel(), NL * B * Hr * d
+    in_h = torch.empty(nq + 2 * nkv, dtype=dt, pin_memory=True)
+    in_h[:nq].copy_(q.cpu().reshape(-1))
+    in_h[nq:nq + nkv].copy_(K[:, :, :, L - 1].cpu().reshape(-1))
+    in_h[nq + nkv:].copy_(V[:, :, :, L - 1].cpu().reshape(-1))
+    in_d = torch.empty_like(in_h, device=dev)
+    q_in = in_d[:nq].view(q.shape)
+    k_new, v_new = in_d[nq:nq + nkv], in_d[nq + nkv:]
+    lay = LL.lyc_kv_layout(n_layers=NL, batch=B, n_kv_heads=Hr, d_head=d,
+                           dtype=LL.DTYPE_BF16 if dt == torch.bfloat16 else LL.DTYPE_F32, pad=0,
+                           seq_cap=seq_cap)
     out_h = torch.empty(out.shape, dtype=dt, pin_memory=True)
     e2e_steps = max(3, args.steps // 2)
 
     def e2e_step():
-        q.copy_(q_h, non_blocking=True)
-        kv_new_d.copy_(kv_new_h, non_blocking=True)
-        K[:, :, :, L - 1].copy_(kv_new_d[0])
-        V[:, :, :, L - 1].copy_(kv_new_d[1])
-        dec.decode_step(q, K, V, L, out, stream=stream)
+        in_d.copy_(in_h, non_blocking=True)
+        LL.check(LL.lib().lyc_kv_write(K.data_ptr(), V.data_ptr(), C.byref(lay), -1, L - 1, 1,
+                                       k_new.data_ptr(), v_new.data_ptr(), stream.cuda_stream))
+        dec.decode_step(q_in, K, V, L, out, stream=stream)
         out_h.copy_(out, non_blocking=True)
 
     with torch.cuda.stream(stream):
@@ -502,7 +511,7 @@ def main():
     e1.synchronize()
     barrier()
     e2e_ms = allmax(e0.elapsed_time(e1) / e2e_steps)
-    h2d = q_h.numel() * esz + kv_new_h.numel() * esz
+    h2d = in_h.numel() * esz
     d2h = out_h.numel() * esz
 
     # ---- CPU baseline (rank 0, N == 1): the reference operator on the host

@@ -225,6 +225,8 @@ int lyc_shard_merge(lyc_decoder* dec, int32_t layer, int32_t world, const float*
  *     every head of the layer at once (the caller advances the length);
  *   KvCache::overwrite (34-42): n_rows = 1 at any pos < length, or a window
  *     (cache correction rewrites the trailing W rows).
+ * layer = -1 writes every layer at once (src [n_layers][B][H][n_rows][d]):
+ * one launch for a decoded token's rows of the whole model.
  * LYC_EINVAL when pos + n_rows > seq_cap or the layer is out of range.
  * Stream-ordered, graph-capturable, no allocation. */
 typedef struct lyc_kv_layout {

@@ -1425,16 +1425,18 @@ int lyc_kv_write(void* k_cache, void* v_cache, const lyc_kv_layout* lay, int32_t
         lay->seq_cap < 1)
       fail(LYC_EINVAL, "KvCache: all dimensions must be >= 1");
     if (lay->dtype != LYC_DTYPE_F32 && lay->dtype != LYC_DTYPE_BF16) fail(LYC_EINVAL, "KvCache: dtype");
-    if (layer < 0 || layer >= lay->n_layers) fail(LYC_EINVAL, "KvCache: layer out of range");
+    if (layer < -1 || layer >= lay->n_layers) fail(LYC_EINVAL, "KvCache: layer out of range");
     if (pos < 0 || n_rows < 0 || pos + n_rows > lay->seq_cap)
       fail(LYC_EINVAL, "KvCache: rows beyond seq_cap");
+    const bool all = layer == -1;  // every layer: src [n_layers][B][H][n_rows][d]
     const int64_t row_bytes = (int64_t)lay->d_head * (lay->dtype == LYC_DTYPE_BF16 ? 2 : 4);
     if (row_bytes % 16) fail(LYC_ENOTSUP, "KvCache: rows must be a multiple of 16 bytes");
     if (n_rows == 0) return LYC_OK;
     const int64_t chunks = row_bytes / 16;
-    const int64_t slabs = (int64_t)lay->batch * lay->n_kv_heads;
+    const int64_t slabs = (int64_t)lay->batch * lay->n_kv_heads * (all ? lay->n_layers : 1);
     const int64_t slab_chunks = lay->seq_cap * chunks;
-    const int64_t dst0 = ((int64_t)layer * slabs) * slab_chunks + pos * chunks;
+    const int64_t dst0 = ((int64_t)(all ? 0 : layer) * lay->batch * lay->n_kv_heads) * slab_chunks +
+                         pos * chunks;
     const int64_t total = slabs * n_rows * chunks;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
     kv_write_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
