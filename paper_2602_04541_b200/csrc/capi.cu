@@ -599,7 +599,10 @@ void plan_step_launch(HostLaunch& L, int batch, int heads, int splits, int group
       // (cells >= free_from): their epilogue classifies while the others
       // stream, without sharing issue slots with busy consumers
       int ns = splits;
-      if (pool >= 1) ns = std::max(1, std::min(splits, free_from - b * splits));
+      if (pool >= 1) {
+        const int usable = std::min(splits, free_from - b * splits);
+        if (usable >= (splits + 1) / 2) ns = usable;  // never squeeze a batch item onto a few CTAs
+      }
       // even cut points, then snapped onto a head boundary within one item:
       // a split that would hold the end of one head and the start of the next
       // (two units: an extra unit epilogue and signal) gets one item more or

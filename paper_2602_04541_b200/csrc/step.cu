@@ -172,6 +172,8 @@ __device__ __forceinline__ LycView layer_view(const LycStepParams& p, const LycL
   v.hist1 = p.sel_mode == SEL_TOKEN_KEYS ? p.hist + (int64_t)(l & 1) * p.max_sel * LYC_H1_STRIDE
                                          : nullptr;
   v.exec_counts = nullptr;
+  v.out_f32 = nullptr;  // single-unit slots write `out` directly
+  v.out_lse = nullptr;
   v.sel_stride = p.sel_stride;
   v.counts_stride = 0;
   v.n_splits = p.n_splits;

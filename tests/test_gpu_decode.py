@@ -446,3 +446,25 @@ def test_topp_bf16_llama_heads_graph_replay(orc):
     st.synchronize()
     assert torch.equal(out2, out)
     assert all(np.array_equal(a, b) for a, b in zip(dec.token_sets()[0], sets[0]))
+
+
+@pytest.mark.parametrize("num_splits", [1, 2])
+def test_fused_step_single_unit_slots(orc, num_splits):
+    """One or two splits per batch item (the default at batch >= 75): slots of
+    a single unit write the output directly from the unit epilogue, with no
+    merge -- against the oracle, every batch item."""
+    import paper_2602_04541_b200 as P
+    NL, B, H, G, d, seq, k = 2, 3, 2, 4, 128, 6000, 300
+    roles = roles_for(NL, H, [(1, 1)])
+    q, K, V = synth(41, NL, B, H, G, d, seq, seq, torch.bfloat16)
+    dec = P.HybridDecoder(n_layers=NL, batch=B, n_kv_heads=H, group_size=G, d_head=d, seq_cap=seq,
+                          roles=roles, policy=P.SparsityPolicy.top_k(k), dtype=torch.bfloat16,
+                          num_splits=num_splits)
+    out = dec.decode_step(q.cuda(), K.cuda(), V.cuda(), seq)
+    torch.cuda.synchronize()
+    assert dec.fused
+    qf, Kf, Vf, of = q.float().numpy(), K.float().numpy(), V.float().numpy(), out.float().cpu().numpy()
+    for b in range(B):
+        r = orc.decode_step(qf[:, b], Kf[:, b], Vf[:, b], roles, seq=seq, scale=1 / np.sqrt(d),
+                            kind="topk", k=k)
+        assert rel_err(of[:, b], r["out"]) < BF16_TOL
