@@ -243,7 +243,8 @@ int lyc_kv_write(void* k_cache, void* v_cache, const lyc_kv_layout* layout, int3
  * after the K/V rows of the last `window` positions [start, start + window)
  * were rewritten (lyc_kv_write), window position i (p = start + i) attends
  * keys [0, p] of layer `layer` -- all window x Hq query rows of a KV head in
- * one prefill-style pass over the cache (bf16, d 64 or 128).
+ * one prefill-style pass over the cache (bf16, d 64 or 128; fp32 caches with
+ * d <= 128 through a simple one-warp-per-row kernel for small configs).
  *   q, out: device [B][window][Hq][d] bf16 (Hq = n_kv_heads * group_size);
  *   workspace: device, >= lyc_window_workspace(...) bytes.
  * The surrounding per-position projections (compute_qkv, attn_project_residual,

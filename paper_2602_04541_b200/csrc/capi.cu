@@ -24,6 +24,9 @@ cudaError_t launch_merge(const LycMergeParams& p, int dtype, cudaStream_t st);
 cudaError_t launch_topk(const LycTopkParams& p, int rows, int cluster, cudaStream_t st);
 cudaError_t launch_policy(const LycPolicyParams& p, int rows, cudaStream_t st);
 int64_t window_workspace_bytes(int B, int H, int G, int W, int n_split);
+cudaError_t launch_window_f32(const void* q, const void* k, const void* v, int layer, int B, int H,
+                              int G, int d, int64_t cap, int64_t start, int W, float scale,
+                              void* out, cudaStream_t st);
 cudaError_t launch_window(const void* q, const void* k, const void* v, int L, int layer, int B,
                           int H, int G, int d, int64_t cap, int64_t start, int W, float scale,
                           float* workspace, int n_split, void* out, cudaStream_t st);
@@ -1464,8 +1467,9 @@ void window_validate(const lyc_kv_layout* lay, int32_t group_size, int32_t windo
   if (lay->n_layers < 1 || lay->batch < 1 || lay->n_kv_heads < 1 || lay->seq_cap < 1)
     fail(LYC_EINVAL, "window: all dimensions must be >= 1");
   if (group_size < 1 || window < 1) fail(LYC_EINVAL, "window: group_size and window must be >= 1");
-  if (lay->dtype != LYC_DTYPE_BF16 || (lay->d_head != 64 && lay->d_head != 128))
-    fail(LYC_ENOTSUP, "window: bf16 caches with d_head 64 or 128");
+  if (lay->dtype == LYC_DTYPE_BF16 ? (lay->d_head != 64 && lay->d_head != 128)
+                                    : (lay->dtype != LYC_DTYPE_F32 || lay->d_head > 128))
+    fail(LYC_ENOTSUP, "window: bf16 caches with d_head 64 or 128, or fp32 with d_head <= 128");
 }
 }  // namespace
 
@@ -1491,6 +1495,14 @@ int lyc_window_attention(const lyc_kv_layout* lay, int32_t layer, const void* k_
                                                        window, ns))
       fail(LYC_EINVAL, "window: workspace too small");
     const float sc = scale != 0.f ? scale : (float)(1.0 / std::sqrt((double)lay->d_head));
+    if (lay->dtype == LYC_DTYPE_F32) {
+      cuda_check(lyc::launch_window_f32(q, k_cache, v_cache, layer, lay->batch, lay->n_kv_heads,
+                                        group_size, lay->d_head, lay->seq_cap, start, window, sc,
+                                        out, (cudaStream_t)stream),
+                 "window launch");
+      ++g_launches;
+      return LYC_OK;
+    }
     cuda_check(lyc::launch_window(q, k_cache, v_cache, lay->n_layers, layer, lay->batch,
                                   lay->n_kv_heads, group_size, lay->d_head, lay->seq_cap, start,
                                   window, sc, static_cast<float*>(workspace), ns, out,

@@ -286,6 +286,74 @@ static cudaError_t launch_window_t(const WinParams& p, void* out, cudaStream_t s
   return cudaGetLastError();
 }
 
+// fp32 caches (small configs): one warp per window row, keys in chunks of 32
+// (a lane per key for the scores, lanes over d for P V), online softmax.
+__global__ void window_attn_f32_kernel(const float* __restrict__ q, const float* __restrict__ k,
+                                       const float* __restrict__ v, int64_t slab0, int64_t cap,
+                                       int B, int H, int G, int W, int d, int64_t start,
+                                       float scale, float* __restrict__ out) {
+  extern __shared__ float qs_all[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;  // (b, i, hq)
+  const int Hq = H * G;
+  if (row >= (int64_t)B * W * Hq) return;
+  const int hq = (int)(row % Hq), i = (int)((row / Hq) % W), b = (int)(row / ((int64_t)Hq * W));
+  const int g = hq / G;
+  float* qs = qs_all + wib * d;
+  const float* qr = q + row * d;
+  for (int c = lane; c < d; c += 32) qs[c] = qr[c];
+  __syncwarp();
+  const float* ks = k + slab0 + ((int64_t)b * H + g) * cap * d;
+  const float* vs = v + slab0 + ((int64_t)b * H + g) * cap * d;
+  const int64_t n = start + i + 1;  // keys [0, start + i]
+  float m = -INFINITY, l = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int64_t t0 = 0; t0 < n; t0 += 32) {
+    const int64_t t = t0 + lane;
+    float sc = -INFINITY;
+    if (t < n) {
+      float acc = 0.f;
+      for (int c = 0; c < d; ++c) acc = fmaf(qs[c], ks[t * d + c], acc);
+      sc = acc * scale;
+    }
+    float mx = sc;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    const float mn = fmaxf(m, mx);
+    const float rs = m == -INFINITY ? 0.f : expf(m - mn);
+    const float w = t < n ? expf(sc - mn) : 0.f;
+    float ws = w;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, off);
+    l = l * rs + ws;
+    m = mn;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) o[c] *= rs;
+    const int cnt = (int)(n - t0 < 32 ? n - t0 : 32);
+    for (int j = 0; j < cnt; ++j) {
+      const float wj = __shfl_sync(0xffffffffu, w, j);
+      const float* vr = vs + (t0 + j) * d;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c * 32 + lane < d) o[c] = fmaf(wj, vr[c * 32 + lane], o[c]);
+    }
+  }
+  float* dst = out + row * d;
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    if (c * 32 + lane < d) dst[c * 32 + lane] = l > 0.f ? o[c] / l : 0.f;
+}
+
+cudaError_t launch_window_f32(const void* q, const void* k, const void* v, int layer, int B, int H,
+                              int G, int d, int64_t cap, int64_t start, int W, float scale,
+                              void* out, cudaStream_t st) {
+  const int64_t rows = (int64_t)B * W * H * G;
+  const int wpb = 8;
+  window_attn_f32_kernel<<<(unsigned)((rows + wpb - 1) / wpb), wpb * 32, wpb * d * 4, st>>>(
+      static_cast<const float*>(q), static_cast<const float*>(k), static_cast<const float*>(v),
+      (int64_t)layer * B * H * cap * d, cap, B, H, G, W, d, start, scale, static_cast<float*>(out));
+  return cudaGetLastError();
+}
+
 // q, out: [B][W][Hq][d] bf16; k, v: cache [L][B][H][cap][d] bf16.
 cudaError_t launch_window(const void* q, const void* k, const void* v, int L, int layer, int B,
                           int H, int G, int d, int64_t cap, int64_t start, int W, float scale,

@@ -65,8 +65,8 @@ def correction_attention(k_cache: torch.Tensor, v_cache: torch.Tensor, layer: in
                          stream=None) -> torch.Tensor:
     """Cache-correction attention (decode_engine.hpp:164-204): window position
     i (p = start + i) of q_window [B][W][Hq][d] attends keys [0, p] of `layer`
-    of the cache [L][B][H][cap][d] (bf16), after the window's K/V rows were
-    rewritten (KvCache.overwrite).  Returns [B][W][Hq][d] bf16."""
+    of the cache [L][B][H][cap][d] (bf16 or fp32), after the window's K/V rows
+    were rewritten (KvCache.overwrite).  Returns [B][W][Hq][d] in the cache dtype."""
     L, B, H, cap, d = k_cache.shape
     Bq, W, Hq, dq = q_window.shape
     if Bq != B or dq != d or Hq % H:
