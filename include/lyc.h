@@ -245,7 +245,7 @@ int lyc_kv_write(void* k_cache, void* v_cache, const lyc_kv_layout* layout, int3
  * keys [0, p] of layer `layer` -- all window x Hq query rows of a KV head in
  * one prefill-style pass over the cache (bf16, d 64 or 128; fp32 caches with
  * d <= 128 through a simple one-warp-per-row kernel for small configs).
- *   q, out: device [B][window][Hq][d] bf16 (Hq = n_kv_heads * group_size);
+ *   q, out: device [B][window][Hq][d] in the cache dtype (Hq = n_kv_heads * group_size);
  *   workspace: device, >= lyc_window_workspace(...) bytes.
  * The surrounding per-position projections (compute_qkv, attn_project_residual,
  * ffn_residual) are the model's, not this library's. */
