@@ -1042,7 +1042,7 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
       if (d->fused && c.select_mode != LYC_SELECT_NONE) {  // pooled-selection scratch
         d->bitmap_stride = (lyc::step_bitmap_words(d->sel_stride) + 3) & ~(int64_t)3;
         cuda_check(cudaMalloc(&d->sel_bitmap, 2 * rows * d->bitmap_stride * 4), "cudaMalloc bitmap");
-        cuda_check(cudaMalloc(&d->sel_cand, 2 * rows * 3 * d->sel_stride * 4), "cudaMalloc cand");
+        cuda_check(cudaMalloc(&d->sel_cand, 2 * rows * 2 * d->sel_stride * 4), "cudaMalloc cand");
         cuda_check(cudaMalloc(&d->sel_ccnt, 2 * rows * 256 * 4), "cudaMalloc ccnt");
         // per row: 64 selection items x 256 u16 bucket starts
         cuda_check(cudaMalloc(&d->sel_csub, 2 * rows * 64 * 128 * 4), "cudaMalloc csub");

@@ -196,9 +196,9 @@ struct LycStepParams {
   uint32_t* hist;            // [2 parity][max_sel][LYC_H1_ROW] fused first-pass histograms
   uint32_t* sel_bitmap;      // [2 parity][max_sel][bitmap_stride] selected-key bitmaps
   int64_t bitmap_stride;
-  uint32_t* sel_cand;        // [2 parity][max_sel][3][sel_stride] boundary-bin candidates: keys, indices, selected flags
+  uint32_t* sel_cand;        // [2 parity][max_sel][2][sel_stride] boundary-bin candidates: keys, indices
   uint32_t* sel_ccnt;        // [2 parity][max_sel][256] per item: candidates [0,64), definite keys [64,128); row prefix [192,195)
-  uint32_t* sel_csub;        // [2 parity][max_sel][256] boundary-bin sub-histograms (zero between uses)
+  uint32_t* sel_csub;        // [2 parity][max_sel][64 items][256 u16] bucket starts of each item's candidates
   uint32_t* sel_rowctr;      // [n_layers][max_sel][16] monotonic: per selection row words 0 / 8
                              // (items classified / holding copies); per SLOT word 12 (units done)
   uint32_t* ctr;             // LYC_CTR counters: [n_layers][CTR_PER_LAYER], then epoch, exits

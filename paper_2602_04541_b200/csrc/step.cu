@@ -276,13 +276,11 @@ struct EpiSmem {
   uint32_t buf[kEpiBufWords];
   uint32_t hist[LYC_BINS];
   uint32_t scan[64];
-  uint32_t seg[72];          // finish: smem start of each item's candidate segment
-  uint32_t cnt[72];          // finish: candidates of each item
-  uint32_t selc[72];         // resolve: selected candidates of each item
+  uint32_t seg[72];          // resolve: start of each item's block in the row's candidate array
+  uint32_t cnt[72];          // resolve: candidates of each item
   uint32_t defc[72];         // resolve: definite keys of each item
   uint64_t bar;
   uint32_t digit, above, last, pad;
-  uint32_t pfx, pabove, pshift, pad2;  // the row's boundary prefix (classify -> finish)
 };
 
 // 64-thread inclusive scan (2 warps).
@@ -321,7 +319,6 @@ struct SelRow {
   uint32_t* bitmap;   // [n_words]
   uint32_t* ckey;     // [n] candidate keys, item q's segment at q*kItemKeys
   uint32_t* cidx;     // [n] candidate indices
-  uint32_t* cflag;    // [n] (unused)
   uint32_t* csub;     // [64 items][256] u16: each item's bucket starts of its boundary-bin
                       // candidates by their next 8 bits (descending: start[b] = #above b)
   uint32_t* ccnt;     // [n_items] candidates per item; +64: definite keys per item;
@@ -335,9 +332,8 @@ __device__ __forceinline__ SelRow sel_row(const LycStepParams& p, int l, int r) 
   s.keys = p.sel_keys + pr * p.sel_stride;
   s.h1 = p.sel_mode == SEL_TOKEN_KEYS ? p.hist + pr * LYC_H1_STRIDE : nullptr;
   s.bitmap = p.sel_bitmap + pr * p.bitmap_stride;
-  s.ckey = p.sel_cand + pr * 3 * p.sel_stride;
+  s.ckey = p.sel_cand + pr * 2 * p.sel_stride;
   s.cidx = s.ckey + p.sel_stride;
-  s.cflag = s.cidx + p.sel_stride;
   s.csub = p.sel_csub + pr * (64 * 128);
   s.ccnt = p.sel_ccnt + pr * 256;
   s.ctr = p.sel_rowctr + ((int64_t)l * p.max_sel + r) * 16;
