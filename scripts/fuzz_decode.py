@@ -17,16 +17,19 @@ from oracle import pyoracle as PO  # noqa: E402
 orc = PO.orc()
 rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
 n_cases = int(sys.argv[2]) if len(sys.argv) > 2 else 12
+edge = len(sys.argv) > 3 and sys.argv[3] == "edge"  # boundary sizes: tiny contexts, k >= seq, odd G
 bad = 0
 for case in range(n_cases):
     dt = torch.bfloat16 if rng.random() < 0.7 else torch.float32
     d = int(rng.choice([64, 128])) if dt == torch.bfloat16 else int(rng.choice([16, 32, 64, 128]))
-    G = int(rng.choice([1, 2, 4, 8]))
+    G = int(rng.integers(1, 9)) if edge else int(rng.choice([1, 2, 4, 8]))
     H = int(rng.choice([1, 2, 4]))
     B = int(rng.choice([1, 2, 3]))
     NL = int(rng.integers(1, 4))
-    seq = int(rng.integers(100, 20000))
-    k = int(rng.integers(1, min(seq, 3000) + 1))
+    seq = int(rng.choice([1, 2, 63, 64, 65, 127, 8191, 8192, 8193, 16385])) if edge \
+        else int(rng.integers(100, 20000))
+    k = int(rng.choice([1, seq, seq + 5, max(1, seq // 2)])) if edge \
+        else int(rng.integers(1, min(seq, 3000) + 1))
     ns = int(rng.choice([0, 1, 2, 5]))
     kind = str(rng.choice(["topk", "topk", "ratio", "topp", "threshold"]))
     value = {"topk": 0.0, "ratio": float(rng.uniform(0.5, 0.99)), "topp": float(rng.uniform(0.05, 0.9)),
