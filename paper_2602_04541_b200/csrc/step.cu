@@ -631,6 +631,13 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
   // the row's sub-histogram from the items' bucket starts:
   // count[b] = start[b - 1] - start[b] (start[-1] = the item's candidates)
   epi_bar();
+  {  // this item's output offset from the definite keys of the items before it
+     // (known now; the taken candidates are added at emission)
+    const uint32_t n_q = et < items ? es.defc[et] : 0u;
+    uint32_t tot;
+    const uint32_t end_q = epi_scan(n_q, es.scan, et, tot);
+    if (et == q) es.pad = end_q - n_q;
+  }
   {  // thread et: bins 4et .. 4et+3 (one 8-B load + the bin below per item)
     uint32_t h0 = 0, h1 = 0, h2 = 0, h3 = 0;
     for (int i = 0; i < items; ++i) {
@@ -814,12 +821,7 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
   if (et == 0) stamp(p, l, EV_SEL0, cta);
   // this item's output offset: definite keys + selected candidates of the
   // items before it
-  const uint32_t n_q = et < items ? es.defc[et] : 0u;
   const uint32_t taken_before = es.scan[44] + es.scan[45] + es.scan[46];
-  uint32_t tot;
-  const uint32_t end_q = epi_scan(n_q, es.scan, et, tot);
-  if (et == q) es.pad = end_q - n_q;
-  epi_bar();
   const uint32_t out0 = es.pad + taken_before;
   const uint4 v = reinterpret_cast<const uint4*>(ws)[et];
   uint32_t wv[4] = {v.x, v.y, v.z, v.w};
@@ -827,6 +829,7 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
   for (int i = 0; i < 4; ++i)
     if (et * 128 + i * 32 >= cnt) wv[i] = 0u;
   const uint32_t c = __popc(wv[0]) + __popc(wv[1]) + __popc(wv[2]) + __popc(wv[3]);
+  uint32_t tot;
   uint32_t pos = epi_scan(c, es.scan, et, tot) - c + out0;
   if (et == 0) stamp(p, l, EV_X0, cta);
 #pragma unroll
