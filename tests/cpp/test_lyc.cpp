@@ -372,6 +372,98 @@ static void test_sharded_decoder_two_ranks() {
   CHECK(o0 == o1);
 }
 
+// kv_cache.hpp:23-42 through lyc::KvCache, then the cache-correction
+// attention (decode_engine.hpp:164-204) against a host two-pass softmax loop.
+static void test_kv_cache_and_correction() {
+  const int L = 2, B = 1, H = 2, G = 2, d = 32, cap = 300, T = 200, W = 8;
+  const std::size_t slab = (std::size_t)cap * d, n = (std::size_t)L * B * H * slab;
+  lyc::DeviceBuffer kc(n * 4), vc(n * 4);
+  cudaMemset(kc.get(), 0, n * 4);
+  cudaMemset(vc.get(), 0, n * 4);
+  lyc::KvCache kv(L, B, H, d, cap, lyc::Dtype::F32, kc.get(), vc.get());
+  std::mt19937 rng(5);
+  std::uniform_real_distribution<float> U(-1.f, 1.f);
+  std::vector<float> hk(n, 0.f), hv(n, 0.f), rowk((std::size_t)B * H * d), rowv(rowk.size());
+  lyc::DeviceBuffer dk(rowk.size() * 4), dv(rowv.size() * 4);
+  for (int t = 0; t < T; ++t) {
+    for (int l = 0; l < L; ++l) {
+      for (std::size_t i = 0; i < rowk.size(); ++i) {
+        rowk[i] = U(rng);
+        rowv[i] = U(rng);
+      }
+      dk.upload(rowk.data(), rowk.size() * 4);
+      dv.upload(rowv.data(), rowv.size() * 4);
+      kv.append(l, dk.get(), dv.get());
+      for (int g = 0; g < H; ++g)
+        for (int c = 0; c < d; ++c) {
+          hk[((std::size_t)l * H + g) * slab + (std::size_t)t * d + c] = rowk[(std::size_t)g * d + c];
+          hv[((std::size_t)l * H + g) * slab + (std::size_t)t * d + c] = rowv[(std::size_t)g * d + c];
+        }
+    }
+    kv.commit_row();
+  }
+  CHECK(kv.length() == (std::size_t)T);
+  // rewrite the trailing window of layer 1 (overwrite, n_rows = W)
+  std::vector<float> wk((std::size_t)H * W * d), wv(wk.size());
+  for (std::size_t i = 0; i < wk.size(); ++i) {
+    wk[i] = U(rng);
+    wv[i] = U(rng);
+  }
+  lyc::DeviceBuffer dwk(wk.size() * 4), dwv(wv.size() * 4);
+  dwk.upload(wk.data(), wk.size() * 4);
+  dwv.upload(wv.data(), wv.size() * 4);
+  const int start = T - W;
+  kv.overwrite(1, start, W, dwk.get(), dwv.get());
+  for (int g = 0; g < H; ++g)
+    for (int i = 0; i < W; ++i)
+      for (int c = 0; c < d; ++c) {
+        hk[((std::size_t)1 * H + g) * slab + (std::size_t)(start + i) * d + c] = wk[((std::size_t)g * W + i) * d + c];
+        hv[((std::size_t)1 * H + g) * slab + (std::size_t)(start + i) * d + c] = wv[((std::size_t)g * W + i) * d + c];
+      }
+  std::vector<float> gk(n), gv(n);
+  kc.download(gk.data(), n * 4);
+  vc.download(gv.data(), n * 4);
+  CHECK(gk == hk && gv == hv);
+  CHECK_THROWS(kv.overwrite(0, T - 2, W, dwk.get(), dwv.get()), std::invalid_argument);
+  // correction attention of layer 1: window position i attends keys [0, start + i]
+  const int Hq = H * G;
+  std::vector<float> q((std::size_t)B * W * Hq * d);
+  for (auto& x : q) x = U(rng);
+  lyc::DeviceBuffer dq(q.size() * 4), dout(q.size() * 4);
+  dq.upload(q.data(), q.size() * 4);
+  lyc_kv_layout lay{L, B, H, d, LYC_DTYPE_F32, 0, cap};
+  const int64_t ws = lyc::check(lyc_window_workspace(&lay, G, W));
+  lyc::DeviceBuffer dws((std::size_t)std::max<int64_t>(ws, 16));
+  lyc::check(lyc_window_attention(&lay, 1, kc.get(), vc.get(), G, 0.f, start, W, dq.get(), dout.get(),
+                                  dws.get(), ws, nullptr));
+  std::vector<float> got(q.size());
+  dout.download(got.data(), got.size() * 4);
+  const double scale = 1.0 / std::sqrt((double)d);
+  double worst = 0.0;
+  for (int i = 0; i < W; ++i)
+    for (int hq = 0; hq < Hq; ++hq) {
+      const int g = hq / G, p = start + i;
+      const float* qr = &q[((std::size_t)i * Hq + hq) * d];
+      const float* K = &hk[((std::size_t)1 * H + g) * slab];
+      const float* V = &hv[((std::size_t)1 * H + g) * slab];
+      std::vector<double> w(p + 1);
+      double m = -1e300, den = 0.0;
+      for (int t = 0; t <= p; ++t) {
+        double acc = 0.0;
+        for (int c = 0; c < d; ++c) acc += (double)qr[c] * K[(std::size_t)t * d + c];
+        w[t] = acc * scale;
+        m = std::max(m, w[t]);
+      }
+      for (int t = 0; t <= p; ++t) den += (w[t] = std::exp(w[t] - m));
+      for (int c = 0; c < d; ++c) {
+        double o = 0.0;
+        for (int t = 0; t <= p; ++t) o += w[t] / den * V[(std::size_t)t * d + c];
+        worst = std::max(worst, std::abs(o - got[((std::size_t)i * Hq + hq) * d + c]));
+      }
+    }
+  CHECK(worst < 1e-5);
+}
+
 int main() {
   const std::pair<const char*, std::function<void()>> tests[] = {
       {"PlanSplits.KnownAnswersAndErrors", test_plan_splits_known},
@@ -382,6 +474,7 @@ int main() {
       {"HybridDecoder.TinyStepMatchesHostLoop", test_hybrid_decoder_tiny},
       {"HybridDecoder.Errors", test_hybrid_decoder_errors},
       {"ShardedDecoder.TwoRanksEqualUnsharded", test_sharded_decoder_two_ranks},
+      {"KvCache.AppendOverwriteAndCorrectionAttention", test_kv_cache_and_correction},
   };
   for (const auto& [name, fn] : tests) {
     const int before = g_fail;
