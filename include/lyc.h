@@ -138,6 +138,18 @@ int lyc_decoder_destroy(lyc_decoder* dec);
 int lyc_decoder_step(lyc_decoder* dec, const void* q, const void* k, const void* v,
                      int64_t seq_len, void* out, void* stream);
 
+/* A variable-length batch: seq_lens is host [B], item b's sequence length
+ * (rows 0..seq_lens[b]-1 of its slabs valid, current token included).  The
+ * reference's Workload has one seq_len for the whole batch (kernel_sim.hpp:126)
+ * and DecodeEngine runs one sequence (decode_engine.hpp:95-151); this is B
+ * independent engines' decode_step in one call: each item's retrieval heads
+ * attend its own rows, select from them with its own budget (TopK: min(k, len),
+ * Ratio: ceil((1 - theta) * len)), and its sparse heads read those sets.  Equal
+ * lengths run exactly as lyc_decoder_step; unequal ones use the per-layer
+ * kernels (not the fused step kernel) and are not supported in shard mode. */
+int lyc_decoder_step_varlen(lyc_decoder* dec, const void* q, const void* k, const void* v,
+                            const int64_t* seq_lens, void* out, void* stream);
+
 /* Single layer (decode_engine.hpp:120-143): q_l/out_l are [B][Hq][d]; k/v are
  * the full caches.  Layers must be issued in order within a step. */
 int lyc_decoder_layer(lyc_decoder* dec, int32_t layer, const void* q_l, const void* k,

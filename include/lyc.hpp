@@ -551,6 +551,13 @@ class HybridDecoder {
                    cudaStream_t st = nullptr) {
     check(lyc_decoder_step(d_, q, k, v, (int64_t)seq_len, out, st));
   }
+  // A variable-length batch: seq_lens[b] for batch item b (B independent
+  // sequences; lyc_decoder_step_varlen).
+  void decode_step(const void* q, const void* k, const void* v, const std::vector<std::size_t>& seq_lens,
+                   void* out, cudaStream_t st = nullptr) {
+    std::vector<int64_t> l(seq_lens.begin(), seq_lens.end());
+    check(lyc_decoder_step_varlen(d_, q, k, v, l.data(), out, st));
+  }
   // One layer (layers issued in order within a step).
   void decode_layer(int layer, const void* q_l, const void* k, const void* v, std::size_t seq_len,
                     void* out_l, cudaStream_t st = nullptr) {

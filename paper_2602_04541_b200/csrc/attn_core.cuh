@@ -151,7 +151,7 @@ __device__ __forceinline__ int tiles_per_item(const LycSlot& s, int bs) {
   return s.kind == ITEM_TOKENS ? 1 : (bs + LYC_TILE - 1) / LYC_TILE;
 }
 
-__device__ __forceinline__ Tile tile_of(const LycSlot& s, int item, int sub, int seq, int bs) {
+__device__ __forceinline__ Tile tile_of(const LycSlot& s, int item, int sub, int bs) {
   Tile t;
   if (s.kind == ITEM_TOKENS) {
     t.ids = s.list + (int64_t)item * LYC_TILE;
@@ -162,7 +162,7 @@ __device__ __forceinline__ Tile tile_of(const LycSlot& s, int item, int sub, int
   } else {
     const int blk = s.kind == ITEM_DENSE ? item : __ldcg(s.list + item);
     const int b0 = blk * bs;
-    const int hi = min(b0 + bs, seq);
+    const int hi = min(b0 + bs, s.seq);  // ragged last block of this slot's sequence
     t.ids = nullptr;
     t.cap = 0;
     t.lo = b0 + sub * LYC_TILE;
@@ -233,7 +233,7 @@ __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMa
     const int tpi = tiles_per_item(s, p.block_size);
     const int row0 = (int)(s.kv_off / D);  // tensor-map row of the slab's row 0
     const int nt = (un.end - un.begin) * tpi;
-    Tile t = tile_of(s, un.begin, 0, p.seq_len, p.block_size);
+    Tile t = tile_of(s, un.begin, 0, p.block_size);
     int rows[kRounds];
     load_rows(t, rows);
     for (int f = 0; f < nt; ++f) {
@@ -243,7 +243,7 @@ __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMa
       Tile tn = t;
       int rows_n[kRounds];
       if (f + 1 < nt) {
-        tn = tile_of(s, un.begin + (f + 1) / tpi, (f + 1) % tpi, p.seq_len, p.block_size);
+        tn = tile_of(s, un.begin + (f + 1) / tpi, (f + 1) % tpi, p.block_size);
         load_rows(tn, rows_n);
       }
       {

@@ -114,6 +114,7 @@ struct HostLaunch {
   std::vector<int32_t> split_off;    // [B*S + 1]
   std::vector<LycMergeTask> merges;
   std::vector<int32_t> sel_rows;     // selection index -> index-cache row
+  std::vector<int32_t> sel_n, sel_k; // variable-length batch: keys / ids kept per selection row
   int batch = 0, heads = 0, splits = 0;
 };
 
@@ -175,6 +176,8 @@ struct DevLaunch {
   int32_t* split_off = nullptr;
   LycMergeTask* merges = nullptr;
   int32_t* sel_rows = nullptr;
+  int32_t* sel_n = nullptr;  // null unless the plan is variable-length
+  int32_t* sel_k = nullptr;
   int n_units = 0, n_merges = 0, n_sel = 0;
 };
 
@@ -186,7 +189,8 @@ size_t launch_bytes(const HostLaunch& L) {
          align_up(std::max<size_t>(1, L.units.size()) * sizeof(LycSlot), 256) +
          align_up(L.split_off.size() * 4, 256) +
          align_up(std::max<size_t>(1, L.merges.size()) * sizeof(LycMergeTask), 256) +
-         align_up(std::max<size_t>(1, L.sel_rows.size()) * 4, 256);
+         align_up(std::max<size_t>(1, L.sel_rows.size()) * 4, 256) +
+         2 * align_up(std::max<size_t>(1, L.sel_n.size()) * 4, 256);
 }
 
 // Serialise L into host staging at `off` and return device pointers relative
@@ -215,6 +219,10 @@ DevLaunch stage_launch(const HostLaunch& L, std::vector<uint8_t>& host, size_t& 
                                 align_up(std::max<size_t>(1, L.merges.size()) * sizeof(LycMergeTask), 256));
   d.sel_rows = (int32_t*)put(L.sel_rows.data(), L.sel_rows.size() * 4,
                              align_up(std::max<size_t>(1, L.sel_rows.size()) * 4, 256));
+  if (!L.sel_n.empty()) {
+    d.sel_n = (int32_t*)put(L.sel_n.data(), L.sel_n.size() * 4, align_up(L.sel_n.size() * 4, 256));
+    d.sel_k = (int32_t*)put(L.sel_k.data(), L.sel_k.size() * 4, align_up(L.sel_k.size() * 4, 256));
+  }
   d.n_units = (int)L.units.size();
   d.n_merges = (int)L.merges.size();
   d.n_sel = (int)L.sel_rows.size();
@@ -381,6 +389,7 @@ int lyc_workload_run(const lyc_workload* w, int64_t num_splits, void* out, uint3
         s.kind = ITEM_BLOCKS;
         s.n_items = (int32_t)(w->blk_off[b * H + g + 1] - w->blk_off[b * H + g]);
         s.list_len = s.n_items;
+        s.seq = (int32_t)w->seq_len;
         s.q_row = (int32_t)(b * H * G + g * G);
         s.sel = -1;
         s.dep = -1;
@@ -519,6 +528,8 @@ struct lyc_decoder {
   uint8_t* blob = nullptr;
   size_t blob_cap = 0;
   int64_t planned_seq = -1;
+  bool planned_varlen = false;        // the plan holds per-item lengths (per-layer kernels)
+  std::vector<int64_t> planned_lens;
   LycAttnParams maps{};         // tensor maps for the last (k, v) pointers
   const void* map_k = nullptr;
   const void* map_v = nullptr;
@@ -674,10 +685,31 @@ void free_dev(void* p) {
   if (p) cudaFree(p);
 }
 
-void decoder_plan(lyc_decoder* d, int64_t seq) {
+// lens (optional, host [B]): per-batch-item sequence lengths (a variable-
+// length batch); seq is then their maximum.  Equal lengths plan the uniform
+// way.  A variable-length plan runs on the per-layer kernels: the dense slots
+// of item b cover its ceil(len_b / bs) blocks (ragged last block by the slot's
+// own length), the selection row of (b, g) ranks len_b keys and keeps
+// budget(len_b) ids, and the sparse slots read budget(len_b) ids.
+void decoder_plan(lyc_decoder* d, int64_t seq, const int64_t* lens = nullptr) {
+  if (lens) {
+    bool same = true;
+    for (int b = 0; b < d->B; ++b) {
+      if (lens[b] < 1) fail(LYC_EINVAL, "decode_step: every seq_len must be >= 1");
+      if (lens[b] > d->cfg.seq_cap) fail(LYC_EINVAL, "decode_step: seq_len exceeds seq_cap");
+      same = same && lens[b] == lens[0];
+    }
+    if (same) {
+      seq = lens[0];
+      lens = nullptr;
+    } else {
+      if (d->shard) fail(LYC_ENOTSUP, "decode_step: variable-length batches are not sharded");
+      seq = *std::max_element(lens, lens + d->B);
+    }
+  }
   if (seq < 1) fail(LYC_EINVAL, "decode_step: seq_len must be >= 1");
   if (seq > d->cfg.seq_cap) fail(LYC_EINVAL, "decode_step: seq_len exceeds seq_cap");
-  if (!d->fused && seq > (int64_t)16 * 32768 && d->cfg.select_mode == LYC_SELECT_TOKENS)
+  if ((!d->fused || lens) && seq > (int64_t)16 * 32768 && d->cfg.select_mode == LYC_SELECT_TOKENS)
     fail(LYC_ENOTSUP, "decode_step: token-mode selection supports seq_len <= 524288");
   if (d->fused && d->cfg.select_mode != LYC_SELECT_NONE) {
     // pooled selection limits: <= 64 items per row; block keys in one item
@@ -688,9 +720,13 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
       d->planned_seq = -1;
     }
   }
-  if (d->planned_seq == seq) return;
+  const bool varlen = lens != nullptr;
+  if (!varlen && !d->planned_varlen && d->planned_seq == seq) return;
+  if (varlen && d->planned_varlen && std::equal(lens, lens + d->B, d->planned_lens.begin())) return;
+  const bool fused = d->fused && !varlen;
   const int B = d->B, H = d->H, G = d->G, D = d->D;
   const int64_t kb = d->budget(seq);
+  auto len_of = [&](int b) { return varlen ? lens[b] : seq; };
   const bool blocks = d->cfg.select_mode == LYC_SELECT_BLOCKS;
   const bool none = d->cfg.select_mode == LYC_SELECT_NONE;
   const int64_t nb = (seq + d->bs - 1) / d->bs;
@@ -708,26 +744,33 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
         s.q_row = b * H * G + g * G;
         s.dep = -1;
         s.sel = -1;
+        const int64_t seq_b = len_of(b), nb_b = (seq_b + d->bs - 1) / d->bs;
+        const int64_t kb_b = varlen ? d->budget(seq_b) : kb;
+        s.seq = (int32_t)seq_b;
         if (d->retrieval(l, g)) {
           s.kind = ITEM_DENSE;
-          s.n_items = (int32_t)nb;
+          s.n_items = (int32_t)nb_b;
           if (!none) {
             s.sel = (int32_t)L.sel_rows.size();
             L.sel_rows.push_back(b * H + g);
+            if (varlen) {
+              L.sel_n.push_back((int32_t)(blocks ? nb_b : seq_b));
+              L.sel_k.push_back((int32_t)kb_b);
+            }
           }
         } else {
           s.kind = blocks ? ITEM_BLOCKS : ITEM_TOKENS;
           s.list = d->idx + (int64_t)(b * H + g) * d->k_cap;
-          s.list_len = (int32_t)kb;
+          s.list_len = (int32_t)kb_b;
           if (d->shard || d->variable_sets())  // this rank's filtered set / a variable-size set
             s.count = d->idx_count + (b * H + g);
-          s.n_items = blocks ? (int32_t)kb : (int32_t)((kb + LYC_TILE - 1) / LYC_TILE);
+          s.n_items = blocks ? (int32_t)kb_b : (int32_t)((kb_b + LYC_TILE - 1) / LYC_TILE);
           s.dep = last_r[(size_t)g];
         }
       }
     for (int g = 0; g < H; ++g)
       if (d->retrieval(l, g)) last_r[(size_t)g] = l;
-    if (d->fused)
+    if (fused)
     {
       // this layer's selection items run on the last n_items CTAs when they
       // fit in half the grid (step.cu split roles)
@@ -816,6 +859,8 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
     tp.out_count = d->idx_count;
     tp.slice = (int32_t)((sel_n + cluster - 1) / cluster);
     tp.clear_keys = blocks ? 1 : 0;
+    tp.row_n = dl.sel_n;
+    tp.row_k = dl.sel_k;
     LycPolicyParams& pp = ly.pp;
     std::memset(&pp, 0, sizeof(pp));
     pp.keys = d->sel_keys;
@@ -829,6 +874,7 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
     pp.out_row = dl.sel_rows;
     pp.out_stride = d->k_cap;
     pp.out_count = d->idx_count;
+    pp.row_n = dl.sel_n;
     ly.n_sel = dl.n_sel;
     ly.cluster = cluster;
     LycLayerDesc& ds = descs[(size_t)l];
@@ -851,7 +897,9 @@ void decoder_plan(lyc_decoder* d, int64_t seq) {
   if (d->sel_rowctr)
     cuda_check(cudaMemset(d->sel_rowctr, 0, (size_t)d->NL * d->B * d->H * 16 * 4), "memset rowctr");
   cuda_check(cudaDeviceSynchronize(), "sync");
-  d->planned_seq = seq;
+  d->planned_seq = varlen ? -1 : seq;
+  d->planned_varlen = varlen;
+  if (varlen) d->planned_lens.assign(lens, lens + d->B);
 }
 
 void ensure_maps(lyc_decoder* d, const void* k, const void* v) {
@@ -902,11 +950,11 @@ void decoder_layer(lyc_decoder* d, int l, const void* q_l, const void* k, const 
 }
 
 void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, int64_t seq,
-                  void* out, cudaStream_t st) {
-  decoder_plan(d, seq);
+                  void* out, cudaStream_t st, const int64_t* lens = nullptr) {
+  decoder_plan(d, seq, lens);
   const int esz = elem_bytes(d->cfg.dtype);
   const size_t qstride = (size_t)d->B * d->Hq * d->D;
-  if (!d->fused) {
+  if (!d->fused || d->planned_varlen) {
     for (int l = 0; l < d->NL; ++l)
       decoder_layer(d, l, (const uint8_t*)q + l * qstride * esz, k, v,
                     (uint8_t*)out + l * qstride * esz, st);
@@ -1098,6 +1146,16 @@ int lyc_decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v
   return (int)guarded([&]() -> int64_t {
     if (!d) fail(LYC_EINVAL, "decoder: null");
     decoder_step(d, q, k, v, seq_len, out, (cudaStream_t)stream);
+    return LYC_OK;
+  });
+}
+
+int lyc_decoder_step_varlen(lyc_decoder* d, const void* q, const void* k, const void* v,
+                            const int64_t* seq_lens, void* out, void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    if (!seq_lens) fail(LYC_EINVAL, "decode_step: seq_lens is null");
+    decoder_step(d, q, k, v, 0, out, (cudaStream_t)stream, seq_lens);
     return LYC_OK;
   });
 }

@@ -44,6 +44,8 @@ struct LycSlot {
   int32_t sel;           // selection output row (-1: none)
   int32_t dep;           // layer whose selection wrote `list` (-1: none / already complete)
   const int32_t* count;  // ITEM_TOKENS: device count of valid ids (<= list_len), or nullptr
+  int32_t seq;           // rows of this slot's sequence (seq_len of its batch item)
+  int32_t pad_;
 };
 
 struct LycUnit {
@@ -132,6 +134,8 @@ struct LycTopkParams {
   int32_t* out_count;       // [cache rows] number of ids written (may be null)
   int32_t slice;            // keys per CTA of the cluster
   int32_t clear_keys;       // zero keys after use (block-max keys are atomicMax'ed)
+  const int32_t* row_n;     // optional [n_sel]: candidates of each row (variable-length batch)
+  const int32_t* row_k;     // optional [n_sel]: ids kept per row (<= row_n)
 };
 
 // TopP / Threshold selection (policy.cu): one CTA per selection row.
@@ -149,6 +153,7 @@ struct LycPolicyParams {
   const int32_t* out_row;   // [n_sel] -> row in the index cache
   int64_t out_stride;       // index cache row stride (k_cap)
   int32_t* out_count;       // [cache rows] size of each set
+  const int32_t* row_n;     // optional [n_sel]: tokens of each row (variable-length batch)
 };
 
 // ---------------------------------------------------------------------------

@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kPolThreads, 1) policy_select_kernel(const __g
   __shared__ PolSmem s;
   const int r = blockIdx.x;
   const uint32_t* kr = p.keys + (int64_t)r * p.key_stride;
-  const int n = p.n;
+  const int n = p.row_n ? p.row_n[r] : p.n;  // variable-length batch: this row's tokens
   const int C = (n + kPolThreads - 1) / kPolThreads;  // contiguous keys per thread
   const int b0 = threadIdx.x * C, b1 = min(n, b0 + C);
   const int orow = p.out_row[r];

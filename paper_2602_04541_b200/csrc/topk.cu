@@ -81,15 +81,17 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_cluster_kernel(const __g
   uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw + sizeof(TopkShared));
 
   uint32_t* gkeys = p.keys + (int64_t)row * p.key_stride;
+  const int n_row = p.row_n ? p.row_n[row] : p.n;  // variable-length batch: this row's keys
+  const int k_row = p.row_k ? p.row_k[row] : p.k;
   const int lo = rank * p.slice;
-  const int cnt = max(0, min(p.slice, p.n - lo));
+  const int cnt = max(0, min(p.slice, n_row - lo));
   for (int i = tid; i < cnt; i += kTopkThreads) {
     keys[i] = gkeys[lo + i];
     if (p.clear_keys) gkeys[lo + i] = 0u;
   }
 
   uint32_t prefix = 0, pmask = 0;
-  uint32_t krem = (uint32_t)p.k;  // still to take among keys matching the prefix
+  uint32_t krem = (uint32_t)k_row;  // still to take among keys matching the prefix
   constexpr int kShift[3] = {21, 10, 0};
   constexpr uint32_t kMask[3] = {0x7ffu, 0x7ffu, 0x3ffu};
 #pragma unroll
@@ -192,7 +194,7 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_cluster_kernel(const __g
     run_gt += tot & 0xffffu;
     run_eq += tot >> 16;
   }
-  if (rank == 0 && tid == 0 && p.out_count) p.out_count[p.out_row[row]] = p.k;
+  if (rank == 0 && tid == 0 && p.out_count) p.out_count[p.out_row[row]] = k_row;
   cluster.sync();  // keep smem alive until every CTA has read our counts
 }
 

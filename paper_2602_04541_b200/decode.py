@@ -134,13 +134,26 @@ class HybridDecoder:
     def _stream(stream):
         return (stream if stream is not None else torch.cuda.current_stream()).cuda_stream
 
-    def decode_step(self, q, k_cache, v_cache, seq_len: int, out=None, *, stream=None):
-        """All layers of one step (decode_engine.hpp:109-151)."""
+    def decode_step(self, q, k_cache, v_cache, seq_len, out=None, *, stream=None):
+        """All layers of one step (decode_engine.hpp:109-151).
+
+        seq_len is an int (every batch item), or one length per batch item (a
+        variable-length batch: B independent sequences, lyc_decoder_step_varlen).
+        """
         if out is None:
             out = torch.empty_like(q)
-        check(lib().lyc_decoder_step(self._h, q.data_ptr(), k_cache.data_ptr(),
-                                     v_cache.data_ptr(), seq_len, out.data_ptr(),
-                                     self._stream(stream)))
+        if isinstance(seq_len, (int, np.integer)):
+            check(lib().lyc_decoder_step(self._h, q.data_ptr(), k_cache.data_ptr(),
+                                         v_cache.data_ptr(), seq_len, out.data_ptr(),
+                                         self._stream(stream)))
+            return out
+        lens = [int(x) for x in seq_len]
+        if len(lens) != self.batch:
+            raise ValueError("decode_step: one seq_len per batch item")
+        arr = (C.c_int64 * len(lens))(*lens)
+        check(lib().lyc_decoder_step_varlen(self._h, q.data_ptr(), k_cache.data_ptr(),
+                                            v_cache.data_ptr(), arr, out.data_ptr(),
+                                            self._stream(stream)))
         return out
 
     def layer(self, l: int, q_l, k_cache, v_cache, seq_len: int, out_l=None, *, stream=None):
