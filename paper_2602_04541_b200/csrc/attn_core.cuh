@@ -256,9 +256,9 @@ __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMa
           bool mine = false;
           if (t.ids) {
 #pragma unroll
-            for (int i = 0; i < kRounds; ++i) mine |= rows[i] == p.seq_len - 1;
+            for (int i = 0; i < kRounds; ++i) mine |= rows[i] == s.seq - 1;
           } else {
-            mine = t.nvalid > 0 && t.lo + t.nvalid == p.seq_len;
+            mine = t.nvalid > 0 && t.lo + t.nvalid == s.seq;
           }
           if (waits.any(mine)) waits.last_tile();
         }

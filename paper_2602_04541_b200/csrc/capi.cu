@@ -723,7 +723,7 @@ void decoder_plan(lyc_decoder* d, int64_t seq, const int64_t* lens = nullptr) {
   const bool varlen = lens != nullptr;
   if (!varlen && !d->planned_varlen && d->planned_seq == seq) return;
   if (varlen && d->planned_varlen && std::equal(lens, lens + d->B, d->planned_lens.begin())) return;
-  const bool fused = d->fused && !varlen;
+  const bool fused = d->fused;
   const int B = d->B, H = d->H, G = d->G, D = d->D;
   const int64_t kb = d->budget(seq);
   auto len_of = [&](int b) { return varlen ? lens[b] : seq; };
@@ -884,6 +884,8 @@ void decoder_plan(lyc_decoder* d, int64_t seq, const int64_t* lens = nullptr) {
     ds.split_off = dl.split_off;
     ds.merges = dl.merges;
     ds.sel_rows = dl.sel_rows;
+    ds.sel_n = dl.sel_n;
+    ds.sel_k = dl.sel_k;
     ds.n_merges = dl.n_merges;
     ds.n_sel = dl.n_sel;
     ly.desc = ds;
@@ -954,7 +956,7 @@ void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, i
   decoder_plan(d, seq, lens);
   const int esz = elem_bytes(d->cfg.dtype);
   const size_t qstride = (size_t)d->B * d->Hq * d->D;
-  if (!d->fused || d->planned_varlen) {
+  if (!d->fused) {
     for (int l = 0; l < d->NL; ++l)
       decoder_layer(d, l, (const uint8_t*)q + l * qstride * esz, k, v,
                     (uint8_t*)out + l * qstride * esz, st);

@@ -165,6 +165,8 @@ struct LycLayerDesc {
   const int32_t* split_off;
   const LycMergeTask* merges;
   const int32_t* sel_rows;  // selection index -> index-cache row
+  const int32_t* sel_n;     // optional [n_sel] (variable-length batch): keys of each row
+  const int32_t* sel_k;     // optional [n_sel]: ids kept per row
   int32_t n_merges;
   int32_t n_sel;
 };

@@ -314,6 +314,8 @@ __device__ __forceinline__ void epi_digit(EpiSmem& es, const uint32_t* h, bool g
 }
 
 struct SelRow {
+  uint32_t k;         // ids kept (variable-length batch: this row's budget)
+  int n;              // keys of this row's sequence (<= p.n_keys; the rest are masked)
   uint32_t* keys;     // keys of the row [n]
   uint32_t* h1;       // fused first-pass (12-bit) histogram (token mode) or nullptr
   uint32_t* bitmap;   // [n_words]
@@ -329,6 +331,9 @@ struct SelRow {
 __device__ __forceinline__ SelRow sel_row(const LycStepParams& p, int l, int r) {
   const int64_t pr = (int64_t)(l & 1) * p.max_sel + r;
   SelRow s;
+  const LycLayerDesc& L = p.layers[l];
+  s.k = L.sel_k ? (uint32_t)__ldg(L.sel_k + r) : (uint32_t)p.k_sel;
+  s.n = L.sel_n ? __ldg(L.sel_n + r) : p.n_keys;
   s.keys = p.sel_keys + pr * p.sel_stride;
   s.h1 = p.sel_mode == SEL_TOKEN_KEYS ? p.hist + pr * LYC_H1_STRIDE : nullptr;
   s.bitmap = p.sel_bitmap + pr * p.bitmap_stride;
@@ -350,7 +355,7 @@ __device__ __forceinline__ void row_prefix(const LycStepParams& p, const SelRow&
     // two coalesced L2 reads by warp 0: the 64 coarse bins, then the 64 fine
     // bins of the chosen coarse bin (lane i holds bins 2(31-i), 2(31-i)+1)
     if (et < 32) {
-      uint32_t k = (uint32_t)p.k_sel, base = 0, above = 0;
+      uint32_t k = R.k, base = 0, above = 0;
       const uint32_t* h = R.h1 + LYC_H1_BINS;
 #pragma unroll
       for (int level = 0; level < 2; ++level) {
@@ -382,7 +387,7 @@ __device__ __forceinline__ void row_prefix(const LycStepParams& p, const SelRow&
     }
     epi_bar();
   } else
-    epi_digit(es, es.hist, false, LYC_BINS, (uint32_t)p.k_sel, et);
+    epi_digit(es, es.hist, false, LYC_BINS, R.k, et);
   if (et == 0) es.last = R.h1 ? 32u - LYC_H1_BITS : 21u;
   epi_bar();
 }
@@ -395,6 +400,9 @@ __device__ void classify_item(const LycStepParams& p, const SelRow& R, int q, Ep
   const int n = p.n_keys;
   const int lo = q * kItemKeys;
   const int cnt = min(kItemKeys, n - lo);
+  // keys of this row's own sequence (a shorter item of a variable-length
+  // batch: the rest of the padded row is masked out, never selected)
+  const int vcnt = min(cnt, R.n - lo);
   if (et == 0) {
     fence_proxy_async();         // earlier generic use of es.buf -> TMA write
     fence_proxy_async_global();  // consumers' key stores (acquired) -> TMA read
@@ -406,7 +414,7 @@ __device__ void classify_item(const LycStepParams& p, const SelRow& R, int q, Ep
     mbar_wait(&es.bar, bar_phase);
     for (int b = et; b < LYC_BINS; b += kEpiThreads) es.hist[b] = 0u;
     epi_bar();
-    for (int i = et; i < cnt; i += kEpiThreads) atomicAdd(&es.hist[es.buf[i] >> 21], 1u);
+    for (int i = et; i < vcnt; i += kEpiThreads) atomicAdd(&es.hist[es.buf[i] >> 21], 1u);
     epi_bar();
   }
   row_prefix(p, R, es, et);
@@ -443,7 +451,7 @@ __device__ void classify_item(const LycStepParams& p, const SelRow& R, int q, Ep
     }
     ta = __funnelshift_l(ta, ta, rot);
     tg = __funnelshift_l(tg, tg, rot);
-    const int valid = cnt - (k0 + w * 32);
+    const int valid = vcnt - (k0 + w * 32);
     const uint32_t vm = valid >= 32 ? 0xffffffffu : valid <= 0 ? 0u : (1u << valid) - 1u;
     words[w] = ta & vm;
     eqm[w] = tg & ~ta & vm;
@@ -576,7 +584,7 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
   }
   uint32_t P = __ldcg(R.ccnt + 192);
   int shift = (int)__ldcg(R.ccnt + 194);
-  uint32_t krem = (uint32_t)p.k_sel - __ldcg(R.ccnt + 193);
+  uint32_t krem = R.k - __ldcg(R.ccnt + 193);
   const int ns = (int)__ldcg(R.ctr + 4);  // candidates of the row
   const uint32_t d_mine = et < items ? __ldcg(R.ccnt + 64 + et) : 0u;
   if (et < items) {
@@ -849,7 +857,7 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
       m4w &= m4w - 1u;
     }
   }
-  if (q == 0 && et == 0 && p.idx_count) p.idx_count[row] = p.k_sel;
+  if (q == 0 && et == 0 && p.idx_count) p.idx_count[row] = (int32_t)R.k;
   if (es.last) {
     if (et == 0) R.ctr[4] = 0u;
     if (p.sel_mode == SEL_BLOCK_KEYS)

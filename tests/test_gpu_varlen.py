@@ -157,3 +157,36 @@ def test_varlen_errors():
         dec.decode_step(qd, Kd, Vd, [100, cap + 1])
     with pytest.raises(ValueError):
         dec.decode_step(qd, Kd, Vd, [100])
+
+
+@pytest.mark.parametrize("select,k", [("tokens", 512), ("blocks", 1024)])
+def test_varlen_fused_equals_per_item_decoders(select, k):
+    """bf16 ragged batches run on the fused step kernel (per-row budgets, the
+    padded tail of shorter rows masked out of the selection): every item's
+    sets equal those of a batch-1 decoder at its own length, and its outputs
+    agree within bf16 rounding (the split-KV partition differs)."""
+    import paper_2602_04541_b200 as P
+    NL, H, G, d, cap = 4, 8, 4, 128, 8192
+    lens = [5000, 8192, 777]
+    roles = roles_for(NL, H, [(1, 3), (2, 5), (3, 0)])
+    B = len(lens)
+    q, K, V = synth(31, NL, B, H, G, d, cap, torch.bfloat16)
+    qd, Kd, Vd = q.cuda(), K.cuda(), V.cuda()
+    mk = lambda b: P.HybridDecoder(n_layers=NL, batch=b, n_kv_heads=H, group_size=G,  # noqa: E731
+                                   d_head=d, seq_cap=cap, roles=roles,
+                                   policy=P.SparsityPolicy.top_k(k), dtype=torch.bfloat16,
+                                   select=select)
+    dec = mk(B)
+    out = dec.decode_step(qd, Kd, Vd, lens)
+    torch.cuda.synchronize()
+    assert dec.fused
+    sets = dec.token_sets()
+    for b, L in enumerate(lens):
+        one = mk(1)
+        o1 = one.decode_step(qd[:, b:b + 1].contiguous(), Kd[:, b:b + 1].contiguous(),
+                             Vd[:, b:b + 1].contiguous(), L)
+        torch.cuda.synchronize()
+        s1 = one.token_sets()[0]
+        for g in range(H):
+            assert np.array_equal(sets[b][g], s1[g]), (b, g)
+        assert rel_err(out[:, b].float().cpu().numpy(), o1[:, 0].float().cpu().numpy()) < 1e-2
