@@ -585,10 +585,10 @@ void plan_step_launch(HostLaunch& L, int batch, int heads, int splits, int group
   L.splits = splits;
   L.units.clear();
   L.merges.clear();
-  L.split_off.assign((size_t)batch * splits + 1, 0);
-  std::vector<std::vector<std::vector<LycUnit>>> per_split((size_t)batch);
+  const int cells = batch * splits;
+  L.split_off.assign((size_t)cells + 1, 0);
+  std::vector<std::vector<LycUnit>> per_cell((size_t)cells);
   for (int b = 0; b < batch; ++b) {
-    per_split[(size_t)b].assign((size_t)splits, {});
     int64_t total = 0;
     for (int g = 0; g < heads; ++g) {
       LycSlot& s = L.slots[(size_t)b * heads + g];
@@ -596,78 +596,87 @@ void plan_step_launch(HostLaunch& L, int batch, int heads, int splits, int group
       total += s.n_items;
     }
     if (total == 0) fail(LYC_EINVAL, "plan_splits: batch item has zero blocks");
-    for (int pool = 0; pool < 3; ++pool) {
-      std::vector<int> hs;
-      int64_t tot = 0;
-      for (int g = 0; g < heads; ++g) {
-        const LycSlot& s = L.slots[(size_t)b * heads + g];
-        const bool late = s.dep >= 0 && s.dep == layer - 1;
-        const int my_pool = s.kind == ITEM_DENSE ? 0 : late ? 2 : 1;
-        if (my_pool == pool && s.n_items > 0) {
-          hs.push_back(g);
-          tot += s.n_items;
-        }
+  }
+  // Equal lengths: each batch item's pools are cut across its own `splits`
+  // cells.  A variable-length batch: each pool is cut across ALL cells
+  // (every item's slots in one list), so short items do not leave their SMs
+  // idle while long ones stream.
+  bool ragged = false;
+  for (int b = 1; b < batch; ++b) ragged = ragged || L.slots[(size_t)b * heads].seq != L.slots[0].seq;
+  const int groups = ragged ? 1 : batch;
+  for (int grp = 0; grp < groups; ++grp)
+  for (int pool = 0; pool < 3; ++pool) {
+    const int b0 = ragged ? 0 : grp, b1 = ragged ? batch : grp + 1;
+    const int c0 = b0 * splits, nc = (b1 - b0) * splits;  // this group's cells
+    std::vector<int> hs;  // slot indices of this pool, in (b, g) order
+    int64_t tot = 0;
+    for (int i = b0 * heads; i < b1 * heads; ++i) {
+      const LycSlot& s = L.slots[(size_t)i];
+      const bool late = s.dep >= 0 && s.dep == layer - 1;
+      const int my_pool = s.kind == ITEM_DENSE ? 0 : late ? 2 : 1;
+      if (my_pool == pool && s.n_items > 0) {
+        hs.push_back(i);
+        tot += s.n_items;
       }
-      if (tot == 0) continue;
-      // the sparse pools skip the CTAs that run this layer's selection items
-      // (cells >= free_from): their epilogue classifies while the others
-      // stream, without sharing issue slots with busy consumers
-      int ns = splits;
-      if (pool >= 1) {
-        const int usable = std::min(splits, free_from - b * splits);
-        if (usable >= (splits + 1) / 2) ns = usable;  // never squeeze a batch item onto a few CTAs
+    }
+    if (tot == 0) continue;
+    // the sparse pools skip the CTAs that run this layer's selection items
+    // (cells >= free_from): their epilogue classifies while the others
+    // stream, without sharing issue slots with busy consumers
+    int ns = nc;
+    if (pool >= 1) {
+      const int usable = std::min(nc, free_from - c0);
+      if (usable >= (nc + 1) / 2) ns = usable;  // never squeeze a group onto a few CTAs
+    }
+    // even cut points, then snapped onto a slot boundary within one item:
+    // a cell that would hold the end of one slot and the start of the next
+    // (two units: an extra unit epilogue and signal) gets one item more or
+    // less instead
+    const int64_t base = tot / ns, rem = tot % ns;
+    constexpr int64_t kSnap = 1;  // items (measured: 1 beats 2 and 3)
+    std::vector<int64_t> cut((size_t)nc + 1);
+    for (int sp = 0; sp <= nc; ++sp)
+      cut[(size_t)sp] = sp <= ns ? sp * base + std::min<int64_t>(sp, rem) : tot;
+    {
+      int64_t hb = 0;
+      for (size_t h = 0; h + 1 < hs.size(); ++h) {
+        hb += L.slots[(size_t)hs[h]].n_items;
+        // the cut nearest to the boundary hb
+        int sp = (int)std::min<int64_t>(ns - 1, std::max<int64_t>(1, hb / std::max<int64_t>(base, 1)));
+        while (sp > 1 && cut[(size_t)sp] > hb) --sp;
+        while (sp < ns - 1 && cut[(size_t)sp + 1] <= hb) ++sp;
+        for (int c = sp; c <= sp + 1 && c < ns; ++c)
+          if (c >= 1 && std::llabs(cut[(size_t)c] - hb) <= kSnap && cut[(size_t)c - 1] < hb &&
+              hb < cut[(size_t)c + 1])
+            cut[(size_t)c] = hb;
       }
-      // even cut points, then snapped onto a head boundary within one item:
-      // a split that would hold the end of one head and the start of the next
-      // (two units: an extra unit epilogue and signal) gets one item more or
-      // less instead
-      const int64_t base = tot / ns, rem = tot % ns;
-      constexpr int64_t kSnap = 1;  // items (measured: 1 beats 2 and 3)
-      std::vector<int64_t> cut((size_t)splits + 1);
-      for (int sp = 0; sp <= splits; ++sp)
-        cut[(size_t)sp] = sp <= ns ? sp * base + std::min<int64_t>(sp, rem) : tot;
-      {
-        int64_t hb = 0;
-        for (size_t h = 0; h + 1 < hs.size(); ++h) {
-          hb += L.slots[(size_t)b * heads + hs[h]].n_items;
-          // the cut nearest to the boundary hb
-          int sp = (int)std::min<int64_t>(ns - 1, std::max<int64_t>(1, hb / std::max<int64_t>(base, 1)));
-          while (sp > 1 && cut[(size_t)sp] > hb) --sp;
-          while (sp < ns - 1 && cut[(size_t)sp + 1] <= hb) ++sp;
-          for (int c = sp; c <= sp + 1 && c < ns; ++c)
-            if (c >= 1 && std::llabs(cut[(size_t)c] - hb) <= kSnap && cut[(size_t)c - 1] < hb &&
-                hb < cut[(size_t)c + 1])
-              cut[(size_t)c] = hb;
+    }
+    size_t hi = 0;
+    int64_t offset = 0;
+    for (int sp = 0; sp < nc; ++sp) {
+      int64_t want = cut[(size_t)sp + 1] - cut[(size_t)sp];
+      while (want > 0) {
+        while (L.slots[(size_t)hs[hi]].n_items == offset) {
+          ++hi;
+          offset = 0;
         }
-      }
-      size_t hi = 0;
-      int64_t offset = 0;
-      for (int sp = 0; sp < splits; ++sp) {
-        int64_t want = cut[(size_t)sp + 1] - cut[(size_t)sp];
-        while (want > 0) {
-          while (L.slots[(size_t)b * heads + hs[hi]].n_items == offset) {
-            ++hi;
-            offset = 0;
-          }
-          LycSlot& sl = L.slots[(size_t)b * heads + hs[hi]];
-          const int64_t take = std::min<int64_t>(sl.n_items - offset, want);
-          LycUnit u;
-          u.slot = b * heads + hs[hi];
-          u.begin = (int32_t)offset;
-          u.end = (int32_t)(offset + take);
-          u.hls = sl.n_units++;
-          per_split[(size_t)b][(size_t)sp].push_back(u);
-          offset += take;
-          want -= take;
-        }
+        LycSlot& sl = L.slots[(size_t)hs[hi]];
+        const int64_t take = std::min<int64_t>(sl.n_items - offset, want);
+        LycUnit u;
+        u.slot = hs[hi];
+        u.begin = (int32_t)offset;
+        u.end = (int32_t)(offset + take);
+        u.hls = sl.n_units++;
+        per_cell[(size_t)(c0 + sp)].push_back(u);
+        offset += take;
+        want -= take;
       }
     }
   }
-  for (int b = 0; b < batch; ++b)
-    for (int sp = 0; sp < splits; ++sp) {
-      L.split_off[(size_t)b * splits + sp] = (int32_t)L.units.size();
-      for (const LycUnit& u : per_split[(size_t)b][(size_t)sp]) L.units.push_back(u);
-    }
+  for (int c = 0; c < cells; ++c) {
+    L.split_off[(size_t)c] = (int32_t)L.units.size();
+    for (const LycUnit& u : per_cell[(size_t)c]) L.units.push_back(u);
+  }
   L.split_off[(size_t)batch * splits] = (int32_t)L.units.size();
   int32_t base = 0;  // partial-output base of every slot (units of a slot need not be adjacent)
   for (auto& s : L.slots) {
