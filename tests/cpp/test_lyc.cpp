@@ -464,6 +464,74 @@ static void test_kv_cache_and_correction() {
   CHECK(worst < 1e-5);
 }
 
+// A variable-length batch (lyc_decoder_step_varlen) equals batch-1 decoders
+// each run at its own item's length (DecodeEngine is one sequence,
+// decode_engine.hpp:95-151).
+static void test_decoder_varlen() {
+  const int NL = 3, B = 2, H = 2, G = 2, d = 64, cap = 4096, K = 128;
+  const std::vector<std::size_t> lens = {3000, 1100};
+  std::vector<uint8_t> roles(NL * H, 1);
+  roles[0] = roles[1] = 0;
+  roles[1 * H + 1] = 0;
+  std::mt19937_64 rng(77);
+  std::uniform_real_distribution<float> U(-1.f, 1.f);
+  const std::size_t qi = (std::size_t)H * G * d, ki = (std::size_t)H * cap * d;
+  std::vector<float> q((size_t)NL * B * qi), k((size_t)NL * B * ki), v(k.size());
+  for (auto* vec : {&q, &k, &v})
+    for (auto& x : *vec) x = U(rng);
+  lyc::HybridDecoder::Config c;
+  c.n_layers = NL;
+  c.batch = B;
+  c.n_kv_heads = H;
+  c.group_size = G;
+  c.d_head = d;
+  c.dtype = lyc::Dtype::F32;
+  c.seq_cap = cap;
+  c.policy = lyc::SparsityPolicy::top_k(K);
+  lyc::DeviceBuffer dq(q.size() * 4), dk(k.size() * 4), dv(v.size() * 4), dout(q.size() * 4);
+  dq.upload(q.data(), q.size() * 4);
+  dk.upload(k.data(), k.size() * 4);
+  dv.upload(v.data(), v.size() * 4);
+  lyc::HybridDecoder dec(c, roles);
+  dec.decode_step(dq.get(), dk.get(), dv.get(), lens, dout.get());
+  cudaDeviceSynchronize();
+  std::vector<float> out(q.size());
+  dout.download(out.data(), out.size() * 4);
+  const auto sets = dec.token_sets();
+  c.batch = 1;
+  double worst = 0.0;
+  bool sets_equal = true;
+  for (int b = 0; b < B; ++b) {
+    std::vector<float> q1((size_t)NL * qi), k1((size_t)NL * ki), v1(k1.size());
+    for (int l = 0; l < NL; ++l) {
+      std::copy_n(q.begin() + ((size_t)l * B + b) * qi, qi, q1.begin() + (size_t)l * qi);
+      std::copy_n(k.begin() + ((size_t)l * B + b) * ki, ki, k1.begin() + (size_t)l * ki);
+      std::copy_n(v.begin() + ((size_t)l * B + b) * ki, ki, v1.begin() + (size_t)l * ki);
+    }
+    lyc::DeviceBuffer eq(q1.size() * 4), ek(k1.size() * 4), ev(v1.size() * 4), eo(q1.size() * 4);
+    eq.upload(q1.data(), q1.size() * 4);
+    ek.upload(k1.data(), k1.size() * 4);
+    ev.upload(v1.data(), v1.size() * 4);
+    lyc::HybridDecoder one(c, roles);
+    one.decode_step(eq.get(), ek.get(), ev.get(), lens[(size_t)b], eo.get());
+    cudaDeviceSynchronize();
+    std::vector<float> o1(q1.size());
+    eo.download(o1.data(), o1.size() * 4);
+    for (int l = 0; l < NL; ++l)
+      for (std::size_t i = 0; i < qi; ++i)
+        worst = std::max(worst, (double)std::abs(out[((size_t)l * B + b) * qi + i] - o1[(size_t)l * qi + i]));
+    const auto s1 = one.token_sets();
+    for (int g = 0; g < H; ++g) sets_equal = sets_equal && sets[(size_t)b * H + g] == s1[(size_t)g];
+  }
+  std::printf("  varlen: max |diff| vs batch-1 decoders %.2e, sets equal: %s\n", worst,
+              sets_equal ? "yes" : "no");
+  CHECK(worst < 1e-5);
+  CHECK(sets_equal);
+  CHECK(sets[1].size() == (std::size_t)K && sets[1].back() < 3000);
+  CHECK_THROWS(dec.decode_step(dq.get(), dk.get(), dv.get(), std::vector<std::size_t>{10, 0}, dout.get()),
+               std::invalid_argument);
+}
+
 int main() {
   const std::pair<const char*, std::function<void()>> tests[] = {
       {"PlanSplits.KnownAnswersAndErrors", test_plan_splits_known},
@@ -475,6 +543,7 @@ int main() {
       {"HybridDecoder.Errors", test_hybrid_decoder_errors},
       {"ShardedDecoder.TwoRanksEqualUnsharded", test_sharded_decoder_two_ranks},
       {"KvCache.AppendOverwriteAndCorrectionAttention", test_kv_cache_and_correction},
+      {"HybridDecoder.VariableLengthBatch", test_decoder_varlen},
   };
   for (const auto& [name, fn] : tests) {
     const int before = g_fail;
