@@ -159,6 +159,10 @@ int lyc_decoder_layer(lyc_decoder* dec, int32_t layer, const void* q_l, const vo
  * then replay it.  replay returns LYC_ESTATE if nothing was captured. */
 int lyc_decoder_capture(lyc_decoder* dec, const void* q, const void* k, const void* v,
                         int64_t seq_len, void* out, void* stream);
+/* The same for a variable-length batch (host seq_lens [B], as in
+ * lyc_decoder_step_varlen); replay re-runs the captured lengths. */
+int lyc_decoder_capture_varlen(lyc_decoder* dec, const void* q, const void* k, const void* v,
+                               const int64_t* seq_lens, void* out, void* stream);
 int lyc_decoder_replay(lyc_decoder* dec, void* stream);
 
 /* The device index cache: ids [B*H][k_cap] int32 (ascending token ids, or

@@ -28,7 +28,7 @@ SYMBOLS = [
     "lyc_decoder_step_bytes", "lyc_decoder_layer_attn_bytes", "lyc_decoder_set_timing",
     "lyc_decoder_attn_ms", "lyc_decoder_is_fused", "lyc_decoder_set_trace", "lyc_decoder_trace",
     "lyc_shard_layer", "lyc_shard_merge", "lyc_kv_write", "lyc_window_workspace",
-    "lyc_window_attention", "lyc_decoder_step_varlen",
+    "lyc_window_attention", "lyc_decoder_step_varlen", "lyc_decoder_capture_varlen",
 ]
 
 
@@ -113,6 +113,8 @@ def lib() -> C.CDLL:
     L.lyc_decoder_step.argtypes = [vp, vp, vp, vp, i64, vp, vp]
     L.lyc_decoder_step_varlen.restype = C.c_int
     L.lyc_decoder_step_varlen.argtypes = [vp, vp, vp, vp, C.POINTER(C.c_int64), vp, vp]
+    L.lyc_decoder_capture_varlen.restype = C.c_int
+    L.lyc_decoder_capture_varlen.argtypes = [vp, vp, vp, vp, C.POINTER(C.c_int64), vp, vp]
     L.lyc_decoder_layer.restype = C.c_int
     L.lyc_decoder_layer.argtypes = [vp, i32, vp, vp, vp, i64, vp, vp]
     L.lyc_decoder_capture.restype = C.c_int

@@ -528,7 +528,8 @@ struct lyc_decoder {
   uint8_t* blob = nullptr;
   size_t blob_cap = 0;
   int64_t planned_seq = -1;
-  bool planned_varlen = false;        // the plan holds per-item lengths (per-layer kernels)
+  bool planned_varlen = false;
+  int64_t captured_launches = 0;      // kernel launches in the captured graph        // the plan holds per-item lengths (per-layer kernels)
   std::vector<int64_t> planned_lens;
   LycAttnParams maps{};         // tensor maps for the last (k, v) pointers
   const void* map_k = nullptr;
@@ -1323,12 +1324,12 @@ int lyc_shard_merge(lyc_decoder* d, int32_t layer, int32_t world, const float* a
   });
 }
 
-int lyc_decoder_capture(lyc_decoder* d, const void* q, const void* k, const void* v,
-                        int64_t seq_len, void* out, void* stream) {
-  return (int)guarded([&]() -> int64_t {
+namespace {
+int64_t decoder_capture(lyc_decoder* d, const void* q, const void* k, const void* v,
+                        int64_t seq_len, const int64_t* lens, void* out, void* stream) {
     if (!d) fail(LYC_EINVAL, "decoder: null");
     cudaStream_t st = (cudaStream_t)stream;
-    decoder_plan(d, seq_len);  // host work + plan upload outside the capture
+    decoder_plan(d, seq_len, lens);  // host work + plan upload outside the capture
     ensure_maps(d, k, v);
     if (d->exec) {
       cudaGraphExecDestroy(d->exec);
@@ -1341,17 +1342,33 @@ int lyc_decoder_capture(lyc_decoder* d, const void* q, const void* k, const void
     const int64_t before = g_launches;
     cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
     try {
-      decoder_step(d, q, k, v, seq_len, out, st);
+      decoder_step(d, q, k, v, seq_len, out, st, lens);
     } catch (...) {
       cudaGraph_t g = nullptr;
       cudaStreamEndCapture(st, &g);
       if (g) cudaGraphDestroy(g);
       throw;
     }
+    d->captured_launches = g_launches - before;
     g_launches = before;  // captured launches execute on replay
     cuda_check(cudaStreamEndCapture(st, &d->graph), "end capture");
     cuda_check(cudaGraphInstantiate(&d->exec, d->graph, 0), "graph instantiate");
     return LYC_OK;
+}
+}  // namespace
+
+int lyc_decoder_capture(lyc_decoder* d, const void* q, const void* k, const void* v,
+                        int64_t seq_len, void* out, void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    return decoder_capture(d, q, k, v, seq_len, nullptr, out, stream);
+  });
+}
+
+int lyc_decoder_capture_varlen(lyc_decoder* d, const void* q, const void* k, const void* v,
+                               const int64_t* seq_lens, void* out, void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    if (!seq_lens) fail(LYC_EINVAL, "decode_step: seq_lens is null");
+    return decoder_capture(d, q, k, v, 0, seq_lens, out, stream);
   });
 }
 
@@ -1359,7 +1376,7 @@ int lyc_decoder_replay(lyc_decoder* d, void* stream) {
   return (int)guarded([&]() -> int64_t {
     if (!d || !d->exec) fail(LYC_ESTATE, "decoder: no captured step");
     cuda_check(cudaGraphLaunch(d->exec, (cudaStream_t)stream), "graph launch");
-    g_launches += lyc_decoder_launches_per_step(d, d->planned_seq);
+    g_launches += d->captured_launches;
     return LYC_OK;
   });
 }

@@ -167,9 +167,18 @@ class HybridDecoder:
 
     def capture(self, q, k_cache, v_cache, seq_len: int, out, *, stream=None):
         """Capture one step into a CUDA graph (fixed pointers and seq_len)."""
-        check(lib().lyc_decoder_capture(self._h, q.data_ptr(), k_cache.data_ptr(),
-                                        v_cache.data_ptr(), seq_len, out.data_ptr(),
-                                        self._stream(stream)))
+        if isinstance(seq_len, (int, np.integer)):
+            check(lib().lyc_decoder_capture(self._h, q.data_ptr(), k_cache.data_ptr(),
+                                            v_cache.data_ptr(), seq_len, out.data_ptr(),
+                                            self._stream(stream)))
+        else:
+            lens = [int(x) for x in seq_len]
+            if len(lens) != self.batch:
+                raise ValueError("capture: one seq_len per batch item")
+            arr = (C.c_int64 * len(lens))(*lens)
+            check(lib().lyc_decoder_capture_varlen(self._h, q.data_ptr(), k_cache.data_ptr(),
+                                                   v_cache.data_ptr(), arr, out.data_ptr(),
+                                                   self._stream(stream)))
         self.captured = (q, k_cache, v_cache, seq_len, out)
 
     def replay(self, *, stream=None):

@@ -190,3 +190,28 @@ def test_varlen_fused_equals_per_item_decoders(select, k):
         for g in range(H):
             assert np.array_equal(sets[b][g], s1[g]), (b, g)
         assert rel_err(out[:, b].float().cpu().numpy(), o1[:, 0].float().cpu().numpy()) < 1e-2
+
+
+def test_varlen_graph_capture_replay():
+    """lyc_decoder_capture_varlen: a replay of the captured ragged step equals
+    the eager step bitwise (fused kernel, bf16)."""
+    import paper_2602_04541_b200 as P
+    NL, B, H, G, d, cap = 3, 3, 8, 4, 128, 4096
+    lens = [4096, 1500, 2900]
+    roles = roles_for(NL, H, [(1, 3), (2, 5)])
+    q, K, V = synth(17, NL, B, H, G, d, cap, torch.bfloat16)
+    qd, Kd, Vd = q.cuda(), K.cuda(), V.cuda()
+    dec = P.HybridDecoder(n_layers=NL, batch=B, n_kv_heads=H, group_size=G, d_head=d, seq_cap=cap,
+                          roles=roles, policy=P.SparsityPolicy.top_k(512), dtype=torch.bfloat16)
+    eager = dec.decode_step(qd, Kd, Vd, lens).clone()
+    sets = dec.token_sets()
+    out = torch.zeros_like(qd)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        dec.capture(qd, Kd, Vd, lens, out, stream=st)
+        dec.replay(stream=st)
+        dec.replay(stream=st)
+    st.synchronize()
+    assert torch.equal(out, eager)
+    s2 = dec.token_sets()
+    assert all(np.array_equal(a, b) for ra, rb in zip(sets, s2) for a, b in zip(ra, rb))
