@@ -152,97 +152,119 @@ def peaks():
 
 
 # ----------------------------------------------------------------------- CPU
-def cpu_sample(wl, roles, K_host=None, V_host=None, q_host=None, reps=1, want_out=False):
-    """Time the reference CPU operator on one layer of the dominant role
-    pattern and extrapolate to a whole decode step by block count.
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-    Returns (us_per_step, info dict)."""
-    from oracle import pyoracle
-    lib = pyoracle.ref()
-    kind = "reference"
-    if lib is None:
-        lib, kind = pyoracle.orc(), "port"
-    NL, H, G, d, L, k, B = (wl[x] for x in ("NL", "H", "G", "d", "L", "k", "B"))
-    bs = 64
-    nb = (L + bs - 1) // bs
-    nblk = min((k + bs - 1) // bs, nb)
-    rng = np.random.default_rng(7)
-    if K_host is None:
-        K_host = rng.uniform(-1, 1, (H, L, d)).astype(np.float32)
-        V_host = rng.uniform(-1, 1, (H, L, d)).astype(np.float32)
-        q_host = rng.uniform(-1, 1, (H * G, d)).astype(np.float32)
-    # sample: one retrieval head (all blocks) + H-1 sparse heads (top-k blocks)
-    blocks = [np.arange(nb)] + [np.sort(rng.choice(nb, nblk, replace=False)) for _ in range(H - 1)]
-    sample_blocks = nb + (H - 1) * nblk
-    total_blocks = B * sum(nb if roles[l, g] == 0 else nblk for l in range(NL) for g in range(H))
-    cores = os.cpu_count() or 1
-    splits = 16 * H
-    if kind == "reference":
-        best, _ = lib.kernel_run_time(K_host, V_host, q_host, blocks, batch=1, group=G, seq_len=L,
-                                      scale=1 / np.sqrt(d), num_splits=splits, n_workers=cores,
-                                      reps=reps)
-    else:
-        cores = 1
-        t0 = time.perf_counter()
-        lib.kernel_run(K_host, V_host, q_host, blocks, batch=1, group=G, seq_len=L,
-                       scale=1 / np.sqrt(d), num_splits=splits, dtype=np.float32)
-        best = time.perf_counter() - t0
-    us = best * 1e6 * total_blocks / sample_blocks
-    # selection pass of one retrieval head (decode_engine.hpp:129-132): pooled
-    # query (gqa_pool_queries), dense_attention weights, select_tokens TopK --
-    # the reference runs it serially per retrieval (layer, head); scaled by the
-    # step's retrieval slot count
-    n_ret = B * int(sum(1 for l in range(NL) for g in range(H) if roles[l, g] == 0))
-    t_sel = 0.0
-    if kind == "reference":
-        pooled = lib.gqa_pool_queries(q_host[:G], G)[0]
-        Kd, Vd = K_host[0].astype(np.float64), V_host[0].astype(np.float64)
-        t0 = time.perf_counter()
-        _, w = lib.dense_attention(pooled, Kd, Vd, 1 / np.sqrt(d))
-        lib.select_tokens("topk", w, k=min(k, L))
-        t_sel = time.perf_counter() - t0
-        us += t_sel * 1e6 * n_ret
-    info = {"kind": kind, "cores": cores,
-            "sample": (f"hh::kernel::run<float> one layer: 1 retrieval head ({nb} blocks) + "
-                       f"{H - 1} sparse heads ({nblk} blocks), L={L}, d={d}, G={G}, "
-                       f"{splits} splits, {cores} workers; {best * 1e3:.1f} ms, scaled x"
-                       f"{total_blocks / sample_blocks:.2f} by block count to one decode step"
-                       + (f"; plus the selection pass of one retrieval head (gqa_pool_queries + "
-                          f"dense_attention f64 weights + select_tokens TopK, 1 thread, "
-                          f"{t_sel * 1e3:.1f} ms) x {n_ret} retrieval slots" if t_sel else
-                          " (selection pass not included)"))}
-    return us, info
+
+class CpuStep:
+    """The reference CPU path for one decode step of the workload, every layer
+    executed (oracle/ref_shim.cpp ref_step_run over the unmodified reference
+    headers): per layer hh::kernel::run<float> (kernel_sim.hpp:237-279) with
+    the reference's own std::thread pool over the layer's block lists
+    (retrieval heads: all ceil(L/64) blocks; sparse heads: a seeded
+    ceil(k/64)-block subset, the same rows as their k-token sets), then the
+    serial f64 selection pass of every retrieval head (gqa_pool_queries +
+    dense_attention weights + select_tokens TopK, decode_engine.hpp:129-132).
+    One layer's K/V (batch item 0) is built once and reused for every layer:
+    the CPU time does not depend on the values.  Batch items are independent,
+    so a batch-B step costs B batch-1 steps (us/token = the batch-1 step)."""
+
+    def __init__(self, wl, roles, K=None, V=None, q=None, seed=7):
+        from oracle import pyoracle
+        self.o = pyoracle.ref()
+        if self.o is None:
+            raise RuntimeError("oracle/_ref (the reference compiled here) is missing")
+        self.kind = "reference"
+        NL, H, G, d, L, k = (wl[x] for x in ("NL", "H", "G", "d", "L", "k"))
+        self.wl, self.roles = wl, roles
+        rng = np.random.default_rng(seed)
+        if K is None:
+            K = rng.uniform(-1, 1, (H, L, d)).astype(np.float32)
+            V = rng.uniform(-1, 1, (H, L, d)).astype(np.float32)
+            q = rng.uniform(-1, 1, (H * G, d)).astype(np.float32)
+        self.ctx = self.o.step_context(K, V, q, group=G, scale=1 / np.sqrt(d))
+        nb = (L + 63) // 64
+        self.nb, self.nblk = nb, min((k + 63) // 64, nb)
+        self.blocks = [[np.arange(nb) if (l == 0 or roles[l, g] == 0)
+                        else np.sort(rng.choice(nb, self.nblk, replace=False)) for g in range(H)]
+                       for l in range(NL)]
+        self.cores = os.cpu_count() or 1
+        self.splits = 16 * H
+
+    def step(self, workers=None):
+        """-> (seconds, attention seconds, selection seconds) of one step."""
+        return self.ctx.run(self.roles, self.blocks, num_splits=self.splits,
+                            n_workers=workers or self.cores, top_k=min(self.wl["k"], self.wl["L"]))
+
+    def thread_scaling(self):
+        """kernel::run time of one hybrid layer (1 retrieval + H-1 sparse heads)
+        at 1, 2, 4, ... workers (ms)."""
+        H = self.wl["H"]
+        r = np.ones((1, H), np.uint8)
+        r[0, 0] = 0
+        blk = [[np.arange(self.nb)] + [self.blocks[-1][g] if self.roles[-1, g] else
+                                       np.arange(self.nblk) for g in range(1, H)]]
+        out, w = {}, 1
+        while True:
+            _, ta, _ = self.ctx.run(r, blk, num_splits=self.splits, n_workers=w,
+                                    top_k=min(self.wl["k"], self.wl["L"]))
+            out[str(w)] = round(ta * 1e3, 2)
+            if w >= self.cores:
+                break
+            w = min(2 * w, self.cores)
+        return out
+
+    def sample(self, nsteps, t_step, t_attn, t_sel):
+        wl = self.wl
+        nret = int(sum(1 for l in range(wl["NL"]) for g in range(wl["H"])
+                       if l == 0 or self.roles[l, g] == 0))
+        return (f"{nsteps} whole decode step(s) of the reference CPU path, all {wl['NL']} layers "
+                f"executed: per layer hh::kernel::run<float> over H={wl['H']} heads "
+                f"(retrieval {self.nb} blocks, sparse {self.nblk} blocks), {self.splits} splits, "
+                f"{self.cores} std::thread workers ({t_attn * 1e3:.0f} ms/step); plus the serial f64 "
+                f"selection pass of each of the {nret} retrieval (layer, head) slots "
+                f"({t_sel * 1e3:.0f} ms/step); L={wl['L']}, d={wl['d']}, G={wl['G']}, batch 1 "
+                f"(a batch-{wl['B']} step = {wl['B']} independent batch-1 steps)")
+
+    def close(self):
+        self.ctx.close()
 
 
 def run_reference_arm(args, wl, roles, rank, world):
     if rank != 0:
         return
-    # warm-up + timed samples of the reference CPU path on the same workload
-    from oracle import pyoracle  # noqa: F401
-    rng = np.random.default_rng(7)
-    H, L, d, G = wl["H"], wl["L"], wl["d"], wl["G"]
-    K = rng.uniform(-1, 1, (H, L, d)).astype(np.float32)
-    V = rng.uniform(-1, 1, (H, L, d)).astype(np.float32)
-    q = rng.uniform(-1, 1, (H * G, d)).astype(np.float32)
+    cs = CpuStep(wl, roles)
     for _ in range(args.warmup):
-        cpu_sample(wl, roles, K, V, q)
-    vals = []
+        cs.step()
+    vals, ta, tsel = [], [], []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        us, info = cpu_sample(wl, roles, K, V, q)
-        vals.append(us)
+        sec, a, sl = cs.step()
+        vals.append(sec)
+        ta.append(a)
+        tsel.append(sl)
     wall = time.perf_counter() - t0
-    v = float(np.mean(vals))
+    v = float(np.mean(vals)) * 1e6  # us per step of one batch item = us/token
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "us/token",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": v / 1e3, "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic U(-1,1)",
+        "ms_per_step": v / 1e3 * wl["B"], "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (selection f64)", "data": "synthetic U(-1,1)",
         "config": config_of(args, wl),
-        "cpu_baseline": {"value": v, "unit": "us/token", **info},
+        "cpu_baseline": {"value": v, "unit": "us/token", "kind": cs.kind, "cores": cs.cores,
+                         "cpu_model": cpu_model(),
+                         "sample": cs.sample(args.steps, np.mean(vals), np.mean(ta), np.mean(tsel)),
+                         "thread_scaling_layer_ms": cs.thread_scaling()},
         "e2e": {"value": v, "unit": "us/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "wall_s": wall,
+        "timed_s": float(np.sum(vals)), "wall_s": wall,
     }
+    cs.close()
     print(json.dumps(line), flush=True)
 
 
@@ -330,7 +352,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="llama3-8b-128k", choices=list(WORKLOADS))
+    ap.add_argument("--workload", default="qwen3-8b-128k", choices=list(WORKLOADS))
     ap.add_argument("--select", default="tokens", choices=["tokens", "blocks"])
     ap.add_argument("--retrieval-frac", type=float, default=0.125)
     ap.add_argument("--top-k", type=int, default=0, help="override the workload's top-k budget")
@@ -514,18 +536,22 @@ def main():
     h2d = in_h.numel() * esz
     d2h = out_h.numel() * esz
 
-    # ---- CPU baseline (rank 0, N == 1): the reference operator on the host
+    # ---- CPU baseline (rank 0, N == 1): the reference CPU path, whole steps
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            nb_ = min(L, 131072)
-            Kh = K[0, 0, :, :nb_].float().cpu().numpy()
-            Vh = V[0, 0, :, :nb_].float().cpu().numpy()
+            Kh = K[0, 0].float().cpu().numpy()
+            Vh = V[0, 0].float().cpu().numpy()
             qh = q[0, 0].float().cpu().numpy()
-            wl_c = dict(wl, L=nb_)
-            us, info = cpu_sample(wl_c, roles, Kh, Vh, qh)
-            us *= L / nb_ if nb_ < L else 1.0
-            cpu = {"value": us, "unit": "us/token", **info}
+            cs = CpuStep(wl, roles, Kh, Vh, qh)
+            cs.step()  # warm-up
+            n_cpu = 2
+            res = [cs.step() for _ in range(n_cpu)]
+            us = float(np.mean([r[0] for r in res])) * 1e6
+            cpu = {"value": us, "unit": "us/token", "kind": cs.kind, "cores": cs.cores,
+                   "cpu_model": cpu_model(),
+                   "sample": cs.sample(n_cpu, *np.mean(np.array(res), axis=0))}
+            cs.close()
         except Exception as e:  # the baseline must not kill the bench line
             cpu = {"value": None, "unit": "us/token", "error": repr(e)[:200]}
 

@@ -198,6 +198,15 @@ int lyc_decoder_is_fused(lyc_decoder* dec);
  * 0-2, selection done.  lyc_decoder_trace copies [n_layers][8][n_ctas]
  * stamps into out (cap entries) and returns the count (out = NULL: size query). */
 int lyc_decoder_set_trace(lyc_decoder* dec, int enable);
+/* Set trace (fused mode, a debugging / parity aid): when enabled, every step
+ * also records each layer's emitted index sets -- the StepTrace of
+ * decode_engine.hpp:26-32, 144-147 -- so per-layer selections of the
+ * whole-step kernel can be checked.  lyc_decoder_traced_sets copies
+ * [n_layers][B*H][k_cap] ids and [n_layers][B*H] counts (-1: no set emitted
+ * at that layer) to host buffers (synchronises) and returns k_cap
+ * (ids = NULL: returns k_cap only). */
+int lyc_decoder_set_trace_sets(lyc_decoder* dec, int enable);
+int64_t lyc_decoder_traced_sets(lyc_decoder* dec, int32_t* ids, int32_t* counts, int64_t cap);
 int64_t lyc_decoder_trace(lyc_decoder* dec, unsigned long long* out, int64_t cap);
 
 /* ---------------------------------------------------------------------------

@@ -555,8 +555,7 @@ class HybridDecoder {
   // sequences; lyc_decoder_step_varlen).
   void decode_step(const void* q, const void* k, const void* v, const std::vector<std::size_t>& seq_lens,
                    void* out, cudaStream_t st = nullptr) {
-    std::vector<int64_t> l(seq_lens.begin(), seq_lens.end());
-    check(lyc_decoder_step_varlen(d_, q, k, v, l.data(), out, st));
+    check(lyc_decoder_step_varlen(d_, q, k, v, lens_of(seq_lens).data(), out, st));
   }
   // One layer (layers issued in order within a step).
   void decode_layer(int layer, const void* q_l, const void* k, const void* v, std::size_t seq_len,
@@ -567,6 +566,11 @@ class HybridDecoder {
   void capture(const void* q, const void* k, const void* v, std::size_t seq_len, void* out,
                cudaStream_t st) {
     check(lyc_decoder_capture(d_, q, k, v, (int64_t)seq_len, out, st));
+  }
+  // The same for a variable-length batch (one length per batch item).
+  void capture(const void* q, const void* k, const void* v, const std::vector<std::size_t>& seq_lens,
+               void* out, cudaStream_t st) {
+    check(lyc_decoder_capture_varlen(d_, q, k, v, lens_of(seq_lens).data(), out, st));
   }
   void replay(cudaStream_t st) { check(lyc_decoder_replay(d_, st)); }
 
@@ -593,6 +597,12 @@ class HybridDecoder {
   lyc_decoder* handle() const { return d_; }
 
  private:
+  std::vector<int64_t> lens_of(const std::vector<std::size_t>& seq_lens) const {
+    if (seq_lens.size() != (std::size_t)cfg_.batch)
+      throw std::invalid_argument("decode_step: one seq_len per batch item");
+    return std::vector<int64_t>(seq_lens.begin(), seq_lens.end());
+  }
+
   Config cfg_;
   lyc_decoder* d_ = nullptr;
 };

@@ -109,7 +109,18 @@ class Oracle:
             fn.restype = C.c_int
             fn.argtypes = [i64, i64, i64, i64, i64, i64, flt, vp, vp, vp, vp, vp, i64, i64, i64,
                            vp, vp]
+        if prefix == "ref":
+            self.lib.ref_step_ctx_create.restype = vp
+            self.lib.ref_step_ctx_create.argtypes = [i64, i64, i64, i64, flt, vp, vp, vp]
+            self.lib.ref_step_ctx_destroy.restype = None
+            self.lib.ref_step_ctx_destroy.argtypes = [vp]
+            self.lib.ref_step_run.restype = C.c_int
+            self.lib.ref_step_run.argtypes = [vp, i64, vp, vp, vp, i64, i64, i64, vp, vp]
         if prefix == "orc":
+            self.lib.orc_decode_layer_f32in.restype = C.c_int
+            self.lib.orc_decode_layer_f32in.argtypes = [
+                i64, i64, i64, i64, i64, dbl, i32, vp, vp, vp, vp, i32, i64, dbl, vp, vp, i64, vp,
+                vp, i32]
             self.lib.orc_block_select_f64.restype = i64
             self.lib.orc_block_select_f64.argtypes = [vp, vp, i64, i64, dbl, i64, i64, vp]
             self.lib.orc_pooled_scores_f64.restype = None
@@ -239,6 +250,10 @@ class Oracle:
                                                 _p(best)))
         return float(best[0]), out
 
+    def step_context(self, K, V, Q, *, group, scale):
+        """ref only: a reusable whole-step timing context (ref_step_run)."""
+        return RefStep(self, K, V, Q, group=group, scale=scale)
+
     # ---- decode_engine.hpp ---------------------------------------------
     def decode_step(self, q, K, V, roles, *, seq, scale, kind="topk", k=1, value=0.0,
                     sets=None, set_cap=None, trace=False):
@@ -271,6 +286,27 @@ class Oracle:
             res["trace"] = [[tr[l, g, : tl[l, g]].copy() for g in range(H)] for l in range(L)]
         return res
 
+    def decode_layer(self, q_l, K_l, V_l, roles_l, state, *, layer0, seq, scale, kind="topk",
+                     k=1, value=0.0, pooled_scores=False, threads=0):
+        """orc only: one layer of decode_engine.hpp:109-151 for one sequence on
+        f32-held inputs (exact upcast to f64; orc_decode_layer_f32in).
+
+        q_l [Hq][d]; K_l, V_l [H][row_stride][d] (f32, rows >= seq ignored);
+        roles_l [H]; state: LayerState (the engine's sets_, carried across
+        layers).  Returns (out [Hq][d] f64, pooled scores [H][seq] or None)."""
+        q_l, K_l, V_l = _f32(q_l), _f32(K_l), _f32(V_l)
+        H, row_stride, d = K_l.shape
+        Hq = q_l.shape[0]
+        roles_l = np.ascontiguousarray(roles_l, dtype=np.uint8)
+        out = np.zeros((Hq, d))
+        ps = np.zeros((H, seq)) if pooled_scores else None
+        th = threads or min(H, os.cpu_count() or 1)
+        _check(self.lib.orc_decode_layer_f32in(H, Hq // H, d, seq, row_stride, scale, int(layer0),
+                                               _p(roles_l), _p(q_l), _p(K_l), _p(V_l), KIND[kind],
+                                               k, value, _p(state.sets), _p(state.len),
+                                               state.cap, _p(out), _p(ps), th))
+        return out, ps
+
     # ---- composition oracles (orc only) --------------------------------
     def block_select(self, pooled_q, Kg, seq, scale, block_size, nblk):
         pooled_q, Kg = _f64(pooled_q), _f64(Kg)
@@ -286,6 +322,67 @@ class Oracle:
         s = np.zeros(seq)
         self.lib.orc_pooled_scores_f64(_p(pooled_q), _p(Kg), seq, pooled_q.shape[0], scale, _p(s))
         return s
+
+
+class LayerState:
+    """The engine's per-KV-head sets_ (decode_engine.hpp:251) for
+    Oracle.decode_layer: sets [H][cap] int64 + lengths [H]."""
+
+    def __init__(self, H, cap):
+        self.cap = int(cap)
+        self.sets = np.zeros((H, max(self.cap, 1)), dtype=np.int64)
+        self.len = np.zeros(H, dtype=np.int64)
+
+    def set(self, g):
+        return self.sets[g, : self.len[g]].copy()
+
+
+class RefStep:
+    """One decode step of the reference CPU path, every layer executed
+    (oracle/ref_shim.cpp ref_step_run): per layer hh::kernel::run<float> over
+    the layer's block lists, then the f64 selection pass of each retrieval
+    head.  K, V: [H][L][d] f32 (one layer's caches, reused for every layer);
+    Q: [H*G][d]."""
+
+    def __init__(self, o: "Oracle", K, V, Q, *, group, scale):
+        self._o = o
+        self.K, self.V, self.Q = _f32(K), _f32(V), _f32(Q)
+        H, L, d = self.K.shape
+        self.H, self.L, self.d = H, L, d
+        self.h = o.lib.ref_step_ctx_create(H, group, d, L, scale, _p(self.K), _p(self.V),
+                                           _p(self.Q))
+
+    def run(self, roles, blocks, *, num_splits, n_workers, top_k):
+        """roles [NL][H]; blocks[l][g] = ascending block ids.  -> (seconds,
+        attention seconds, selection seconds)."""
+        roles = np.ascontiguousarray(roles, dtype=np.uint8)
+        NL = roles.shape[0]
+        off = np.zeros((NL, self.H + 1), dtype=np.int64)
+        flat = []
+        n = 0
+        for l in range(NL):
+            for g in range(self.H):
+                off[l, g] = n
+                flat.append(np.asarray(blocks[l][g], dtype=np.int64))
+                n += len(blocks[l][g])
+            off[l, self.H] = n
+        ids = _i64(np.concatenate(flat) if n else np.zeros(1, dtype=np.int64))
+        sec = np.zeros(1)
+        parts = np.zeros(2)
+        _check(self._o.lib.ref_step_run(self.h, NL, _p(roles), _p(off), _p(ids), num_splits,
+                                        n_workers, top_k, _p(sec), _p(parts)))
+        return float(sec[0]), float(parts[0]), float(parts[1])
+
+    def close(self):
+        if self.h:
+            self._o.lib.ref_step_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 _cache: dict = {}

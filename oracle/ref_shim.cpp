@@ -323,4 +323,89 @@ int ref_decode_step_f64(int64_t n_layers, int64_t n_kv, int64_t group, int64_t d
   });
 }
 
+// ---------------------------------------------------------------------------
+// Timed CPU decode step for bench.py's reference arm (BASELINE metric, whole
+// step, every layer executed).  Per layer, as the reference does it:
+//   * the layer's attention through the reference's own multi-threaded
+//     operator hh::kernel::run<float> (kernel_sim.hpp:237-279): retrieval heads
+//     list every block, sparse heads a ceil(k/64)-block subset -- the
+//     BlockIndexSet form of their k-token sets (same rows touched);
+//   * the selection pass of every retrieval head (decode_engine.hpp:129-132):
+//     gqa_pool_queries, dense_attention<double> weights over the head's seq
+//     rows, select_tokens(TopK) -- serial f64, as DecodeEngine runs it.
+// One Workload (K/V of H heads, batch 1) is built once and reused for every
+// layer (CPU time does not depend on the values); only the block lists
+// change per layer.  The f64 selection pass reuses one head's upcast K/V.
+struct RefStepCtx {
+  hh::kernel::Workload<float> w;
+  std::vector<double> k64, v64;
+  int64_t H = 0, G = 0, d = 0, L = 0;
+  float scale = 1.f;
+};
+
+void* ref_step_ctx_create(int64_t n_kv, int64_t group, int64_t d, int64_t seq, float scale,
+                          const float* K, const float* V, const float* Q) {
+  auto* c = new RefStepCtx();
+  const int64_t off0 = 0;
+  std::vector<int64_t> off(n_kv + 1, 0);
+  c->w = make_workload<float>(1, n_kv, group, d, seq, 64, scale, K, V, Q, off.data(), &off0);
+  c->H = n_kv;
+  c->G = group;
+  c->d = d;
+  c->L = seq;
+  c->scale = scale;
+  c->k64.assign(K, K + seq * d);
+  c->v64.assign(V, V + seq * d);
+  return c;
+}
+
+void ref_step_ctx_destroy(void* ctx) { delete static_cast<RefStepCtx*>(ctx); }
+
+// roles [n_layers][H] (0 = Retrieval); blocks: per layer per head CSR
+// (blk_off [n_layers][H + 1] offsets into blk_ids).  Returns seconds of the
+// step in *seconds and the attention / selection parts in parts[2].
+int ref_step_run(void* ctx, int64_t n_layers, const uint8_t* roles, const int64_t* blk_off,
+                 const int64_t* blk_ids, int64_t num_splits, int64_t n_workers, int64_t top_k,
+                 double* seconds, double* parts) {
+  return (int)guard([&]() -> int64_t {
+    auto* c = static_cast<RefStepCtx*>(ctx);
+    const auto clk = [] { return std::chrono::steady_clock::now(); };
+    double t_attn = 0, t_sel = 0;
+    const auto t0 = clk();
+    for (int64_t l = 0; l < n_layers; ++l) {
+      const int64_t* off = blk_off + l * (c->H + 1);
+      for (int64_t g = 0; g < c->H; ++g) {
+        auto& ids = c->w.blocks.ids[g];
+        ids.clear();
+        for (int64_t i = off[g]; i < off[g + 1]; ++i) ids.push_back((std::uint32_t)blk_ids[i]);
+      }
+      const auto ta = clk();
+      auto res = hh::kernel::run(c->w, num_splits, n_workers < 1 ? 1 : n_workers);
+      const auto tb = clk();
+      t_attn += std::chrono::duration<double>(tb - ta).count();
+      std::vector<std::vector<double>> qh(c->H * c->G);
+      std::optional<std::vector<std::vector<double>>> pooled;
+      for (int64_t g = 0; g < c->H; ++g) {
+        if (!(l == 0 || roles[l * c->H + g] == 0)) continue;
+        if (!pooled) {
+          for (int64_t h = 0; h < c->H * c->G; ++h)
+            qh[h].assign(c->w.queries[h].begin(), c->w.queries[h].end());
+          pooled = hh::gqa_pool_queries(qh, c->G);
+        }
+        hh::MatView<double> kv(c->k64.data(), c->L, c->d), vv(c->v64.data(), c->L, c->d);
+        hh::AttnInput<double> sel{(*pooled)[g], kv, vv, (double)c->scale};
+        auto set = hh::select_tokens(hh::SparsityPolicy::top_k(top_k),
+                                     hh::dense_attention(sel).weights, c->L);
+        if (set.empty()) throw std::logic_error("empty selection");
+      }
+      t_sel += std::chrono::duration<double>(clk() - tb).count();
+      if (res.outputs.empty()) throw std::logic_error("no outputs");
+    }
+    *seconds = std::chrono::duration<double>(clk() - t0).count();
+    parts[0] = t_attn;
+    parts[1] = t_sel;
+    return 0;
+  });
+}
+
 }  // extern "C"

@@ -6,13 +6,9 @@ shared object is missing the import fails loudly with the build command.
 from __future__ import annotations
 
 import ctypes as C
-import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "liblyc.so"
-# A/B measurement of an alternative in-tree build (debug scripts only)
-if os.environ.get("LYC_LIB_VARIANT"):
-    LIB_PATH = LIB_PATH.with_name("liblyc_" + os.environ["LYC_LIB_VARIANT"] + ".so")
 
 LYC_OK, LYC_EINVAL, LYC_ESTATE, LYC_ECUDA, LYC_ENOTSUP, LYC_ENCCL = 0, -1, -2, -3, -4, -5
 DTYPE_F32, DTYPE_BF16 = 0, 1
@@ -29,6 +25,7 @@ SYMBOLS = [
     "lyc_decoder_attn_ms", "lyc_decoder_is_fused", "lyc_decoder_set_trace", "lyc_decoder_trace",
     "lyc_shard_layer", "lyc_shard_merge", "lyc_kv_write", "lyc_window_workspace",
     "lyc_window_attention", "lyc_decoder_step_varlen", "lyc_decoder_capture_varlen",
+    "lyc_decoder_set_trace_sets", "lyc_decoder_traced_sets",
 ]
 
 
@@ -139,6 +136,10 @@ def lib() -> C.CDLL:
     L.lyc_decoder_set_trace.argtypes = [vp, C.c_int]
     L.lyc_decoder_trace.restype = i64
     L.lyc_decoder_trace.argtypes = [vp, vp, i64]
+    L.lyc_decoder_set_trace_sets.restype = C.c_int
+    L.lyc_decoder_set_trace_sets.argtypes = [vp, C.c_int]
+    L.lyc_decoder_traced_sets.restype = i64
+    L.lyc_decoder_traced_sets.argtypes = [vp, vp, vp, i64]
     L.lyc_shard_layer.restype = C.c_int
     L.lyc_shard_layer.argtypes = [vp, i32, vp, vp, vp, i64, i64, vp, vp, vp, vp, vp]
     L.lyc_shard_merge.restype = C.c_int

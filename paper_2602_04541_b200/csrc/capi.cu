@@ -522,6 +522,8 @@ struct lyc_decoder {
   int stages = 0;               // attention ring stages in use (0 = all; env LYC_STAGES)
   uint32_t* ctr = nullptr;      // [NL][CTR_PER_LAYER] + 2
   unsigned long long* trace = nullptr;  // optional step timeline [NL][LYC_TRACE_EVENTS][n_ctas]
+  int32_t* set_trace = nullptr;        // optional per-layer sets [NL][B*H][k_cap] (fused path)
+  int32_t* set_trace_count = nullptr;  // [NL][B*H], -1 where no set was emitted
   float* part_o = nullptr;
   float* part_lse = nullptr;
   size_t part_units = 0;
@@ -999,6 +1001,8 @@ void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, i
   p.idx_stride = d->k_cap;
   p.idx_count = d->idx_count;
   p.trace = d->trace;
+  p.set_trace = d->set_trace;
+  p.set_trace_count = d->set_trace_count;
   p.n_layers = d->NL;
   p.max_sel = d->B * d->H;
   p.n_keys = (int32_t)d->n_keys;
@@ -1140,6 +1144,8 @@ int lyc_decoder_destroy(lyc_decoder* d) {
   free_dev(d->sel_rowctr);
   free_dev(d->ctr);
   free_dev(d->trace);
+  free_dev(d->set_trace);
+  free_dev(d->set_trace_count);
   free_dev(d->part_o);
   free_dev(d->part_lse);
   free_dev(d->blob);
@@ -1471,6 +1477,41 @@ int lyc_decoder_set_trace(lyc_decoder* d, int enable) {
       d->trace = nullptr;
     }
     return LYC_OK;
+  });
+}
+
+int lyc_decoder_set_trace_sets(lyc_decoder* d, int enable) {
+  return (int)guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    const size_t rows = (size_t)d->NL * d->B * d->H;
+    if (enable && !d->set_trace) {
+      cuda_check(cudaMalloc(&d->set_trace, rows * d->k_cap * 4), "cudaMalloc set trace");
+      cuda_check(cudaMalloc(&d->set_trace_count, rows * 4), "cudaMalloc set trace");
+      cuda_check(cudaMemset(d->set_trace_count, 0xff, rows * 4), "memset set trace");
+    }
+    if (!enable) {
+      free_dev(d->set_trace);
+      free_dev(d->set_trace_count);
+      d->set_trace = d->set_trace_count = nullptr;
+    }
+    return LYC_OK;
+  });
+}
+
+int64_t lyc_decoder_traced_sets(lyc_decoder* d, int32_t* ids, int32_t* counts, int64_t cap) {
+  return guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    if (!d->set_trace) fail(LYC_ESTATE, "decoder: set tracing is off");
+    const int64_t rows = (int64_t)d->NL * d->B * d->H;
+    if (!ids) return d->k_cap;  // size query: ids hold [rows][k_cap]
+    if (cap < rows * d->k_cap) fail(LYC_EINVAL, "decoder: set trace buffer too small");
+    cuda_check(cudaDeviceSynchronize(), "sync");
+    cuda_check(cudaMemcpy(ids, d->set_trace, (size_t)rows * d->k_cap * 4, cudaMemcpyDeviceToHost),
+               "D2H set trace");
+    if (counts)
+      cuda_check(cudaMemcpy(counts, d->set_trace_count, (size_t)rows * 4, cudaMemcpyDeviceToHost),
+                 "D2H set trace");
+    return d->k_cap;
   });
 }
 

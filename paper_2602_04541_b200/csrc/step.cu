@@ -839,6 +839,7 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
   const uint32_t c = __popc(wv[0]) + __popc(wv[1]) + __popc(wv[2]) + __popc(wv[3]);
   uint32_t tot;
   uint32_t pos = epi_scan(c, es.scan, et, tot) - c + out0;
+  const uint32_t pos0 = pos;
   if (et == 0) stamp(p, l, EV_X0, cta);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -858,6 +859,11 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
     }
   }
   if (q == 0 && et == 0 && p.idx_count) p.idx_count[row] = (int32_t)R.k;
+  if (p.set_trace) {  // debug: this layer's set (the StepTrace of decode_engine.hpp:144-147)
+    int32_t* tr = p.set_trace + ((int64_t)l * p.max_sel + row) * p.idx_stride;
+    for (uint32_t i = pos0; i < pos0 + c; ++i) tr[i] = out[i];
+    if (q == 0 && et == 0) p.set_trace_count[(int64_t)l * p.max_sel + row] = (int32_t)R.k;
+  }
   if (es.last) {
     if (et == 0) R.ctr[4] = 0u;
     if (p.sel_mode == SEL_BLOCK_KEYS)

@@ -227,6 +227,21 @@ class HybridDecoder:
         check(lib().lyc_decoder_trace(self._h, buf.ctypes.data, n))
         return buf.reshape(self.n_layers, 24, -1)
 
+    def set_trace_sets(self, enable: bool = True):
+        """Record every layer's emitted index sets (fused step kernel)."""
+        check(lib().lyc_decoder_set_trace_sets(self._h, int(bool(enable))))
+
+    def traced_sets(self):
+        """(ids [n_layers][B*H][k_cap] int32, counts [n_layers][B*H]; -1 = no
+        set emitted at that layer) of the last traced step."""
+        kcap = check(lib().lyc_decoder_traced_sets(self._h, None, None, 0))
+        rows = self.n_layers * self.batch * self.n_kv_heads
+        ids = np.zeros((rows, kcap), dtype=np.int32)
+        cnt = np.zeros(rows, dtype=np.int32)
+        check(lib().lyc_decoder_traced_sets(self._h, ids.ctypes.data, cnt.ctypes.data, ids.size))
+        H = self.batch * self.n_kv_heads
+        return ids.reshape(self.n_layers, H, kcap), cnt.reshape(self.n_layers, H)
+
     def set_timing(self, enable: bool = True):
         """CUDA events around every attention-kernel launch (graph-capturable)."""
         check(lib().lyc_decoder_set_timing(self._h, int(bool(enable))))

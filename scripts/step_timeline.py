@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--workload", default="llama3-8b-128k")
     ap.add_argument("--select", default="tokens")
     ap.add_argument("--layers", type=int, default=0)
+    ap.add_argument("--save", default="")
     a = ap.parse_args()
     wl = dict(bench.WORKLOADS[a.workload])
     if a.layers:
@@ -47,6 +48,8 @@ def main():
     out = dec.decode_step(q, K, V, L)
     torch.cuda.synchronize()
     tr = dec.trace().astype(np.int64)
+    if a.save:
+        np.save(a.save, tr)
     t0 = tr[0, 0].min()
     rel = (tr - t0) / 1e3
     # selection events in chronological order (max over CTAs; NaN = no selection)

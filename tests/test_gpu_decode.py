@@ -130,6 +130,7 @@ def test_llama_like_bf16_token_mode(orc):
             sc = pooled_scores(q[src, 0], K[src, 0, g], G, g, seq)
             swaps += check_set(traces[l][0][g], r["trace"][l][g], sc, 512)
     print("tie-band swaps:", swaps)
+    assert swaps == 0
 
 
 def test_batch_and_ratio_policy(orc):

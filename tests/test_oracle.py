@@ -198,3 +198,35 @@ def test_decode_step_sparse_head_empty_set_is_logic_error(orc):
     K = np.zeros((1, 1, 5, 4))
     out = orc.decode_step(q, K, K, np.zeros((1, 1), dtype=np.uint8), seq=5, scale=1.0, k=2)
     assert out["sets"][0].tolist() == [0, 1]
+
+
+@pytest.mark.parametrize("kind,k,value", [("topk", 100, 0.0), ("ratio", 0, 0.9), ("topp", 0, 0.5)])
+def test_decode_layer_equals_decode_step(orc, kind, k, value):
+    """The layer-at-a-time restatement over f32-held inputs (used by the
+    BASELINE-size GPU parity tests) is bitwise the whole-step restatement
+    (decode_engine.hpp:109-151), per layer outputs and sets, for any thread
+    count."""
+    from oracle import pyoracle
+    rng = np.random.default_rng(5)
+    NL, H, G, d, seq, cap = 4, 3, 2, 32, 700, 768
+    q = rng.uniform(-1, 1, (NL, H * G, d)).astype(np.float32)
+    K = rng.uniform(-1, 1, (NL, H, cap, d)).astype(np.float32)
+    V = rng.uniform(-1, 1, (NL, H, cap, d)).astype(np.float32)
+    roles = np.ones((NL, H), np.uint8)
+    roles[0] = 0
+    roles[2, 1] = 0
+    r = orc.decode_step(q, K, V, roles, seq=seq, scale=0.2, kind=kind, k=k, value=value,
+                        trace=True)
+    for threads in (1, 3):
+        st = pyoracle.LayerState(H, seq)
+        for l in range(NL):
+            out, ps = orc.decode_layer(q[l], K[l], V[l], roles[l], st, layer0=(l == 0), seq=seq,
+                                       scale=0.2, kind=kind, k=k, value=value,
+                                       pooled_scores=True, threads=threads)
+            assert np.array_equal(out, r["out"][l])
+            for g in range(H):
+                assert np.array_equal(st.set(g), r["trace"][l][g])
+                if l == 0 or roles[l, g] == 0:
+                    pooled = q[l, g * G:(g + 1) * G].astype(np.float64).sum(0) / G
+                    np.testing.assert_allclose(ps[g], K[l, g, :seq].astype(np.float64) @ pooled * 0.2,
+                                               rtol=1e-12, atol=1e-12)
