@@ -187,6 +187,45 @@ enum {
 #define LYC_CTR(base, l, e) ((base) + ((size_t)(l) * CTR_PER_LAYER + (e)) * LYC_CTR_STRIDE)
 #define LYC_CTR_WORDS(n_layers) (((size_t)(n_layers) * CTR_PER_LAYER + 2) * LYC_CTR_STRIDE)
 
+// ---------------------------------------------------------------------------
+// Seq-parametric plan of the fused step (plan.cuh): computed on the device by
+// one CTA per layer from the static role map and the step's lengths, so a
+// token-after-token decode never re-plans on the host.
+#define LYC_PLAN_MAX_B 160   // batch items whose lengths travel by value
+#define LYC_PLAN_THREADS 256
+
+struct LycPlanHdr {          // written by the planner, read by the step kernel
+  int32_t seq_len;           // max over the batch
+  int32_t n_keys;            // selection keys per row (seq_len, or blocks)
+  int32_t k_sel;             // ids kept per row at seq_len
+  int32_t status;            // 0 ok; 1 invalid lengths (the step kernel does nothing)
+  int32_t bad_item;          // first batch item with an invalid length
+  int32_t pad[3];
+};
+
+struct LycPlanIn {
+  int32_t NL, B, H, G, D, S;  // layers, batch, KV heads, group, head dim, splits per item
+  int32_t bs;                 // block size (64)
+  int32_t select_mode;        // LYC_SELECT_* (include/lyc.h)
+  int32_t policy_kind;        // LYC_POLICY_TOPK / RATIO
+  int32_t item_keys;          // selection keys per epilogue item (step.cu kItemKeys)
+  int64_t seq_cap, k_cap, top_k;
+  double ratio;
+  const uint8_t* roles;       // device [NL][H], 0 = Retrieval
+  int32_t* idx;               // device index cache (values stored in token / block slots)
+  LycLayerDesc* layers;       // [NL]: per-layer arrays (fixed at create); n_merges / n_sel written
+  LycPlanHdr* hdr;
+  int32_t max_units;          // capacity of each layer's unit arrays
+  int32_t max_merges;
+  // the step's lengths: dlens (device [B], current token included) when set,
+  // else lens[b] (by value) when has_lens, else seq for every item
+  const int64_t* dlens;
+  int64_t seq;
+  int32_t has_lens;
+  int32_t pad_;
+  int32_t lens[LYC_PLAN_MAX_B];
+};
+
 struct LycStepParams {
   CUtensorMap tmap_k;
   CUtensorMap tmap_v;
@@ -213,6 +252,8 @@ struct LycStepParams {
   int64_t idx_stride;
   int32_t* idx_count;        // [B*H]
   unsigned long long* trace; // optional [n_layers][8 events][n_ctas] %globaltimer stamps
+  int32_t* set_trace;        // optional [n_layers][B*H][idx_stride]: each layer's emitted sets
+  int32_t* set_trace_count;  // optional [n_layers][B*H]
   int32_t n_layers;
   int32_t max_sel;
   int32_t n_keys;            // selection candidates per row (seq_len or n_blocks)
