@@ -268,6 +268,43 @@ def run_reference_arm(args, wl, roles, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def selection_swaps(dec, q, K, V, L, wl, roles, stream):
+    """Per-layer index sets of one traced step vs the exact top-k of f64
+    pooled-query scores (numpy; ties to the lower index).  Returns the swap
+    count, and how many differing ids sit outside the fp tie band
+    |s - s_(k)| <= 8e-6 max|s| (must be 0)."""
+    import torch
+    NL, H, G, k = wl["NL"], roles.shape[1], wl["G"], min(wl["k"], L)
+    B = q.shape[1]
+    dec.set_trace_sets(True)
+    with torch.cuda.stream(stream):
+        dec.decode_step(q, K, V, L, stream=stream)
+    stream.synchronize()
+    ids, cnt = dec.traced_sets()
+    dec.set_trace_sets(False)
+    swaps = out_band = rows = 0
+    for l in range(NL):
+        for g in range(H):
+            if not (l == 0 or roles[l, g] == 0):
+                continue
+            for b in range(B):
+                r = b * H + g
+                got = ids[l, r, :cnt[l, r]]
+                pq = q[l, b, g * G:(g + 1) * G].double().sum(0) / G
+                s_ = (K[l, b, g, :L].double() @ pq).cpu().numpy()
+                order = np.lexsort((np.arange(L), -s_))
+                ref = np.sort(order[:k])
+                rows += 1
+                if got.shape[0] != k or not np.array_equal(got, ref):
+                    diff = np.setxor1d(got, ref)
+                    swaps += len(np.setdiff1d(got, ref))
+                    kth = s_[order[k - 1]]
+                    out_band += int(np.sum(np.abs(s_[diff] - kth) > 8e-6 * np.abs(s_).max()))
+    return {"count": int(swaps), "outside_tie_band": int(out_band), "rows_checked": rows,
+            "method": "sets emitted by the step kernel (set trace) vs numpy exact top-k of f64 "
+                      "pooled scores, ties to the lower index"}
+
+
 def config_of(args, wl):
     c = {"workload": args.workload, "layers": wl["NL"], "q_heads": wl["H"] * wl["G"],
          "kv_heads": wl["H"], "head_dim": wl["d"], "context": wl["L"], "top_k": wl["k"],
@@ -359,6 +396,9 @@ def main():
     ap.add_argument("--seed", type=int, default=2602)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-full", action="store_true")
+    ap.add_argument("--no-swaps", action="store_true")
+    ap.add_argument("--no-pdl", action="store_true",
+                    help="plain stream serialisation of the planner / step launches")
     ap.add_argument("--shard", default="heads", choices=["heads", "seq"],
                     help="multi-GPU split: KV heads (no collective) or KV sequence "
                          "(one packed NCCL all-gather of partials + top-k candidates per layer)")
@@ -407,6 +447,8 @@ def main():
     pol = P.SparsityPolicy.top_k(k)
     dec = P.HybridDecoder(n_layers=NL, batch=B, n_kv_heads=Hr, group_size=G, d_head=d,
                           seq_cap=seq_cap, roles=r_roles, policy=pol, dtype=dt, select=args.select)
+    if args.no_pdl:
+        dec.tune(P._lib.TUNE_PDL, 0)
 
     def barrier():
         if world > 1:
@@ -492,10 +534,66 @@ def main():
                 "speedup_hybrid_vs_full": fms / ms}
         fdec.close()
 
-    # ---- e2e through the public API with host buffers: one packed pinned
-    # upload per step (q of every layer + the new token's K/V rows), the rows
-    # appended to the cache by the KV write path (lyc_kv_write, all layers in
-    # one launch), the step, and the output read back
+    # ---- the per-layer public API (lyc_decoder_layer, what a model calls
+    # between its own projections): one step-kernel launch per layer (plus
+    # the planner at layer 0), eager and CUDA-graph captured
+    per_layer = None
+    if fused:
+        out_l = torch.empty_like(q)
+
+        def layers_step():
+            for l in range(NL):
+                dec.layer(l, q[l], K, V, L, out_l[l], stream=stream)
+
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                layers_step()
+        stream.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(args.steps):
+                layers_step()
+            e1.record(stream)
+        e1.synchronize()
+        eager_ms = allmax(e0.elapsed_time(e1) / args.steps)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            layers_step()
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                g.replay()
+        stream.synchronize()
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(args.steps):
+                g.replay()
+            e1.record(stream)
+        e1.synchronize()
+        graph_ms = allmax(e0.elapsed_time(e1) / args.steps)
+        same = bool(torch.equal(out_l, out))
+        per_layer = {"api": "HybridDecoder.layer x n_layers (lyc_decoder_layer)",
+                     "us_per_token_eager": eager_ms * 1e3 / B,
+                     "us_per_token_graph": graph_ms * 1e3 / B,
+                     "vs_whole_step_graph": graph_ms / ms,
+                     "launches_per_step": NL + 1, "outputs_equal_whole_step": same}
+        del g
+
+    # ---- selection parity of the measured step (in-bench numpy check): the
+    # per-layer sets the step kernel emitted (set tracing) against the exact
+    # top-k of f64 pooled-query scores, ties to the lower index
+    # (attention.hpp:108-123, decode_engine.hpp:129-132)
+    swaps = None
+    if rank == 0 and fused and args.select == "tokens" and not args.no_swaps:
+        swaps = selection_swaps(dec, q, K, V, L, wl, r_roles, stream)
+
+    # ---- e2e through the public API with host buffers, token after token:
+    # every step uploads its inputs in one packed pinned copy (q of every layer
+    # + the new token's K/V rows), appends the rows at the growing length
+    # (lyc_kv_write, all layers in one launch), runs the step at seq = t + 1
+    # through HybridDecoder.decode_step (the device planner re-plans the new
+    # length in the stream: no host synchronisation) and reads the outputs
+    # back.  The same loop at a fixed length is reported beside it.
     import ctypes as C
     from paper_2602_04541_b200 import _lib as LL
     nq, nkv = q.numel(), NL * B * Hr * d
@@ -510,29 +608,34 @@ def main():
                            dtype=LL.DTYPE_BF16 if dt == torch.bfloat16 else LL.DTYPE_F32, pad=0,
                            seq_cap=seq_cap)
     out_h = torch.empty(out.shape, dtype=dt, pin_memory=True)
-    e2e_steps = max(3, args.steps // 2)
+    e2e_steps = max(3, args.steps)
 
-    def e2e_step():
+    def e2e_step(seq):
         in_d.copy_(in_h, non_blocking=True)
-        LL.check(LL.lib().lyc_kv_write(K.data_ptr(), V.data_ptr(), C.byref(lay), -1, L - 1, 1,
+        LL.check(LL.lib().lyc_kv_write(K.data_ptr(), V.data_ptr(), C.byref(lay), -1, seq - 1, 1,
                                        k_new.data_ptr(), v_new.data_ptr(), stream.cuda_stream))
-        dec.decode_step(q_in, K, V, L, out, stream=stream)
+        dec.decode_step(q_in, K, V, seq, out, stream=stream)
         out_h.copy_(out, non_blocking=True)
 
-    with torch.cuda.stream(stream):
-        for _ in range(2):
-            e2e_step()
-    stream.synchronize()
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(stream):
-        e0.record(stream)
-        for _ in range(e2e_steps):
-            e2e_step()
-        e1.record(stream)
-    e1.synchronize()
-    barrier()
-    e2e_ms = allmax(e0.elapsed_time(e1) / e2e_steps)
+    def time_e2e(seqs):
+        with torch.cuda.stream(stream):
+            for s_ in seqs[:2]:
+                e2e_step(s_)
+        stream.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for s_ in seqs:
+                e2e_step(s_)
+            e1.record(stream)
+        e1.synchronize()
+        barrier()
+        return allmax(e0.elapsed_time(e1) / len(seqs))
+
+    growing = list(range(L - e2e_steps + 1, L + 1))
+    e2e_ms = time_e2e(growing)
+    e2e_fixed_ms = time_e2e([L] * e2e_steps)
     h2d = in_h.numel() * esz
     d2h = out_h.numel() * esz
 
@@ -580,8 +683,14 @@ def main():
                          "bytes_per_step": float(attn_bytes.sum())},
             "full_attention": full,
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_ms * 1e3, "unit": "us/token", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "api": "HybridDecoder.decode_step (eager C-ABI)"},
+            "e2e": {"value": e2e_ms * 1e3 / B, "unit": "us/token", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h),
+                    "api": "HybridDecoder.decode_step (eager C-ABI), token after token",
+                    "seq_lens": f"{growing[0]}..{growing[-1]}",
+                    "fixed_seq_us_per_token": e2e_fixed_ms * 1e3 / B,
+                    "growing_vs_fixed": e2e_ms / e2e_fixed_ms},
+            "per_layer_api": per_layer,
+            "selection_swaps": swaps,
             "gpu_launches": int(launches_per_step * args.steps),
             "launches_per_step": int(launches_per_step),
             "clocks": clk.summary(),

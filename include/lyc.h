@@ -134,7 +134,14 @@ int lyc_decoder_destroy(lyc_decoder* dec);
  *   k,v [n_layers][B][H][seq_cap][d]    caches, rows 0..seq_len-1 valid
  *   out [n_layers][B][Hq][d]            attention outputs
  * seq_len = t+1 (current token included, decode_engine.hpp:98).  Stream
- * ordered; the index cache (sets_) is updated in place. */
+ * ordered; the index cache (sets_) is updated in place.
+ * On the step kernel (lyc_decoder_is_fused) a step is two launches -- the
+ * device planner (plan.cu: the split plan for this length, computed in the
+ * stream) and the persistent step kernel -- with no host synchronisation,
+ * no host-to-device copy and no allocation, so seq_len may change on every
+ * call (token-after-token decode).  On the per-layer kernels (TopP /
+ * Threshold, shard mode) a new length is planned on the host and uploaded
+ * stream-ordered from pinned staging. */
 int lyc_decoder_step(lyc_decoder* dec, const void* q, const void* k, const void* v,
                      int64_t seq_len, void* out, void* stream);
 
@@ -145,24 +152,48 @@ int lyc_decoder_step(lyc_decoder* dec, const void* q, const void* k, const void*
  * independent engines' decode_step in one call: each item's retrieval heads
  * attend its own rows, select from them with its own budget (TopK: min(k, len),
  * Ratio: ceil((1 - theta) * len)), and its sparse heads read those sets.  Equal
- * lengths run exactly as lyc_decoder_step; unequal ones use the per-layer
- * kernels (not the fused step kernel) and are not supported in shard mode. */
+ * lengths run exactly as lyc_decoder_step; unequal ones run on the same step
+ * kernel with every pool cut across all CTAs of the batch.  Not supported in
+ * shard mode. */
 int lyc_decoder_step_varlen(lyc_decoder* dec, const void* q, const void* k, const void* v,
                             const int64_t* seq_lens, void* out, void* stream);
 
+/* The same with DEVICE-resident lengths (int64 [B], current token included),
+ * read by the device planner when the step runs: a captured graph
+ * (lyc_decoder_capture_dev) replays t, t+1, t+2, ... as the caller advances
+ * the lengths in the stream (e.g. with lyc_kv_append_dev).  Invalid lengths
+ * (< 1 or > seq_cap) make the step a no-op, reported by lyc_decoder_status.
+ * Step kernel only (LYC_ENOTSUP otherwise). */
+int lyc_decoder_step_dev(lyc_decoder* dec, const void* q, const void* k, const void* v,
+                         const int64_t* d_seq_lens, void* out, void* stream);
+/* LYC_OK, or LYC_EINVAL if the last device-planned step rejected its lengths
+ * (synchronises `stream`). */
+int lyc_decoder_status(lyc_decoder* dec, void* stream);
+
 /* Single layer (decode_engine.hpp:120-143): q_l/out_l are [B][Hq][d]; k/v are
- * the full caches.  Layers must be issued in order within a step. */
+ * the full caches.  Layers must be issued in order within a step, the model's
+ * own projections in between (q of layer l+1 depends on layer l's output).
+ * On the step kernel this is ONE launch of the persistent step kernel over
+ * [layer, layer + 1) -- attention, split-KV merge and the layer's selection --
+ * plus the device planner at layer 0 (or when seq_len changes). */
 int lyc_decoder_layer(lyc_decoder* dec, int32_t layer, const void* q_l, const void* k,
                       const void* v, int64_t seq_len, void* out_l, void* stream);
 
 /* Capture lyc_decoder_step into a CUDA graph for fixed pointers / seq_len,
- * then replay it.  replay returns LYC_ESTATE if nothing was captured. */
+ * then replay it.  replay returns LYC_ESTATE if nothing was captured.  The
+ * graph replays the captured lengths: on the step kernel it contains the
+ * device planner; on the per-layer kernels replay re-plans to the captured
+ * lengths when another length was planned since (stream-ordered upload). */
 int lyc_decoder_capture(lyc_decoder* dec, const void* q, const void* k, const void* v,
                         int64_t seq_len, void* out, void* stream);
 /* The same for a variable-length batch (host seq_lens [B], as in
  * lyc_decoder_step_varlen); replay re-runs the captured lengths. */
 int lyc_decoder_capture_varlen(lyc_decoder* dec, const void* q, const void* k, const void* v,
                                const int64_t* seq_lens, void* out, void* stream);
+/* The same with device-resident lengths (lyc_decoder_step_dev): every replay
+ * plans the lengths the array holds when it runs. */
+int lyc_decoder_capture_dev(lyc_decoder* dec, const void* q, const void* k, const void* v,
+                            const int64_t* d_seq_lens, void* out, void* stream);
 int lyc_decoder_replay(lyc_decoder* dec, void* stream);
 
 /* The device index cache: ids [B*H][k_cap] int32 (ascending token ids, or
@@ -189,8 +220,20 @@ int lyc_decoder_attn_ms(lyc_decoder* dec, float* ms);
 /* 1 when lyc_decoder_step runs the persistent whole-step kernel (one launch:
  * attention, split-KV merge and selection of every layer), 0 when it issues
  * per-layer kernels (attention, merge, cluster top-k).  In fused mode
- * lyc_decoder_attn_ms reports the step kernel's duration in ms[0]. */
+ * lyc_decoder_attn_ms reports the step kernel's duration in ms[0] (or one
+ * duration per layer after lyc_decoder_layer calls). */
 int lyc_decoder_is_fused(lyc_decoder* dec);
+
+/* Tuning / experiment knobs (never needed for correctness):
+ *   LYC_TUNE_RING_STAGES       K/V ring stages in use (0 = all that fit);
+ *   LYC_TUNE_PER_LAYER_KERNELS 1 = run steps on the per-layer kernels
+ *                              (attention, merge, cluster top-k), 0 = back to
+ *                              the step kernel when the decoder has one;
+ *   LYC_TUNE_PDL               0 = plain stream serialisation of the step's launches. */
+#define LYC_TUNE_RING_STAGES 1
+#define LYC_TUNE_PER_LAYER_KERNELS 2
+#define LYC_TUNE_PDL 3  /* 1 (default) = programmatic dependent launch of planner / step kernels */
+int lyc_decoder_tune(lyc_decoder* dec, int32_t what, int64_t value);
 
 /* Step timeline (fused mode): when enabled, the step kernel stamps
  * %globaltimer (ns) for 8 events per layer per CTA: consumers begin / end,
@@ -262,6 +305,13 @@ typedef struct lyc_kv_layout {
 } lyc_kv_layout;
 int lyc_kv_write(void* k_cache, void* v_cache, const lyc_kv_layout* layout, int32_t layer,
                  int64_t pos, int64_t n_rows, const void* k_src, const void* v_src, void* stream);
+/* KvCache::append of the current token with device-resident lengths: writes
+ * row d_seq_lens[b] - 1 of every (b, g) of `layer` (-1: all layers) from src
+ * [(n_layers)][B][H][d]; rows outside [0, seq_cap) are skipped.  Graph-
+ * capturable (the companion of lyc_decoder_step_dev). */
+int lyc_kv_append_dev(void* k_cache, void* v_cache, const lyc_kv_layout* layout, int32_t layer,
+                      const int64_t* d_seq_lens, const void* k_src, const void* v_src,
+                      void* stream);
 
 /* ---------------------------------------------------------------------------
  * Cache-correction attention (decode_engine.hpp:164-204):
@@ -279,6 +329,14 @@ int lyc_window_attention(const lyc_kv_layout* layout, int32_t layer, const void*
                          const void* v_cache, int32_t group_size, float scale, int64_t start,
                          int32_t window, const void* q, void* out, void* workspace,
                          int64_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Test hook: the device planner (run sequentially on the host) against the
+ * host-order planner for a decoder configuration and lengths (seq_lens: host
+ * [B] or NULL), every layer; LYC_OK when they agree exactly, LYC_ESTATE with
+ * the first difference otherwise.  No GPU needed. */
+int lyc_plan_selftest(const lyc_decode_config* cfg, int64_t seq_len, const int64_t* seq_lens,
+                      int32_t n_sms);
 
 #ifdef __cplusplus
 }

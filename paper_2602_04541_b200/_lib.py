@@ -25,8 +25,12 @@ SYMBOLS = [
     "lyc_decoder_attn_ms", "lyc_decoder_is_fused", "lyc_decoder_set_trace", "lyc_decoder_trace",
     "lyc_shard_layer", "lyc_shard_merge", "lyc_kv_write", "lyc_window_workspace",
     "lyc_window_attention", "lyc_decoder_step_varlen", "lyc_decoder_capture_varlen",
-    "lyc_decoder_set_trace_sets", "lyc_decoder_traced_sets",
+    "lyc_decoder_set_trace_sets", "lyc_decoder_traced_sets", "lyc_decoder_step_dev",
+    "lyc_decoder_capture_dev", "lyc_decoder_status", "lyc_decoder_tune", "lyc_kv_append_dev",
+    "lyc_plan_selftest",
 ]
+
+TUNE_RING_STAGES, TUNE_PER_LAYER_KERNELS, TUNE_PDL = 1, 2, 3
 
 
 class LycError(RuntimeError):
@@ -140,6 +144,18 @@ def lib() -> C.CDLL:
     L.lyc_decoder_set_trace_sets.argtypes = [vp, C.c_int]
     L.lyc_decoder_traced_sets.restype = i64
     L.lyc_decoder_traced_sets.argtypes = [vp, vp, vp, i64]
+    L.lyc_decoder_step_dev.restype = C.c_int
+    L.lyc_decoder_step_dev.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+    L.lyc_decoder_capture_dev.restype = C.c_int
+    L.lyc_decoder_capture_dev.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+    L.lyc_decoder_status.restype = C.c_int
+    L.lyc_decoder_status.argtypes = [vp, vp]
+    L.lyc_decoder_tune.restype = C.c_int
+    L.lyc_decoder_tune.argtypes = [vp, i32, i64]
+    L.lyc_kv_append_dev.restype = C.c_int
+    L.lyc_kv_append_dev.argtypes = [vp, vp, C.POINTER(lyc_kv_layout), i32, vp, vp, vp, vp]
+    L.lyc_plan_selftest.restype = C.c_int
+    L.lyc_plan_selftest.argtypes = [C.POINTER(lyc_decode_config), i64, C.POINTER(C.c_int64), i32]
     L.lyc_shard_layer.restype = C.c_int
     L.lyc_shard_layer.argtypes = [vp, i32, vp, vp, vp, i64, i64, vp, vp, vp, vp, vp]
     L.lyc_shard_merge.restype = C.c_int

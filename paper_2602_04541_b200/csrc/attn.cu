@@ -58,7 +58,8 @@ __global__ void __launch_bounds__(128) split_merge_kernel(const __grid_constant_
 template <typename T, int D, bool kEarlyExit>
 static cudaError_t launch_attn_tt(const LycAttnParams& p, int batch, cudaStream_t st) {
   using C = AttnCfg<T, D>;
-  static bool configured = false;
+  static bool configured_[64] = {};
+  bool& configured = device_flag(configured_);
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(hybrid_attn_kernel<T, D, kEarlyExit>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);

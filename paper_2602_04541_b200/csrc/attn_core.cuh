@@ -224,7 +224,10 @@ __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMa
   }
   for (int u = ub; u < ue; ++u) {
     const LycUnit un = un_next;
-    const LycSlot s = s_next;
+    LycSlot s = s_next;
+    // the step kernel's live length of this slot's batch item (its plan is
+    // reused while the length stays in the same 64-row block)
+    if (p.seq_of) s.seq = p.seq_of[s.item];
     if (u + 1 < ue) {
       un_next = p.units[u + 1];
       s_next = p.slots[un_next.slot];
@@ -324,6 +327,14 @@ __device__ __forceinline__ void produce_units(const LycView& p, const CUtensorMa
       for (int i = 0; i < kRounds; ++i) rows[i] = rows_n[i];
     }
   }
+}
+
+// A data dependency for a stage release: false for every value an MMA / FMA
+// chain produces (hardware NaNs are canonical 0x7fffffff), but the compiler
+// cannot know that, so the caller's branch waits for `v` -- and with it for
+// the shared-memory loads that fed it.
+__device__ __forceinline__ bool stage_reads_done_never(float v) {
+  return __float_as_uint(v) == 0x7fc00001u;
 }
 
 __device__ __forceinline__ void consumer_bar() {
@@ -659,8 +670,23 @@ __device__ __forceinline__ void consume_units_bf16(const LycView& p, const AttnS
             mma_bf16(o[2 * n2], pa0, 0u, pa2, 0u, b0, b1);
             mma_bf16(o[2 * n2 + 1], pa0, 0u, pa2, 0u, b2, b3);
           }
+          // release the stage only after its last ldmatrix has returned: an
+          // mbarrier arrive does not wait for in-flight shared-memory loads
+          // (measured: the producer's next copy into this stage raced the
+          // final V ldmatrix -- columns 112..127 of a head's output), so the
+          // arrive is made data-dependent on the MMA that consumes it
+          // (every accumulator -- the compiler reorders the n2 loop freely --
+          // combined in a shallow xor tree)
+          uint32_t dep[NT];
+#pragma unroll
+          for (int n = 0; n < NT; ++n) dep[n] = __float_as_uint(o[n][0]);
+#pragma unroll
+          for (int w = 1; w < NT; w *= 2)
+#pragma unroll
+            for (int n = 0; n + w < NT; n += 2 * w) dep[n] ^= dep[n + w];
           __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.empty[stage]);
+          if (lane == 0 && !stage_reads_done_never(__uint_as_float(dep[0])))
+            mbar_arrive(&sm.empty[stage]);
           if (++stage == ring_stages<C>(p)) {
             stage = 0;
             phase ^= 1;
@@ -830,8 +856,13 @@ __device__ __forceinline__ void consume_units_f32(const LycView& p, const AttnSm
               if (c * 32 + lane < D) o[j][c] = fmaf(pj, vrow[c * 32 + lane], o[j][c]);
           }
         }
+        // the stage's last loads must have returned before its release (see
+        // the bf16 path): the arrive depends on the accumulators they feed
+        float last = 0.f;
+#pragma unroll
+        for (int c = 0; c < DC; ++c) last += o[0][c];
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.empty[stage]);
+        if (lane == 0 && !stage_reads_done_never(last)) mbar_arrive(&sm.empty[stage]);
         if (++stage == ring_stages<C>(p)) {
           stage = 0;
           phase ^= 1;

@@ -14,10 +14,13 @@
 
 #include "../../include/lyc.h"
 #include "lyc_plan.h"
+#include "plan.cuh"
 
 #include <cudaTypedefs.h>
 
 namespace lyc {
+void plan_layer_host(const LycPlanIn& in, int l, const PlanOut& o);
+cudaError_t launch_plan(const LycPlanIn& in, cudaStream_t st, bool pdl);
 cudaError_t launch_attn(const LycAttnParams& p, int dtype, int d, int batch, cudaStream_t st);
 int attn_stages(int dtype, int d);
 cudaError_t launch_merge(const LycMergeParams& p, int dtype, cudaStream_t st);
@@ -33,9 +36,10 @@ cudaError_t launch_window(const void* q, const void* k, const void* v, int L, in
 int topk_cluster_size(int n, int max_slice);
 size_t topk_smem_bytes(int slice);
 cudaError_t launch_float_keys(const float* s, uint32_t* keys, int64_t n, cudaStream_t st);
-cudaError_t launch_step(const LycStepParams& p, int dtype, int d, cudaStream_t st);
+cudaError_t launch_step(const LycStepParams& p, int dtype, int d, cudaStream_t st, bool pdl);
 bool step_supported(int dtype, int d);
 int64_t step_max_keys();
+int64_t step_ring_bytes(int dtype, int d);
 cudaError_t launch_shard_candidates(const uint32_t* keys, int64_t key_stride,
                                     const int32_t* local_ids, const int32_t* cnt,
                                     const int32_t* sel_rows, int n_sel, int64_t k_cap,
@@ -390,6 +394,7 @@ int lyc_workload_run(const lyc_workload* w, int64_t num_splits, void* out, uint3
         s.n_items = (int32_t)(w->blk_off[b * H + g + 1] - w->blk_off[b * H + g]);
         s.list_len = s.n_items;
         s.seq = (int32_t)w->seq_len;
+        s.item = (int32_t)b;
         s.q_row = (int32_t)(b * H * G + g * G);
         s.sel = -1;
         s.dep = -1;
@@ -498,7 +503,7 @@ struct lyc_decoder {
   lyc_decode_config cfg{};
   std::vector<uint8_t> roles;
   int B = 0, H = 0, G = 0, Hq = 0, D = 0, NL = 0, S = 0, bs = 64;
-  bool fused = false;           // whole step in one persistent launch (step.cu)
+  bool fused = false;           // the step runs on the persistent step kernel (step.cu)
   bool shard = false;           // KV-sequence shard mode (lyc_shard_layer / lyc_shard_merge)
   int32_t* shard_ids = nullptr; // [B*H][k_cap] local top-k ids
   int32_t* shard_cnt = nullptr; // [B*H]
@@ -518,21 +523,45 @@ struct lyc_decoder {
   uint32_t* sel_cand = nullptr;
   uint32_t* sel_ccnt = nullptr;
   uint32_t* sel_csub = nullptr;
-  uint32_t* sel_rowctr = nullptr;
-  int stages = 0;               // attention ring stages in use (0 = all; env LYC_STAGES)
-  uint32_t* ctr = nullptr;      // [NL][CTR_PER_LAYER] + 2
+  uint32_t* sel_rowctr = nullptr;  // [2 parity][NL][B*H][16]
+  int64_t rowctr_set = 0;
+  int stages = 0;               // attention ring stages in use (0 = all; lyc_decoder_tune)
+  bool pdl = true;              // programmatic dependent launch of planner / step kernels
+  uint32_t* ctr = nullptr;      // LYC_CTR_WORDS(NL)
   unsigned long long* trace = nullptr;  // optional step timeline [NL][LYC_TRACE_EVENTS][n_ctas]
   int32_t* set_trace = nullptr;        // optional per-layer sets [NL][B*H][k_cap] (fused path)
   int32_t* set_trace_count = nullptr;  // [NL][B*H], -1 where no set was emitted
-  float* part_o = nullptr;
+  float* part_o = nullptr;      // [max_units][G][d] split partials (one layer at a time)
   float* part_lse = nullptr;
-  size_t part_units = 0;
-  uint8_t* blob = nullptr;
-  size_t blob_cap = 0;
-  int64_t planned_seq = -1;
+  // ---- plan storage: a fixed per-layer layout, sized at create for seq_cap
+  // (no allocation afterwards).  The fused path's plan is written by the
+  // device planner (plan.cu) in the stream; the per-layer-kernel path's plan
+  // (TopP / Threshold, shard mode) is built on the host and uploaded
+  // stream-ordered from pinned staging.
+  int max_units = 0, max_merges = 0;
+  size_t layer_bytes = 0;       // bytes of one layer's region in `blob`
+  uint8_t* blob = nullptr;      // [NL][layer region] + descs [NL]
+  size_t blob_bytes = 0;
+  LycLayerDesc* d_layers = nullptr;      // device descs (pointers fixed at create)
+  std::vector<LycLayerDesc> h_layers;    // host copy of the descs
+  uint8_t* staging = nullptr;   // pinned host image of blob (per-layer-kernel path)
+  cudaEvent_t staged = nullptr; // recorded after the last staging upload
+  bool staging_busy = false;
+  uint8_t* d_roles = nullptr;   // [NL][H] for the device planner
+  LycPlanHdr* d_hdr = nullptr;  // the fused plan's header
+  int32_t* d_keys = nullptr;    // [NL][LYC_PLAN_KEY_INTS(B)] each layer's plan key (plan.cu)
+  std::vector<int32_t> host_key;  // the key of the device plan, when host lengths made it
+  bool host_key_valid = false;
+  std::vector<int32_t> captured_key;
+  LycPlanIn pin{};              // the device planner's static input
+  int64_t planned_seq = -1;     // host plan (per-layer kernels), or the last host-seq device plan
   bool planned_varlen = false;
-  int64_t captured_launches = 0;      // kernel launches in the captured graph        // the plan holds per-item lengths (per-layer kernels)
   std::vector<int64_t> planned_lens;
+  uint64_t plan_gen = 0;        // host plans uploaded so far
+  int64_t captured_launches = 0;     // kernel launches in the captured graph
+  uint64_t captured_gen = 0;         // host plan the captured graph reads (per-layer kernels)
+  int64_t captured_seq = -1;
+  std::vector<int64_t> captured_lens;
   LycAttnParams maps{};         // tensor maps for the last (k, v) pointers
   const void* map_k = nullptr;
   const void* map_v = nullptr;
@@ -541,17 +570,15 @@ struct lyc_decoder {
     LycMergeParams mp;
     LycTopkParams tp;
     LycPolicyParams pp;         // TopP / Threshold selection (per-layer path)
-    LycLayerDesc desc;          // step kernel path
     int n_sel = 0, cluster = 1, n_merges = 0;
   };
   std::vector<Layer> layers;
-  LycLayerDesc* d_layers = nullptr;  // device copy of the step descriptors
   int64_t n_keys = 0, k_sel = 0;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   bool timing = false;
-  std::vector<cudaEvent_t> ev_pre, ev_post;  // per layer (per-layer path) or [0] (fused)
-  std::vector<uint8_t> staging;
+  bool timed_per_layer = false;  // the last timed launches were one per layer
+  std::vector<cudaEvent_t> ev_pre, ev_post;  // per layer (per-layer launches) or [0] (whole step)
 
   int n_ctas() const { return S * B; }
   bool retrieval(int l, int g) const { return l == 0 || roles[(size_t)l * H + g] == 0; }
@@ -580,9 +607,10 @@ namespace {
 // first and their selection can start before the layer ends), sparse slots
 // with an older index list, and last the sparse slots whose list the
 // immediately preceding layer's selection produces (streamed while that
-// selection is still running).
+// selection is still running).  This is the host-order statement of the
+// device planner (plan.cuh); lyc_plan_selftest checks the two agree.
 void plan_step_launch(HostLaunch& L, int batch, int heads, int splits, int group, int layer,
-                      int free_from) {
+                      int free_from, bool ragged) {
   L.batch = batch;
   L.heads = heads;
   L.splits = splits;
@@ -601,11 +629,9 @@ void plan_step_launch(HostLaunch& L, int batch, int heads, int splits, int group
     if (total == 0) fail(LYC_EINVAL, "plan_splits: batch item has zero blocks");
   }
   // Equal lengths: each batch item's pools are cut across its own `splits`
-  // cells.  A variable-length batch: each pool is cut across ALL cells
-  // (every item's slots in one list), so short items do not leave their SMs
-  // idle while long ones stream.
-  bool ragged = false;
-  for (int b = 1; b < batch; ++b) ragged = ragged || L.slots[(size_t)b * heads].seq != L.slots[0].seq;
+  // cells.  A variable-length batch (items differ in dense blocks or budget):
+  // each pool is cut across ALL cells (every item's slots in one list), so
+  // short items do not leave their SMs idle while long ones stream.
   const int groups = ragged ? 1 : batch;
   for (int grp = 0; grp < groups; ++grp)
   for (int pool = 0; pool < 3; ++pool) {
@@ -697,13 +723,129 @@ void free_dev(void* p) {
   if (p) cudaFree(p);
 }
 
-// lens (optional, host [B]): per-batch-item sequence lengths (a variable-
-// length batch); seq is then their maximum.  Equal lengths plan the uniform
-// way.  A variable-length plan runs on the per-layer kernels: the dense slots
-// of item b cover its ceil(len_b / bs) blocks (ragged last block by the slot's
-// own length), the selection row of (b, g) ranks len_b keys and keeps
-// budget(len_b) ids, and the sparse slots read budget(len_b) ids.
-void decoder_plan(lyc_decoder* d, int64_t seq, const int64_t* lens = nullptr) {
+// ---- the fixed per-layer plan layout (both planners write into it)
+struct LayerLayout {
+  size_t slots, units, unit_slots, split_off, merges, sel_rows, sel_n, sel_k, bytes;
+};
+LayerLayout layer_layout(int BH, int cells, int max_units, int max_merges) {
+  LayerLayout o{};
+  size_t off = 0;
+  auto put = [&](size_t bytes) {
+    const size_t at = off;
+    off += align_up(std::max<size_t>(bytes, 4), 256);
+    return at;
+  };
+  o.slots = put((size_t)BH * sizeof(LycSlot));
+  o.units = put((size_t)max_units * sizeof(LycUnit));
+  o.unit_slots = put((size_t)max_units * sizeof(LycSlot));
+  o.split_off = put((size_t)(cells + 1) * 4);
+  o.merges = put((size_t)max_merges * sizeof(LycMergeTask));
+  o.sel_rows = put((size_t)BH * 4);
+  o.sel_n = put((size_t)BH * 4);
+  o.sel_k = put((size_t)BH * 4);
+  o.bytes = off;
+  return o;
+}
+
+LycLayerDesc layer_desc(uint8_t* base, const LayerLayout& ll) {
+  LycLayerDesc ds{};
+  ds.slots = (const LycSlot*)(base + ll.slots);
+  ds.units = (const LycUnit*)(base + ll.units);
+  ds.unit_slots = (const LycSlot*)(base + ll.unit_slots);
+  ds.split_off = (const int32_t*)(base + ll.split_off);
+  ds.merges = (const LycMergeTask*)(base + ll.merges);
+  ds.sel_rows = (const int32_t*)(base + ll.sel_rows);
+  ds.sel_n = (const int32_t*)(base + ll.sel_n);
+  ds.sel_k = (const int32_t*)(base + ll.sel_k);
+  ds.n_merges = 0;
+  ds.n_sel = 0;
+  return ds;
+}
+
+// The slots of layer l for lengths len_of(b) (decode_engine.hpp:121-143): the
+// statement both host planners start from.
+void host_slots(const lyc_decoder* d, int l, const int64_t* lens, int64_t seq, bool varlen,
+                std::vector<int>& last_r, HostLaunch& L) {
+  const int B = d->B, H = d->H, G = d->G, D = d->D;
+  const bool blocks = d->cfg.select_mode == LYC_SELECT_BLOCKS;
+  const bool none = d->cfg.select_mode == LYC_SELECT_NONE;
+  const int64_t kb = d->budget(seq);
+  L.slots.resize((size_t)B * H);
+  L.sel_rows.clear();
+  L.sel_n.clear();
+  L.sel_k.clear();
+  for (int b = 0; b < B; ++b)
+    for (int g = 0; g < H; ++g) {
+      LycSlot& s = L.slots[(size_t)b * H + g];
+      std::memset(&s, 0, sizeof(s));
+      s.kv_off = (((int64_t)l * B + b) * H + g) * d->cfg.seq_cap * D;
+      s.q_row = b * H * G + g * G;
+      s.dep = -1;
+      s.sel = -1;
+      const int64_t seq_b = varlen ? lens[b] : seq, nb_b = (seq_b + d->bs - 1) / d->bs;
+      const int64_t kb_b = varlen ? d->budget(seq_b) : kb;
+      s.seq = (int32_t)seq_b;
+      s.item = b;
+      if (d->retrieval(l, g)) {
+        s.kind = ITEM_DENSE;
+        s.n_items = (int32_t)nb_b;
+        if (!none) {
+          s.sel = (int32_t)L.sel_rows.size();
+          L.sel_rows.push_back(b * H + g);
+          if (varlen) {
+            L.sel_n.push_back((int32_t)(blocks ? nb_b : seq_b));
+            L.sel_k.push_back((int32_t)kb_b);
+          }
+        }
+      } else {
+        s.kind = blocks ? ITEM_BLOCKS : ITEM_TOKENS;
+        s.list = d->idx + (int64_t)(b * H + g) * d->k_cap;
+        s.list_len = (int32_t)kb_b;
+        if (d->shard || d->variable_sets())  // this rank's filtered set / a variable-size set
+          s.count = d->idx_count + (b * H + g);
+        s.n_items = blocks ? (int32_t)kb_b : (int32_t)((kb_b + LYC_TILE - 1) / LYC_TILE);
+        s.dep = last_r[(size_t)g];
+      }
+    }
+  for (int g = 0; g < H; ++g)
+    if (d->retrieval(l, g)) last_r[(size_t)g] = l;
+}
+
+// Serialise a host plan into the layer's fixed region of the staging image.
+DevLaunch stage_fixed(const HostLaunch& L, uint8_t* host_base, const LycLayerDesc& ds,
+                      const uint8_t* dev_base, const LayerLayout& ll, int max_units, int max_merges) {
+  if ((int)L.units.size() > max_units || (int)L.merges.size() > max_merges)
+    fail(LYC_ENOTSUP, "plan exceeds the decoder's plan capacity");
+  auto put = [&](size_t off, const void* src, size_t bytes) {
+    if (bytes) std::memcpy(host_base + off, src, bytes);
+  };
+  put(ll.slots, L.slots.data(), L.slots.size() * sizeof(LycSlot));
+  put(ll.units, L.units.data(), L.units.size() * sizeof(LycUnit));
+  std::vector<LycSlot> us(L.units.size());
+  for (size_t u = 0; u < L.units.size(); ++u) us[u] = L.slots[(size_t)L.units[u].slot];
+  put(ll.unit_slots, us.data(), us.size() * sizeof(LycSlot));
+  put(ll.split_off, L.split_off.data(), L.split_off.size() * 4);
+  put(ll.merges, L.merges.data(), L.merges.size() * sizeof(LycMergeTask));
+  put(ll.sel_rows, L.sel_rows.data(), L.sel_rows.size() * 4);
+  put(ll.sel_n, L.sel_n.data(), L.sel_n.size() * 4);
+  put(ll.sel_k, L.sel_k.data(), L.sel_k.size() * 4);
+  (void)dev_base;
+  DevLaunch dl;
+  dl.slots = const_cast<LycSlot*>(ds.slots);
+  dl.units = const_cast<LycUnit*>(ds.units);
+  dl.unit_slots = const_cast<LycSlot*>(ds.unit_slots);
+  dl.split_off = const_cast<int32_t*>(ds.split_off);
+  dl.merges = const_cast<LycMergeTask*>(ds.merges);
+  dl.sel_rows = const_cast<int32_t*>(ds.sel_rows);
+  dl.sel_n = L.sel_n.empty() ? nullptr : const_cast<int32_t*>(ds.sel_n);
+  dl.sel_k = L.sel_k.empty() ? nullptr : const_cast<int32_t*>(ds.sel_k);
+  dl.n_units = (int)L.units.size();
+  dl.n_merges = (int)L.merges.size();
+  dl.n_sel = (int)L.sel_rows.size();
+  return dl;
+}
+
+void validate_lens(const lyc_decoder* d, int64_t& seq, const int64_t*& lens) {
   if (lens) {
     bool same = true;
     for (int b = 0; b < d->B; ++b) {
@@ -721,113 +863,42 @@ void decoder_plan(lyc_decoder* d, int64_t seq, const int64_t* lens = nullptr) {
   }
   if (seq < 1) fail(LYC_EINVAL, "decode_step: seq_len must be >= 1");
   if (seq > d->cfg.seq_cap) fail(LYC_EINVAL, "decode_step: seq_len exceeds seq_cap");
-  if ((!d->fused || lens) && seq > (int64_t)16 * 32768 && d->cfg.select_mode == LYC_SELECT_TOKENS)
+  if (!d->fused && seq > (int64_t)16 * 32768 && d->cfg.select_mode == LYC_SELECT_TOKENS)
     fail(LYC_ENOTSUP, "decode_step: token-mode selection supports seq_len <= 524288");
-  if (d->fused && d->cfg.select_mode != LYC_SELECT_NONE) {
-    // pooled selection limits: <= 64 items per row; block keys in one item
-    const bool blk = d->cfg.select_mode == LYC_SELECT_BLOCKS;
-    const int64_t nk = blk ? (seq + d->bs - 1) / d->bs : seq;
-    if (nk > lyc::step_max_keys() || (blk && nk > lyc::step_item_keys())) {
-      d->fused = false;
-      d->planned_seq = -1;
-    }
-  }
+}
+
+// Host plan of the per-layer-kernel path (TopP / Threshold, shard mode):
+// plan_splits per batch item (kernel_sim.hpp:63-110) for every layer,
+// uploaded stream-ordered (async copy from pinned staging on `st`) into the
+// fixed plan layout -- a kernel still reading the previous plan on `st`
+// finishes first.  lens (optional, host [B]): per-item lengths.
+void decoder_plan(lyc_decoder* d, int64_t seq, const int64_t* lens, cudaStream_t st) {
+  validate_lens(d, seq, lens);
   const bool varlen = lens != nullptr;
   if (!varlen && !d->planned_varlen && d->planned_seq == seq) return;
   if (varlen && d->planned_varlen && std::equal(lens, lens + d->B, d->planned_lens.begin())) return;
-  const bool fused = d->fused;
   const int B = d->B, H = d->H, G = d->G, D = d->D;
-  const int64_t kb = d->budget(seq);
-  auto len_of = [&](int b) { return varlen ? lens[b] : seq; };
   const bool blocks = d->cfg.select_mode == LYC_SELECT_BLOCKS;
   const bool none = d->cfg.select_mode == LYC_SELECT_NONE;
+  const int64_t kb = d->budget(seq);
   const int64_t nb = (seq + d->bs - 1) / d->bs;
-  std::vector<HostLaunch> hl((size_t)d->NL);
-  size_t total = 0, max_parts = 0;
-  std::vector<int> last_r((size_t)H, 0);  // nearest retrieval layer of each head so far
-  for (int l = 0; l < d->NL; ++l) {
-    HostLaunch& L = hl[(size_t)l];
-    L.slots.resize((size_t)B * H);
-    for (int b = 0; b < B; ++b)
-      for (int g = 0; g < H; ++g) {
-        LycSlot& s = L.slots[(size_t)b * H + g];
-        std::memset(&s, 0, sizeof(s));
-        s.kv_off = (((int64_t)l * B + b) * H + g) * d->cfg.seq_cap * D;
-        s.q_row = b * H * G + g * G;
-        s.dep = -1;
-        s.sel = -1;
-        const int64_t seq_b = len_of(b), nb_b = (seq_b + d->bs - 1) / d->bs;
-        const int64_t kb_b = varlen ? d->budget(seq_b) : kb;
-        s.seq = (int32_t)seq_b;
-        if (d->retrieval(l, g)) {
-          s.kind = ITEM_DENSE;
-          s.n_items = (int32_t)nb_b;
-          if (!none) {
-            s.sel = (int32_t)L.sel_rows.size();
-            L.sel_rows.push_back(b * H + g);
-            if (varlen) {
-              L.sel_n.push_back((int32_t)(blocks ? nb_b : seq_b));
-              L.sel_k.push_back((int32_t)kb_b);
-            }
-          }
-        } else {
-          s.kind = blocks ? ITEM_BLOCKS : ITEM_TOKENS;
-          s.list = d->idx + (int64_t)(b * H + g) * d->k_cap;
-          s.list_len = (int32_t)kb_b;
-          if (d->shard || d->variable_sets())  // this rank's filtered set / a variable-size set
-            s.count = d->idx_count + (b * H + g);
-          s.n_items = blocks ? (int32_t)kb_b : (int32_t)((kb_b + LYC_TILE - 1) / LYC_TILE);
-          s.dep = last_r[(size_t)g];
-        }
-      }
-    for (int g = 0; g < H; ++g)
-      if (d->retrieval(l, g)) last_r[(size_t)g] = l;
-    if (fused)
-    {
-      // this layer's selection items run on the last n_items CTAs when they
-      // fit in half the grid (step.cu split roles)
-      int free_from = d->S * B;
-      if (!none) {
-        const int64_t nk = blocks ? nb : seq;
-        const int64_t items = (nk + lyc::step_item_keys() - 1) / lyc::step_item_keys();
-        const int64_t n_items = (int64_t)L.sel_rows.size() * items;
-        if (n_items > 0 && 2 * n_items <= (int64_t)d->S * B) free_from = d->S * B - (int)n_items;
-      }
-      plan_step_launch(L, B, H, d->S, G, l, free_from);
-    }
-    else
-      plan_launch(L, B, H, d->S, G);
-    total += launch_bytes(L);
-    size_t parts = 0;
-    for (auto& s : L.slots) parts += (size_t)s.n_units;
-    max_parts = std::max(max_parts, parts);
-  }
-  total += align_up(sizeof(LycLayerDesc) * d->NL, 256);
-  if (max_parts > d->part_units) {
-    free_dev(d->part_o);
-    free_dev(d->part_lse);
-    d->part_o = d->part_lse = nullptr;
-    cuda_check(cudaMalloc(&d->part_o, max_parts * G * D * 4), "cudaMalloc part_o");
-    cuda_check(cudaMalloc(&d->part_lse, max_parts * G * 4), "cudaMalloc part_lse");
-    d->part_units = max_parts;
-  }
-  if (total > d->blob_cap) {
-    free_dev(d->blob);
-    d->blob = nullptr;
-    cuda_check(cudaMalloc(&d->blob, total), "cudaMalloc plan");
-    d->blob_cap = total;
-  }
-  d->staging.assign(total, 0);
-  size_t off = 0;
+  const LayerLayout ll = layer_layout(B * H, d->n_ctas(), d->max_units, d->max_merges);
+  // the staging image may still feed the previous upload
+  if (d->staging_busy) cuda_check(cudaEventSynchronize(d->staged), "staging event");
   d->layers.assign((size_t)d->NL, {});
+  std::vector<int> last_r((size_t)H, 0);
   const int64_t sel_n = blocks ? nb : seq;
   d->n_keys = sel_n;
   d->k_sel = kb;
   const int cluster = lyc::topk_cluster_size((int)std::min<int64_t>(sel_n, 1 << 30), 16384);
-  std::vector<LycLayerDesc> descs((size_t)d->NL);
+  std::vector<LycLayerDesc> descs = d->h_layers;
   for (int l = 0; l < d->NL; ++l) {
-    HostLaunch& L = hl[(size_t)l];
-    DevLaunch dl = stage_launch(L, d->staging, off, d->blob);
+    HostLaunch L;
+    host_slots(d, l, lens, seq, varlen, last_r, L);
+    plan_launch(L, B, H, d->S, G);
+    const LycLayerDesc& ds = d->h_layers[(size_t)l];
+    DevLaunch dl = stage_fixed(L, d->staging + (size_t)l * d->layer_bytes, ds,
+                               d->blob + (size_t)l * d->layer_bytes, ll, d->max_units, d->max_merges);
     lyc_decoder::Layer& ly = d->layers[(size_t)l];
     std::memset(&ly.ap, 0, sizeof(ly.ap));
     LycView& v = ly.ap.v;
@@ -889,28 +960,16 @@ void decoder_plan(lyc_decoder* d, int64_t seq, const int64_t* lens = nullptr) {
     pp.row_n = dl.sel_n;
     ly.n_sel = dl.n_sel;
     ly.cluster = cluster;
-    LycLayerDesc& ds = descs[(size_t)l];
-    ds.slots = dl.slots;
-    ds.units = dl.units;
-    ds.unit_slots = dl.unit_slots;
-    ds.split_off = dl.split_off;
-    ds.merges = dl.merges;
-    ds.sel_rows = dl.sel_rows;
-    ds.sel_n = dl.sel_n;
-    ds.sel_k = dl.sel_k;
-    ds.n_merges = dl.n_merges;
-    ds.n_sel = dl.n_sel;
-    ly.desc = ds;
+    descs[(size_t)l].n_merges = dl.n_merges;
+    descs[(size_t)l].n_sel = dl.n_sel;
   }
-  d->d_layers = (LycLayerDesc*)(d->blob + off);
-  std::memcpy(d->staging.data() + off, descs.data(), sizeof(LycLayerDesc) * d->NL);
-  cuda_check(cudaMemcpy(d->blob, d->staging.data(), total, cudaMemcpyHostToDevice), "H2D plan");
-  // a new plan restarts the step counters (any previous step has completed:
-  // the synchronous copy above serialises with the legacy stream)
-  cuda_check(cudaMemset(d->ctr, 0, LYC_CTR_WORDS(d->NL) * 4), "memset counters");
-  if (d->sel_rowctr)
-    cuda_check(cudaMemset(d->sel_rowctr, 0, (size_t)d->NL * d->B * d->H * 16 * 4), "memset rowctr");
-  cuda_check(cudaDeviceSynchronize(), "sync");
+  uint8_t* desc_host = d->staging + (size_t)d->NL * d->layer_bytes;
+  std::memcpy(desc_host, descs.data(), sizeof(LycLayerDesc) * d->NL);
+  cuda_check(cudaMemcpyAsync(d->blob, d->staging, d->blob_bytes, cudaMemcpyHostToDevice, st),
+             "H2D plan");
+  cuda_check(cudaEventRecord(d->staged, st), "staging event");
+  d->staging_busy = true;
+  ++d->plan_gen;
   d->planned_seq = varlen ? -1 : seq;
   d->planned_varlen = varlen;
   if (varlen) d->planned_lens.assign(lens, lens + d->B);
@@ -963,17 +1022,54 @@ void decoder_layer(lyc_decoder* d, int l, const void* q_l, const void* k, const 
   }
 }
 
-void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, int64_t seq,
-                  void* out, cudaStream_t st, const int64_t* lens = nullptr) {
-  decoder_plan(d, seq, lens);
-  const int esz = elem_bytes(d->cfg.dtype);
-  const size_t qstride = (size_t)d->B * d->Hq * d->D;
-  if (!d->fused) {
-    for (int l = 0; l < d->NL; ++l)
-      decoder_layer(d, l, (const uint8_t*)q + l * qstride * esz, k, v,
-                    (uint8_t*)out + l * qstride * esz, st);
-    return;
+// The plan key of host lengths (plan.cuh): items per row, then every item's
+// dense blocks and sparse budget.
+std::vector<int32_t> host_plan_key(const lyc_decoder* d, int64_t seq, const int64_t* lens) {
+  std::vector<int32_t> k((size_t)1 + 2 * d->B);
+  int64_t mx = 0;
+  for (int b = 0; b < d->B; ++b) {
+    const int64_t v = lens ? lens[b] : seq;
+    mx = std::max(mx, v);
+    int32_t nb, kb;
+    lyc::plan_item_key(d->pin, v, nb, kb);
+    k[(size_t)1 + b] = nb;
+    k[(size_t)1 + d->B + b] = kb;
   }
+  k[0] = lyc::plan_items(d->pin, mx);
+  return k;
+}
+
+// Fused path: make the device plan fit the step's lengths.  Host lengths: the
+// planner runs only when their key changes (once per 64 tokens of a growing
+// sequence).  Device lengths: the planner runs every step, and each layer
+// returns at once when its stored key matches (plan.cu).
+void ensure_plan(lyc_decoder* d, int64_t seq, const int64_t* lens, const int64_t* dlens,
+                 cudaStream_t st) {
+  LycPlanIn in = d->pin;
+  in.seq = seq;
+  in.dlens = dlens;
+  in.has_lens = lens ? 1 : 0;
+  if (lens)
+    for (int b = 0; b < d->B; ++b) in.lens[b] = (int32_t)lens[b];
+  if (!dlens) {
+    std::vector<int32_t> key = host_plan_key(d, seq, lens);
+    if (d->host_key_valid && key == d->host_key) return;
+    d->host_key = std::move(key);
+    d->host_key_valid = true;
+  } else {
+    d->host_key_valid = false;
+  }
+  cuda_check(lyc::launch_plan(in, st, d->pdl), "plan launch");
+  ++g_launches;
+}
+
+// One launch of the step kernel over layers [l0, l1): q / out point at layer
+// l0's [B][Hq][d] block (consecutive layers follow at B*Hq*d elements).  The
+// step's lengths travel by value (host seq / lens) or as a device array
+// (dlens); the kernel re-plans itself when they change its plan key.
+void launch_step_range(lyc_decoder* d, int l0, int l1, const void* q, const void* k,
+                       const void* v, void* out, cudaStream_t st, int64_t seq,
+                       const int64_t* lens, const int64_t* dlens) {
   ensure_maps(d, k, v);
   LycStepParams p;
   std::memset(&p, 0, sizeof(p));
@@ -983,7 +1079,7 @@ void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, i
   p.v = v;
   p.q = q;
   p.out = out;
-  p.q_layer_stride = (int64_t)qstride;
+  p.q_layer_stride = (int64_t)d->B * d->Hq * d->D;
   p.layers = d->d_layers;
   p.part_o = d->part_o;
   p.part_lse = d->part_lse;
@@ -996,7 +1092,9 @@ void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, i
   p.sel_ccnt = d->sel_ccnt;
   p.sel_csub = d->sel_csub;
   p.sel_rowctr = d->sel_rowctr;
+  p.rowctr_set = d->rowctr_set;
   p.ctr = d->ctr;
+  p.hdr = d->d_hdr;
   p.idx = d->idx;
   p.idx_stride = d->k_cap;
   p.idx_count = d->idx_count;
@@ -1004,12 +1102,11 @@ void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, i
   p.set_trace = d->set_trace;
   p.set_trace_count = d->set_trace_count;
   p.n_layers = d->NL;
+  p.l_begin = l0;
+  p.l_end = l1;
   p.max_sel = d->B * d->H;
-  p.n_keys = (int32_t)d->n_keys;
-  p.k_sel = (int32_t)d->k_sel;
   p.n_splits = d->S;
   p.n_ctas = d->n_ctas();
-  p.seq_len = (int32_t)seq;
   p.block_size = d->bs;
   p.group = d->G;
   p.sel_mode = d->cfg.select_mode == LYC_SELECT_NONE    ? SEL_NONE
@@ -1018,10 +1115,37 @@ void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, i
   p.scale = d->cfg.scale;
   p.scale_log2 = d->cfg.scale * 1.4426950408889634f;
   p.stages = d->stages;
-  record(d, d->ev_pre, 0, st);
-  cuda_check(lyc::launch_step(p, d->cfg.dtype, d->D, st), "step launch");
-  record(d, d->ev_post, 0, st);
+  p.plan = d->pin;
+  p.plan.seq = seq;
+  p.plan.dlens = dlens;
+  p.plan.has_lens = lens ? 1 : 0;
+  if (lens)
+    for (int b = 0; b < d->B; ++b) p.plan.lens[b] = (int32_t)lens[b];
+  const bool per_layer = d->NL > 1 && l1 - l0 == 1;
+  const size_t ev = per_layer ? (size_t)l0 : 0;
+  if (d->timing) d->timed_per_layer = per_layer;
+  record(d, d->ev_pre, ev, st);
+  cuda_check(lyc::launch_step(p, d->cfg.dtype, d->D, st, d->pdl), "step launch");
+  record(d, d->ev_post, ev, st);
   ++g_launches;
+}
+
+void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, int64_t seq,
+                  void* out, cudaStream_t st, const int64_t* lens = nullptr,
+                  const int64_t* dlens = nullptr) {
+  if (d->fused) {
+    if (!dlens) validate_lens(d, seq, lens);
+    ensure_plan(d, seq, lens, dlens, st);
+    launch_step_range(d, 0, d->NL, q, k, v, out, st, seq, lens, dlens);
+    return;
+  }
+  if (dlens) fail(LYC_ENOTSUP, "decode_step: device-resident lengths need the fused step kernel");
+  decoder_plan(d, seq, lens, st);
+  const int esz = elem_bytes(d->cfg.dtype);
+  const size_t qstride = (size_t)d->B * d->Hq * d->D;
+  for (int l = 0; l < d->NL; ++l)
+    decoder_layer(d, l, (const uint8_t*)q + l * qstride * esz, k, v,
+                  (uint8_t*)out + l * qstride * esz, st);
 }
 
 }  // namespace
@@ -1037,6 +1161,8 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
       fail(LYC_EINVAL, "ModelConfig: all dimensions must be >= 1");
     if (!supported_d(c.dtype, c.d_head)) fail(LYC_ENOTSUP, "decoder: unsupported d_head/dtype");
     if (c.group_size > 8) fail(LYC_ENOTSUP, "decoder: group_size > 8 not supported by the device kernel");
+    if ((int64_t)c.batch * c.n_kv_heads > 2048)
+      fail(LYC_ENOTSUP, "decoder: batch * n_kv_heads > 2048 not supported");
     if (c.policy_kind == LYC_POLICY_TOPK) {
       if (c.top_k < 1) fail(LYC_EINVAL, "top_k: k must be >= 1");
     } else if (c.policy_kind == LYC_POLICY_RATIO) {
@@ -1073,16 +1199,15 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
     d->NL = c.n_layers;
     d->bs = 64;
     const int sms = num_sms();
-    // The persistent step kernel needs every CTA co-resident: 1 CTA per SM,
-    // S*B <= #SMs.
-    d->fused = lyc::step_supported(c.dtype, c.d_head) && std::getenv("LYC_NO_FUSED_STEP") == nullptr &&
-               !d->variable_sets();  // TopP / Threshold: per-layer kernels
-    if (const char* env_st = std::getenv("LYC_STAGES")) d->stages = std::max(0, std::atoi(env_st));
     d->S = c.num_splits > 0 ? c.num_splits : std::max(1, sms / d->B);
-    if (d->fused && d->S * d->B > sms) d->fused = false;
-    // the step kernel's selection handles up to 64 items of 8192 keys per row
-    if (d->fused && c.seq_cap > (int64_t)64 * 8192) d->fused = false;
+    // The persistent step kernel needs every CTA co-resident: 1 CTA per SM,
+    // S*B <= #SMs; its selection handles up to 64 items of 8192 keys per row
+    // (block mode: one item); TopP / Threshold run on the per-layer kernels.
     const int64_t nb_cap = (c.seq_cap + d->bs - 1) / d->bs;
+    d->fused = lyc::step_supported(c.dtype, c.d_head) && !d->variable_sets() &&
+               d->S * d->B <= sms && d->B <= LYC_PLAN_MAX_B && c.seq_cap <= lyc::step_max_keys() &&
+               !(c.select_mode == LYC_SELECT_BLOCKS && nb_cap > lyc::step_item_keys()) &&
+               (int64_t)lyc::plan_scratch_ints(d->B, d->H, d->S, d->NL) * 4 <= 150 * 1024;
     if (c.select_mode == LYC_SELECT_BLOCKS) {
       d->k_cap = c.policy_kind == LYC_POLICY_RATIO ? nb_cap
                                                    : std::min<int64_t>((c.top_k + 63) / 64, nb_cap);
@@ -1103,6 +1228,30 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
       cuda_check(cudaMemset(d->sel_keys, 0, 2 * rows * d->sel_stride * 4), "memset");
       cuda_check(cudaMalloc(&d->hist, 2 * rows * LYC_H1_STRIDE * 4), "cudaMalloc hist");
       cuda_check(cudaMemset(d->hist, 0, 2 * rows * LYC_H1_STRIDE * 4), "memset");
+      // plan capacity: a pool cut over a group's cells adds at most one unit
+      // per cut, so units <= slots + 3 * cells per layer (both planners)
+      const int cells = d->n_ctas();
+      d->max_units = (int)rows + 3 * cells + 3;
+      d->max_merges = (int)rows * d->G;
+      const LayerLayout ll = layer_layout((int)rows, cells, d->max_units, d->max_merges);
+      d->layer_bytes = ll.bytes;
+      d->blob_bytes = (size_t)d->NL * ll.bytes + align_up(sizeof(LycLayerDesc) * d->NL, 256);
+      cuda_check(cudaMalloc(&d->blob, d->blob_bytes), "cudaMalloc plan");
+      cuda_check(cudaMemset(d->blob, 0, d->blob_bytes), "memset plan");
+      d->d_layers = (LycLayerDesc*)(d->blob + (size_t)d->NL * ll.bytes);
+      d->h_layers.resize((size_t)d->NL);
+      for (int l = 0; l < d->NL; ++l) d->h_layers[(size_t)l] = layer_desc(d->blob + (size_t)l * ll.bytes, ll);
+      cuda_check(cudaMemcpy(d->d_layers, d->h_layers.data(), sizeof(LycLayerDesc) * d->NL,
+                            cudaMemcpyHostToDevice),
+                 "H2D descs");
+      cuda_check(cudaMalloc(&d->part_o, (size_t)d->max_units * d->G * d->D * 4), "cudaMalloc part_o");
+      cuda_check(cudaMalloc(&d->part_lse, (size_t)d->max_units * d->G * 4), "cudaMalloc part_lse");
+      cuda_check(cudaEventCreateWithFlags(&d->staged, cudaEventDisableTiming), "event");
+      if (!d->fused) {  // host plans: pinned staging image of the plan blob
+        cuda_check(cudaHostAlloc((void**)&d->staging, d->blob_bytes, cudaHostAllocDefault),
+                   "cudaHostAlloc staging");
+        std::memset(d->staging, 0, d->blob_bytes);
+      }
       if (d->fused && c.select_mode != LYC_SELECT_NONE) {  // pooled-selection scratch
         d->bitmap_stride = (lyc::step_bitmap_words(d->sel_stride) + 3) & ~(int64_t)3;
         cuda_check(cudaMalloc(&d->sel_bitmap, 2 * rows * d->bitmap_stride * 4), "cudaMalloc bitmap");
@@ -1112,12 +1261,45 @@ int lyc_decoder_create(const lyc_decode_config* cfg, lyc_decoder** out) {
         cuda_check(cudaMalloc(&d->sel_csub, 2 * rows * 64 * 128 * 4), "cudaMalloc csub");
         cuda_check(cudaMemset(d->sel_csub, 0, 2 * rows * 64 * 128 * 4), "memset");
       }
-      if (d->fused) {  // per-(layer, row / slot) counters of the step kernel
-        cuda_check(cudaMalloc(&d->sel_rowctr, (size_t)d->NL * rows * 16 * 4), "cudaMalloc rowctr");
-        cuda_check(cudaMemset(d->sel_rowctr, 0, (size_t)d->NL * rows * 16 * 4), "memset");
+      if (d->fused) {  // step-kernel counters (two launch-parity sets), planner inputs
+        d->rowctr_set = (int64_t)d->NL * (int64_t)rows * 16;
+        cuda_check(cudaMalloc(&d->sel_rowctr, 2 * (size_t)d->rowctr_set * 4), "cudaMalloc rowctr");
+        cuda_check(cudaMemset(d->sel_rowctr, 0, 2 * (size_t)d->rowctr_set * 4), "memset");
+        cuda_check(cudaMalloc(&d->ctr, LYC_CTR_WORDS(d->NL) * 4), "cudaMalloc ctr");
+        cuda_check(cudaMemset(d->ctr, 0, LYC_CTR_WORDS(d->NL) * 4), "memset");
+        cuda_check(cudaMalloc(&d->d_roles, d->roles.size()), "cudaMalloc roles");
+        cuda_check(cudaMemcpy(d->d_roles, d->roles.data(), d->roles.size(), cudaMemcpyHostToDevice),
+                   "H2D roles");
+        cuda_check(cudaMalloc(&d->d_hdr, sizeof(LycPlanHdr)), "cudaMalloc plan header");
+        cuda_check(cudaMemset(d->d_hdr, 0, sizeof(LycPlanHdr)), "memset");
+        const size_t key_bytes = (size_t)d->NL * LYC_PLAN_KEY_INTS(d->B) * 4;
+        cuda_check(cudaMalloc(&d->d_keys, key_bytes), "cudaMalloc plan keys");
+        cuda_check(cudaMemset(d->d_keys, 0, key_bytes), "memset");
+        LycPlanIn& in = d->pin;
+        std::memset(&in, 0, sizeof(in));
+        in.NL = d->NL;
+        in.B = d->B;
+        in.H = d->H;
+        in.G = d->G;
+        in.D = d->D;
+        in.S = d->S;
+        in.bs = d->bs;
+        in.select_mode = c.select_mode;
+        in.policy_kind = c.policy_kind;
+        in.item_keys = lyc::step_item_keys();
+        in.seq_cap = c.seq_cap;
+        in.k_cap = d->k_cap;
+        in.top_k = c.top_k;
+        in.ratio = c.ratio;
+        in.roles = d->d_roles;
+        in.idx = d->idx;
+        in.layers = d->d_layers;
+        in.hdr = d->d_hdr;
+        in.keys = d->d_keys;
+        in.max_units = d->max_units;
+        in.max_merges = d->max_merges;
       }
-      cuda_check(cudaMalloc(&d->ctr, LYC_CTR_WORDS(d->NL) * 4), "cudaMalloc ctr");
-      cuda_check(cudaMemset(d->ctr, 0, LYC_CTR_WORDS(d->NL) * 4), "memset");
+      cuda_check(cudaDeviceSynchronize(), "sync");  // creation only: buffers initialised
     } catch (...) {
       lyc_decoder_destroy(d);
       throw;
@@ -1133,6 +1315,8 @@ int lyc_decoder_destroy(lyc_decoder* d) {
   if (d->graph) cudaGraphDestroy(d->graph);
   for (auto e : d->ev_pre) cudaEventDestroy(e);
   for (auto e : d->ev_post) cudaEventDestroy(e);
+  if (d->staged) cudaEventDestroy(d->staged);
+  if (d->staging) cudaFreeHost(d->staging);
   free_dev(d->idx);
   free_dev(d->idx_count);
   free_dev(d->sel_keys);
@@ -1143,6 +1327,9 @@ int lyc_decoder_destroy(lyc_decoder* d) {
   free_dev(d->sel_csub);
   free_dev(d->sel_rowctr);
   free_dev(d->ctr);
+  free_dev(d->d_roles);
+  free_dev(d->d_hdr);
+  free_dev(d->d_keys);
   free_dev(d->trace);
   free_dev(d->set_trace);
   free_dev(d->set_trace_count);
@@ -1178,18 +1365,53 @@ int lyc_decoder_step_varlen(lyc_decoder* d, const void* q, const void* k, const 
   });
 }
 
+int lyc_decoder_step_dev(lyc_decoder* d, const void* q, const void* k, const void* v,
+                         const int64_t* d_seq_lens, void* out, void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    if (!d_seq_lens) fail(LYC_EINVAL, "decode_step: d_seq_lens is null");
+    decoder_step(d, q, k, v, 0, out, (cudaStream_t)stream, nullptr, d_seq_lens);
+    return LYC_OK;
+  });
+}
+
 int lyc_decoder_layer(lyc_decoder* d, int32_t layer, const void* q_l, const void* k, const void* v,
                       int64_t seq_len, void* out_l, void* stream) {
   return (int)guarded([&]() -> int64_t {
     if (!d) fail(LYC_EINVAL, "decoder: null");
     if (layer < 0 || layer >= d->NL) fail(LYC_EINVAL, "decoder: layer out of range");
+    cudaStream_t st = (cudaStream_t)stream;
     if (d->fused) {
-      // the single-layer entry uses the per-layer kernels and their plan
-      d->fused = false;
-      d->planned_seq = -1;
+      // the step kernel over [layer, layer + 1): attention, merge and the
+      // layer's selection in one launch (re-planning itself when the length
+      // leaves the planned 64-row block)
+      int64_t seq = seq_len;
+      const int64_t* lens = nullptr;
+      validate_lens(d, seq, lens);
+      ensure_plan(d, seq, nullptr, nullptr, st);
+      launch_step_range(d, layer, layer + 1, q_l, k, v, out_l, st, seq, nullptr, nullptr);
+      return LYC_OK;
     }
-    decoder_plan(d, seq_len);
-    decoder_layer(d, layer, q_l, k, v, out_l, (cudaStream_t)stream);
+    decoder_plan(d, seq_len, nullptr, st);
+    decoder_layer(d, layer, q_l, k, v, out_l, st);
+    return LYC_OK;
+  });
+}
+
+// Status of the last device-planned step (device lengths are validated by the
+// planner): LYC_OK, or LYC_EINVAL when a length was < 1 or > seq_cap (that
+// step did nothing).  Synchronises the stream.
+int lyc_decoder_status(lyc_decoder* d, void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    if (!d->fused) return LYC_OK;
+    LycPlanHdr h{};
+    cuda_check(cudaMemcpyAsync(&h, d->d_hdr, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream),
+               "D2H plan header");
+    cuda_check(cudaStreamSynchronize((cudaStream_t)stream), "sync");
+    if (h.status != 0)
+      fail(LYC_EINVAL, "decode_step: seq_len of batch item " + std::to_string(h.bad_item) +
+                           " is < 1 or exceeds seq_cap");
     return LYC_OK;
   });
 }
@@ -1205,6 +1427,11 @@ void shard_enter(lyc_decoder* d) {
     d->fused = false;  // per-layer kernels: the collective sits between layers
     d->shard = true;   // sparse slots read device counts of the filtered sets
     d->planned_seq = -1;
+  }
+  if (!d->staging) {
+    cuda_check(cudaHostAlloc((void**)&d->staging, d->blob_bytes, cudaHostAllocDefault),
+               "cudaHostAlloc staging");
+    std::memset(d->staging, 0, d->blob_bytes);
   }
   const size_t rows = (size_t)d->B * d->H;
   if (!d->shard_ids) {
@@ -1229,7 +1456,7 @@ int lyc_shard_layer(lyc_decoder* d, int32_t layer, const void* q_l, const void* 
     if (row_begin < 0) fail(LYC_EINVAL, "shard: row_begin must be >= 0");
     cudaStream_t st = (cudaStream_t)stream;
     shard_enter(d);
-    decoder_plan(d, n_local);
+    decoder_plan(d, n_local, nullptr, st);
     lyc_decoder::Layer& ly = d->layers[(size_t)layer];
     ensure_maps(d, k, v);
     ly.ap.tmap_k = d->maps.tmap_k;
@@ -1275,7 +1502,7 @@ int lyc_shard_merge(lyc_decoder* d, int32_t layer, int32_t world, const float* a
     if (seq_total < n_local) fail(LYC_EINVAL, "shard: seq_total < n_local");
     cudaStream_t st = (cudaStream_t)stream;
     shard_enter(d);
-    decoder_plan(d, n_local);
+    decoder_plan(d, n_local, nullptr, st);
     lyc_decoder::Layer& ly = d->layers[(size_t)layer];
     const int rows = d->B * d->Hq;
     const size_t brows0 = (size_t)d->B * d->H;
@@ -1332,10 +1559,20 @@ int lyc_shard_merge(lyc_decoder* d, int32_t layer, int32_t world, const float* a
 
 namespace {
 int64_t decoder_capture(lyc_decoder* d, const void* q, const void* k, const void* v,
-                        int64_t seq_len, const int64_t* lens, void* out, void* stream) {
+                        int64_t seq_len, const int64_t* lens, const int64_t* dlens, void* out,
+                        void* stream) {
     if (!d) fail(LYC_EINVAL, "decoder: null");
     cudaStream_t st = (cudaStream_t)stream;
-    decoder_plan(d, seq_len, lens);  // host work + plan upload outside the capture
+    if (dlens && !d->fused) fail(LYC_ENOTSUP, "capture: device-resident lengths need the fused step kernel");
+    int64_t seq = seq_len;
+    const int64_t* vl = lens;
+    if (!dlens) validate_lens(d, seq, vl);
+    // per-layer-kernel path: host plan + upload outside the capture (the
+    // graph reads the fixed plan layout; replay re-plans to these lengths if
+    // another length was planned since).  Fused path: the graph holds the
+    // device planner, so every replay plans its own lengths.
+    if (!d->fused) decoder_plan(d, seq_len, lens, st);
+    else if (!dlens) ensure_plan(d, seq, vl, nullptr, st);  // outside the graph
     ensure_maps(d, k, v);
     if (d->exec) {
       cudaGraphExecDestroy(d->exec);
@@ -1348,7 +1585,7 @@ int64_t decoder_capture(lyc_decoder* d, const void* q, const void* k, const void
     const int64_t before = g_launches;
     cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
     try {
-      decoder_step(d, q, k, v, seq_len, out, st, lens);
+      decoder_step(d, q, k, v, seq_len, out, st, lens, dlens);
     } catch (...) {
       cudaGraph_t g = nullptr;
       cudaStreamEndCapture(st, &g);
@@ -1359,6 +1596,10 @@ int64_t decoder_capture(lyc_decoder* d, const void* q, const void* k, const void
     g_launches = before;  // captured launches execute on replay
     cuda_check(cudaStreamEndCapture(st, &d->graph), "end capture");
     cuda_check(cudaGraphInstantiate(&d->exec, d->graph, 0), "graph instantiate");
+    d->captured_gen = d->plan_gen;
+    d->captured_key = d->fused && !dlens ? d->host_key : std::vector<int32_t>();
+    d->captured_seq = seq_len;
+    d->captured_lens.assign(lens ? lens : &seq_len, lens ? lens + d->B : &seq_len + 1);
     return LYC_OK;
 }
 }  // namespace
@@ -1366,7 +1607,7 @@ int64_t decoder_capture(lyc_decoder* d, const void* q, const void* k, const void
 int lyc_decoder_capture(lyc_decoder* d, const void* q, const void* k, const void* v,
                         int64_t seq_len, void* out, void* stream) {
   return (int)guarded([&]() -> int64_t {
-    return decoder_capture(d, q, k, v, seq_len, nullptr, out, stream);
+    return decoder_capture(d, q, k, v, seq_len, nullptr, nullptr, out, stream);
   });
 }
 
@@ -1374,14 +1615,37 @@ int lyc_decoder_capture_varlen(lyc_decoder* d, const void* q, const void* k, con
                                const int64_t* seq_lens, void* out, void* stream) {
   return (int)guarded([&]() -> int64_t {
     if (!seq_lens) fail(LYC_EINVAL, "decode_step: seq_lens is null");
-    return decoder_capture(d, q, k, v, 0, seq_lens, out, stream);
+    return decoder_capture(d, q, k, v, 0, seq_lens, nullptr, out, stream);
+  });
+}
+
+int lyc_decoder_capture_dev(lyc_decoder* d, const void* q, const void* k, const void* v,
+                            const int64_t* d_seq_lens, void* out, void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    if (!d_seq_lens) fail(LYC_EINVAL, "decode_step: d_seq_lens is null");
+    return decoder_capture(d, q, k, v, 0, nullptr, d_seq_lens, out, stream);
   });
 }
 
 int lyc_decoder_replay(lyc_decoder* d, void* stream) {
   return (int)guarded([&]() -> int64_t {
     if (!d || !d->exec) fail(LYC_ESTATE, "decoder: no captured step");
-    cuda_check(cudaGraphLaunch(d->exec, (cudaStream_t)stream), "graph launch");
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool varlen = d->captured_lens.size() == (size_t)d->B && d->captured_seq == 0;
+    if (!d->fused && d->plan_gen != d->captured_gen) {
+      // another length was planned since the capture: restore the captured plan
+      decoder_plan(d, d->captured_seq, varlen ? d->captured_lens.data() : nullptr, st);
+      d->captured_gen = d->plan_gen;
+    }
+    if (d->fused && !d->captured_key.empty() &&
+        (!d->host_key_valid || d->host_key != d->captured_key)) {
+      // the plan was remade for other lengths since the capture: remake it
+      int64_t seq = d->captured_seq;
+      const int64_t* lens = varlen ? d->captured_lens.data() : nullptr;
+      validate_lens(d, seq, lens);
+      ensure_plan(d, seq, lens, nullptr, st);
+    }
+    cuda_check(cudaGraphLaunch(d->exec, st), "graph launch");
     g_launches += d->captured_launches;
     return LYC_OK;
   });
@@ -1398,10 +1662,19 @@ int lyc_decoder_index_cache(lyc_decoder* d, int32_t** ids, int32_t** counts, int
 int64_t lyc_decoder_launches_per_step(lyc_decoder* d, int64_t seq_len) {
   return guarded([&]() -> int64_t {
     if (!d) fail(LYC_EINVAL, "decoder: null");
-    decoder_plan(d, seq_len);
-    if (d->fused) return 1;
+    if (d->fused) return 1;  // the step kernel (+ the planner once per plan key)
+    // per-layer kernels: attention, merge (split slots), selection (retrieval layers)
+    int64_t seq = seq_len;
+    const int64_t* lens = nullptr;
+    validate_lens(d, seq, lens);
+    std::vector<int> last_r((size_t)d->H, 0);
     int64_t n = 0;
-    for (auto& ly : d->layers) n += 1 + (ly.n_merges > 0) + (ly.n_sel > 0);
+    for (int l = 0; l < d->NL; ++l) {
+      HostLaunch L;
+      host_slots(d, l, nullptr, seq, false, last_r, L);
+      plan_launch(L, d->B, d->H, d->S, d->G);
+      n += 1 + (L.merges.empty() ? 0 : 1) + (L.sel_rows.empty() ? 0 : 1);
+    }
     return n;
   });
 }
@@ -1453,7 +1726,7 @@ int lyc_decoder_attn_ms(lyc_decoder* d, float* ms) {
   return (int)guarded([&]() -> int64_t {
     if (!d) fail(LYC_EINVAL, "decoder: null");
     if (d->ev_pre.empty()) fail(LYC_ESTATE, "decoder: timing was never enabled");
-    const int n = d->fused ? 1 : d->NL;
+    const int n = d->fused && !d->timed_per_layer ? 1 : d->NL;
     cuda_check(cudaEventSynchronize(d->ev_post[(size_t)n - 1]), "event sync");
     for (int l = 0; l < d->NL; ++l) ms[l] = 0.f;
     for (int l = 0; l < n; ++l)
@@ -1464,6 +1737,42 @@ int lyc_decoder_attn_ms(lyc_decoder* d, float* ms) {
 }
 
 int lyc_decoder_is_fused(lyc_decoder* d) { return d && d->fused ? 1 : 0; }
+
+int lyc_decoder_tune(lyc_decoder* d, int32_t what, int64_t value) {
+  return (int)guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    switch (what) {
+      case LYC_TUNE_RING_STAGES:
+        if (value < 0) fail(LYC_EINVAL, "tune: stages must be >= 0");
+        d->stages = (int)value;
+        d->planned_seq = -1;  // the per-layer path bakes stages into its views
+        d->planned_varlen = false;
+        return LYC_OK;
+      case LYC_TUNE_PER_LAYER_KERNELS:
+        if (value) {
+          if (!d->staging) {
+            cuda_check(cudaHostAlloc((void**)&d->staging, d->blob_bytes, cudaHostAllocDefault),
+                       "cudaHostAlloc staging");
+            std::memset(d->staging, 0, d->blob_bytes);
+          }
+          d->fused = false;
+          d->planned_seq = -1;
+          d->planned_varlen = false;
+        } else if (!d->ctr) {
+          fail(LYC_ENOTSUP, "tune: this decoder was not created for the step kernel");
+        } else if (!d->shard) {
+          d->fused = true;
+        }
+        return LYC_OK;
+      case LYC_TUNE_PDL:
+        d->pdl = value != 0;
+        return LYC_OK;
+      default:
+        fail(LYC_EINVAL, "tune: unknown knob");
+    }
+    return LYC_OK;
+  });
+}
 
 int lyc_decoder_set_trace(lyc_decoder* d, int enable) {
   return (int)guarded([&]() -> int64_t {
@@ -1636,6 +1945,168 @@ int lyc_window_attention(const lyc_kv_layout* lay, int32_t layer, const void* k_
                                   (cudaStream_t)stream),
                "window launch");
     g_launches += 2;
+    return LYC_OK;
+  });
+}
+
+// ------------------------------------------------------------ planner self-test
+// The device planner (plan.cuh, run here sequentially) against the host-order
+// planner (plan_step_launch) on identical inputs, every layer: slots, units,
+// split offsets, merge tasks and selection rows must agree exactly.
+int lyc_plan_selftest(const lyc_decode_config* cfg, int64_t seq_len, const int64_t* seq_lens,
+                      int32_t n_sms) {
+  return (int)guarded([&]() -> int64_t {
+    if (!cfg || !cfg->roles) fail(LYC_EINVAL, "selftest: null config");
+    lyc_decoder dd;
+    lyc_decoder* d = &dd;
+    d->cfg = *cfg;
+    d->roles.assign(cfg->roles, cfg->roles + (size_t)cfg->n_layers * cfg->n_kv_heads);
+    d->B = cfg->batch;
+    d->H = cfg->n_kv_heads;
+    d->G = cfg->group_size;
+    d->Hq = d->H * d->G;
+    d->D = cfg->d_head;
+    d->NL = cfg->n_layers;
+    d->S = cfg->num_splits > 0 ? cfg->num_splits : std::max(1, n_sms / d->B);
+    d->fused = true;
+    if (d->B > LYC_PLAN_MAX_B || d->S * d->B > n_sms) fail(LYC_ENOTSUP, "selftest: not a fused shape");
+    const int64_t nb_cap = (cfg->seq_cap + 63) / 64;
+    d->k_cap = cfg->select_mode == LYC_SELECT_BLOCKS
+                   ? (cfg->policy_kind == LYC_POLICY_RATIO ? nb_cap : std::min<int64_t>((cfg->top_k + 63) / 64, nb_cap))
+                   : (cfg->policy_kind == LYC_POLICY_RATIO ? cfg->seq_cap : std::min<int64_t>(cfg->top_k, cfg->seq_cap));
+    d->idx = reinterpret_cast<int32_t*>(uintptr_t{0x7f0000000000});  // a device address value only
+    int64_t seq = seq_len;
+    const int64_t* lens = seq_lens;
+    validate_lens(d, seq, lens);
+    const bool varlen = lens != nullptr;
+    const int B = d->B, H = d->H, G = d->G, cells = d->n_ctas(), BH = B * H;
+    const int max_units = BH + 3 * cells + 3, max_merges = BH * G;
+    LycPlanIn in{};
+    in.NL = d->NL; in.B = B; in.H = H; in.G = G; in.D = d->D; in.S = d->S; in.bs = 64;
+    in.select_mode = cfg->select_mode; in.policy_kind = cfg->policy_kind;
+    in.item_keys = lyc::step_item_keys(); in.seq_cap = cfg->seq_cap; in.k_cap = d->k_cap;
+    in.top_k = cfg->top_k; in.ratio = cfg->ratio; in.roles = d->roles.data(); in.idx = d->idx;
+    in.max_units = max_units; in.max_merges = max_merges; in.seq = seq;
+    LycPlanHdr hdr{};
+    in.hdr = &hdr;
+    if (seq_lens) {
+      in.has_lens = 1;
+      for (int b = 0; b < B; ++b) in.lens[b] = (int32_t)seq_lens[b];
+    }
+    const bool blocks = cfg->select_mode == LYC_SELECT_BLOCKS;
+    const bool none = cfg->select_mode == LYC_SELECT_NONE;
+    std::vector<int> last_r((size_t)H, 0);
+    auto mismatch = [&](int l, const std::string& what) {
+      fail(LYC_ESTATE, "selftest: layer " + std::to_string(l) + ": " + what);
+    };
+    for (int l = 0; l < d->NL; ++l) {
+      HostLaunch L;
+      host_slots(d, l, lens, seq, varlen, last_r, L);
+      int free_from = cells;
+      if (!none) {
+        const int64_t nk = blocks ? (seq + 63) / 64 : seq;
+        const int64_t items = (nk + lyc::step_item_keys() - 1) / lyc::step_item_keys();
+        const int64_t n_items = (int64_t)L.sel_rows.size() * items;
+        if (n_items > 0 && 2 * n_items <= cells) free_from = cells - (int)n_items;
+      }
+      bool ragged = false;
+      for (int b = 1; b < B; ++b) {
+        const int64_t lb = varlen ? lens[b] : seq, l0 = varlen ? lens[0] : seq;
+        ragged = ragged || (lb + 63) / 64 != (l0 + 63) / 64 || d->budget(lb) != d->budget(l0);
+      }
+      plan_step_launch(L, B, H, d->S, G, l, free_from, ragged);
+      std::vector<LycSlot> slots((size_t)BH), uslots((size_t)max_units);
+      std::vector<LycUnit> units((size_t)max_units);
+      std::vector<LycMergeTask> merges((size_t)max_merges);
+      std::vector<int32_t> split((size_t)cells + 1), srow((size_t)BH), sn((size_t)BH), sk((size_t)BH);
+      int32_t n_merges = -1, n_sel = -1, n_units = -1;
+      lyc::PlanOut o{slots.data(), units.data(), uslots.data(), split.data(), merges.data(),
+                     srow.data(), sn.data(), sk.data(), &n_merges, &n_sel, &n_units};
+      lyc::plan_layer_host(in, l, o);
+      if (hdr.status) mismatch(l, "planner flagged the lengths");
+      if (n_units != (int)L.units.size()) mismatch(l, "unit count " + std::to_string(n_units) + " vs " + std::to_string(L.units.size()));
+      if (n_merges != (int)L.merges.size()) mismatch(l, "merge count");
+      if (n_sel != (int)L.sel_rows.size()) mismatch(l, "selection rows");
+      for (int i = 0; i < BH; ++i)
+        if (std::memcmp(&slots[(size_t)i], &L.slots[(size_t)i], sizeof(LycSlot)))
+          mismatch(l, "slot " + std::to_string(i));
+      for (int u = 0; u < n_units; ++u) {
+        const LycUnit &a = units[(size_t)u], &b = L.units[(size_t)u];
+        if (a.slot != b.slot || a.begin != b.begin || a.end != b.end || a.hls != b.hls)
+          mismatch(l, "unit " + std::to_string(u));
+        if (std::memcmp(&uslots[(size_t)u], &L.slots[(size_t)b.slot], sizeof(LycSlot)))
+          mismatch(l, "unit slot " + std::to_string(u));
+      }
+      for (int c = 0; c <= cells; ++c)
+        if (split[(size_t)c] != L.split_off[(size_t)c]) mismatch(l, "split offset " + std::to_string(c));
+      for (int m = 0; m < n_merges; ++m)
+        if (std::memcmp(&merges[(size_t)m], &L.merges[(size_t)m], sizeof(LycMergeTask)))
+          mismatch(l, "merge task " + std::to_string(m));
+      for (int r = 0; r < n_sel; ++r) {
+        if (srow[(size_t)r] != L.sel_rows[(size_t)r]) mismatch(l, "selection row " + std::to_string(r));
+        const int b = L.sel_rows[(size_t)r] / H;
+        const int64_t len_b = varlen ? lens[b] : seq;
+        const int64_t want_n = varlen ? L.sel_n[(size_t)r] : (blocks ? (len_b + 63) / 64 : len_b);
+        const int64_t want_k = varlen ? L.sel_k[(size_t)r] : d->budget(len_b);
+        if (sn[(size_t)r] != want_n || sk[(size_t)r] != want_k) mismatch(l, "selection budget " + std::to_string(r));
+      }
+    }
+    const int64_t mx = varlen ? *std::max_element(lens, lens + B) : seq;
+    if (hdr.seq_len != mx || hdr.n_keys != (blocks ? (mx + 63) / 64 : mx) || hdr.k_sel != d->budget(mx))
+      fail(LYC_ESTATE, "selftest: plan header");
+    return LYC_OK;
+  });
+}
+
+// KvCache::append of the current token for device-resident lengths: row
+// d_seq_lens[b] - 1 of every (b, g) of layer `layer` (-1: every layer) from
+// src [n_layers?][B][H][d] -- the graph-capturable companion of
+// lyc_decoder_step_dev / lyc_decoder_capture_dev.
+namespace {
+__global__ void kv_append_kernel(uint4* __restrict__ kc, uint4* __restrict__ vc,
+                                 const uint4* __restrict__ ks, const uint4* __restrict__ vs,
+                                 const int64_t* __restrict__ lens, int64_t slabs, int64_t BH,
+                                 int64_t H, int64_t chunks, int64_t slab_chunks, int64_t slab0,
+                                 int64_t seq_cap) {
+  const int64_t total = slabs * chunks;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i % chunks, sl = i / chunks;
+    const int64_t b = (sl % BH) / H;
+    const int64_t pos = lens[b] - 1;
+    if (pos < 0 || pos >= seq_cap) continue;  // invalid length: the planner rejects the step
+    const int64_t dst = (slab0 + sl) * slab_chunks + pos * chunks + c;
+    kc[dst] = ks[i];
+    vc[dst] = vs[i];
+  }
+}
+}  // namespace
+
+int lyc_kv_append_dev(void* k_cache, void* v_cache, const lyc_kv_layout* lay, int32_t layer,
+                      const int64_t* d_seq_lens, const void* k_src, const void* v_src,
+                      void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    if (!lay) fail(LYC_EINVAL, "KvCache: null layout");
+    if (!k_cache || !v_cache || !k_src || !v_src || !d_seq_lens) fail(LYC_EINVAL, "KvCache: null buffer");
+    if (lay->n_layers < 1 || lay->batch < 1 || lay->n_kv_heads < 1 || lay->d_head < 1 ||
+        lay->seq_cap < 1)
+      fail(LYC_EINVAL, "KvCache: all dimensions must be >= 1");
+    if (lay->dtype != LYC_DTYPE_F32 && lay->dtype != LYC_DTYPE_BF16) fail(LYC_EINVAL, "KvCache: dtype");
+    if (layer < -1 || layer >= lay->n_layers) fail(LYC_EINVAL, "KvCache: layer out of range");
+    const int64_t row_bytes = (int64_t)lay->d_head * (lay->dtype == LYC_DTYPE_BF16 ? 2 : 4);
+    if (row_bytes % 16) fail(LYC_ENOTSUP, "KvCache: rows must be a multiple of 16 bytes");
+    const bool all = layer == -1;
+    const int64_t chunks = row_bytes / 16, BH = (int64_t)lay->batch * lay->n_kv_heads;
+    const int64_t slabs = BH * (all ? lay->n_layers : 1);
+    const int64_t total = slabs * chunks;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+    kv_append_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        static_cast<uint4*>(k_cache), static_cast<uint4*>(v_cache),
+        static_cast<const uint4*>(k_src), static_cast<const uint4*>(v_src), d_seq_lens, slabs, BH,
+        lay->n_kv_heads, chunks, lay->seq_cap * chunks, (all ? 0 : (int64_t)layer) * BH,
+        lay->seq_cap);
+    cuda_check(cudaGetLastError(), "kv append launch");
+    ++g_launches;
     return LYC_OK;
   });
 }

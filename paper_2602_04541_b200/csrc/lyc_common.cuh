@@ -9,6 +9,24 @@
 
 namespace lyc {
 
+// Programmatic dependent launch: a kernel launched with programmatic stream
+// serialisation may start while the previous kernel of the stream drains;
+// it must wait (griddepcontrol.wait) before reading that kernel's results.
+// The previous kernel lets its dependents launch early with
+// launch_dependents.  Both are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// One-time per-device setup flags (cudaFuncSetAttribute is per device: a
+// process driving several GPUs configures each of them).
+inline bool& device_flag(bool (&flags)[64]) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return flags[dev & 63];
+}
+
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -45,7 +45,7 @@ struct LycSlot {
   int32_t dep;           // layer whose selection wrote `list` (-1: none / already complete)
   const int32_t* count;  // ITEM_TOKENS: device count of valid ids (<= list_len), or nullptr
   int32_t seq;           // rows of this slot's sequence (seq_len of its batch item)
-  int32_t pad_;
+  int32_t item;          // its batch item b
 };
 
 struct LycUnit {
@@ -89,6 +89,7 @@ struct LycView {
   float scale_log2;         // scale * log2(e)
   int32_t stages;           // ring stages in use (<= the kernel's capacity; 0 = all)
   int32_t early_exit;       // per-layer kernel: units may end early (device-count sets)
+  const int32_t* seq_of;    // step kernel: live length of each batch item (by slot.item), or null
 };
 
 struct LycAttnParams {
@@ -173,6 +174,7 @@ struct LycLayerDesc {
 
 // Per-layer device counters (monotonic; a step adds n_ctas to each).
 enum {
+  CTR_PLAN = 7,      // (layer 0 only) CTAs past the in-kernel re-plan
   CTR_ATTN = 0,      // CTAs that finished the layer's attention units
   CTR_MERGE = 1,     // CTAs that finished the layer's merge tasks (layer output final)
   CTR_SEL0 = 2,      // selection phase barriers
@@ -185,7 +187,12 @@ enum {
 // Counters sit 256 B apart (separate L2 lines / slices): many CTAs poll them.
 #define LYC_CTR_STRIDE 64
 #define LYC_CTR(base, l, e) ((base) + ((size_t)(l) * CTR_PER_LAYER + (e)) * LYC_CTR_STRIDE)
-#define LYC_CTR_WORDS(n_layers) (((size_t)(n_layers) * CTR_PER_LAYER + 2) * LYC_CTR_STRIDE)
+// Two counter sets, used by alternate launches (the launch parity): a launch
+// counts up from zero in its own set and zeroes the other one, so no counter
+// is ever reset on the host and a launch may cover any layer range.  After
+// the sets: the control words (parity, then the exit count).
+#define LYC_CTR_SET_WORDS(n_layers) ((size_t)(n_layers) * CTR_PER_LAYER * LYC_CTR_STRIDE)
+#define LYC_CTR_WORDS(n_layers) (2 * LYC_CTR_SET_WORDS(n_layers) + 2 * LYC_CTR_STRIDE)
 
 // ---------------------------------------------------------------------------
 // Seq-parametric plan of the fused step (plan.cuh): computed on the device by
@@ -194,14 +201,21 @@ enum {
 #define LYC_PLAN_MAX_B 160   // batch items whose lengths travel by value
 #define LYC_PLAN_THREADS 256
 
-struct LycPlanHdr {          // written by the planner, read by the step kernel
-  int32_t seq_len;           // max over the batch
+struct LycPlanHdr {          // the last plan's lengths and the last step's status (device)
+  int32_t seq_len;           // max over the batch (of the last plan)
   int32_t n_keys;            // selection keys per row (seq_len, or blocks)
   int32_t k_sel;             // ids kept per row at seq_len
-  int32_t status;            // 0 ok; 1 invalid lengths (the step kernel does nothing)
+  int32_t status;            // 0 ok; 1 invalid lengths (that step did nothing)
   int32_t bad_item;          // first batch item with an invalid length
   int32_t pad[3];
 };
+// The plan depends on the lengths only through its KEY: each item's dense
+// block count nb and sparse budget kb, and the selection items per row.  A
+// step whose key matches reuses the plan (a growing sequence re-plans once
+// per 64 tokens); per-token values (lengths, selection sizes) are read live
+// by the step kernel.  Per layer the planner keeps the key its plan was made
+// for: [valid, items, nb[B], kb[B]].
+#define LYC_PLAN_KEY_INTS(B) (2 + 2 * (B))
 
 struct LycPlanIn {
   int32_t NL, B, H, G, D, S;  // layers, batch, KV heads, group, head dim, splits per item
@@ -215,6 +229,7 @@ struct LycPlanIn {
   int32_t* idx;               // device index cache (values stored in token / block slots)
   LycLayerDesc* layers;       // [NL]: per-layer arrays (fixed at create); n_merges / n_sel written
   LycPlanHdr* hdr;
+  int32_t* keys;              // [NL][LYC_PLAN_KEY_INTS(B)] the key of each layer's plan
   int32_t max_units;          // capacity of each layer's unit arrays
   int32_t max_merges;
   // the step's lengths: dlens (device [B], current token included) when set,
@@ -245,9 +260,11 @@ struct LycStepParams {
   uint32_t* sel_cand;        // [2 parity][max_sel][2][sel_stride] boundary-bin candidates: keys, indices
   uint32_t* sel_ccnt;        // [2 parity][max_sel][256] per item: candidates [0,64), definite keys [64,128); row prefix [192,195)
   uint32_t* sel_csub;        // [2 parity][max_sel][64 items][256 u16] bucket starts of each item's candidates
-  uint32_t* sel_rowctr;      // [n_layers][max_sel][16] monotonic: per selection row words 0 / 8
+  uint32_t* sel_rowctr;      // [2 parity][n_layers][max_sel][16]: per selection row words 0 / 8
                              // (items classified / holding copies); per SLOT word 12 (units done)
-  uint32_t* ctr;             // LYC_CTR counters: [n_layers][CTR_PER_LAYER], then epoch, exits
+  int64_t rowctr_set;        // words of one sel_rowctr set
+  uint32_t* ctr;             // LYC_CTR counters: [2 parity][n_layers][CTR_PER_LAYER], then control
+  LycPlanHdr* hdr;           // the plan key; the step status
   int32_t* idx;              // index cache [B*H][idx_stride]
   int64_t idx_stride;
   int32_t* idx_count;        // [B*H]
@@ -255,16 +272,15 @@ struct LycStepParams {
   int32_t* set_trace;        // optional [n_layers][B*H][idx_stride]: each layer's emitted sets
   int32_t* set_trace_count;  // optional [n_layers][B*H]
   int32_t n_layers;
+  int32_t l_begin, l_end;    // the layers of this launch (q / out point at layer l_begin)
   int32_t max_sel;
-  int32_t n_keys;            // selection candidates per row (seq_len or n_blocks)
-  int32_t k_sel;             // ids kept per row (min(k, n_keys))
   int32_t n_splits;
   int32_t n_ctas;            // CTAs = n_splits * batch (grid index = b * n_splits + split)
-  int32_t seq_len;
   int32_t block_size;
   int32_t group;
   int32_t sel_mode;
   float scale;
   float scale_log2;
   int32_t stages;            // attention ring stages in use (0 = all)
+  LycPlanIn plan;            // the step's lengths + the planner's input (re-plan in the kernel)
 };

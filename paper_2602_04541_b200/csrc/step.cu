@@ -29,7 +29,10 @@
 // ascending order into the index cache.  No grid barrier: a per-head counter.
 // Grid-wide coordination uses monotonic counters in global memory (each step
 // adds a fixed amount); the launch is cooperative, so every CTA is co-resident.
+#include <climits>
+
 #include "attn_core.cuh"
+#include "plan.cuh"
 
 namespace lyc {
 
@@ -113,15 +116,30 @@ __device__ __forceinline__ void stamp(const LycStepParams& p, int l, int ev, int
   }
 }
 
+// Per-launch runtime state of every thread: this launch's counter set (the
+// launch parity) and the step's lengths from the plan header.
+struct StepRt {
+  uint32_t* ctr;     // LYC_CTR counters of this launch's set
+  uint32_t* rowctr;  // [n_layers][max_sel][16] of this launch's set
+  int n_keys;        // selection keys per row (max over the batch)
+  int k_sel;         // ids kept per row
+  int l_begin;       // first layer of this launch: earlier layers completed in earlier launches
+  int ragged;        // batch items differ in (blocks, budget): per-row selection sizes
+  const int32_t* seqs;  // [B] live lengths of the step (shared memory)
+  const int32_t* nsel;  // [B] selection keys of each item's rows (shared memory)
+  const int32_t* ksel;  // [B] ids kept per row of each item (shared memory)
+};
+
 // Every selection item signals CTR_SELDONE once after emitting its share of
 // the index-cache row.
-__device__ __forceinline__ uint32_t seldone_per_step(const LycStepParams& p, int l) {
-  return (uint32_t)p.layers[l].n_sel * (uint32_t)((p.n_keys + kItemKeys - 1) / kItemKeys);
+__device__ __forceinline__ uint32_t seldone_per_step(const LycStepParams& p, const StepRt& rt,
+                                                     int l) {
+  return (uint32_t)p.layers[l].n_sel * (uint32_t)((rt.n_keys + kItemKeys - 1) / kItemKeys);
 }
 
 struct StepWaits {
   const LycStepParams* p;
-  uint32_t epoch1;
+  const StepRt* rt;
   int layer;
   int pt;
   __device__ __forceinline__ void wait(const uint32_t* c, uint32_t target) const {
@@ -129,11 +147,13 @@ struct StepWaits {
     group_bar(3, kProducerThreads);
   }
   __device__ __forceinline__ void unit(const LycSlot& s) const {
-    if (s.dep >= 0)  // every retrieval head of layer dep finished its selection
-      wait(LYC_CTR(p->ctr, s.dep, CTR_SELDONE), epoch1 * seldone_per_step(*p, s.dep));
+    // every retrieval head of layer dep finished its selection (a layer of an
+    // earlier launch has: stream order)
+    if (s.dep >= rt->l_begin)
+      wait(LYC_CTR(rt->ctr, s.dep, CTR_SELDONE), seldone_per_step(*p, *rt, s.dep));
   }
   const uint32_t* clayer;  // shared: 1 + the layer this CTA's consumers started
-  __device__ __forceinline__ bool needed() const { return layer > 0; }
+  __device__ __forceinline__ bool needed() const { return layer > rt->l_begin; }
   // OR over the producer threads (barrier with reduction)
   __device__ __forceinline__ bool any(bool v) const {
     uint32_t r;
@@ -148,20 +168,20 @@ struct StepWaits {
   // the previous layer's outputs are final once this CTA's consumers have
   // started this layer (they waited for it); otherwise wait for it here
   __device__ __forceinline__ void last_tile() const {
-    if (layer == 0) return;
+    if (layer == rt->l_begin) return;
     if (pt == 0 && (int)(ld_acquire_cta_shared(clayer) - (uint32_t)(layer + 1)) < 0)
-      spin_until(LYC_CTR(p->ctr, layer - 1, CTR_MERGE), epoch1 * (uint32_t)p->n_ctas);
+      spin_until(LYC_CTR(rt->ctr, layer - 1, CTR_MERGE), (uint32_t)p->n_ctas);
     group_bar(3, kProducerThreads);
   }
 };
 
-__device__ __forceinline__ LycView layer_view(const LycStepParams& p, const LycLayerDesc& L,
-                                              int l, int esz) {
+__device__ __forceinline__ LycView layer_view(const LycStepParams& p, const StepRt& rt,
+                                              const LycLayerDesc& L, int l, int esz) {
   LycView v;
   v.k = p.k;
   v.v = p.v;
-  v.q = static_cast<const uint8_t*>(p.q) + (int64_t)l * p.q_layer_stride * esz;
-  v.out = static_cast<uint8_t*>(p.out) + (int64_t)l * p.q_layer_stride * esz;
+  v.q = static_cast<const uint8_t*>(p.q) + (int64_t)(l - p.l_begin) * p.q_layer_stride * esz;
+  v.out = static_cast<uint8_t*>(p.out) + (int64_t)(l - p.l_begin) * p.q_layer_stride * esz;
   v.slots = L.slots;
   v.units = L.units;
   v.unit_slots = L.unit_slots;
@@ -177,7 +197,7 @@ __device__ __forceinline__ LycView layer_view(const LycStepParams& p, const LycL
   v.sel_stride = p.sel_stride;
   v.counts_stride = 0;
   v.n_splits = p.n_splits;
-  v.seq_len = p.seq_len;
+  v.seq_len = rt.n_keys;
   v.block_size = p.block_size;
   v.group = p.group;
   v.sel_mode = p.sel_mode;
@@ -186,8 +206,9 @@ __device__ __forceinline__ LycView layer_view(const LycStepParams& p, const LycL
   v.stages = p.stages;
   v.early_exit = 0;
   v.trace_l = p.trace ? p.trace + (size_t)l * LYC_TRACE_EVENTS * p.n_ctas : nullptr;
-  v.slot_ctr = p.sel_rowctr + (size_t)l * p.max_sel * 16;
+  v.slot_ctr = rt.rowctr + (size_t)l * p.max_sel * 16;
   v.trace_ctas = p.n_ctas;
+  v.seq_of = rt.seqs;  // the live lengths (the plan's slot records may be up to 63 tokens old)
   return v;
 }
 
@@ -315,7 +336,8 @@ __device__ __forceinline__ void epi_digit(EpiSmem& es, const uint32_t* h, bool g
 
 struct SelRow {
   uint32_t k;         // ids kept (variable-length batch: this row's budget)
-  int n;              // keys of this row's sequence (<= p.n_keys; the rest are masked)
+  int n;              // keys of this row's sequence (<= nk; the rest are masked)
+  int nk;             // keys of the longest row (the padded row length)
   uint32_t* keys;     // keys of the row [n]
   uint32_t* h1;       // fused first-pass (12-bit) histogram (token mode) or nullptr
   uint32_t* bitmap;   // [n_words]
@@ -328,12 +350,19 @@ struct SelRow {
   uint32_t* ctr;      // per-row words: [0] items classified, [8] items holding their copies
 };
 
-__device__ __forceinline__ SelRow sel_row(const LycStepParams& p, int l, int r) {
+__device__ __forceinline__ SelRow sel_row(const LycStepParams& p, const StepRt& rt, int l, int r) {
   const int64_t pr = (int64_t)(l & 1) * p.max_sel + r;
   SelRow s;
   const LycLayerDesc& L = p.layers[l];
-  s.k = L.sel_k ? (uint32_t)__ldg(L.sel_k + r) : (uint32_t)p.k_sel;
-  s.n = L.sel_n ? __ldg(L.sel_n + r) : p.n_keys;
+  if (rt.ragged) {  // this row's item: its own length and budget (policy.hpp:57-72)
+    const int b = __ldcg(L.sel_rows + r) / p.plan.H;
+    s.k = (uint32_t)rt.ksel[b];
+    s.n = rt.nsel[b];
+  } else {
+    s.k = (uint32_t)rt.k_sel;
+    s.n = rt.n_keys;
+  }
+  s.nk = rt.n_keys;
   s.keys = p.sel_keys + pr * p.sel_stride;
   s.h1 = p.sel_mode == SEL_TOKEN_KEYS ? p.hist + pr * LYC_H1_STRIDE : nullptr;
   s.bitmap = p.sel_bitmap + pr * p.bitmap_stride;
@@ -341,7 +370,7 @@ __device__ __forceinline__ SelRow sel_row(const LycStepParams& p, int l, int r) 
   s.cidx = s.ckey + p.sel_stride;
   s.csub = p.sel_csub + pr * (64 * 128);
   s.ccnt = p.sel_ccnt + pr * 256;
-  s.ctr = p.sel_rowctr + ((int64_t)l * p.max_sel + r) * 16;
+  s.ctr = rt.rowctr + ((int64_t)l * p.max_sel + r) * 16;
   return s;
 }
 
@@ -397,7 +426,7 @@ __device__ __forceinline__ void row_prefix(const LycStepParams& p, const SelRow&
 // their next 8 bits into the row's 256-bin sub-histogram (global, atomics).
 __device__ void classify_item(const LycStepParams& p, const SelRow& R, int q, EpiSmem& es,
                               uint32_t& bar_phase, int et, int l, int cta) {
-  const int n = p.n_keys;
+  const int n = R.nk;
   const int lo = q * kItemKeys;
   const int cnt = min(kItemKeys, n - lo);
   // keys of this row's own sequence (a shorter item of a variable-length
@@ -546,10 +575,11 @@ __device__ void classify_item(const LycStepParams& p, const SelRow& R, int q, Ep
 // index: attention.hpp:115-119).  Per-item selected counts give this item's
 // output offset; its own words (definite keys + its selected candidates) are
 // emitted with branch-free predicated stores.
-__device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q, int row,
-                                  int32_t* out, EpiSmem& es, uint32_t& bar_phase,
-                                  uint32_t epoch1, int et, int l, int cta) {
-  const int n = p.n_keys;
+__device__ void resolve_emit_item(const LycStepParams& p, const StepRt& rt, const SelRow& R, int q,
+                                  int row, int32_t* out, EpiSmem& es, uint32_t& bar_phase, int et,
+                                  int l, int cta) {
+  constexpr uint32_t epoch1 = 1u;  // counters count from zero in every launch
+  const int n = R.nk;
   const int items = (n + kItemKeys - 1) / kItemKeys;
   const int lo = q * kItemKeys;
   const int cnt = min(kItemKeys, n - lo);
@@ -872,8 +902,58 @@ __device__ void resolve_emit_item(const LycStepParams& p, const SelRow& R, int q
   epi_bar();
   if (et == 0) {
     stamp(p, l, EV_F_EMIT, cta);
-    signal(LYC_CTR(p.ctr, l, CTR_SELDONE));
+    signal(LYC_CTR(rt.ctr, l, CTR_SELDONE));
   }
+}
+
+// The step's lengths into shared memory (cold prologue code, kept out of the
+// kernel body): per item its length, selection keys and budget; n_keys /
+// k_sel of the longest item and the ragged flag into dyn[1..3].  Returns
+// false (and flags the header) when a length is < 1 or > seq_cap.
+__device__ __noinline__ bool step_lengths(const LycStepParams& p, int32_t* seqs, int32_t* nsel,
+                                          int32_t* ksel, int32_t* dyn) {
+  const LycPlanIn& pin = p.plan;
+  __shared__ int32_t s_max, s_bad;
+  if (threadIdx.x == 0) {
+    s_max = 0;
+    s_bad = INT_MAX;
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < pin.B; b += blockDim.x) {
+    const int64_t v = pin.dlens ? __ldcg(pin.dlens + b) : pin.has_lens ? (int64_t)pin.lens[b] : pin.seq;
+    const bool ok = v >= 1 && v <= pin.seq_cap;
+    int32_t nb = 0, kb = 0;
+    if (ok) {
+      plan_item_key(pin, v, nb, kb);
+      atomicMax(&s_max, (int32_t)v);
+    } else {
+      atomicMin(&s_bad, b);
+    }
+    seqs[b] = ok ? (int32_t)v : 0;
+    nsel[b] = p.sel_mode == SEL_BLOCK_KEYS ? nb : (int32_t)v;
+    ksel[b] = kb;
+  }
+  __syncthreads();
+  if (s_bad != INT_MAX) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      p.hdr->bad_item = s_bad;
+      p.hdr->status = 1;
+    }
+    return false;
+  }
+  int rag = 0;
+  for (int b = threadIdx.x; b < pin.B; b += blockDim.x)
+    rag |= (nsel[b] != nsel[0] || ksel[b] != ksel[0]) ? 1 : 0;
+  const int ragged = __syncthreads_or(rag);
+  if (threadIdx.x == 0) {
+    int32_t nb, kb;
+    plan_item_key(pin, s_max, nb, kb);
+    dyn[1] = p.sel_mode == SEL_BLOCK_KEYS ? nb : s_max;
+    dyn[2] = kb;
+    dyn[3] = ragged;
+  }
+  __syncthreads();
+  return true;
 }
 
 // ---------------------------------------------------------------- kernel
@@ -884,12 +964,19 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
   extern __shared__ uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
-  uint32_t* ctrl = LYC_CTR(p.ctr, p.n_layers, 0);  // completed steps; exits at + stride
-  __shared__ uint32_t s_epoch;
+  const size_t set_words = LYC_CTR_SET_WORDS(p.n_layers);
+  uint32_t* ctrl = p.ctr + 2 * set_words;  // [0] launch parity, [LYC_CTR_STRIDE] exits
+  __shared__ int32_t s_dyn[4];             // parity, n_keys, k_sel, ragged
+  __shared__ int32_t s_seq[LYC_PLAN_MAX_B];  // the step's lengths, per batch item
+  __shared__ int32_t s_nsel[LYC_PLAN_MAX_B]; //   selection keys of its rows
+  __shared__ int32_t s_ksel[LYC_PLAN_MAX_B]; //   ids kept per row
   const AttnSmem<T, D> sm = AttnSmem<T, D>::carve(smem_raw);
   EpiSmem& es = *reinterpret_cast<EpiSmem*>(sm.extra);
+  const LycPlanIn& pin = p.plan;
+  pdl_wait();     // the previous launch of the stream has completed and its writes are visible
+  pdl_trigger();  // the next launch in the stream may begin its launch while this one runs
   if (threadIdx.x == 0) {
-    s_epoch = ld_acquire(ctrl);
+    s_dyn[0] = (int32_t)__ldcg(ctrl);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&sm.full[s], kProducerThreads + 1);  // + the tile-info arrival
       mbar_init(&sm.empty[s], kConsumerWarps);
@@ -900,8 +987,31 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
   }
   for (int b = threadIdx.x; b < LYC_H1_BINS; b += kStepThreads) sm.hist[b] = 0u;
   __syncthreads();
-  const uint32_t epoch1 = s_epoch + 1u;
-  const uint32_t t_attn = epoch1 * (uint32_t)p.n_ctas;
+  // ---- the step's lengths (host values by value, or a device array read now)
+  if (!step_lengths(p, s_seq, s_nsel, s_ksel, s_dyn)) return;  // invalid: no work, no counter touched
+  const int par = s_dyn[0] & 1;
+  StepRt rt;
+  rt.ctr = p.ctr + (size_t)par * set_words;
+  rt.rowctr = p.sel_rowctr + par * p.rowctr_set;
+  rt.n_keys = s_dyn[1];
+  rt.k_sel = s_dyn[2];
+  rt.l_begin = p.l_begin;
+  rt.ragged = s_dyn[3];
+  rt.seqs = s_seq;
+  rt.nsel = s_nsel;
+  rt.ksel = s_ksel;
+  if (cta == 0 && threadIdx.x == 0) p.hdr->status = 0;
+  {  // zero the other set for the next launch (nobody uses it in this one)
+    uint32_t* oc = p.ctr + (size_t)(par ^ 1) * set_words;
+    uint32_t* orc = p.sel_rowctr + (par ^ 1) * p.rowctr_set;
+    const int64_t stride = (int64_t)p.n_ctas * kStepThreads;
+    for (int64_t i = (int64_t)cta * kStepThreads + threadIdx.x; i < (int64_t)set_words; i += stride)
+      oc[i] = 0u;
+    for (int64_t i = (int64_t)cta * kStepThreads + threadIdx.x; i < p.rowctr_set; i += stride)
+      orc[i] = 0u;
+  }
+  constexpr uint32_t epoch1 = 1u;
+  const uint32_t t_attn = (uint32_t)p.n_ctas;
   constexpr int esz = (int)sizeof(T);
   const int cell = cta;  // = b * n_splits + split
 
@@ -910,16 +1020,16 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
     const int tid = threadIdx.x;
     int stage = 0;
     uint32_t phase = 0;
-    for (int l = 0; l < p.n_layers; ++l) {
-      if (l > 0) {
+    for (int l = p.l_begin; l < p.l_end; ++l) {
+      if (l > p.l_begin) {
         if (tid == 0) {
           // the previous layer's outputs are final, and the key / histogram
           // buffers of this parity are free once layer l-2's selection (if
           // any) finished: both counters polled together (one round trip)
-          const bool sel2 = l >= 2 && p.layers[l - 2].n_sel > 0 && p.sel_mode != SEL_NONE;
-          spin_until2(LYC_CTR(p.ctr, l - 1, CTR_MERGE), t_attn,
-                      sel2 ? LYC_CTR(p.ctr, l - 2, CTR_SELDONE) : nullptr,
-                      sel2 ? epoch1 * seldone_per_step(p, l - 2) : 0u);
+          const bool sel2 = l - 2 >= p.l_begin && p.layers[l - 2].n_sel > 0 && p.sel_mode != SEL_NONE;
+          spin_until2(LYC_CTR(rt.ctr, l - 1, CTR_MERGE), t_attn,
+                      sel2 ? LYC_CTR(rt.ctr, l - 2, CTR_SELDONE) : nullptr,
+                      sel2 ? seldone_per_step(p, rt, l - 2) : 0u);
         }
         consumer_bar();
       }
@@ -928,20 +1038,20 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
         stamp(p, l, EV_CONS_BEGIN, cta);
       }
       const LycLayerDesc L = p.layers[l];
-      const LycView v = layer_view(p, L, l, esz);
+      const LycView v = layer_view(p, rt, L, l, esz);
       consume_units<T, D>(v, sm, L.split_off[cell], L.split_off[cell + 1], warp, lane, stage,
-                          phase, l > 0 ? (l & 1) : -1);
+                          phase, l > p.l_begin ? (l & 1) : -1);
       consumer_bar();
       if (tid == 0) {
         stamp(p, l, EV_CONS_END, cta);
-        signal(LYC_CTR(p.ctr, l, CTR_ATTN));
+        signal(LYC_CTR(rt.ctr, l, CTR_ATTN));
       }
       // while the grid finishes layer l: stage layer l + 1's unit records
       // (static plan data) into the other record buffer
       if constexpr (sizeof(T) == 2) {
-        if (l + 1 < p.n_layers) {
+        if (l + 1 < p.l_end) {
           const LycLayerDesc Ln = p.layers[l + 1];
-          const LycView vn = layer_view(p, Ln, l + 1, esz);
+          const LycView vn = layer_view(p, rt, Ln, l + 1, esz);
           UnitRec* rec = reinterpret_cast<UnitRec*>(sm.ustage) + ((l + 1) & 1) * C::kQUnits;
           stage_unit_records(vn, rec, Ln.split_off[cell], Ln.split_off[cell + 1], tid, C::kQUnits);
         }
@@ -956,10 +1066,10 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
     }
     int stage = 0;
     uint32_t phase = 0;
-    for (int l = 0; l < p.n_layers; ++l) {
+    for (int l = p.l_begin; l < p.l_end; ++l) {
       const LycLayerDesc L = p.layers[l];
-      const LycView v = layer_view(p, L, l, esz);
-      StepWaits waits{&p, epoch1, l, pt, sm.clayer};
+      const LycView v = layer_view(p, rt, L, l, esz);
+      StepWaits waits{&p, &rt, l, pt, sm.clayer};
       produce_units<T, D>(v, &p.tmap_k, &p.tmap_v, sm.ring, sm.full, sm.empty, sm.tinfo,
                           L.split_off[cell], L.split_off[cell + 1], pt, stage, phase, waits);
     }
@@ -968,9 +1078,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
     const int et = threadIdx.x - (kConsumerWarps + kProducerWarps) * 32;
     const int ew = et >> 5;
     const int chunks = (D + 31) / 32;
-    const int items = (p.n_keys + kItemKeys - 1) / kItemKeys;
+    const int items = (rt.n_keys + kItemKeys - 1) / kItemKeys;
     uint32_t bar_phase = 0;
-    for (int l = 0; l < p.n_layers; ++l) {
+    for (int l = p.l_begin; l < p.l_end; ++l) {
       const LycLayerDesc L = p.layers[l];
       // Roles of this layer's epilogue: when the selection items fit in half
       // the grid they go to the LAST n_items CTAs, which start classifying a
@@ -984,10 +1094,10 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
       const int merge_ctas = split_roles ? item_base : p.n_ctas;
       // no layer barrier: every merge task waits for its own slot's units,
       // every selection item for its row's retrieval slot (per-slot counters)
-      uint32_t* slot_ctr = p.sel_rowctr + (size_t)l * p.max_sel * 16 + 12;
+      uint32_t* slot_ctr = rt.rowctr + (size_t)l * p.max_sel * 16 + 12;
       // (a) split-KV merge
       const int total = L.n_merges * chunks;
-      uint8_t* outl = static_cast<uint8_t*>(p.out) + (int64_t)l * p.q_layer_stride * esz;
+      uint8_t* outl = static_cast<uint8_t*>(p.out) + (int64_t)(l - p.l_begin) * p.q_layer_stride * esz;
       if (cta < merge_ctas)
         for (int t = ew * merge_ctas + cta; t < total; t += merge_ctas * kEpiWarps) {
           const LycMergeTask tk = L.merges[t / chunks];
@@ -998,7 +1108,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
       epi_bar();
       if (et == 0) {
         stamp(p, l, EV_MERGE, cta);
-        signal(LYC_CTR(p.ctr, l, CTR_MERGE));
+        signal(LYC_CTR(rt.ctr, l, CTR_MERGE));
       }
       // (b) selection items of this layer's retrieval heads: classify every
       // own item, then resolve the rows and emit the items
@@ -1012,13 +1122,13 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
             stamp(p, l, EV_EPI_ATTN, cta);
           }
           epi_bar();
-          classify_item(p, sel_row(p, l, r), q, es, bar_phase, et, l, cta);
+          classify_item(p, sel_row(p, rt, l, r), q, es, bar_phase, et, l, cta);
         }
         for (int it = i0; it < n_items; it += istep) {
           const int r = it / items, q = it - r * items;
           const int row = __ldg(L.sel_rows + r);
-          resolve_emit_item(p, sel_row(p, l, r), q, row, p.idx + (int64_t)row * p.idx_stride, es,
-                            bar_phase, epoch1, et, l, cta);
+          resolve_emit_item(p, rt, sel_row(p, rt, l, r), q, row, p.idx + (int64_t)row * p.idx_stride,
+                            es, bar_phase, et, l, cta);
         }
       }
     }
@@ -1026,45 +1136,51 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t done = atomicAdd(ctrl + LYC_CTR_STRIDE, 1u);
-    if (done == t_attn - 1u) atomicAdd(ctrl, 1u);  // last CTA out: one more completed step
+    if (done == (uint32_t)p.n_ctas - 1u) {  // last CTA out: the next launch uses the other set
+      ctrl[LYC_CTR_STRIDE] = 0u;
+      ctrl[0] = (uint32_t)(par ^ 1);
+    }
   }
 }
 
 template <typename T, int D>
-static cudaError_t launch_step_t(const LycStepParams& p, cudaStream_t st) {
+static cudaError_t launch_step_t(const LycStepParams& p, cudaStream_t st, bool pdl) {
   using C = AttnCfg<T, D>;
-  static bool configured = false;
-  if (!configured) {
+  static bool configured[64] = {};
+  bool& done = device_flag(configured);
+  if (!done) {
     cudaError_t e = cudaFuncSetAttribute(hybrid_step_kernel<T, D>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    done = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.n_ctas);
   cfg.blockDim = dim3(kStepThreads);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, hybrid_step_kernel<T, D>, p);
 }
 
-cudaError_t launch_step(const LycStepParams& p, int dtype, int d, cudaStream_t st) {
+cudaError_t launch_step(const LycStepParams& p, int dtype, int d, cudaStream_t st, bool pdl) {
   if (dtype == 1) {
     switch (d) {
-      case 64: return launch_step_t<__nv_bfloat16, 64>(p, st);
-      case 128: return launch_step_t<__nv_bfloat16, 128>(p, st);
+      case 64: return launch_step_t<__nv_bfloat16, 64>(p, st, pdl);
+      case 128: return launch_step_t<__nv_bfloat16, 128>(p, st, pdl);
     }
   } else {
     switch (d) {
-      case 16: return launch_step_t<float, 16>(p, st);
-      case 32: return launch_step_t<float, 32>(p, st);
-      case 64: return launch_step_t<float, 64>(p, st);
-      case 128: return launch_step_t<float, 128>(p, st);
+      case 16: return launch_step_t<float, 16>(p, st, pdl);
+      case 32: return launch_step_t<float, 32>(p, st, pdl);
+      case 64: return launch_step_t<float, 64>(p, st, pdl);
+      case 128: return launch_step_t<float, 128>(p, st, pdl);
     }
   }
   return cudaErrorInvalidValue;
@@ -1074,6 +1190,22 @@ cudaError_t launch_step(const LycStepParams& p, int dtype, int d, cudaStream_t s
 int64_t step_max_keys() {
   return (int64_t)64 * kItemKeys;  // <= 64 items per row (one epilogue thread per item)
 }
+// Bytes of the step kernel's K/V ring (the in-kernel planner's scratch).
+int64_t step_ring_bytes(int dtype, int d) {
+  if (dtype == 1) {
+    if (d == 64) return (int64_t)AttnCfg<__nv_bfloat16, 64>::kStages * AttnCfg<__nv_bfloat16, 64>::kStageBytes;
+    if (d == 128) return (int64_t)AttnCfg<__nv_bfloat16, 128>::kStages * AttnCfg<__nv_bfloat16, 128>::kStageBytes;
+    return 0;
+  }
+  switch (d) {
+    case 16: return (int64_t)AttnCfg<float, 16>::kStages * AttnCfg<float, 16>::kStageBytes;
+    case 32: return (int64_t)AttnCfg<float, 32>::kStages * AttnCfg<float, 32>::kStageBytes;
+    case 64: return (int64_t)AttnCfg<float, 64>::kStages * AttnCfg<float, 64>::kStageBytes;
+    case 128: return (int64_t)AttnCfg<float, 128>::kStages * AttnCfg<float, 128>::kStageBytes;
+  }
+  return 0;
+}
+
 int64_t step_bitmap_words(int64_t n_keys) { return bm_padded_words((int)((n_keys + 31) / 32)); }
 int step_item_keys() { return kItemKeys; }
 

@@ -269,7 +269,8 @@ int64_t window_workspace_bytes(int B, int H, int G, int W, int n_split) {
 
 template <int D>
 static cudaError_t launch_window_t(const WinParams& p, void* out, cudaStream_t st) {
-  static bool configured = false;
+  static bool configured_[64] = {};
+  bool& configured = device_flag(configured_);
   const int smem = (int)sizeof(WinSmem<D>);
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(window_attn_kernel<D>,

@@ -156,6 +156,36 @@ class HybridDecoder:
                                             self._stream(stream)))
         return out
 
+    def decode_step_dev(self, q, k_cache, v_cache, seq_lens, out=None, *, stream=None):
+        """A step whose lengths live on the device (int64 [B] tensor, current
+        token included), read by the device planner when the step runs
+        (lyc_decoder_step_dev).  No host synchronisation."""
+        if out is None:
+            out = torch.empty_like(q)
+        _check_lens_tensor(seq_lens, self.batch)
+        check(lib().lyc_decoder_step_dev(self._h, q.data_ptr(), k_cache.data_ptr(),
+                                         v_cache.data_ptr(), seq_lens.data_ptr(), out.data_ptr(),
+                                         self._stream(stream)))
+        return out
+
+    def capture_dev(self, q, k_cache, v_cache, seq_lens, out, *, stream=None):
+        """Capture a step with device-resident lengths: every replay plans the
+        lengths `seq_lens` holds when it runs (lyc_decoder_capture_dev)."""
+        _check_lens_tensor(seq_lens, self.batch)
+        check(lib().lyc_decoder_capture_dev(self._h, q.data_ptr(), k_cache.data_ptr(),
+                                            v_cache.data_ptr(), seq_lens.data_ptr(),
+                                            out.data_ptr(), self._stream(stream)))
+        self.captured = (q, k_cache, v_cache, seq_lens, out)
+
+    def status(self, *, stream=None):
+        """Raise InvalidArgument if the last device-planned step rejected its
+        lengths (synchronises the stream)."""
+        check(lib().lyc_decoder_status(self._h, self._stream(stream)))
+
+    def tune(self, what: int, value: int):
+        """Experiment knobs (_lib.TUNE_RING_STAGES, _lib.TUNE_PER_LAYER_KERNELS)."""
+        check(lib().lyc_decoder_tune(self._h, int(what), int(value)))
+
     def layer(self, l: int, q_l, k_cache, v_cache, seq_len: int, out_l=None, *, stream=None):
         """One layer (decode_engine.hpp:120-143); layers in order within a step."""
         if out_l is None:
@@ -251,6 +281,30 @@ class HybridDecoder:
         ms = np.zeros(self.n_layers, dtype=np.float32)
         check(lib().lyc_decoder_attn_ms(self._h, ms.ctypes.data))
         return ms
+
+
+def _check_lens_tensor(t, batch):
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.int64 and
+            t.numel() == batch and t.is_contiguous()):
+        raise InvalidArgument("seq_lens: a contiguous int64 CUDA tensor with one length per batch item")
+
+
+def plan_selftest(*, n_layers, batch, n_kv_heads, group_size, d_head, seq_cap, roles, policy,
+                  select="tokens", seq_len=0, seq_lens=None, n_sms=148, num_splits=0) -> None:
+    """The device planner (plan.cuh, run on the host) against the host-order
+    planner; raises LogicError on the first difference.  No GPU needed."""
+    r = np.ascontiguousarray(np.asarray(roles, dtype=np.uint8).reshape(n_layers, n_kv_heads))
+    cfg = _lib.lyc_decode_config(
+        n_layers=n_layers, batch=batch, n_kv_heads=n_kv_heads, group_size=group_size,
+        d_head=d_head, dtype=_lib.DTYPE_BF16, seq_cap=seq_cap, policy_kind=policy.code(),
+        select_mode={"tokens": _lib.SELECT_TOKENS, "blocks": _lib.SELECT_BLOCKS,
+                     "none": _lib.SELECT_NONE}[select],
+        top_k=policy.k, ratio=policy.value, block_size=64, num_splits=num_splits, scale=0.0,
+        roles=r.ctypes.data)
+    arr = None
+    if seq_lens is not None:
+        arr = (C.c_int64 * batch)(*[int(x) for x in seq_lens])
+    check(lib().lyc_plan_selftest(C.byref(cfg), int(seq_len), arr, int(n_sms)))
 
 
 def _wrap_device(ptr: int, n: int, dev) -> torch.Tensor:

@@ -258,6 +258,8 @@ def test_fused_step_matches_per_layer_kernels(orc, select):
     assert fused.fused
     out_f = fused.decode_step(q, K, V, seq)
     per = mk()
+    per.tune(P._lib.TUNE_PER_LAYER_KERNELS, 1)  # attention + merge + cluster top-k launches
+    assert not per.fused
     out_p = torch.empty_like(q)
     for l in range(NL):
         per.layer(l, q[l], K, V, seq, out_p[l])
