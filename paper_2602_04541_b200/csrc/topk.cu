@@ -210,7 +210,10 @@ int topk_cluster_size(int n, int max_slice) {
 cudaError_t launch_topk(const LycTopkParams& p, int rows, int cluster, cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
   const size_t smem = topk_smem_bytes(p.slice);
-  static size_t configured = 0;
+  static size_t configured_[64] = {};  // per device: attributes are per-device state
+  int dev = 0;
+  cudaGetDevice(&dev);
+  size_t& configured = configured_[dev & 63];
   if (configured < smem) {
     cudaError_t e = cudaFuncSetAttribute(topk_cluster_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -2,7 +2,8 @@
 their row slices of the same cache and one shared gathered buffer (the packed
 all-gather layout of lyc_shard_merge).  Every rank must produce bitwise the
 same outputs and global index sets; those must match the unsharded decoder
-(and the oracle) within the north_star tolerances, index sets exactly."""
+and the oracle's decode_step (decode_engine.hpp:109-151, oracle/hh_oracle.c)
+within the north_star tolerances, index sets exactly."""
 import numpy as np
 import pytest
 import torch
@@ -47,8 +48,23 @@ def _last_retrieval(roles, g):
     return max(l for l in range(roles.shape[0]) if l == 0 or roles[l, g] == 0)
 
 
+def _vs_oracle(orc, q, K, V, roles, seq, k, d, out, gsets, tol):
+    """The rank-0 output and global sets against the oracle, per batch item."""
+    NL, B, H = K.shape[0], K.shape[1], K.shape[2]
+    g0 = gsets[0].cpu().numpy()
+    for b in range(B):
+        ref = orc.decode_step(q[:, b].float().numpy(), K[:, b].float().numpy(),
+                              V[:, b].float().numpy(), roles, seq=seq, scale=1 / np.sqrt(d),
+                              kind="topk", k=k)
+        err = rel_err(out[:, b].float().cpu().numpy(), ref["out"])
+        assert err < tol, (b, err)
+        for g in range(H):
+            l = _last_retrieval(roles, g)
+            np.testing.assert_array_equal(g0[l, b * H + g, :k], ref["sets"][g])
+
+
 @pytest.mark.parametrize("P_", [2, 3, 4, 8])
-def test_sequence_shards_fp32_match_unsharded(P_):
+def test_sequence_shards_fp32_match_unsharded(orc, P_):
     NL, B, H, G, d, seq, k = 4, 1, 2, 4, 64, 4096, 256
     roles = roles_for(NL, H, [(2, 1)])
     q, K, V, full, ref_out, ref_sets, decs, outs, gsets = _run(
@@ -62,10 +78,11 @@ def test_sequence_shards_fp32_match_unsharded(P_):
     for g in range(H):
         l = _last_retrieval(roles, g)
         np.testing.assert_array_equal(g0[l, g, :k], ref_sets[0][g])
+    _vs_oracle(orc, q, K, V, roles, seq, k, d, outs[0], gsets, FP32_TOL)
 
 
 @pytest.mark.parametrize("P_", [2, 8])
-def test_sequence_shards_bf16_llama_like(P_):
+def test_sequence_shards_bf16_llama_like(orc, P_):
     NL, B, H, G, d, seq, k = 3, 2, 8, 4, 128, 16384, 1024
     roles = roles_for(NL, H, [(1, 3), (2, 5), (2, 0)])
     q, K, V, full, ref_out, ref_sets, decs, outs, gsets = _run(
@@ -79,6 +96,7 @@ def test_sequence_shards_bf16_llama_like(P_):
         for g in range(H):
             l = _last_retrieval(roles, g)
             np.testing.assert_array_equal(g0[l, b * H + g, :k], ref_sets[b][g])
+    _vs_oracle(orc, q, K, V, roles, seq, k, d, outs[0], gsets, BF16_TOL)
 
 
 def test_sequence_shard_local_sets_partition_the_global_set():
