@@ -5,27 +5,38 @@
                     [--select tokens|blocks]
 
 A STEP is one decode step of hybrid-head attention over ALL layers
-(decode_engine.hpp:109-151): per layer the pooled split-KV attention kernel
-(retrieval + sparse heads), the split-KV merge and the cluster top-k into the
-per-head index cache, in layer order, CUDA-graph replayed.  Inputs (q, K/V
-caches, 17 GiB at 128K) are resident in HBM and far larger than the 126 MB L2,
-so no flush is needed between steps.
+(decode_engine.hpp:109-151): per layer the retrieval heads' dense split-KV
+attention with the fused pooled-query scoring, the sparse heads' attention over
+the index sets of earlier layers, the split-KV merge and the top-k selection
+into the per-head index cache -- one launch of the persistent step kernel,
+CUDA-graph replayed.  Default workload: BASELINE's 128K single-GPU config
+(Qwen3-8B shapes, 36 layers).  Inputs (q, K/V caches, 19 GiB at 128K) are
+resident in HBM and far larger than the 126 MB L2, so no flush is needed.
 
 value     : device time per decode step in us (= us/token at batch 1), max over
             ranks, CUDA events around exactly K replays.
-e2e       : the same step through the public C-ABI call (HybridDecoder.decode_step,
-            eager) with the step's inputs copied from pinned host memory (q of
-            every layer + the new token's K/V row of every layer) and the
-            attention outputs copied back, all inside the timed region.
-roofline  : dominant kernel = hybrid_attn_kernel; achieved = its algorithmic
-            bytes (K/V rows touched + Q + O) / its CUDA-event
-            duration, measured inside the graph on the launching stream.
-cpu_baseline / --impl reference : the reference's own CPU operator
-            hh::kernel::run<float> (kernel_sim.hpp:237-279, oracle/_ref built from
-            the reference headers) on a bounded sample (one layer of the
-            workload's dominant role pattern), extrapolated by block count.
+e2e       : token after token through the public C-ABI call
+            (HybridDecoder.decode_step, eager): every step uploads q of every
+            layer + the new token's K/V rows from pinned host memory, appends
+            the rows at the growing length (lyc_kv_write), runs the step at
+            seq = t + 1 (device-side re-plan, no host sync) and copies the
+            outputs back, all inside the timed region.
+roofline  : dominant kernel = hybrid_step_kernel (the whole step); achieved =
+            algorithmic bytes (K/V rows touched + q + out + index reads,
+            SURVEY.md 8(d)) / its CUDA-event duration on the launching stream.
+per_layer_api : the same step through lyc_decoder_layer (one launch per layer,
+            the entry a model calls between its own projections).
+selection_swaps : the step kernel's per-layer sets vs an exact f64 top-k.
+cpu_baseline / --impl reference : the reference's own CPU path (oracle/_ref,
+            the unmodified reference headers compiled here): hh::kernel::run<float>
+            for every layer with std::thread workers on all host cores, plus the
+            f64 selection pass of every retrieval head -- whole steps, timed.
 Multi-GPU (torchrun): KV heads are sharded across ranks (index propagation is
-per head index, so no collective is needed on the data path).
+per head index, so the attention needs no collective); the headline for N > 1
+keeps the model's per-layer dependency -- one lyc_decoder_layer launch and one
+all-gather of the layer's [B][Hq][d] outputs per layer, max over ranks.
+--shard seq: KV-sequence sharding with one packed NCCL all-gather of
+partials + top-k candidates per layer.
 """
 from __future__ import annotations
 
@@ -399,6 +410,9 @@ def main():
     ap.add_argument("--no-swaps", action="store_true")
     ap.add_argument("--no-pdl", action="store_true",
                     help="plain stream serialisation of the planner / step launches")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: host-staged, for checking the "
+                         "multi-rank code path with several ranks on one GPU)")
     ap.add_argument("--shard", default="heads", choices=["heads", "seq"],
                     help="multi-GPU split: KV heads (no collective) or KV sequence "
                          "(one packed NCCL all-gather of partials + top-k candidates per layer)")
@@ -419,9 +433,15 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # one rank per GPU; ranks beyond the visible GPUs share them (a protocol
+    # check of the multi-rank code path with --dist-backend gloo on one GPU)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     import paper_2602_04541_b200 as P
 
     if world > 1 and args.shard == "seq":
@@ -457,7 +477,8 @@ def main():
     def allmax(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64,
+                         device=dev if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -498,6 +519,53 @@ def main():
     ms = allmax(ms)
     step_us = ms * 1e3
     step_bytes = dec.step_bytes(L)
+
+    # ---- N > 1, head sharding with the model's per-layer dependency: the
+    # o-projection of layer l needs every head's output, so each layer is one
+    # lyc_decoder_layer launch followed by an all-gather of the [B][Hq][d]
+    # outputs of all ranks (decode_engine.hpp:149-150); layer l+1 starts after
+    # it.  The critical path is sum_l max_p work(l, p).  This is the headline
+    # for N > 1; the independent whole-step time is reported beside it.
+    layer_sync = None
+    head_ms = ms  # the headline step time (N > 1: the layer-synchronous step)
+    if world > 1:
+        hmax = max(len(shard_heads(roles, L, k, world, r)) for r in range(world))
+        send = torch.zeros((B, hmax * G, d), dtype=dt, device=dev)
+        out_s = torch.empty_like(q)
+        staged = args.dist_backend != "nccl"
+        gath = torch.empty((world * B, hmax * G, d), dtype=dt,
+                           device="cpu" if staged else dev)
+
+        def sync_step():
+            for l in range(NL):
+                dec.layer(l, q[l], K, V, L, out_s[l], stream=stream)
+                send[:, :Hr * G].copy_(out_s[l])
+                if staged:
+                    stream.synchronize()
+                    dist.all_gather_into_tensor(gath, send.cpu())
+                else:
+                    dist.all_gather_into_tensor(gath, send)
+
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                sync_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(args.steps):
+                sync_step()
+            e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        barrier()
+        sync_ms = allmax(e0.elapsed_time(e1) / args.steps)
+        layer_sync = {"us_per_token": sync_ms * 1e3 / B, "ms_per_step": sync_ms,
+                      "fused_independent_us_per_token": step_us / B,
+                      "collective": f"all_gather of [B][Hq][d] per layer ({args.dist_backend})",
+                      "heads_per_rank": Hr, "launches_per_step": NL}
+        head_ms = sync_ms
 
     # ---- roofline of the dominant kernel (attention), events inside the graph
     dec.set_timing(True)
@@ -660,13 +728,13 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": step_us / B if B > 1 else step_us,
+            "metric": METRIC, "value": head_ms * 1e3 / B,
             "unit": "us/token", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": False,
+            "ms_per_step": head_ms, "higher_is_better": False,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
             "dtype": wl["dtype"], "data": "synthetic U(-1,1) q/K/V, seeded roles",
             "config": config_of(args, wl),
-            "tokens_per_s": B / (ms / 1e3),
+            "tokens_per_s": B / (head_ms / 1e3),
             "step_hbm_gbs": step_bytes / (ms / 1e3) / 1e9 if world == 1 else None,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
@@ -690,9 +758,10 @@ def main():
                     "fixed_seq_us_per_token": e2e_fixed_ms * 1e3 / B,
                     "growing_vs_fixed": e2e_ms / e2e_fixed_ms},
             "per_layer_api": per_layer,
+            "head_shard_layer_sync": layer_sync,
             "selection_swaps": swaps,
-            "gpu_launches": int(launches_per_step * args.steps),
-            "launches_per_step": int(launches_per_step),
+            "gpu_launches": int((NL if layer_sync else launches_per_step) * args.steps),
+            "launches_per_step": int(NL if layer_sync else launches_per_step),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
