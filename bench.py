@@ -403,6 +403,9 @@ def main():
     ap.add_argument("--workload", default="qwen3-8b-128k", choices=list(WORKLOADS))
     ap.add_argument("--select", default="tokens", choices=["tokens", "blocks"])
     ap.add_argument("--retrieval-frac", type=float, default=0.125)
+    ap.add_argument("--r-per-layer", type=int, default=-1,
+                    help="(diagnostic) exactly this many seeded retrieval heads in every layer "
+                         "above 0, instead of --retrieval-frac")
     ap.add_argument("--top-k", type=int, default=0, help="override the workload's top-k budget")
     ap.add_argument("--seed", type=int, default=2602)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -422,6 +425,11 @@ def main():
     if args.top_k:
         wl["k"] = args.top_k
     roles = make_roles(wl["NL"], wl["H"], args.retrieval_frac, args.seed)
+    if args.r_per_layer >= 0:
+        rng = np.random.default_rng(args.seed)
+        roles[1:] = 1
+        for l in range(1, wl["NL"]):
+            roles[l, rng.choice(wl["H"], size=min(args.r_per_layer, wl["H"]), replace=False)] = 0
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -26,12 +26,21 @@ def main():
     ap.add_argument("--select", default="tokens")
     ap.add_argument("--layers", type=int, default=0)
     ap.add_argument("--save", default="")
+    ap.add_argument("--top-k", type=int, default=0)
+    ap.add_argument("--r-per-layer", type=int, default=-1)
     a = ap.parse_args()
     wl = dict(bench.WORKLOADS[a.workload])
     if a.layers:
         wl["NL"] = a.layers
     NL, H, G, d, L, k, B = (wl[x] for x in ("NL", "H", "G", "d", "L", "k", "B"))
+    if a.top_k:
+        k = a.top_k
     roles = bench.make_roles(NL, H, 0.125, 2602)
+    if a.r_per_layer >= 0:
+        rng = np.random.default_rng(2602)
+        roles[1:] = 1
+        for l in range(1, NL):
+            roles[l, rng.choice(H, size=min(a.r_per_layer, H), replace=False)] = 0
     dt = torch.bfloat16 if wl["dtype"] == "bf16" else torch.float32
     K = torch.empty((NL, B, H, L, d), dtype=dt, device="cuda")
     V = torch.empty_like(K)
@@ -42,6 +51,7 @@ def main():
     dec = P.HybridDecoder(n_layers=NL, batch=B, n_kv_heads=H, group_size=G, d_head=d, seq_cap=L,
                           roles=roles, policy=P.SparsityPolicy.top_k(k), dtype=dt, select=a.select)
     assert dec.fused, "timeline needs the fused step kernel"
+
     for _ in range(3):
         out = dec.decode_step(q, K, V, L)
     dec.set_trace(True)
