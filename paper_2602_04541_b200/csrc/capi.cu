@@ -30,9 +30,10 @@ int64_t window_workspace_bytes(int B, int H, int G, int W, int n_split);
 cudaError_t launch_window_f32(const void* q, const void* k, const void* v, int layer, int B, int H,
                               int G, int d, int64_t cap, int64_t start, int W, float scale,
                               void* out, cudaStream_t st);
-cudaError_t launch_window(const void* q, const void* k, const void* v, int L, int layer, int B,
-                          int H, int G, int d, int64_t cap, int64_t start, int W, float scale,
-                          float* workspace, int n_split, void* out, cudaStream_t st);
+cudaError_t launch_window_tc(const CUtensorMap& tmap_k, const CUtensorMap& tmap_v, const void* q,
+                             int layer, int B, int H, int G, int d, int64_t start, int W,
+                             float scale, float* workspace, int n_split, void* out,
+                             cudaStream_t st);
 int topk_cluster_size(int n, int max_slice);
 size_t topk_smem_bytes(int slice);
 cudaError_t launch_float_keys(const float* s, uint32_t* keys, int64_t n, cudaStream_t st);
@@ -262,6 +263,35 @@ void encode_kv_maps(LycAttnParams& ap, const void* k, const void* v, int64_t row
                         bf16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(LYC_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  }
+}
+
+// 3-D TMA views of one cache for the window attention: {d, rows, slabs} with
+// the row extent cut at the live length (rows past it load as zeros), box
+// {64 columns, 64 rows, 1 slab}, 128B swizzle.
+void encode_window_maps(CUtensorMap* mk, CUtensorMap* mv, const void* k, const void* v,
+                        int64_t slabs, int64_t rows, int64_t cap, int D) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cuda_check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q),
+               "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
+    if (q != cudaDriverEntryPointSuccess || !fn) fail(LYC_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  if (rows >= ((int64_t)1 << 31) || slabs >= ((int64_t)1 << 31)) fail(LYC_ENOTSUP, "window: cache too large");
+  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)rows, (cuuint64_t)slabs};
+  cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)cap * D * 2};
+  cuuint32_t box[3] = {64u, 64u, 1u};
+  cuuint32_t estr[3] = {1, 1, 1};
+  const void* ptrs[2] = {k, v};
+  CUtensorMap* maps[2] = {mk, mv};
+  for (int i = 0; i < 2; ++i) {
+    CUresult r = encode(maps[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptrs[i]), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(LYC_ECUDA, "cuTensorMapEncodeTiled (window) failed (" + std::to_string((int)r) + ")");
   }
 }
 
@@ -1893,10 +1923,12 @@ int lyc_kv_write(void* k_cache, void* v_cache, const lyc_kv_layout* lay, int32_t
 
 // ------------------------------------------------------------ cache correction
 namespace {
+// key splits per (b, g, 128-row block): about one CTA per SM (the tensor-core
+// kernel holds a whole SM); clamped to the key tiles at launch
 int window_splits(const lyc_kv_layout* lay, int32_t group_size, int32_t window) {
   const int rows = window * group_size, rb = (rows + 127) / 128;
   const int ctas = lay->batch * lay->n_kv_heads * rb;
-  return std::max(1, (2 * num_sms() + ctas - 1) / ctas);
+  return std::max(1, num_sms() / ctas);
 }
 void window_validate(const lyc_kv_layout* lay, int32_t group_size, int32_t window) {
   if (!lay) fail(LYC_EINVAL, "window: null layout");
@@ -1939,10 +1971,12 @@ int lyc_window_attention(const lyc_kv_layout* lay, int32_t layer, const void* k_
       ++g_launches;
       return LYC_OK;
     }
-    cuda_check(lyc::launch_window(q, k_cache, v_cache, lay->n_layers, layer, lay->batch,
-                                  lay->n_kv_heads, group_size, lay->d_head, lay->seq_cap, start,
-                                  window, sc, static_cast<float*>(workspace), ns, out,
-                                  (cudaStream_t)stream),
+    CUtensorMap mk, mv;
+    encode_window_maps(&mk, &mv, k_cache, v_cache, (int64_t)lay->n_layers * lay->batch * lay->n_kv_heads,
+                       start + window, lay->seq_cap, lay->d_head);
+    cuda_check(lyc::launch_window_tc(mk, mv, q, layer, lay->batch, lay->n_kv_heads, group_size,
+                                     lay->d_head, start, window, sc, static_cast<float*>(workspace),
+                                     ns, out, (cudaStream_t)stream),
                "window launch");
     g_launches += 2;
     return LYC_OK;

@@ -110,6 +110,9 @@ def test_decode_over_appended_cache_matches_prefilled():
 @pytest.mark.parametrize("d,G,W,start,dtype", [(128, 4, 32, 3000, torch.bfloat16),
                                                 (64, 8, 16, 1000, torch.bfloat16),
                                                 (128, 4, 5, 70, torch.bfloat16),
+                                                (128, 4, 64, 3977, torch.bfloat16),
+                                                (64, 8, 32, 1, torch.bfloat16),
+                                                (128, 1, 3, 4000, torch.bfloat16),
                                                 (64, 4, 8, 500, torch.float32)])
 def test_correction_attention_vs_oracle(orc, d, G, W, start, dtype):
     """decode_engine.hpp:164-204 attention part: after the window's rows are
