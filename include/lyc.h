@@ -330,6 +330,20 @@ int lyc_window_attention(const lyc_kv_layout* layout, int32_t layer, const void*
                          int32_t window, const void* q, void* out, void* workspace,
                          int64_t workspace_bytes, void* stream);
 
+/* Index-set refresh of cache correction (decode_engine.hpp:190-197,
+ * refresh_sets_on_correction): every KV head's set is re-selected from the
+ * pooled query (gqa_pool_queries, attention.hpp:127-146) of the LAST window
+ * position against keys [0, len) of `layer`, with the decoder's policy
+ * (select_tokens on the dense-attention weights, policy.hpp:64-104), into the
+ * decoder's index cache (sets_ of every (b, g)).  q_last: device [B][Hq][d],
+ * that position's queries at `layer`; k: the decoder's K cache
+ * [n_layers][B][H][seq_cap][d].  The reference refreshes at every layer of the
+ * window pass, each layer overwriting sets_, so the state it leaves is this
+ * call for its last layer.  Stream-ordered; allocates its key scratch on the
+ * first call only. */
+int lyc_decoder_refresh_sets(lyc_decoder* dec, int32_t layer, const void* q_last, const void* k,
+                             int64_t len, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Test hook: the device planner (run sequentially on the host) against the
  * host-order planner for a decoder configuration and lengths (seq_lens: host

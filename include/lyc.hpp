@@ -562,6 +562,12 @@ class HybridDecoder {
                     void* out_l, cudaStream_t st = nullptr) {
     check(lyc_decoder_layer(d_, layer, q_l, k, v, (int64_t)seq_len, out_l, st));
   }
+  // cache_correction's set refresh (decode_engine.hpp:190-197): every KV head's
+  // set re-selected from the last window position's pooled query at `layer`.
+  void refresh_sets(int layer, const void* q_last, const void* k, std::size_t len,
+                    cudaStream_t st = nullptr) {
+    check(lyc_decoder_refresh_sets(d_, layer, q_last, k, (int64_t)len, st));
+  }
   // CUDA-graph capture of decode_step for fixed pointers / seq_len, then replay.
   void capture(const void* q, const void* k, const void* v, std::size_t seq_len, void* out,
                cudaStream_t st) {

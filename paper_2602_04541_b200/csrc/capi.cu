@@ -35,6 +35,9 @@ cudaError_t launch_window_tc(const CUtensorMap& tmap_k, const CUtensorMap& tmap_
                              float scale, float* workspace, int n_split, void* out,
                              cudaStream_t st);
 int topk_cluster_size(int n, int max_slice);
+cudaError_t launch_refresh_scores(const void* q, const void* k_layer, int64_t cap, int B, int H,
+                                  int G, int d, int dtype, int64_t len, uint32_t* keys,
+                                  int64_t key_stride, int blocks, cudaStream_t st);
 size_t topk_smem_bytes(int slice);
 cudaError_t launch_float_keys(const float* s, uint32_t* keys, int64_t n, cudaStream_t st);
 cudaError_t launch_step(const LycStepParams& p, int dtype, int d, cudaStream_t st, bool pdl);
@@ -546,6 +549,8 @@ struct lyc_decoder {
   int32_t* idx = nullptr;       // [B*H][k_cap]
   int32_t* idx_count = nullptr;
   uint32_t* sel_keys = nullptr; // [2][B*H][sel_stride]
+  uint32_t* refresh_keys = nullptr;  // [B*H][sel_stride] (lyc_decoder_refresh_sets, lazily)
+  int32_t* ident_rows = nullptr;     // [B*H] 0..B*H-1 (lazily)
   int64_t sel_stride = 0;
   uint32_t* hist = nullptr;     // [2][B*H][LYC_H1_BINS] fused first-pass histograms
   uint32_t* sel_bitmap = nullptr;  // fused-mode pooled selection scratch (see LycStepParams)
@@ -1350,6 +1355,8 @@ int lyc_decoder_destroy(lyc_decoder* d) {
   free_dev(d->idx);
   free_dev(d->idx_count);
   free_dev(d->sel_keys);
+  free_dev(d->refresh_keys);
+  free_dev(d->ident_rows);
   free_dev(d->hist);
   free_dev(d->sel_bitmap);
   free_dev(d->sel_cand);
@@ -1979,6 +1986,71 @@ int lyc_window_attention(const lyc_kv_layout* lay, int32_t layer, const void* k_
                                      ns, out, (cudaStream_t)stream),
                "window launch");
     g_launches += 2;
+    return LYC_OK;
+  });
+}
+
+// ------------------------------------------------------------ set refresh
+int lyc_decoder_refresh_sets(lyc_decoder* d, int32_t layer, const void* q_last, const void* k,
+                             int64_t len, void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "refresh: null decoder");
+    if (layer < 0 || layer >= d->NL) fail(LYC_EINVAL, "refresh: layer out of range");
+    if (!q_last || !k) fail(LYC_EINVAL, "refresh: null buffer");
+    if (len < 1 || len > d->cfg.seq_cap) fail(LYC_EINVAL, "refresh: len must be in [1, seq_cap]");
+    if (d->cfg.select_mode == LYC_SELECT_NONE) fail(LYC_ESTATE, "refresh: the decoder selects nothing");
+    if (d->shard) fail(LYC_ENOTSUP, "refresh: not in sequence-shard mode");
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t rows = (size_t)d->B * d->H;
+    if (!d->refresh_keys) {
+      cuda_check(cudaMalloc(&d->refresh_keys, rows * d->sel_stride * 4), "cudaMalloc refresh keys");
+      cuda_check(cudaMalloc(&d->ident_rows, rows * 4), "cudaMalloc rows");
+      std::vector<int32_t> id(rows);
+      for (size_t i = 0; i < rows; ++i) id[i] = (int32_t)i;
+      cuda_check(cudaMemcpy(d->ident_rows, id.data(), rows * 4, cudaMemcpyHostToDevice), "H2D rows");
+    }
+    const bool blocks = d->cfg.select_mode == LYC_SELECT_BLOCKS;
+    const int64_t n = blocks ? (len + d->bs - 1) / d->bs : len;
+    if (blocks) cuda_check(cudaMemsetAsync(d->refresh_keys, 0, rows * d->sel_stride * 4, st), "memset keys");
+    const int esz = d->cfg.dtype == LYC_DTYPE_BF16 ? 2 : 4;
+    const char* k_layer = static_cast<const char*>(k) + (size_t)layer * rows * d->cfg.seq_cap * d->D * esz;
+    cuda_check(lyc::launch_refresh_scores(q_last, k_layer, d->cfg.seq_cap, d->B, d->H, d->G, d->D,
+                                          d->cfg.dtype == LYC_DTYPE_BF16 ? 1 : 0, len,
+                                          d->refresh_keys, d->sel_stride, blocks ? 1 : 0, st),
+               "refresh launch");
+    ++g_launches;
+    if (d->variable_sets()) {  // TopP / Threshold (policy.hpp:73-101)
+      LycPolicyParams pp{};
+      pp.keys = d->refresh_keys;
+      pp.key_stride = d->sel_stride;
+      pp.n = (int32_t)n;
+      pp.kind = d->cfg.policy_kind == LYC_POLICY_TOPP ? LYC_POLICY_KIND_TOPP : LYC_POLICY_KIND_THRESHOLD;
+      pp.value = d->cfg.ratio;
+      pp.score_scale = d->cfg.scale;  // keys are pooled-mean scores
+      pp.out = d->idx;
+      pp.out_row = d->ident_rows;
+      pp.out_stride = d->k_cap;
+      pp.out_count = d->idx_count;
+      pp.row_n = nullptr;
+      cuda_check(lyc::launch_policy(pp, (int)rows, st), "policy launch");
+    } else {  // TopK / Ratio (policy.hpp:57-72)
+      const int cluster = lyc::topk_cluster_size((int)n, 16384);
+      LycTopkParams tp{};
+      tp.keys = d->refresh_keys;
+      tp.key_stride = d->sel_stride;
+      tp.n = (int32_t)n;
+      tp.k = (int32_t)d->budget(len);
+      tp.out = d->idx;
+      tp.out_row = d->ident_rows;
+      tp.out_stride = d->k_cap;
+      tp.out_count = d->idx_count;
+      tp.slice = (int32_t)((n + cluster - 1) / cluster);
+      tp.clear_keys = 0;
+      tp.row_n = nullptr;
+      tp.row_k = nullptr;
+      cuda_check(lyc::launch_topk(tp, (int)rows, cluster, st), "topk launch");
+    }
+    ++g_launches;
     return LYC_OK;
   });
 }

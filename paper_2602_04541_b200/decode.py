@@ -195,6 +195,13 @@ class HybridDecoder:
                                       self._stream(stream)))
         return out_l
 
+    def refresh_sets(self, layer: int, q_last, k_cache, length: int, *, stream=None):
+        """Cache-correction set refresh (decode_engine.hpp:190-197): re-select
+        every KV head's index set from the pooled query of the last window
+        position (q_last [B][Hq][d] at `layer`) over keys [0, length)."""
+        check(lib().lyc_decoder_refresh_sets(self._h, layer, q_last.data_ptr(), k_cache.data_ptr(),
+                                             int(length), self._stream(stream)))
+
     def capture(self, q, k_cache, v_cache, seq_len: int, out, *, stream=None):
         """Capture one step into a CUDA graph (fixed pointers and seq_len)."""
         if isinstance(seq_len, (int, np.integer)):

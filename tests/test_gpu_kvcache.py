@@ -147,3 +147,54 @@ def test_correction_attention_vs_oracle(orc, d, G, W, start, dtype):
                                              Vn[b, hd // G, : p + 1], scale)
                 worst = max(worst, np.abs(on[b, i, hd] - ref).max() / max(np.abs(ref).max(), 1e-3))
     assert worst < (2e-2 if dtype == torch.bfloat16 else 1e-5), worst
+
+
+@pytest.mark.parametrize("dtype,d,G,H,B,L,policy,select", [
+    (torch.float32, 64, 4, 2, 1, 4096, ("topk", 256), "tokens"),
+    (torch.bfloat16, 128, 4, 8, 2, 5000, ("topk", 512), "tokens"),
+    (torch.bfloat16, 128, 4, 4, 1, 3000, ("ratio", 0.9), "tokens"),
+    (torch.float32, 64, 4, 2, 1, 2000, ("topp", 0.5), "tokens"),
+    (torch.float32, 64, 4, 2, 1, 2000, ("threshold", 0.001), "tokens"),
+    (torch.bfloat16, 128, 4, 4, 2, 6000, ("topk", 1024), "blocks"),
+])
+def test_refresh_sets_vs_oracle(orc, dtype, d, G, H, B, L, policy, select):
+    """decode_engine.hpp:190-197: after correction, each KV head's set is
+    select_tokens(policy, dense_attention(pooled q of the last window
+    position, K[:len]).weights) -- the device refresh against the oracle
+    (sets exact except documented fp ties; block mode: the composed
+    block-max top-k of the oracle)."""
+    import paper_2602_04541_b200 as P
+    from tests.test_gpu_decode import check_policy_set, check_set
+    NL, cap, layer = 2, L + 64, 1
+    kind, val = policy
+    pol = {"topk": lambda: P.SparsityPolicy.top_k(val), "ratio": lambda: P.SparsityPolicy.ratio(val),
+           "topp": lambda: P.SparsityPolicy.top_p(val),
+           "threshold": lambda: P.SparsityPolicy.threshold(val)}[kind]()
+    roles = np.ones((NL, H), np.uint8)
+    roles[0] = 0
+    dec = P.HybridDecoder(n_layers=NL, batch=B, n_kv_heads=H, group_size=G, d_head=d, seq_cap=cap,
+                          roles=roles, policy=pol, dtype=dtype, select=select)
+    g = torch.Generator(device="cuda").manual_seed(21)
+    K = (torch.rand((NL, B, H, cap, d), generator=g, device="cuda") * 2 - 1).to(dtype)
+    q = (torch.rand((B, H * G, d), generator=g, device="cuda") * 2 - 1).to(dtype)
+    dec.refresh_sets(layer, q, K, L)
+    torch.cuda.synchronize()
+    sets = dec.token_sets()
+    Kn, qn = K[layer].float().cpu().numpy(), q.float().cpu().numpy()
+    scale = 1 / np.sqrt(d)
+    for b in range(B):
+        pooled = orc.gqa_pool_queries(qn[b], G)
+        for hg in range(H):
+            if select == "blocks":
+                nblk = min((val + 63) // 64, (L + 63) // 64)
+                ref = orc.block_select(pooled[hg], Kn[b, hg], L, scale, 64, nblk)
+                np.testing.assert_array_equal(sets[b][hg], ref)
+                continue
+            _, w = orc.dense_attention(pooled[hg], Kn[b, hg, :L], Kn[b, hg, :L], scale)
+            k = val if kind == "topk" else 1
+            ref = orc.select_tokens(kind, w, k=k, value=0.0 if kind == "topk" else val)
+            scores = Kn[b, hg, :L].astype(np.float64) @ pooled[hg]
+            if kind in ("topk", "ratio"):
+                check_set(sets[b][hg], ref, scores, len(ref))
+            else:
+                check_policy_set(sets[b][hg], ref, w, kind, val)
