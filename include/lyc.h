@@ -174,8 +174,12 @@ int lyc_decoder_status(lyc_decoder* dec, void* stream);
  * the full caches.  Layers must be issued in order within a step, the model's
  * own projections in between (q of layer l+1 depends on layer l's output).
  * On the step kernel this is ONE launch of the persistent step kernel over
- * [layer, layer + 1) -- attention, split-KV merge and the layer's selection --
- * plus the device planner at layer 0 (or when seq_len changes). */
+ * [layer, layer + 1) -- attention and split-KV merge of the layer, and the
+ * PREVIOUS layer's selection (deferred into this launch, LYC_TUNE_DEFER_SELECTION;
+ * the last layer selects in its own launch) -- plus the device planner at
+ * layer 0 (or when seq_len changes).  out_l is final when the call's work
+ * completes; the layer's index sets when the next layer's does (or after
+ * lyc_decoder_sync_sets). */
 int lyc_decoder_layer(lyc_decoder* dec, int32_t layer, const void* q_l, const void* k,
                       const void* v, int64_t seq_len, void* out_l, void* stream);
 
@@ -197,7 +201,11 @@ int lyc_decoder_capture_dev(lyc_decoder* dec, const void* q, const void* k, cons
 int lyc_decoder_replay(lyc_decoder* dec, void* stream);
 
 /* The device index cache: ids [B*H][k_cap] int32 (ascending token ids, or
- * block ids in blocks mode), counts [B*H] int32. */
+ * block ids in blocks mode), counts [B*H] int32.  After per-layer calls the
+ * selection of the last layer issued may still be pending (it runs with the
+ * next layer's launch): lyc_decoder_sync_sets completes it in `stream`
+ * (every other entry point does so itself). */
+int lyc_decoder_sync_sets(lyc_decoder* dec, void* stream);
 int lyc_decoder_index_cache(lyc_decoder* dec, int32_t** ids, int32_t** counts, int64_t* k_cap);
 
 /* Number of kernel launches one step issues (for the bench's gpu_launches). */
@@ -233,6 +241,10 @@ int lyc_decoder_is_fused(lyc_decoder* dec);
 #define LYC_TUNE_RING_STAGES 1
 #define LYC_TUNE_PER_LAYER_KERNELS 2
 #define LYC_TUNE_PDL 3  /* 1 (default) = programmatic dependent launch of planner / step kernels */
+/* 1 (default): with per-layer calls (lyc_decoder_layer) a layer's selection
+ * runs in the NEXT layer's launch, beside its attention (only the units that
+ * read those sets wait for it) instead of at the tail of its own launch */
+#define LYC_TUNE_DEFER_SELECTION 4
 int lyc_decoder_tune(lyc_decoder* dec, int32_t what, int64_t value);
 
 /* Step timeline (fused mode): when enabled, the step kernel stamps

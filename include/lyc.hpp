@@ -587,6 +587,8 @@ class HybridDecoder {
     int64_t kcap = 0;
     check(lyc_decoder_index_cache(d_, &ids, &counts, &kcap));
     cuda_check(cudaDeviceSynchronize(), "sync");
+    check(lyc_decoder_sync_sets(d_, nullptr));  // a selection deferred by decode_layer
+    cuda_check(cudaDeviceSynchronize(), "sync");
     const std::size_t rows = (std::size_t)cfg_.batch * cfg_.n_kv_heads;
     std::vector<int32_t> n(rows), all(rows * (std::size_t)kcap);
     cuda_check(cudaMemcpy(n.data(), counts, rows * 4, cudaMemcpyDeviceToHost), "D2H");

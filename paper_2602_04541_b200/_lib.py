@@ -27,10 +27,10 @@ SYMBOLS = [
     "lyc_window_attention", "lyc_decoder_step_varlen", "lyc_decoder_capture_varlen",
     "lyc_decoder_set_trace_sets", "lyc_decoder_traced_sets", "lyc_decoder_step_dev",
     "lyc_decoder_capture_dev", "lyc_decoder_status", "lyc_decoder_tune", "lyc_kv_append_dev",
-    "lyc_plan_selftest", "lyc_decoder_refresh_sets",
+    "lyc_plan_selftest", "lyc_decoder_refresh_sets", "lyc_decoder_sync_sets",
 ]
 
-TUNE_RING_STAGES, TUNE_PER_LAYER_KERNELS, TUNE_PDL = 1, 2, 3
+TUNE_RING_STAGES, TUNE_PER_LAYER_KERNELS, TUNE_PDL, TUNE_DEFER_SELECTION = 1, 2, 3, 4
 
 
 class LycError(RuntimeError):
@@ -118,6 +118,8 @@ def lib() -> C.CDLL:
     L.lyc_decoder_capture_varlen.argtypes = [vp, vp, vp, vp, C.POINTER(C.c_int64), vp, vp]
     L.lyc_decoder_layer.restype = C.c_int
     L.lyc_decoder_layer.argtypes = [vp, i32, vp, vp, vp, i64, vp, vp]
+    L.lyc_decoder_sync_sets.restype = C.c_int
+    L.lyc_decoder_sync_sets.argtypes = [vp, vp]
     L.lyc_decoder_refresh_sets.restype = C.c_int
     L.lyc_decoder_refresh_sets.argtypes = [vp, i32, vp, vp, i64, vp]
     L.lyc_decoder_capture.restype = C.c_int

@@ -562,6 +562,9 @@ struct lyc_decoder {
   int64_t rowctr_set = 0;
   int stages = 0;               // attention ring stages in use (0 = all; lyc_decoder_tune)
   bool pdl = true;              // programmatic dependent launch of planner / step kernels
+  bool defer_sel = true;        // per-layer launches: a layer's selection runs in the next launch
+  int pending_sel = -1;         // layer whose selection was deferred to the next launch (-1: none)
+  int64_t pending_seq = 0;      //   at this length
   uint32_t* ctr = nullptr;      // LYC_CTR_WORDS(NL)
   unsigned long long* trace = nullptr;  // optional step timeline [NL][LYC_TRACE_EVENTS][n_ctas]
   int32_t* set_trace = nullptr;        // optional per-layer sets [NL][B*H][k_cap] (fused path)
@@ -1104,7 +1107,8 @@ void ensure_plan(lyc_decoder* d, int64_t seq, const int64_t* lens, const int64_t
 // (dlens); the kernel re-plans itself when they change its plan key.
 void launch_step_range(lyc_decoder* d, int l0, int l1, const void* q, const void* k,
                        const void* v, void* out, cudaStream_t st, int64_t seq,
-                       const int64_t* lens, const int64_t* dlens) {
+                       const int64_t* lens, const int64_t* dlens, bool defer_in = false,
+                       bool defer_out = false) {
   ensure_maps(d, k, v);
   LycStepParams p;
   std::memset(&p, 0, sizeof(p));
@@ -1150,6 +1154,8 @@ void launch_step_range(lyc_decoder* d, int l0, int l1, const void* q, const void
   p.scale = d->cfg.scale;
   p.scale_log2 = d->cfg.scale * 1.4426950408889634f;
   p.stages = d->stages;
+  p.sel_defer_in = defer_in ? 1 : 0;
+  p.sel_defer_out = defer_out ? 1 : 0;
   p.plan = d->pin;
   p.plan.seq = seq;
   p.plan.dlens = dlens;
@@ -1158,16 +1164,34 @@ void launch_step_range(lyc_decoder* d, int l0, int l1, const void* q, const void
     for (int b = 0; b < d->B; ++b) p.plan.lens[b] = (int32_t)lens[b];
   const bool per_layer = d->NL > 1 && l1 - l0 == 1;
   const size_t ev = per_layer ? (size_t)l0 : 0;
-  if (d->timing) d->timed_per_layer = per_layer;
-  record(d, d->ev_pre, ev, st);
+  if (d->timing && l1 > l0) d->timed_per_layer = per_layer;
+  if (l1 > l0) record(d, d->ev_pre, ev, st);
   cuda_check(lyc::launch_step(p, d->cfg.dtype, d->D, st, d->pdl), "step launch");
-  record(d, d->ev_post, ev, st);
+  if (l1 > l0) record(d, d->ev_post, ev, st);
   ++g_launches;
+}
+
+bool layer_selects(const lyc_decoder* d, int l) {
+  if (d->cfg.select_mode == LYC_SELECT_NONE) return false;
+  for (int g = 0; g < d->H; ++g)
+    if (d->retrieval(l, g)) return true;
+  return false;
+}
+
+// Completes a selection deferred by the last per-layer launch: a launch over
+// no layers that runs only that selection (at the length it was made for).
+void flush_pending(lyc_decoder* d, cudaStream_t st) {
+  if (d->pending_sel < 0) return;
+  const int l = d->pending_sel + 1;
+  d->pending_sel = -1;
+  launch_step_range(d, l, l, nullptr, d->map_k, d->map_v, nullptr, st, d->pending_seq, nullptr,
+                    nullptr, true, false);
 }
 
 void decoder_step(lyc_decoder* d, const void* q, const void* k, const void* v, int64_t seq,
                   void* out, cudaStream_t st, const int64_t* lens = nullptr,
                   const int64_t* dlens = nullptr) {
+  flush_pending(d, st);
   if (d->fused) {
     if (!dlens) validate_lens(d, seq, lens);
     ensure_plan(d, seq, lens, dlens, st);
@@ -1425,8 +1449,17 @@ int lyc_decoder_layer(lyc_decoder* d, int32_t layer, const void* q_l, const void
       int64_t seq = seq_len;
       const int64_t* lens = nullptr;
       validate_lens(d, seq, lens);
+      // a selection deferred by the previous launch runs in this one when this
+      // is the next layer at the same length; otherwise it is completed first
+      if (d->pending_sel >= 0 && (d->pending_sel != layer - 1 || d->pending_seq != seq))
+        flush_pending(d, st);
+      const bool defer_in = d->pending_sel >= 0;
+      const bool defer_out = d->defer_sel && layer + 1 < d->NL && layer_selects(d, layer);
       ensure_plan(d, seq, nullptr, nullptr, st);
-      launch_step_range(d, layer, layer + 1, q_l, k, v, out_l, st, seq, nullptr, nullptr);
+      launch_step_range(d, layer, layer + 1, q_l, k, v, out_l, st, seq, nullptr, nullptr, defer_in,
+                        defer_out);
+      d->pending_sel = defer_out ? layer : -1;
+      d->pending_seq = seq;
       return LYC_OK;
     }
     decoder_plan(d, seq_len, nullptr, st);
@@ -1608,6 +1641,7 @@ int64_t decoder_capture(lyc_decoder* d, const void* q, const void* k, const void
     // graph reads the fixed plan layout; replay re-plans to these lengths if
     // another length was planned since).  Fused path: the graph holds the
     // device planner, so every replay plans its own lengths.
+    flush_pending(d, st);  // outside the graph
     if (!d->fused) decoder_plan(d, seq_len, lens, st);
     else if (!dlens) ensure_plan(d, seq, vl, nullptr, st);  // outside the graph
     ensure_maps(d, k, v);
@@ -1668,6 +1702,7 @@ int lyc_decoder_replay(lyc_decoder* d, void* stream) {
   return (int)guarded([&]() -> int64_t {
     if (!d || !d->exec) fail(LYC_ESTATE, "decoder: no captured step");
     cudaStream_t st = (cudaStream_t)stream;
+    flush_pending(d, st);
     const bool varlen = d->captured_lens.size() == (size_t)d->B && d->captured_seq == 0;
     if (!d->fused && d->plan_gen != d->captured_gen) {
       // another length was planned since the capture: restore the captured plan
@@ -1684,6 +1719,14 @@ int lyc_decoder_replay(lyc_decoder* d, void* stream) {
     }
     cuda_check(cudaGraphLaunch(d->exec, st), "graph launch");
     g_launches += d->captured_launches;
+    return LYC_OK;
+  });
+}
+
+int lyc_decoder_sync_sets(lyc_decoder* d, void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    if (!d) fail(LYC_EINVAL, "decoder: null");
+    flush_pending(d, (cudaStream_t)stream);
     return LYC_OK;
   });
 }
@@ -1804,6 +1847,9 @@ int lyc_decoder_tune(lyc_decoder* d, int32_t what, int64_t value) {
       case LYC_TUNE_PDL:
         d->pdl = value != 0;
         return LYC_OK;
+      case LYC_TUNE_DEFER_SELECTION:
+        d->defer_sel = value != 0;
+        return LYC_OK;
       default:
         fail(LYC_EINVAL, "tune: unknown knob");
     }
@@ -1852,6 +1898,10 @@ int64_t lyc_decoder_traced_sets(lyc_decoder* d, int32_t* ids, int32_t* counts, i
     if (!ids) return d->k_cap;  // size query: ids hold [rows][k_cap]
     if (cap < rows * d->k_cap) fail(LYC_EINVAL, "decoder: set trace buffer too small");
     cuda_check(cudaDeviceSynchronize(), "sync");
+    if (d->pending_sel >= 0) {  // a deferred selection (per-layer launches) completes first
+      flush_pending(d, nullptr);
+      cuda_check(cudaDeviceSynchronize(), "sync");
+    }
     cuda_check(cudaMemcpy(ids, d->set_trace, (size_t)rows * d->k_cap * 4, cudaMemcpyDeviceToHost),
                "D2H set trace");
     if (counts)
@@ -2001,6 +2051,7 @@ int lyc_decoder_refresh_sets(lyc_decoder* d, int32_t layer, const void* q_last, 
     if (d->cfg.select_mode == LYC_SELECT_NONE) fail(LYC_ESTATE, "refresh: the decoder selects nothing");
     if (d->shard) fail(LYC_ENOTSUP, "refresh: not in sequence-shard mode");
     cudaStream_t st = (cudaStream_t)stream;
+    flush_pending(d, st);
     const size_t rows = (size_t)d->B * d->H;
     if (!d->refresh_keys) {
       cuda_check(cudaMalloc(&d->refresh_keys, rows * d->sel_stride * 4), "cudaMalloc refresh keys");

@@ -106,7 +106,7 @@ __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* ctr, uint32_t v) 
 __device__ __forceinline__ void epi_bar() { group_bar(2, kEpiThreads); }
 
 // Debug timeline: %globaltimer (ns) of event ev of layer l on CTA `cta`.
-enum { EV_CONS_BEGIN = 0, EV_CONS_END, EV_EPI_ATTN, EV_MERGE, EV_SEL0, EV_SEL1, EV_SEL2, EV_SELDONE,
+enum { EV_CONS_BEGIN = 0, EV_CONS_END, EV_EPI_ATTN, EV_MERGE, EV_SEL0, EV_ENTRY, EV_SEL2, EV_PDL,
        EV_C_PREFIX, EV_C_KEYS, EV_C_DONE, EV_F_PREFIX, EV_F_SCAN, EV_F_EMIT, EV_X0, EV_X1 };
 __device__ __forceinline__ void stamp(const LycStepParams& p, int l, int ev, int cta) {
   if (p.trace) {
@@ -148,8 +148,9 @@ struct StepWaits {
   }
   __device__ __forceinline__ void unit(const LycSlot& s) const {
     // every retrieval head of layer dep finished its selection (a layer of an
-    // earlier launch has: stream order)
-    if (s.dep >= rt->l_begin)
+    // earlier launch has: stream order -- except a selection deferred into
+    // this launch, counted in this launch's set)
+    if (s.dep >= rt->l_begin - p->sel_defer_in)
       wait(LYC_CTR(rt->ctr, s.dep, CTR_SELDONE), seldone_per_step(*p, *rt, s.dep));
   }
   const uint32_t* clayer;  // shared: 1 + the layer this CTA's consumers started
@@ -973,8 +974,10 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
   const AttnSmem<T, D> sm = AttnSmem<T, D>::carve(smem_raw);
   EpiSmem& es = *reinterpret_cast<EpiSmem*>(sm.extra);
   const LycPlanIn& pin = p.plan;
+  if (threadIdx.x == 0) stamp(p, p.l_begin, EV_ENTRY, cta);
   pdl_wait();     // the previous launch of the stream has completed and its writes are visible
   pdl_trigger();  // the next launch in the stream may begin its launch while this one runs
+  if (threadIdx.x == 0) stamp(p, p.l_begin, EV_PDL, cta);
   if (threadIdx.x == 0) {
     s_dyn[0] = (int32_t)__ldcg(ctrl);
     for (int s = 0; s < C::kStages; ++s) {
@@ -1000,6 +1003,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
   rt.seqs = s_seq;
   rt.nsel = s_nsel;
   rt.ksel = s_ksel;
+  if (threadIdx.x == 0) stamp(p, p.l_begin, 17, cta);  // prologue done
   if (cta == 0 && threadIdx.x == 0) p.hdr->status = 0;
   {  // zero the other set for the next launch (nobody uses it in this one)
     uint32_t* oc = p.ctr + (size_t)(par ^ 1) * set_words;
@@ -1080,6 +1084,46 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
     const int chunks = (D + 31) / 32;
     const int items = (rt.n_keys + kItemKeys - 1) / kItemKeys;
     uint32_t bar_phase = 0;
+    // the selection items of layer l: classify every own item, then resolve
+    // the rows and emit the items.  A deferred selection (the previous
+    // layer's, carried into this launch) finds its slots complete already.
+    auto run_items = [&](int l, int n_items, int item_base, bool split_roles, bool deferred) {
+      const LycLayerDesc& L = p.layers[l];
+      uint32_t* slot_ctr = rt.rowctr + (size_t)l * p.max_sel * 16 + 12;
+      const int i0 = cta - item_base, istep = split_roles ? n_items : p.n_ctas;
+      for (int it = i0; it < n_items; it += istep) {
+        const int r = it / items, q = it - r * items;
+        if (et == 0) {  // the row's retrieval slot is complete
+          if (!deferred) {
+            const int slot = __ldg(L.sel_rows + r);
+            spin_until(slot_ctr + (size_t)slot * 16, epoch1 * (uint32_t)L.slots[slot].n_units);
+          }
+          stamp(p, l, EV_EPI_ATTN, cta);
+        }
+        epi_bar();
+        classify_item(p, sel_row(p, rt, l, r), q, es, bar_phase, et, l, cta);
+      }
+      for (int it = i0; it < n_items; it += istep) {
+        const int r = it / items, q = it - r * items;
+        const int row = __ldg(L.sel_rows + r);
+        resolve_emit_item(p, rt, sel_row(p, rt, l, r), q, row, p.idx + (int64_t)row * p.idx_stride,
+                          es, bar_phase, et, l, cta);
+      }
+    };
+    auto layer_items = [&](int l) {
+      const LycLayerDesc& L = p.layers[l];
+      return (L.n_sel > 0 && p.sel_mode != SEL_NONE) ? L.n_sel * items : 0;
+    };
+    if (p.sel_defer_in) {
+      // the previous layer's selection, deferred from the previous launch
+      // (one launch per layer): it runs while this layer's attention streams;
+      // only this layer's units that read its sets wait for it
+      const int l = p.l_begin - 1;
+      const int n_items = layer_items(l);
+      const bool split_roles = n_items > 0 && 2 * n_items <= p.n_ctas;
+      const int item_base = split_roles ? p.n_ctas - n_items : 0;
+      if (n_items > 0 && cta >= item_base) run_items(l, n_items, item_base, split_roles, true);
+    }
     for (int l = p.l_begin; l < p.l_end; ++l) {
       const LycLayerDesc L = p.layers[l];
       // Roles of this layer's epilogue: when the selection items fit in half
@@ -1087,8 +1131,10 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
       // row as soon as its retrieval slot's units are all done (per-row unit
       // counter; retrieval units come first in every split) -- without waiting
       // for the rest of the layer -- while the other CTAs merge; otherwise
-      // every CTA merges, then classifies.
-      const int n_items = (L.n_sel > 0 && p.sel_mode != SEL_NONE) ? L.n_sel * items : 0;
+      // every CTA merges, then classifies.  The last layer's selection of a
+      // launch with sel_defer_out is left to the next launch.
+      const bool defer = p.sel_defer_out && l == p.l_end - 1;
+      const int n_items = defer ? 0 : layer_items(l);
       const bool split_roles = n_items > 0 && 2 * n_items <= p.n_ctas;
       const int item_base = split_roles ? p.n_ctas - n_items : 0;
       const int merge_ctas = split_roles ? item_base : p.n_ctas;
@@ -1110,30 +1156,12 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
         stamp(p, l, EV_MERGE, cta);
         signal(LYC_CTR(rt.ctr, l, CTR_MERGE));
       }
-      // (b) selection items of this layer's retrieval heads: classify every
-      // own item, then resolve the rows and emit the items
-      if (n_items > 0 && cta >= item_base) {
-        const int i0 = cta - item_base, istep = split_roles ? n_items : p.n_ctas;
-        for (int it = i0; it < n_items; it += istep) {
-          const int r = it / items, q = it - r * items;
-          if (et == 0) {  // the row's retrieval slot is complete
-            const int slot = __ldg(L.sel_rows + r);
-            spin_until(slot_ctr + (size_t)slot * 16, epoch1 * (uint32_t)L.slots[slot].n_units);
-            stamp(p, l, EV_EPI_ATTN, cta);
-          }
-          epi_bar();
-          classify_item(p, sel_row(p, rt, l, r), q, es, bar_phase, et, l, cta);
-        }
-        for (int it = i0; it < n_items; it += istep) {
-          const int r = it / items, q = it - r * items;
-          const int row = __ldg(L.sel_rows + r);
-          resolve_emit_item(p, rt, sel_row(p, rt, l, r), q, row, p.idx + (int64_t)row * p.idx_stride,
-                            es, bar_phase, et, l, cta);
-        }
-      }
+      // (b) selection items of this layer's retrieval heads
+      if (n_items > 0 && cta >= item_base) run_items(l, n_items, item_base, split_roles, false);
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) stamp(p, max(p.l_begin, p.l_end - 1), 19, cta);  // CTA exit
   if (threadIdx.x == 0) {
     const uint32_t done = atomicAdd(ctrl + LYC_CTR_STRIDE, 1u);
     if (done == (uint32_t)p.n_ctas - 1u) {  // last CTA out: the next launch uses the other set

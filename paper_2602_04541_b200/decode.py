@@ -221,8 +221,13 @@ class HybridDecoder:
     def replay(self, *, stream=None):
         check(lib().lyc_decoder_replay(self._h, self._stream(stream)))
 
+    def sync_sets(self, *, stream=None):
+        """Complete a selection deferred by the last per-layer call (in `stream`)."""
+        check(lib().lyc_decoder_sync_sets(self._h, self._stream(stream)))
+
     def index_cache(self):
         """(ids [B*H][k_cap] int32 device view, counts [B*H]) -- the sets_."""
+        self.sync_sets()
         ids, cnt, kcap = C.c_void_p(), C.c_void_p(), C.c_int64()
         check(lib().lyc_decoder_index_cache(self._h, C.byref(ids), C.byref(cnt), C.byref(kcap)))
         rows = self.batch * self.n_kv_heads
