@@ -411,6 +411,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-full", action="store_true")
     ap.add_argument("--no-swaps", action="store_true")
+    ap.add_argument("--no-model", action="store_true",
+                    help="skip the end-to-end toy-model TPOT (hybrid vs full attention)")
     ap.add_argument("--no-pdl", action="store_true",
                     help="plain stream serialisation of the planner / step launches")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -715,6 +717,55 @@ def main():
     h2d = in_h.numel() * esz
     d2h = out_h.numel() * esz
 
+    # ---- end-to-end TPOT of the toy model's decode step:
+    # per layer the Q/K/V GEMV (rmsnorm + rotary + cache append fused), the
+    # attention through lyc_decoder_layer, the output projection and the FFN
+    # GEMVs (lyc_gemv), then the logits -- hybrid vs full attention on the same
+    # weights and cache, each token one CUDA graph replay
+    model_tpot = None
+    if world == 1 and not args.no_model and dt == torch.bfloat16 and B == 1:
+        from paper_2602_04541_b200.model import PRESETS, DecodeModel, ModelConfig
+        preset = "qwen3-8b" if NL == 36 else "llama3-8b"
+        mcfg = ModelConfig(max_seq_len=seq_cap, **PRESETS[preset])
+        if mcfg.n_layers == NL and mcfg.n_kv_heads == Hr and mcfg.d_head == d:
+            dm = DecodeModel(mcfg, roles=r_roles, policy=pol, attention="hybrid", seed=args.seed,
+                             k_cache=K, v_cache=V)
+            res = {}
+            for att in ("hybrid", "full"):
+                dm.set_attention(att)
+                with torch.cuda.stream(stream):
+                    for _ in range(3):
+                        dm.decode_token(7, L - 1, stream=stream)
+                stream.synchronize()
+                gph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gph, stream=stream):
+                    dm.decode_token(7, L - 1, stream=stream)
+                with torch.cuda.stream(stream):
+                    for _ in range(args.warmup):
+                        gph.replay()
+                stream.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                n_rep = max(5, args.steps // 2)
+                with torch.cuda.stream(stream):
+                    e0.record(stream)
+                    for _ in range(n_rep):
+                        gph.replay()
+                    e1.record(stream)
+                e1.synchronize()
+                res[att] = e0.elapsed_time(e1) / n_rep * 1e3
+                del gph
+            wb = dm.weight_bytes()
+            model_tpot = {
+                "model": f"{preset} shapes, toy_model.hpp structure (two-matrix FFN), random bf16 "
+                         f"weights, batch 1, context {L}",
+                "tpot_us_hybrid": res["hybrid"], "tpot_us_full": res["full"],
+                "speedup_hybrid_vs_full": res["full"] / res["hybrid"],
+                "weight_bytes": wb,
+                "launches_per_token": 4 * NL + 1 + NL,
+                "api": "DecodeModel.decode_token: lyc_gemv x (4 per layer + logits) + "
+                       "lyc_decoder_layer per layer, CUDA-graph replayed"}
+            dm.close()
+
     # ---- CPU baseline (rank 0, N == 1): the reference CPU path, whole steps
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -766,6 +817,7 @@ def main():
                     "fixed_seq_us_per_token": e2e_fixed_ms * 1e3 / B,
                     "growing_vs_fixed": e2e_ms / e2e_fixed_ms},
             "per_layer_api": per_layer,
+            "model_tpot": model_tpot,
             "head_shard_layer_sync": layer_sync,
             "selection_swaps": swaps,
             "gpu_launches": int((NL if layer_sync else launches_per_step) * args.steps),

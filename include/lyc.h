@@ -357,6 +357,46 @@ int lyc_decoder_refresh_sets(lyc_decoder* dec, int32_t layer, const void* q_last
                              int64_t len, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * The decode operations around the attention in the reference's toy model
+ * (toy_model.hpp:161-274), for an end-to-end decode step:
+ * one bf16 GEMV kernel (HBM-bound at batch 1) with the vector work fused in.
+ *   y = W . x,  W bf16 [M][K] (row-major per output: the transpose of the
+ *   reference's Matrix [in][out], matvec_f :171-180), x fp32 (the residual
+ *   stream) or bf16 [K]; with `gain` the input is rmsnorm'ed first
+ *   (:161-169, eps default 1e-6).  Epilogues:
+ *   STORE      y = W x (fp32 [M])                      -- output_logits (:269-274)
+ *   RESIDUAL   y += W x (fp32)                         -- attn_project_residual /
+ *                                                          ffn_residual adds (:245-267)
+ *   SILU_BF16  yb = silu(W x) (bf16)                   -- the FFN's W1 (:259-267)
+ *   QKV_ROPE   rows [0, nq*d): q (rotary, :184-194) -> q_out bf16 [nq][d];
+ *              rows [nq*d, (nq+nkv)*d): the token's K rows (rotary), the rest
+ *              its V rows, written to cache row `pos` of KV head g at
+ *              k_cache / v_cache + g * slab_stride (bf16)  -- compute_qkv (:218-240)
+ * K must be a multiple of 8 and <= 49152; W 16-B aligned. */
+#define LYC_GEMV_STORE 0
+#define LYC_GEMV_RESIDUAL 1
+#define LYC_GEMV_SILU_BF16 2
+#define LYC_GEMV_QKV_ROPE 3
+typedef struct lyc_gemv_desc {
+  int64_t M, K;
+  const void* w;          /* bf16 [M][K] */
+  const float* x;         /* fp32 [K], or NULL */
+  const void* xb;         /* bf16 [K], or NULL */
+  const float* gain;      /* rmsnorm gain [K], or NULL */
+  float eps;
+  int32_t mode;           /* LYC_GEMV_* */
+  float* y;               /* STORE / RESIDUAL: fp32 [M] */
+  void* yb;               /* SILU_BF16: bf16 [M] */
+  void* q_out;            /* QKV_ROPE */
+  void* k_cache;
+  void* v_cache;
+  int64_t slab_stride;
+  int32_t nq, nkv, d, pad;
+  int64_t pos;
+} lyc_gemv_desc;
+int lyc_gemv(const lyc_gemv_desc* g, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Test hook: the device planner (run sequentially on the host) against the
  * host-order planner for a decoder configuration and lengths (seq_lens: host
  * [B] or NULL), every layer; LYC_OK when they agree exactly, LYC_ESTATE with

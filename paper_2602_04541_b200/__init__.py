@@ -12,13 +12,15 @@ the built library raises ImportError.
 from ._lib import (CudaError, InvalidArgument, LogicError, LycError, NotSupported, lib)
 from .decode import HybridDecoder, SparsityPolicy, args_top_k, fraction_budget
 from .kvcache import KvCache, correction_attention
+from .model import DecodeModel, ModelConfig
 from .kernel import (BlockIndexSet, CostReport, RunResult, SplitSchedule, WorkUnit, Workload,
                      latency_model, plan_splits, run)
 
 lib()  # fail loudly at import when the native library is missing
 
 __all__ = [
-    "BlockIndexSet", "CostReport", "CudaError", "HybridDecoder", "InvalidArgument", "KvCache",
+    "BlockIndexSet", "CostReport", "CudaError", "DecodeModel", "HybridDecoder", "InvalidArgument",
+    "KvCache", "ModelConfig",
     "LogicError",
     "LycError", "NotSupported", "RunResult", "SparsityPolicy", "SplitSchedule", "WorkUnit",
     "Workload", "args_top_k", "correction_attention", "fraction_budget", "latency_model",

@@ -27,8 +27,10 @@ SYMBOLS = [
     "lyc_window_attention", "lyc_decoder_step_varlen", "lyc_decoder_capture_varlen",
     "lyc_decoder_set_trace_sets", "lyc_decoder_traced_sets", "lyc_decoder_step_dev",
     "lyc_decoder_capture_dev", "lyc_decoder_status", "lyc_decoder_tune", "lyc_kv_append_dev",
-    "lyc_plan_selftest", "lyc_decoder_refresh_sets", "lyc_decoder_sync_sets",
+    "lyc_plan_selftest", "lyc_decoder_refresh_sets", "lyc_decoder_sync_sets", "lyc_gemv",
 ]
+
+GEMV_STORE, GEMV_RESIDUAL, GEMV_SILU_BF16, GEMV_QKV_ROPE = 0, 1, 2, 3
 
 TUNE_RING_STAGES, TUNE_PER_LAYER_KERNELS, TUNE_PDL, TUNE_DEFER_SELECTION = 1, 2, 3, 4
 
@@ -80,6 +82,16 @@ class lyc_kv_layout(C.Structure):
     ]
 
 
+class lyc_gemv_desc(C.Structure):
+    _fields_ = [
+        ("M", C.c_int64), ("K", C.c_int64), ("w", C.c_void_p), ("x", C.c_void_p),
+        ("xb", C.c_void_p), ("gain", C.c_void_p), ("eps", C.c_float), ("mode", C.c_int32),
+        ("y", C.c_void_p), ("yb", C.c_void_p), ("q_out", C.c_void_p), ("k_cache", C.c_void_p),
+        ("v_cache", C.c_void_p), ("slab_stride", C.c_int64), ("nq", C.c_int32),
+        ("nkv", C.c_int32), ("d", C.c_int32), ("pad", C.c_int32), ("pos", C.c_int64),
+    ]
+
+
 _lib = None
 
 
@@ -118,6 +130,8 @@ def lib() -> C.CDLL:
     L.lyc_decoder_capture_varlen.argtypes = [vp, vp, vp, vp, C.POINTER(C.c_int64), vp, vp]
     L.lyc_decoder_layer.restype = C.c_int
     L.lyc_decoder_layer.argtypes = [vp, i32, vp, vp, vp, i64, vp, vp]
+    L.lyc_gemv.restype = C.c_int
+    L.lyc_gemv.argtypes = [C.POINTER(lyc_gemv_desc), vp]
     L.lyc_decoder_sync_sets.restype = C.c_int
     L.lyc_decoder_sync_sets.argtypes = [vp, vp]
     L.lyc_decoder_refresh_sets.restype = C.c_int

@@ -34,6 +34,7 @@ cudaError_t launch_window_tc(const CUtensorMap& tmap_k, const CUtensorMap& tmap_
                              int layer, int B, int H, int G, int d, int64_t start, int W,
                              float scale, float* workspace, int n_split, void* out,
                              cudaStream_t st);
+cudaError_t launch_gemv(const LycGemvParams& p, int n_sms, cudaStream_t st);
 int topk_cluster_size(int n, int max_slice);
 cudaError_t launch_refresh_scores(const void* q, const void* k_layer, int64_t cap, int B, int H,
                                   int G, int d, int dtype, int64_t len, uint32_t* keys,
@@ -2036,6 +2037,57 @@ int lyc_window_attention(const lyc_kv_layout* lay, int32_t layer, const void* k_
                                      ns, out, (cudaStream_t)stream),
                "window launch");
     g_launches += 2;
+    return LYC_OK;
+  });
+}
+
+// ------------------------------------------------------------ toy-model decode ops
+
+int lyc_gemv(const lyc_gemv_desc* g, void* stream) {
+  return (int)guarded([&]() -> int64_t {
+    if (!g || !g->w) fail(LYC_EINVAL, "gemv: null descriptor or weights");
+    if (g->M < 1 || g->K < 8 || g->K % 8) fail(LYC_EINVAL, "gemv: M >= 1 and K a multiple of 8");
+    if (g->K > 49152) fail(LYC_ENOTSUP, "gemv: K > 49152 (the input vector lives in shared memory)");
+    if ((g->x == nullptr) == (g->xb == nullptr)) fail(LYC_EINVAL, "gemv: exactly one of x (fp32) / xb (bf16)");
+    if ((uintptr_t)g->w % 16) fail(LYC_EINVAL, "gemv: weights must be 16-B aligned");
+    LycGemvParams p{};
+    p.w = g->w;
+    p.M = g->M;
+    p.K = g->K;
+    p.x = g->x;
+    p.xb = g->xb;
+    p.gain = g->gain;
+    p.eps = g->eps > 0.f ? g->eps : 1e-6f;
+    p.mode = g->mode;
+    switch (g->mode) {
+      case LYC_GEMV_STORE:
+      case LYC_GEMV_RESIDUAL:
+        if (!g->y) fail(LYC_EINVAL, "gemv: y is null");
+        p.y = g->y;
+        break;
+      case LYC_GEMV_SILU_BF16:
+        if (!g->yb) fail(LYC_EINVAL, "gemv: yb is null");
+        p.yb = g->yb;
+        break;
+      case LYC_GEMV_QKV_ROPE:
+        if (!g->q_out || !g->k_cache || !g->v_cache) fail(LYC_EINVAL, "gemv: q / k / v outputs are null");
+        if (g->d < 2 || g->d % 2 || g->nq < 1 || g->nkv < 1 || g->pos < 0)
+          fail(LYC_EINVAL, "gemv: qkv shapes");
+        if (g->M != (int64_t)(g->nq + 2 * g->nkv) * g->d) fail(LYC_EINVAL, "gemv: M != (nq + 2 nkv) d");
+        p.q_out = g->q_out;
+        p.k_cache = g->k_cache;
+        p.v_cache = g->v_cache;
+        p.slab_stride = g->slab_stride;
+        p.nq = g->nq;
+        p.nkv = g->nkv;
+        p.d = g->d;
+        p.pos = g->pos;
+        break;
+      default:
+        fail(LYC_EINVAL, "gemv: unknown mode");
+    }
+    cuda_check(lyc::launch_gemv(p, num_sms(), (cudaStream_t)stream), "gemv launch");
+    ++g_launches;
     return LYC_OK;
   });
 }

@@ -286,3 +286,25 @@ struct LycStepParams {
   int32_t sel_defer_out;     // leave layer l_end - 1's selection to the next launch
   LycPlanIn plan;            // the step's lengths + the planner's input (re-plan in the kernel)
 };
+
+// Toy-model decode GEMV (model.cu, include/lyc.h lyc_gemv).
+struct LycGemvParams {
+  const void* w;            // bf16 [M][K]
+  int64_t M, K;
+  const float* x;           // fp32 input [K] (the residual stream), or null
+  const void* xb;           // bf16 input [K], or null
+  const float* gain;        // rmsnorm gain [K] (prologue) or null
+  float eps;
+  int32_t mode;             // LYC_GEMV_*
+  float* y;                 // STORE: y = Wx; RESIDUAL: y += Wx (fp32 [M])
+  void* yb;                 // SILU_BF16: yb = silu(Wx) (bf16)
+  // QKV_ROPE: rows [0, nq*d) -> q (rotary), [nq*d, (nq+nkv)*d) -> K rows
+  // (rotary), the rest -> V rows; K / V rows go to cache row `pos` of each
+  // KV head's slab: k_cache + g * slab_stride + pos * d
+  void* q_out;
+  void* k_cache;
+  void* v_cache;
+  int64_t slab_stride;      // elements between consecutive KV heads' slabs
+  int32_t nq, nkv, d, pad;
+  int64_t pos;
+};
