@@ -1161,6 +1161,13 @@ void launch_step_range(lyc_decoder* d, int l0, int l1, const void* q, const void
   p.plan.seq = seq;
   p.plan.dlens = dlens;
   p.plan.has_lens = lens ? 1 : 0;
+  if (!lens && !dlens) {  // one validated host length: the kernel's lengths prologue is skipped
+    int32_t nb = 0, kb = 0;
+    lyc::plan_item_key(d->pin, seq, nb, kb);
+    p.uniform = 1;
+    p.uni_nsel = d->cfg.select_mode == LYC_SELECT_BLOCKS ? nb : (int32_t)seq;
+    p.uni_ksel = kb;
+  }
   if (lens)
     for (int b = 0; b < d->B; ++b) p.plan.lens[b] = (int32_t)lens[b];
   const bool per_layer = d->NL > 1 && l1 - l0 == 1;

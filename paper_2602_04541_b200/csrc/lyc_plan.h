@@ -282,6 +282,8 @@ struct LycStepParams {
   float scale;
   float scale_log2;
   int32_t stages;            // attention ring stages in use (0 = all)
+  int32_t uniform;           // host lengths, every batch item plan.seq: the lengths below hold
+  int32_t uni_nsel, uni_ksel;  //   selection keys / ids kept per row at plan.seq (plan_item_key)
   int32_t sel_defer_in;      // run layer l_begin - 1's selection (deferred by the previous launch)
   int32_t sel_defer_out;     // leave layer l_end - 1's selection to the next launch
   LycPlanIn plan;            // the step's lengths + the planner's input (re-plan in the kernel)

@@ -990,8 +990,24 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
   }
   for (int b = threadIdx.x; b < LYC_H1_BINS; b += kStepThreads) sm.hist[b] = 0u;
   __syncthreads();
-  // ---- the step's lengths (host values by value, or a device array read now)
-  if (!step_lengths(p, s_seq, s_nsel, s_ksel, s_dyn)) return;  // invalid: no work, no counter touched
+  if (threadIdx.x == 0) stamp(p, p.l_begin, 23, cta);  // barriers initialised
+  // ---- the step's lengths (host values by value, or a device array read now);
+  // one host length for the whole batch arrives pre-digested (no prologue pass)
+  if (p.uniform) {
+    for (int b = threadIdx.x; b < pin.B; b += kStepThreads) {
+      s_seq[b] = (int32_t)pin.seq;
+      s_nsel[b] = p.uni_nsel;
+      s_ksel[b] = p.uni_ksel;
+    }
+    if (threadIdx.x == 0) {
+      s_dyn[1] = p.uni_nsel;
+      s_dyn[2] = p.uni_ksel;
+      s_dyn[3] = 0;
+    }
+    __syncthreads();
+  } else if (!step_lengths(p, s_seq, s_nsel, s_ksel, s_dyn)) {
+    return;  // invalid: no work, no counter touched
+  }
   const int par = s_dyn[0] & 1;
   StepRt rt;
   rt.ctr = p.ctr + (size_t)par * set_words;

@@ -35,7 +35,7 @@ torch.cuda.synchronize()
 tr = dec.trace().astype(np.int64)
 t0 = tr[0, 0].min()
 r = (tr - t0) / 1e3
-print(f"{'l':>3} {'R':>2} {'entry0':>8} {'pdl0':>8} {'prolog':>8} {'beg':>8} {'end':>8} {'merge':>8} "
+print(f"{'l':>3} {'R':>2} {'entry0':>8} {'pdl0':>8} {'bars':>8} {'prolog':>8} {'beg':>8} {'end':>8} {'merge':>8} "
       f"{'seldone':>8} {'exit':>8} {'next_beg':>8} {'gap':>6}")
 for l in range(NL):
     nr = int((roles[l] == 0).sum()) if l else H
@@ -44,5 +44,6 @@ for l in range(NL):
     nb = r[l + 1, 0].min() if l + 1 < NL else float("nan")
     last = max(end, mrg, sd if sd == sd else 0)
     ent, pdl, pro, ex = r[l, 5].min(), r[l, 7].max(), r[l, 17].max(), r[l, 19].max()
-    print(f"{l:3d} {nr:2d} {ent:8.1f} {pdl:8.1f} {pro:8.1f} {beg:8.1f} {end:8.1f} {mrg:8.1f} {sd:8.1f} "
+    bars = r[l, 23].max()
+    print(f"{l:3d} {nr:2d} {ent:8.1f} {pdl:8.1f} {bars:8.1f} {pro:8.1f} {beg:8.1f} {end:8.1f} {mrg:8.1f} {sd:8.1f} "
           f"{ex:8.1f} {nb:8.1f} {nb - last:6.1f}")
