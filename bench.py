@@ -411,6 +411,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-full", action="store_true")
     ap.add_argument("--no-swaps", action="store_true")
+    ap.add_argument("--no-flashinfer", action="store_true",
+                    help="skip the external full-attention bar (FlashInfer decode)")
     ap.add_argument("--no-model", action="store_true",
                     help="skip the end-to-end toy-model TPOT (hybrid vs full attention)")
     ap.add_argument("--no-pdl", action="store_true",
@@ -612,6 +614,47 @@ def main():
                 "speedup_hybrid_vs_full": fms / ms}
         fdec.close()
 
+    # ---- external full-attention bar: FlashInfer's decode
+    # attention (library code, JIT-compiled on first use) over every layer's
+    # full cache in our HND layout, CUDA-graph replayed
+    flashinfer_full = None
+    if world == 1 and not args.no_flashinfer and dt == torch.bfloat16 and B == 1:
+        try:
+            import flashinfer
+            fo = torch.empty((NL, Hr * G, d), dtype=dt, device=dev)
+
+            def fi_step():
+                for l in range(NL):
+                    fo[l] = flashinfer.single_decode_with_kv_cache(
+                        q[l, 0], K[l, 0], V[l, 0], kv_layout="HND", use_tensor_cores=True)
+            with torch.cuda.stream(stream):
+                for _ in range(3):
+                    fi_step()
+                stream.synchronize()
+                gfi = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gfi, stream=stream):
+                    fi_step()
+                for _ in range(args.warmup):
+                    gfi.replay()
+            stream.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                e0.record(stream)
+                for _ in range(args.steps):
+                    gfi.replay()
+                e1.record(stream)
+            e1.synchronize()
+            fi_us = e0.elapsed_time(e1) / args.steps * 1e3
+            flashinfer_full = {"us_per_token": fi_us, "version": flashinfer.__version__,
+                               "api": "flashinfer.single_decode_with_kv_cache (tensor cores), "
+                                      "every layer, full cache",
+                               "speedup_hybrid_vs_flashinfer_full": fi_us / step_us}
+            if full:
+                flashinfer_full["our_full_vs_flashinfer_full"] = fi_us / full["us_per_token"]
+            del gfi
+        except Exception as e:  # an external bar must not kill the bench line
+            flashinfer_full = {"error": repr(e)[:200]}
+
     # ---- the per-layer public API (lyc_decoder_layer, what a model calls
     # between its own projections): one step-kernel launch per layer (plus
     # the planner at layer 0), eager and CUDA-graph captured
@@ -809,6 +852,7 @@ def main():
                                        else attn_bytes[0] / (per_layer[0] / 1e3) / 1e9,
                          "bytes_per_step": float(attn_bytes.sum())},
             "full_attention": full,
+            "flashinfer_full_attention": flashinfer_full,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_ms * 1e3 / B, "unit": "us/token", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
