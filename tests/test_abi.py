@@ -71,3 +71,43 @@ def test_fraction_budget_matches_oracle(orc):
     for n in (1, 2, 7, 100, 4096, 131072):
         for f in (1e-9, 0.1, 0.3, 0.5, 0.7, 0.999):
             assert fraction_budget(f, n) == orc.fraction_budget(f, n)
+
+
+def test_gemv_validates_before_launch():
+    """lyc_gemv (toy_model.hpp:161-274 ops) rejects bad descriptors on the host
+    with LYC_EINVAL / LYC_ENOTSUP -- no device needed."""
+    import ctypes as C
+
+    from paper_2602_04541_b200 import _lib as LL
+    L = LL.lib()
+
+    def rc(**kw):
+        base = dict(M=64, K=64, w=0x1000, x=0x2000, xb=None, gain=None, eps=0.0,
+                    mode=LL.GEMV_STORE, y=0x3000)
+        base.update(kw)
+        return L.lyc_gemv(C.byref(LL.lyc_gemv_desc(**base)), None)
+
+    assert rc(w=None) == -1                       # null weights
+    assert rc(K=60) == -1                         # K not a multiple of 8
+    assert rc(K=50000) == -4                      # the input vector exceeds shared memory
+    assert rc(xb=0x4000) == -1                    # both inputs
+    assert rc(x=None) == -1                       # no input
+    assert rc(w=0x1008) == -1                     # misaligned weights
+    assert rc(mode=9) == -1                       # unknown epilogue
+    assert rc(mode=LL.GEMV_STORE, y=None) == -1
+    assert rc(mode=LL.GEMV_SILU_BF16, y=None) == -1
+    # QKV_ROPE: M must be (nq + 2 nkv) d, d even
+    assert rc(mode=LL.GEMV_QKV_ROPE, q_out=0x5000, k_cache=0x6000, v_cache=0x7000,
+              nq=2, nkv=1, d=16, M=63) == -1
+    assert rc(mode=LL.GEMV_QKV_ROPE, q_out=0x5000, k_cache=0x6000, v_cache=0x7000,
+              nq=2, nkv=1, d=15, M=60) == -1
+    assert b"gemv" in L.lyc_last_error()
+
+
+def test_decoder_entry_points_validate_before_launch():
+    """refresh / sync on a null decoder, bad layers and lengths: host errors."""
+    from paper_2602_04541_b200 import _lib as LL
+    L = LL.lib()
+    assert L.lyc_decoder_refresh_sets(None, 0, None, None, 1, None) == -1
+    assert L.lyc_decoder_sync_sets(None, None) == -1
+    assert L.lyc_decoder_tune(None, LL.TUNE_DEFER_SELECTION, 0) == -1
