@@ -411,6 +411,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-full", action="store_true")
     ap.add_argument("--no-swaps", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip the 25 %% / 50 %% retrieval-fraction points (BASELINE config 3)")
     ap.add_argument("--no-flashinfer", action="store_true",
                     help="skip the external full-attention bar (FlashInfer decode)")
     ap.add_argument("--no-model", action="store_true",
@@ -655,6 +657,28 @@ def main():
         except Exception as e:  # an external bar must not kill the bench line
             flashinfer_full = {"error": repr(e)[:200]}
 
+    # ---- BASELINE config 3 is a retrieval-head fraction sweep at fixed top-k:
+    # the same caches and queries with 25 % and 50 % retrieval heads (the
+    # headline is the 12.5 % point), whole-step time, graph replayed
+    sweep = None
+    if world == 1 and fused and not args.no_sweep:
+        sweep = []
+        for fr in (0.25, 0.5):
+            sroles = make_roles(NL, H, fr, args.seed)
+            sdec = P.HybridDecoder(n_layers=NL, batch=B, n_kv_heads=H, group_size=G, d_head=d,
+                                   seq_cap=seq_cap, roles=sroles, policy=pol, dtype=dt,
+                                   select=args.select)
+            sout = torch.empty_like(q)
+            with torch.cuda.stream(stream):
+                sdec.capture(q, K, V, L, sout, stream=stream)
+            sms = time_graph(sdec, args.steps, args.warmup)
+            sbytes = sdec.step_bytes(L)
+            sweep.append({"retrieval_fraction": fr, "us_per_token": sms * 1e3 / B,
+                          "bytes_per_step": sbytes,
+                          "hbm_gbs": sbytes / (sms / 1e3) / 1e9,
+                          "frac": sbytes / (sms / 1e3) / 1e9 / peak})
+            sdec.close()
+
     # ---- the per-layer public API (lyc_decoder_layer, what a model calls
     # between its own projections): one step-kernel launch per layer (plus
     # the planner at layer 0), eager and CUDA-graph captured
@@ -852,6 +876,7 @@ def main():
                                        else attn_bytes[0] / (per_layer[0] / 1e3) / 1e9,
                          "bytes_per_step": float(attn_bytes.sum())},
             "full_attention": full,
+            "retrieval_fraction_sweep": sweep,
             "flashinfer_full_attention": flashinfer_full,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_ms * 1e3 / B, "unit": "us/token", "h2d_bytes_per_step": int(h2d),

@@ -3,7 +3,7 @@
 cd $GRAFT_REPO_ROOT
 IFS=';' read -ra CS <<< "$CASES"
 for c in "${CS[@]}"; do
-  timeout 600 python bench.py --steps ${STEPS:-20} --warmup 5 --no-cpu-baseline --no-full --no-swaps ${EXTRA:---no-model} $c 2>gpurun_out/case_err.txt | python -c "
+  timeout 600 python bench.py --steps ${STEPS:-20} --warmup 5 --no-cpu-baseline --no-full --no-swaps --no-sweep ${EXTRA:---no-model} $c 2>gpurun_out/case_err.txt | python -c "
 import json,sys
 try:
     d=json.loads(sys.stdin.read().strip().splitlines()[-1])

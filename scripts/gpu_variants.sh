@@ -9,7 +9,7 @@ for v in build/variants/*/; do
   cp $v/liblyc.so paper_2602_04541_b200/liblyc.so
   for w in ${WORKLOADS:-qwen3-8b-128k}; do
     timeout 300 python bench.py --steps ${STEPS:-30} --warmup 5 --no-cpu-baseline --no-full --no-swaps \
-      --no-model --no-flashinfer --workload $w $ARGS 2>gpurun_out/var_err.txt | tail -1 | python -c "
+      --no-model --no-flashinfer --no-sweep --workload $w $ARGS 2>gpurun_out/var_err.txt | tail -1 | python -c "
 import json,sys
 try:
     d=json.loads(sys.stdin.read())
