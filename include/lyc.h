@@ -372,7 +372,7 @@ int lyc_decoder_refresh_sets(lyc_decoder* dec, int32_t layer, const void* q_last
  *              rows [nq*d, (nq+nkv)*d): the token's K rows (rotary), the rest
  *              its V rows, written to cache row `pos` of KV head g at
  *              k_cache / v_cache + g * slab_stride (bf16)  -- compute_qkv (:218-240)
- * K must be a multiple of 8 and <= 49152; W 16-B aligned. */
+ * K must be a multiple of 8 and <= 49152; W, x / xb and gain 16-B aligned. */
 #define LYC_GEMV_STORE 0
 #define LYC_GEMV_RESIDUAL 1
 #define LYC_GEMV_SILU_BF16 2
@@ -393,6 +393,12 @@ typedef struct lyc_gemv_desc {
   int64_t slab_stride;
   int32_t nq, nkv, d, pad;
   int64_t pos;
+  /* optional L2 prefetch hint: the first prefetch_bytes of the NEXT launch's
+   * weights (16-B aligned, or NULL / 0).  Each warp issues its share after its
+   * own rows, so the next GEMV's first loads hit L2 instead of waiting out the
+   * launch boundary on HBM. */
+  const void* prefetch;
+  int64_t prefetch_bytes;
 } lyc_gemv_desc;
 int lyc_gemv(const lyc_gemv_desc* g, void* stream);
 

@@ -89,6 +89,7 @@ class lyc_gemv_desc(C.Structure):
         ("y", C.c_void_p), ("yb", C.c_void_p), ("q_out", C.c_void_p), ("k_cache", C.c_void_p),
         ("v_cache", C.c_void_p), ("slab_stride", C.c_int64), ("nq", C.c_int32),
         ("nkv", C.c_int32), ("d", C.c_int32), ("pad", C.c_int32), ("pos", C.c_int64),
+        ("prefetch", C.c_void_p), ("prefetch_bytes", C.c_int64),
     ]
 
 

@@ -2057,6 +2057,8 @@ int lyc_gemv(const lyc_gemv_desc* g, void* stream) {
     if (g->K > 49152) fail(LYC_ENOTSUP, "gemv: K > 49152 (the input vector lives in shared memory)");
     if ((g->x == nullptr) == (g->xb == nullptr)) fail(LYC_EINVAL, "gemv: exactly one of x (fp32) / xb (bf16)");
     if ((uintptr_t)g->w % 16) fail(LYC_EINVAL, "gemv: weights must be 16-B aligned");
+    if ((uintptr_t)g->x % 16 || (uintptr_t)g->xb % 16 || (uintptr_t)g->gain % 16)
+      fail(LYC_EINVAL, "gemv: x / xb / gain must be 16-B aligned");
     LycGemvParams p{};
     p.w = g->w;
     p.M = g->M;
@@ -2092,6 +2094,11 @@ int lyc_gemv(const lyc_gemv_desc* g, void* stream) {
         break;
       default:
         fail(LYC_EINVAL, "gemv: unknown mode");
+    }
+    if (g->prefetch && g->prefetch_bytes > 0) {
+      if ((uintptr_t)g->prefetch % 16) fail(LYC_EINVAL, "gemv: prefetch must be 16-B aligned");
+      p.pf = g->prefetch;
+      p.pf_bytes = g->prefetch_bytes & ~(int64_t)15;
     }
     cuda_check(lyc::launch_gemv(p, num_sms(), (cudaStream_t)stream), "gemv launch");
     ++g_launches;

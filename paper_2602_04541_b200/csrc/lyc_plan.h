@@ -309,4 +309,6 @@ struct LycGemvParams {
   int64_t slab_stride;      // elements between consecutive KV heads' slabs
   int32_t nq, nkv, d, pad;
   int64_t pos;
+  const void* pf;           // L2 prefetch of the next launch's weights [pf_bytes], or null
+  int64_t pf_bytes;
 };

@@ -53,78 +53,10 @@ __device__ __forceinline__ float dot8(const uint4& w, const float* x) {
   return fmaf(e.y, x1.w, s);
 }
 
-__global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const __grid_constant__ LycGemvParams p) {
-  extern __shared__ float xs[];  // [K] the (normalised) input vector
-  __shared__ float red[kGemvThreads / 32];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int K = (int)p.K;
-  const int64_t pairs = (p.M + 1) / 2;
-  const int chunks = K / 8;
-  // ---- the first weight chunks of this warp's first row pair are loaded
-  // before waiting for the previous kernel (programmatic dependent launch):
-  // weights do not depend on it, so their HBM stream overlaps its tail
-  int64_t pr = (int64_t)blockIdx.x * (kGemvThreads / 32) + warp;
-  uint4 a[kGemvUnroll], b[kGemvUnroll];
-  auto load_batch = [&](int64_t r0, int c0) {
-    const bool two = r0 + 1 < p.M;
-    const __nv_bfloat16* w0 = static_cast<const __nv_bfloat16*>(p.w) + r0 * p.K;
-    const __nv_bfloat16* w1 = two ? w0 + p.K : w0;
-#pragma unroll
-    for (int u = 0; u < kGemvUnroll; ++u) {
-      const int c = c0 + u * 32;
-      if (c < chunks) {
-        a[u] = ld_stream(w0 + (int64_t)c * 8);
-        b[u] = ld_stream(w1 + (int64_t)c * 8);
-      }
-    }
-  };
-  if (pr < pairs) load_batch(2 * pr, lane);
-  pdl_wait();  // (no early launch_dependents: measured slower in the decode step)
-  // ---- prologue: x (fp32 or bf16) into shared memory, rmsnorm'ed when a
-  // gain is given (toy_model.hpp:161-169: x * inv_rms * gain, eps 1e-6)
-  float ss = 0.f;
-  for (int i = tid; i < K; i += kGemvThreads) {
-    const float v = p.x ? p.x[i] : __bfloat162float(static_cast<const __nv_bfloat16*>(p.xb)[i]);
-    xs[i] = v;
-    ss = fmaf(v, v, ss);
-  }
-  if (p.gain) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
-    if (lane == 0) red[warp] = ss;
-    __syncthreads();
-    float tot = 0.f;
-#pragma unroll
-    for (int w = 0; w < kGemvThreads / 32; ++w) tot += red[w];
-    const float inv = rsqrtf(tot / (float)K + p.eps);
-    for (int i = tid; i < K; i += kGemvThreads) xs[i] = xs[i] * inv * p.gain[i];
-  }
-  __syncthreads();
-  // ---- two adjacent rows per warp
-  bool first = true;
-  for (; pr < pairs; pr += (int64_t)gridDim.x * (kGemvThreads / 32)) {
-    const int64_t r0 = 2 * pr;
-    const bool two = r0 + 1 < p.M;
-    float s0 = 0.f, s1 = 0.f;
-    for (int c0 = lane; c0 < chunks; c0 += 32 * kGemvUnroll) {
-      if (!first) load_batch(r0, c0);  // (the first batch was loaded before the wait)
-      first = false;
-#pragma unroll
-      for (int u = 0; u < kGemvUnroll; ++u) {
-        const int c = c0 + u * 32;
-        if (c < chunks) {
-          s0 += dot8(a[u], xs + c * 8);
-          s1 += dot8(b[u], xs + c * 8);
-        }
-      }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      s0 += __shfl_xor_sync(0xffffffffu, s0, off);
-      s1 += __shfl_xor_sync(0xffffffffu, s1, off);
-    }
-    if (lane != 0) continue;
-    // ---- epilogue
+// The epilogue of one row pair (lane 0 of its warp).
+__device__ __forceinline__ void gemv_epilogue(const LycGemvParams& p, int64_t r0, bool two,
+                                              float s0, float s1) {
+  {  // (one block: the modes are exclusive)
     if (p.mode == GEMV_STORE) {
       p.y[r0] = s0;
       if (two) p.y[r0 + 1] = s1;
@@ -163,6 +95,166 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const __grid_constan
       }
     }
   }
+}
+
+// This warp's share of the next launch's weights into L2 (bulk prefetches
+// through the TMA engine; fire and forget), after its own rows.
+__device__ __forceinline__ void gemv_prefetch_next(const LycGemvParams& p, int warp, int lane) {
+  if (p.pf && lane == 0) {
+    const int64_t warps = (int64_t)gridDim.x * (kGemvThreads / 32);
+    const int64_t wid = (int64_t)blockIdx.x * (kGemvThreads / 32) + warp;
+    const int64_t share = ((p.pf_bytes / 16 + warps - 1) / warps) * 16;
+    const int64_t b0 = wid * share, b1 = b0 + share < p.pf_bytes ? b0 + share : p.pf_bytes;
+    for (int64_t b = b0; b < b1; b += 65536) {
+      const uint32_t n = (uint32_t)(b1 - b < 65536 ? b1 - b : 65536);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(static_cast<const char*>(p.pf) + b),
+                   "r"(n)
+                   : "memory");
+    }
+  }
+}
+
+// The input vector into shared memory, rmsnorm'ed when a gain is given
+// (toy_model.hpp:161-169: x * inv_rms * gain, eps 1e-6); all threads of the
+// CTA, ends with a barrier.
+__device__ __forceinline__ void gemv_stage_x(const LycGemvParams& p, float* xs, float* red, int tid,
+                                             int warp, int lane) {
+  const int K = (int)p.K;
+  // 16-B vectors, kPro of them in flight per thread before any is used: one
+  // L2 round trip per kPro * 256 vectors (K = 4096: one) -- an element loop
+  // would wait for every load in turn.
+  constexpr int kPro = 4;
+  float ss = 0.f;
+  if (p.x) {
+    const float4* x4 = reinterpret_cast<const float4*>(p.x);
+    for (int c0 = tid; c0 < K / 4; c0 += kGemvThreads * kPro) {
+      float4 v[kPro];
+#pragma unroll
+      for (int u = 0; u < kPro; ++u)
+        if (c0 + u * kGemvThreads < K / 4) v[u] = __ldcg(x4 + c0 + u * kGemvThreads);
+#pragma unroll
+      for (int u = 0; u < kPro; ++u) {
+        const int c = c0 + u * kGemvThreads;
+        if (c < K / 4) {
+          reinterpret_cast<float4*>(xs)[c] = v[u];
+          ss = fmaf(v[u].x, v[u].x, fmaf(v[u].y, v[u].y, fmaf(v[u].z, v[u].z, fmaf(v[u].w, v[u].w, ss))));
+        }
+      }
+    }
+  } else {
+    const uint4* x8 = static_cast<const uint4*>(p.xb);
+    for (int c0 = tid; c0 < K / 8; c0 += kGemvThreads * kPro) {
+      uint4 v[kPro];
+#pragma unroll
+      for (int u = 0; u < kPro; ++u)
+        if (c0 + u * kGemvThreads < K / 8) v[u] = __ldcg(x8 + c0 + u * kGemvThreads);
+#pragma unroll
+      for (int u = 0; u < kPro; ++u) {
+        const int c = c0 + u * kGemvThreads;
+        if (c < K / 8) {
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
+          float f[8];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 t = __bfloat1622float2(h[e]);
+            f[2 * e] = t.x;
+            f[2 * e + 1] = t.y;
+          }
+          reinterpret_cast<float4*>(xs)[2 * c] = make_float4(f[0], f[1], f[2], f[3]);
+          reinterpret_cast<float4*>(xs)[2 * c + 1] = make_float4(f[4], f[5], f[6], f[7]);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) ss = fmaf(f[e], f[e], ss);
+        }
+      }
+    }
+  }
+  if (p.gain) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    if (lane == 0) red[warp] = ss;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < kGemvThreads / 32; ++w) tot += red[w];
+    const float inv = rsqrtf(tot / (float)K + p.eps);
+    const float4* g4 = reinterpret_cast<const float4*>(p.gain);
+    for (int c0 = tid; c0 < K / 4; c0 += kGemvThreads * kPro) {
+      float4 g[kPro];
+#pragma unroll
+      for (int u = 0; u < kPro; ++u)
+        if (c0 + u * kGemvThreads < K / 4) g[u] = __ldg(g4 + c0 + u * kGemvThreads);
+#pragma unroll
+      for (int u = 0; u < kPro; ++u) {
+        const int c = c0 + u * kGemvThreads;
+        if (c < K / 4) {
+          float4 v = reinterpret_cast<float4*>(xs)[c];
+          v.x = v.x * inv * g[u].x;
+          v.y = v.y * inv * g[u].y;
+          v.z = v.z * inv * g[u].z;
+          v.w = v.w * inv * g[u].w;
+          reinterpret_cast<float4*>(xs)[c] = v;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const __grid_constant__ LycGemvParams p) {
+  extern __shared__ float xs[];  // [K] the (normalised) input vector
+  __shared__ float red[kGemvThreads / 32];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int K = (int)p.K;
+  const int64_t pairs = (p.M + 1) / 2;
+  const int chunks = K / 8;
+  // ---- the first weight chunks of this warp's first row pair are loaded
+  // before waiting for the previous kernel (programmatic dependent launch):
+  // weights do not depend on it, so their HBM stream overlaps its tail
+  int64_t pr = (int64_t)blockIdx.x * (kGemvThreads / 32) + warp;
+  uint4 a[kGemvUnroll], b[kGemvUnroll];
+  auto load_batch = [&](int64_t r0, int c0) {
+    const bool two = r0 + 1 < p.M;
+    const __nv_bfloat16* w0 = static_cast<const __nv_bfloat16*>(p.w) + r0 * p.K;
+    const __nv_bfloat16* w1 = two ? w0 + p.K : w0;
+#pragma unroll
+    for (int u = 0; u < kGemvUnroll; ++u) {
+      const int c = c0 + u * 32;
+      if (c < chunks) {
+        a[u] = ld_stream(w0 + (int64_t)c * 8);
+        b[u] = ld_stream(w1 + (int64_t)c * 8);
+      }
+    }
+  };
+  if (pr < pairs) load_batch(2 * pr, lane);
+  pdl_wait();  // (no early launch_dependents: measured slower in the decode step)
+  gemv_stage_x(p, xs, red, tid, warp, lane);
+  // ---- two adjacent rows per warp
+  bool first = true;
+  for (; pr < pairs; pr += (int64_t)gridDim.x * (kGemvThreads / 32)) {
+    const int64_t r0 = 2 * pr;
+    const bool two = r0 + 1 < p.M;
+    float s0 = 0.f, s1 = 0.f;
+    for (int c0 = lane; c0 < chunks; c0 += 32 * kGemvUnroll) {
+      if (!first) load_batch(r0, c0);  // (the first batch was loaded before the wait)
+      first = false;
+#pragma unroll
+      for (int u = 0; u < kGemvUnroll; ++u) {
+        const int c = c0 + u * 32;
+        if (c < chunks) {
+          s0 += dot8(a[u], xs + c * 8);
+          s1 += dot8(b[u], xs + c * 8);
+        }
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, off);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+    }
+    if (lane != 0) continue;
+    gemv_epilogue(p, r0, two, s0, s1);
+  }
+  gemv_prefetch_next(p, warp, lane);
 }
 
 cudaError_t launch_gemv(const LycGemvParams& p, int n_sms, cudaStream_t st) {

@@ -61,8 +61,11 @@ PRESETS = {
 
 
 def gemv(w, x=None, xb=None, *, mode, y=None, yb=None, gain=None, eps=1e-6, q_out=None,
-         k_cache=None, v_cache=None, slab_stride=0, nq=0, nkv=0, d=0, pos=0, stream=None):
-    """One lyc_gemv launch (include/lyc.h): w bf16 [M][K]."""
+         k_cache=None, v_cache=None, slab_stride=0, nq=0, nkv=0, d=0, pos=0, stream=None,
+         prefetch=None, prefetch_bytes=0):
+    """One lyc_gemv launch (include/lyc.h): w bf16 [M][K]; `prefetch`: the
+    next launch's weight tensor, whose first prefetch_bytes (default all) are
+    pulled into L2 as this launch's warps finish."""
     M, K = w.shape
     g = LL.lyc_gemv_desc(M=M, K=K, w=w.data_ptr(), x=x.data_ptr() if x is not None else None,
                          xb=xb.data_ptr() if xb is not None else None,
@@ -72,7 +75,10 @@ def gemv(w, x=None, xb=None, *, mode, y=None, yb=None, gain=None, eps=1e-6, q_ou
                          q_out=q_out.data_ptr() if q_out is not None else None,
                          k_cache=k_cache.data_ptr() if k_cache is not None else None,
                          v_cache=v_cache.data_ptr() if v_cache is not None else None,
-                         slab_stride=slab_stride, nq=nq, nkv=nkv, d=d, pad=0, pos=pos)
+                         slab_stride=slab_stride, nq=nq, nkv=nkv, d=d, pad=0, pos=pos,
+                         prefetch=prefetch.data_ptr() if prefetch is not None else None,
+                         prefetch_bytes=(prefetch_bytes or prefetch.numel() * prefetch.element_size())
+                         if prefetch is not None else 0)
     st = (stream if stream is not None else torch.cuda.current_stream()).cuda_stream
     check(lib().lyc_gemv(C.byref(g), st))
 
@@ -115,6 +121,9 @@ class DecodeModel:
             self.k = torch.zeros((NL, 1, H, cap, d), dtype=bf, device=dev)
             self.v = torch.zeros_like(self.k)
         self.roles, self.policy = roles, policy or SparsityPolicy.top_k(4096)
+        # L2 prefetch of the next GEMV's first weight bytes (lyc_gemv_desc.prefetch);
+        # 0 disables (scripts/bench_gemv_chain.py: 8 MB measured best)
+        self.prefetch_bytes = 8 << 20
         self.dec = None
         self.set_attention(attention)
         # per-token buffers
@@ -155,16 +164,24 @@ class DecodeModel:
         cfg, NL, d = self.cfg, self.cfg.n_layers, self.cfg.d_head
         H, nq = cfg.n_kv_heads, cfg.n_q_heads
         cap = cfg.max_seq_len
+
+        def pf(w):  # the next GEMV's first weight bytes into L2 as this one finishes
+            if not self.prefetch_bytes:
+                return {}
+            return dict(prefetch=w, prefetch_bytes=min(self.prefetch_bytes, w.numel() * 2))
+
         self.x.copy_(self.embedding[token].float())
         for l in range(NL):
+            nxt = self.wqkv[l + 1] if l + 1 < NL else self.lm_head
             gemv(self.wqkv[l], x=self.x, gain=self.attn_norm[l], mode=LL.GEMV_QKV_ROPE,
                  q_out=self.q[l], k_cache=self.k[l, 0], v_cache=self.v[l, 0], slab_stride=cap * d,
-                 nq=nq, nkv=H, d=d, pos=pos, stream=stream)
+                 nq=nq, nkv=H, d=d, pos=pos, stream=stream, **pf(self.wo[l]))
             self.dec.layer(l, self.q[l], self.k, self.v, pos + 1, self.o[l], stream=stream)
-            gemv(self.wo[l], xb=self.o[l].view(-1), mode=LL.GEMV_RESIDUAL, y=self.x, stream=stream)
+            gemv(self.wo[l], xb=self.o[l].view(-1), mode=LL.GEMV_RESIDUAL, y=self.x, stream=stream,
+                 **pf(self.w1[l]))
             gemv(self.w1[l], x=self.x, gain=self.ffn_norm[l], mode=LL.GEMV_SILU_BF16, yb=self.mid,
-                 stream=stream)
-            gemv(self.w2[l], xb=self.mid, mode=LL.GEMV_RESIDUAL, y=self.x, stream=stream)
+                 stream=stream, **pf(self.w2[l]))
+            gemv(self.w2[l], xb=self.mid, mode=LL.GEMV_RESIDUAL, y=self.x, stream=stream, **pf(nxt))
         gemv(self.lm_head, x=self.x, gain=self.final_norm, mode=LL.GEMV_STORE, y=self.logits,
              stream=stream)
         return self.logits
