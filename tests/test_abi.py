@@ -93,6 +93,9 @@ def test_gemv_validates_before_launch():
     assert rc(xb=0x4000) == -1                    # both inputs
     assert rc(x=None) == -1                       # no input
     assert rc(w=0x1008) == -1                     # misaligned weights
+    assert rc(x=0x2004) == -1                     # misaligned input vector
+    assert rc(gain=0x2008) == -1                  # misaligned rmsnorm gain
+    assert rc(prefetch=0x8004, prefetch_bytes=4096) == -1  # misaligned prefetch hint
     assert rc(mode=9) == -1                       # unknown epilogue
     assert rc(mode=LL.GEMV_STORE, y=None) == -1
     assert rc(mode=LL.GEMV_SILU_BF16, y=None) == -1

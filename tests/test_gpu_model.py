@@ -65,6 +65,24 @@ def test_gemv_modes_vs_torch(M, K):
     assert rel(yb.float(), ref) < 1e-2
 
 
+def test_prefetch_hint_leaves_results_unchanged():
+    """lyc_gemv_desc.prefetch (L2 prefetch of the next launch's weights) is a
+    hint only: outputs bitwise equal with and without it."""
+    from paper_2602_04541_b200 import _lib as LL
+    from paper_2602_04541_b200.model import gemv
+    g = torch.Generator(device="cuda").manual_seed(11)
+    w = torch.randn((3000, 4096), generator=g, device="cuda").bfloat16()
+    nxt = torch.randn((4096, 4096), generator=g, device="cuda").bfloat16()
+    x = torch.randn(4096, generator=g, device="cuda")
+    gain = torch.ones(4096, device="cuda")
+    y0, y1 = torch.empty(3000, device="cuda"), torch.empty(3000, device="cuda")
+    gemv(w, x=x, gain=gain, mode=LL.GEMV_STORE, y=y0)
+    gemv(w, x=x, gain=gain, mode=LL.GEMV_STORE, y=y1, prefetch=nxt)
+    gemv(w, x=x, gain=gain, mode=LL.GEMV_STORE, y=y1, prefetch=nxt, prefetch_bytes=1 << 20)
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1)
+
+
 def test_qkv_rope_writes_q_and_cache_rows():
     from paper_2602_04541_b200 import _lib as LL
     from paper_2602_04541_b200.model import gemv
