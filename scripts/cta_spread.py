@@ -1,4 +1,5 @@
-"""Per-CTA spread of the consumer spans of selected layers (debug, run under gpurun)."""
+"""Per-CTA spread of the consumer phase of selected layers of one fused step
+(debug, run under gpurun): python scripts/cta_spread.py [workload] [layers...]"""
 import sys
 from pathlib import Path
 
@@ -10,7 +11,8 @@ sys.path.insert(0, str(ROOT))
 import bench  # noqa: E402
 import paper_2602_04541_b200 as P  # noqa: E402
 
-wl = dict(bench.WORKLOADS["llama3-8b-128k"])
+wname = sys.argv[1] if len(sys.argv) > 1 else "qwen3-8b-128k"
+wl = dict(bench.WORKLOADS[wname])
 NL, H, G, d, L, k, B = (wl[x] for x in ("NL", "H", "G", "d", "L", "k", "B"))
 roles = bench.make_roles(NL, H, 0.125, 2602)
 K = torch.empty((NL, B, H, L, d), dtype=torch.bfloat16, device="cuda")
@@ -26,16 +28,20 @@ for _ in range(3):
 dec.set_trace(True)
 dec.decode_step(q, K, V, L)
 torch.cuda.synchronize()
-tr = dec.trace().astype(np.int64)
+tr = dec.trace().astype(np.int64)  # [NL][events][ctas]
 t0 = tr[0, 0].min()
 rel = (tr - t0) / 1e3
-for l in range(NL):
-    nr = int((roles[l] == 0).sum()) if l else H
-    b, e = rel[l, 0], rel[l, 1]
-    span = e - b
-    qs, t1, u1, tl = rel[l, 16] - b, rel[l, 17] - b, rel[l, 18] - b, rel[l, 19] - b
-    print(f"l{l:2d} R{nr} begin max {b.max():7.1f} end p50/max {np.percentile(e,50):7.1f}/{e.max():7.1f}"
-          f"  span p50 {np.percentile(span,50):5.1f} | q_staged p50 {np.percentile(qs,50):4.1f} "
-          f"first_tile p50 {np.percentile(t1,50):4.1f} first_unit_done p50 {np.percentile(u1,50):5.1f} "
-          f"last_tile p50 {np.percentile(tl,50):5.1f} | ue_enter {np.percentile(rel[l,20]-b,50):5.1f} "
-          f"ue_bar {np.percentile(rel[l,21]-b,50):5.1f} ue_stored {np.percentile(rel[l,22]-b,50):5.1f}")
+layers = [int(x) for x in sys.argv[2:]] or list(range(1, 10))
+for l in layers:
+    nr = int((roles[l] == 0).sum())
+    b = rel[l, 0]
+    e = rel[l, 1]
+    b0 = b.min()
+    pe = np.percentile(e - b0, [10, 50, 90, 100])
+    pb = np.percentile(b - b0, [50, 100])
+    q16 = np.percentile(rel[l, 16] - b0, [50, 100])
+    u18 = np.percentile(rel[l, 18] - b0, [10, 50, 90, 100])
+    slow = np.argsort(-e)[:6]
+    print(f"l{l:2d} R{nr} begin p50/max {pb[0]:4.1f}/{pb[1]:4.1f}  q_staged p50/max {q16[0]:4.1f}/{q16[1]:4.1f}  "
+          f"first-unit-done p10/50/90/max {u18[0]:5.1f}/{u18[1]:5.1f}/{u18[2]:5.1f}/{u18[3]:5.1f}  "
+          f"end p10/50/90/max {pe[0]:5.1f}/{pe[1]:5.1f}/{pe[2]:5.1f}/{pe[3]:5.1f}  slowest CTAs {slow.tolist()}")
