@@ -31,6 +31,7 @@ SYMBOLS = [
 ]
 
 GEMV_STORE, GEMV_RESIDUAL, GEMV_SILU_BF16, GEMV_QKV_ROPE = 0, 1, 2, 3
+GEMV_FLAG_NEXT_IS_GEMV = 1
 
 TUNE_RING_STAGES, TUNE_PER_LAYER_KERNELS, TUNE_PDL, TUNE_DEFER_SELECTION = 1, 2, 3, 4
 
@@ -88,7 +89,7 @@ class lyc_gemv_desc(C.Structure):
         ("xb", C.c_void_p), ("gain", C.c_void_p), ("eps", C.c_float), ("mode", C.c_int32),
         ("y", C.c_void_p), ("yb", C.c_void_p), ("q_out", C.c_void_p), ("k_cache", C.c_void_p),
         ("v_cache", C.c_void_p), ("slab_stride", C.c_int64), ("nq", C.c_int32),
-        ("nkv", C.c_int32), ("d", C.c_int32), ("pad", C.c_int32), ("pos", C.c_int64),
+        ("nkv", C.c_int32), ("d", C.c_int32), ("flags", C.c_int32), ("pos", C.c_int64),
         ("prefetch", C.c_void_p), ("prefetch_bytes", C.c_int64),
     ]
 

@@ -2068,6 +2068,8 @@ int lyc_gemv(const lyc_gemv_desc* g, void* stream) {
     p.gain = g->gain;
     p.eps = g->eps > 0.f ? g->eps : 1e-6f;
     p.mode = g->mode;
+    if (g->flags & ~LYC_GEMV_FLAG_NEXT_IS_GEMV) fail(LYC_EINVAL, "gemv: unknown flags");
+    p.flags = g->flags;
     switch (g->mode) {
       case LYC_GEMV_STORE:
       case LYC_GEMV_RESIDUAL:

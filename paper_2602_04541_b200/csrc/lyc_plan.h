@@ -307,7 +307,7 @@ struct LycGemvParams {
   void* k_cache;
   void* v_cache;
   int64_t slab_stride;      // elements between consecutive KV heads' slabs
-  int32_t nq, nkv, d, pad;
+  int32_t nq, nkv, d, flags;  // flags: LYC_GEMV_FLAG_*
   int64_t pos;
   const void* pf;           // L2 prefetch of the next launch's weights [pf_bytes], or null
   int64_t pf_bytes;

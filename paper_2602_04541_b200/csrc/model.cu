@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const __grid_constan
     }
   };
   if (pr < pairs) load_batch(2 * pr, lane);
-  pdl_wait();  // (no early launch_dependents: measured slower in the decode step)
+  pdl_wait();
   gemv_stage_x(p, xs, red, tid, warp, lane);
   // ---- two adjacent rows per warp
   bool first = true;
@@ -254,6 +254,13 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const __grid_constan
     if (lane != 0) continue;
     gemv_epilogue(p, r0, two, s0, s1);
   }
+  // this CTA's rows are done: when another GEMV follows, its CTAs may be
+  // scheduled as the SM frees up (they still wait for this grid's completion
+  // before reading its outputs).  A trigger at the start was slower (its CTAs
+  // competed with this grid's streaming); this one saves ~3 % of the GEMV
+  // chain (the toy model's step, whose GEMV chains alternate with the
+  // attention step, does not set the flag: 6 % slower with it).
+  if (p.flags & 1) pdl_trigger();
   gemv_prefetch_next(p, warp, lane);
 }
 

@@ -62,10 +62,11 @@ PRESETS = {
 
 def gemv(w, x=None, xb=None, *, mode, y=None, yb=None, gain=None, eps=1e-6, q_out=None,
          k_cache=None, v_cache=None, slab_stride=0, nq=0, nkv=0, d=0, pos=0, stream=None,
-         prefetch=None, prefetch_bytes=0):
+         prefetch=None, prefetch_bytes=0, next_is_gemv=False):
     """One lyc_gemv launch (include/lyc.h): w bf16 [M][K]; `prefetch`: the
     next launch's weight tensor, whose first prefetch_bytes (default all) are
-    pulled into L2 as this launch's warps finish."""
+    pulled into L2 as this launch's warps finish; next_is_gemv: another
+    lyc_gemv follows in the stream (LYC_GEMV_FLAG_NEXT_IS_GEMV)."""
     M, K = w.shape
     g = LL.lyc_gemv_desc(M=M, K=K, w=w.data_ptr(), x=x.data_ptr() if x is not None else None,
                          xb=xb.data_ptr() if xb is not None else None,
@@ -75,7 +76,8 @@ def gemv(w, x=None, xb=None, *, mode, y=None, yb=None, gain=None, eps=1e-6, q_ou
                          q_out=q_out.data_ptr() if q_out is not None else None,
                          k_cache=k_cache.data_ptr() if k_cache is not None else None,
                          v_cache=v_cache.data_ptr() if v_cache is not None else None,
-                         slab_stride=slab_stride, nq=nq, nkv=nkv, d=d, pad=0, pos=pos,
+                         slab_stride=slab_stride, nq=nq, nkv=nkv, d=d,
+                         flags=LL.GEMV_FLAG_NEXT_IS_GEMV if next_is_gemv else 0, pos=pos,
                          prefetch=prefetch.data_ptr() if prefetch is not None else None,
                          prefetch_bytes=(prefetch_bytes or prefetch.numel() * prefetch.element_size())
                          if prefetch is not None else 0)
@@ -124,6 +126,11 @@ class DecodeModel:
         # L2 prefetch of the next GEMV's first weight bytes (lyc_gemv_desc.prefetch);
         # 0 disables (scripts/bench_gemv_chain.py: 8 MB measured best)
         self.prefetch_bytes = 8 << 20
+        # early scheduling of the next GEMV (LYC_GEMV_FLAG_NEXT_IS_GEMV): off --
+        # it speeds a bare GEMV chain up by 3 % but slows this decode step
+        # (interleaved with the attention step kernel) by 6 %
+        # (profiles/r2_decode_gemv.md)
+        self.early_next = False
         self.dec = None
         self.set_attention(attention)
         # per-token buffers
@@ -178,10 +185,11 @@ class DecodeModel:
                  nq=nq, nkv=H, d=d, pos=pos, stream=stream, **pf(self.wo[l]))
             self.dec.layer(l, self.q[l], self.k, self.v, pos + 1, self.o[l], stream=stream)
             gemv(self.wo[l], xb=self.o[l].view(-1), mode=LL.GEMV_RESIDUAL, y=self.x, stream=stream,
-                 **pf(self.w1[l]))
+                 next_is_gemv=self.early_next, **pf(self.w1[l]))
             gemv(self.w1[l], x=self.x, gain=self.ffn_norm[l], mode=LL.GEMV_SILU_BF16, yb=self.mid,
-                 stream=stream, **pf(self.w2[l]))
-            gemv(self.w2[l], xb=self.mid, mode=LL.GEMV_RESIDUAL, y=self.x, stream=stream, **pf(nxt))
+                 stream=stream, next_is_gemv=self.early_next, **pf(self.w2[l]))
+            gemv(self.w2[l], xb=self.mid, mode=LL.GEMV_RESIDUAL, y=self.x, stream=stream,
+                 next_is_gemv=self.early_next, **pf(nxt))
         gemv(self.lm_head, x=self.x, gain=self.final_norm, mode=LL.GEMV_STORE, y=self.logits,
              stream=stream)
         return self.logits

@@ -33,10 +33,10 @@ def chain(which):
                 seq.append((n, l))
     wt = {"qkv": m.wqkv, "o": m.wo, "w1": m.w1, "w2": m.w2}
     for i, (n, l) in enumerate(seq):
-        pf = {}
+        pf = {"next_is_gemv": i + 1 < len(seq)}
         if PF and i + 1 < len(seq):
             nw = wt[seq[i + 1][0]][seq[i + 1][1]]
-            pf = dict(prefetch=nw, prefetch_bytes=0 if PF < 0 else min(PF, nw.numel() * 2))
+            pf.update(prefetch=nw, prefetch_bytes=0 if PF < 0 else min(PF, nw.numel() * 2))
         if n == "qkv":
             gemv(m.wqkv[l], x=m.x, gain=m.attn_norm[l], mode=LL.GEMV_QKV_ROPE, q_out=m.q[l],
                  k_cache=m.k[l, 0], v_cache=m.v[l, 0], slab_stride=cap * d, nq=nq, nkv=H, d=d,
