@@ -975,11 +975,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
   EpiSmem& es = *reinterpret_cast<EpiSmem*>(sm.extra);
   const LycPlanIn& pin = p.plan;
   if (threadIdx.x == 0) stamp(p, p.l_begin, EV_ENTRY, cta);
-  pdl_wait();     // the previous launch of the stream has completed and its writes are visible
-  pdl_trigger();  // the next launch in the stream may begin its launch while this one runs
-  if (threadIdx.x == 0) stamp(p, p.l_begin, EV_PDL, cta);
+  // on-chip setup before the wait for the previous launch (it touches no
+  // global memory): barriers, the layer mark, the first-pass histogram
   if (threadIdx.x == 0) {
-    s_dyn[0] = (int32_t)__ldcg(ctrl);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&sm.full[s], kProducerThreads + 1);  // + the tile-info arrival
       mbar_init(&sm.empty[s], kConsumerWarps);
@@ -989,6 +987,10 @@ __global__ void __launch_bounds__(kStepThreads, 1) hybrid_step_kernel(const __gr
     *sm.clayer = 0u;
   }
   for (int b = threadIdx.x; b < LYC_H1_BINS; b += kStepThreads) sm.hist[b] = 0u;
+  pdl_wait();     // the previous launch of the stream has completed and its writes are visible
+  pdl_trigger();  // the next launch in the stream may begin its launch while this one runs
+  if (threadIdx.x == 0) stamp(p, p.l_begin, EV_PDL, cta);
+  if (threadIdx.x == 0) s_dyn[0] = (int32_t)__ldcg(ctrl);
   __syncthreads();
   if (threadIdx.x == 0) stamp(p, p.l_begin, 23, cta);  // barriers initialised
   // ---- the step's lengths (host values by value, or a device array read now);
