@@ -456,6 +456,79 @@ struct SparsityPolicy {
 enum class Dtype { F32 = LYC_DTYPE_F32, BF16 = LYC_DTYPE_BF16 };
 enum class Select { Tokens = LYC_SELECT_TOKENS, Blocks = LYC_SELECT_BLOCKS, None = LYC_SELECT_NONE };
 
+// The toy model's decode operations around the attention (toy_model.hpp:218-274)
+// on device buffers through lyc_gemv: weights bf16 [out][in] (the transpose of
+// the reference's Matrix<float> [in][out]: the same sums, coalesced per output
+// row), the residual stream x fp32 [d_model].  Each call is one launch.
+namespace model {
+
+inline lyc_gemv_desc gemv_desc(const void* w, int64_t M, int64_t K, int32_t mode) {
+  lyc_gemv_desc g{};
+  g.w = w;
+  g.M = M;
+  g.K = K;
+  g.mode = mode;
+  return g;
+}
+
+// compute_qkv (toy_model.hpp:218-241): h = rmsnorm(x, attn_norm); q = W_q h,
+// k = W_k h, v = W_v h (W_qkv = [W_q; W_k; W_v]); rotary on q and k; q -> q_out
+// bf16 [nq][d]; the K / V rows of every KV head g -> row `pos` of
+// k_cache / v_cache + g * slab_stride (the layer's [H][S_cap][d] slabs, bf16).
+inline void compute_qkv(const void* w_qkv, int64_t d_model, const float* x, const float* attn_norm,
+                        int nq, int nkv, int d, int64_t pos, void* q_out, void* k_cache,
+                        void* v_cache, int64_t slab_stride, void* stream = nullptr) {
+  lyc_gemv_desc g = gemv_desc(w_qkv, (int64_t)(nq + 2 * nkv) * d, d_model, LYC_GEMV_QKV_ROPE);
+  g.x = x;
+  g.gain = attn_norm;
+  g.nq = nq;
+  g.nkv = nkv;
+  g.d = d;
+  g.pos = pos;
+  g.q_out = q_out;
+  g.k_cache = k_cache;
+  g.v_cache = v_cache;
+  g.slab_stride = slab_stride;
+  check(lyc_gemv(&g, stream));
+}
+
+// attn_project_residual (toy_model.hpp:243-255): x += W_o concat(head_outputs)
+// (head outputs bf16 [Hq * d], the attention's output layout).
+inline void attn_project_residual(const void* w_o, int64_t d_model, const void* head_outputs,
+                                  int64_t hq_d, float* x, void* stream = nullptr) {
+  lyc_gemv_desc g = gemv_desc(w_o, d_model, hq_d, LYC_GEMV_RESIDUAL);
+  g.xb = head_outputs;
+  g.y = x;
+  check(lyc_gemv(&g, stream));
+}
+
+// ffn_residual (toy_model.hpp:257-267): x += W_2 silu(W_1 rmsnorm(x, ffn_norm)),
+// two launches; mid bf16 [d_ff] holds silu(W_1 h) between them.
+inline void ffn_residual(const void* w1, const void* w2, int64_t d_model, int64_t d_ff,
+                         const float* ffn_norm, float* x, void* mid, void* stream = nullptr) {
+  lyc_gemv_desc g1 = gemv_desc(w1, d_ff, d_model, LYC_GEMV_SILU_BF16);
+  g1.x = x;
+  g1.gain = ffn_norm;
+  g1.yb = mid;
+  check(lyc_gemv(&g1, stream));
+  lyc_gemv_desc g2 = gemv_desc(w2, d_model, d_ff, LYC_GEMV_RESIDUAL);
+  g2.xb = mid;
+  g2.y = x;
+  check(lyc_gemv(&g2, stream));
+}
+
+// output_logits (toy_model.hpp:269-274): logits = W_lm rmsnorm(x, final_norm).
+inline void output_logits(const void* w_lm, int64_t vocab, int64_t d_model, const float* x,
+                          const float* final_norm, float* logits, void* stream = nullptr) {
+  lyc_gemv_desc g = gemv_desc(w_lm, vocab, d_model, LYC_GEMV_STORE);
+  g.x = x;
+  g.gain = final_norm;
+  g.y = logits;
+  check(lyc_gemv(&g, stream));
+}
+
+}  // namespace model
+
 // Device KV cache write path (kv_cache.hpp:14-69) over caller-owned device
 // caches in the decoder layout [n_layers][B][H][seq_cap][d]: append writes one
 // row per (b, g) of a layer at length() (KvCache::append, 23-29), commit_row

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <functional>
 #include <memory>
 #include <numeric>
@@ -532,6 +533,145 @@ static void test_decoder_varlen() {
                std::invalid_argument);
 }
 
+
+// toy_model.hpp:161-274 decode operations (lyc::model, through lyc_gemv)
+// against plain double loops of the reference's own formulas on the same
+// bf16-rounded weights.
+static uint16_t to_bf16(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  u += 0x7fffu + ((u >> 16) & 1u);  // round to nearest even
+  return (uint16_t)(u >> 16);
+}
+static float from_bf16(uint16_t h) {
+  const uint32_t u = (uint32_t)h << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+static double rel_err(const std::vector<double>& a, const std::vector<double>& b) {
+  double num = 0.0, den = 1e-3;
+  for (std::size_t i = 0; i < a.size(); ++i) {
+    num = std::max(num, std::abs(a[i] - b[i]));
+    den = std::max(den, std::abs(b[i]));
+  }
+  return num / den;
+}
+
+static void test_model_ops() {
+  const int D = 256, nq = 4, nkv = 2, d = 32, dff = 512, vocab = 300, cap = 8, pos = 5;
+  const int Mqkv = (nq + 2 * nkv) * d, hqd = nq * d;
+  std::mt19937_64 rng(91);
+  std::normal_distribution<float> N(0.f, 1.f);
+  auto weights = [&](int M, int K, std::vector<uint16_t>& hb, std::vector<double>& hd) {
+    hb.resize((size_t)M * K);
+    hd.resize(hb.size());
+    for (size_t i = 0; i < hb.size(); ++i) {
+      hb[i] = to_bf16(N(rng) / std::sqrt((float)K));
+      hd[i] = from_bf16(hb[i]);
+    }
+  };
+  std::vector<uint16_t> bqkv, bo, b1, b2, blm;
+  std::vector<double> wqkv, wo, w1, w2, wlm;
+  weights(Mqkv, D, bqkv, wqkv);
+  weights(D, hqd, bo, wo);
+  weights(dff, D, b1, w1);
+  weights(D, dff, b2, w2);
+  weights(vocab, D, blm, wlm);
+  std::vector<float> x(D), g(D), o(hqd);
+  for (auto& v : x) v = N(rng);
+  for (auto& v : g) v = 1.f + 0.1f * N(rng);
+  std::vector<uint16_t> ob(hqd);
+  for (int i = 0; i < hqd; ++i) ob[i] = to_bf16(N(rng) * 0.5f);
+  auto up = [](const void* src, std::size_t bytes) {
+    lyc::DeviceBuffer b(bytes);
+    b.upload(src, bytes);
+    return b;
+  };
+  lyc::DeviceBuffer dwqkv = up(bqkv.data(), bqkv.size() * 2), dwo = up(bo.data(), bo.size() * 2),
+                    dw1 = up(b1.data(), b1.size() * 2), dw2 = up(b2.data(), b2.size() * 2),
+                    dwlm = up(blm.data(), blm.size() * 2), dx = up(x.data(), D * 4),
+                    dg = up(g.data(), D * 4), dob = up(ob.data(), hqd * 2);
+  lyc::DeviceBuffer dq(hqd * 2), dk((size_t)nkv * cap * d * 2), dv((size_t)nkv * cap * d * 2),
+      dmid((size_t)dff * 2), dlog((size_t)vocab * 4);
+  cudaMemset(dk.get(), 0, dk.bytes());
+  cudaMemset(dv.get(), 0, dv.bytes());
+  // host references (toy_model.hpp formulas, double)
+  auto rms = [&](const std::vector<double>& v) {
+    double ss = 0.0;
+    for (double e : v) ss += e * e;
+    const double inv = 1.0 / std::sqrt(ss / (double)v.size() + 1e-6);
+    std::vector<double> y(v.size());
+    for (size_t i = 0; i < v.size(); ++i) y[i] = v[i] * inv * (double)g[i];
+    return y;
+  };
+  auto matvec = [](const std::vector<double>& w, int M, int K, const std::vector<double>& in) {
+    std::vector<double> y((size_t)M, 0.0);
+    for (int r = 0; r < M; ++r)
+      for (int c = 0; c < K; ++c) y[(size_t)r] += w[(size_t)r * K + c] * in[(size_t)c];
+    return y;
+  };
+  auto rope = [&](double* h) {
+    for (int i = 0; i + 1 < d; i += 2) {
+      const double f = std::pow(10000.0, -(double)i / (double)d), a = pos * f;
+      const double c = std::cos(a), sn = std::sin(a), u = h[i], w = h[i + 1];
+      h[i] = u * c - w * sn;
+      h[i + 1] = u * sn + w * c;
+    }
+  };
+  std::vector<double> xd(x.begin(), x.end());
+  // compute_qkv
+  lyc::model::compute_qkv(dwqkv.get(), D, dx.as<float>(), dg.as<float>(), nq, nkv, d, pos, dq.get(),
+                          dk.get(), dv.get(), (int64_t)cap * d);
+  std::vector<double> y = matvec(wqkv, Mqkv, D, rms(xd));
+  for (int h = 0; h < nq + nkv; ++h) rope(&y[(size_t)h * d]);
+  std::vector<uint16_t> qh(hqd), kh((size_t)nkv * cap * d), vh(kh.size());
+  dq.download(qh.data(), qh.size() * 2);
+  dk.download(kh.data(), kh.size() * 2);
+  dv.download(vh.data(), vh.size() * 2);
+  std::vector<double> got(Mqkv), want(y);
+  for (int i = 0; i < hqd; ++i) got[(size_t)i] = from_bf16(qh[(size_t)i]);
+  for (int gk = 0; gk < nkv; ++gk)
+    for (int i = 0; i < d; ++i) {
+      got[(size_t)hqd + gk * d + i] = from_bf16(kh[((size_t)gk * cap + pos) * d + i]);
+      got[(size_t)hqd + nkv * d + gk * d + i] = from_bf16(vh[((size_t)gk * cap + pos) * d + i]);
+    }
+  CHECK(rel_err(got, want) < 1e-2);
+  CHECK(from_bf16(kh[((size_t)0 * cap + pos - 1) * d]) == 0.f);  // only row `pos` written
+  // attn_project_residual: x += W_o o
+  lyc::model::attn_project_residual(dwo.get(), D, dob.get(), hqd, dx.as<float>());
+  std::vector<double> od(hqd);
+  for (int i = 0; i < hqd; ++i) od[(size_t)i] = from_bf16(ob[(size_t)i]);
+  const std::vector<double> pr = matvec(wo, D, hqd, od);
+  for (int i = 0; i < D; ++i) xd[(size_t)i] += pr[(size_t)i];
+  std::vector<float> xh(D);
+  dx.download(xh.data(), D * 4);
+  CHECK(rel_err(std::vector<double>(xh.begin(), xh.end()), xd) < 1e-4);
+  // ffn_residual: x += W2 silu(W1 rmsnorm(x))   (mid rounded to bf16 on the device)
+  lyc::model::ffn_residual(dw1.get(), dw2.get(), D, dff, dg.as<float>(), dx.as<float>(), dmid.get());
+  std::vector<double> mid = matvec(w1, dff, D, rms(xd));
+  for (auto& v : mid) v = (double)from_bf16(to_bf16((float)(v / (1.0 + std::exp(-v)))));
+  const std::vector<double> f2 = matvec(w2, D, dff, mid);
+  for (int i = 0; i < D; ++i) xd[(size_t)i] += f2[(size_t)i];
+  dx.download(xh.data(), D * 4);
+  CHECK(rel_err(std::vector<double>(xh.begin(), xh.end()), xd) < 2e-3);
+  // output_logits
+  lyc::model::output_logits(dwlm.get(), vocab, D, dx.as<float>(), dg.as<float>(), dlog.as<float>());
+  const std::vector<double> lg = matvec(wlm, vocab, D, rms(xd));
+  std::vector<float> lh(vocab);
+  cudaDeviceSynchronize();
+  dlog.download(lh.data(), lh.size() * 4);
+  CHECK(rel_err(std::vector<double>(lh.begin(), lh.end()), lg) < 2e-3);
+  std::printf("  model ops: qkv / o-proj / ffn / logits match the double loops\n");
+  // errors as the reference's: shape violations throw std::invalid_argument
+  CHECK_THROWS(lyc::model::compute_qkv(dwqkv.get(), D, dx.as<float>(), dg.as<float>(), nq, nkv, d + 1,
+                                       pos, dq.get(), dk.get(), dv.get(), (int64_t)cap * d),
+               std::invalid_argument);
+  CHECK_THROWS(lyc::model::output_logits(dwlm.get(), vocab, D - 4, dx.as<float>(), dg.as<float>(),
+                                         dlog.as<float>()),
+               std::invalid_argument);
+}
+
 int main() {
   const std::pair<const char*, std::function<void()>> tests[] = {
       {"PlanSplits.KnownAnswersAndErrors", test_plan_splits_known},
@@ -544,6 +684,7 @@ int main() {
       {"ShardedDecoder.TwoRanksEqualUnsharded", test_sharded_decoder_two_ranks},
       {"KvCache.AppendOverwriteAndCorrectionAttention", test_kv_cache_and_correction},
       {"HybridDecoder.VariableLengthBatch", test_decoder_varlen},
+      {"Model.DecodeOpsMatchDoubleLoops", test_model_ops},
   };
   for (const auto& [name, fn] : tests) {
     const int before = g_fail;
