@@ -1,5 +1,8 @@
 """lyc_gemv (csrc/model.cu) at the toy model's Qwen3-8B / Llama-3-8B shapes:
-us per launch and weight GB/s, back-to-back launches (run under gpurun)."""
+us per launch and weight GB/s, back-to-back launches of ONE matrix (run under
+gpurun).  Matrices below the 126 MB L2 are then served from L2: this measures
+the kernel, not the model's HBM stream -- scripts/bench_gemv_chain.py times
+the model's chain with distinct weights per layer."""
 import sys
 from pathlib import Path
 
