@@ -96,6 +96,7 @@ def test_gemv_validates_before_launch():
     assert rc(x=0x2004) == -1                     # misaligned input vector
     assert rc(gain=0x2008) == -1                  # misaligned rmsnorm gain
     assert rc(prefetch=0x8004, prefetch_bytes=4096) == -1  # misaligned prefetch hint
+    assert rc(flags=2) == -1                      # unknown flag
     assert rc(mode=9) == -1                       # unknown epilogue
     assert rc(mode=LL.GEMV_STORE, y=None) == -1
     assert rc(mode=LL.GEMV_SILU_BF16, y=None) == -1

@@ -83,6 +83,33 @@ def test_prefetch_hint_leaves_results_unchanged():
     assert torch.equal(y0, y1)
 
 
+def test_next_is_gemv_flag_chain_equals_plain_chain():
+    """LYC_GEMV_FLAG_NEXT_IS_GEMV only lets the next launch be scheduled
+    early (it still waits for this one's completion): a dependent chain
+    x -> W_o residual -> W_1 silu -> W_2 residual gives bitwise-equal results."""
+    from paper_2602_04541_b200 import _lib as LL
+    from paper_2602_04541_b200.model import gemv
+    g = torch.Generator(device="cuda").manual_seed(12)
+    D, F = 1024, 3072
+    wo = torch.randn((D, D), generator=g, device="cuda").mul_(D ** -0.5).bfloat16()
+    w1 = torch.randn((F, D), generator=g, device="cuda").mul_(D ** -0.5).bfloat16()
+    w2 = torch.randn((D, F), generator=g, device="cuda").mul_(F ** -0.5).bfloat16()
+    o = torch.randn(D, generator=g, device="cuda").bfloat16()
+    gain = 1 + 0.1 * torch.randn(D, generator=g, device="cuda")
+    x0 = torch.randn(D, generator=g, device="cuda")
+    outs = []
+    for flag in (False, True):
+        x = x0.clone()
+        mid = torch.empty(F, dtype=torch.bfloat16, device="cuda")
+        for _ in range(3):
+            gemv(wo, xb=o, mode=LL.GEMV_RESIDUAL, y=x, next_is_gemv=flag)
+            gemv(w1, x=x, gain=gain, mode=LL.GEMV_SILU_BF16, yb=mid, next_is_gemv=flag)
+            gemv(w2, xb=mid, mode=LL.GEMV_RESIDUAL, y=x, next_is_gemv=False)
+        torch.cuda.synchronize()
+        outs.append(x)
+    assert torch.equal(outs[0], outs[1])
+
+
 def test_qkv_rope_writes_q_and_cache_rows():
     from paper_2602_04541_b200 import _lib as LL
     from paper_2602_04541_b200.model import gemv
